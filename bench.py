@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""bench.py -- Image-GS train iteration on B200 (BASELINE.json configs[1]).
+
+One step = one training iteration of the reference's fit loop
+(fit.cpp:149-157): 10k sampled pixel centres, exact global top-K (K=10) over
+the whole set, normalised blend, L1 loss, analytic backward with the
+sample-ordered gradient reduction, Adam + constrain -- on a 2048x2048
+photo-like target with 100k Gaussians (the C2 budget) in the fit-start
+state (sigma = 2 px, theta = 0), the worst case for candidate culling.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+* value   device-resident iterations/s (sample indices pre-uploaded), device
+          time from CUDA events on the library's stream, L2 flushed (512 MiB
+          memset) before every timed step; max over ranks.
+* e2e     the same iteration through the public C-ABI call
+          igs_train_iteration with HOST buffers: every step copies its 10k
+          sample indices host->device and reads the loss (+ status) back.
+* N > 1   one process per GPU (torchrun); the step's 10k samples are split
+          across ranks and the per-Gaussian gradients are summed with an NCCL
+          all-reduce before the (replicated) Adam step: strong scaling.
+* --impl reference times the reference's own OpenMP implementation
+          (oracle/_ref: the unmodified reference library, all host threads) on
+          the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BASE = json.loads((ROOT / "BASELINE.json").read_text())
+METRIC = BASE["metric"]
+W_IMG = H_IMG = 2048
+N_GAUSS = 100_000
+NS = 10_000
+K = 10
+LR = (2e-4, 2e-3, 1e-3, 1e-3)
+FLUSH_BYTES = 512 << 20
+WORKLOAD = ("C2 train iteration: 2048x2048 photo-like target, 100k Gaussians (fit-start state: sigma 2 px, "
+            "theta 0, uniform centres), 10k sampled pixels, exact global top-K K=10, L1 loss + backward "
+            "(sample-ordered reduction) + Adam/constrain")
+# FP64 pipe ops per evaluated (pixel, candidate) pair: 13 arithmetic ops of
+# mahalanobis_sq (renderer.cpp:17-23) + the threshold compare.
+OPS_PER_PAIR = 14
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-render", action="store_true")
+    return ap.parse_args()
+
+
+def workload():
+    from paper_2407_01866_b200 import synth
+    params = synth.init_set(N_GAUSS, W_IMG, H_IMG, seed=11)
+    target = synth.photo_like_image(W_IMG, H_IMG, 31001)
+    return params, target
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def physical_gpu(local_rank: int) -> int:
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        ids = [v for v in vis.split(",") if v.strip()]
+        if local_rank < len(ids) and ids[local_rank].strip().isdigit():
+            return int(ids[local_rank])
+    return local_rank
+
+
+# --------------------------------------------------------------------------- ours
+def run_ours(args, rank, world, local_rank, dist):
+    from paper_2407_01866_b200 import Context, synth
+    from paper_2407_01866_b200.igs import PROF_NAMES, PROF_SCAN, PROF_ADAM
+
+    params, target = workload()
+    total_steps = args.warmup + args.steps
+    samples = synth.sample_indices(NS, W_IMG, H_IMG, seed=99, steps=total_steps)
+    mine = np.ascontiguousarray(samples[:, rank::world])  # this rank's share of every step
+    ctx = Context(local_rank)
+    ctx.set_params(params)
+    ctx.set_target(target)
+    if world > 1:
+        uid = [Context.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.comm_init(uid[0], world, rank)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local_rank}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    fp64_peak = ctx.fp64_peak()
+
+    # ---- device-resident value ------------------------------------------------
+    ctx.upload_samples(mine)
+    ctx.train_iterations(args.warmup, K, LR, 1, want_losses=False)
+    ctx.sync()
+    clocks = Clocks(physical_gpu(local_rank))
+    barrier()
+    ctx.sync()
+    clocks.start()
+    launches0 = ctx.kernel_launches
+    ctx.profile_enable(True)
+    step_ms = []
+    for s in range(args.steps):
+        ctx.flush_l2(FLUSH_BYTES)
+        ctx.timer_begin()
+        ctx.train_iterations(1, K, LR, args.warmup + 1 + s, want_losses=False)
+        step_ms.append(ctx.timer_end())
+    ctx.sync()
+    barrier()
+    clk = clocks.stop()
+    launches = ctx.kernel_launches - launches0 - 0  # includes the flush memsets? no: memsets are not kernels we count
+    prof = {PROF_NAMES[f]: ctx.profile_read(f) for f in range(len(PROF_NAMES))}
+    ctx.profile_enable(False)
+    total_ms = max_over_ranks(sum(step_ms))
+    ms_per_step = total_ms / args.steps
+    value = args.steps / (total_ms / 1e3)
+
+    # ---- e2e through the public host-buffer call --------------------------------
+    ctx.set_params(params)  # fresh state: moments zero, same trajectory start
+    for s in range(args.warmup):
+        ctx.train_iteration(mine[s], K, LR, s + 1)
+    barrier()
+    e2e_ms = []
+    for s in range(args.steps):
+        ctx.flush_l2(FLUSH_BYTES)
+        ctx.timer_begin()
+        ctx.train_iteration(mine[args.warmup + s], K, LR, args.warmup + 1 + s)
+        e2e_ms.append(ctx.timer_end())
+    barrier()
+    e2e_total = max_over_ranks(sum(e2e_ms))
+    e2e_value = args.steps / (e2e_total / 1e3)
+
+    # ---- roofline of the dominant kernel family ----------------------------------
+    fam_ms = {k: v[0] for k, v in prof.items()}
+    dom = max(fam_ms, key=fam_ms.get)
+    scan_ms, scan_launches, scan_pairs = prof["scan"]
+    roof = None
+    if scan_ms > 0:
+        achieved = scan_pairs * OPS_PER_PAIR / (scan_ms * 1e-3)
+        roof = {"kernel": "top-K candidate scan (IGS_PROF_SCAN)", "bound": "fp64",
+                "achieved": achieved / 1e9, "peak": fp64_peak / 1e9, "unit": "Gop/s (fp64 add/mul pipe)",
+                "frac": achieved / fp64_peak, "traffic": None,
+                "work_per_launch": f"{scan_pairs / max(scan_launches, 1):.4g} (pixel, candidate) pairs x "
+                                   f"{OPS_PER_PAIR} fp64 ops",
+                "peak_source": "measured in this run (igs_fp64_peak: independent DMUL/DADD chains, all SMs); "
+                               "MEASURED_PEAKS.json has no fp64 figure",
+                "avg_launch_us": scan_ms * 1e3 / max(scan_launches, 1)}
+    adam_ms, adam_launches, adam_bytes = prof["adam"]
+    hbm = None
+    try:
+        hbm = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("hbm_gbs")
+    except Exception:
+        pass
+    adam_roof = None
+    if adam_ms > 0 and hbm:
+        gbs = adam_bytes / (adam_ms * 1e-3) / 1e9
+        adam_roof = {"kernel": "fused Adam+constrain+prepare", "bound": "hbm", "achieved": gbs, "peak": hbm,
+                     "unit": "GB/s", "frac": gbs / hbm, "traffic": None, "bytes_per_gaussian": 544}
+
+    # ---- secondary: full render Mpix/s (the eval render of the same set) ------------
+    render = None
+    if not args.no_render:
+        ctx.render_image(W_IMG, H_IMG, K, host=False)
+        ctx.sync()
+        rms = []
+        for _ in range(3):
+            ctx.flush_l2(FLUSH_BYTES)
+            ctx.timer_begin()
+            ctx.render_image(W_IMG, H_IMG, K, host=False)
+            rms.append(ctx.timer_end())
+        r_ms = max_over_ranks(min(rms))
+        render = {"metric": "global top-K render Mpix/s (render_image, 2048x2048, 100k G, K=10)",
+                  "value": W_IMG * H_IMG / (r_ms * 1e-3) / 1e6, "unit": "Mpix/s", "ms": r_ms,
+                  "note": "every GPU renders the full image here; tile-row sharding splits rows (igs_render_image_rows)"}
+
+    out = {
+        "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded mt19937_64 generators of the reference test suite)",
+        "config": {"workload": WORKLOAD, "image": f"{W_IMG}x{H_IMG}", "gaussians": N_GAUSS, "samples_per_iter": NS,
+                   "k": K, "parallelism": f"dp{world} (samples split across ranks, NCCL all-reduce of grads)",
+                   "l2": "flushed before every timed step (512 MiB memset on the stream, outside the events)",
+                   "cull": ctx.get_option(1), "deterministic_reduction": ctx.get_option(2)},
+        "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": int(mine.shape[1]) * 4,
+                "d2h_bytes_per_step": 8 + 32,
+                "call": "igs_train_iteration (host sample indices in, host loss out)"},
+        "roofline": roof, "roofline_adam": adam_roof,
+        "profile_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
+        "dominant_family": dom,
+        "clocks": clk, "gpu_launches": int(launches),
+        "render": render,
+    }
+    return out, ctx
+
+
+# ---------------------------------------------------------------------- reference
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference_steps(steps: int, warmup: int, budget_s: float):
+    """The unmodified reference (oracle/_ref) fit iteration on the same workload."""
+    import oracle
+    from paper_2407_01866_b200 import synth
+    if not oracle.available("reference"):
+        return None
+    R = oracle.get("reference")
+    params, target = workload()
+    samples = synth.sample_indices(NS, W_IMG, H_IMG, seed=99, steps=max(steps + warmup, 1))
+    import ctypes as C
+    p = np.ascontiguousarray(params.copy())
+    m = np.zeros_like(p); v = np.zeros_like(p)
+    tg = np.ascontiguousarray(target)
+    lr = np.ascontiguousarray(LR, np.float64)
+    loss = C.c_double(0)
+    dp = C.POINTER(C.c_double)
+
+    def one(s, t):
+        si = np.ascontiguousarray(samples[s])
+        code = R.lib.ref_train_iteration(p.ctypes.data_as(dp), p.shape[0], m.ctypes.data_as(dp),
+                                         v.ctypes.data_as(dp), tg.ctypes.data_as(C.POINTER(C.c_float)), W_IMG,
+                                         H_IMG, si.ctypes.data_as(C.POINTER(C.c_uint32)), NS, K,
+                                         lr.ctypes.data_as(dp), t, C.byref(loss))
+        if code:
+            raise RuntimeError(f"reference train iteration failed: {code}")
+
+    for s in range(warmup):
+        one(s, s + 1)
+    times = []
+    t_start = time.perf_counter()
+    for s in range(steps):
+        t0 = time.perf_counter()
+        one(warmup + s, warmup + s + 1)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > budget_s and len(times) >= 2:
+            break
+    return times
+
+
+def cpu_baseline_block(budget_s=20.0):
+    times = run_reference_steps(steps=1000, warmup=1, budget_s=budget_s)
+    if times is None:
+        return None
+    return {"value": len(times) / sum(times), "unit": "iters/s", "cores": cpu_threads(), "kind": "reference",
+            "sample": f"{len(times)} full C2 iterations (100k G, 10k samples, K=10) of the unmodified reference "
+                      f"(oracle/_ref, OpenMP, {cpu_threads()} threads) after 1 warm-up, ~{budget_s:.0f} s budget"}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        steps = args.steps
+        times = run_reference_steps(steps, args.warmup, budget_s=150.0)
+        if times is None:
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libigs_ref.so not built"}))
+            return 0
+        v = len(times) / sum(times)
+        out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": world,
+               "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+               "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic", "config": {"workload": WORKLOAD, "image": f"{W_IMG}x{H_IMG}",
+                                               "gaussians": N_GAUSS, "samples_per_iter": NS, "k": K},
+               "cpu_baseline": {"value": v, "unit": "iters/s", "cores": cpu_threads(), "kind": "reference",
+                                "sample": f"{len(times)} of {steps} requested full iterations (150 s cap)"},
+               "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(out))
+        return 0
+
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    out, ctx = run_ours(args, rank, world, local_rank, dist)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline_block()
+    if rank == 0:
+        print(json.dumps(out))
+    ctx.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

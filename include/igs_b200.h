@@ -1,0 +1,198 @@
+/*
+ * igs_b200.h -- C-ABI of the B200-native Image-GS hot path.
+ *
+ * The reference (/root/reference/proj) exposes its hot path as a C++ header
+ * API in namespace igs (proj/include/igs/*.hpp); it has no FFI of its own.
+ * This header is the thin C boundary a maintainer binds to replace that
+ * path: plain pointers and sizes, no C++ or torch types.
+ * shows the C++ shim (same igs:: signatures) and the Python ctypes binding.
+ *
+ * Layouts are zero-copy with the reference's structs:
+ *   Gaussian record  double[8] = mu_u, mu_v, theta, s1, s2, r, g, b
+ *                    (gaussian.hpp:19-24 Gaussian2D; GaussianGrad
+ *                    renderer.hpp:95-100 and the Adam slots adam.hpp:20-31
+ *                    use the same order)
+ *   PixelSample      double[5] = u, v, up_r, up_g, up_b (renderer.hpp:102-105)
+ *   Image            float32[H][W][3] row-major (image.hpp:24-59)
+ *   Rect             double[4] = x1, y1, x2, y2 (bsp.hpp:14-16)
+ *   LearningRates    double[4] = mu, color, scale, theta (adam.hpp:11-16)
+ *
+ * Every host pointer argument may be NULL where marked "nullable"; a NULL
+ * output keeps the result device-resident in the context (used by the
+ * device-resident benchmark and by fused multi-step calls).
+ *
+ * Errors: every call returns 0 or 1 + igs::ErrorKind (error.hpp:8-17);
+ * IGS_E_CUDA for device failures.  igs_last_error() returns the message of
+ * the last failing call on that context (text matches the reference where
+ * its tests inspect it, e.g. "non-finite gradient for Gaussian 1
+ * parameter s2", adam.cpp:29-31).  Validation happens before any launch, as
+ * in the reference (renderer.cpp:224-226).
+ *
+ * Threading: a context is externally synchronized (one host thread at a
+ * time), like the reference's fit().  One context per GPU.
+ */
+#ifndef IGS_B200_H
+#define IGS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IGS_OK 0
+#define IGS_E_INVALID_PARAMETER 1 /* ErrorKind::invalid_parameter  */
+#define IGS_E_DIMENSION_MISMATCH 2 /* ErrorKind::dimension_mismatch */
+#define IGS_E_BAD_MAGIC 3
+#define IGS_E_BAD_VERSION 4
+#define IGS_E_TRUNCATED 5
+#define IGS_E_EMPTY_SET 6 /* ErrorKind::empty_set */
+#define IGS_E_IO 7
+#define IGS_E_UNSUPPORTED_FORMAT 8
+#define IGS_E_CUDA 100 /* device / driver failure (no reference analogue) */
+
+typedef struct igs_ctx igs_ctx;
+
+/* ---- context ------------------------------------------------------------ */
+int igs_ctx_create(int device, igs_ctx** out);
+void igs_ctx_destroy(igs_ctx* ctx);
+const char* igs_last_error(const igs_ctx* ctx);
+/* Waits for all work queued on the context's stream. */
+int igs_sync(igs_ctx* ctx);
+/* Number of kernels this context launched since creation (diagnostics). */
+uint64_t igs_kernel_launches(const igs_ctx* ctx);
+
+/* Options (igs_set_option):                                                  */
+#define IGS_OPT_CULL 1          /* 1 = certified tile culling for global top-K (default), 0 = brute force */
+#define IGS_OPT_DETERMINISTIC 2 /* 1 = sample-ordered gradient reduction, bit-exact (default); 0 = fp64 atomics */
+#define IGS_OPT_TILE 3          /* tile edge in pixels for culling (default 16) */
+int igs_set_option(igs_ctx* ctx, int option, int64_t value);
+int64_t igs_get_option(const igs_ctx* ctx, int option);
+
+/* ---- Gaussian set (GaussianSet, gaussian.hpp:27-33) ------------------------ */
+/* Uploads n records and re-derives the per-Gaussian cache (PreparedSet,
+ * renderer.cpp:32-51).  Resets Adam moments; invalidates the partition. */
+int igs_set_params(igs_ctx* ctx, const double* params8, uint32_t n);
+/* Appends n records (densification, fit.cpp:185-199): indices stay stable,
+ * new Adam moments are zero (AdamState::resize, adam.hpp:26-29). */
+int igs_append_params(igs_ctx* ctx, const double* params8, uint32_t n);
+int igs_get_params(igs_ctx* ctx, double* params8 /* n*8 */, uint32_t n);
+uint32_t igs_num_gaussians(const igs_ctx* ctx);
+/* Device pointer of the resident params (double[n][8]) for zero-copy use. */
+const double* igs_device_params(const igs_ctx* ctx);
+
+/* ---- renderer (renderer.hpp:107-138) --------------------------------------- */
+/* render_image (renderer.cpp:209): global normalized top-K blend at every
+ * pixel center, clamped to [0,1], float32.  out_rgb nullable (keeps the
+ * image on device); topk_idx nullable: H*W*min(k,n) indices, sorted
+ * best-first, unused slots 0xFFFFFFFF (debug / parity). */
+int igs_render_image(igs_ctx* ctx, int width, int height, int k, float* out_rgb, uint32_t* topk_idx);
+/* Rows [row0, row1) of the same raster (tile-row sharding across GPUs);
+ * out_rgb receives (row1-row0)*W*3 floats. */
+int igs_render_image_rows(igs_ctx* ctx, int width, int height, int k, int row0, int row1, float* out_rgb);
+/* Device pointer of the last rendered image (float32 H*W*3). */
+const float* igs_device_image(const igs_ctx* ctx);
+
+/* select_top_k at npts points (renderer.cpp:134-148): idx/weights are
+ * npts*min(k,n), best-first; counts (nullable) per point. */
+int igs_select_top_k(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* idx, double* weights,
+                     int32_t* counts);
+/* render_topk at npts points (renderer.cpp:150-157): unclamped double RGB. */
+int igs_render_points(igs_ctx* ctx, const double* uv, uint32_t npts, int k, double* rgb);
+
+/* backward (renderer.cpp:254-260): loss gradients for arbitrary samples,
+ * reduced per Gaussian in sample order.  grads8 nullable (device-resident). */
+int igs_backward(igs_ctx* ctx, const double* samples5, uint32_t ns, int k, double* grads8);
+
+/* ---- training (fit.cpp:51-106, 149-157) --------------------------------- */
+/* Uploads the target image once (float32 H*W*3). */
+int igs_set_target(igs_ctx* ctx, const float* rgb, int width, int height);
+/* train_step_gradients: forward + L1 loss + backward at the sampled pixel
+ * centers (flat indices h*W+w into the target).  loss/grads8 nullable. */
+int igs_train_step(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, int k, double* loss, double* grads8);
+/* adam_step (adam.cpp:10-52) on the resident gradients; lr4 = mu, color,
+ * scale, theta; t = 1-based step (bias correction 1 - beta^t uses the
+ * host's libm pow exactly like the reference). */
+int igs_adam_step(igs_ctx* ctx, const double* lr4, long long t);
+/* Fused iteration: train_step + adam_step (+ NCCL gradient all-reduce
+ * between them when a communicator is attached). */
+int igs_train_iteration(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, int k, const double* lr4,
+                        long long t, double* loss);
+/* Uploads per-step sample indices to a device buffer of `steps` x ns
+ * entries so igs_train_iterations can run fully device-resident. */
+int igs_upload_samples(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, uint32_t steps);
+/* Runs `steps` fused iterations t = t0..t0+steps-1; step t uses uploaded
+ * sample slot (t-1) mod steps_uploaded.  losses (nullable): one per step. */
+int igs_train_iterations(igs_ctx* ctx, uint32_t steps, int k, const double* lr4, long long t0, double* losses);
+/* Resident gradient buffer (double[n][8]). */
+const double* igs_device_grads(const igs_ctx* ctx);
+int igs_get_grads(igs_ctx* ctx, double* grads8, uint32_t n);
+/* Adam moments in record order (AdamState m/v). */
+int igs_get_adam_state(igs_ctx* ctx, double* m, double* v, uint32_t n);
+int igs_set_adam_state(igs_ctx* ctx, const double* m, const double* v, uint32_t n);
+
+/* ---- error map & metrics (sampling.cpp:77-94, metrics.cpp:12-27) -------- */
+/* add_distribution(rendered, target): per-pixel L1 error normalized to a
+ * distribution (uniform when zero).  rendered nullable = last device image. */
+int igs_add_distribution(igs_ctx* ctx, const float* rendered, int width, int height, double* p);
+/* psnr(rendered, target); rendered nullable = last device image. */
+int igs_psnr(igs_ctx* ctx, const float* rendered, int width, int height, double* out);
+
+/* ---- BSP acceleration (bsp.hpp:70-106) ------------------------------------ */
+/* build_partition(set, n_max) over the resident set. */
+int igs_partition_build(igs_ctx* ctx, int n_max);
+/* rebuild_partition(blocks, set): shells and memberships re-derived from
+ * bare block corners (decode path, bsp.cpp:197-218). */
+int igs_partition_rebuild(igs_ctx* ctx, const double* rects4, uint32_t n_blocks);
+int igs_partition_info(igs_ctx* ctx, uint32_t* n_blocks, uint64_t* shell_total);
+int igs_partition_get(igs_ctx* ctx, double* blocks4, double* shells4, uint32_t* shell_offsets /* nb+1 */,
+                      uint32_t* shell_members);
+/* locate_block at npts points. */
+int igs_locate_blocks(igs_ctx* ctx, const double* uv, uint32_t npts, int32_t* blocks);
+/* render_image_blocked (bsp.cpp:334) through the resident partition. */
+int igs_render_image_blocked(igs_ctx* ctx, int width, int height, int k, float* out_rgb);
+/* render_topk_blocked at npts points (random-access decode queries). */
+int igs_render_points_blocked(igs_ctx* ctx, const double* uv, uint32_t npts, int k, double* rgb);
+
+/* ---- culling introspection (tile lists for parity tests) ------------------ */
+/* Builds the certified candidate lists for a W x H raster at k and returns
+ * the CSR (offsets ntiles+1, members ascending within each tile).  Pass
+ * NULL arrays to query sizes via ntiles/total. */
+int igs_tile_lists(igs_ctx* ctx, int width, int height, int k, uint32_t* ntiles, uint64_t* total,
+                   uint32_t* offsets, uint32_t* members, double* tau);
+
+/* ---- benchmark support (device timing on the context's stream) ----------- */
+int igs_timer_begin(igs_ctx* ctx);
+/* Records the stop event (unless igs_train_iterations already recorded it
+ * right after its last kernel), waits for it, returns elapsed ms. */
+int igs_timer_end(igs_ctx* ctx, float* ms);
+/* Overwrites a scratch buffer of `bytes` (choose > 126 MB L2) on the stream. */
+int igs_flush_l2(igs_ctx* ctx, size_t bytes);
+/* Microbenchmarks the FP64 add/mul pipe (independent DADD/DMUL chains,
+ * every SM): returns operations per second. */
+int igs_fp64_peak(igs_ctx* ctx, double* ops_per_s);
+/* Per-kernel-family CUDA-event profiling of the launches the context issues. */
+#define IGS_PROF_SCAN 0    /* top-K candidate scans (raster, point/sample scans) */
+#define IGS_PROF_FINISH 1  /* per-sample blend + loss + contributions */
+#define IGS_PROF_REDUCE 2  /* sample-ordered gradient reduction (sort + segment sum) */
+#define IGS_PROF_ADAM 3    /* fused Adam + constrain + prepare */
+#define IGS_PROF_CULL 4    /* certified tile-list construction */
+#define IGS_PROF_BLOCKED 5 /* BSP shell binning + blocked raster */
+#define IGS_PROF_FAMILIES 8
+int igs_profile_enable(igs_ctx* ctx, int on);
+/* total ms, launch count and algorithmic work (pairs for scans, bytes for
+ * Adam) accumulated since igs_profile_enable(ctx, 1). */
+int igs_profile_read(igs_ctx* ctx, int family, double* ms, uint64_t* launches, double* work);
+
+/* ---- multi-GPU (one context per GPU, one process or thread each) --------- */
+int igs_comm_unique_id(uint8_t id[128]);
+/* NCCL communicator over NVLink; training steps then all-reduce the
+ * per-Gaussian gradients (sum) before Adam. */
+int igs_comm_init(igs_ctx* ctx, const uint8_t id[128], int nranks, int rank);
+int igs_comm_destroy(igs_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

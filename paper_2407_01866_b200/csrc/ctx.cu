@@ -1,0 +1,775 @@
+// ctx.cu -- the C-ABI (include/igs_b200.h): context, device memory,
+// validation with the reference's error kinds/messages, and the host-side
+// drivers of the kernels in render.cu / train.cu / cull.cu / bsp.cu.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "igs_internal.cuh"
+
+using namespace igs_dev;
+
+// train.cu
+int igs_status_reset(igs_ctx* ctx);
+int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint32_t* dev_sidx,
+                         const double* dev_samples5, double* dev_loss, double inv_n);
+int igs_grad_check(igs_ctx* ctx);
+int igs_adam_launch(igs_ctx* ctx, const double* lr4, long long t);
+int igs_weights(igs_ctx* ctx, const double* q, const uint32_t* idx, size_t total, double* w);
+int igs_blend_points(igs_ctx* ctx, const double* lq, const uint32_t* li, uint32_t npts, int kk, double* rgb);
+// cull.cu
+int igs_raster_culled(igs_ctx* ctx, int W, int H, int k, int row0, int row1, float* out, uint32_t* topk);
+int igs_cull_lists(igs_ctx* ctx, int W, int H, int k, uint32_t* ntiles, uint64_t* total, uint32_t* offsets,
+                   uint32_t* members, double* tau);
+int igs_topk_samples_culled(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq);
+// metrics.cu
+int igs_error_map(igs_ctx* ctx, const float* dev_rendered, int W, int H, double* dev_p);
+int igs_psnr_dev(igs_ctx* ctx, const float* dev_a, const float* dev_b, size_t count, double* out);
+
+
+// ---------------------------------------------------------------------------
+// NCCL, resolved at first use with dlopen: the process may already hold a
+// libnccl.so.2 (e.g. torch's bundled 2.28 when torch.distributed is the
+// plumbing); linking the system one at load time would shadow it.
+// ---------------------------------------------------------------------------
+#ifndef IGS_NO_NCCL
+namespace {
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+};
+NcclApi& nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api;
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return api;
+    api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+    api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+    api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
+    api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce;
+    return api;
+}
+}  // namespace
+#endif
+
+// ---------------------------------------------------------------------------
+// plumbing
+// ---------------------------------------------------------------------------
+int igs_fail(igs_ctx* ctx, int code, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return code;
+}
+
+int igs_cuda_check(igs_ctx* ctx, cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return IGS_OK;
+    return igs_fail(ctx, IGS_E_CUDA, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+void* igs_scratch(igs_ctx* ctx, int slot, size_t bytes) {
+    DevBuf& b = ctx->scratch[slot];
+    if (bytes == 0) bytes = 16;
+    if (b.bytes >= bytes) return b.p;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    size_t want = std::max(bytes, b.bytes * 3 / 2);
+    if (cudaMalloc(&b.p, want) != cudaSuccess) {
+        cudaGetLastError();
+        if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            b.p = nullptr;
+            return nullptr;
+        }
+        want = bytes;
+    }
+    b.bytes = want;
+    return b.p;
+}
+
+static void* grow(DevBuf& b, size_t bytes) {
+    if (b.bytes >= bytes) return b.p;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        b.p = nullptr;
+        return nullptr;
+    }
+    b.bytes = bytes;
+    return b.p;
+}
+
+void* igs_pinned(igs_ctx* ctx, size_t bytes) {
+    if (ctx->pinned_bytes >= bytes) return ctx->pinned;
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    ctx->pinned = nullptr;
+    ctx->pinned_bytes = 0;
+    if (cudaMallocHost(&ctx->pinned, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    ctx->pinned_bytes = bytes;
+    return ctx->pinned;
+}
+
+int igs_ensure_image(igs_ctx* ctx, int w, int h) {
+    if (!grow(ctx->image, (size_t)w * h * 3 * sizeof(float)))
+        return igs_fail(ctx, IGS_E_CUDA, "out of device memory (image)");
+    ctx->img_w = w;
+    ctx->img_h = h;
+    return IGS_OK;
+}
+
+static int ensure_capacity(igs_ctx* ctx, uint32_t n, bool keep) {
+    if (n <= ctx->cap) return IGS_OK;
+    uint32_t cap = std::max<uint32_t>(n, ctx->cap + ctx->cap / 2);
+    cap = std::max<uint32_t>(cap, 64);
+    double *p, *g, *m, *v;
+    ScanRec* s;
+    ShadeRec* h;
+    const size_t rb = (size_t)cap * 8 * sizeof(double);
+    if (cudaMalloc(&p, rb) != cudaSuccess || cudaMalloc(&g, rb) != cudaSuccess || cudaMalloc(&m, rb) != cudaSuccess ||
+        cudaMalloc(&v, rb) != cudaSuccess || cudaMalloc(&s, (size_t)cap * sizeof(ScanRec)) != cudaSuccess ||
+        cudaMalloc(&h, (size_t)cap * sizeof(ShadeRec)) != cudaSuccess) {
+        cudaGetLastError();
+        return igs_fail(ctx, IGS_E_CUDA, "out of device memory (Gaussian set)");
+    }
+    if (keep && ctx->n) {
+        const size_t ob = (size_t)ctx->n * 8 * sizeof(double);
+        IGS_CUDA(ctx, cudaMemcpyAsync(p, ctx->params, ob, cudaMemcpyDeviceToDevice, ctx->stream));
+        IGS_CUDA(ctx, cudaMemcpyAsync(g, ctx->grads, ob, cudaMemcpyDeviceToDevice, ctx->stream));
+        IGS_CUDA(ctx, cudaMemcpyAsync(m, ctx->adam_m, ob, cudaMemcpyDeviceToDevice, ctx->stream));
+        IGS_CUDA(ctx, cudaMemcpyAsync(v, ctx->adam_v, ob, cudaMemcpyDeviceToDevice, ctx->stream));
+        IGS_CUDA(ctx, cudaMemcpyAsync(s, ctx->scan, (size_t)ctx->n * sizeof(ScanRec), cudaMemcpyDeviceToDevice,
+                                      ctx->stream));
+        IGS_CUDA(ctx, cudaMemcpyAsync(h, ctx->shade, (size_t)ctx->n * sizeof(ShadeRec), cudaMemcpyDeviceToDevice,
+                                      ctx->stream));
+        IGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    cudaFree(ctx->params);
+    cudaFree(ctx->grads);
+    cudaFree(ctx->adam_m);
+    cudaFree(ctx->adam_v);
+    cudaFree(ctx->scan);
+    cudaFree(ctx->shade);
+    ctx->params = p;
+    ctx->grads = g;
+    ctx->adam_m = m;
+    ctx->adam_v = v;
+    ctx->scan = s;
+    ctx->shade = h;
+    ctx->cap = cap;
+    return IGS_OK;
+}
+
+static int host_to_dev(igs_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    // Stage through pinned memory so the copy is a true async DMA.
+    void* pin = igs_pinned(ctx, bytes);
+    if (!pin) {
+        IGS_CUDA(ctx, cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+        return IGS_OK;
+    }
+    std::memcpy(pin, src, bytes);
+    IGS_CUDA(ctx, cudaMemcpyAsync(dst, pin, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    IGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return IGS_OK;
+}
+
+static int dev_to_host(igs_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    void* pin = igs_pinned(ctx, bytes);
+    if (!pin) {
+        IGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        IGS_CUDA(ctx, cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+        return IGS_OK;
+    }
+    IGS_CUDA(ctx, cudaMemcpyAsync(pin, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    IGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    std::memcpy(dst, pin, bytes);
+    return IGS_OK;
+}
+
+#define CHECK_CTX(ctx) \
+    if (!(ctx)) return IGS_E_INVALID_PARAMETER
+
+// renderer.cpp:12-14 require_nonempty
+static int require_nonempty(igs_ctx* ctx) {
+    if (ctx->n == 0) return igs_fail(ctx, IGS_E_EMPTY_SET, "operation requires a non-empty GaussianSet");
+    return IGS_OK;
+}
+static int require_k(igs_ctx* ctx, int k) {
+    if (k < 1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "k must be >= 1");
+    return IGS_OK;
+}
+
+extern "C" {
+
+int igs_ctx_create(int device, igs_ctx** out) {
+    if (!out) return IGS_E_INVALID_PARAMETER;
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return IGS_E_CUDA;
+    }
+    if (device < 0 || device >= ndev) return IGS_E_INVALID_PARAMETER;
+    if (cudaSetDevice(device) != cudaSuccess) return IGS_E_CUDA;
+    igs_ctx* ctx = new igs_ctx();
+    ctx->device = device;
+    cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMalloc(&ctx->status, 4 * sizeof(long long)) != cudaSuccess) {
+        delete ctx;
+        return IGS_E_CUDA;
+    }
+    *out = ctx;
+    return IGS_OK;
+}
+
+void igs_ctx_destroy(igs_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    igs_partition_free(ctx);
+#ifndef IGS_NO_NCCL
+    if (ctx->comm) nccl().commDestroy(ctx->comm);
+#endif
+    cudaFree(ctx->params);
+    cudaFree(ctx->grads);
+    cudaFree(ctx->adam_m);
+    cudaFree(ctx->adam_v);
+    cudaFree(ctx->scan);
+    cudaFree(ctx->shade);
+    cudaFree(ctx->image.p);
+    cudaFree(ctx->target.p);
+    cudaFree(ctx->samples.p);
+    cudaFree(ctx->status);
+    cudaFree(ctx->flush.p);
+    cudaFree(ctx->prof_dev_work);
+    for (auto& b : ctx->scratch) cudaFree(b.p);
+    for (auto& v : ctx->prof_ev)
+        for (auto e : v) cudaEventDestroy(e);
+    for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    for (auto e : ctx->timer)
+        if (e) cudaEventDestroy(e);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char* igs_last_error(const igs_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int igs_sync(igs_ctx* ctx) {
+    CHECK_CTX(ctx);
+    IGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return IGS_OK;
+}
+
+uint64_t igs_kernel_launches(const igs_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int igs_set_option(igs_ctx* ctx, int option, int64_t value) {
+    CHECK_CTX(ctx);
+    switch (option) {
+        case IGS_OPT_CULL: ctx->opt_cull = value ? 1 : 0; return IGS_OK;
+        case IGS_OPT_DETERMINISTIC: ctx->opt_deterministic = value ? 1 : 0; return IGS_OK;
+        case IGS_OPT_TILE:
+            if (value != 8 && value != 16 && value != 32)
+                return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "tile must be 8, 16 or 32");
+            ctx->opt_tile = (int)value;
+            return IGS_OK;
+    }
+    return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "unknown option");
+}
+
+int64_t igs_get_option(const igs_ctx* ctx, int option) {
+    if (!ctx) return -1;
+    switch (option) {
+        case IGS_OPT_CULL: return ctx->opt_cull;
+        case IGS_OPT_DETERMINISTIC: return ctx->opt_deterministic;
+        case IGS_OPT_TILE: return ctx->opt_tile;
+    }
+    return -1;
+}
+
+// ---- Gaussian set ----------------------------------------------------------
+int igs_set_params(igs_ctx* ctx, const double* params8, uint32_t n) {
+    CHECK_CTX(ctx);
+    if (n && !params8) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "null params");
+    cudaSetDevice(ctx->device);
+    int e = ensure_capacity(ctx, n, false);
+    if (e) return e;
+    ctx->n = n;
+    ctx->grads_valid = false;
+    igs_partition_free(ctx);
+    if (n == 0) return IGS_OK;
+    const size_t rb = (size_t)n * 8 * sizeof(double);
+    if ((e = host_to_dev(ctx, ctx->params, params8, rb))) return e;
+    IGS_CUDA(ctx, cudaMemsetAsync(ctx->adam_m, 0, rb, ctx->stream));
+    IGS_CUDA(ctx, cudaMemsetAsync(ctx->adam_v, 0, rb, ctx->stream));
+    IGS_CUDA(ctx, cudaMemsetAsync(ctx->grads, 0, rb, ctx->stream));
+    return igs_prepare_all(ctx, 0);
+}
+
+int igs_append_params(igs_ctx* ctx, const double* params8, uint32_t n) {
+    CHECK_CTX(ctx);
+    if (n == 0) return IGS_OK;
+    if (!params8) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "null params");
+    cudaSetDevice(ctx->device);
+    const uint32_t old = ctx->n;
+    int e = ensure_capacity(ctx, old + n, true);
+    if (e) return e;
+    const size_t rb = (size_t)n * 8 * sizeof(double);
+    if ((e = host_to_dev(ctx, ctx->params + (size_t)old * 8, params8, rb))) return e;
+    IGS_CUDA(ctx, cudaMemsetAsync(ctx->adam_m + (size_t)old * 8, 0, rb, ctx->stream));
+    IGS_CUDA(ctx, cudaMemsetAsync(ctx->adam_v + (size_t)old * 8, 0, rb, ctx->stream));
+    IGS_CUDA(ctx, cudaMemsetAsync(ctx->grads + (size_t)old * 8, 0, rb, ctx->stream));
+    ctx->n = old + n;
+    ctx->grads_valid = false;
+    igs_partition_free(ctx);  // a partition refers to the old count (bsp.cpp:278-282)
+    return igs_prepare_all(ctx, old);
+}
+
+int igs_get_params(igs_ctx* ctx, double* params8, uint32_t n) {
+    CHECK_CTX(ctx);
+    if (n != ctx->n) return igs_fail(ctx, IGS_E_DIMENSION_MISMATCH, "parameter count mismatch");
+    if (n == 0) return IGS_OK;
+    return dev_to_host(ctx, params8, ctx->params, (size_t)n * 8 * sizeof(double));
+}
+
+uint32_t igs_num_gaussians(const igs_ctx* ctx) { return ctx ? ctx->n : 0; }
+const double* igs_device_params(const igs_ctx* ctx) { return ctx ? ctx->params : nullptr; }
+const float* igs_device_image(const igs_ctx* ctx) { return ctx ? (const float*)ctx->image.p : nullptr; }
+const double* igs_device_grads(const igs_ctx* ctx) { return ctx ? ctx->grads : nullptr; }
+
+// ---- renderer ---------------------------------------------------------------
+static int render_rows(igs_ctx* ctx, int W, int H, int k, int row0, int row1, float* out_rgb, uint32_t* topk_idx) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    int e;
+    if ((e = require_nonempty(ctx))) return e;
+    if (W < 1 || H < 1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "render target must be at least 1x1");
+    if ((e = require_k(ctx, k))) return e;
+    if (row0 < 0 || row1 > H || row0 >= row1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "bad row range");
+    if ((e = igs_ensure_image(ctx, W, row1 - row0))) return e;
+    ctx->img_h = row1 - row0;
+    const int kk = (int)std::min<uint32_t>((uint32_t)k, ctx->n);
+    uint32_t* dtopk = nullptr;
+    if (topk_idx) {
+        dtopk = (uint32_t*)igs_scratch(ctx, 16, (size_t)W * H * kk * sizeof(uint32_t));
+        if (!dtopk) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (top-k dump)");
+    }
+    float* dout = (float*)ctx->image.p;
+    if (ctx->opt_cull) e = igs_raster_culled(ctx, W, H, k, row0, row1, dout, dtopk);
+    else e = igs_raster_global(ctx, W, H, k, row0, row1, dout, dtopk);
+    if (e) return e;
+    if (out_rgb && (e = dev_to_host(ctx, out_rgb, dout, (size_t)W * (row1 - row0) * 3 * sizeof(float)))) return e;
+    if (topk_idx &&
+        (e = dev_to_host(ctx, topk_idx + (size_t)row0 * W * kk, dtopk + (size_t)row0 * W * kk,
+                         (size_t)W * (row1 - row0) * kk * sizeof(uint32_t))))
+        return e;
+    return IGS_OK;
+}
+
+int igs_render_image(igs_ctx* ctx, int width, int height, int k, float* out_rgb, uint32_t* topk_idx) {
+    return render_rows(ctx, width, height, k, 0, height, out_rgb, topk_idx);
+}
+
+int igs_render_image_rows(igs_ctx* ctx, int width, int height, int k, int row0, int row1, float* out_rgb) {
+    return render_rows(ctx, width, height, k, row0, row1, out_rgb, nullptr);
+}
+
+static int points_topk(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t** dli, double** dlq,
+                       int* kk_out) {
+    int e;
+    if ((e = require_nonempty(ctx))) return e;
+    if ((e = require_k(ctx, k))) return e;
+    const int kk = (int)std::min<uint32_t>((uint32_t)k, ctx->n);
+    double* duv = (double*)igs_scratch(ctx, 17, (size_t)npts * 2 * sizeof(double));
+    uint32_t* li = (uint32_t*)igs_scratch(ctx, 18, (size_t)npts * kk * sizeof(uint32_t));
+    double* lq = (double*)igs_scratch(ctx, 19, (size_t)npts * kk * sizeof(double));
+    if (!duv || !li || !lq) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (points)");
+    if ((e = host_to_dev(ctx, duv, uv, (size_t)npts * 2 * sizeof(double)))) return e;
+    if (ctx->opt_cull) e = igs_topk_samples_culled(ctx, duv, npts, k, li, lq);
+    else e = igs_topk_points(ctx, duv, npts, k, li, lq);
+    if (e) return e;
+    *dli = li;
+    *dlq = lq;
+    *kk_out = kk;
+    return IGS_OK;
+}
+
+int igs_select_top_k(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* idx, double* weights,
+                     int32_t* counts) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    if (npts == 0) return IGS_OK;
+    uint32_t* li;
+    double* lq;
+    int kk, e;
+    if ((e = points_topk(ctx, uv, npts, k, &li, &lq, &kk))) return e;
+    const size_t total = (size_t)npts * kk;
+    double* w = (double*)igs_scratch(ctx, 20, total * sizeof(double));
+    if (!w) return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
+    if ((e = igs_weights(ctx, lq, li, total, w))) return e;
+    std::string tmp;
+    if (idx && (e = dev_to_host(ctx, idx, li, total * sizeof(uint32_t)))) return e;
+    if (weights && (e = dev_to_host(ctx, weights, w, total * sizeof(double)))) return e;
+    if (counts) {
+        uint32_t* h = idx;
+        std::vector<uint32_t> local;
+        if (!h) {
+            local.resize(total);
+            if ((e = dev_to_host(ctx, local.data(), li, total * sizeof(uint32_t)))) return e;
+            h = local.data();
+        }
+        for (uint32_t p = 0; p < npts; ++p) {
+            int c = 0;
+            while (c < kk && h[(size_t)p * kk + c] != kNoIdx) ++c;
+            counts[p] = c;
+        }
+    }
+    return IGS_OK;
+}
+
+int igs_render_points(igs_ctx* ctx, const double* uv, uint32_t npts, int k, double* rgb) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    if (npts == 0) return IGS_OK;
+    uint32_t* li;
+    double* lq;
+    int kk, e;
+    if ((e = points_topk(ctx, uv, npts, k, &li, &lq, &kk))) return e;
+    double* drgb = (double*)igs_scratch(ctx, 20, (size_t)npts * 3 * sizeof(double));
+    if (!drgb) return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
+    if ((e = igs_blend_points(ctx, lq, li, npts, kk, drgb))) return e;
+    if (rgb) return dev_to_host(ctx, rgb, drgb, (size_t)npts * 3 * sizeof(double));
+    return IGS_OK;
+}
+
+int igs_backward(igs_ctx* ctx, const double* samples5, uint32_t ns, int k, double* grads8) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    int e;
+    if (ctx->n == 0) return igs_fail(ctx, IGS_E_EMPTY_SET, "backward requires a non-empty GaussianSet");
+    if ((e = require_k(ctx, k))) return e;
+    // renderer.cpp:224-226: validate before any work
+    for (uint32_t i = 0; i < ns; ++i)
+        for (int c = 2; c < 5; ++c)
+            if (!std::isfinite(samples5[(size_t)i * 5 + c]))
+                return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "non-finite upstream gradient");
+    if (ns == 0) {
+        IGS_CUDA(ctx, cudaMemsetAsync(ctx->grads, 0, (size_t)ctx->n * 64, ctx->stream));
+    } else {
+        double* ds = (double*)igs_scratch(ctx, 15, (size_t)ns * 5 * sizeof(double));
+        if (!ds) return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
+        if ((e = host_to_dev(ctx, ds, samples5, (size_t)ns * 5 * sizeof(double)))) return e;
+        if ((e = igs_status_reset(ctx))) return e;
+        if ((e = igs_forward_backward(ctx, ns, k, 1, nullptr, ds, nullptr, 1.0))) return e;
+    }
+    ctx->grads_valid = true;
+    if (grads8) return dev_to_host(ctx, grads8, ctx->grads, (size_t)ctx->n * 64);
+    return IGS_OK;
+}
+
+// ---- training -----------------------------------------------------------------
+int igs_set_target(igs_ctx* ctx, const float* rgb, int width, int height) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    if (width < 1 || height < 1 || !rgb) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "bad target image");
+    const size_t bytes = (size_t)width * height * 3 * sizeof(float);
+    if (!grow(ctx->target, bytes)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (target)");
+    ctx->tgt_w = width;
+    ctx->tgt_h = height;
+    return host_to_dev(ctx, ctx->target.p, rgb, bytes);
+}
+
+static int allreduce_grads(igs_ctx* ctx, double* dev_loss) {
+#ifndef IGS_NO_NCCL
+    if (ctx->comm && ctx->nranks > 1) {
+        if (nccl().allReduce(ctx->grads, ctx->grads, (size_t)ctx->n * 8, ncclDouble, ncclSum, ctx->comm, ctx->stream) !=
+            ncclSuccess)
+            return igs_fail(ctx, IGS_E_CUDA, "ncclAllReduce(grads) failed");
+        if (dev_loss &&
+            nccl().allReduce(dev_loss, dev_loss, 1, ncclDouble, ncclSum, ctx->comm, ctx->stream) != ncclSuccess)
+            return igs_fail(ctx, IGS_E_CUDA, "ncclAllReduce(loss) failed");
+    }
+#else
+    (void)ctx;
+    (void)dev_loss;
+#endif
+    return IGS_OK;
+}
+
+static int train_checks(igs_ctx* ctx, uint32_t ns, int k) {
+    int e;
+    if ((e = require_nonempty(ctx))) return e;
+    if ((e = require_k(ctx, k))) return e;
+    if (!ctx->target.p) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "no target image (igs_set_target)");
+    if (ns < 1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "sample count must be >= 1");
+    return IGS_OK;
+}
+
+// status block layout on device: [0] first bad grad slot, [1] first bad
+// constrained Gaussian, [2] first non-finite loss sample (LLONG_MAX = none)
+static int read_status(igs_ctx* ctx, double* dev_loss, double* loss_out, int check_grads) {
+    struct {
+        long long st[4];
+        double loss;
+    } h;
+    int e;
+    if ((e = dev_to_host(ctx, h.st, ctx->status, sizeof(h.st)))) return e;
+    h.loss = 0.0;
+    if (dev_loss && (e = dev_to_host(ctx, &h.loss, dev_loss, sizeof(double)))) return e;
+    if (h.st[2] != LLONG_MAX) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "training loss became non-finite");
+    if (check_grads && h.st[0] != LLONG_MAX) {
+        static const char* names[8] = {"mu_u", "mu_v", "theta", "s1", "s2", "r", "g", "b"};
+        const long long slot = h.st[0];
+        return igs_fail(ctx, IGS_E_INVALID_PARAMETER,
+                        "non-finite gradient for Gaussian " + std::to_string(slot / 8) + " parameter " +
+                            names[slot % 8]);
+    }
+    if (h.st[1] != LLONG_MAX) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "non-finite Gaussian parameters");
+    if (loss_out) *loss_out = h.loss;
+    return IGS_OK;
+}
+
+static int upload_sidx(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, uint32_t** dev) {
+    const uint64_t npx = (uint64_t)ctx->tgt_w * ctx->tgt_h;
+    for (uint32_t i = 0; i < ns; ++i)
+        if (sample_idx[i] >= npx) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "sample index outside the target");
+    uint32_t* d = (uint32_t*)igs_scratch(ctx, 21, (size_t)ns * sizeof(uint32_t));
+    if (!d) return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
+    int e = host_to_dev(ctx, d, sample_idx, (size_t)ns * sizeof(uint32_t));
+    *dev = d;
+    return e;
+}
+
+int igs_train_step(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, int k, double* loss, double* grads8) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    int e;
+    if ((e = train_checks(ctx, ns, k))) return e;
+    uint32_t* dsidx;
+    if ((e = upload_sidx(ctx, sample_idx, ns, &dsidx))) return e;
+    double* dloss = (double*)igs_scratch(ctx, 14, 64 * sizeof(double));
+    if ((e = igs_status_reset(ctx))) return e;
+    const uint32_t ns_total = ns * (uint32_t)ctx->nranks;
+    if ((e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss, 1.0 / (double)ns_total))) return e;
+    if ((e = allreduce_grads(ctx, dloss))) return e;
+    if ((e = read_status(ctx, dloss, loss, 0))) return e;
+    if (grads8) return dev_to_host(ctx, grads8, ctx->grads, (size_t)ctx->n * 64);
+    return IGS_OK;
+}
+
+int igs_adam_step(igs_ctx* ctx, const double* lr4, long long t) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    if (t < 1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "Adam step index must be >= 1");
+    if (!lr4) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "null learning rates");
+    if (ctx->n == 0) return IGS_OK;
+    int e;
+    if ((e = igs_status_reset(ctx))) return e;
+    if ((e = igs_grad_check(ctx))) return e;
+    if ((e = igs_adam_launch(ctx, lr4, t))) return e;
+    return read_status(ctx, nullptr, nullptr, 1);
+}
+
+int igs_train_iteration(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, int k, const double* lr4,
+                        long long t, double* loss) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    int e;
+    if ((e = train_checks(ctx, ns, k))) return e;
+    if (t < 1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "Adam step index must be >= 1");
+    uint32_t* dsidx;
+    if ((e = upload_sidx(ctx, sample_idx, ns, &dsidx))) return e;
+    double* dloss = (double*)igs_scratch(ctx, 14, 64 * sizeof(double));
+    if ((e = igs_status_reset(ctx))) return e;
+    const uint32_t ns_total = ns * (uint32_t)ctx->nranks;
+    if ((e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss, 1.0 / (double)ns_total))) return e;
+    if ((e = allreduce_grads(ctx, dloss))) return e;
+    if ((e = igs_grad_check(ctx))) return e;
+    if ((e = igs_adam_launch(ctx, lr4, t))) return e;
+    return read_status(ctx, dloss, loss, 1);
+}
+
+int igs_upload_samples(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, uint32_t steps) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    if (!ctx->target.p) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "no target image (igs_set_target)");
+    const size_t total = (size_t)ns * steps;
+    const uint64_t npx = (uint64_t)ctx->tgt_w * ctx->tgt_h;
+    for (size_t i = 0; i < total; ++i)
+        if (sample_idx[i] >= npx) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "sample index outside the target");
+    if (!grow(ctx->samples, total * sizeof(uint32_t))) return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
+    ctx->samples_ns = ns;
+    ctx->samples_steps = steps;
+    return host_to_dev(ctx, ctx->samples.p, sample_idx, total * sizeof(uint32_t));
+}
+
+int igs_train_iterations(igs_ctx* ctx, uint32_t steps, int k, const double* lr4, long long t0, double* losses) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    int e;
+    const uint32_t ns = ctx->samples_ns;
+    if ((e = train_checks(ctx, ns, k))) return e;
+    if (ctx->samples_steps == 0) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "no uploaded samples");
+    if (t0 < 1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "Adam step index must be >= 1");
+    double* dloss = (double*)igs_scratch(ctx, 22, (size_t)std::max<uint32_t>(steps, 1) * sizeof(double));
+    if ((e = igs_status_reset(ctx))) return e;
+    const uint32_t ns_total = ns * (uint32_t)ctx->nranks;
+    for (uint32_t s = 0; s < steps; ++s) {
+        // step t uses uploaded slot (t-1) mod steps_uploaded
+        const uint32_t slot = (uint32_t)((t0 + s - 1) % (long long)ctx->samples_steps);
+        const uint32_t* dsidx = (const uint32_t*)ctx->samples.p + (size_t)slot * ns;
+        if ((e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss + s, 1.0 / (double)ns_total))) return e;
+        if ((e = allreduce_grads(ctx, dloss + s))) return e;
+        if ((e = igs_grad_check(ctx))) return e;
+        if ((e = igs_adam_launch(ctx, lr4, t0 + s))) return e;
+    }
+    igs_timer_autostop(ctx);  // device time of the loop excludes the status readback
+    if ((e = read_status(ctx, nullptr, nullptr, 1))) return e;
+    if (losses) return dev_to_host(ctx, losses, dloss, (size_t)steps * sizeof(double));
+    return IGS_OK;
+}
+
+int igs_get_grads(igs_ctx* ctx, double* grads8, uint32_t n) {
+    CHECK_CTX(ctx);
+    if (n != ctx->n) return igs_fail(ctx, IGS_E_DIMENSION_MISMATCH, "gradient count != Gaussian count");
+    if (n == 0) return IGS_OK;
+    return dev_to_host(ctx, grads8, ctx->grads, (size_t)n * 64);
+}
+
+int igs_get_adam_state(igs_ctx* ctx, double* m, double* v, uint32_t n) {
+    CHECK_CTX(ctx);
+    if (n != ctx->n) return igs_fail(ctx, IGS_E_DIMENSION_MISMATCH, "state size mismatch");
+    if (n == 0) return IGS_OK;
+    int e;
+    if (m && (e = dev_to_host(ctx, m, ctx->adam_m, (size_t)n * 64))) return e;
+    if (v && (e = dev_to_host(ctx, v, ctx->adam_v, (size_t)n * 64))) return e;
+    return IGS_OK;
+}
+
+int igs_set_adam_state(igs_ctx* ctx, const double* m, const double* v, uint32_t n) {
+    CHECK_CTX(ctx);
+    if (n != ctx->n) return igs_fail(ctx, IGS_E_DIMENSION_MISMATCH, "state size mismatch");
+    if (n == 0) return IGS_OK;
+    int e;
+    if (m && (e = host_to_dev(ctx, ctx->adam_m, m, (size_t)n * 64))) return e;
+    if (v && (e = host_to_dev(ctx, ctx->adam_v, v, (size_t)n * 64))) return e;
+    return IGS_OK;
+}
+
+// ---- error map & metrics -----------------------------------------------------
+static int stage_rendered(igs_ctx* ctx, const float* rendered, int W, int H, const float** dev) {
+    if (W != ctx->tgt_w || H != ctx->tgt_h || !ctx->target.p)
+        return igs_fail(ctx, IGS_E_DIMENSION_MISMATCH, "rendered/target dimensions differ");
+    if (!rendered) {
+        if (!ctx->image.p || ctx->img_w != W || ctx->img_h != H)
+            return igs_fail(ctx, IGS_E_DIMENSION_MISMATCH, "rendered/target dimensions differ");
+        *dev = (const float*)ctx->image.p;
+        return IGS_OK;
+    }
+    const size_t bytes = (size_t)W * H * 3 * sizeof(float);
+    float* d = (float*)igs_scratch(ctx, 23, bytes);
+    if (!d) return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
+    *dev = d;
+    return host_to_dev(ctx, d, rendered, bytes);
+}
+
+int igs_add_distribution(igs_ctx* ctx, const float* rendered, int width, int height, double* p) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    const float* dr;
+    int e;
+    if ((e = stage_rendered(ctx, rendered, width, height, &dr))) return e;
+    double* dp = (double*)igs_scratch(ctx, 12, (size_t)width * height * sizeof(double));
+    if (!dp) return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
+    if ((e = igs_error_map(ctx, dr, width, height, dp))) return e;
+    if (p) return dev_to_host(ctx, p, dp, (size_t)width * height * sizeof(double));
+    return IGS_OK;
+}
+
+int igs_psnr(igs_ctx* ctx, const float* rendered, int width, int height, double* out) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    const float* dr;
+    int e;
+    if ((e = stage_rendered(ctx, rendered, width, height, &dr))) return e;
+    return igs_psnr_dev(ctx, dr, (const float*)ctx->target.p, (size_t)width * height * 3, out);
+}
+
+int igs_tile_lists(igs_ctx* ctx, int width, int height, int k, uint32_t* ntiles, uint64_t* total, uint32_t* offsets,
+                   uint32_t* members, double* tau) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    int e;
+    if ((e = require_nonempty(ctx))) return e;
+    if (width < 1 || height < 1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "render target must be at least 1x1");
+    if ((e = require_k(ctx, k))) return e;
+    return igs_cull_lists(ctx, width, height, k, ntiles, total, offsets, members, tau);
+}
+
+// ---- multi-GPU -------------------------------------------------------------------
+int igs_comm_unique_id(uint8_t id[128]) {
+#ifndef IGS_NO_NCCL
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId u;
+    if (!nccl().ok || nccl().getUniqueId(&u) != ncclSuccess) return IGS_E_CUDA;
+    std::memcpy(id, &u, 128);
+    return IGS_OK;
+#else
+    (void)id;
+    return IGS_E_CUDA;
+#endif
+}
+
+int igs_comm_init(igs_ctx* ctx, const uint8_t id[128], int nranks, int rank) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    if (nranks < 1 || rank < 0 || rank >= nranks) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "bad rank");
+#ifndef IGS_NO_NCCL
+    if (!nccl().ok) return igs_fail(ctx, IGS_E_CUDA, "libnccl.so.2 not found");
+    if (ctx->comm) {
+        nccl().commDestroy(ctx->comm);
+        ctx->comm = nullptr;
+    }
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    if (nccl().commInitRank(&ctx->comm, nranks, u, rank) != ncclSuccess)
+        return igs_fail(ctx, IGS_E_CUDA, "ncclCommInitRank failed");
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+    return IGS_OK;
+#else
+    (void)id;
+    return igs_fail(ctx, IGS_E_CUDA, "built without NCCL");
+#endif
+}
+
+int igs_comm_destroy(igs_ctx* ctx) {
+    CHECK_CTX(ctx);
+#ifndef IGS_NO_NCCL
+    if (ctx->comm) nccl().commDestroy(ctx->comm);
+    ctx->comm = nullptr;
+#endif
+    ctx->nranks = 1;
+    ctx->rank = 0;
+    return IGS_OK;
+}
+
+}  // extern "C"

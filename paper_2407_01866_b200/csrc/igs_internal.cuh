@@ -1,0 +1,243 @@
+// igs_internal.cuh -- shared device records, context and helpers.
+//
+// Data layout in HBM (all device-resident across calls, grow-only):
+//   params   double[n][8]   the reference's Gaussian2D records (64 B/G)
+//   scan     ScanRec[n]     48 B: the ScanGaussian fields the top-K scan reads
+//                           (renderer.hpp:31-34), 16-B aligned for LDG.128
+//   shade    ShadeRec[n]    48 B: color + 1/s for blend and gradients
+//   grads    double[n][8]   GaussianGrad records (renderer.hpp:95-100)
+//   m, v     double[n][8]   Adam moments in record order (adam.hpp:20-31)
+//   image    float[H][W][3] last render; target float[H][W][3]
+// Compiled with -fmad=false: every double operation on a parity path rounds
+// like the reference's SSE2 code; FMAs only where written explicitly.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/igs_b200.h"
+#include "igs_math.cuh"
+
+#ifndef IGS_NO_NCCL
+#include <nccl.h>
+#endif
+
+namespace igs_dev {
+
+constexpr double kNormEps = 1e-8;   // renderer.hpp:14
+constexpr double kScaleMin = 1e-4;  // gaussian.hpp:12
+constexpr double kScaleMax = 2.0;   // gaussian.hpp:13
+constexpr double kPi = 3.141592653589793;
+constexpr uint32_t kNoIdx = 0xFFFFFFFFu;
+
+struct __align__(16) ScanRec {
+    double mu_x, mu_y, cos_t, sin_t, inv_a, inv_b;
+};
+struct __align__(16) ShadeRec {
+    double r, g, b, inv_s1, inv_s2, pad;
+};
+static_assert(sizeof(ScanRec) == 48, "ScanRec");
+static_assert(sizeof(ShadeRec) == 48, "ShadeRec");
+
+// renderer.cpp:17-23 mahalanobis_sq, each op rounded separately (no FMA).
+__device__ __forceinline__ double maha(const ScanRec& g, double x, double y) {
+    const double dx = __dsub_rn(x, g.mu_x);
+    const double dy = __dsub_rn(y, g.mu_y);
+    const double e1 = __dadd_rn(__dmul_rn(g.cos_t, dx), __dmul_rn(g.sin_t, dy));
+    const double e2 = __dadd_rn(__dmul_rn(-g.sin_t, dx), __dmul_rn(g.cos_t, dy));
+    return __dadd_rn(__dmul_rn(__dmul_rn(e1, e1), g.inv_a), __dmul_rn(__dmul_rn(e2, e2), g.inv_b));
+}
+
+// Register-resident top-K, sorted ascending by (q, idx) -- the strict total
+// order of select_top_k_entries (renderer.cpp:53-74).  Because the order is
+// total, the kept set and its order do not depend on scan order, so any
+// candidate order (tile lists, split scans) yields the reference's result.
+//
+// Layout: the kk live slots are the LAST kk of KCAP registers; the first
+// KCAP-kk hold a (-inf, 0) sentinel that compares below every candidate and
+// therefore never moves.  The current worst kept entry is always slot
+// KCAP-1, a static register index (a runtime "slot kk-1" would force the
+// array into local memory).  Unfilled live slots hold (+inf, kNoIdx).
+template <int KCAP>
+struct TopK {
+    double q[KCAP];
+    uint32_t i[KCAP];
+    int off;  // = KCAP - kk: first live slot
+
+    __device__ __forceinline__ void init(int kk) {
+        off = KCAP - kk;
+#pragma unroll
+        for (int j = 0; j < KCAP; ++j) {
+            const bool dead = j < off;
+            q[j] = __longlong_as_double(dead ? (long long)0xfff0000000000000ULL : 0x7ff0000000000000LL);
+            i[j] = dead ? 0u : kNoIdx;
+        }
+    }
+    __device__ __forceinline__ double tq() const { return q[KCAP - 1]; }
+    __device__ __forceinline__ bool beats(double cq, uint32_t ci) const {
+        return cq < q[KCAP - 1] || (cq == q[KCAP - 1] && ci < i[KCAP - 1]);
+    }
+    __device__ __forceinline__ void insert(double cq, uint32_t ci) {
+#pragma unroll
+        for (int j = 0; j < KCAP; ++j) {
+            const bool lt = cq < q[j] || (cq == q[j] && ci < i[j]);
+            const double tq2 = q[j];
+            const uint32_t ti2 = i[j];
+            q[j] = lt ? cq : tq2;
+            i[j] = lt ? ci : ti2;
+            cq = lt ? tq2 : cq;
+            ci = lt ? ti2 : ci;
+        }
+    }
+    __device__ __forceinline__ void offer(double cq, uint32_t ci) {
+        if (beats(cq, ci)) insert(cq, ci);
+    }
+    // j-th best (0-based) lives in slot off + j.
+    __device__ __forceinline__ bool live(int slot) const { return slot >= off && i[slot] != kNoIdx; }
+};
+
+// blend_entries (renderer.cpp:76-89) over the kept entries, best first.
+template <int KCAP>
+__device__ __forceinline__ double blend_topk(const TopK<KCAP>& t, const ShadeRec* __restrict__ shade, double* c) {
+    double total = 0.0, ar = 0.0, ag = 0.0, ab = 0.0;
+#pragma unroll
+    for (int j = 0; j < KCAP; ++j) {
+        if (t.live(j)) {
+            const double w = exp(__dmul_rn(-0.5, t.q[j]));
+            const ShadeRec s = shade[t.i[j]];
+            total = __dadd_rn(total, w);
+            ar = __dadd_rn(ar, __dmul_rn(w, s.r));
+            ag = __dadd_rn(ag, __dmul_rn(w, s.g));
+            ab = __dadd_rn(ab, __dmul_rn(w, s.b));
+        }
+    }
+    const double inv = __ddiv_rn(1.0, __dadd_rn(kNormEps, total));
+    c[0] = __dmul_rn(ar, inv);
+    c[1] = __dmul_rn(ag, inv);
+    c[2] = __dmul_rn(ab, inv);
+    return total;
+}
+
+// Writes the kk kept entries best-first to dq/di (either nullable).
+template <int KCAP>
+__device__ __forceinline__ void store_topk(const TopK<KCAP>& t, double* dq, uint32_t* di) {
+#pragma unroll
+    for (int j = 0; j < KCAP; ++j)
+        if (j >= t.off) {
+            if (dq) dq[j - t.off] = t.q[j];
+            if (di) di[j - t.off] = t.i[j];
+        }
+}
+
+__device__ __forceinline__ float clamp01f(double v) { return (float)(v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v)); }
+
+// pixel_center (image.hpp:18-20)
+__device__ __forceinline__ double center(int i, int n) { return __ddiv_rn(__dadd_rn((double)i, 0.5), (double)n); }
+
+}  // namespace igs_dev
+
+// ---------------------------------------------------------------------------
+// Context
+// ---------------------------------------------------------------------------
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+struct PartitionDev;  // bsp.cu
+
+struct igs_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    uint64_t launches = 0;
+    int sm_count = 148;
+
+    // options
+    int opt_cull = 1;
+    int opt_deterministic = 1;
+    int opt_tile = 16;
+
+    // set
+    uint32_t n = 0;
+    uint32_t cap = 0;
+    double* params = nullptr;
+    double* grads = nullptr;
+    double* adam_m = nullptr;
+    double* adam_v = nullptr;
+    igs_dev::ScanRec* scan = nullptr;
+    igs_dev::ShadeRec* shade = nullptr;
+    bool grads_valid = false;
+
+    // images
+    DevBuf image;
+    int img_w = 0, img_h = 0;
+    DevBuf target;
+    int tgt_w = 0, tgt_h = 0;
+
+    // per-call scratch (grow-only), indexed by purpose
+    DevBuf scratch[24];
+    // pinned host staging
+    void* pinned = nullptr;
+    size_t pinned_bytes = 0;
+    // device status word block: [0] error code flag, [1] first bad slot
+    long long* status = nullptr;
+
+    // uploaded samples for device-resident training
+    DevBuf samples;
+    uint32_t samples_ns = 0, samples_steps = 0;
+
+    PartitionDev* part = nullptr;
+
+    // profiling (igs_profile_*)
+    bool prof_on = false;
+    std::vector<cudaEvent_t> prof_ev[IGS_PROF_FAMILIES];  // begin/end pairs
+    double prof_work[IGS_PROF_FAMILIES] = {};
+    unsigned long long* prof_dev_work = nullptr;  // device work counters (pairs) per family
+    cudaEvent_t timer[2] = {nullptr, nullptr};
+    bool timer_armed = false;     // igs_timer_begin called, stop not yet recorded
+    bool timer_stopped = false;   // stop event already recorded by a device loop
+    DevBuf flush;
+    int flush_salt = 0;
+    std::vector<cudaEvent_t> ev_pool;
+
+#ifndef IGS_NO_NCCL
+    ncclComm_t comm = nullptr;
+#endif
+    int nranks = 1, rank = 0;
+};
+
+// helpers implemented in ctx.cu
+int igs_fail(igs_ctx* ctx, int code, const std::string& msg);
+int igs_cuda_check(igs_ctx* ctx, cudaError_t e, const char* what);
+void* igs_scratch(igs_ctx* ctx, int slot, size_t bytes);
+void* igs_pinned(igs_ctx* ctx, size_t bytes);
+int igs_ensure_image(igs_ctx* ctx, int w, int h);
+
+#define IGS_LAUNCHED(ctx)                                                   \
+    do {                                                                    \
+        (ctx)->launches++;                                                  \
+        cudaError_t _e = cudaGetLastError();                                \
+        if (_e != cudaSuccess) return igs_cuda_check((ctx), _e, "launch");  \
+    } while (0)
+
+#define IGS_CUDA(ctx, call)                                                 \
+    do {                                                                    \
+        cudaError_t _e = (call);                                            \
+        if (_e != cudaSuccess) return igs_cuda_check((ctx), _e, #call);     \
+    } while (0)
+
+// profiling helpers (prof.cu): bracket a family's launches
+void igs_prof_begin(igs_ctx* ctx, int fam);
+void igs_prof_end(igs_ctx* ctx, int fam, double host_work);
+unsigned long long* igs_prof_counter(igs_ctx* ctx, int fam);  // nullptr unless profiling
+// records the armed timer's stop event right after a device loop's last kernel
+void igs_timer_autostop(igs_ctx* ctx);
+
+// internal entry points shared between translation units
+int igs_prepare_all(igs_ctx* ctx, uint32_t first);
+int igs_raster_global(igs_ctx* ctx, int W, int H, int k, int row0, int row1, float* dev_out, uint32_t* dev_topk);
+int igs_topk_points(igs_ctx* ctx, const double* dev_uv, uint32_t npts, int k, uint32_t* dev_idx, double* dev_q);
+int igs_partition_free(igs_ctx* ctx);

@@ -1,0 +1,442 @@
+// train.cu -- kernel 4 (backward with sample-ordered reduction) and
+// kernel 5 (fused Adam + constrain + re-prepare).
+//
+// Reference: renderer.cpp:91-122 (sample_gradients), :193-252
+// (backward_into / ordered reduction), fit.cpp:51-106
+// (train_step_gradients), adam.cpp:10-52 (adam_step), gaussian.cpp:74-90
+// (constrain).
+//
+// Gradient reduction.  The reference accumulates grads[idx] += d in sample
+// order (renderer.cpp:251, fit.cpp:91-104).  Each sample contributes at most
+// once per Gaussian (its top-K indices are distinct), so the per-Gaussian
+// sum is the sequence of that Gaussian's contributions in ascending sample
+// index.  Deterministic mode (default) reproduces it bit for bit: a stable
+// radix sort of the NS*K contribution keys by Gaussian index keeps sample
+// order inside each key, then one thread per Gaussian sums its segment
+// sequentially starting from 0.0 -- the exact operation sequence of the
+// reference.  Fast mode accumulates with fp64 atomics instead
+// (order-nondeterministic, ~1e-16 relative).
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "igs_internal.cuh"
+
+using namespace igs_dev;
+
+int igs_topk_samples_culled(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq);
+
+namespace {
+
+__device__ __forceinline__ double sign_of(double v) { return v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : 0.0); }
+
+// Per-sample coordinates from flat target indices (fit.cpp:67-70).
+__global__ void sample_coords_kernel(const uint32_t* __restrict__ sidx, uint32_t ns, int W, int H,
+                                     double* __restrict__ uv) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ns) return;
+    const int f = (int)sidx[i];
+    const int h = f / W, w = f % W;
+    uv[2 * (size_t)i] = center(w, W);
+    uv[2 * (size_t)i + 1] = center(h, H);
+}
+
+// One thread per sample: blend its top-K, derive the upstream gradient
+// (train: sign(diff)/ns of the L1 loss; backward: given), and emit the K
+// SampleContrib records (renderer.cpp:91-122) plus a sort key per record.
+// mode 0 = train (target image), 1 = backward (samples5 upstream).
+__global__ void sample_finish_kernel(const ScanRec* __restrict__ scan, const ShadeRec* __restrict__ shade,
+                                     uint32_t n, const double* __restrict__ lq, const uint32_t* __restrict__ li,
+                                     int kk, uint32_t ns, const double* __restrict__ uv, int mode,
+                                     const uint32_t* __restrict__ sidx, const float* __restrict__ target, int W,
+                                     const double* __restrict__ samples5, double inv_n, double* __restrict__ losses,
+                                     double* __restrict__ contrib, uint32_t* __restrict__ keys,
+                                     double* __restrict__ grads_atomic, long long* __restrict__ status) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= ns) return;
+    const double x = uv[2 * (size_t)s], y = uv[2 * (size_t)s + 1];
+    const double* q = lq + (size_t)s * kk;
+    const uint32_t* ix = li + (size_t)s * kk;
+    int cnt = 0;
+    double total = 0.0, ar = 0.0, ag = 0.0, ab = 0.0;
+    for (int j = 0; j < kk; ++j) {
+        const uint32_t ci = ix[j];
+        if (ci == kNoIdx) break;
+        const double w = exp(__dmul_rn(-0.5, q[j]));
+        const ShadeRec h = shade[ci];
+        total = __dadd_rn(total, w);
+        ar = __dadd_rn(ar, __dmul_rn(w, h.r));
+        ag = __dadd_rn(ag, __dmul_rn(w, h.g));
+        ab = __dadd_rn(ab, __dmul_rn(w, h.b));
+        ++cnt;
+    }
+    const double inv_denom = __ddiv_rn(1.0, __dadd_rn(kNormEps, total));
+    const double c0 = __dmul_rn(ar, inv_denom), c1 = __dmul_rn(ag, inv_denom), c2 = __dmul_rn(ab, inv_denom);
+    double up0, up1, up2;
+    if (mode == 0) {
+        const float* t = target + (size_t)sidx[s] * 3;
+        const double d0 = __dsub_rn(c0, (double)t[0]);
+        const double d1 = __dsub_rn(c1, (double)t[1]);
+        const double d2 = __dsub_rn(c2, (double)t[2]);
+        const double l = __dadd_rn(__dadd_rn(fabs(d0), fabs(d1)), fabs(d2));
+        losses[s] = l;
+        if (!isfinite(l)) atomicMin(status + 2, (long long)s);  // fit.cpp:155 non-finite loss
+        up0 = __dmul_rn(sign_of(d0), inv_n);
+        up1 = __dmul_rn(sign_of(d1), inv_n);
+        up2 = __dmul_rn(sign_of(d2), inv_n);
+    } else {
+        up0 = samples5[(size_t)s * 5 + 2];
+        up1 = samples5[(size_t)s * 5 + 3];
+        up2 = samples5[(size_t)s * 5 + 4];
+    }
+    for (int j = 0; j < kk; ++j) {
+        const size_t slot = (size_t)s * kk + j;
+        if (j >= cnt) {
+            if (keys) keys[slot] = n;  // sorts past every real index
+            continue;
+        }
+        const uint32_t ci = ix[j];
+        const ScanRec g = scan[ci];
+        const ShadeRec h = shade[ci];
+        const double w = exp(__dmul_rn(-0.5, q[j]));
+        const double dL_dw = __dmul_rn(
+            __dadd_rn(__dadd_rn(__dmul_rn(up0, __dsub_rn(h.r, c0)), __dmul_rn(up1, __dsub_rn(h.g, c1))),
+                      __dmul_rn(up2, __dsub_rn(h.b, c2))),
+            inv_denom);
+        const double wc = __dmul_rn(w, inv_denom);
+        const double dx = __dsub_rn(x, g.mu_x);
+        const double dy = __dsub_rn(y, g.mu_y);
+        const double e1 = __dadd_rn(__dmul_rn(g.cos_t, dx), __dmul_rn(g.sin_t, dy));
+        const double e2 = __dadd_rn(__dmul_rn(-g.sin_t, dx), __dmul_rn(g.cos_t, dy));
+        const double v1 = __dmul_rn(e1, g.inv_a);
+        const double v2 = __dmul_rn(e2, g.inv_b);
+        const double lw = __dmul_rn(dL_dw, w);
+        double d[8];
+        d[0] = __dmul_rn(lw, __dsub_rn(__dmul_rn(g.cos_t, v1), __dmul_rn(g.sin_t, v2)));
+        d[1] = __dmul_rn(lw, __dadd_rn(__dmul_rn(g.sin_t, v1), __dmul_rn(g.cos_t, v2)));
+        d[2] = __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(dL_dw, -w), e1), e2), __dsub_rn(g.inv_a, g.inv_b));
+        d[3] = __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(lw, e1), e1), g.inv_a), h.inv_s1);
+        d[4] = __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(lw, e2), e2), g.inv_b), h.inv_s2);
+        d[5] = __dmul_rn(up0, wc);
+        d[6] = __dmul_rn(up1, wc);
+        d[7] = __dmul_rn(up2, wc);
+        if (grads_atomic) {
+#pragma unroll
+            for (int p = 0; p < 8; ++p) atomicAdd(grads_atomic + (size_t)ci * 8 + p, d[p]);
+        } else {
+            double2* o = reinterpret_cast<double2*>(contrib + slot * 8);
+            o[0] = make_double2(d[0], d[1]);
+            o[1] = make_double2(d[2], d[3]);
+            o[2] = make_double2(d[4], d[5]);
+            o[3] = make_double2(d[6], d[7]);
+            keys[slot] = ci;
+        }
+    }
+}
+
+// One thread per Gaussian: its contributions are the sorted segment
+// [lower_bound(g), lower_bound(g+1)); summed in sample order from 0.0.
+__global__ void segment_reduce_kernel(const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
+                                      uint32_t nitems, const double* __restrict__ contrib, uint32_t n,
+                                      double* __restrict__ grads) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    uint32_t lo = 0, hi = nitems;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (skeys[mid] < g) lo = mid + 1;
+        else hi = mid;
+    }
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (uint32_t e = lo; e < nitems && skeys[e] == g; ++e) {
+        const double2* c = reinterpret_cast<const double2*>(contrib + (size_t)svals[e] * 8);
+        const double2 a = c[0], b = c[1], cc = c[2], d = c[3];
+        acc[0] = __dadd_rn(acc[0], a.x);
+        acc[1] = __dadd_rn(acc[1], a.y);
+        acc[2] = __dadd_rn(acc[2], b.x);
+        acc[3] = __dadd_rn(acc[3], b.y);
+        acc[4] = __dadd_rn(acc[4], cc.x);
+        acc[5] = __dadd_rn(acc[5], cc.y);
+        acc[6] = __dadd_rn(acc[6], d.x);
+        acc[7] = __dadd_rn(acc[7], d.y);
+    }
+    double2* o = reinterpret_cast<double2*>(grads + (size_t)g * 8);
+    o[0] = make_double2(acc[0], acc[1]);
+    o[1] = make_double2(acc[2], acc[3]);
+    o[2] = make_double2(acc[4], acc[5]);
+    o[3] = make_double2(acc[6], acc[7]);
+}
+
+__global__ void iota_kernel(uint32_t* v, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = i;
+}
+
+// Deterministic loss sum (fixed tree order), times 1/ns.  One CTA.
+__global__ void loss_reduce_kernel(const double* __restrict__ losses, uint32_t ns, double inv_n,
+                                   double* __restrict__ out) {
+    __shared__ double sm[1024];
+    double acc = 0.0;
+    for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) acc = __dadd_rn(acc, losses[i]);
+    sm[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) sm[threadIdx.x] = __dadd_rn(sm[threadIdx.x], sm[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = __dmul_rn(sm[0], inv_n);
+}
+
+// Non-finite gradient scan: status[0] <- first bad slot i*8+p (min).
+__global__ void grad_check_kernel(const double* __restrict__ grads, uint32_t n, long long* __restrict__ status) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+        if (!isfinite(grads[(size_t)i * 8 + p])) {
+            atomicMin(status, (long long)i * 8 + p);
+            return;
+        }
+}
+
+__device__ __forceinline__ double clamp01d(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
+__device__ __forceinline__ double clamp_scale(double v) {
+    return v < kScaleMin ? kScaleMin : (v > kScaleMax ? kScaleMax : v);
+}
+
+// Kernel 5: Adam (adam.cpp:21-51) + constrain (gaussian.cpp:74-90) +
+// PreparedSet refresh for the next step, one thread per Gaussian.  Skips
+// all writes when a non-finite gradient or loss was flagged this step, so a
+// failed step leaves the set untouched.  HBM: 256 B read + 192 B written
+// for params/grads/m/v, plus 96 B of refreshed scan/shade records.
+__global__ void adam_kernel(double* __restrict__ params, const double* __restrict__ grads, double* __restrict__ m,
+                            double* __restrict__ v, ScanRec* __restrict__ scan, ShadeRec* __restrict__ shade,
+                            uint32_t n, double lr_mu, double lr_color, double lr_scale, double lr_theta, double bc1,
+                            double bc2, const long long* __restrict__ status) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (status[0] != LLONG_MAX || status[2] != LLONG_MAX) return;
+    const double b1 = 0.9, b2 = 0.999, eps = 1e-8;  // adam.hpp:33-35
+    const double omb1 = 1.0 - b1, omb2 = 1.0 - b2;  // folded exactly like the reference's constants
+    const double lr8[8] = {lr_mu, lr_mu, lr_theta, lr_scale, lr_scale, lr_color, lr_color, lr_color};
+    double gp[8], gg[8], mm[8], vv[8];
+    const double2* P = reinterpret_cast<const double2*>(params + (size_t)i * 8);
+    const double2* G = reinterpret_cast<const double2*>(grads + (size_t)i * 8);
+    const double2* M = reinterpret_cast<const double2*>(m + (size_t)i * 8);
+    const double2* V = reinterpret_cast<const double2*>(v + (size_t)i * 8);
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+        const double2 a = P[h], b = G[h], c = M[h], d = V[h];
+        gp[2 * h] = a.x; gp[2 * h + 1] = a.y;
+        gg[2 * h] = b.x; gg[2 * h + 1] = b.y;
+        mm[2 * h] = c.x; mm[2 * h + 1] = c.y;
+        vv[2 * h] = d.x; vv[2 * h + 1] = d.y;
+    }
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+        const double g = gg[p];
+        mm[p] = __dadd_rn(__dmul_rn(b1, mm[p]), __dmul_rn(omb1, g));
+        vv[p] = __dadd_rn(__dmul_rn(b2, vv[p]), __dmul_rn(__dmul_rn(omb2, g), g));
+        const double m_hat = __ddiv_rn(mm[p], bc1);
+        const double v_hat = __ddiv_rn(vv[p], bc2);
+        const double upd = __ddiv_rn(__dmul_rn(lr8[p], m_hat), __dadd_rn(__dsqrt_rn(v_hat), eps));
+        gp[p] = __dsub_rn(gp[p], upd);
+    }
+    // constrain (gaussian.cpp:74-90); a non-finite result raises there.
+    bool finite_all = true;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) finite_all = finite_all && isfinite(gp[p]);
+    if (!finite_all) {
+        atomicMin((long long*)status + 1, (long long)i);
+        return;
+    }
+    gp[0] = clamp01d(gp[0]);
+    gp[1] = clamp01d(gp[1]);
+    double th = fmod(gp[2], kPi);
+    if (th < 0.0) th = __dadd_rn(th, kPi);
+    if (th >= kPi) th = 0.0;
+    gp[2] = th;
+    gp[3] = clamp_scale(gp[3]);
+    gp[4] = clamp_scale(gp[4]);
+    gp[5] = clamp01d(gp[5]);
+    gp[6] = clamp01d(gp[6]);
+    gp[7] = clamp01d(gp[7]);
+    double2* Pw = reinterpret_cast<double2*>(params + (size_t)i * 8);
+    double2* Mw = reinterpret_cast<double2*>(m + (size_t)i * 8);
+    double2* Vw = reinterpret_cast<double2*>(v + (size_t)i * 8);
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+        Pw[h] = make_double2(gp[2 * h], gp[2 * h + 1]);
+        Mw[h] = make_double2(mm[2 * h], mm[2 * h + 1]);
+        Vw[h] = make_double2(vv[2 * h], vv[2 * h + 1]);
+    }
+    // refresh the prepared records (renderer.cpp:37-50) for the next step
+    double s, co;
+    igs_math::cr_sincos(gp[2], &s, &co);
+    const double inv_s1 = __ddiv_rn(1.0, gp[3]);
+    const double inv_s2 = __ddiv_rn(1.0, gp[4]);
+    ScanRec r;
+    r.mu_x = gp[0];
+    r.mu_y = gp[1];
+    r.cos_t = co;
+    r.sin_t = s;
+    r.inv_a = __dmul_rn(inv_s1, inv_s1);
+    r.inv_b = __dmul_rn(inv_s2, inv_s2);
+    scan[i] = r;
+    ShadeRec hh;
+    hh.r = gp[5];
+    hh.g = gp[6];
+    hh.b = gp[7];
+    hh.inv_s1 = inv_s1;
+    hh.inv_s2 = inv_s2;
+    hh.pad = 0.0;
+    shade[i] = hh;
+}
+
+__global__ void reset_status_kernel(long long* status) {
+    if (threadIdx.x < 4) status[threadIdx.x] = LLONG_MAX;
+}
+
+__global__ void weights_kernel(const double* __restrict__ q, const uint32_t* __restrict__ idx, size_t total,
+                               double* __restrict__ w) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    w[i] = idx[i] == kNoIdx ? 0.0 : exp(__dmul_rn(-0.5, q[i]));
+}
+
+__global__ void blend_points_kernel(const double* __restrict__ lq, const uint32_t* __restrict__ li,
+                                    const ShadeRec* __restrict__ shade, uint32_t npts, int kk,
+                                    double* __restrict__ rgb) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= npts) return;
+    double total = 0.0, ar = 0.0, ag = 0.0, ab = 0.0;
+    for (int j = 0; j < kk; ++j) {
+        const uint32_t ci = li[(size_t)p * kk + j];
+        if (ci == kNoIdx) break;
+        const double w = exp(__dmul_rn(-0.5, lq[(size_t)p * kk + j]));
+        const ShadeRec s = shade[ci];
+        total = __dadd_rn(total, w);
+        ar = __dadd_rn(ar, __dmul_rn(w, s.r));
+        ag = __dadd_rn(ag, __dmul_rn(w, s.g));
+        ab = __dadd_rn(ab, __dmul_rn(w, s.b));
+    }
+    const double inv = __ddiv_rn(1.0, __dadd_rn(kNormEps, total));
+    rgb[(size_t)p * 3 + 0] = __dmul_rn(ar, inv);
+    rgb[(size_t)p * 3 + 1] = __dmul_rn(ag, inv);
+    rgb[(size_t)p * 3 + 2] = __dmul_rn(ab, inv);
+}
+
+}  // namespace
+
+// Scratch slot map (igs_scratch): 0 uv, 1 list q, 2 list idx, 3 contrib,
+// 4 keys, 5 keys sorted, 6 vals, 7 vals sorted, 8 cub temp, 9 losses,
+// 10/11 point partials, 12/13 generic lists, 14 loss out, 15 upstream samples.
+
+int igs_status_reset(igs_ctx* ctx) {
+    reset_status_kernel<<<1, 32, 0, ctx->stream>>>(ctx->status);
+    IGS_LAUNCHED(ctx);
+    return IGS_OK;
+}
+
+// Shared forward/backward over ns device points.  mode 0: train (sidx +
+// target), mode 1: backward (samples5 on device).  Writes ctx->grads and,
+// in train mode, the loss into *dev_loss.
+int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint32_t* dev_sidx,
+                         const double* dev_samples5, double* dev_loss, double inv_n) {
+    const uint32_t n = ctx->n;
+    const int kk = (int)std::min<uint32_t>((uint32_t)k, n);
+    double* uv = (double*)igs_scratch(ctx, 0, (size_t)ns * 2 * sizeof(double));
+    double* lq = (double*)igs_scratch(ctx, 1, (size_t)ns * kk * sizeof(double));
+    uint32_t* li = (uint32_t*)igs_scratch(ctx, 2, (size_t)ns * kk * sizeof(uint32_t));
+    double* losses = (double*)igs_scratch(ctx, 9, (size_t)std::max<uint32_t>(ns, 1) * sizeof(double));
+    if (!uv || !lq || !li || !losses) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (train)");
+    const int tb = 256;
+    if (mode == 0) {
+        sample_coords_kernel<<<(ns + tb - 1) / tb, tb, 0, ctx->stream>>>(dev_sidx, ns, ctx->tgt_w, ctx->tgt_h, uv);
+        IGS_LAUNCHED(ctx);
+    } else {
+        IGS_CUDA(ctx, cudaMemcpy2DAsync(uv, 2 * sizeof(double), dev_samples5, 5 * sizeof(double),
+                                        2 * sizeof(double), ns, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    int e = ctx->opt_cull ? igs_topk_samples_culled(ctx, uv, ns, k, li, lq) : igs_topk_points(ctx, uv, ns, k, li, lq);
+    if (e) return e;
+    const size_t items = (size_t)ns * kk;
+    if (ctx->opt_deterministic) {
+        double* contrib = (double*)igs_scratch(ctx, 3, items * 8 * sizeof(double));
+        uint32_t* keys = (uint32_t*)igs_scratch(ctx, 4, items * sizeof(uint32_t));
+        uint32_t* skeys = (uint32_t*)igs_scratch(ctx, 5, items * sizeof(uint32_t));
+        uint32_t* vals = (uint32_t*)igs_scratch(ctx, 6, items * sizeof(uint32_t));
+        uint32_t* svals = (uint32_t*)igs_scratch(ctx, 7, items * sizeof(uint32_t));
+        if (!contrib || !keys || !skeys || !vals || !svals) return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
+        igs_prof_begin(ctx, IGS_PROF_FINISH);
+        sample_finish_kernel<<<(ns + 127) / 128, 128, 0, ctx->stream>>>(
+            ctx->scan, ctx->shade, n, lq, li, kk, ns, uv, mode, dev_sidx, (const float*)ctx->target.p, ctx->tgt_w,
+            dev_samples5, inv_n, losses, contrib, keys, nullptr, ctx->status);
+        IGS_LAUNCHED(ctx);
+        igs_prof_end(ctx, IGS_PROF_FINISH, (double)items);
+        igs_prof_begin(ctx, IGS_PROF_REDUCE);
+        iota_kernel<<<(unsigned)((items + 255) / 256), 256, 0, ctx->stream>>>(vals, (uint32_t)items);
+        IGS_LAUNCHED(ctx);
+        int end_bit = 1;
+        while (end_bit < 32 && ((uint64_t)1 << end_bit) <= (uint64_t)n) ++end_bit;
+        size_t temp_bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys, skeys, vals, svals, (int)items, 0, end_bit,
+                                        ctx->stream);
+        void* temp = igs_scratch(ctx, 8, temp_bytes);
+        if (!temp) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (sort)");
+        IGS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, skeys, vals, svals, (int)items, 0,
+                                                      end_bit, ctx->stream));
+        ctx->launches += (uint64_t)((end_bit + 7) / 8) * 3;  // onesweep: histogram + per-pass kernels (approx.)
+        segment_reduce_kernel<<<(n + 255) / 256, 256, 0, ctx->stream>>>(skeys, svals, (uint32_t)items, contrib, n,
+                                                                        ctx->grads);
+        IGS_LAUNCHED(ctx);
+        igs_prof_end(ctx, IGS_PROF_REDUCE, (double)items);
+    } else {
+        IGS_CUDA(ctx, cudaMemsetAsync(ctx->grads, 0, (size_t)n * 8 * sizeof(double), ctx->stream));
+        sample_finish_kernel<<<(ns + 127) / 128, 128, 0, ctx->stream>>>(
+            ctx->scan, ctx->shade, n, lq, li, kk, ns, uv, mode, dev_sidx, (const float*)ctx->target.p, ctx->tgt_w,
+            dev_samples5, inv_n, losses, nullptr, nullptr, ctx->grads, ctx->status);
+        IGS_LAUNCHED(ctx);
+    }
+    if (mode == 0 && dev_loss) {
+        loss_reduce_kernel<<<1, 1024, 0, ctx->stream>>>(losses, ns, inv_n, dev_loss);
+        IGS_LAUNCHED(ctx);
+    }
+    ctx->grads_valid = true;
+    return IGS_OK;
+}
+
+int igs_grad_check(igs_ctx* ctx) {
+    grad_check_kernel<<<(ctx->n + 255) / 256, 256, 0, ctx->stream>>>(ctx->grads, ctx->n, ctx->status);
+    IGS_LAUNCHED(ctx);
+    return IGS_OK;
+}
+
+int igs_adam_launch(igs_ctx* ctx, const double* lr4, long long t) {
+    // Bias corrections with the host libm pow, as adam.cpp:16-17.
+    const double bc1 = 1.0 - std::pow(0.9, (double)t);
+    const double bc2 = 1.0 - std::pow(0.999, (double)t);
+    igs_prof_begin(ctx, IGS_PROF_ADAM);
+    adam_kernel<<<(ctx->n + 255) / 256, 256, 0, ctx->stream>>>(ctx->params, ctx->grads, ctx->adam_m, ctx->adam_v,
+                                                               ctx->scan, ctx->shade, ctx->n, lr4[0], lr4[1], lr4[2],
+                                                               lr4[3], bc1, bc2, ctx->status);
+    IGS_LAUNCHED(ctx);
+    // algorithmic bytes: read params/grads/m/v (256 B), write params/m/v
+    // (192 B) and the refreshed 96 B of scan+shade records
+    igs_prof_end(ctx, IGS_PROF_ADAM, (double)ctx->n * 544.0);
+    return IGS_OK;
+}
+
+int igs_weights(igs_ctx* ctx, const double* q, const uint32_t* idx, size_t total, double* w) {
+    weights_kernel<<<(unsigned)((total + 255) / 256), 256, 0, ctx->stream>>>(q, idx, total, w);
+    IGS_LAUNCHED(ctx);
+    return IGS_OK;
+}
+
+int igs_blend_points(igs_ctx* ctx, const double* lq, const uint32_t* li, uint32_t npts, int kk, double* rgb) {
+    blend_points_kernel<<<(npts + 127) / 128, 128, 0, ctx->stream>>>(lq, li, ctx->shade, npts, kk, rgb);
+    IGS_LAUNCHED(ctx);
+    return IGS_OK;
+}

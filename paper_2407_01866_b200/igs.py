@@ -1,0 +1,406 @@
+"""Python binding of the B200 C-ABI (include/igs_b200.h) via ctypes.
+
+Mirrors the reference's hot-path API (proj/include/igs/*.hpp) with the same
+names, argument meaning and error kinds:
+
+    reference (C++)                            here (Python)
+    render_image(set, W, H, k)                 Context.render_image(W, H, k)
+    select_top_k(set, x, k)                    Context.select_top_k(uv, k)
+    render_topk(set, x, k)                     Context.render_points(uv, k)
+    backward(set, samples, k)                  Context.backward(samples, k)
+    train_step_gradients(ps, target, idx, k)   Context.train_step(idx, k)
+    adam_step(set, grads, state, lr, t)        Context.adam_step(lr, t)
+    add_distribution(rendered, target)         Context.add_distribution(W, H)
+    psnr(rendered, target)                     Context.psnr(W, H)
+    build_partition(set, n_max)                Context.partition_build(n_max)
+    rebuild_partition(blocks, set)             Context.partition_rebuild(rects)
+    render_image_blocked(set, p, W, H, k)      Context.render_image_blocked(W, H, k)
+    render_topk_blocked(set, p, x, k)          Context.render_points_blocked(uv, k)
+    locate_block(p, x)                         Context.locate_blocks(uv)
+
+The Gaussian set is device-resident in the Context (set_params /
+append_params / get_params); records are the reference's 8-double layout.
+Errors raise IgsError whose .kind is the reference ErrorKind name.
+
+There is no CPU fallback: importing this module without the built CUDA
+extension raises, and every call runs on the GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "libigs_b200.so"
+
+ERROR_KINDS = {
+    1: "invalid_parameter",
+    2: "dimension_mismatch",
+    3: "bad_magic",
+    4: "bad_version",
+    5: "truncated",
+    6: "empty_set",
+    7: "io",
+    8: "unsupported_format",
+    100: "cuda",
+}
+
+OPT_CULL, OPT_DETERMINISTIC, OPT_TILE = 1, 2, 3
+PROF_SCAN, PROF_FINISH, PROF_REDUCE, PROF_ADAM, PROF_CULL, PROF_BLOCKED = range(6)
+PROF_NAMES = ["scan", "finish", "reduce", "adam", "cull", "blocked"]
+
+# Learning rates in the reference's LearningRates field order (adam.hpp:11-16).
+DEFAULT_LR = (2e-4, 2e-3, 1e-3, 1e-3)  # mu, color, scale, theta
+DEFAULT_K = 10  # renderer.hpp:16 kDefaultTopK
+
+
+class IgsError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        self.code = code
+        self.kind = ERROR_KINDS.get(code, f"code{code}")
+        super().__init__(f"[{self.kind}] {msg}")
+
+
+_dp = C.POINTER(C.c_double)
+_fp = C.POINTER(C.c_float)
+_up = C.POINTER(C.c_uint32)
+_u8p = C.POINTER(C.c_uint8)
+_i32p = C.POINTER(C.c_int32)
+_u64p = C.POINTER(C.c_uint64)
+_vp = C.c_void_p
+
+# name -> (restype, argtypes); the full export set of include/igs_b200.h
+SIGNATURES = {
+    "igs_ctx_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
+    "igs_ctx_destroy": (None, [_vp]),
+    "igs_last_error": (C.c_char_p, [_vp]),
+    "igs_sync": (C.c_int, [_vp]),
+    "igs_kernel_launches": (C.c_uint64, [_vp]),
+    "igs_set_option": (C.c_int, [_vp, C.c_int, C.c_int64]),
+    "igs_get_option": (C.c_int64, [_vp, C.c_int]),
+    "igs_set_params": (C.c_int, [_vp, _dp, C.c_uint32]),
+    "igs_append_params": (C.c_int, [_vp, _dp, C.c_uint32]),
+    "igs_get_params": (C.c_int, [_vp, _dp, C.c_uint32]),
+    "igs_num_gaussians": (C.c_uint32, [_vp]),
+    "igs_device_params": (_vp, [_vp]),
+    "igs_render_image": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _fp, _up]),
+    "igs_render_image_rows": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _fp]),
+    "igs_device_image": (_vp, [_vp]),
+    "igs_select_top_k": (C.c_int, [_vp, _dp, C.c_uint32, C.c_int, _up, _dp, _i32p]),
+    "igs_render_points": (C.c_int, [_vp, _dp, C.c_uint32, C.c_int, _dp]),
+    "igs_backward": (C.c_int, [_vp, _dp, C.c_uint32, C.c_int, _dp]),
+    "igs_set_target": (C.c_int, [_vp, _fp, C.c_int, C.c_int]),
+    "igs_train_step": (C.c_int, [_vp, _up, C.c_uint32, C.c_int, _dp, _dp]),
+    "igs_adam_step": (C.c_int, [_vp, _dp, C.c_longlong]),
+    "igs_train_iteration": (C.c_int, [_vp, _up, C.c_uint32, C.c_int, _dp, C.c_longlong, _dp]),
+    "igs_upload_samples": (C.c_int, [_vp, _up, C.c_uint32, C.c_uint32]),
+    "igs_train_iterations": (C.c_int, [_vp, C.c_uint32, C.c_int, _dp, C.c_longlong, _dp]),
+    "igs_device_grads": (_vp, [_vp]),
+    "igs_get_grads": (C.c_int, [_vp, _dp, C.c_uint32]),
+    "igs_get_adam_state": (C.c_int, [_vp, _dp, _dp, C.c_uint32]),
+    "igs_set_adam_state": (C.c_int, [_vp, _dp, _dp, C.c_uint32]),
+    "igs_add_distribution": (C.c_int, [_vp, _fp, C.c_int, C.c_int, _dp]),
+    "igs_psnr": (C.c_int, [_vp, _fp, C.c_int, C.c_int, _dp]),
+    "igs_partition_build": (C.c_int, [_vp, C.c_int]),
+    "igs_partition_rebuild": (C.c_int, [_vp, _dp, C.c_uint32]),
+    "igs_partition_info": (C.c_int, [_vp, _up, _u64p]),
+    "igs_partition_get": (C.c_int, [_vp, _dp, _dp, _up, _up]),
+    "igs_locate_blocks": (C.c_int, [_vp, _dp, C.c_uint32, _i32p]),
+    "igs_render_image_blocked": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _fp]),
+    "igs_render_points_blocked": (C.c_int, [_vp, _dp, C.c_uint32, C.c_int, _dp]),
+    "igs_tile_lists": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _up, _u64p, _up, _up, _dp]),
+    "igs_timer_begin": (C.c_int, [_vp]),
+    "igs_timer_end": (C.c_int, [_vp, C.POINTER(C.c_float)]),
+    "igs_flush_l2": (C.c_int, [_vp, C.c_size_t]),
+    "igs_fp64_peak": (C.c_int, [_vp, _dp]),
+    "igs_profile_enable": (C.c_int, [_vp, C.c_int]),
+    "igs_profile_read": (C.c_int, [_vp, C.c_int, _dp, _u64p, _dp]),
+    "igs_comm_unique_id": (C.c_int, [_u8p]),
+    "igs_comm_init": (C.c_int, [_vp, _u8p, C.c_int, C.c_int]),
+    "igs_comm_destroy": (C.c_int, [_vp]),
+}
+
+_lib = None
+
+
+def load_library() -> C.CDLL:
+    """Loads libigs_b200.so; raises if it has not been built."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                              "(there is no CPU fallback)")
+        lib = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(lib, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def _p(a, t):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+def _f64(a, shape_last=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if shape_last is not None:
+        a = a.reshape(-1, shape_last)
+    return a
+
+
+class Context:
+    """One GPU context (igs_ctx): device-resident set, Adam state, images."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load_library()
+        h = _vp()
+        code = self.lib.igs_ctx_create(device, C.byref(h))
+        if code:
+            raise IgsError(code, f"igs_ctx_create(device={device}) failed (no CUDA device?)")
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.igs_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _chk(self, code):
+        if code:
+            raise IgsError(code, (self.lib.igs_last_error(self.h) or b"").decode())
+
+    # ---- options / diagnostics ---------------------------------------------
+    def set_option(self, opt: int, value: int):
+        self._chk(self.lib.igs_set_option(self.h, opt, int(value)))
+
+    def get_option(self, opt: int) -> int:
+        return int(self.lib.igs_get_option(self.h, opt))
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(self.lib.igs_kernel_launches(self.h))
+
+    def sync(self):
+        self._chk(self.lib.igs_sync(self.h))
+
+    # ---- set -----------------------------------------------------------------
+    @property
+    def n(self) -> int:
+        return int(self.lib.igs_num_gaussians(self.h))
+
+    def set_params(self, params):
+        p = _f64(params, 8)
+        self._chk(self.lib.igs_set_params(self.h, _p(p, _dp), p.shape[0]))
+
+    def append_params(self, params):
+        p = _f64(params, 8)
+        self._chk(self.lib.igs_append_params(self.h, _p(p, _dp), p.shape[0]))
+
+    def get_params(self):
+        out = np.zeros((self.n, 8))
+        self._chk(self.lib.igs_get_params(self.h, _p(out, _dp), out.shape[0]))
+        return out
+
+    # ---- renderer ---------------------------------------------------------------
+    def render_image(self, width: int, height: int, k: int = DEFAULT_K, want_topk: bool = False, host: bool = True):
+        out = np.zeros((height, width, 3), np.float32) if host else None
+        topk = None
+        if want_topk:
+            kk = max(1, min(k, self.n))
+            topk = np.zeros((height, width, kk), np.uint32)
+        self._chk(self.lib.igs_render_image(self.h, width, height, k, _p(out, _fp), _p(topk, _up)))
+        return (out, topk) if want_topk else out
+
+    def render_image_rows(self, width: int, height: int, k: int, row0: int, row1: int):
+        out = np.zeros((row1 - row0, width, 3), np.float32)
+        self._chk(self.lib.igs_render_image_rows(self.h, width, height, k, row0, row1, _p(out, _fp)))
+        return out
+
+    def select_top_k(self, uv, k: int = DEFAULT_K):
+        uv = _f64(uv, 2)
+        kk = max(1, min(k, self.n))
+        idx = np.zeros((uv.shape[0], kk), np.uint32)
+        w = np.zeros((uv.shape[0], kk))
+        cnt = np.zeros(uv.shape[0], np.int32)
+        self._chk(self.lib.igs_select_top_k(self.h, _p(uv, _dp), uv.shape[0], k, _p(idx, _up), _p(w, _dp),
+                                            _p(cnt, _i32p)))
+        return idx, w, cnt
+
+    def render_points(self, uv, k: int = DEFAULT_K):
+        uv = _f64(uv, 2)
+        out = np.zeros((uv.shape[0], 3))
+        self._chk(self.lib.igs_render_points(self.h, _p(uv, _dp), uv.shape[0], k, _p(out, _dp)))
+        return out
+
+    def backward(self, samples, k: int = DEFAULT_K):
+        s = _f64(samples, 5)
+        out = np.zeros((self.n, 8))
+        self._chk(self.lib.igs_backward(self.h, _p(s, _dp), s.shape[0], k, _p(out, _dp)))
+        return out
+
+    # ---- training -------------------------------------------------------------------
+    def set_target(self, img):
+        img = np.ascontiguousarray(img, np.float32)
+        H, W, _ = img.shape
+        self._chk(self.lib.igs_set_target(self.h, _p(img, _fp), W, H))
+
+    def train_step(self, sample_idx, k: int = DEFAULT_K, want_grads: bool = True):
+        s = np.ascontiguousarray(sample_idx, np.uint32)
+        loss = C.c_double(0)
+        g = np.zeros((self.n, 8)) if want_grads else None
+        self._chk(self.lib.igs_train_step(self.h, _p(s, _up), s.shape[0], k, C.byref(loss), _p(g, _dp)))
+        return loss.value, g
+
+    def adam_step(self, lr=DEFAULT_LR, t: int = 1):
+        lr = np.ascontiguousarray(lr, np.float64)
+        self._chk(self.lib.igs_adam_step(self.h, _p(lr, _dp), int(t)))
+
+    def train_iteration(self, sample_idx, k: int = DEFAULT_K, lr=DEFAULT_LR, t: int = 1) -> float:
+        s = np.ascontiguousarray(sample_idx, np.uint32)
+        lr = np.ascontiguousarray(lr, np.float64)
+        loss = C.c_double(0)
+        self._chk(self.lib.igs_train_iteration(self.h, _p(s, _up), s.shape[0], k, _p(lr, _dp), int(t),
+                                               C.byref(loss)))
+        return loss.value
+
+    def upload_samples(self, sample_idx_steps):
+        s = np.ascontiguousarray(sample_idx_steps, np.uint32)
+        steps, ns = s.shape
+        self._chk(self.lib.igs_upload_samples(self.h, _p(s, _up), ns, steps))
+
+    def train_iterations(self, steps: int, k: int = DEFAULT_K, lr=DEFAULT_LR, t0: int = 1, want_losses=True):
+        lr = np.ascontiguousarray(lr, np.float64)
+        losses = np.zeros(steps) if want_losses else None
+        self._chk(self.lib.igs_train_iterations(self.h, steps, k, _p(lr, _dp), int(t0), _p(losses, _dp)))
+        return losses
+
+    def get_grads(self):
+        out = np.zeros((self.n, 8))
+        self._chk(self.lib.igs_get_grads(self.h, _p(out, _dp), out.shape[0]))
+        return out
+
+    def get_adam_state(self):
+        m = np.zeros((self.n, 8)); v = np.zeros((self.n, 8))
+        self._chk(self.lib.igs_get_adam_state(self.h, _p(m, _dp), _p(v, _dp), self.n))
+        return m, v
+
+    def set_adam_state(self, m, v):
+        m = _f64(m, 8); v = _f64(v, 8)
+        self._chk(self.lib.igs_set_adam_state(self.h, _p(m, _dp), _p(v, _dp), m.shape[0]))
+
+    # ---- error map / metrics -----------------------------------------------------------
+    def add_distribution(self, width: int, height: int, rendered=None):
+        r = None if rendered is None else np.ascontiguousarray(rendered, np.float32)
+        out = np.zeros((height, width))
+        self._chk(self.lib.igs_add_distribution(self.h, _p(r, _fp), width, height, _p(out, _dp)))
+        return out
+
+    def psnr(self, width: int, height: int, rendered=None) -> float:
+        r = None if rendered is None else np.ascontiguousarray(rendered, np.float32)
+        out = C.c_double(0)
+        self._chk(self.lib.igs_psnr(self.h, _p(r, _fp), width, height, C.byref(out)))
+        return out.value
+
+    # ---- BSP ------------------------------------------------------------------------------
+    def partition_build(self, n_max: int):
+        self._chk(self.lib.igs_partition_build(self.h, n_max))
+
+    def partition_rebuild(self, rects):
+        r = _f64(rects, 4)
+        self._chk(self.lib.igs_partition_rebuild(self.h, _p(r, _dp), r.shape[0]))
+
+    def partition_info(self):
+        nb = C.c_uint32(0); tot = C.c_uint64(0)
+        self._chk(self.lib.igs_partition_info(self.h, C.byref(nb), C.byref(tot)))
+        return nb.value, tot.value
+
+    def partition_get(self):
+        nb, tot = self.partition_info()
+        b = np.zeros((nb, 4)); s = np.zeros((nb, 4))
+        off = np.zeros(nb + 1, np.uint32); mem = np.zeros(max(tot, 1), np.uint32)
+        self._chk(self.lib.igs_partition_get(self.h, _p(b, _dp), _p(s, _dp), _p(off, _up), _p(mem, _up)))
+        return b, s, off, mem[:tot]
+
+    def locate_blocks(self, uv):
+        uv = _f64(uv, 2)
+        out = np.zeros(uv.shape[0], np.int32)
+        self._chk(self.lib.igs_locate_blocks(self.h, _p(uv, _dp), uv.shape[0], _p(out, _i32p)))
+        return out
+
+    def render_image_blocked(self, width: int, height: int, k: int = DEFAULT_K, host: bool = True):
+        out = np.zeros((height, width, 3), np.float32) if host else None
+        self._chk(self.lib.igs_render_image_blocked(self.h, width, height, k, _p(out, _fp)))
+        return out
+
+    def render_points_blocked(self, uv, k: int = DEFAULT_K):
+        uv = _f64(uv, 2)
+        out = np.zeros((uv.shape[0], 3))
+        self._chk(self.lib.igs_render_points_blocked(self.h, _p(uv, _dp), uv.shape[0], k, _p(out, _dp)))
+        return out
+
+    # ---- culling introspection -------------------------------------------------------------
+    def tile_lists(self, width: int, height: int, k: int = DEFAULT_K):
+        nt = C.c_uint32(0); tot = C.c_uint64(0)
+        self._chk(self.lib.igs_tile_lists(self.h, width, height, k, C.byref(nt), C.byref(tot), None, None, None))
+        off = np.zeros(nt.value + 1, np.uint32); mem = np.zeros(max(tot.value, 1), np.uint32)
+        tau = np.zeros(nt.value)
+        self._chk(self.lib.igs_tile_lists(self.h, width, height, k, C.byref(nt), C.byref(tot), _p(off, _up),
+                                          _p(mem, _up), _p(tau, _dp)))
+        return off, mem[:tot.value], tau
+
+    # ---- benchmark support ----------------------------------------------------------------------
+    def timer_begin(self):
+        self._chk(self.lib.igs_timer_begin(self.h))
+
+    def timer_end(self) -> float:
+        ms = C.c_float(0)
+        self._chk(self.lib.igs_timer_end(self.h, C.byref(ms)))
+        return ms.value
+
+    def flush_l2(self, nbytes: int = 512 << 20):
+        self._chk(self.lib.igs_flush_l2(self.h, nbytes))
+
+    def fp64_peak(self) -> float:
+        out = C.c_double(0)
+        self._chk(self.lib.igs_fp64_peak(self.h, C.byref(out)))
+        return out.value
+
+    def profile_enable(self, on: bool = True):
+        self._chk(self.lib.igs_profile_enable(self.h, 1 if on else 0))
+
+    def profile_read(self, family: int):
+        ms = C.c_double(0); n = C.c_uint64(0); work = C.c_double(0)
+        self._chk(self.lib.igs_profile_read(self.h, family, C.byref(ms), C.byref(n), C.byref(work)))
+        return ms.value, n.value, work.value
+
+    # ---- multi-GPU ---------------------------------------------------------------------------
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        lib = load_library()
+        buf = (C.c_uint8 * 128)()
+        code = lib.igs_comm_unique_id(buf)
+        if code:
+            raise IgsError(code, "ncclGetUniqueId failed")
+        return bytes(buf)
+
+    def comm_init(self, uid: bytes, nranks: int, rank: int):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        self._chk(self.lib.igs_comm_init(self.h, buf, nranks, rank))
+
+    def comm_destroy(self):
+        self._chk(self.lib.igs_comm_destroy(self.h))

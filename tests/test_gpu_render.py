@@ -1,0 +1,158 @@
+"""GPU parity: kernel 1 (prepare) + kernel 3 (exact top-K raster) through
+the C-ABI, against the reference's golden outputs and the CPU oracle.
+
+Bars (BASELINE.json north_star): top-K indices bit-exact (ties by index);
+pixels within 1e-4 and PSNR(GPU vs CPU) >= 80 dB.  In practice the pixels
+are bit-identical except where the CPU's glibc sin/cos is not correctly
+rounded (~0.14 % of angles, see csrc/igs_math.cuh) -- those flip only
+last-ulp decisions, so we also require >= 99.99 % exact pixels.
+"""
+import numpy as np
+import pytest
+
+from paper_2407_01866_b200 import OPT_CULL, IgsError, synth
+
+pytestmark = pytest.mark.gpu
+
+PIX_TOL = 1e-4
+
+
+def psnr(a, b):
+    mse = np.mean((a.astype(np.float64) - b.astype(np.float64)) ** 2)
+    return np.inf if mse == 0 else 10 * np.log10(1.0 / mse)
+
+
+def check_image(got, want):
+    assert got.shape == want.shape
+    assert np.max(np.abs(got.astype(np.float64) - want)) <= PIX_TOL
+    assert psnr(got, want) >= 80.0
+    assert np.mean(got == want) >= 0.9999
+
+
+@pytest.fixture(params=[1, 0], ids=["cull", "brute"])
+def mode(request, gctx):
+    gctx.set_option(OPT_CULL, request.param)
+    yield request.param
+    gctx.set_option(OPT_CULL, 1)
+
+
+def test_golden_render_topk(gctx, golden, mode):
+    g = golden("render_global")
+    gctx.set_params(g["params"])
+    img, topk = gctx.render_image(int(g["W"]), int(g["H"]), int(g["k"]), want_topk=True)
+    assert np.array_equal(topk, g["topk"])
+    check_image(img, g["image"])
+
+
+def test_golden_local_k10_k1(gctx, golden, mode):
+    g = golden("render_local")
+    gctx.set_params(g["params"])
+    img, topk = gctx.render_image(int(g["W"]), int(g["H"]), 10, want_topk=True)
+    assert np.array_equal(topk, g["topk10"])
+    check_image(img, g["image10"])
+    check_image(gctx.render_image(int(g["W"]), int(g["H"]), 1), g["image1"])
+
+
+@pytest.mark.parametrize("k", [1, 3, 8, 10, 16, 17, 32, 40])
+def test_k_sweep_vs_oracle(gctx, port, k, mode):
+    params = synth.random_set(700, 1000 + k, 0.004, 0.06)
+    gctx.set_params(params)
+    want, wtk = port.render_image(params, 37, 29, k, want_topk=True)
+    got, gtk = gctx.render_image(37, 29, k, want_topk=True)
+    assert np.array_equal(gtk, wtk)
+    check_image(got, want)
+
+
+def test_init_state_set(gctx, port, mode):
+    """Fit-start sets (sigma = 2 px, theta = 0): q_K is far beyond 3 sigma."""
+    params = synth.init_set(3000, 160, 120, seed=3)
+    gctx.set_params(params)
+    want, wtk = port.render_image(params, 160, 120, 10, want_topk=True)
+    got, gtk = gctx.render_image(160, 120, 10, want_topk=True)
+    assert np.array_equal(gtk, wtk)
+    check_image(got, want)
+
+
+def test_k_ge_n_and_tiny_sets(gctx, port, mode):
+    for n in (1, 2, 3, 9):
+        params = synth.random_set(n, 77 + n, 0.05, 0.3)
+        gctx.set_params(params)
+        for k in (1, n, 10, 50):
+            want, wtk = port.render_image(params, 19, 23, k, want_topk=True)
+            got, gtk = gctx.render_image(19, 23, k, want_topk=True)
+            assert np.array_equal(gtk, wtk)
+            check_image(got, want)
+
+
+def test_exact_tie_breaks_to_lower_index(gctx, mode):
+    """test_renderer.cpp:94-105: mirrored Gaussians, identical density."""
+    p = np.array([[0.4, 0.5, 0, 0.1, 0.1, 1, 0, 0], [0.6, 0.5, 0, 0.1, 0.1, 0, 1, 0]], float)
+    gctx.set_params(p)
+    idx, w, cnt = gctx.select_top_k([[0.5, 0.5]], 1)
+    assert idx[0, 0] == 0 and cnt[0] == 1
+    # column u = 0.5 exactly in a 2-wide raster: pixel centres 0.25/0.75 -- no tie; use 3-wide
+    _, topk = gctx.render_image(3, 3, 1, want_topk=True)
+    assert topk[1, 1, 0] == 0
+
+
+def test_one_sigma_saturation(gctx, mode):
+    """test_renderer.cpp:226-249: a single red Gaussian saturates its 1-sigma ellipse."""
+    p = np.array([[0.5, 0.5, 0.8, 0.1, 0.05, 1.0, 0.0, 0.0]])
+    gctx.set_params(p)
+    img = gctx.render_image(64, 64, 10)
+    c, s = np.cos(0.8), np.sin(0.8)
+    uu, vv = np.meshgrid((np.arange(64) + 0.5) / 64, (np.arange(64) + 0.5) / 64)
+    dx, dy = uu - 0.5, vv - 0.5
+    e1, e2 = c * dx + s * dy, -s * dx + c * dy
+    inside = e1 ** 2 / 0.01 + e2 ** 2 / 0.0025 <= 1.0
+    assert inside.sum() > 10
+    assert np.all(img[inside] == np.array([1, 0, 0], np.float32))
+
+
+def test_points_select_and_render(gctx, port, golden, mode):
+    params = synth.random_set(900, 202, 0.01, 0.2)
+    gctx.set_params(params)
+    uv = np.random.default_rng(203).random((257, 2))
+    idx, w, cnt = gctx.select_top_k(uv, 10)
+    for p in range(0, 257, 16):
+        wi, ww = port.select_top_k(params, uv[p, 0], uv[p, 1], 10)
+        assert np.array_equal(idx[p, :cnt[p]], wi)
+        np.testing.assert_allclose(w[p, :cnt[p]], ww, rtol=1e-14, atol=0)
+    got = gctx.render_points(uv, 10)
+    want = port.render_topk(params, uv, 10)
+    np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-14)
+
+
+def test_rows_sharding_equals_full(gctx, mode):
+    """Tile-row sharding (the multi-GPU render split) stitches to the full raster."""
+    params = synth.random_local_set(4000, 200, 150)
+    gctx.set_params(params)
+    full = gctx.render_image(200, 150, 10)
+    bands = [gctx.render_image_rows(200, 150, 10, r0, min(150, r0 + 40)) for r0 in range(0, 150, 40)]
+    assert np.array_equal(np.concatenate(bands, axis=0), full)
+
+
+def test_errors_match_reference_kinds(gctx):
+    gctx.set_params(np.zeros((0, 8)))
+    with pytest.raises(IgsError) as e:
+        gctx.render_image(8, 8, 10)
+    assert e.value.kind == "empty_set"
+    gctx.set_params(synth.random_set(3, 1))
+    with pytest.raises(IgsError) as e:
+        gctx.render_image(8, 8, 0)
+    assert e.value.kind == "invalid_parameter"
+    with pytest.raises(IgsError) as e:
+        gctx.render_image(0, 8, 10)
+    assert e.value.kind == "invalid_parameter"
+
+
+def test_append_keeps_indices(gctx, port, mode):
+    a = synth.random_set(500, 5, 0.01, 0.1)
+    b = synth.random_set(300, 6, 0.01, 0.1)
+    gctx.set_params(a)
+    gctx.append_params(b)
+    assert np.array_equal(gctx.get_params(), np.concatenate([a, b]))
+    want, wtk = port.render_image(np.concatenate([a, b]), 48, 40, 10, want_topk=True)
+    got, gtk = gctx.render_image(48, 40, 10, want_topk=True)
+    assert np.array_equal(gtk, wtk)
+    check_image(got, want)
