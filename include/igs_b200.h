@@ -155,6 +155,10 @@ int igs_render_image_blocked(igs_ctx* ctx, int width, int height, int k, float* 
 /* render_topk_blocked at npts points (random-access decode queries). */
 int igs_render_points_blocked(igs_ctx* ctx, const double* uv, uint32_t npts, int k, double* rgb);
 
+/* The device's prepared scan records (mu_x, mu_y, cos, sin, 1/s1^2, 1/s2^2)
+ * per Gaussian (PreparedSet::scan, renderer.hpp:31-34): n*6 doubles. */
+int igs_get_prepared(igs_ctx* ctx, double* scan6, uint32_t n);
+
 /* ---- culling introspection (tile lists for parity tests) ------------------ */
 /* Builds the certified candidate lists for a W x H raster at k and returns
  * the CSR (offsets ntiles+1, members ascending within each tile).  Pass

@@ -104,6 +104,8 @@ _PORT_ONLY = [
     ("vector_like_image", None, [C.c_int, C.c_int, C.c_uint64, _fp]),
     ("texture_like_image", None, [C.c_int, C.c_int, C.c_uint64, _fp]),
     ("alias_build", C.c_int, [_dp, C.c_size_t, _dp, _up]),
+    ("cull_lists", C.c_uint64, [_dp, C.c_uint32, C.c_int, C.c_int, C.c_int, C.c_int, _up, _up, _dp]),
+    ("prepare_scan", None, [_dp, C.c_uint32, _dp]),
 ]
 
 _REF_ONLY = [
@@ -315,6 +317,23 @@ class Oracle:
         a = np.ascontiguousarray(a, np.float32).ravel()
         b = np.ascontiguousarray(b, np.float32).ravel()
         return float(self._f("psnr")(_ptr(a, _fp), _ptr(b, _fp), a.size))
+
+    # ---- certified culling (port back-end only) ----------------------------------
+    def prepare_scan(self, params):
+        params = np.ascontiguousarray(params, np.float64)
+        out = np.zeros((params.shape[0], 6))
+        self._f("prepare_scan")(_ptr(params, _dp), params.shape[0], _ptr(out, _dp))
+        return out
+
+    def cull_lists(self, scan6, W, H, k, T=16):
+        scan6 = np.ascontiguousarray(scan6, np.float64)
+        n = scan6.shape[0]
+        nt = ((W + T - 1) // T) * ((H + T - 1) // T)
+        off = np.zeros(nt + 1, np.uint32); tau = np.zeros(nt)
+        total = int(self._f("cull_lists")(_ptr(scan6, _dp), n, W, H, k, T, _ptr(off, _up), None, _ptr(tau, _dp)))
+        mem = np.zeros(max(total, 1), np.uint32)
+        self._f("cull_lists")(_ptr(scan6, _dp), n, W, H, k, T, _ptr(off, _up), _ptr(mem, _up), _ptr(tau, _dp))
+        return off, mem[:total], tau
 
     # ---- BSP ------------------------------------------------------------------
     def partition_build(self, params, n_max):

@@ -253,6 +253,16 @@ static prep_t* prepare(const double* p8, uint32_t n) {
     return ps;
 }
 
+void orc_prepare_scan(const double* p8, uint32_t n, double* scan6) {
+    prep_t* ps = prepare(p8, n);
+    for (uint32_t i = 0; i < n; ++i) {
+        double* o = scan6 + (size_t)i * 6;
+        o[0] = ps[i].mu_x; o[1] = ps[i].mu_y; o[2] = ps[i].cos_t; o[3] = ps[i].sin_t;
+        o[4] = ps[i].inv_a; o[5] = ps[i].inv_b;
+    }
+    free(ps);
+}
+
 /* renderer.cpp:17-23 mahalanobis_sq: no FMA, left-to-right. */
 static inline double maha(const prep_t* g, double x, double y) {
     const double dx = x - g->mu_x;
@@ -1092,4 +1102,122 @@ int orc_render_points_blocked(const double* p8, uint32_t n, const orc_partition*
     free(e);
     free(ps);
     return ORC_OK;
+}
+
+/* ======================================================================= */
+/* Certified tile culling: restatement of the B200 build's predicate        */
+/* (paper_2407_01866_b200/csrc/cull_math.cuh, cull.cu), op for op, so the    */
+/* device's tile lists can be compared bit-exactly.  Not a reference         */
+/* algorithm: the reference has no culling (renderer.cpp:168-176 ranks all   */
+/* N); the predicate's soundness is what tests/test_cull.py checks against   */
+/* the reference's own top-K.  Input: prepared records                       */
+/* (mu_x, mu_y, cos, sin, inv_a, inv_b) as the device computed them.        */
+/* ======================================================================= */
+typedef struct { double mx, my, c, s, ia, ib, A, B, C; } cg_t;
+#define CULL_ERRU (64.0 * 1.1102230246251565e-16)
+#define CULL_UP (1.0 + 9.313225746154785e-10)
+#define CULL_DN (1.0 - 9.313225746154785e-10)
+
+static double cq_at(const cg_t* g, double x, double y) {
+    const double dx = x - g->mx, dy = y - g->my;
+    const double e1 = g->c * dx + g->s * dy;
+    const double e2 = -g->s * dx + g->c * dy;
+    return e1 * e1 * g->ia + e2 * e2 * g->ib;
+}
+static double c_err(const cg_t* g, double x0, double x1, double y0, double y1) {
+    const double ax = fmax(fabs(x0 - g->mx), fabs(x1 - g->mx));
+    const double ay = fmax(fabs(y0 - g->my), fabs(y1 - g->my));
+    const double l = ax + ay;
+    return CULL_ERRU * (g->ia + g->ib) * l * l;
+}
+static double c_qmax(const cg_t* g, double x0, double x1, double y0, double y1) {
+    const double a = cq_at(g, x0, y0), b = cq_at(g, x1, y0), c = cq_at(g, x0, y1), d = cq_at(g, x1, y1);
+    const double m = fmax(fmax(a, b), fmax(c, d));
+    return m * CULL_UP + 2.0 * c_err(g, x0, x1, y0, y1);
+}
+static double c_qmin(const cg_t* g, double x0, double x1, double y0, double y1) {
+    const int in_x = g->mx >= x0 && g->mx <= x1, in_y = g->my >= y0 && g->my <= y1;
+    if (in_x && in_y) return 0.0;
+    double best = INFINITY;
+    const double det = g->ia * g->ib;
+    if (!in_x) {
+        const double xe = g->mx < x0 ? x0 : x1, dx = xe - g->mx;
+        double v = (det * (dx * dx)) / g->C;
+        const double ys = g->my - (g->B * dx) / g->C;
+        if (ys < y0) v = fmax(v, cq_at(g, xe, y0) * CULL_DN);
+        else if (ys > y1) v = fmax(v, cq_at(g, xe, y1) * CULL_DN);
+        best = fmin(best, v);
+    }
+    if (!in_y) {
+        const double ye = g->my < y0 ? y0 : y1, dy = ye - g->my;
+        double v = (det * (dy * dy)) / g->A;
+        const double xs = g->mx - (g->B * dy) / g->A;
+        if (xs < x0) v = fmax(v, cq_at(g, x0, ye) * CULL_DN);
+        else if (xs > x1) v = fmax(v, cq_at(g, x1, ye) * CULL_DN);
+        best = fmin(best, v);
+    }
+    const double lb = best * CULL_DN - 2.0 * c_err(g, x0, x1, y0, y1);
+    return lb > 0.0 ? lb : 0.0;
+}
+static double ccenter(int i, int n) { return ((double)i + 0.5) / (double)n; }
+static int cmp_dbl(const void* a, const void* b) {
+    const double x = *(const double*)a, y = *(const double*)b;
+    return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+/* Returns the total list length; offsets[ntiles+1], tau[ntiles] and
+ * members (ascending per tile; nullable on a sizing call). */
+uint64_t orc_cull_lists(const double* scan6, uint32_t n, int W, int H, int k, int T, uint32_t* offsets,
+                        uint32_t* members, double* tau) {
+    const int TX = (W + T - 1) / T, TY = (H + T - 1) / T, nt = TX * TY;
+    const int kk = (int)((uint32_t)k < n ? (uint32_t)k : n);
+    cg_t* g = (cg_t*)malloc(sizeof(cg_t) * (n ? n : 1));
+    int* bin = (int*)malloc(sizeof(int) * (n ? n : 1));
+    uint32_t* bcnt = (uint32_t*)calloc(nt, sizeof(uint32_t));
+    for (uint32_t i = 0; i < n; ++i) {
+        const double* r = scan6 + (size_t)i * 6;
+        g[i].mx = r[0]; g[i].my = r[1]; g[i].c = r[2]; g[i].s = r[3]; g[i].ia = r[4]; g[i].ib = r[5];
+        const double c2 = g[i].c * g[i].c, s2 = g[i].s * g[i].s, cs = g[i].c * g[i].s;
+        g[i].A = c2 * g[i].ia + s2 * g[i].ib;
+        g[i].B = cs * (g[i].ia - g[i].ib);
+        g[i].C = s2 * g[i].ia + c2 * g[i].ib;
+        const double fx = floor(g[i].mx * (double)W), fy = floor(g[i].my * (double)H);
+        const int cx = isfinite(fx) ? (int)fmin(fmax(fx, 0.0), (double)(W - 1)) : 0;
+        const int cy = isfinite(fy) ? (int)fmin(fmax(fy, 0.0), (double)(H - 1)) : 0;
+        bin[i] = (cy / T) * TX + cx / T;
+        bcnt[bin[i]]++;
+    }
+    double* vals = (double*)malloc(sizeof(double) * (n ? n : 1));
+    uint64_t total = 0;
+    for (int t = 0; t < nt; ++t) {
+        const int tx = t % TX, ty = t / TX;
+        const double x0 = ccenter(tx * T, W), x1 = ccenter((W < (tx + 1) * T ? W : (tx + 1) * T) - 1, W);
+        const double y0 = ccenter(ty * T, H), y1 = ccenter((H < (ty + 1) * T ? H : (ty + 1) * T) - 1, H);
+        int r = 1, ax, bx, ay, by;
+        for (;; ++r) {
+            ax = tx - r > 0 ? tx - r : 0; bx = tx + r < TX - 1 ? tx + r : TX - 1;
+            ay = ty - r > 0 ? ty - r : 0; by = ty + r < TY - 1 ? ty + r : TY - 1;
+            uint64_t c = 0;
+            for (int yy = ay; yy <= by; ++yy)
+                for (int xx = ax; xx <= bx; ++xx) c += bcnt[yy * TX + xx];
+            if (c >= (uint64_t)kk || (ax == 0 && ay == 0 && bx == TX - 1 && by == TY - 1)) break;
+        }
+        size_t nv = 0;
+        for (uint32_t i = 0; i < n; ++i) {
+            const int bt = bin[i], bxx = bt % TX, byy = bt / TX;
+            if (bxx >= ax && bxx <= bx && byy >= ay && byy <= by) vals[nv++] = c_qmax(&g[i], x0, x1, y0, y1);
+        }
+        qsort(vals, nv, sizeof(double), cmp_dbl);
+        const double tt = vals[kk - 1];
+        if (tau) tau[t] = tt;
+        if (offsets) offsets[t] = (uint32_t)total;
+        for (uint32_t i = 0; i < n; ++i)
+            if (c_qmin(&g[i], x0, x1, y0, y1) <= tt) {
+                if (members) members[total] = i;
+                ++total;
+            }
+    }
+    if (offsets) offsets[nt] = (uint32_t)total;
+    free(vals); free(bcnt); free(bin); free(g);
+    return total;
 }

@@ -116,6 +116,14 @@ int orc_render_image_blocked(const double* p8, uint32_t n, const orc_partition* 
 int orc_render_points_blocked(const double* p8, uint32_t n, const orc_partition* part, const double* uv,
                               uint32_t npts, int k, double* rgb);
 
+/* ---- certified tile culling (restates the B200 build's predicate) ------- */
+/* scan6: prepared records (mu_x, mu_y, cos, sin, inv_a, inv_b).  Returns the
+ * total list length; offsets[ntiles+1], tau[ntiles], members nullable. */
+uint64_t orc_cull_lists(const double* scan6, uint32_t n, int W, int H, int k, int T, uint32_t* offsets,
+                        uint32_t* members, double* tau);
+/* PreparedSet scan records (renderer.cpp:32-51) with glibc sin/cos. */
+void orc_prepare_scan(const double* p8, uint32_t n, double* scan6);
+
 #ifdef __cplusplus
 }
 #endif

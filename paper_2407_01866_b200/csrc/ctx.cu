@@ -26,7 +26,6 @@ int igs_blend_points(igs_ctx* ctx, const double* lq, const uint32_t* li, uint32_
 int igs_raster_culled(igs_ctx* ctx, int W, int H, int k, int row0, int row1, float* out, uint32_t* topk);
 int igs_cull_lists(igs_ctx* ctx, int W, int H, int k, uint32_t* ntiles, uint64_t* total, uint32_t* offsets,
                    uint32_t* members, double* tau);
-int igs_topk_samples_culled(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq);
 // metrics.cu
 int igs_error_map(igs_ctx* ctx, const float* dev_rendered, int W, int H, double* dev_p);
 int igs_psnr_dev(igs_ctx* ctx, const float* dev_a, const float* dev_b, size_t count, double* out);
@@ -245,6 +244,7 @@ void igs_ctx_destroy(igs_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     igs_partition_free(ctx);
+    igs_cull_free(ctx);
 #ifndef IGS_NO_NCCL
     if (ctx->comm) nccl().commDestroy(ctx->comm);
 #endif
@@ -314,6 +314,7 @@ int igs_set_params(igs_ctx* ctx, const double* params8, uint32_t n) {
     if (e) return e;
     ctx->n = n;
     ctx->grads_valid = false;
+    ctx->params_version++;
     igs_partition_free(ctx);
     if (n == 0) return IGS_OK;
     const size_t rb = (size_t)n * 8 * sizeof(double);
@@ -339,6 +340,7 @@ int igs_append_params(igs_ctx* ctx, const double* params8, uint32_t n) {
     IGS_CUDA(ctx, cudaMemsetAsync(ctx->grads + (size_t)old * 8, 0, rb, ctx->stream));
     ctx->n = old + n;
     ctx->grads_valid = false;
+    ctx->params_version++;
     igs_partition_free(ctx);  // a partition refers to the old count (bsp.cpp:278-282)
     return igs_prepare_all(ctx, old);
 }
@@ -351,6 +353,14 @@ int igs_get_params(igs_ctx* ctx, double* params8, uint32_t n) {
 }
 
 uint32_t igs_num_gaussians(const igs_ctx* ctx) { return ctx ? ctx->n : 0; }
+
+int igs_get_prepared(igs_ctx* ctx, double* scan6, uint32_t n) {
+    CHECK_CTX(ctx);
+    if (n != ctx->n) return igs_fail(ctx, IGS_E_DIMENSION_MISMATCH, "count mismatch");
+    if (n == 0) return IGS_OK;
+    static_assert(sizeof(ScanRec) == 6 * sizeof(double), "ScanRec layout");
+    return dev_to_host(ctx, scan6, ctx->scan, (size_t)n * sizeof(ScanRec));
+}
 const double* igs_device_params(const igs_ctx* ctx) { return ctx ? ctx->params : nullptr; }
 const float* igs_device_image(const igs_ctx* ctx) { return ctx ? (const float*)ctx->image.p : nullptr; }
 const double* igs_device_grads(const igs_ctx* ctx) { return ctx ? ctx->grads : nullptr; }

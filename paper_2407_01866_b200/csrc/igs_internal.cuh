@@ -190,6 +190,8 @@ struct igs_ctx {
     uint32_t samples_ns = 0, samples_steps = 0;
 
     PartitionDev* part = nullptr;
+    void* cull = nullptr;            // CullBufs (cull.cu)
+    uint64_t params_version = 0;     // bumped on every change of the set
 
     // profiling (igs_profile_*)
     bool prof_on = false;
@@ -241,3 +243,7 @@ int igs_prepare_all(igs_ctx* ctx, uint32_t first);
 int igs_raster_global(igs_ctx* ctx, int W, int H, int k, int row0, int row1, float* dev_out, uint32_t* dev_topk);
 int igs_topk_points(igs_ctx* ctx, const double* dev_uv, uint32_t npts, int k, uint32_t* dev_idx, double* dev_q);
 int igs_partition_free(igs_ctx* ctx);
+void igs_cull_free(igs_ctx* ctx);
+int igs_topk_samples_culled(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq);
+int igs_topk_pixels_culled(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq, int W,
+                           int H);

@@ -26,8 +26,6 @@
 
 using namespace igs_dev;
 
-int igs_topk_samples_culled(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq);
-
 namespace {
 
 __device__ __forceinline__ double sign_of(double v) { return v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : 0.0); }
@@ -360,7 +358,10 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
         IGS_CUDA(ctx, cudaMemcpy2DAsync(uv, 2 * sizeof(double), dev_samples5, 5 * sizeof(double),
                                         2 * sizeof(double), ns, cudaMemcpyDeviceToDevice, ctx->stream));
     }
-    int e = ctx->opt_cull ? igs_topk_samples_culled(ctx, uv, ns, k, li, lq) : igs_topk_points(ctx, uv, ns, k, li, lq);
+    int e;
+    if (!ctx->opt_cull) e = igs_topk_points(ctx, uv, ns, k, li, lq);
+    else if (mode == 0) e = igs_topk_pixels_culled(ctx, uv, ns, k, li, lq, ctx->tgt_w, ctx->tgt_h);
+    else e = igs_topk_samples_culled(ctx, uv, ns, k, li, lq);
     if (e) return e;
     const size_t items = (size_t)ns * kk;
     if (ctx->opt_deterministic) {
@@ -418,6 +419,7 @@ int igs_adam_launch(igs_ctx* ctx, const double* lr4, long long t) {
     // Bias corrections with the host libm pow, as adam.cpp:16-17.
     const double bc1 = 1.0 - std::pow(0.9, (double)t);
     const double bc2 = 1.0 - std::pow(0.999, (double)t);
+    ctx->params_version++;
     igs_prof_begin(ctx, IGS_PROF_ADAM);
     adam_kernel<<<(ctx->n + 255) / 256, 256, 0, ctx->stream>>>(ctx->params, ctx->grads, ctx->adam_m, ctx->adam_v,
                                                                ctx->scan, ctx->shade, ctx->n, lr4[0], lr4[1], lr4[2],

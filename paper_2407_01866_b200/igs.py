@@ -109,6 +109,7 @@ SIGNATURES = {
     "igs_locate_blocks": (C.c_int, [_vp, _dp, C.c_uint32, _i32p]),
     "igs_render_image_blocked": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _fp]),
     "igs_render_points_blocked": (C.c_int, [_vp, _dp, C.c_uint32, C.c_int, _dp]),
+    "igs_get_prepared": (C.c_int, [_vp, _dp, C.c_uint32]),
     "igs_tile_lists": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _up, _u64p, _up, _up, _dp]),
     "igs_timer_begin": (C.c_int, [_vp]),
     "igs_timer_end": (C.c_int, [_vp, C.POINTER(C.c_float)]),
@@ -351,6 +352,11 @@ class Context:
         uv = _f64(uv, 2)
         out = np.zeros((uv.shape[0], 3))
         self._chk(self.lib.igs_render_points_blocked(self.h, _p(uv, _dp), uv.shape[0], k, _p(out, _dp)))
+        return out
+
+    def get_prepared(self):
+        out = np.zeros((self.n, 6))
+        self._chk(self.lib.igs_get_prepared(self.h, _p(out, _dp), out.shape[0]))
         return out
 
     # ---- culling introspection -------------------------------------------------------------
