@@ -234,6 +234,14 @@ def run_ours(args, rank, world, local_rank, dist):
         adam_roof = {"kernel": "fused Adam+constrain+prepare", "bound": "hbm", "achieved": gbs, "peak": hbm,
                      "unit": "GB/s", "frac": gbs / hbm, "traffic": None, "bytes_per_gaussian": 544}
 
+    # ---- culling statistics of the last state (target raster, K) -----------------------
+    cull_stats = None
+    if ctx.get_option(1):
+        off, mem, tau = ctx.tile_lists(W_IMG, H_IMG, K)
+        sizes = np.diff(off.astype(np.int64))
+        cull_stats = {"tiles": int(sizes.size), "mean_list": float(sizes.mean()), "max_list": int(sizes.max()),
+                      "tau_median": float(np.median(tau)), "pairs_vs_brute_force": float(sizes.mean() / N_GAUSS)}
+
     # ---- secondary: full render Mpix/s (the eval render of the same set) ------------
     render = None
     if not args.no_render:
@@ -265,6 +273,7 @@ def run_ours(args, rank, world, local_rank, dist):
         "roofline": roof, "roofline_adam": adam_roof,
         "profile_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
         "dominant_family": dom,
+        "cull": cull_stats,
         "clocks": clk, "gpu_launches": int(launches),
         "render": render,
     }

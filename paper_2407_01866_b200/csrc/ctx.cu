@@ -245,6 +245,7 @@ void igs_ctx_destroy(igs_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     igs_partition_free(ctx);
     igs_cull_free(ctx);
+    igs_knn_free(ctx);
 #ifndef IGS_NO_NCCL
     if (ctx->comm) nccl().commDestroy(ctx->comm);
 #endif
@@ -413,7 +414,7 @@ static int points_topk(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uin
     double* lq = (double*)igs_scratch(ctx, 19, (size_t)npts * kk * sizeof(double));
     if (!duv || !li || !lq) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (points)");
     if ((e = host_to_dev(ctx, duv, uv, (size_t)npts * 2 * sizeof(double)))) return e;
-    if (ctx->opt_cull) e = igs_topk_samples_culled(ctx, duv, npts, k, li, lq);
+    if (ctx->opt_cull) e = igs_topk_knn(ctx, duv, npts, k, li, lq);
     else e = igs_topk_points(ctx, duv, npts, k, li, lq);
     if (e) return e;
     *dli = li;

@@ -249,6 +249,11 @@ __global__ void emit_fill_kernel(const ScanRec* __restrict__ scan, uint32_t n, G
     });
 }
 
+__global__ void total_kernel(const uint32_t* __restrict__ off, const uint32_t* __restrict__ cnt, int ntiles,
+                             unsigned long long* __restrict__ total) {
+    *total = (unsigned long long)off[ntiles - 1] + cnt[ntiles - 1];
+}
+
 // ---------------------------------------------------------------------------
 // Consumers
 // ---------------------------------------------------------------------------
@@ -440,10 +445,12 @@ int build_lists(igs_ctx* ctx, int W, int H, int pts_cells, int kk) {
     const int pyr = gr.loff[gr.levels - 1] + 1;
     if (gr.levels > kMaxLevels || gr.TX > 8191 || gr.TY > 8191)
         return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "raster too large for the tile pyramid");
-    if (b.cap == 0) b.cap = std::max<uint32_t>(1u << 20, n * 16u);
-    // lazily grow from the previous build's observed total
+    if (b.cap == 0) b.cap = std::max<uint32_t>(1u << 21, n * 48u);
+    // Grow from the previous build's total (copied to pinned memory at the
+    // end of that build; the stream has synchronised since in every caller).
+    // Tiles that overflowed were still exact (consumers fall back to all N).
     if (b.total_pinned && *b.total_pinned > b.cap) b.cap = (uint32_t)std::min<unsigned long long>(
-        0xF0000000ull, *b.total_pinned + *b.total_pinned / 4);
+        0xF0000000ull, *b.total_pinned + *b.total_pinned / 2);
     if (!grow(b.bin_cnt, (size_t)ntiles * 4) || !grow(b.bin_off, (size_t)ntiles * 4) || !grow(b.bin_of, (size_t)n * 4) ||
         !grow(b.bins, (size_t)n * 4) || !grow(b.tau, (size_t)pyr * 8) || !grow(b.tile_cnt, (size_t)ntiles * 8) ||
         !grow(b.tile_off, (size_t)ntiles * 4) || !grow(b.list, (size_t)b.cap * 4) || !grow(b.total, 16))
@@ -495,9 +502,9 @@ int build_lists(igs_ctx* ctx, int W, int H, int pts_cells, int kk) {
                                                                tile_off, tile_cur, (uint32_t*)b.list.p, b.cap);
     IGS_LAUNCHED(ctx);
     // total pairs = off[last] + cnt[last] -> pinned host word, read at the next build
-    IGS_CUDA(ctx, cudaMemcpyAsync(b.total.p, tile_off + ntiles - 1, 4, cudaMemcpyDeviceToDevice, ctx->stream));
-    IGS_CUDA(ctx, cudaMemcpyAsync((char*)b.total.p + 4, tile_cnt + ntiles - 1, 4, cudaMemcpyDeviceToDevice,
-                                  ctx->stream));
+    total_kernel<<<1, 1, 0, ctx->stream>>>(tile_off, tile_cnt, ntiles, (unsigned long long*)b.total.p);
+    IGS_LAUNCHED(ctx);
+    IGS_CUDA(ctx, cudaMemcpyAsync(b.total_pinned, b.total.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
     igs_prof_end(ctx, IGS_PROF_CULL, 0.0);
     b.version = ctx->params_version;
     b.W = W;
@@ -511,9 +518,7 @@ int build_lists(igs_ctx* ctx, int W, int H, int pts_cells, int kk) {
 // host read of the last build's total pairs (syncs)
 uint64_t last_total(igs_ctx* ctx) {
     CullBufs& b = bufs(ctx);
-    uint32_t t[2] = {0, 0};
-    cudaMemcpy(t, b.total.p, 8, cudaMemcpyDeviceToHost);
-    *b.total_pinned = (unsigned long long)t[0] + t[1];
+    cudaStreamSynchronize(ctx->stream);
     return *b.total_pinned;
 }
 

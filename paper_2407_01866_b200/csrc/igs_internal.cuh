@@ -191,6 +191,7 @@ struct igs_ctx {
 
     PartitionDev* part = nullptr;
     void* cull = nullptr;            // CullBufs (cull.cu)
+    void* knn = nullptr;             // KnnBufs (knn.cu)
     uint64_t params_version = 0;     // bumped on every change of the set
 
     // profiling (igs_profile_*)
@@ -244,6 +245,8 @@ int igs_raster_global(igs_ctx* ctx, int W, int H, int k, int row0, int row1, flo
 int igs_topk_points(igs_ctx* ctx, const double* dev_uv, uint32_t npts, int k, uint32_t* dev_idx, double* dev_q);
 int igs_partition_free(igs_ctx* ctx);
 void igs_cull_free(igs_ctx* ctx);
+void igs_knn_free(igs_ctx* ctx);
+int igs_topk_knn(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq);
 int igs_topk_samples_culled(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq);
 int igs_topk_pixels_culled(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq, int W,
                            int H);

@@ -360,8 +360,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
     }
     int e;
     if (!ctx->opt_cull) e = igs_topk_points(ctx, uv, ns, k, li, lq);
-    else if (mode == 0) e = igs_topk_pixels_culled(ctx, uv, ns, k, li, lq, ctx->tgt_w, ctx->tgt_h);
-    else e = igs_topk_samples_culled(ctx, uv, ns, k, li, lq);
+    else e = igs_topk_knn(ctx, uv, ns, k, li, lq);
     if (e) return e;
     const size_t items = (size_t)ns * kk;
     if (ctx->opt_deterministic) {
