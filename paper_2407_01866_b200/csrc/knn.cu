@@ -1,23 +1,36 @@
 // knn.cu -- exact top-K at scattered points (training samples, point
-// queries) by branch-and-bound over a quadtree of Gaussian-centre bins.
+// queries) by branch-and-bound over a loose quadtree of the Gaussians.
 //
 // The reference scans all N Gaussians per sample (fit.cpp:65-84 ->
-// select_top_k_entries over ps.all_indices(), renderer.cpp:53-74).  Here:
-//   build (per set state): Gaussians bucketed into G x G centre cells
-//     (count / scan / fill), then a pyramid whose node stores the bbox of its
-//     members' centres, the smallest eigenvalue of their Sigma^-1
-//     (min(1/s1^2, 1/s2^2)), the largest anisotropy and a member count.
-//   query: one warp per point walks the pyramid near-first with an explicit
-//     stack.  A node is pruned iff its lower bound lb > tq, the current kk-th
-//     best q (strict, so index ties are never pruned).  lb = lambda_min *
-//     dist(p, bbox)^2 * (1 - slack): q >= lambda_min |x - mu|^2 in exact
-//     arithmetic, and slack covers |fl(q) - q| <= 9u (ia+ib) L1^2 <=
-//     18u (1 + aniso) q (forward error of renderer.cpp:17-23) plus the
-//     rounding of the bound itself.  Leaves: lanes evaluate 32 members at a
-//     time with maha() (the scan's exact op sequence); candidates that beat
-//     tq are inserted in lane order into a top-K replicated in every lane,
-//     so the kept set is exactly the kk smallest (q, idx) -- the reference's
-//     selection -- whatever the visit order.
+// select_top_k_entries over ps.all_indices(), renderer.cpp:53-74).
+//
+// Structure (rebuilt whenever the set changes): level l is a G_l x G_l grid
+// (G_l = G0 >> l) over [0,1]^2.  Each Gaussian is stored at the finest
+// level whose cell is at least twice its largest standard deviation
+// (sigma_max = 1/sqrt(min(1/s1^2, 1/s2^2))), in the cell holding its
+// centre -- so a cell's own members have sizes comparable to the cell and
+// Adam's quickly diverging scales (0.2 px .. 30 px after a dozen steps at
+// 2048^2) never loosen a bound.  Every cell keeps two summaries: its own
+// members and its whole subtree (own + children): centre bbox, smallest
+// Sigma^-1 eigenvalue lambda_min, a safety factor and a count.
+//
+// Certified bound: for every member g of a summary and point p,
+//   fl(q(g, p)) >= lambda_min * dist(p, bbox)^2 * slack,
+// since q >= lambda_min |p - mu|^2 in exact arithmetic and |fl(q) - q| <=
+// 9u (ia+ib) L1^2 <= 18u (1 + aniso) q (forward error of renderer.cpp:17-23);
+// slack = 1 - 2^-20 - 256u (1 + max aniso) also absorbs the bound's own
+// rounding.  A summary is skipped only if its bound exceeds tq, the current
+// kk-th best q (strictly, so index ties are never pruned).
+//
+// Query: one warp per point.  (1) Seed: the own members of the 3x3 cells
+// around the point at every level (big Gaussians included) give a tight tq
+// at once.  (2) Level-synchronous descent from the root: frontier nodes'
+// own members (outside the seed windows) are evaluated, children whose
+// subtree bound <= tq form the next frontier.  Members are evaluated 32 at a
+// time with maha() (the scan's exact op sequence); those beating tq are
+// inserted in lane order into a top-K replicated in every lane, so the kept
+// set is exactly the kk smallest (q, idx) -- the reference's selection.
+// A frontier larger than the per-warp queue restarts over all N (exact).
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
@@ -29,19 +42,20 @@ using namespace igs_dev;
 
 namespace {
 
-constexpr int kMaxLv = 12;
+constexpr int kMaxLv = 13;
+constexpr int kQueue = 512;  // per-warp frontier capacity
 
-struct Node {
-    double x0, y0, x1, y1;  // bbox of member centres (empty: +inf, -inf)
-    double lmin;            // min over members of min(ia, ib)
-    float slack;            // multiplicative safety factor for lb (0 = no pruning)
-    uint32_t count;         // members in the subtree
+struct Sum {
+    double x0, y0, x1, y1;  // centre bbox (empty: +inf/-inf)
+    double lmin;            // smallest Sigma^-1 eigenvalue
+    float slack;            // bound safety factor (0 = never prune)
+    uint32_t count;
 };
 
-struct Pyr {
-    int G;  // cells per side at level 0
-    int levels;
-    int lw[kMaxLv], loff[kMaxLv];
+struct Lq {
+    int G0, levels;
+    int lw[kMaxLv];    // cells per side
+    int loff[kMaxLv];  // first cell id of the level
 };
 
 __device__ __forceinline__ int cell_of(double v, int G) {
@@ -49,99 +63,167 @@ __device__ __forceinline__ int cell_of(double v, int G) {
     return isfinite(f) ? (int)fmin(fmax(f, 0.0), (double)(G - 1)) : 0;
 }
 
-__global__ void knn_bin_count(const ScanRec* __restrict__ scan, uint32_t n, int G, uint32_t* __restrict__ cnt,
-                              uint32_t* __restrict__ bin_of) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int c = cell_of(scan[i].mu_y, G) * G + cell_of(scan[i].mu_x, G);
-    bin_of[i] = (uint32_t)c;
-    atomicAdd(cnt + c, 1u);
-}
-
-__global__ void knn_bin_fill(uint32_t n, const uint32_t* __restrict__ bin_of, const uint32_t* __restrict__ off,
-                             uint32_t* __restrict__ cur, uint32_t* __restrict__ bins) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t c = bin_of[i];
-    bins[off[c] + atomicAdd(cur + c, 1u)] = i;
-}
-
 __device__ __forceinline__ float slack_for(double aniso) {
-    // 1 - (2^-20 + 256 u (1 + aniso)); no pruning if the bound degrades
     const double s = 1.0 - (9.5367431640625e-07 + 256.0 * 1.1102230246251565e-16 * (1.0 + aniso));
-    return s > 0.5 ? (float)(s - 1e-7) : 0.0f;  // round the float down
+    return s > 0.5 ? (float)(s - 1e-7) : 0.0f;
 }
 
-// level-0 nodes: one thread per cell reduces its members
-__global__ void knn_leaf_nodes(const ScanRec* __restrict__ scan, int G, const uint32_t* __restrict__ cnt,
-                               const uint32_t* __restrict__ off, const uint32_t* __restrict__ bins,
-                               Node* __restrict__ nodes) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= G * G) return;
+// Level whose cell (1/G_l) is >= 2 sigma_max: 4 G_l^2 <= lmin.
+__device__ __forceinline__ int level_of(const Lq& L, double lmin) {
+    int l = 0;
+    while (l < L.levels - 1 && !(4.0 * (double)L.lw[l] * (double)L.lw[l] <= lmin)) ++l;
+    return l;
+}
+
+__device__ __forceinline__ uint32_t key_of(const Lq& L, const ScanRec& r) {
+    const int l = level_of(L, fmin(r.inv_a, r.inv_b));
+    const int G = L.lw[l];
+    return (uint32_t)(L.loff[l] + cell_of(r.mu_y, G) * G + cell_of(r.mu_x, G));
+}
+
+__global__ void lq_count(const ScanRec* __restrict__ scan, uint32_t n, Lq L, uint32_t* __restrict__ cnt,
+                         uint32_t* __restrict__ key) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t k = key_of(L, scan[i]);
+    key[i] = k;
+    atomicAdd(cnt + k, 1u);
+}
+
+__global__ void lq_fill(uint32_t n, const uint32_t* __restrict__ key, const uint32_t* __restrict__ off,
+                        uint32_t* __restrict__ cur, uint32_t* __restrict__ mem) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t k = key[i];
+    mem[off[k] + atomicAdd(cur + k, 1u)] = i;
+}
+
+__device__ __forceinline__ Sum empty_sum() {
     const double inf = __longlong_as_double(0x7ff0000000000000LL);
-    Node nd;
-    nd.x0 = inf; nd.y0 = inf; nd.x1 = -inf; nd.y1 = -inf;
-    nd.lmin = inf;
+    Sum s;
+    s.x0 = inf; s.y0 = inf; s.x1 = -inf; s.y1 = -inf;
+    s.lmin = inf;
+    s.slack = 1.0f;
+    s.count = 0;
+    return s;
+}
+
+__device__ __forceinline__ void merge(Sum& a, const Sum& b) {
+    if (b.count == 0) return;
+    a.x0 = fmin(a.x0, b.x0); a.x1 = fmax(a.x1, b.x1);
+    a.y0 = fmin(a.y0, b.y0); a.y1 = fmax(a.y1, b.y1);
+    a.lmin = fmin(a.lmin, b.lmin);
+    a.slack = fminf(a.slack, b.slack);
+    a.count += b.count;
+}
+
+// own summary of every cell (all levels), one thread per cell
+__global__ void lq_own(const ScanRec* __restrict__ scan, uint32_t ncells, const uint32_t* __restrict__ cnt,
+                       const uint32_t* __restrict__ off, const uint32_t* __restrict__ mem, Sum* __restrict__ own) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncells) return;
+    Sum s = empty_sum();
     double aniso = 1.0;
     const uint32_t o = off[c], m = cnt[c];
     for (uint32_t j = 0; j < m; ++j) {
-        const ScanRec r = scan[bins[o + j]];
-        nd.x0 = fmin(nd.x0, r.mu_x); nd.x1 = fmax(nd.x1, r.mu_x);
-        nd.y0 = fmin(nd.y0, r.mu_y); nd.y1 = fmax(nd.y1, r.mu_y);
+        const ScanRec r = scan[mem[o + j]];
+        s.x0 = fmin(s.x0, r.mu_x); s.x1 = fmax(s.x1, r.mu_x);
+        s.y0 = fmin(s.y0, r.mu_y); s.y1 = fmax(s.y1, r.mu_y);
         const double lo = fmin(r.inv_a, r.inv_b), hi = fmax(r.inv_a, r.inv_b);
-        nd.lmin = fmin(nd.lmin, lo);
+        s.lmin = fmin(s.lmin, lo);
         aniso = fmax(aniso, hi / lo);
-        if (!(lo > 0.0) || !isfinite(hi) || !isfinite(r.mu_x) || !isfinite(r.mu_y)) aniso = inf;
+        if (!(lo > 0.0) || !isfinite(hi) || !isfinite(r.mu_x) || !isfinite(r.mu_y)) aniso = __longlong_as_double(0x7ff0000000000000LL);
     }
-    nd.slack = slack_for(aniso);
-    nd.count = m;
-    nodes[c] = nd;
+    s.slack = slack_for(aniso);
+    s.count = m;
+    own[c] = s;
 }
 
-__global__ void knn_up_nodes(Pyr p, int level, Node* __restrict__ nodes) {
-    const int w = p.lw[level];
+// subtree summaries of one level from its own + the finer level's subtrees
+__global__ void lq_subtree(Lq L, int level, const Sum* __restrict__ own, Sum* __restrict__ sub) {
+    const int w = L.lw[level];
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= w * w) return;
-    const int x = i % w, y = i / w, cw = p.lw[level - 1];
-    const Node* ch = nodes + p.loff[level - 1];
-    const double inf = __longlong_as_double(0x7ff0000000000000LL);
-    Node nd;
-    nd.x0 = inf; nd.y0 = inf; nd.x1 = -inf; nd.y1 = -inf;
-    nd.lmin = inf;
-    nd.slack = 1.0f;
-    nd.count = 0;
-    for (int dy = 0; dy < 2; ++dy)
-        for (int dx = 0; dx < 2; ++dx) {
-            const int cx = 2 * x + dx, cy = 2 * y + dy;
-            if (cx >= cw || cy >= cw) continue;
-            const Node c = ch[cy * cw + cx];
-            if (c.count == 0) continue;
-            nd.x0 = fmin(nd.x0, c.x0); nd.x1 = fmax(nd.x1, c.x1);
-            nd.y0 = fmin(nd.y0, c.y0); nd.y1 = fmax(nd.y1, c.y1);
-            nd.lmin = fmin(nd.lmin, c.lmin);
-            nd.slack = fminf(nd.slack, c.slack);
-            nd.count += c.count;
-        }
-    nodes[p.loff[level] + i] = nd;
+    Sum s = own[L.loff[level] + i];
+    if (level > 0) {
+        const int x = i % w, y = i / w, cw = L.lw[level - 1];
+        for (int dy = 0; dy < 2; ++dy)
+            for (int dx = 0; dx < 2; ++dx) {
+                const int cx = 2 * x + dx, cy = 2 * y + dy;
+                if (cx < cw && cy < cw) merge(s, sub[L.loff[level - 1] + cy * cw + cx]);
+            }
+    }
+    sub[L.loff[level] + i] = s;
 }
 
-// Certified lower bound of fl(q(g, p)) for every member g of the node.
-__device__ __forceinline__ double node_lb(const Node& nd, double px, double py) {
-    if (nd.count == 0) return __longlong_as_double(0x7ff0000000000000LL);
-    const double dx = fmax(fmax(nd.x0 - px, px - nd.x1), 0.0);
-    const double dy = fmax(fmax(nd.y0 - py, py - nd.y1), 0.0);
-    return nd.lmin * (dx * dx + dy * dy) * (double)nd.slack;
+__device__ __forceinline__ double sum_lb(const Sum& s, double px, double py) {
+    if (s.count == 0) return __longlong_as_double(0x7ff0000000000000LL);
+    const double dx = fmax(fmax(s.x0 - px, px - s.x1), 0.0);
+    const double dy = fmax(fmax(s.y0 - py, py - s.y1), 0.0);
+    return s.lmin * (dx * dx + dy * dy) * (double)s.slack;
+}
+
+// Evaluates the members of up to 32 cells (lane i: range [o_i, o_i + m_i)),
+// flattened so that all lanes work on members.
+template <int KCAP>
+__device__ __forceinline__ void eval_members(TopK<KCAP>& t, uint32_t o_mine, uint32_t m_mine, int lane,
+                                             const ScanRec* __restrict__ scan, const uint32_t* __restrict__ mem,
+                                             double px, double py, unsigned long long& evaluated) {
+    uint32_t incl = m_mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += v;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t excl = incl - m_mine;
+    evaluated += total;
+    for (uint32_t base = 0; base < total; base += 32) {
+        const uint32_t f = base + lane;
+        // cell holding flat member f: largest i with excl_i <= f (excl is
+        // non-decreasing; an empty cell never beats the one holding f)
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const uint32_t ex = __shfl_sync(0xffffffffu, excl, lo + step);
+            if (ex <= f) lo += step;
+        }
+        const uint32_t lo_ex = __shfl_sync(0xffffffffu, excl, lo);
+        const uint32_t lo_o = __shfl_sync(0xffffffffu, o_mine, lo);
+        double q = 0.0;
+        uint32_t gi = kNoIdx;
+        bool cand = false;
+        if (f < total) {
+            gi = __ldg(mem + lo_o + (f - lo_ex));
+            q = maha(scan[gi], px, py);
+            cand = t.beats(q, gi);
+        }
+        unsigned msk = __ballot_sync(0xffffffffu, cand);
+        while (msk) {
+            const int src = __ffs(msk) - 1;
+            msk &= msk - 1;
+            const double qq = __shfl_sync(0xffffffffu, q, src);
+            const uint32_t ii = __shfl_sync(0xffffffffu, gi, src);
+            t.offer(qq, ii);
+        }
+    }
+}
+
+__device__ __forceinline__ bool in_seed(int l, int x, int y, const int* scx, const int* scy) {
+    return x >= scx[l] - 1 && x <= scx[l] + 1 && y >= scy[l] - 1 && y <= scy[l] + 1;
 }
 
 // One warp per point.
 template <int KCAP>
-__global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restrict__ scan, Pyr p,
-                                                         const Node* __restrict__ nodes,
+__global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restrict__ scan, uint32_t n, Lq L,
+                                                         const Sum* __restrict__ own, const Sum* __restrict__ sub,
                                                          const uint32_t* __restrict__ off,
-                                                         const uint32_t* __restrict__ bins,
+                                                         const uint32_t* __restrict__ mem,
                                                          const double* __restrict__ uv, uint32_t npts, int kk,
                                                          double* __restrict__ oq, uint32_t* __restrict__ oi,
                                                          unsigned long long* __restrict__ pairs) {
+    __shared__ uint32_t queue[4][2][kQueue];
+    const int warp = threadIdx.x >> 5;
     const uint32_t pt = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (pt >= npts) return;  // warp-uniform
@@ -149,78 +231,118 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
     TopK<KCAP> t;
     t.init(kk);
     unsigned long long evaluated = 0;
-    uint32_t stack[3 * kMaxLv + 4];
-    int sp = 0;
-    stack[sp++] = (uint32_t)(p.levels - 1) << 26;
-    while (sp > 0) {
-        const uint32_t e = stack[--sp];
-        const int l = e >> 26, x = (e >> 13) & 0x1fff, y = e & 0x1fff;
-        const int w = p.lw[l];
-        const Node nd = nodes[p.loff[l] + y * w + x];
-        if (!(node_lb(nd, px, py) <= t.tq())) continue;
-        if (l == 0) {
-            const uint32_t o = off[y * w + x], m = nd.count;
-            for (uint32_t base = 0; base < m; base += 32) {
-                const uint32_t j = base + lane;
-                double q = 0.0;
-                uint32_t gi = kNoIdx;
-                bool cand = false;
-                if (j < m) {
-                    gi = __ldg(bins + o + j);
-                    q = maha(scan[gi], px, py);
-                    cand = t.beats(q, gi);
-                }
-                evaluated += min(32u, m - base);
-                unsigned msk = __ballot_sync(0xffffffffu, cand);
-                while (msk) {
-                    const int src = __ffs(msk) - 1;
-                    msk &= msk - 1;
-                    const double qq = __shfl_sync(0xffffffffu, q, src);
-                    const uint32_t ii = __shfl_sync(0xffffffffu, gi, src);
-                    t.offer(qq, ii);
-                }
-            }
-            continue;
-        }
-        // children: lane c < 4 computes child c's bound; push far-first
-        const int cw = p.lw[l - 1];
-        double lb = __longlong_as_double(0x7ff0000000000000LL);
-        uint32_t code = 0;
-        if (lane < 4) {
-            const int cx = 2 * x + (lane & 1), cy = 2 * y + (lane >> 1);
-            if (cx < cw && cy < cw) {
-                lb = node_lb(nodes[p.loff[l - 1] + cy * cw + cx], px, py);
-                code = ((uint32_t)(l - 1) << 26) | ((uint32_t)cx << 13) | (uint32_t)cy;
+    int scx[kMaxLv], scy[kMaxLv];
+#pragma unroll
+    for (int l = 0; l < kMaxLv; ++l) {
+        scx[l] = l < L.levels ? cell_of(px, L.lw[l]) : 0;
+        scy[l] = l < L.levels ? cell_of(py, L.lw[l]) : 0;
+    }
+
+    // (1) seeds: own members of the 3x3 window at every level
+    const int nseed = L.levels * 9;
+    for (int base = 0; base < nseed; base += 32) {
+        const int it = base + lane;
+        uint32_t o = 0, m = 0;
+        if (it < nseed) {
+            const int l = it / 9, d = it % 9;
+            const int x = scx[l] + d % 3 - 1, y = scy[l] + d / 3 - 1, G = L.lw[l];
+            if (x >= 0 && x < G && y >= 0 && y < G) {
+                const uint32_t c = (uint32_t)(L.loff[l] + y * G + x);
+                o = off[c];
+                m = own[c].count;
             }
         }
-        double cl[4];
-        uint32_t cc[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            cl[c] = __shfl_sync(0xffffffffu, lb, c);
-            cc[c] = __shfl_sync(0xffffffffu, code, c);
-        }
-        // sort 4 descending by bound (uniform across lanes)
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-            for (int b = 0; b < 3 - a; ++b)
-                if (cl[b] < cl[b + 1]) {
-                    const double tl = cl[b]; cl[b] = cl[b + 1]; cl[b + 1] = tl;
-                    const uint32_t tc = cc[b]; cc[b] = cc[b + 1]; cc[b + 1] = tc;
+        eval_members(t, o, m, lane, scan, mem, px, py, evaluated);
+    }
+
+    // (2) descent: evaluate own members of frontier nodes, expand children
+    uint32_t* cur = queue[warp][0];
+    uint32_t* nxt = queue[warp][1];
+    int ncur = 1;
+    if (lane == 0) cur[0] = 0;  // root cell of the top level
+    __syncwarp();
+    bool overflow = false;
+    for (int l = L.levels - 1; l >= 0 && ncur > 0; --l) {
+        const int w = L.lw[l];
+        // own members of the frontier (outside the seed window)
+        for (int base = 0; base < ncur; base += 32) {
+            const int i = base + lane;
+            uint32_t o = 0, m = 0;
+            if (i < ncur) {
+                const uint32_t node = cur[i];
+                const int x = node % w, y = node / w;
+                const uint32_t c = (uint32_t)L.loff[l] + node;
+                if (!in_seed(l, x, y, scx, scy)) {
+                    const Sum so = own[c];
+                    if (so.count && sum_lb(so, px, py) <= t.tq()) {
+                        o = off[c];
+                        m = so.count;
+                    }
                 }
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-            if (cl[c] <= t.tq() && sp < 3 * kMaxLv + 4) stack[sp++] = cc[c];
+            }
+            eval_members(t, o, m, lane, scan, mem, px, py, evaluated);
+        }
+        if (l == 0) break;
+        const int cw = L.lw[l - 1];
+        int nnext = 0;
+        for (int base = 0; base < ncur * 4; base += 32) {
+            const int item = base + lane;
+            bool keep = false;
+            uint32_t child = 0;
+            if (item < ncur * 4) {
+                const uint32_t node = cur[item >> 2];
+                const int x = node % w, y = node / w;
+                const int ccx = 2 * x + (item & 1), ccy = 2 * y + ((item >> 1) & 1);
+                if (ccx < cw && ccy < cw) {
+                    child = (uint32_t)(ccy * cw + ccx);
+                    keep = sum_lb(sub[L.loff[l - 1] + child], px, py) <= t.tq();
+                }
+            }
+            const unsigned msk = __ballot_sync(0xffffffffu, keep);
+            const int pos = nnext + __popc(msk & ((1u << lane) - 1));
+            if (keep && pos < kQueue) nxt[pos] = child;
+            nnext += __popc(msk);
+        }
+        __syncwarp();
+        if (nnext > kQueue) {
+            overflow = true;
+            break;
+        }
+        uint32_t* tmp = cur;
+        cur = nxt;
+        nxt = tmp;
+        ncur = nnext;
+    }
+
+    if (overflow) {
+        // exact fallback: restart and offer every Gaussian once, in index order
+        t.init(kk);
+        for (uint32_t base = 0; base < n; base += 32) {
+            const uint32_t gi = base + lane;
+            double q = 0.0;
+            bool cand = false;
+            if (gi < n) {
+                q = maha(scan[gi], px, py);
+                cand = t.beats(q, gi);
+            }
+            unsigned msk = __ballot_sync(0xffffffffu, cand);
+            while (msk) {
+                const int src = __ffs(msk) - 1;
+                msk &= msk - 1;
+                const double qq = __shfl_sync(0xffffffffu, q, src);
+                t.offer(qq, base + src);
+            }
+        }
+        evaluated += n;
     }
     if (pairs && lane == 0) atomicAdd(pairs, evaluated);
     if (lane == 0) store_topk(t, oq + (size_t)pt * kk, oi + (size_t)pt * kk);
 }
 
 struct KnnBufs {
-    DevBuf cnt, off, bin_of, bins, nodes, cub_tmp;
+    DevBuf cnt, off, key, mem, own, sub, cub_tmp;
     uint64_t version = ~0ull;
-    Pyr pyr{};
+    Lq lq{};
 };
 
 void* grow(DevBuf& b, size_t bytes) {
@@ -242,50 +364,49 @@ int knn_build(igs_ctx* ctx) {
     KnnBufs& b = *static_cast<KnnBufs*>(ctx->knn);
     if (b.version == ctx->params_version) return IGS_OK;
     const uint32_t n = ctx->n;
-    int G = 16;  // ~4 centres per cell
-    while (G < 2048 && (uint64_t)G * G * 4 < n) G *= 2;
-    Pyr p{};
-    p.G = G;
-    int l = 0, w = G, o = 0;
+    int G0 = 16;  // finest grid: about 2 centres per cell
+    while (G0 < 4096 && (uint64_t)G0 * G0 * 2 < n) G0 *= 2;
+    Lq L{};
+    L.G0 = G0;
+    int l = 0, w = G0, o = 0;
     for (;;) {
-        p.lw[l] = w;
-        p.loff[l] = o;
+        L.lw[l] = w;
+        L.loff[l] = o;
         o += w * w;
         ++l;
         if (w == 1) break;
         w /= 2;
     }
-    p.levels = l;
-    const int cells = G * G;
-    if (!grow(b.cnt, (size_t)cells * 8) || !grow(b.off, (size_t)cells * 4) || !grow(b.bin_of, (size_t)n * 4) ||
-        !grow(b.bins, (size_t)n * 4) || !grow(b.nodes, (size_t)o * sizeof(Node)))
+    L.levels = l;
+    const uint32_t cells = (uint32_t)o;
+    if (!grow(b.cnt, (size_t)cells * 8) || !grow(b.off, (size_t)cells * 4) || !grow(b.key, (size_t)n * 4) ||
+        !grow(b.mem, (size_t)n * 4) || !grow(b.own, (size_t)cells * sizeof(Sum)) ||
+        !grow(b.sub, (size_t)cells * sizeof(Sum)))
         return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
     uint32_t* cnt = (uint32_t*)b.cnt.p;
     uint32_t* cur = cnt + cells;
     uint32_t* off = (uint32_t*)b.off.p;
     igs_prof_begin(ctx, IGS_PROF_CULL);
     IGS_CUDA(ctx, cudaMemsetAsync(cnt, 0, (size_t)cells * 8, ctx->stream));
-    knn_bin_count<<<(n + 255) / 256, 256, 0, ctx->stream>>>(ctx->scan, n, G, cnt, (uint32_t*)b.bin_of.p);
+    lq_count<<<(n + 255) / 256, 256, 0, ctx->stream>>>(ctx->scan, n, L, cnt, (uint32_t*)b.key.p);
     IGS_LAUNCHED(ctx);
     size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, cells, ctx->stream);
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, (int)cells, ctx->stream);
     if (!grow(b.cub_tmp, tb)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn scan)");
-    IGS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(b.cub_tmp.p, tb, cnt, off, cells, ctx->stream));
+    IGS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(b.cub_tmp.p, tb, cnt, off, (int)cells, ctx->stream));
     ctx->launches += 2;
-    knn_bin_fill<<<(n + 255) / 256, 256, 0, ctx->stream>>>(n, (const uint32_t*)b.bin_of.p, off, cur,
-                                                           (uint32_t*)b.bins.p);
+    lq_fill<<<(n + 255) / 256, 256, 0, ctx->stream>>>(n, (const uint32_t*)b.key.p, off, cur, (uint32_t*)b.mem.p);
     IGS_LAUNCHED(ctx);
-    Node* nodes = (Node*)b.nodes.p;
-    knn_leaf_nodes<<<(cells + 127) / 128, 128, 0, ctx->stream>>>(ctx->scan, G, cnt, off, (const uint32_t*)b.bins.p,
-                                                                 nodes);
+    lq_own<<<(cells + 127) / 128, 128, 0, ctx->stream>>>(ctx->scan, cells, cnt, off, (const uint32_t*)b.mem.p,
+                                                         (Sum*)b.own.p);
     IGS_LAUNCHED(ctx);
-    for (int lv = 1; lv < p.levels; ++lv) {
-        const int m = p.lw[lv] * p.lw[lv];
-        knn_up_nodes<<<(m + 127) / 128, 128, 0, ctx->stream>>>(p, lv, nodes);
+    for (int lv = 0; lv < L.levels; ++lv) {
+        const int m = L.lw[lv] * L.lw[lv];
+        lq_subtree<<<(m + 127) / 128, 128, 0, ctx->stream>>>(L, lv, (const Sum*)b.own.p, (Sum*)b.sub.p);
         IGS_LAUNCHED(ctx);
     }
     igs_prof_end(ctx, IGS_PROF_CULL, 0.0);
-    b.pyr = p;
+    b.lq = L;
     b.version = ctx->params_version;
     return IGS_OK;
 }
@@ -296,8 +417,8 @@ int launch_knn(igs_ctx* ctx, const double* uv, uint32_t npts, int kk, uint32_t* 
     igs_prof_begin(ctx, IGS_PROF_SCAN);
     const uint64_t threads = (uint64_t)npts * 32;
     knn_points_kernel<KCAP><<<(unsigned)((threads + 127) / 128), 128, 0, ctx->stream>>>(
-        ctx->scan, b.pyr, (const Node*)b.nodes.p, (const uint32_t*)b.off.p, (const uint32_t*)b.bins.p, uv, npts, kk,
-        oq, oi, igs_prof_counter(ctx, IGS_PROF_SCAN));
+        ctx->scan, ctx->n, b.lq, (const Sum*)b.own.p, (const Sum*)b.sub.p, (const uint32_t*)b.off.p,
+        (const uint32_t*)b.mem.p, uv, npts, kk, oq, oi, igs_prof_counter(ctx, IGS_PROF_SCAN));
     IGS_LAUNCHED(ctx);
     igs_prof_end(ctx, IGS_PROF_SCAN, 0.0);
     return IGS_OK;
@@ -308,7 +429,7 @@ int launch_knn(igs_ctx* ctx, const double* uv, uint32_t npts, int kk, uint32_t* 
 void igs_knn_free(igs_ctx* ctx) {
     if (!ctx->knn) return;
     KnnBufs* b = static_cast<KnnBufs*>(ctx->knn);
-    for (DevBuf* d : {&b->cnt, &b->off, &b->bin_of, &b->bins, &b->nodes, &b->cub_tmp}) cudaFree(d->p);
+    for (DevBuf* d : {&b->cnt, &b->off, &b->key, &b->mem, &b->own, &b->sub, &b->cub_tmp}) cudaFree(d->p);
     delete b;
     ctx->knn = nullptr;
 }
