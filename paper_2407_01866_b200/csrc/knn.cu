@@ -209,19 +209,24 @@ __device__ __forceinline__ void eval_members(TopK<KCAP>& t, uint32_t o_mine, uin
     }
 }
 
-__device__ __forceinline__ bool in_seed(int l, int x, int y, const int* scx, const int* scy) {
-    return x >= scx[l] - 1 && x <= scx[l] + 1 && y >= scy[l] - 1 && y <= scy[l] + 1;
+__device__ __forceinline__ bool in_seed(const Lq& L, int l, int x, int y, double px, double py) {
+    const int sx = cell_of(px, L.lw[l]), sy = cell_of(py, L.lw[l]);
+    return x >= sx - 1 && x <= sx + 1 && y >= sy - 1 && y <= sy + 1;
 }
 
 // One warp per point.
+constexpr uint32_t kHardCap = 256;
+
 template <int KCAP>
-__global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restrict__ scan, uint32_t n, Lq L,
-                                                         const Sum* __restrict__ own, const Sum* __restrict__ sub,
-                                                         const uint32_t* __restrict__ off,
-                                                         const uint32_t* __restrict__ mem,
-                                                         const double* __restrict__ uv, uint32_t npts, int kk,
-                                                         double* __restrict__ oq, uint32_t* __restrict__ oi,
-                                                         unsigned long long* __restrict__ pairs) {
+__global__ void __launch_bounds__(128, 4) knn_points_kernel(const ScanRec* __restrict__ scan, uint32_t n, Lq L,
+                                                            const Sum* __restrict__ own, const Sum* __restrict__ sub,
+                                                            const uint32_t* __restrict__ off,
+                                                            const uint32_t* __restrict__ mem,
+                                                            const double* __restrict__ uv, uint32_t npts, int kk,
+                                                            double* __restrict__ oq, uint32_t* __restrict__ oi,
+                                                            unsigned long long* __restrict__ pairs,
+                                                            uint32_t* __restrict__ hard_count,
+                                                            uint32_t* __restrict__ hard_list) {
     __shared__ uint32_t queue[4][2][kQueue];
     const int warp = threadIdx.x >> 5;
     const uint32_t pt = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -231,12 +236,6 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
     TopK<KCAP> t;
     t.init(kk);
     unsigned long long evaluated = 0;
-    int scx[kMaxLv], scy[kMaxLv];
-#pragma unroll
-    for (int l = 0; l < kMaxLv; ++l) {
-        scx[l] = l < L.levels ? cell_of(px, L.lw[l]) : 0;
-        scy[l] = l < L.levels ? cell_of(py, L.lw[l]) : 0;
-    }
 
     // (1) seeds: own members of the 3x3 window at every level
     const int nseed = L.levels * 9;
@@ -244,8 +243,8 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
         const int it = base + lane;
         uint32_t o = 0, m = 0;
         if (it < nseed) {
-            const int l = it / 9, d = it % 9;
-            const int x = scx[l] + d % 3 - 1, y = scy[l] + d / 3 - 1, G = L.lw[l];
+            const int l = it / 9, d = it % 9, G = L.lw[l];
+            const int x = cell_of(px, G) + d % 3 - 1, y = cell_of(py, G) + d / 3 - 1;
             if (x >= 0 && x < G && y >= 0 && y < G) {
                 const uint32_t c = (uint32_t)(L.loff[l] + y * G + x);
                 o = off[c];
@@ -272,7 +271,7 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
                 const uint32_t node = cur[i];
                 const int x = node % w, y = node / w;
                 const uint32_t c = (uint32_t)L.loff[l] + node;
-                if (!in_seed(l, x, y, scx, scy)) {
+                if (!in_seed(L, l, x, y, px, py)) {
                     const Sum so = own[c];
                     if (so.count && sum_lb(so, px, py) <= t.tq()) {
                         o = off[c];
@@ -315,7 +314,15 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
     }
 
     if (overflow) {
-        // exact fallback: restart and offer every Gaussian once, in index order
+        // the frontier outgrew the queue: hand the point to hard_points_kernel
+        // (one CTA scans all N); beyond its capacity, scan all N here
+        uint32_t slot = 0;
+        if (lane == 0) slot = atomicAdd(hard_count, 1u);
+        slot = __shfl_sync(0xffffffffu, slot, 0);
+        if (slot < kHardCap) {
+            if (lane == 0) hard_list[slot] = pt;
+            return;
+        }
         t.init(kk);
         for (uint32_t base = 0; base < n; base += 32) {
             const uint32_t gi = base + lane;
@@ -339,8 +346,73 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
     if (lane == 0) store_topk(t, oq + (size_t)pt * kk, oi + (size_t)pt * kk);
 }
 
+// One CTA per hard point: 128 threads scan all N (coalesced 48-B records),
+// each keeping a private top-K; warp 0 folds the 128 lists into 32 lane
+// lists, then kk rounds of a warp-wide (q, idx) minimum emit the result.
+// Exact: the kept set is the kk smallest (q, idx) of the union.
+constexpr int kHardThreads = 128;
+
+template <int KCAP>
+__global__ void __launch_bounds__(kHardThreads) hard_points_kernel(const ScanRec* __restrict__ scan, uint32_t n,
+                                                                   const double* __restrict__ uv, int kk,
+                                                                   const uint32_t* __restrict__ hard_count,
+                                                                   const uint32_t* __restrict__ hard_list,
+                                                                   double* __restrict__ oq, uint32_t* __restrict__ oi,
+                                                                   unsigned long long* __restrict__ pairs) {
+    __shared__ double sq[kHardThreads * KCAP];
+    __shared__ uint32_t si[kHardThreads * KCAP];
+    const uint32_t cnt = min(*hard_count, kHardCap);
+    if (blockIdx.x >= cnt) return;
+    const uint32_t pt = hard_list[blockIdx.x];
+    const double px = uv[2 * (size_t)pt], py = uv[2 * (size_t)pt + 1];
+    TopK<KCAP> t;
+    t.init(kk);
+    for (uint32_t g = threadIdx.x; g < n; g += kHardThreads) {
+        const double q = maha(scan[g], px, py);
+        if (q <= t.tq()) t.offer(q, g);
+    }
+    store_topk(t, sq + threadIdx.x * KCAP, si + threadIdx.x * KCAP);
+    __syncthreads();
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    TopK<KCAP> m;
+    m.init(kk);
+    for (int th = lane; th < kHardThreads; th += 32)
+        for (int j = 0; j < kk; ++j) {
+            const uint32_t ci = si[th * KCAP + j];
+            if (ci == kNoIdx) break;
+            m.offer(sq[th * KCAP + j], ci);
+        }
+    __syncwarp();
+    store_topk(m, sq + lane * KCAP, si + lane * KCAP);
+    __syncwarp();
+    int head = 0;
+    for (int r = 0; r < kk; ++r) {
+        double v = head < kk ? sq[lane * KCAP + head] : __longlong_as_double(0x7ff0000000000000LL);
+        uint32_t vi = head < kk ? si[lane * KCAP + head] : kNoIdx;
+        int who = lane;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+            const uint32_t ovi = __shfl_xor_sync(0xffffffffu, vi, o);
+            const int ow = __shfl_xor_sync(0xffffffffu, who, o);
+            if (ov < v || (ov == v && ovi < vi) || (ov == v && ovi == vi && ow < who)) {
+                v = ov;
+                vi = ovi;
+                who = ow;
+            }
+        }
+        if (lane == who) ++head;
+        if (lane == 0) {
+            oq[(size_t)pt * kk + r] = v;
+            oi[(size_t)pt * kk + r] = vi;
+        }
+    }
+    if (pairs && lane == 0) atomicAdd(pairs, (unsigned long long)n);
+}
+
 struct KnnBufs {
-    DevBuf cnt, off, key, mem, own, sub, cub_tmp;
+    DevBuf cnt, off, key, mem, own, sub, cub_tmp, hard;
     uint64_t version = ~0ull;
     Lq lq{};
 };
@@ -414,11 +486,19 @@ int knn_build(igs_ctx* ctx) {
 template <int KCAP>
 int launch_knn(igs_ctx* ctx, const double* uv, uint32_t npts, int kk, uint32_t* oi, double* oq) {
     KnnBufs& b = *static_cast<KnnBufs*>(ctx->knn);
+    if (!grow(b.hard, (kHardCap + 1) * 4)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
+    uint32_t* hard_count = (uint32_t*)b.hard.p;
+    uint32_t* hard_list = hard_count + 1;
     igs_prof_begin(ctx, IGS_PROF_SCAN);
+    IGS_CUDA(ctx, cudaMemsetAsync(hard_count, 0, 4, ctx->stream));
     const uint64_t threads = (uint64_t)npts * 32;
     knn_points_kernel<KCAP><<<(unsigned)((threads + 127) / 128), 128, 0, ctx->stream>>>(
         ctx->scan, ctx->n, b.lq, (const Sum*)b.own.p, (const Sum*)b.sub.p, (const uint32_t*)b.off.p,
-        (const uint32_t*)b.mem.p, uv, npts, kk, oq, oi, igs_prof_counter(ctx, IGS_PROF_SCAN));
+        (const uint32_t*)b.mem.p, uv, npts, kk, oq, oi, igs_prof_counter(ctx, IGS_PROF_SCAN), hard_count,
+        hard_list);
+    IGS_LAUNCHED(ctx);
+    hard_points_kernel<KCAP><<<kHardCap, kHardThreads, 0, ctx->stream>>>(ctx->scan, ctx->n, uv, kk, hard_count, hard_list,
+                                                                oq, oi, igs_prof_counter(ctx, IGS_PROF_SCAN));
     IGS_LAUNCHED(ctx);
     igs_prof_end(ctx, IGS_PROF_SCAN, 0.0);
     return IGS_OK;
@@ -429,7 +509,7 @@ int launch_knn(igs_ctx* ctx, const double* uv, uint32_t npts, int kk, uint32_t* 
 void igs_knn_free(igs_ctx* ctx) {
     if (!ctx->knn) return;
     KnnBufs* b = static_cast<KnnBufs*>(ctx->knn);
-    for (DevBuf* d : {&b->cnt, &b->off, &b->key, &b->mem, &b->own, &b->sub, &b->cub_tmp}) cudaFree(d->p);
+    for (DevBuf* d : {&b->cnt, &b->off, &b->key, &b->mem, &b->own, &b->sub, &b->cub_tmp, &b->hard}) cudaFree(d->p);
     delete b;
     ctx->knn = nullptr;
 }

@@ -156,3 +156,20 @@ def test_append_keeps_indices(gctx, port, mode):
     got, gtk = gctx.render_image(48, 40, 10, want_topk=True)
     assert np.array_equal(gtk, wtk)
     check_image(got, want)
+
+
+def test_knn_hard_points_fallback(gctx, port):
+    """Points far from every Gaussian: the seed windows are empty, the frontier
+    overflows and the point is resolved by the one-CTA-per-point full scan."""
+    rng = np.random.default_rng(77)
+    params = synth.random_set(6000, 78, 0.0005, 0.002)
+    params[:, 0:2] = rng.random((6000, 2)) * 0.5
+    gctx.set_params(params)
+    uv = np.concatenate([rng.uniform(0.85, 1.0, (40, 2)), rng.random((200, 2)) * 0.5])
+    for k in (1, 10, 20):
+        idx, w, cnt = gctx.select_top_k(uv, k)
+        for p in range(0, uv.shape[0], 7):
+            wi, ww = port.select_top_k(params, uv[p, 0], uv[p, 1], k)
+            assert np.array_equal(idx[p, :cnt[p]], wi), (k, p)
+        np.testing.assert_allclose(gctx.render_points(uv, k), port.render_topk(params, uv, k), rtol=1e-12,
+                                   atol=1e-14)
