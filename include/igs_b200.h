@@ -183,6 +183,7 @@ int igs_fp64_peak(igs_ctx* ctx, double* ops_per_s);
 #define IGS_PROF_ADAM 3    /* fused Adam + constrain + prepare */
 #define IGS_PROF_CULL 4    /* certified tile-list construction */
 #define IGS_PROF_BLOCKED 5 /* BSP shell binning + blocked raster */
+#define IGS_PROF_KNN_HARD 6 /* work = points resolved by the full-scan fallback */
 #define IGS_PROF_FAMILIES 8
 int igs_profile_enable(igs_ctx* ctx, int on);
 /* total ms, launch count and algorithmic work (pairs for scans, bytes for

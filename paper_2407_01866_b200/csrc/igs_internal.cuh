@@ -247,6 +247,9 @@ int igs_partition_free(igs_ctx* ctx);
 void igs_cull_free(igs_ctx* ctx);
 void igs_knn_free(igs_ctx* ctx);
 int igs_topk_knn(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq);
+int igs_knn_forward_backward(igs_ctx* ctx, int mode, const uint32_t* sidx, const double* samples5, uint32_t npts,
+                             int kk, double inv_n, double* losses, double* contrib, uint32_t* keys,
+                             double* grads_atomic);
 int igs_topk_samples_culled(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq);
 int igs_topk_pixels_culled(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq, int W,
                            int H);

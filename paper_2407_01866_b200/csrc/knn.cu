@@ -163,10 +163,55 @@ __device__ __forceinline__ double sum_lb(const Sum& s, double px, double py) {
     return s.lmin * (dx * dx + dy * dy) * (double)s.slack;
 }
 
+// Warp-distributed top-K: lane j holds the j-th best (q, idx) for j < kk,
+// ascending in the strict (q, idx) order of select_top_k_entries
+// (renderer.cpp:53-74); lanes >= kk hold the (inf, kNoIdx) sentinel.  The
+// threshold (entry kk-1) is cached in every lane.  Insertion is
+// warp-uniform: the first lane whose entry exceeds the candidate takes it
+// and the tail shifts up one lane.
+struct WarpTopK {
+    double q;
+    uint32_t i;
+    double tq_;
+    uint32_t ti;
+    int kk, lane;
+
+    __device__ __forceinline__ void init(int kk_, int lane_) {
+        kk = kk_;
+        lane = lane_;
+        q = __longlong_as_double(0x7ff0000000000000LL);
+        i = kNoIdx;
+        tq_ = q;
+        ti = kNoIdx;
+    }
+    __device__ __forceinline__ double tq() const { return tq_; }
+    __device__ __forceinline__ bool beats(double cq, uint32_t ci) const {
+        return cq < tq_ || (cq == tq_ && ci < ti);
+    }
+    // warp-uniform (cq, ci); no effect unless it beats the threshold
+    __device__ __forceinline__ void offer(double cq, uint32_t ci) {
+        if (!beats(cq, ci)) return;
+        const bool gt = lane < kk && (cq < q || (cq == q && ci < i));
+        const unsigned m = __ballot_sync(0xffffffffu, gt);
+        const int pos = __ffs(m) - 1;
+        const double pq = __shfl_up_sync(0xffffffffu, q, 1);
+        const uint32_t pi = __shfl_up_sync(0xffffffffu, i, 1);
+        if (lane == pos) {
+            q = cq;
+            i = ci;
+        } else if (lane > pos && lane < kk) {
+            q = pq;
+            i = pi;
+        }
+        tq_ = __shfl_sync(0xffffffffu, q, kk - 1);
+        ti = __shfl_sync(0xffffffffu, i, kk - 1);
+    }
+};
+
 // Evaluates the members of up to 32 cells (lane i: range [o_i, o_i + m_i)),
 // flattened so that all lanes work on members.
-template <int KCAP>
-__device__ __forceinline__ void eval_members(TopK<KCAP>& t, uint32_t o_mine, uint32_t m_mine, int lane,
+template <class TK>
+__device__ __forceinline__ void eval_members(TK& t, uint32_t o_mine, uint32_t m_mine, int lane,
                                              const ScanRec* __restrict__ scan, const uint32_t* __restrict__ mem,
                                              double px, double py, unsigned long long& evaluated) {
     uint32_t incl = m_mine;
@@ -217,24 +262,156 @@ __device__ __forceinline__ bool in_seed(const Lq& L, int l, int x, int y, double
 // One warp per point.
 constexpr uint32_t kHardCap = 256;
 
-template <int KCAP>
-__global__ void __launch_bounds__(128, 4) knn_points_kernel(const ScanRec* __restrict__ scan, uint32_t n, Lq L,
+// What the warp does with its final top-K (lane j < kk holds entry j).
+struct Epi {
+    int mode;                    // 0 train (target L1), 1 backward (given upstream), 2 query (top-K out)
+    const uint32_t* sidx;        // mode 0: flat target pixel per point
+    const float* target;         // mode 0
+    const double* samples5;      // mode 1: upstream in columns 2..4
+    double inv_n;                // mode 0: 1 / (total samples over all ranks)
+    const ShadeRec* shade;
+    double* losses;              // mode 0: per point
+    double* contrib;             // modes 0/1: [pt][kk][8] (deterministic reduction) or null
+    uint32_t* keys;              // modes 0/1: [pt][kk] Gaussian index, n for empty slots
+    double* grads_atomic;        // modes 0/1: fast mode (fp64 atomics) or null
+    long long* status;           // status[2]: first non-finite loss
+    double* oq;                  // mode 2
+    uint32_t* oi;                // mode 2
+    uint32_t n;
+};
+
+// Query point: the centre of target pixel sidx[pt] (mode 0; pixel_center,
+// image.hpp:18-20 / fit.cpp:67-70), the sample's (u, v) (mode 1), or uv[pt].
+__device__ __forceinline__ void point_of(const double* __restrict__ uv, const Epi& E, int W, int H, uint32_t pt,
+                                         double& px, double& py) {
+    if (E.mode == 0) {
+        const int f = (int)E.sidx[pt];
+        px = center(f % W, W);
+        py = center(f / W, H);
+    } else if (E.mode == 1) {
+        px = E.samples5[(size_t)pt * 5];
+        py = E.samples5[(size_t)pt * 5 + 1];
+    } else {
+        px = uv[2 * (size_t)pt];
+        py = uv[2 * (size_t)pt + 1];
+    }
+}
+
+__device__ __forceinline__ double sign_of(double v) { return v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : 0.0); }
+
+// blend_entries (renderer.cpp:76-89) + the L1 loss / upstream (fit.cpp:67-80)
+// + sample_gradients (renderer.cpp:91-122), one lane per selected entry.  The
+// blend sums run in entry order through a shuffle chain so every lane holds
+// the reference's exact sequential totals.
+__device__ __forceinline__ void warp_epilogue(const Epi& E, const ScanRec* __restrict__ scan, uint32_t pt, int kk,
+                                              int lane, double myq, uint32_t myi, double px, double py) {
+    if (E.mode == 2) {
+        if (lane < kk) {
+            E.oq[(size_t)pt * kk + lane] = myq;
+            E.oi[(size_t)pt * kk + lane] = myi;
+        }
+        return;
+    }
+    const bool live = lane < kk && myi != kNoIdx;
+    double w = 0.0;
+    ShadeRec h{};
+    if (live) {
+        w = exp(__dmul_rn(-0.5, myq));
+        h = E.shade[myi];
+    }
+    double total = 0.0, ar = 0.0, ag = 0.0, ab = 0.0;
+    for (int j = 0; j < kk; ++j) {
+        const double wj = __shfl_sync(0xffffffffu, w, j);
+        const double rj = __shfl_sync(0xffffffffu, h.r, j);
+        const double gj = __shfl_sync(0xffffffffu, h.g, j);
+        const double bj = __shfl_sync(0xffffffffu, h.b, j);
+        if (__shfl_sync(0xffffffffu, live ? 1 : 0, j)) {
+            total = __dadd_rn(total, wj);
+            ar = __dadd_rn(ar, __dmul_rn(wj, rj));
+            ag = __dadd_rn(ag, __dmul_rn(wj, gj));
+            ab = __dadd_rn(ab, __dmul_rn(wj, bj));
+        }
+    }
+    const double inv_denom = __ddiv_rn(1.0, __dadd_rn(kNormEps, total));
+    const double c0 = __dmul_rn(ar, inv_denom), c1 = __dmul_rn(ag, inv_denom), c2 = __dmul_rn(ab, inv_denom);
+    double up0, up1, up2;
+    if (E.mode == 0) {
+        const float* t = E.target + (size_t)E.sidx[pt] * 3;
+        const double d0 = __dsub_rn(c0, (double)t[0]);
+        const double d1 = __dsub_rn(c1, (double)t[1]);
+        const double d2 = __dsub_rn(c2, (double)t[2]);
+        if (lane == 0) {
+            const double l = __dadd_rn(__dadd_rn(fabs(d0), fabs(d1)), fabs(d2));
+            E.losses[pt] = l;
+            if (!isfinite(l)) atomicMin(E.status + 2, (long long)pt);
+        }
+        up0 = __dmul_rn(sign_of(d0), E.inv_n);
+        up1 = __dmul_rn(sign_of(d1), E.inv_n);
+        up2 = __dmul_rn(sign_of(d2), E.inv_n);
+    } else {
+        up0 = E.samples5[(size_t)pt * 5 + 2];
+        up1 = E.samples5[(size_t)pt * 5 + 3];
+        up2 = E.samples5[(size_t)pt * 5 + 4];
+    }
+    if (lane >= kk) return;
+    const size_t slot = (size_t)pt * kk + lane;
+    if (!live) {
+        if (E.keys) E.keys[slot] = E.n;  // sorts past every real index
+        return;
+    }
+    const ScanRec g = scan[myi];
+    const double dL_dw = __dmul_rn(
+        __dadd_rn(__dadd_rn(__dmul_rn(up0, __dsub_rn(h.r, c0)), __dmul_rn(up1, __dsub_rn(h.g, c1))),
+                  __dmul_rn(up2, __dsub_rn(h.b, c2))),
+        inv_denom);
+    const double wc = __dmul_rn(w, inv_denom);
+    const double dx = __dsub_rn(px, g.mu_x);
+    const double dy = __dsub_rn(py, g.mu_y);
+    const double e1 = __dadd_rn(__dmul_rn(g.cos_t, dx), __dmul_rn(g.sin_t, dy));
+    const double e2 = __dadd_rn(__dmul_rn(-g.sin_t, dx), __dmul_rn(g.cos_t, dy));
+    const double v1 = __dmul_rn(e1, g.inv_a);
+    const double v2 = __dmul_rn(e2, g.inv_b);
+    const double lw = __dmul_rn(dL_dw, w);
+    double d[8];
+    d[0] = __dmul_rn(lw, __dsub_rn(__dmul_rn(g.cos_t, v1), __dmul_rn(g.sin_t, v2)));
+    d[1] = __dmul_rn(lw, __dadd_rn(__dmul_rn(g.sin_t, v1), __dmul_rn(g.cos_t, v2)));
+    d[2] = __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(dL_dw, -w), e1), e2), __dsub_rn(g.inv_a, g.inv_b));
+    d[3] = __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(lw, e1), e1), g.inv_a), h.inv_s1);
+    d[4] = __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(lw, e2), e2), g.inv_b), h.inv_s2);
+    d[5] = __dmul_rn(up0, wc);
+    d[6] = __dmul_rn(up1, wc);
+    d[7] = __dmul_rn(up2, wc);
+    if (E.grads_atomic) {
+#pragma unroll
+        for (int p = 0; p < 8; ++p) atomicAdd(E.grads_atomic + (size_t)myi * 8 + p, d[p]);
+    } else {
+        double2* o = reinterpret_cast<double2*>(E.contrib + slot * 8);
+        o[0] = make_double2(d[0], d[1]);
+        o[1] = make_double2(d[2], d[3]);
+        o[2] = make_double2(d[4], d[5]);
+        o[3] = make_double2(d[6], d[7]);
+        E.keys[slot] = myi;
+    }
+}
+
+__global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restrict__ scan, uint32_t n, Lq L,
                                                             const Sum* __restrict__ own, const Sum* __restrict__ sub,
                                                             const uint32_t* __restrict__ off,
                                                             const uint32_t* __restrict__ mem,
-                                                            const double* __restrict__ uv, uint32_t npts, int kk,
-                                                            double* __restrict__ oq, uint32_t* __restrict__ oi,
-                                                            unsigned long long* __restrict__ pairs,
+                                                            const double* __restrict__ uv, int W, int H, uint32_t npts,
+                                                            int kk, Epi E, unsigned long long* __restrict__ pairs,
                                                             uint32_t* __restrict__ hard_count,
-                                                            uint32_t* __restrict__ hard_list) {
+                                                            uint32_t* __restrict__ hard_list,
+                                                            unsigned long long* __restrict__ hard_stat) {
     __shared__ uint32_t queue[4][2][kQueue];
     const int warp = threadIdx.x >> 5;
     const uint32_t pt = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (pt >= npts) return;  // warp-uniform
-    const double px = uv[2 * (size_t)pt], py = uv[2 * (size_t)pt + 1];
-    TopK<KCAP> t;
-    t.init(kk);
+    double px, py;
+    point_of(uv, E, W, H, pt, px, py);
+    WarpTopK t;
+    t.init(kk, lane);
     unsigned long long evaluated = 0;
 
     // (1) seeds: own members of the 3x3 window at every level
@@ -318,12 +495,13 @@ __global__ void __launch_bounds__(128, 4) knn_points_kernel(const ScanRec* __res
         // (one CTA scans all N); beyond its capacity, scan all N here
         uint32_t slot = 0;
         if (lane == 0) slot = atomicAdd(hard_count, 1u);
+        if (lane == 0 && hard_stat) atomicAdd(hard_stat, 1ull);
         slot = __shfl_sync(0xffffffffu, slot, 0);
         if (slot < kHardCap) {
             if (lane == 0) hard_list[slot] = pt;
             return;
         }
-        t.init(kk);
+        t.init(kk, lane);
         for (uint32_t base = 0; base < n; base += 32) {
             const uint32_t gi = base + lane;
             double q = 0.0;
@@ -343,7 +521,7 @@ __global__ void __launch_bounds__(128, 4) knn_points_kernel(const ScanRec* __res
         evaluated += n;
     }
     if (pairs && lane == 0) atomicAdd(pairs, evaluated);
-    if (lane == 0) store_topk(t, oq + (size_t)pt * kk, oi + (size_t)pt * kk);
+    warp_epilogue(E, scan, pt, kk, lane, t.q, t.i, px, py);
 }
 
 // One CTA per hard point: 128 threads scan all N (coalesced 48-B records),
@@ -354,17 +532,17 @@ constexpr int kHardThreads = 128;
 
 template <int KCAP>
 __global__ void __launch_bounds__(kHardThreads) hard_points_kernel(const ScanRec* __restrict__ scan, uint32_t n,
-                                                                   const double* __restrict__ uv, int kk,
+                                                                   const double* __restrict__ uv, int W, int H, int kk,
                                                                    const uint32_t* __restrict__ hard_count,
-                                                                   const uint32_t* __restrict__ hard_list,
-                                                                   double* __restrict__ oq, uint32_t* __restrict__ oi,
+                                                                   const uint32_t* __restrict__ hard_list, Epi E,
                                                                    unsigned long long* __restrict__ pairs) {
     __shared__ double sq[kHardThreads * KCAP];
     __shared__ uint32_t si[kHardThreads * KCAP];
     const uint32_t cnt = min(*hard_count, kHardCap);
     if (blockIdx.x >= cnt) return;
     const uint32_t pt = hard_list[blockIdx.x];
-    const double px = uv[2 * (size_t)pt], py = uv[2 * (size_t)pt + 1];
+    double px, py;
+    point_of(uv, E, W, H, pt, px, py);
     TopK<KCAP> t;
     t.init(kk);
     for (uint32_t g = threadIdx.x; g < n; g += kHardThreads) {
@@ -387,6 +565,8 @@ __global__ void __launch_bounds__(kHardThreads) hard_points_kernel(const ScanRec
     store_topk(m, sq + lane * KCAP, si + lane * KCAP);
     __syncwarp();
     int head = 0;
+    double myq = __longlong_as_double(0x7ff0000000000000LL);
+    uint32_t myi = kNoIdx;
     for (int r = 0; r < kk; ++r) {
         double v = head < kk ? sq[lane * KCAP + head] : __longlong_as_double(0x7ff0000000000000LL);
         uint32_t vi = head < kk ? si[lane * KCAP + head] : kNoIdx;
@@ -403,12 +583,13 @@ __global__ void __launch_bounds__(kHardThreads) hard_points_kernel(const ScanRec
             }
         }
         if (lane == who) ++head;
-        if (lane == 0) {
-            oq[(size_t)pt * kk + r] = v;
-            oi[(size_t)pt * kk + r] = vi;
+        if (lane == r) {
+            myq = v;
+            myi = vi;
         }
     }
     if (pairs && lane == 0) atomicAdd(pairs, (unsigned long long)n);
+    warp_epilogue(E, scan, pt, kk, lane, myq, myi, px, py);
 }
 
 struct KnnBufs {
@@ -484,7 +665,7 @@ int knn_build(igs_ctx* ctx) {
 }
 
 template <int KCAP>
-int launch_knn(igs_ctx* ctx, const double* uv, uint32_t npts, int kk, uint32_t* oi, double* oq) {
+int launch_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int kk, const Epi& E) {
     KnnBufs& b = *static_cast<KnnBufs*>(ctx->knn);
     if (!grow(b.hard, (kHardCap + 1) * 4)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
     uint32_t* hard_count = (uint32_t*)b.hard.p;
@@ -492,16 +673,25 @@ int launch_knn(igs_ctx* ctx, const double* uv, uint32_t npts, int kk, uint32_t* 
     igs_prof_begin(ctx, IGS_PROF_SCAN);
     IGS_CUDA(ctx, cudaMemsetAsync(hard_count, 0, 4, ctx->stream));
     const uint64_t threads = (uint64_t)npts * 32;
-    knn_points_kernel<KCAP><<<(unsigned)((threads + 127) / 128), 128, 0, ctx->stream>>>(
+    knn_points_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, ctx->stream>>>(
         ctx->scan, ctx->n, b.lq, (const Sum*)b.own.p, (const Sum*)b.sub.p, (const uint32_t*)b.off.p,
-        (const uint32_t*)b.mem.p, uv, npts, kk, oq, oi, igs_prof_counter(ctx, IGS_PROF_SCAN), hard_count,
-        hard_list);
+        (const uint32_t*)b.mem.p, uv, W, H, npts, kk, E, igs_prof_counter(ctx, IGS_PROF_SCAN), hard_count,
+        hard_list, igs_prof_counter(ctx, IGS_PROF_KNN_HARD));
     IGS_LAUNCHED(ctx);
-    hard_points_kernel<KCAP><<<kHardCap, kHardThreads, 0, ctx->stream>>>(ctx->scan, ctx->n, uv, kk, hard_count, hard_list,
-                                                                oq, oi, igs_prof_counter(ctx, IGS_PROF_SCAN));
+    hard_points_kernel<KCAP><<<kHardCap, kHardThreads, 0, ctx->stream>>>(
+        ctx->scan, ctx->n, uv, W, H, kk, hard_count, hard_list, E, igs_prof_counter(ctx, IGS_PROF_SCAN));
     IGS_LAUNCHED(ctx);
     igs_prof_end(ctx, IGS_PROF_SCAN, 0.0);
     return IGS_OK;
+}
+
+int run_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int kk, const Epi& E) {
+    int e = knn_build(ctx);
+    if (e) return e;
+    if (kk <= 4) return launch_knn<4>(ctx, uv, W, H, npts, kk, E);
+    if (kk <= 8) return launch_knn<8>(ctx, uv, W, H, npts, kk, E);
+    if (kk <= 16) return launch_knn<16>(ctx, uv, W, H, npts, kk, E);
+    return launch_knn<32>(ctx, uv, W, H, npts, kk, E);
 }
 
 }  // namespace
@@ -518,10 +708,34 @@ void igs_knn_free(igs_ctx* ctx) {
 int igs_topk_knn(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq) {
     const int kk = (int)std::min<uint32_t>((uint32_t)k, ctx->n);
     if (kk > 32 || npts == 0) return igs_topk_points(ctx, uv, npts, k, oi, oq);
-    int e = knn_build(ctx);
-    if (e) return e;
-    if (kk <= 4) return launch_knn<4>(ctx, uv, npts, kk, oi, oq);
-    if (kk <= 8) return launch_knn<8>(ctx, uv, npts, kk, oi, oq);
-    if (kk <= 16) return launch_knn<16>(ctx, uv, npts, kk, oi, oq);
-    return launch_knn<32>(ctx, uv, npts, kk, oi, oq);
+    Epi E{};
+    E.mode = 2;
+    E.oq = oq;
+    E.oi = oi;
+    E.n = ctx->n;
+    return run_knn(ctx, uv, 0, 0, npts, kk, E);
+}
+
+// Fused forward + backward at points (kk <= 32): the top-K search with the
+// blend / loss / gradient epilogue.  mode 0: sampled target pixels (sidx),
+// mode 1: samples5 (u, v, upstream).  Writes losses and either the
+// contribution records + sort keys (contrib != null) or fp64 atomics into
+// grads_atomic.
+int igs_knn_forward_backward(igs_ctx* ctx, int mode, const uint32_t* sidx, const double* samples5, uint32_t npts,
+                             int kk, double inv_n, double* losses, double* contrib, uint32_t* keys,
+                             double* grads_atomic) {
+    Epi E{};
+    E.mode = mode;
+    E.sidx = sidx;
+    E.target = (const float*)ctx->target.p;
+    E.samples5 = samples5;
+    E.inv_n = inv_n;
+    E.shade = ctx->shade;
+    E.losses = losses;
+    E.contrib = contrib;
+    E.keys = keys;
+    E.grads_atomic = grads_atomic;
+    E.status = ctx->status;
+    E.n = ctx->n;
+    return run_knn(ctx, nullptr, ctx->tgt_w, ctx->tgt_h, npts, kk, E);
 }

@@ -345,37 +345,50 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
                          const double* dev_samples5, double* dev_loss, double inv_n) {
     const uint32_t n = ctx->n;
     const int kk = (int)std::min<uint32_t>((uint32_t)k, n);
-    double* uv = (double*)igs_scratch(ctx, 0, (size_t)ns * 2 * sizeof(double));
-    double* lq = (double*)igs_scratch(ctx, 1, (size_t)ns * kk * sizeof(double));
-    uint32_t* li = (uint32_t*)igs_scratch(ctx, 2, (size_t)ns * kk * sizeof(uint32_t));
-    double* losses = (double*)igs_scratch(ctx, 9, (size_t)std::max<uint32_t>(ns, 1) * sizeof(double));
-    if (!uv || !lq || !li || !losses) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (train)");
-    const int tb = 256;
-    if (mode == 0) {
-        sample_coords_kernel<<<(ns + tb - 1) / tb, tb, 0, ctx->stream>>>(dev_sidx, ns, ctx->tgt_w, ctx->tgt_h, uv);
-        IGS_LAUNCHED(ctx);
-    } else {
-        IGS_CUDA(ctx, cudaMemcpy2DAsync(uv, 2 * sizeof(double), dev_samples5, 5 * sizeof(double),
-                                        2 * sizeof(double), ns, cudaMemcpyDeviceToDevice, ctx->stream));
-    }
-    int e;
-    if (!ctx->opt_cull) e = igs_topk_points(ctx, uv, ns, k, li, lq);
-    else e = igs_topk_knn(ctx, uv, ns, k, li, lq);
-    if (e) return e;
     const size_t items = (size_t)ns * kk;
+    double* losses = (double*)igs_scratch(ctx, 9, (size_t)std::max<uint32_t>(ns, 1) * sizeof(double));
+    double* contrib = nullptr;
+    uint32_t *keys = nullptr, *skeys = nullptr, *vals = nullptr, *svals = nullptr;
     if (ctx->opt_deterministic) {
-        double* contrib = (double*)igs_scratch(ctx, 3, items * 8 * sizeof(double));
-        uint32_t* keys = (uint32_t*)igs_scratch(ctx, 4, items * sizeof(uint32_t));
-        uint32_t* skeys = (uint32_t*)igs_scratch(ctx, 5, items * sizeof(uint32_t));
-        uint32_t* vals = (uint32_t*)igs_scratch(ctx, 6, items * sizeof(uint32_t));
-        uint32_t* svals = (uint32_t*)igs_scratch(ctx, 7, items * sizeof(uint32_t));
+        contrib = (double*)igs_scratch(ctx, 3, items * 8 * sizeof(double));
+        keys = (uint32_t*)igs_scratch(ctx, 4, items * sizeof(uint32_t));
+        skeys = (uint32_t*)igs_scratch(ctx, 5, items * sizeof(uint32_t));
+        vals = (uint32_t*)igs_scratch(ctx, 6, items * sizeof(uint32_t));
+        svals = (uint32_t*)igs_scratch(ctx, 7, items * sizeof(uint32_t));
         if (!contrib || !keys || !skeys || !vals || !svals) return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
+    } else {
+        IGS_CUDA(ctx, cudaMemsetAsync(ctx->grads, 0, (size_t)n * 8 * sizeof(double), ctx->stream));
+    }
+    if (!losses) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (train)");
+    int e;
+    if (ctx->opt_cull && kk <= 32) {
+        // fused: exact top-K search + blend / loss / gradient epilogue per warp
+        e = igs_knn_forward_backward(ctx, mode, dev_sidx, dev_samples5, ns, kk, inv_n, losses, contrib, keys,
+                                     ctx->opt_deterministic ? nullptr : ctx->grads);
+        if (e) return e;
+    } else {
+        double* uv = (double*)igs_scratch(ctx, 0, (size_t)ns * 2 * sizeof(double));
+        double* lq = (double*)igs_scratch(ctx, 1, (size_t)ns * kk * sizeof(double));
+        uint32_t* li = (uint32_t*)igs_scratch(ctx, 2, (size_t)ns * kk * sizeof(uint32_t));
+        if (!uv || !lq || !li) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (train)");
+        const int tb = 256;
+        if (mode == 0) {
+            sample_coords_kernel<<<(ns + tb - 1) / tb, tb, 0, ctx->stream>>>(dev_sidx, ns, ctx->tgt_w, ctx->tgt_h,
+                                                                             uv);
+            IGS_LAUNCHED(ctx);
+        } else {
+            IGS_CUDA(ctx, cudaMemcpy2DAsync(uv, 2 * sizeof(double), dev_samples5, 5 * sizeof(double),
+                                            2 * sizeof(double), ns, cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+        if ((e = igs_topk_points(ctx, uv, ns, k, li, lq))) return e;
         igs_prof_begin(ctx, IGS_PROF_FINISH);
         sample_finish_kernel<<<(ns + 127) / 128, 128, 0, ctx->stream>>>(
             ctx->scan, ctx->shade, n, lq, li, kk, ns, uv, mode, dev_sidx, (const float*)ctx->target.p, ctx->tgt_w,
-            dev_samples5, inv_n, losses, contrib, keys, nullptr, ctx->status);
+            dev_samples5, inv_n, losses, contrib, keys, ctx->opt_deterministic ? nullptr : ctx->grads, ctx->status);
         IGS_LAUNCHED(ctx);
         igs_prof_end(ctx, IGS_PROF_FINISH, (double)items);
+    }
+    if (ctx->opt_deterministic) {
         igs_prof_begin(ctx, IGS_PROF_REDUCE);
         iota_kernel<<<(unsigned)((items + 255) / 256), 256, 0, ctx->stream>>>(vals, (uint32_t)items);
         IGS_LAUNCHED(ctx);
@@ -388,17 +401,11 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
         if (!temp) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (sort)");
         IGS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, skeys, vals, svals, (int)items, 0,
                                                       end_bit, ctx->stream));
-        ctx->launches += (uint64_t)((end_bit + 7) / 8) * 3;  // onesweep: histogram + per-pass kernels (approx.)
+        ctx->launches += (uint64_t)((end_bit + 7) / 8) + 2;  // histogram, exclusive sum, one onesweep per pass
         segment_reduce_kernel<<<(n + 255) / 256, 256, 0, ctx->stream>>>(skeys, svals, (uint32_t)items, contrib, n,
                                                                         ctx->grads);
         IGS_LAUNCHED(ctx);
         igs_prof_end(ctx, IGS_PROF_REDUCE, (double)items);
-    } else {
-        IGS_CUDA(ctx, cudaMemsetAsync(ctx->grads, 0, (size_t)n * 8 * sizeof(double), ctx->stream));
-        sample_finish_kernel<<<(ns + 127) / 128, 128, 0, ctx->stream>>>(
-            ctx->scan, ctx->shade, n, lq, li, kk, ns, uv, mode, dev_sidx, (const float*)ctx->target.p, ctx->tgt_w,
-            dev_samples5, inv_n, losses, nullptr, nullptr, ctx->grads, ctx->status);
-        IGS_LAUNCHED(ctx);
     }
     if (mode == 0 && dev_loss) {
         loss_reduce_kernel<<<1, 1024, 0, ctx->stream>>>(losses, ns, inv_n, dev_loss);

@@ -47,8 +47,8 @@ ERROR_KINDS = {
 }
 
 OPT_CULL, OPT_DETERMINISTIC, OPT_TILE = 1, 2, 3
-PROF_SCAN, PROF_FINISH, PROF_REDUCE, PROF_ADAM, PROF_CULL, PROF_BLOCKED = range(6)
-PROF_NAMES = ["scan", "finish", "reduce", "adam", "cull", "blocked"]
+PROF_SCAN, PROF_FINISH, PROF_REDUCE, PROF_ADAM, PROF_CULL, PROF_BLOCKED, PROF_KNN_HARD = range(7)
+PROF_NAMES = ["scan", "finish", "reduce", "adam", "cull", "blocked", "knn_hard"]
 
 # Learning rates in the reference's LearningRates field order (adam.hpp:11-16).
 DEFAULT_LR = (2e-4, 2e-3, 1e-3, 1e-3)  # mu, color, scale, theta
