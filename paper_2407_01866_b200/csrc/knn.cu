@@ -117,11 +117,9 @@ __device__ __forceinline__ void merge(Sum& a, const Sum& b) {
     a.count += b.count;
 }
 
-// own summary of every cell (all levels), one thread per cell
-__global__ void lq_own(const ScanRec* __restrict__ scan, uint32_t ncells, const uint32_t* __restrict__ cnt,
-                       const uint32_t* __restrict__ off, const uint32_t* __restrict__ mem, Sum* __restrict__ own) {
-    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= ncells) return;
+// Own summary of cell c: reduce its members.
+__device__ __forceinline__ Sum own_of(const ScanRec* __restrict__ scan, const uint32_t* __restrict__ cnt,
+                                      const uint32_t* __restrict__ off, const uint32_t* __restrict__ mem, uint32_t c) {
     Sum s = empty_sum();
     double aniso = 1.0;
     const uint32_t o = off[c], m = cnt[c];
@@ -132,28 +130,80 @@ __global__ void lq_own(const ScanRec* __restrict__ scan, uint32_t ncells, const 
         const double lo = fmin(r.inv_a, r.inv_b), hi = fmax(r.inv_a, r.inv_b);
         s.lmin = fmin(s.lmin, lo);
         aniso = fmax(aniso, hi / lo);
-        if (!(lo > 0.0) || !isfinite(hi) || !isfinite(r.mu_x) || !isfinite(r.mu_y)) aniso = __longlong_as_double(0x7ff0000000000000LL);
+        if (!(lo > 0.0) || !isfinite(hi) || !isfinite(r.mu_x) || !isfinite(r.mu_y))
+            aniso = __longlong_as_double(0x7ff0000000000000LL);
     }
     s.slack = slack_for(aniso);
     s.count = m;
-    own[c] = s;
+    return s;
 }
 
-// subtree summaries of one level from its own + the finer level's subtrees
-__global__ void lq_subtree(Lq L, int level, const Sum* __restrict__ own, Sum* __restrict__ sub) {
-    const int w = L.lw[level];
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= w * w) return;
-    Sum s = own[L.loff[level] + i];
-    if (level > 0) {
-        const int x = i % w, y = i / w, cw = L.lw[level - 1];
-        for (int dy = 0; dy < 2; ++dy)
-            for (int dx = 0; dx < 2; ++dx) {
-                const int cx = 2 * x + dx, cy = 2 * y + dy;
-                if (cx < cw && cy < cw) merge(s, sub[L.loff[level - 1] + cy * cw + cx]);
+// All own + subtree summaries in one launch.  CTA (bx, by) owns a 16 x 16
+// block of level-0 cells and builds levels 0..4 of that block in shared
+// memory (subtree = own + the four children); the last CTA to finish (atomic
+// ticket after a fence) builds the levels above from global memory.
+constexpr int kBlk = 16;
+
+__global__ void __launch_bounds__(256) lq_tree_kernel(const ScanRec* __restrict__ scan, Lq L,
+                                                      const uint32_t* __restrict__ cnt,
+                                                      const uint32_t* __restrict__ off,
+                                                      const uint32_t* __restrict__ mem, Sum* __restrict__ own,
+                                                      Sum* __restrict__ sub, unsigned int* __restrict__ ticket) {
+    __shared__ Sum sm[2][kBlk * kBlk];
+    const int t = threadIdx.x;
+    const int nb = (L.G0 + kBlk - 1) / kBlk;
+    const int bx = blockIdx.x % nb, by = blockIdx.x / nb;
+    int cur = 0;
+    const int inlv = min(L.levels, 5);  // levels 0..4 live inside a block
+    for (int l = 0; l < inlv; ++l) {
+        const int side = kBlk >> l;  // this block's cells per side at level l
+        const int G = L.lw[l];
+        if (t < side * side) {
+            const int x = bx * side + t % side, y = by * side + t / side;
+            Sum s = empty_sum();
+            if (x < G && y < G) {
+                const uint32_t c = (uint32_t)(L.loff[l] + y * G + x);
+                const Sum o = own_of(scan, cnt, off, mem, c);
+                own[c] = o;
+                s = o;
+                if (l > 0) {
+                    const int cs = side * 2;
+                    for (int dy = 0; dy < 2; ++dy)
+                        for (int dx = 0; dx < 2; ++dx) merge(s, sm[cur][(2 * (t / side) + dy) * cs + 2 * (t % side) + dx]);
+                }
+                sub[c] = s;
             }
+            sm[cur ^ 1][t] = s;
+        }
+        __syncthreads();
+        cur ^= 1;
     }
-    sub[L.loff[level] + i] = s;
+    if (L.levels <= 5) return;
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (t == 0) last = atomicAdd(ticket, 1u) == (unsigned)(nb * nb - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int l = 5; l < L.levels; ++l) {
+        const int G = L.lw[l], cw = L.lw[l - 1];
+        for (int i = t; i < G * G; i += 256) {
+            const int x = i % G, y = i / G;
+            const uint32_t c = (uint32_t)(L.loff[l] + i);
+            Sum s = own_of(scan, cnt, off, mem, c);
+            own[c] = s;
+            for (int dy = 0; dy < 2; ++dy)
+                for (int dx = 0; dx < 2; ++dx) {
+                    const int cx = 2 * x + dx, cy = 2 * y + dy;
+                    if (cx < cw && cy < cw) merge(s, sub[L.loff[l - 1] + cy * cw + cx]);
+                }
+            sub[c] = s;
+        }
+        __threadfence();
+        __syncthreads();
+    }
+    if (t == 0) *ticket = 0;  // ready for the next build
 }
 
 __device__ __forceinline__ double sum_lb(const Sum& s, double px, double py) {
@@ -593,7 +643,7 @@ __global__ void __launch_bounds__(kHardThreads) hard_points_kernel(const ScanRec
 }
 
 struct KnnBufs {
-    DevBuf cnt, off, key, mem, own, sub, cub_tmp, hard;
+    DevBuf cnt, off, key, mem, own, sub, cub_tmp, hard, ticket;
     uint64_t version = ~0ull;
     Lq lq{};
 };
@@ -636,6 +686,10 @@ int knn_build(igs_ctx* ctx) {
         !grow(b.mem, (size_t)n * 4) || !grow(b.own, (size_t)cells * sizeof(Sum)) ||
         !grow(b.sub, (size_t)cells * sizeof(Sum)))
         return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
+    if (!b.ticket.p) {
+        if (!grow(b.ticket, 16)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
+        IGS_CUDA(ctx, cudaMemsetAsync(b.ticket.p, 0, 16, ctx->stream));
+    }
     uint32_t* cnt = (uint32_t*)b.cnt.p;
     uint32_t* cur = cnt + cells;
     uint32_t* off = (uint32_t*)b.off.p;
@@ -650,14 +704,10 @@ int knn_build(igs_ctx* ctx) {
     ctx->launches += 2;
     lq_fill<<<(n + 255) / 256, 256, 0, ctx->stream>>>(n, (const uint32_t*)b.key.p, off, cur, (uint32_t*)b.mem.p);
     IGS_LAUNCHED(ctx);
-    lq_own<<<(cells + 127) / 128, 128, 0, ctx->stream>>>(ctx->scan, cells, cnt, off, (const uint32_t*)b.mem.p,
-                                                         (Sum*)b.own.p);
+    const int nb = (G0 + kBlk - 1) / kBlk;
+    lq_tree_kernel<<<nb * nb, 256, 0, ctx->stream>>>(ctx->scan, L, cnt, off, (const uint32_t*)b.mem.p,
+                                                     (Sum*)b.own.p, (Sum*)b.sub.p, (unsigned int*)b.ticket.p);
     IGS_LAUNCHED(ctx);
-    for (int lv = 0; lv < L.levels; ++lv) {
-        const int m = L.lw[lv] * L.lw[lv];
-        lq_subtree<<<(m + 127) / 128, 128, 0, ctx->stream>>>(L, lv, (const Sum*)b.own.p, (Sum*)b.sub.p);
-        IGS_LAUNCHED(ctx);
-    }
     igs_prof_end(ctx, IGS_PROF_CULL, 0.0);
     b.lq = L;
     b.version = ctx->params_version;
@@ -699,7 +749,8 @@ int run_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int kk,
 void igs_knn_free(igs_ctx* ctx) {
     if (!ctx->knn) return;
     KnnBufs* b = static_cast<KnnBufs*>(ctx->knn);
-    for (DevBuf* d : {&b->cnt, &b->off, &b->key, &b->mem, &b->own, &b->sub, &b->cub_tmp, &b->hard}) cudaFree(d->p);
+    for (DevBuf* d : {&b->cnt, &b->off, &b->key, &b->mem, &b->own, &b->sub, &b->cub_tmp, &b->hard, &b->ticket})
+        cudaFree(d->p);
     delete b;
     ctx->knn = nullptr;
 }
