@@ -613,7 +613,8 @@ int igs_train_iteration(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, i
     const uint32_t ns_total = ns * (uint32_t)ctx->nranks;
     if ((e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss, 1.0 / (double)ns_total))) return e;
     if ((e = allreduce_grads(ctx, dloss))) return e;
-    if ((e = igs_grad_check(ctx))) return e;
+    // the deterministic reduction already flags non-finite gradients (single rank)
+    if ((ctx->nranks > 1 || !ctx->grads_checked) && (e = igs_grad_check(ctx))) return e;
     if ((e = igs_adam_launch(ctx, lr4, t))) return e;
     return read_status(ctx, dloss, loss, 1);
 }
@@ -649,7 +650,7 @@ int igs_train_iterations(igs_ctx* ctx, uint32_t steps, int k, const double* lr4,
         const uint32_t* dsidx = (const uint32_t*)ctx->samples.p + (size_t)slot * ns;
         if ((e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss + s, 1.0 / (double)ns_total))) return e;
         if ((e = allreduce_grads(ctx, dloss + s))) return e;
-        if ((e = igs_grad_check(ctx))) return e;
+        if ((ctx->nranks > 1 || !ctx->grads_checked) && (e = igs_grad_check(ctx))) return e;
         if ((e = igs_adam_launch(ctx, lr4, t0 + s))) return e;
     }
     igs_timer_autostop(ctx);  // device time of the loop excludes the status readback

@@ -170,6 +170,7 @@ struct igs_ctx {
     igs_dev::ScanRec* scan = nullptr;
     igs_dev::ShadeRec* shade = nullptr;
     bool grads_valid = false;
+    bool grads_checked = false;  // the reduction already flagged non-finite gradients
 
     // images
     DevBuf image;
@@ -178,7 +179,7 @@ struct igs_ctx {
     int tgt_w = 0, tgt_h = 0;
 
     // per-call scratch (grow-only), indexed by purpose
-    DevBuf scratch[24];
+    DevBuf scratch[32];
     // pinned host staging
     void* pinned = nullptr;
     size_t pinned_bytes = 0;
@@ -248,7 +249,7 @@ void igs_cull_free(igs_ctx* ctx);
 void igs_knn_free(igs_ctx* ctx);
 int igs_topk_knn(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq);
 int igs_knn_forward_backward(igs_ctx* ctx, int mode, const uint32_t* sidx, const double* samples5, uint32_t npts,
-                             int kk, double inv_n, double* losses, double* contrib, uint32_t* keys,
+                             int kk, double inv_n, double* losses, double* contrib, uint32_t* keys, uint32_t* gcnt,
                              double* grads_atomic);
 int igs_topk_samples_culled(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq);
 int igs_topk_pixels_culled(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq, int W,

@@ -323,6 +323,7 @@ struct Epi {
     double* losses;              // mode 0: per point
     double* contrib;             // modes 0/1: [pt][kk][8] (deterministic reduction) or null
     uint32_t* keys;              // modes 0/1: [pt][kk] Gaussian index, n for empty slots
+    uint32_t* gcnt;              // modes 0/1 (deterministic): contributions per Gaussian
     double* grads_atomic;        // modes 0/1: fast mode (fp64 atomics) or null
     long long* status;           // status[2]: first non-finite loss
     double* oq;                  // mode 2
@@ -441,6 +442,7 @@ __device__ __forceinline__ void warp_epilogue(const Epi& E, const ScanRec* __res
         o[2] = make_double2(d[4], d[5]);
         o[3] = make_double2(d[6], d[7]);
         E.keys[slot] = myi;
+        atomicAdd(E.gcnt + myi, 1u);
     }
 }
 
@@ -574,76 +576,112 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
     warp_epilogue(E, scan, pt, kk, lane, t.q, t.i, px, py);
 }
 
-// One CTA per hard point: 128 threads scan all N (coalesced 48-B records),
-// each keeping a private top-K; warp 0 folds the 128 lists into 32 lane
-// lists, then kk rounds of a warp-wide (q, idx) minimum emit the result.
-// Exact: the kept set is the kk smallest (q, idx) of the union.
+// Hard points (frontier overflow) are resolved by an exact split scan:
+// hard_scan_kernel -- a persistent grid walks (point, split) items; each CTA
+// scans a contiguous 1/kHardSplit of the set with per-thread top-K lists and
+// folds them (warp 0) into one partial list; hard_merge_kernel -- one warp
+// per point offers the kHardSplit partial lists to a warp top-K (any order:
+// (q, idx) is a strict total order) and runs the epilogue.
 constexpr int kHardThreads = 128;
+constexpr int kHardSplit = 16;
 
 template <int KCAP>
-__global__ void __launch_bounds__(kHardThreads) hard_points_kernel(const ScanRec* __restrict__ scan, uint32_t n,
-                                                                   const double* __restrict__ uv, int W, int H, int kk,
-                                                                   const uint32_t* __restrict__ hard_count,
-                                                                   const uint32_t* __restrict__ hard_list, Epi E,
-                                                                   unsigned long long* __restrict__ pairs) {
+__global__ void __launch_bounds__(kHardThreads) hard_scan_kernel(const ScanRec* __restrict__ scan, uint32_t n,
+                                                                 const double* __restrict__ uv, int W, int H, int kk,
+                                                                 const uint32_t* __restrict__ hard_count,
+                                                                 const uint32_t* __restrict__ hard_list, Epi E,
+                                                                 double* __restrict__ part_q,
+                                                                 uint32_t* __restrict__ part_i) {
     __shared__ double sq[kHardThreads * KCAP];
     __shared__ uint32_t si[kHardThreads * KCAP];
     const uint32_t cnt = min(*hard_count, kHardCap);
-    if (blockIdx.x >= cnt) return;
-    const uint32_t pt = hard_list[blockIdx.x];
-    double px, py;
-    point_of(uv, E, W, H, pt, px, py);
-    TopK<KCAP> t;
-    t.init(kk);
-    for (uint32_t g = threadIdx.x; g < n; g += kHardThreads) {
-        const double q = maha(scan[g], px, py);
-        if (q <= t.tq()) t.offer(q, g);
-    }
-    store_topk(t, sq + threadIdx.x * KCAP, si + threadIdx.x * KCAP);
-    __syncthreads();
-    if (threadIdx.x >= 32) return;
-    const int lane = threadIdx.x;
-    TopK<KCAP> m;
-    m.init(kk);
-    for (int th = lane; th < kHardThreads; th += 32)
-        for (int j = 0; j < kk; ++j) {
-            const uint32_t ci = si[th * KCAP + j];
-            if (ci == kNoIdx) break;
-            m.offer(sq[th * KCAP + j], ci);
+    const uint32_t per = (n + kHardSplit - 1) / kHardSplit;
+    for (uint32_t item = blockIdx.x; item < cnt * kHardSplit; item += gridDim.x) {
+        const uint32_t slot = item / kHardSplit, split = item % kHardSplit;
+        const uint32_t pt = hard_list[slot];
+        double px, py;
+        point_of(uv, E, W, H, pt, px, py);
+        const uint32_t g0 = split * per, g1 = min(n, g0 + per);
+        TopK<KCAP> t;
+        t.init(kk);
+        for (uint32_t g = g0 + threadIdx.x; g < g1; g += kHardThreads) {
+            const double q = maha(scan[g], px, py);
+            if (q <= t.tq()) t.offer(q, g);
         }
-    __syncwarp();
-    store_topk(m, sq + lane * KCAP, si + lane * KCAP);
-    __syncwarp();
-    int head = 0;
-    double myq = __longlong_as_double(0x7ff0000000000000LL);
-    uint32_t myi = kNoIdx;
-    for (int r = 0; r < kk; ++r) {
-        double v = head < kk ? sq[lane * KCAP + head] : __longlong_as_double(0x7ff0000000000000LL);
-        uint32_t vi = head < kk ? si[lane * KCAP + head] : kNoIdx;
-        int who = lane;
+        __syncthreads();
+        store_topk(t, sq + threadIdx.x * KCAP, si + threadIdx.x * KCAP);
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            TopK<KCAP> m;
+            m.init(kk);
+            for (int th = lane; th < kHardThreads; th += 32)
+                for (int j = 0; j < kk; ++j) {
+                    const uint32_t ci = si[th * KCAP + j];
+                    if (ci == kNoIdx) break;
+                    m.offer(sq[th * KCAP + j], ci);
+                }
+            __syncwarp();
+            store_topk(m, sq + lane * KCAP, si + lane * KCAP);
+            __syncwarp();
+            int head = 0;
+            for (int r = 0; r < kk; ++r) {
+                double v = head < kk ? sq[lane * KCAP + head] : __longlong_as_double(0x7ff0000000000000LL);
+                uint32_t vi = head < kk ? si[lane * KCAP + head] : kNoIdx;
+                int who = lane;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-            const uint32_t ovi = __shfl_xor_sync(0xffffffffu, vi, o);
-            const int ow = __shfl_xor_sync(0xffffffffu, who, o);
-            if (ov < v || (ov == v && ovi < vi) || (ov == v && ovi == vi && ow < who)) {
-                v = ov;
-                vi = ovi;
-                who = ow;
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+                    const uint32_t ovi = __shfl_xor_sync(0xffffffffu, vi, o);
+                    const int ow = __shfl_xor_sync(0xffffffffu, who, o);
+                    if (ov < v || (ov == v && ovi < vi) || (ov == v && ovi == vi && ow < who)) {
+                        v = ov;
+                        vi = ovi;
+                        who = ow;
+                    }
+                }
+                if (lane == who) ++head;
+                if (lane == 0) {
+                    part_q[(size_t)item * kk + r] = v;
+                    part_i[(size_t)item * kk + r] = vi;
+                }
             }
         }
-        if (lane == who) ++head;
-        if (lane == r) {
-            myq = v;
-            myi = vi;
+    }
+}
+
+__global__ void __launch_bounds__(128) hard_merge_kernel(const ScanRec* __restrict__ scan, uint32_t n,
+                                                         const double* __restrict__ uv, int W, int H, int kk,
+                                                         const uint32_t* __restrict__ hard_count,
+                                                         const uint32_t* __restrict__ hard_list, Epi E,
+                                                         const double* __restrict__ part_q,
+                                                         const uint32_t* __restrict__ part_i,
+                                                         unsigned long long* __restrict__ pairs) {
+    const uint32_t slot = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (slot >= min(*hard_count, kHardCap)) return;
+    const uint32_t pt = hard_list[slot];
+    double px, py;
+    point_of(uv, E, W, H, pt, px, py);
+    WarpTopK t;
+    t.init(kk, lane);
+    for (int sp = 0; sp < kHardSplit; ++sp) {
+        const size_t o = ((size_t)slot * kHardSplit + sp) * kk;
+        const double q = lane < kk ? part_q[o + lane] : 0.0;
+        const uint32_t i = lane < kk ? part_i[o + lane] : kNoIdx;
+        for (int j = 0; j < kk; ++j) {
+            const uint32_t ij = __shfl_sync(0xffffffffu, i, j);
+            const double qj = __shfl_sync(0xffffffffu, q, j);
+            if (ij == kNoIdx) break;
+            t.offer(qj, ij);
         }
     }
     if (pairs && lane == 0) atomicAdd(pairs, (unsigned long long)n);
-    warp_epilogue(E, scan, pt, kk, lane, myq, myi, px, py);
+    warp_epilogue(E, scan, pt, kk, lane, t.q, t.i, px, py);
 }
 
 struct KnnBufs {
-    DevBuf cnt, off, key, mem, own, sub, cub_tmp, hard, ticket;
+    DevBuf cnt, off, key, mem, own, sub, cub_tmp, hard, ticket, part;
     uint64_t version = ~0ull;
     Lq lq{};
 };
@@ -728,8 +766,16 @@ int launch_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int 
         (const uint32_t*)b.mem.p, uv, W, H, npts, kk, E, igs_prof_counter(ctx, IGS_PROF_SCAN), hard_count,
         hard_list, igs_prof_counter(ctx, IGS_PROF_KNN_HARD));
     IGS_LAUNCHED(ctx);
-    hard_points_kernel<KCAP><<<kHardCap, kHardThreads, 0, ctx->stream>>>(
-        ctx->scan, ctx->n, uv, W, H, kk, hard_count, hard_list, E, igs_prof_counter(ctx, IGS_PROF_SCAN));
+    const size_t pitems = (size_t)kHardCap * kHardSplit * kk;
+    if (!grow(b.part, pitems * 12)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
+    double* part_q = (double*)b.part.p;
+    uint32_t* part_i = (uint32_t*)(part_q + pitems);
+    hard_scan_kernel<KCAP><<<2 * ctx->sm_count, kHardThreads, 0, ctx->stream>>>(
+        ctx->scan, ctx->n, uv, W, H, kk, hard_count, hard_list, E, part_q, part_i);
+    IGS_LAUNCHED(ctx);
+    hard_merge_kernel<<<kHardCap * 32 / 128, 128, 0, ctx->stream>>>(ctx->scan, ctx->n, uv, W, H, kk, hard_count,
+                                                                    hard_list, E, part_q, part_i,
+                                                                    igs_prof_counter(ctx, IGS_PROF_SCAN));
     IGS_LAUNCHED(ctx);
     igs_prof_end(ctx, IGS_PROF_SCAN, 0.0);
     return IGS_OK;
@@ -749,7 +795,8 @@ int run_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int kk,
 void igs_knn_free(igs_ctx* ctx) {
     if (!ctx->knn) return;
     KnnBufs* b = static_cast<KnnBufs*>(ctx->knn);
-    for (DevBuf* d : {&b->cnt, &b->off, &b->key, &b->mem, &b->own, &b->sub, &b->cub_tmp, &b->hard, &b->ticket})
+    for (DevBuf* d : {&b->cnt, &b->off, &b->key, &b->mem, &b->own, &b->sub, &b->cub_tmp, &b->hard, &b->ticket,
+                      &b->part})
         cudaFree(d->p);
     delete b;
     ctx->knn = nullptr;
@@ -773,9 +820,10 @@ int igs_topk_knn(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t*
 // contribution records + sort keys (contrib != null) or fp64 atomics into
 // grads_atomic.
 int igs_knn_forward_backward(igs_ctx* ctx, int mode, const uint32_t* sidx, const double* samples5, uint32_t npts,
-                             int kk, double inv_n, double* losses, double* contrib, uint32_t* keys,
+                             int kk, double inv_n, double* losses, double* contrib, uint32_t* keys, uint32_t* gcnt,
                              double* grads_atomic) {
     Epi E{};
+    E.gcnt = gcnt;
     E.mode = mode;
     E.sidx = sidx;
     E.target = (const float*)ctx->target.p;

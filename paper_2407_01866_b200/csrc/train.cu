@@ -167,6 +167,143 @@ __global__ void segment_reduce_kernel(const uint32_t* __restrict__ skeys, const 
     o[3] = make_double2(acc[6], acc[7]);
 }
 
+// --- counting-sort reduction (deterministic, reference summation order) ----
+// keys[slot] = Gaussian of contribution slot (slot = sample * kk + entry, so
+// slot order is sample order).  gcnt/goff: per-Gaussian count / offset.
+__global__ void scatter_slots_kernel(const uint32_t* __restrict__ keys, uint32_t items, uint32_t n,
+                                     const uint32_t* __restrict__ goff, uint32_t* __restrict__ gcur,
+                                     uint32_t* __restrict__ perm) {
+    const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
+    if (slot >= items) return;
+    const uint32_t g = keys[slot];
+    if (g >= n) return;
+    perm[goff[g] + atomicAdd(gcur + g, 1u)] = slot;
+}
+
+__device__ __forceinline__ void sum_sorted(const double* __restrict__ contrib, const uint32_t* slots, uint32_t m,
+                                           double* acc) {
+    for (uint32_t e = 0; e < m; ++e) {
+        const double2* c = reinterpret_cast<const double2*>(contrib + (size_t)slots[e] * 8);
+        const double2 a = c[0], b = c[1], cc = c[2], d = c[3];
+        acc[0] = __dadd_rn(acc[0], a.x);
+        acc[1] = __dadd_rn(acc[1], a.y);
+        acc[2] = __dadd_rn(acc[2], b.x);
+        acc[3] = __dadd_rn(acc[3], b.y);
+        acc[4] = __dadd_rn(acc[4], cc.x);
+        acc[5] = __dadd_rn(acc[5], cc.y);
+        acc[6] = __dadd_rn(acc[6], d.x);
+        acc[7] = __dadd_rn(acc[7], d.y);
+    }
+}
+
+__device__ __forceinline__ void store_grad(double* __restrict__ grads, uint32_t g, const double* acc,
+                                           long long* __restrict__ status) {
+    double2* o = reinterpret_cast<double2*>(grads + (size_t)g * 8);
+    o[0] = make_double2(acc[0], acc[1]);
+    o[1] = make_double2(acc[2], acc[3]);
+    o[2] = make_double2(acc[4], acc[5]);
+    o[3] = make_double2(acc[6], acc[7]);
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+        if (!isfinite(acc[p])) {  // adam.cpp:29-31: first offending (i, p)
+            atomicMin(status, (long long)g * 8 + p);
+            break;
+        }
+}
+
+constexpr uint32_t kShortSeg = 32;
+
+// Thread per Gaussian: sort its (short) slot list, sum from 0.0 in slot
+// (= sample) order -- the reference's operation sequence.  Long segments are
+// queued for long_segment_kernel.
+__global__ void segment_sum_kernel(const uint32_t* __restrict__ gcnt, const uint32_t* __restrict__ goff,
+                                   const uint32_t* __restrict__ perm, const double* __restrict__ contrib, uint32_t n,
+                                   double* __restrict__ grads, uint32_t* __restrict__ long_count,
+                                   uint32_t* __restrict__ long_list, long long* __restrict__ status) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    const uint32_t m = gcnt[g];
+    if (m > kShortSeg) {
+        long_list[atomicAdd(long_count, 1u)] = g;
+        return;
+    }
+    uint32_t sl[kShortSeg];
+    const uint32_t o = goff[g];
+    for (uint32_t e = 0; e < m; ++e) {
+        const uint32_t v = perm[o + e];
+        uint32_t pos = e;
+        while (pos > 0 && sl[pos - 1] > v) {
+            sl[pos] = sl[pos - 1];
+            --pos;
+        }
+        sl[pos] = v;
+    }
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    sum_sorted(contrib, sl, m, acc);
+    store_grad(grads, g, acc, status);
+}
+
+// One CTA per long segment (persistent over the queue): rank sort in shared
+// memory (slot ids are unique: rank = number of smaller ids), then thread 0
+// sums in order.  Segments beyond the shared capacity sort in place in perm.
+constexpr uint32_t kLongCap = 4096;
+
+__global__ void __launch_bounds__(256) long_segment_kernel(const uint32_t* __restrict__ gcnt,
+                                                           const uint32_t* __restrict__ goff,
+                                                           uint32_t* __restrict__ perm,
+                                                           const double* __restrict__ contrib,
+                                                           double* __restrict__ grads,
+                                                           const uint32_t* __restrict__ long_count,
+                                                           const uint32_t* __restrict__ long_list,
+                                                           long long* __restrict__ status) {
+    __shared__ uint32_t in[kLongCap], outs[kLongCap];
+    const uint32_t total = *long_count;
+    for (uint32_t it = blockIdx.x; it < total; it += gridDim.x) {
+        const uint32_t g = long_list[it];
+        const uint32_t m = gcnt[g], o = goff[g];
+        __syncthreads();
+        if (m <= kLongCap) {
+            for (uint32_t e = threadIdx.x; e < m; e += blockDim.x) in[e] = perm[o + e];
+            __syncthreads();
+            for (uint32_t e = threadIdx.x; e < m; e += blockDim.x) {
+                const uint32_t v = in[e];
+                uint32_t r = 0;
+                for (uint32_t f = 0; f < m; ++f) r += in[f] < v;
+                outs[r] = v;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                sum_sorted(contrib, outs, m, acc);
+                store_grad(grads, g, acc, status);
+            }
+        } else if (threadIdx.x == 0) {
+            // huge segment (degenerate sets): in-place insertion sort in global memory
+            uint32_t* s = perm + o;
+            for (uint32_t e = 1; e < m; ++e) {
+                const uint32_t v = s[e];
+                uint32_t pos = e;
+                while (pos > 0 && s[pos - 1] > v) {
+                    s[pos] = s[pos - 1];
+                    --pos;
+                }
+                s[pos] = v;
+            }
+            double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            sum_sorted(contrib, s, m, acc);
+            store_grad(grads, g, acc, status);
+        }
+    }
+}
+
+__global__ void count_keys_kernel(const uint32_t* __restrict__ keys, uint32_t items, uint32_t n,
+                                  uint32_t* __restrict__ gcnt) {
+    const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
+    if (slot >= items) return;
+    const uint32_t g = keys[slot];
+    if (g < n) atomicAdd(gcnt + g, 1u);
+}
+
 __global__ void iota_kernel(uint32_t* v, uint32_t n) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) v[i] = i;
@@ -330,7 +467,8 @@ __global__ void blend_points_kernel(const double* __restrict__ lq, const uint32_
 
 // Scratch slot map (igs_scratch): 0 uv, 1 list q, 2 list idx, 3 contrib,
 // 4 keys, 5 keys sorted, 6 vals, 7 vals sorted, 8 cub temp, 9 losses,
-// 10/11 point partials, 12/13 generic lists, 14 loss out, 15 upstream samples.
+// 10/11 point partials, 12/13 generic lists, 14 loss out, 15 upstream samples,
+// 24 long-segment queue.
 
 int igs_status_reset(igs_ctx* ctx) {
     reset_status_kernel<<<1, 32, 0, ctx->stream>>>(ctx->status);
@@ -348,14 +486,19 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
     const size_t items = (size_t)ns * kk;
     double* losses = (double*)igs_scratch(ctx, 9, (size_t)std::max<uint32_t>(ns, 1) * sizeof(double));
     double* contrib = nullptr;
-    uint32_t *keys = nullptr, *skeys = nullptr, *vals = nullptr, *svals = nullptr;
+    uint32_t *keys = nullptr, *gcnt = nullptr, *goff = nullptr, *perm = nullptr, *long_ctl = nullptr;
+    bool gcnt_filled = false;
     if (ctx->opt_deterministic) {
         contrib = (double*)igs_scratch(ctx, 3, items * 8 * sizeof(double));
         keys = (uint32_t*)igs_scratch(ctx, 4, items * sizeof(uint32_t));
-        skeys = (uint32_t*)igs_scratch(ctx, 5, items * sizeof(uint32_t));
-        vals = (uint32_t*)igs_scratch(ctx, 6, items * sizeof(uint32_t));
-        svals = (uint32_t*)igs_scratch(ctx, 7, items * sizeof(uint32_t));
-        if (!contrib || !keys || !skeys || !vals || !svals) return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
+        gcnt = (uint32_t*)igs_scratch(ctx, 5, (size_t)n * 2 * sizeof(uint32_t));  // counts | cursors
+        goff = (uint32_t*)igs_scratch(ctx, 6, (size_t)n * sizeof(uint32_t));
+        perm = (uint32_t*)igs_scratch(ctx, 7, items * sizeof(uint32_t));
+        long_ctl = (uint32_t*)igs_scratch(ctx, 24, ((size_t)n + 1) * sizeof(uint32_t));
+        if (!contrib || !keys || !gcnt || !goff || !perm || !long_ctl)
+            return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
+        IGS_CUDA(ctx, cudaMemsetAsync(gcnt, 0, (size_t)n * 2 * sizeof(uint32_t), ctx->stream));
+        IGS_CUDA(ctx, cudaMemsetAsync(long_ctl, 0, sizeof(uint32_t), ctx->stream));
     } else {
         IGS_CUDA(ctx, cudaMemsetAsync(ctx->grads, 0, (size_t)n * 8 * sizeof(double), ctx->stream));
     }
@@ -363,9 +506,10 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
     int e;
     if (ctx->opt_cull && kk <= 32) {
         // fused: exact top-K search + blend / loss / gradient epilogue per warp
-        e = igs_knn_forward_backward(ctx, mode, dev_sidx, dev_samples5, ns, kk, inv_n, losses, contrib, keys,
+        e = igs_knn_forward_backward(ctx, mode, dev_sidx, dev_samples5, ns, kk, inv_n, losses, contrib, keys, gcnt,
                                      ctx->opt_deterministic ? nullptr : ctx->grads);
         if (e) return e;
+        gcnt_filled = true;
     } else {
         double* uv = (double*)igs_scratch(ctx, 0, (size_t)ns * 2 * sizeof(double));
         double* lq = (double*)igs_scratch(ctx, 1, (size_t)ns * kk * sizeof(double));
@@ -390,22 +534,31 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
     }
     if (ctx->opt_deterministic) {
         igs_prof_begin(ctx, IGS_PROF_REDUCE);
-        iota_kernel<<<(unsigned)((items + 255) / 256), 256, 0, ctx->stream>>>(vals, (uint32_t)items);
+        if (!gcnt_filled) {
+            // fallback path: per-Gaussian counts from the keys
+            count_keys_kernel<<<(unsigned)((items + 255) / 256), 256, 0, ctx->stream>>>(keys, (uint32_t)items, n,
+                                                                                        gcnt);
+            IGS_LAUNCHED(ctx);
+        }
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, gcnt, goff, (int)n, ctx->stream);
+        void* temp = igs_scratch(ctx, 8, tb);
+        if (!temp) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (scan)");
+        IGS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(temp, tb, gcnt, goff, (int)n, ctx->stream));
+        ctx->launches += 2;
+        scatter_slots_kernel<<<(unsigned)((items + 255) / 256), 256, 0, ctx->stream>>>(keys, (uint32_t)items, n, goff,
+                                                                                       gcnt + n, perm);
         IGS_LAUNCHED(ctx);
-        int end_bit = 1;
-        while (end_bit < 32 && ((uint64_t)1 << end_bit) <= (uint64_t)n) ++end_bit;
-        size_t temp_bytes = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys, skeys, vals, svals, (int)items, 0, end_bit,
-                                        ctx->stream);
-        void* temp = igs_scratch(ctx, 8, temp_bytes);
-        if (!temp) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (sort)");
-        IGS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, skeys, vals, svals, (int)items, 0,
-                                                      end_bit, ctx->stream));
-        ctx->launches += (uint64_t)((end_bit + 7) / 8) + 2;  // histogram, exclusive sum, one onesweep per pass
-        segment_reduce_kernel<<<(n + 255) / 256, 256, 0, ctx->stream>>>(skeys, svals, (uint32_t)items, contrib, n,
-                                                                        ctx->grads);
+        segment_sum_kernel<<<(n + 255) / 256, 256, 0, ctx->stream>>>(gcnt, goff, perm, contrib, n, ctx->grads,
+                                                                     long_ctl, long_ctl + 1, ctx->status);
         IGS_LAUNCHED(ctx);
+        long_segment_kernel<<<ctx->sm_count, 256, 0, ctx->stream>>>(gcnt, goff, perm, contrib, ctx->grads, long_ctl,
+                                                                    long_ctl + 1, ctx->status);
+        IGS_LAUNCHED(ctx);
+        ctx->grads_checked = true;
         igs_prof_end(ctx, IGS_PROF_REDUCE, (double)items);
+    } else {
+        ctx->grads_checked = false;
     }
     if (mode == 0 && dev_loss) {
         loss_reduce_kernel<<<1, 1024, 0, ctx->stream>>>(losses, ns, inv_n, dev_loss);
