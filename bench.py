@@ -272,6 +272,8 @@ def run_ours(args, rank, world, local_rank, dist):
                 "call": "igs_train_iteration (host sample indices in, host loss out)"},
         "roofline": roof, "roofline_adam": adam_roof,
         "profile_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
+        "knn_hard_points_per_step": prof["knn_hard"][2] / args.steps,
+        "pairs_per_sample": prof["scan"][2] / args.steps / NS,
         "dominant_family": dom,
         "cull": cull_stats,
         "clocks": clk, "gpu_launches": int(launches),

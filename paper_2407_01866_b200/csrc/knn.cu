@@ -56,6 +56,7 @@ struct Lq {
     int G0, levels;
     int lw[kMaxLv];    // cells per side
     int loff[kMaxLv];  // first cell id of the level
+    const uint32_t* lcount;  // Gaussians stored per level (device)
 };
 
 __device__ __forceinline__ int cell_of(double v, int G) {
@@ -82,12 +83,16 @@ __device__ __forceinline__ uint32_t key_of(const Lq& L, const ScanRec& r) {
 }
 
 __global__ void lq_count(const ScanRec* __restrict__ scan, uint32_t n, Lq L, uint32_t* __restrict__ cnt,
-                         uint32_t* __restrict__ key) {
+                         uint32_t* __restrict__ key, uint32_t* __restrict__ lcount) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const uint32_t k = key_of(L, scan[i]);
+    const ScanRec r = scan[i];
+    const int l = level_of(L, fmin(r.inv_a, r.inv_b));
+    const int G = L.lw[l];
+    const uint32_t k = (uint32_t)(L.loff[l] + cell_of(r.mu_y, G) * G + cell_of(r.mu_x, G));
     key[i] = k;
     atomicAdd(cnt + k, 1u);
+    atomicAdd(lcount + l, 1u);
 }
 
 __global__ void lq_fill(uint32_t n, const uint32_t* __restrict__ key, const uint32_t* __restrict__ off,
@@ -466,13 +471,20 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
     t.init(kk, lane);
     unsigned long long evaluated = 0;
 
-    // (1) seeds: own members of the 3x3 window at every level
-    const int nseed = L.levels * 9;
+    // (1) seeds: own members of the 3x3 window at every populated level
+    unsigned lvmask = 0;
+    if (lane < L.levels && L.lcount[lane] > 0) lvmask = 1u;
+    lvmask = __ballot_sync(0xffffffffu, lvmask);
+    const int npop = __popc(lvmask);
+    const int nseed = npop * 9;
     for (int base = 0; base < nseed; base += 32) {
         const int it = base + lane;
         uint32_t o = 0, m = 0;
         if (it < nseed) {
-            const int l = it / 9, d = it % 9, G = L.lw[l];
+            // it-th populated level
+            unsigned mm = lvmask;
+            for (int skip = it / 9; skip > 0; --skip) mm &= mm - 1;
+            const int l = __ffs(mm) - 1, d = it % 9, G = L.lw[l];
             const int x = cell_of(px, G) + d % 3 - 1, y = cell_of(py, G) + d / 3 - 1;
             if (x >= 0 && x < G && y >= 0 && y < G) {
                 const uint32_t c = (uint32_t)(L.loff[l] + y * G + x);
@@ -483,13 +495,17 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
         eval_members(t, o, m, lane, scan, mem, px, py, evaluated);
     }
 
+    // A frontier node at level l holds only Gaussians of sigma <= cell_l / 2,
+    // so its bound is >= 4 (d / cell_l)^2: at most (sqrt(tq) + 3)^2 nodes per
+    // level can survive.  If that may exceed the queue, go straight to the
+    // exact split scan instead of walking a huge frontier first.
+    bool overflow = !(t.tq() < 387.0);
     // (2) descent: evaluate own members of frontier nodes, expand children
     uint32_t* cur = queue[warp][0];
     uint32_t* nxt = queue[warp][1];
-    int ncur = 1;
+    int ncur = overflow ? 0 : 1;
     if (lane == 0) cur[0] = 0;  // root cell of the top level
     __syncwarp();
-    bool overflow = false;
     for (int l = L.levels - 1; l >= 0 && ncur > 0; --l) {
         const int w = L.lw[l];
         // own members of the frontier (outside the seed window)
@@ -681,7 +697,7 @@ __global__ void __launch_bounds__(128) hard_merge_kernel(const ScanRec* __restri
 }
 
 struct KnnBufs {
-    DevBuf cnt, off, key, mem, own, sub, cub_tmp, hard, ticket, part;
+    DevBuf cnt, off, key, mem, own, sub, cub_tmp, hard, ticket, part, lcount;
     uint64_t version = ~0ull;
     Lq lq{};
 };
@@ -728,12 +744,16 @@ int knn_build(igs_ctx* ctx) {
         if (!grow(b.ticket, 16)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
         IGS_CUDA(ctx, cudaMemsetAsync(b.ticket.p, 0, 16, ctx->stream));
     }
+    if (!grow(b.lcount, kMaxLv * 4)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
+    L.lcount = (const uint32_t*)b.lcount.p;
+    IGS_CUDA(ctx, cudaMemsetAsync(b.lcount.p, 0, kMaxLv * 4, ctx->stream));
     uint32_t* cnt = (uint32_t*)b.cnt.p;
     uint32_t* cur = cnt + cells;
     uint32_t* off = (uint32_t*)b.off.p;
     igs_prof_begin(ctx, IGS_PROF_CULL);
     IGS_CUDA(ctx, cudaMemsetAsync(cnt, 0, (size_t)cells * 8, ctx->stream));
-    lq_count<<<(n + 255) / 256, 256, 0, ctx->stream>>>(ctx->scan, n, L, cnt, (uint32_t*)b.key.p);
+    lq_count<<<(n + 255) / 256, 256, 0, ctx->stream>>>(ctx->scan, n, L, cnt, (uint32_t*)b.key.p,
+                                                       (uint32_t*)b.lcount.p);
     IGS_LAUNCHED(ctx);
     size_t tb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, (int)cells, ctx->stream);
@@ -796,7 +816,7 @@ void igs_knn_free(igs_ctx* ctx) {
     if (!ctx->knn) return;
     KnnBufs* b = static_cast<KnnBufs*>(ctx->knn);
     for (DevBuf* d : {&b->cnt, &b->off, &b->key, &b->mem, &b->own, &b->sub, &b->cub_tmp, &b->hard, &b->ticket,
-                      &b->part})
+                      &b->part, &b->lcount})
         cudaFree(d->p);
     delete b;
     ctx->knn = nullptr;
