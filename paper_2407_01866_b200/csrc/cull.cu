@@ -298,13 +298,14 @@ __global__ void __launch_bounds__(256) raster_culled_kernel(const ScanRec* __res
             sidx[tid] = gi;
         }
         __syncthreads();
-        if (live) {
+        // every thread runs the loop (warp votes need the full warp); only live
+        // threads write results
 #pragma unroll 1
             for (uint32_t j = 0; j < cnt; ++j) {
                 const double q = maha(sm[j], x, y);
-                if (q <= t.tq()) t.offer(q, sidx[j]);
+                if (__any_sync(0xffffffffu, q <= t.tq()))
+                    if (q <= t.tq()) t.offer(q, sidx[j]);
             }
-        }
     }
     if (pairs && tid == 0) atomicAdd(pairs, (unsigned long long)total * (min(gr.W - tx * kTilePx, kTilePx) *
                                                                          min(row1 - ty * kTilePx, kTilePx)));

@@ -85,14 +85,18 @@ __device__ __forceinline__ uint32_t key_of(const Lq& L, const ScanRec& r) {
 __global__ void lq_count(const ScanRec* __restrict__ scan, uint32_t n, Lq L, uint32_t* __restrict__ cnt,
                          uint32_t* __restrict__ key, uint32_t* __restrict__ lcount) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const ScanRec r = scan[i];
-    const int l = level_of(L, fmin(r.inv_a, r.inv_b));
-    const int G = L.lw[l];
-    const uint32_t k = (uint32_t)(L.loff[l] + cell_of(r.mu_y, G) * G + cell_of(r.mu_x, G));
-    key[i] = k;
-    atomicAdd(cnt + k, 1u);
-    atomicAdd(lcount + l, 1u);
+    int l = -1;
+    if (i < n) {
+        const ScanRec r = scan[i];
+        l = level_of(L, fmin(r.inv_a, r.inv_b));
+        const int G = L.lw[l];
+        const uint32_t k = (uint32_t)(L.loff[l] + cell_of(r.mu_y, G) * G + cell_of(r.mu_x, G));
+        key[i] = k;
+        atomicAdd(cnt + k, 1u);
+    }
+    // per-level population, warp-aggregated (13 addresses would serialise)
+    const unsigned same = __match_any_sync(0xffffffffu, l);
+    if (l >= 0 && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(lcount + l, (unsigned)__popc(same));
 }
 
 __global__ void lq_fill(uint32_t n, const uint32_t* __restrict__ key, const uint32_t* __restrict__ off,
@@ -599,7 +603,7 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
 // per point offers the kHardSplit partial lists to a warp top-K (any order:
 // (q, idx) is a strict total order) and runs the epilogue.
 constexpr int kHardThreads = 128;
-constexpr int kHardSplit = 16;
+constexpr int kHardSplit = 64;
 
 template <int KCAP>
 __global__ void __launch_bounds__(kHardThreads) hard_scan_kernel(const ScanRec* __restrict__ scan, uint32_t n,
@@ -620,9 +624,22 @@ __global__ void __launch_bounds__(kHardThreads) hard_scan_kernel(const ScanRec* 
         const uint32_t g0 = split * per, g1 = min(n, g0 + per);
         TopK<KCAP> t;
         t.init(kk);
-        for (uint32_t g = g0 + threadIdx.x; g < g1; g += kHardThreads) {
-            const double q = maha(scan[g], px, py);
-            if (q <= t.tq()) t.offer(q, g);
+        // 4 independent records in flight per thread; the (rare) insertion
+        // sits behind a warp vote so it stays a branch, not predicated code
+        for (uint32_t base = g0; base < g1; base += 4 * kHardThreads) {
+            double q[4];
+            uint32_t gi[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                gi[j] = base + j * kHardThreads + threadIdx.x;
+                q[j] = gi[j] < g1 ? maha(scan[gi[j]], px, py) : __longlong_as_double(0x7ff0000000000000LL);
+            }
+            const double qm = fmin(fmin(q[0], q[1]), fmin(q[2], q[3]));
+            if (__any_sync(0xffffffffu, qm <= t.tq())) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (gi[j] < g1 && q[j] <= t.tq()) t.offer(q[j], gi[j]);
+            }
         }
         __syncthreads();
         store_topk(t, sq + threadIdx.x * KCAP, si + threadIdx.x * KCAP);

@@ -79,13 +79,14 @@ __global__ void __launch_bounds__(256) raster_global_kernel(const ScanRec* __res
         __syncthreads();
         stage_chunk(sm, scan, base, cnt, tid, kTile * kTile);
         __syncthreads();
-        if (live) {
+        // every thread runs the loop (warp votes need the full warp); only live
+        // threads write results
 #pragma unroll 1
             for (uint32_t c = 0; c < cnt; ++c) {
                 const double q = maha(sm[c], x, y);
-                if (q <= t.tq()) t.offer(q, base + c);
+                if (__any_sync(0xffffffffu, q <= t.tq()))
+                    if (q <= t.tq()) t.offer(q, base + c);
             }
-        }
     }
     if (!live) return;
     double col[3];
@@ -128,13 +129,14 @@ __global__ void __launch_bounds__(kPtThreads) points_partial_kernel(const ScanRe
         __syncthreads();
         stage_chunk(sm, scan, base, cnt, tid, kPtThreads);
         __syncthreads();
-        if (live) {
+        // every thread runs the loop (warp votes need the full warp); only live
+        // threads write results
 #pragma unroll 1
             for (uint32_t c = 0; c < cnt; ++c) {
                 const double q = maha(sm[c], x, y);
-                if (q <= t.tq()) t.offer(q, base + c);
+                if (__any_sync(0xffffffffu, q <= t.tq()))
+                    if (q <= t.tq()) t.offer(q, base + c);
             }
-        }
     }
     if (!live) return;
     const size_t o = ((size_t)blockIdx.y * npts + p) * kk;
