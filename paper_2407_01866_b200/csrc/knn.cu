@@ -499,15 +499,11 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
         eval_members(t, o, m, lane, scan, mem, px, py, evaluated);
     }
 
-    // A frontier node at level l holds only Gaussians of sigma <= cell_l / 2,
-    // so its bound is >= 4 (d / cell_l)^2: at most (sqrt(tq) + 3)^2 nodes per
-    // level can survive.  If that may exceed the queue, go straight to the
-    // exact split scan instead of walking a huge frontier first.
-    bool overflow = !(t.tq() < 387.0);
+    bool overflow = false;
     // (2) descent: evaluate own members of frontier nodes, expand children
     uint32_t* cur = queue[warp][0];
     uint32_t* nxt = queue[warp][1];
-    int ncur = overflow ? 0 : 1;
+    int ncur = 1;
     if (lane == 0) cur[0] = 0;  // root cell of the top level
     __syncwarp();
     for (int l = L.levels - 1; l >= 0 && ncur > 0; --l) {
@@ -603,7 +599,7 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
 // per point offers the kHardSplit partial lists to a warp top-K (any order:
 // (q, idx) is a strict total order) and runs the epilogue.
 constexpr int kHardThreads = 128;
-constexpr int kHardSplit = 64;
+constexpr int kHardSplit = 32;
 
 template <int KCAP>
 __global__ void __launch_bounds__(kHardThreads) hard_scan_kernel(const ScanRec* __restrict__ scan, uint32_t n,
