@@ -72,7 +72,9 @@ int64_t igs_get_option(const igs_ctx* ctx, int option);
 
 /* ---- Gaussian set (GaussianSet, gaussian.hpp:27-33) ------------------------ */
 /* Uploads n records and re-derives the per-Gaussian cache (PreparedSet,
- * renderer.cpp:32-51).  Resets Adam moments; invalidates the partition. */
+ * renderer.cpp:32-51).  Resets Adam moments.  A resident partition is kept
+ * (like a caller-held BspPartition); blocked renders reject it once the
+ * Gaussian count differs from the one it was built for. */
 int igs_set_params(igs_ctx* ctx, const double* params8, uint32_t n);
 /* Appends n records (densification, fit.cpp:185-199): indices stay stable,
  * new Adam moments are zero (AdamState::resize, adam.hpp:26-29). */

@@ -316,7 +316,8 @@ int igs_set_params(igs_ctx* ctx, const double* params8, uint32_t n) {
     ctx->n = n;
     ctx->grads_valid = false;
     ctx->params_version++;
-    igs_partition_free(ctx);
+    // a partition outlives the set like the reference's BspPartition; renders
+    // through it reject a changed count (bsp.cpp:278-282)
     if (n == 0) return IGS_OK;
     const size_t rb = (size_t)n * 8 * sizeof(double);
     if ((e = host_to_dev(ctx, ctx->params, params8, rb))) return e;
@@ -342,7 +343,6 @@ int igs_append_params(igs_ctx* ctx, const double* params8, uint32_t n) {
     ctx->n = old + n;
     ctx->grads_valid = false;
     ctx->params_version++;
-    igs_partition_free(ctx);  // a partition refers to the old count (bsp.cpp:278-282)
     return igs_prepare_all(ctx, old);
 }
 
