@@ -121,6 +121,13 @@ int igs_adam_step(igs_ctx* ctx, const double* lr4, long long t);
  * between them when a communicator is attached). */
 int igs_train_iteration(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, int k, const double* lr4,
                         long long t, double* loss);
+/* Asynchronous form for pipelined drivers: enqueues the iteration (the
+ * sample indices are staged through pinned memory; returns immediately) --
+ * igs_train_wait() then waits, checks the step's status and reports its
+ * loss.  At most one iteration may be outstanding. */
+int igs_train_iteration_async(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, int k, const double* lr4,
+                              long long t);
+int igs_train_wait(igs_ctx* ctx, double* loss);
 /* Uploads per-step sample indices to a device buffer of `steps` x ns
  * entries so igs_train_iterations can run fully device-resident. */
 int igs_upload_samples(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, uint32_t steps);
@@ -140,6 +147,43 @@ int igs_set_adam_state(igs_ctx* ctx, const double* m, const double* v, uint32_t 
 int igs_add_distribution(igs_ctx* ctx, const float* rendered, int width, int height, double* p);
 /* psnr(rendered, target); rendered nullable = last device image. */
 int igs_psnr(igs_ctx* ctx, const float* rendered, int width, int height, double* out);
+
+/* ssim(rendered, target) (metrics.cpp:33-112); rendered nullable = last image. */
+int igs_ssim(igs_ctx* ctx, const float* rendered, int width, int height, double* out);
+
+/* ---- encoder (fit.hpp:19-64) -------------------------------------------------- */
+typedef struct {
+    int budget;          /* target Gaussian count (final = budget/2 + 4*(budget/8)) */
+    int k;               /* top-K */
+    double lambda_init, lambda_opt;
+    int iterations, samples_per_iter;
+    double lr[4];        /* mu, color, scale, theta */
+    int eval_interval, plateau_patience;
+    double lr_decay;     /* multiplier, applied at most once */
+    int warmup_iters, densify_interval;
+    uint64_t seed;
+    int compute_ssim;    /* 1 = evaluate SSIM like the reference, 0 = skip (logged as 0) */
+} igs_fit_config;
+typedef struct {
+    int iteration, count;
+    double loss, psnr, ssim, best_psnr;
+} igs_eval_record;
+/* LoD checkpoint (fit.hpp:56-58): stage, iteration, id "lod<s>_iter<i>_n<c>", the set. */
+typedef void (*igs_checkpoint_fn)(void* user, int stage, int iteration, const char* id, const double* params8,
+                                  uint32_t n);
+/* FitConfig defaults (fit.hpp:19-33). */
+void igs_fit_config_default(igs_fit_config* cfg);
+/* fit() (fit.cpp:116-207): content-adaptive init, importance-sampled L1
+ * optimisation with Adam, periodic BSP-render evaluation with one-shot LR
+ * decay, error-guided densification, LoD checkpoints.  RNG draws (mt19937_64,
+ * Walker alias tables) run on the host in the reference's order; every
+ * render, train step, Adam step and metric runs on the device.  The final
+ * set stays resident (igs_get_params).  evals (nullable) receives up to
+ * max_evals records; log (nullable) receives FitReport::write's text
+ * (fit.cpp:209-231), NUL-terminated, truncated to log_cap. */
+int igs_fit(igs_ctx* ctx, const float* target, int width, int height, const igs_fit_config* cfg,
+            igs_checkpoint_fn cb, void* user, igs_eval_record* evals, int max_evals, int* n_evals,
+            int* lr_decay_iteration, int* final_count, char* log, size_t log_cap);
 
 /* ---- BSP acceleration (bsp.hpp:70-106) ------------------------------------ */
 /* build_partition(set, n_max) over the resident set. */

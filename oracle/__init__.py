@@ -108,7 +108,17 @@ _PORT_ONLY = [
     ("prepare_scan", None, [_dp, C.c_uint32, _dp]),
 ]
 
+class RefFitConfig(C.Structure):
+    _fields_ = [("budget", C.c_int), ("k", C.c_int), ("lambda_init", C.c_double), ("lambda_opt", C.c_double),
+                ("iterations", C.c_int), ("samples_per_iter", C.c_int), ("lr", C.c_double * 4),
+                ("eval_interval", C.c_int), ("plateau_patience", C.c_int), ("lr_decay", C.c_double),
+                ("warmup_iters", C.c_int), ("densify_interval", C.c_int), ("seed", C.c_uint64),
+                ("compute_ssim", C.c_int)]
+
+
 _REF_ONLY = [
+    ("fit", C.c_int, [_fp, C.c_int, C.c_int, C.POINTER(RefFitConfig), _dp, C.c_uint32, _up, C.c_char_p,
+                      C.c_size_t]),
     ("backward_mode", C.c_int, [_dp, C.c_uint32, _dp, C.c_uint32, C.c_int, _dp, C.c_int]),
     ("sample_pixel_indices", C.c_int, [_dp, C.c_int, C.c_int, C.c_int, C.c_uint64, _up]),
     ("ssim", C.c_double, [_fp, _fp, C.c_int, C.c_int]),
@@ -334,6 +344,28 @@ class Oracle:
         mem = np.zeros(max(total, 1), np.uint32)
         self._f("cull_lists")(_ptr(scan6, _dp), n, W, H, k, T, _ptr(off, _up), _ptr(mem, _up), _ptr(tau, _dp))
         return off, mem[:total], tau
+
+    # ---- encoder (reference back-end) -----------------------------------------
+    def fit(self, target, **cfg):
+        """The reference's fit(); cfg keys as FitConfig; returns (set, log)."""
+        target = np.ascontiguousarray(target, np.float32)
+        H, W, _ = target.shape
+        c = RefFitConfig(budget=0, k=10, lambda_init=0.3, lambda_opt=0.8, iterations=50000, samples_per_iter=10000,
+                         eval_interval=1000, plateau_patience=3, lr_decay=0.1, warmup_iters=10000,
+                         densify_interval=5000, seed=0, compute_ssim=1)
+        for i, x in enumerate((2e-4, 2e-3, 1e-3, 1e-3)):
+            c.lr[i] = x
+        for k, v in cfg.items():
+            if k == "lr":
+                for i, x in enumerate(v):
+                    c.lr[i] = x
+            else:
+                setattr(c, k, v)
+        cap = max(c.budget, 8) * 2
+        out = np.zeros((cap, 8)); n = C.c_uint32(0); log = C.create_string_buffer(1 << 20)
+        self._chk(self._f("fit")(_ptr(target, _fp), W, H, C.byref(c), _ptr(out, _dp), cap, C.byref(n), log,
+                                 len(log)), "fit")
+        return out[:n.value], log.value.decode()
 
     # ---- BSP ------------------------------------------------------------------
     def partition_build(self, params, n_max):

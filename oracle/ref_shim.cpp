@@ -7,6 +7,7 @@
 // bench.py --impl reference can time the reference's own OpenMP code path.
 #include <cmath>
 #include <cstring>
+#include <sstream>
 #include <span>
 #include <vector>
 
@@ -367,6 +368,55 @@ int ref_render_points_blocked(const double* p8, uint32_t n, const ref_partition*
             rgb[3 * i + 1] = c.g;
             rgb[3 * i + 2] = c.b;
         }
+        return 0;
+    } catch (const Error& e) {
+        return code_of(e);
+    }
+}
+
+// The reference's fit() (fit.cpp:116-207) on a float32 target; config in
+// the layout of igs_fit_config (budget, k, lambda_init, lambda_opt,
+// iterations, samples, lr[4], eval_interval, patience, lr_decay, warmup,
+// densify_interval, seed, compute_ssim).  Writes the final set (capacity
+// max_n records) and the FitReport log.
+struct RefFitConfig {
+    int budget, k;
+    double lambda_init, lambda_opt;
+    int iterations, samples_per_iter;
+    double lr[4];
+    int eval_interval, plateau_patience;
+    double lr_decay;
+    int warmup_iters, densify_interval;
+    uint64_t seed;
+    int compute_ssim;
+};
+
+int ref_fit(const float* target, int W, int H, const RefFitConfig* c, double* out8, uint32_t max_n, uint32_t* n_out,
+            char* log, size_t cap) {
+    try {
+        FitConfig fc;
+        fc.budget = c->budget;
+        fc.k = c->k;
+        fc.lambda_init = c->lambda_init;
+        fc.lambda_opt = c->lambda_opt;
+        fc.iterations = c->iterations;
+        fc.samples_per_iter = c->samples_per_iter;
+        fc.lr = LearningRates{c->lr[0], c->lr[1], c->lr[2], c->lr[3]};
+        fc.eval_interval = c->eval_interval;
+        fc.plateau_patience = c->plateau_patience;
+        fc.lr_decay = c->lr_decay;
+        fc.warmup_iters = c->warmup_iters;
+        fc.densify_interval = c->densify_interval;
+        fc.seed = c->seed;
+        auto [set, report] = fit(to_image(target, W, H), fc);
+        *n_out = static_cast<uint32_t>(set.size());
+        std::memcpy(out8, set.gaussians.data(), sizeof(double) * 8 * std::min<size_t>(set.size(), max_n));
+        std::ostringstream os;
+        report.write(os, fc);
+        const std::string s = os.str();
+        const size_t m = std::min(s.size(), cap - 1);
+        std::memcpy(log, s.data(), m);
+        log[m] = 0;
         return 0;
     } catch (const Error& e) {
         return code_of(e);

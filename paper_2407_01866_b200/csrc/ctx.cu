@@ -29,6 +29,7 @@ int igs_cull_lists(igs_ctx* ctx, int W, int H, int k, uint32_t* ntiles, uint64_t
 // metrics.cu
 int igs_error_map(igs_ctx* ctx, const float* dev_rendered, int W, int H, double* dev_p);
 int igs_psnr_dev(igs_ctx* ctx, const float* dev_a, const float* dev_b, size_t count, double* out);
+int igs_ssim_dev(igs_ctx* ctx, const float* a, const float* b, int W, int H, double* out);
 
 
 // ---------------------------------------------------------------------------
@@ -217,6 +218,9 @@ static int require_k(igs_ctx* ctx, int k) {
 
 extern "C" {
 
+// internal (not in igs_b200.h): lets host-side drivers (fit.cpp) record errors
+int igs_internal_fail(igs_ctx* ctx, int code, const char* msg) { return igs_fail(ctx, code, msg); }
+
 int igs_ctx_create(int device, igs_ctx** out) {
     if (!out) return IGS_E_INVALID_PARAMETER;
     *out = nullptr;
@@ -268,6 +272,8 @@ void igs_ctx_destroy(igs_ctx* ctx) {
     for (auto e : ctx->timer)
         if (e) cudaEventDestroy(e);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    for (auto& b : ctx->async_pin)
+        if (b.p) cudaFreeHost(b.p);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -617,6 +623,81 @@ int igs_train_iteration(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, i
     if ((ctx->nranks > 1 || !ctx->grads_checked) && (e = igs_grad_check(ctx))) return e;
     if ((e = igs_adam_launch(ctx, lr4, t))) return e;
     return read_status(ctx, dloss, loss, 1);
+}
+
+static int stage_rendered(igs_ctx* ctx, const float* rendered, int W, int H, const float** dev);
+
+// Pinned staging for the async iteration: [0] sample buffer, [1] result
+// block {status[4], loss}.
+static void* async_pinned(igs_ctx* ctx, int which, size_t bytes) {
+    DevBuf& b = ctx->async_pin[which];
+    if (b.bytes >= bytes) return b.p;
+    if (b.p) cudaFreeHost(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    if (cudaMallocHost(&b.p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    b.bytes = bytes;
+    return b.p;
+}
+
+int igs_train_iteration_async(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, int k, const double* lr4,
+                              long long t) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    int e;
+    if (ctx->async_pending) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "an iteration is already outstanding");
+    if ((e = train_checks(ctx, ns, k))) return e;
+    if (t < 1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "Adam step index must be >= 1");
+    const uint64_t npx = (uint64_t)ctx->tgt_w * ctx->tgt_h;
+    for (uint32_t i = 0; i < ns; ++i)
+        if (sample_idx[i] >= npx) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "sample index outside the target");
+    uint32_t* pin = (uint32_t*)async_pinned(ctx, 0, (size_t)ns * 4);
+    long long* res = (long long*)async_pinned(ctx, 1, 64);
+    uint32_t* dsidx = (uint32_t*)igs_scratch(ctx, 21, (size_t)ns * sizeof(uint32_t));
+    double* dloss = (double*)igs_scratch(ctx, 14, 64 * sizeof(double));
+    if (!pin || !res || !dsidx || !dloss) return igs_fail(ctx, IGS_E_CUDA, "out of memory (async iteration)");
+    std::memcpy(pin, sample_idx, (size_t)ns * 4);
+    IGS_CUDA(ctx, cudaMemcpyAsync(dsidx, pin, (size_t)ns * 4, cudaMemcpyHostToDevice, ctx->stream));
+    if ((e = igs_status_reset(ctx))) return e;
+    const uint32_t ns_total = ns * (uint32_t)ctx->nranks;
+    if ((e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss, 1.0 / (double)ns_total))) return e;
+    if ((e = allreduce_grads(ctx, dloss))) return e;
+    if ((ctx->nranks > 1 || !ctx->grads_checked) && (e = igs_grad_check(ctx))) return e;
+    if ((e = igs_adam_launch(ctx, lr4, t))) return e;
+    IGS_CUDA(ctx, cudaMemcpyAsync(res, ctx->status, 4 * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+    IGS_CUDA(ctx, cudaMemcpyAsync(res + 4, dloss, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->async_pending = true;
+    return IGS_OK;
+}
+
+int igs_train_wait(igs_ctx* ctx, double* loss) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    if (!ctx->async_pending) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "no outstanding iteration");
+    ctx->async_pending = false;
+    IGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    const long long* st = (const long long*)ctx->async_pin[1].p;
+    if (st[2] != LLONG_MAX) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "training loss became non-finite");
+    if (st[0] != LLONG_MAX) {
+        static const char* names[8] = {"mu_u", "mu_v", "theta", "s1", "s2", "r", "g", "b"};
+        return igs_fail(ctx, IGS_E_INVALID_PARAMETER,
+                        "non-finite gradient for Gaussian " + std::to_string(st[0] / 8) + " parameter " + names[st[0] % 8]);
+    }
+    if (st[1] != LLONG_MAX) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "non-finite Gaussian parameters");
+    if (loss) std::memcpy(loss, st + 4, sizeof(double));
+    return IGS_OK;
+}
+
+int igs_ssim(igs_ctx* ctx, const float* rendered, int width, int height, double* out) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    const float* dr;
+    int e;
+    if ((e = stage_rendered(ctx, rendered, width, height, &dr))) return e;
+    return igs_ssim_dev(ctx, dr, (const float*)ctx->target.p, width, height, out);
 }
 
 int igs_upload_samples(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, uint32_t steps) {

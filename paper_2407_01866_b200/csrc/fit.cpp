@@ -1,0 +1,331 @@
+// fit.cpp -- the encoder loop (fit.cpp:116-207 of the reference) as native
+// host code driving the device through the C-ABI.
+//
+// Host side (exactly the reference's arithmetic and RNG order, compiled with
+// -ffp-contract=off): std::mt19937_64 with rng.hpp's draw helpers, the Sobel
+// / mixture init distribution (sampling.cpp:14-75), Walker/Vose alias tables
+// (sampling.cpp:96-133), initialize_set (:154-174), the schedule, plateau
+// LR decay, densification appends and the log format.
+// Device side: every train iteration (exact top-K + loss + backward + Adam),
+// the evaluation renders (BSP partition with n_max = 64 + blocked raster,
+// fit.cpp:34-37), PSNR, SSIM and the Eq. 8 error map.
+//
+// Pipelining: iteration t's sample indices are drawn before it is launched;
+// while the device runs iteration t the host draws iteration t+1's samples
+// -- unless iteration t evaluates or densifies, in which case the host waits,
+// does that work first and then draws (the reference's RNG order: samples_t,
+// densification draws at t, samples_{t+1}).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "igs_b200.h"
+
+// ctx.cu: records the message returned by igs_last_error
+extern "C" int igs_internal_fail(igs_ctx* ctx, int code, const char* msg);
+
+namespace {
+
+// rng.hpp:11-28
+struct Rng {
+    std::mt19937_64 e;
+    explicit Rng(uint64_t seed) : e(seed) {}
+    double next_double() { return (e() >> 11) * 0x1.0p-53; }
+    uint64_t next_index(uint64_t n) { return e() % n; }
+};
+
+// sampling.cpp:14-23
+double kahan_sum(const std::vector<double>& v) {
+    double sum = 0.0, comp = 0.0;
+    for (double x : v) {
+        const double y = x - comp;
+        const double t = sum + y;
+        comp = (t - sum) - y;
+        sum = t;
+    }
+    return sum;
+}
+
+// sampling.cpp:44-67
+std::vector<double> gradient_magnitude(const float* img, int W, int H) {
+    std::vector<double> mag((size_t)W * H);
+    auto cl = [](int v, int hi) { return v < 0 ? 0 : (v > hi ? hi : v); };
+    auto at = [&](int h, int w, int c) { return (double)img[((size_t)h * W + w) * 3 + c]; };
+    for (int h = 0; h < H; ++h)
+        for (int w = 0; w < W; ++w) {
+            const int hm = cl(h - 1, H - 1), hp = cl(h + 1, H - 1), wm = cl(w - 1, W - 1), wp = cl(w + 1, W - 1);
+            double acc = 0.0;
+            for (int c = 0; c < 3; ++c) {
+                const double tl = at(hm, wm, c), tc = at(hm, w, c), tr = at(hm, wp, c);
+                const double ml = at(h, wm, c), mr = at(h, wp, c);
+                const double bl = at(hp, wm, c), bc = at(hp, w, c), br = at(hp, wp, c);
+                const double gx = (tr + 2.0 * mr + br) - (tl + 2.0 * ml + bl);
+                const double gy = (bl + 2.0 * bc + br) - (tl + 2.0 * tc + tr);
+                acc += gx * gx + gy * gy;
+            }
+            mag[(size_t)h * W + w] = std::sqrt(acc);
+        }
+    return mag;
+}
+
+// sampling.cpp:25-40 gradient_mixture (init_distribution / opt_distribution)
+std::vector<double> gradient_mixture(const float* img, int W, int H, double lambda) {
+    std::vector<double> p = gradient_magnitude(img, W, H);
+    const double total = kahan_sum(p);
+    const double uniform = 1.0 / (double)p.size();
+    if (total > 0.0) {
+        const double scale = (1.0 - lambda) / total;
+        for (double& v : p) v = v * scale + lambda * uniform;
+    } else {
+        std::fill(p.begin(), p.end(), uniform);
+    }
+    return p;
+}
+
+// sampling.cpp:96-133 Walker/Vose table; draw = index, then coin
+struct Alias {
+    std::vector<double> prob;
+    std::vector<uint32_t> alias;
+    bool ok = false;
+
+    explicit Alias(const std::vector<double>& w) {
+        const size_t n = w.size();
+        if (n == 0) return;
+        const double total = kahan_sum(w);
+        if (!(total > 0.0)) return;
+        prob.assign(n, 0.0);
+        alias.assign(n, 0);
+        std::vector<double> scaled(n);
+        for (size_t i = 0; i < n; ++i) {
+            if (w[i] < 0.0) return;
+            scaled[i] = w[i] * n / total;
+        }
+        std::vector<uint32_t> small, large;
+        small.reserve(n);
+        large.reserve(n);
+        for (size_t i = 0; i < n; ++i) (scaled[i] < 1.0 ? small : large).push_back((uint32_t)i);
+        while (!small.empty() && !large.empty()) {
+            const uint32_t s = small.back(), l = large.back();
+            small.pop_back();
+            large.pop_back();
+            prob[s] = scaled[s];
+            alias[s] = l;
+            scaled[l] = (scaled[l] + scaled[s]) - 1.0;
+            (scaled[l] < 1.0 ? small : large).push_back(l);
+        }
+        for (uint32_t i : large) prob[i] = 1.0;
+        for (uint32_t i : small) prob[i] = 1.0;
+        ok = true;
+    }
+    uint32_t sample(Rng& r) const {
+        const size_t i = (size_t)r.next_index(prob.size());
+        return r.next_double() < prob[i] ? (uint32_t)i : alias[i];
+    }
+};
+
+void add_gaussian(std::vector<double>& out, const float* img, int W, int H, uint32_t flat, double s0) {
+    const int h = (int)flat / W, w = (int)flat % W;
+    out.push_back((w + 0.5) / W);  // pixel_center (image.hpp:18-20)
+    out.push_back((h + 0.5) / H);
+    out.push_back(0.0);
+    out.push_back(s0);
+    out.push_back(s0);
+    out.push_back((double)img[((size_t)h * W + w) * 3]);
+    out.push_back((double)img[((size_t)h * W + w) * 3 + 1]);
+    out.push_back((double)img[((size_t)h * W + w) * 3 + 2]);
+}
+
+struct Fail {
+    int code;
+};
+
+}  // namespace
+
+extern "C" {
+
+void igs_fit_config_default(igs_fit_config* c) {
+    c->budget = 0;
+    c->k = 10;
+    c->lambda_init = 0.3;
+    c->lambda_opt = 0.8;
+    c->iterations = 50000;
+    c->samples_per_iter = 10000;
+    c->lr[0] = 2e-4;  // mu
+    c->lr[1] = 2e-3;  // color
+    c->lr[2] = 1e-3;  // scale
+    c->lr[3] = 1e-3;  // theta
+    c->eval_interval = 1000;
+    c->plateau_patience = 3;
+    c->lr_decay = 0.1;
+    c->warmup_iters = 10000;
+    c->densify_interval = 5000;
+    c->seed = 0;
+    c->compute_ssim = 1;
+}
+
+int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_config* cfg, igs_checkpoint_fn cb,
+            void* user, igs_eval_record* evals, int max_evals, int* n_evals, int* lr_decay_iteration,
+            int* final_count, char* log, size_t log_cap) {
+    if (!ctx || !cfg || !target) return IGS_E_INVALID_PARAMETER;
+    const igs_fit_config& c = *cfg;
+    // fit.cpp:19-29 validate (messages are the reference's; see igs_last_error)
+    auto bad = [&](const char* msg) { return igs_internal_fail(ctx, IGS_E_INVALID_PARAMETER, msg); };
+    if (c.budget < 8) return bad("budget must be >= 8");
+    if (c.k < 1) return bad("k must be >= 1");
+    if (c.lambda_init < 0.0 || c.lambda_init > 1.0 || c.lambda_opt < 0.0 || c.lambda_opt > 1.0)
+        return bad("lambda values must lie in [0,1]");
+    if (c.iterations < 1 || c.samples_per_iter < 1 || c.eval_interval < 1 || c.plateau_patience < 1 ||
+        c.warmup_iters < 1 || c.densify_interval < 1)
+        return bad("schedule counts must be >= 1");
+    if (c.lr[0] <= 0.0 || c.lr[1] <= 0.0 || c.lr[2] <= 0.0 || c.lr[3] <= 0.0 || c.lr_decay <= 0.0)
+        return bad("rates must be positive");
+    if (W < 1 || H < 1) return bad("image dimensions must be positive");
+
+    int e;
+    std::string text;
+    char line[512];
+    std::snprintf(line, sizeof(line),
+                  "config budget=%d k=%d lambda_init=%.6g lambda_opt=%.6g iterations=%d samples=%d "
+                  "lr_mu=%.6g lr_color=%.6g lr_scale=%.6g lr_theta=%.6g eval_interval=%d patience=%d "
+                  "lr_decay=%.6g warmup=%d densify_interval=%d seed=%llu\n",
+                  c.budget, c.k, c.lambda_init, c.lambda_opt, c.iterations, c.samples_per_iter, c.lr[0], c.lr[1],
+                  c.lr[2], c.lr[3], c.eval_interval, c.plateau_patience, c.lr_decay, c.warmup_iters,
+                  c.densify_interval, (unsigned long long)c.seed);
+    text += line;
+
+    Rng rng(c.seed);
+    // initialize_set(target, budget/2, lambda_init, rng) (sampling.cpp:154-174)
+    const int init_count = c.budget / 2;
+    std::vector<double> set;
+    {
+        const Alias init(gradient_mixture(target, W, H, c.lambda_init));
+        if (!init.ok) return bad("alias table weights must have positive sum");
+        const double s0 = 2.0 / std::max(W, H);
+        set.reserve((size_t)init_count * 8);
+        for (int i = 0; i < init_count; ++i) add_gaussian(set, target, W, H, init.sample(rng), s0);
+    }
+    const Alias opt(gradient_mixture(target, W, H, c.lambda_opt));
+    if (!opt.ok) return bad("alias table weights must have positive sum");
+    if ((e = igs_set_target(ctx, target, W, H))) return e;
+    if ((e = igs_set_params(ctx, set.data(), (uint32_t)init_count))) return e;
+
+    double lr[4] = {c.lr[0], c.lr[1], c.lr[2], c.lr[3]};
+    bool decayed = false;
+    int decay_iter = -1;
+    double best_psnr = -std::numeric_limits<double>::infinity();
+    int streak = 0;
+    const double default_scale = 2.0 / std::max(W, H);
+    const int add_count = c.budget / 8;
+    int stage = 0;
+    std::vector<igs_eval_record> recs;
+    std::vector<std::string> checkpoints;
+    std::vector<float> rendered((size_t)W * H * 3);
+    std::vector<double> dist((size_t)W * H);
+    std::vector<uint32_t> cur((size_t)c.samples_per_iter), next((size_t)c.samples_per_iter);
+    auto draw = [&](std::vector<uint32_t>& s) {
+        for (auto& v : s) v = opt.sample(rng);
+    };
+    auto emit_checkpoint = [&](int iteration) -> int {
+        const uint32_t n = igs_num_gaussians(ctx);
+        char id[64];
+        std::snprintf(id, sizeof(id), "lod%d_iter%d_n%u", stage, iteration, n);
+        checkpoints.push_back(id);
+        if (cb) {
+            std::vector<double> p((size_t)n * 8);
+            int ee = igs_get_params(ctx, p.data(), n);
+            if (ee) return ee;
+            cb(user, stage, iteration, id, p.data(), n);
+        }
+        return IGS_OK;
+    };
+    // fit.cpp:34-37 render_current: build_partition(set, 64) + render_image_blocked
+    auto render_current = [&]() -> int {
+        int ee = igs_partition_build(ctx, 64);
+        if (ee) return ee;
+        return igs_render_image_blocked(ctx, W, H, c.k, nullptr);
+    };
+
+    draw(cur);
+    for (int iter = 1; iter <= c.iterations; ++iter) {
+        if ((e = igs_train_iteration_async(ctx, cur.data(), (uint32_t)cur.size(), c.k, lr, iter))) return e;
+        const bool do_eval = iter % c.eval_interval == 0 || iter == c.iterations;
+        const bool do_densify = stage < 4 && iter == c.warmup_iters + stage * c.densify_interval;
+        double loss = 0.0;
+        if (!do_eval && !do_densify) {
+            if (iter < c.iterations) draw(next);  // overlaps the device step
+            if ((e = igs_train_wait(ctx, &loss))) return e;
+            std::swap(cur, next);
+            continue;
+        }
+        if ((e = igs_train_wait(ctx, &loss))) return e;
+        bool have_render = false;
+        if (do_eval) {
+            if ((e = render_current())) return e;
+            have_render = true;
+            double p = 0.0, s = 0.0;
+            if ((e = igs_psnr(ctx, nullptr, W, H, &p))) return e;
+            if (c.compute_ssim && (e = igs_ssim(ctx, nullptr, W, H, &s))) return e;
+            if (p >= best_psnr + 0.01) {
+                best_psnr = p;
+                streak = 0;
+            } else {
+                best_psnr = std::max(best_psnr, p);
+                ++streak;
+                if (!decayed && streak >= c.plateau_patience) {
+                    for (double& v : lr) v *= c.lr_decay;  // LearningRates::scaled
+                    decayed = true;
+                    decay_iter = iter;
+                }
+            }
+            recs.push_back({iter, (int)igs_num_gaussians(ctx), loss, p, s, best_psnr});
+        }
+        if (do_densify) {
+            if ((e = emit_checkpoint(iter))) return e;
+            if (!have_render && (e = render_current())) return e;
+            // add_distribution(rendered, target) on the device, Vose + draws here
+            if ((e = igs_add_distribution(ctx, nullptr, W, H, dist.data()))) return e;
+            const Alias add(dist);
+            if (!add.ok) return bad("alias table weights must have positive sum");
+            std::vector<double> fresh;
+            fresh.reserve((size_t)add_count * 8);
+            for (int a = 0; a < add_count; ++a) add_gaussian(fresh, target, W, H, add.sample(rng), default_scale);
+            if (add_count > 0 && (e = igs_append_params(ctx, fresh.data(), (uint32_t)add_count))) return e;
+            ++stage;
+        }
+        if (iter < c.iterations) draw(next);
+        std::swap(cur, next);
+    }
+    if ((e = emit_checkpoint(c.iterations))) return e;
+
+    // FitReport::write (fit.cpp:209-231)
+    for (const auto& r : recs) {
+        std::snprintf(line, sizeof(line), "eval iter=%d n=%d loss=%.9e psnr=%.6f ssim=%.8f best=%.6f\n", r.iteration,
+                      r.count, r.loss, r.psnr, r.ssim, r.best_psnr);
+        text += line;
+    }
+    if (decay_iter >= 0) {
+        std::snprintf(line, sizeof(line), "event lr_decay iter=%d\n", decay_iter);
+        text += line;
+    }
+    for (const auto& id : checkpoints) text += "checkpoint id=" + id + "\n";
+    const int fc = (int)igs_num_gaussians(ctx);
+    text += "final n=" + std::to_string(fc) + "\n";
+
+    if (evals) std::memcpy(evals, recs.data(), sizeof(igs_eval_record) * std::min<size_t>(recs.size(), max_evals));
+    if (n_evals) *n_evals = (int)recs.size();
+    if (lr_decay_iteration) *lr_decay_iteration = decay_iter;
+    if (final_count) *final_count = fc;
+    if (log && log_cap) {
+        const size_t m = std::min(text.size(), log_cap - 1);
+        std::memcpy(log, text.data(), m);
+        log[m] = 0;
+    }
+    return IGS_OK;
+}
+
+}  // extern "C"

@@ -186,6 +186,10 @@ struct igs_ctx {
     // device status word block: [0] error code flag, [1] first bad slot
     long long* status = nullptr;
 
+    // pinned staging of the async iteration (igs_train_iteration_async)
+    DevBuf async_pin[2];
+    bool async_pending = false;
+
     // uploaded samples for device-resident training
     DevBuf samples;
     uint32_t samples_ns = 0, samples_steps = 0;

@@ -10,6 +10,9 @@
 // 1 ulp.  HBM-bound: 24 B/px read + 8 B/px written.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cmath>
+
 #include "igs_internal.cuh"
 
 namespace {
@@ -133,5 +136,107 @@ int igs_psnr_dev(igs_ctx* ctx, const float* a, const float* b, size_t count, dou
     }
     const double mse = se / (double)count;
     *out = 10.0 * std::log10(1.0 / mse);
+    return IGS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// SSIM (metrics.cpp:33-112): 11x11 separable Gaussian window (sigma 1.5),
+// replicate padding, C1 = 0.01^2, C2 = 0.03^2, mean over pixels, averaged
+// over RGB.  The window is built on the host with the same libm exp and
+// sequential normalisation as ssim_window(); both filter passes accumulate
+// the 11 taps in order (no FMA), so each filtered value matches the
+// reference bit for bit; the per-channel mean is the double-double total.
+// ---------------------------------------------------------------------------
+namespace {
+
+struct Win11 {
+    double w[11];
+};
+
+__device__ __forceinline__ int clampi(int v, int hi) { return v < 0 ? 0 : (v > hi ? hi : v); }
+
+// horizontal pass of the five maps x, y, xx, yy, xy for channel c
+__global__ void ssim_h_kernel(const float* __restrict__ a, const float* __restrict__ b, int W, int H, int c, Win11 win,
+                              double* __restrict__ tmp /* 5 * H * W */) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x, h = blockIdx.y;
+    if (w >= W) return;
+    double s[5] = {0, 0, 0, 0, 0};
+    for (int i = 0; i < 11; ++i) {
+        const size_t o = ((size_t)h * W + clampi(w - 5 + i, W - 1)) * 3 + c;
+        const double x = (double)a[o], y = (double)b[o];
+        const double wi = win.w[i];
+        s[0] = __dadd_rn(s[0], __dmul_rn(wi, x));
+        s[1] = __dadd_rn(s[1], __dmul_rn(wi, y));
+        s[2] = __dadd_rn(s[2], __dmul_rn(wi, __dmul_rn(x, x)));
+        s[3] = __dadd_rn(s[3], __dmul_rn(wi, __dmul_rn(y, y)));
+        s[4] = __dadd_rn(s[4], __dmul_rn(wi, __dmul_rn(x, y)));
+    }
+    const size_t n = (size_t)W * H, p = (size_t)h * W + w;
+#pragma unroll
+    for (int m = 0; m < 5; ++m) tmp[m * n + p] = s[m];
+}
+
+// vertical pass + SSIM map + per-block double-double partial sums
+__global__ void __launch_bounds__(kRedThreads) ssim_v_kernel(const double* __restrict__ tmp, int W, int H, Win11 win,
+                                                            double* __restrict__ part) {
+    const size_t n = (size_t)W * H;
+    const double c1 = 0.01 * 0.01, c2 = 0.03 * 0.03;
+    DD acc = {0.0, 0.0};
+    for (size_t p = (size_t)blockIdx.x * kRedThreads + threadIdx.x; p < n; p += (size_t)gridDim.x * kRedThreads) {
+        const int h = (int)(p / W), w = (int)(p % W);
+        double s[5] = {0, 0, 0, 0, 0};
+        for (int i = 0; i < 11; ++i) {
+            const size_t q = (size_t)clampi(h - 5 + i, H - 1) * W + w;
+            const double wi = win.w[i];
+#pragma unroll
+            for (int m = 0; m < 5; ++m) s[m] = __dadd_rn(s[m], __dmul_rn(wi, tmp[m * n + q]));
+        }
+        const double mx = s[0], my = s[1];
+        const double var_x = __dsub_rn(s[2], __dmul_rn(mx, mx));
+        const double var_y = __dsub_rn(s[3], __dmul_rn(my, my));
+        const double cov = __dsub_rn(s[4], __dmul_rn(mx, my));
+        const double num = __dmul_rn(__dadd_rn(__dmul_rn(__dmul_rn(2.0, mx), my), c1), __dadd_rn(__dmul_rn(2.0, cov), c2));
+        const double den = __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(mx, mx), __dmul_rn(my, my)), c1),
+                                     __dadd_rn(__dadd_rn(var_x, var_y), c2));
+        acc = dd_add(acc, {__ddiv_rn(num, den), 0.0});
+    }
+    const DD r = block_reduce(acc);
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = r.hi;
+        part[2 * blockIdx.x + 1] = r.lo;
+    }
+}
+
+}  // namespace
+
+int igs_ssim_dev(igs_ctx* ctx, const float* a, const float* b, int W, int H, double* out) {
+    if (W < 11 || H < 11) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "ssim: image smaller than the 11x11 window");
+    Win11 win;
+    double sum = 0.0;
+    for (int i = 0; i < 11; ++i) {  // metrics.cpp:33-44
+        const double d = i - (11 - 1) / 2.0;
+        win.w[i] = std::exp(-d * d / (2.0 * 1.5 * 1.5));
+        sum += win.w[i];
+    }
+    for (double& v : win.w) v /= sum;
+    const size_t n = (size_t)W * H;
+    double* tmp = (double*)igs_scratch(ctx, 27, 5 * n * sizeof(double));
+    const int blocks = (int)std::min<size_t>(4 * ctx->sm_count, (n + kRedThreads - 1) / kRedThreads);
+    double* part = (double*)igs_scratch(ctx, 28, (size_t)(2 * blocks + 2) * sizeof(double));
+    if (!tmp || !part) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (ssim)");
+    double channel_sum = 0.0;
+    for (int c = 0; c < 3; ++c) {
+        ssim_h_kernel<<<dim3((W + 127) / 128, H), 128, 0, ctx->stream>>>(a, b, W, H, c, win, tmp);
+        IGS_LAUNCHED(ctx);
+        ssim_v_kernel<<<blocks, kRedThreads, 0, ctx->stream>>>(tmp, W, H, win, part);
+        IGS_LAUNCHED(ctx);
+        finish_sum_kernel<<<1, kRedThreads, 0, ctx->stream>>>(part, blocks, part + 2 * blocks);
+        IGS_LAUNCHED(ctx);
+        double acc = 0.0;
+        IGS_CUDA(ctx, cudaMemcpyAsync(&acc, part + 2 * blocks, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        IGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        channel_sum += acc / (double)n;
+    }
+    *out = channel_sum / 3.0;
     return IGS_OK;
 }

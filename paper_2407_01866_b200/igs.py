@@ -55,6 +55,23 @@ DEFAULT_LR = (2e-4, 2e-3, 1e-3, 1e-3)  # mu, color, scale, theta
 DEFAULT_K = 10  # renderer.hpp:16 kDefaultTopK
 
 
+class FitConfig(C.Structure):
+    """igs_fit_config == FitConfig (fit.hpp:19-33) + compute_ssim."""
+    _fields_ = [("budget", C.c_int), ("k", C.c_int), ("lambda_init", C.c_double), ("lambda_opt", C.c_double),
+                ("iterations", C.c_int), ("samples_per_iter", C.c_int), ("lr", C.c_double * 4),
+                ("eval_interval", C.c_int), ("plateau_patience", C.c_int), ("lr_decay", C.c_double),
+                ("warmup_iters", C.c_int), ("densify_interval", C.c_int), ("seed", C.c_uint64),
+                ("compute_ssim", C.c_int)]
+
+
+class EvalRecord(C.Structure):
+    _fields_ = [("iteration", C.c_int), ("count", C.c_int), ("loss", C.c_double), ("psnr", C.c_double),
+                ("ssim", C.c_double), ("best_psnr", C.c_double)]
+
+
+CHECKPOINT_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.c_int, C.c_char_p, C.POINTER(C.c_double), C.c_uint32)
+
+
 class IgsError(RuntimeError):
     def __init__(self, code: int, msg: str):
         self.code = code
@@ -117,6 +134,13 @@ SIGNATURES = {
     "igs_fp64_peak": (C.c_int, [_vp, _dp]),
     "igs_profile_enable": (C.c_int, [_vp, C.c_int]),
     "igs_profile_read": (C.c_int, [_vp, C.c_int, _dp, _u64p, _dp]),
+    "igs_train_iteration_async": (C.c_int, [_vp, _up, C.c_uint32, C.c_int, _dp, C.c_longlong]),
+    "igs_train_wait": (C.c_int, [_vp, _dp]),
+    "igs_ssim": (C.c_int, [_vp, _fp, C.c_int, C.c_int, _dp]),
+    "igs_fit_config_default": (None, [C.POINTER(FitConfig)]),
+    "igs_fit": (C.c_int, [_vp, _fp, C.c_int, C.c_int, C.POINTER(FitConfig), CHECKPOINT_FN, C.c_void_p,
+                          C.POINTER(EvalRecord), C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                          C.POINTER(C.c_int), C.c_char_p, C.c_size_t]),
     "igs_comm_unique_id": (C.c_int, [_u8p]),
     "igs_comm_init": (C.c_int, [_vp, _u8p, C.c_int, C.c_int]),
     "igs_comm_destroy": (C.c_int, [_vp]),
@@ -316,6 +340,58 @@ class Context:
         out = C.c_double(0)
         self._chk(self.lib.igs_psnr(self.h, _p(r, _fp), width, height, C.byref(out)))
         return out.value
+
+    def ssim(self, width: int, height: int, rendered=None) -> float:
+        r = None if rendered is None else np.ascontiguousarray(rendered, np.float32)
+        out = C.c_double(0)
+        self._chk(self.lib.igs_ssim(self.h, _p(r, _fp), width, height, C.byref(out)))
+        return out.value
+
+    def train_iteration_async(self, sample_idx, k: int = DEFAULT_K, lr=DEFAULT_LR, t: int = 1):
+        self._async_keep = np.ascontiguousarray(sample_idx, np.uint32)
+        lr = np.ascontiguousarray(lr, np.float64)
+        self._chk(self.lib.igs_train_iteration_async(self.h, _p(self._async_keep, _up), self._async_keep.shape[0],
+                                                     k, _p(lr, _dp), int(t)))
+
+    def train_wait(self) -> float:
+        loss = C.c_double(0)
+        self._chk(self.lib.igs_train_wait(self.h, C.byref(loss)))
+        return loss.value
+
+    # ---- encoder (fit.cpp) -----------------------------------------------------------------
+    @staticmethod
+    def fit_config(**overrides) -> FitConfig:
+        cfg = FitConfig()
+        load_library().igs_fit_config_default(C.byref(cfg))
+        for k, v in overrides.items():
+            if k == "lr":
+                for i, x in enumerate(v):
+                    cfg.lr[i] = x
+            else:
+                setattr(cfg, k, v)
+        return cfg
+
+    def fit(self, target, config: FitConfig, on_checkpoint=None, max_evals: int = 4096):
+        """fit() on the device; returns a dict like FitReport + the log text.
+        on_checkpoint(stage, iteration, id, params (n, 8)) mirrors CheckpointFn."""
+        target = np.ascontiguousarray(target, np.float32)
+        H, W, _ = target.shape
+
+        def _cb(user, stage, iteration, cid, p, n):
+            if on_checkpoint is not None:
+                arr = np.ctypeslib.as_array(p, shape=(n * 8,)).reshape(n, 8).copy() if n else np.zeros((0, 8))
+                on_checkpoint(stage, iteration, cid.decode(), arr)
+
+        cb = CHECKPOINT_FN(_cb)
+        evals = (EvalRecord * max_evals)()
+        n_evals = C.c_int(0); decay = C.c_int(-1); final = C.c_int(0)
+        log = C.create_string_buffer(1 << 20)
+        self._chk(self.lib.igs_fit(self.h, _p(target, _fp), W, H, C.byref(config), cb, None, evals, max_evals,
+                                   C.byref(n_evals), C.byref(decay), C.byref(final), log, len(log)))
+        recs = [dict(iteration=e.iteration, count=e.count, loss=e.loss, psnr=e.psnr, ssim=e.ssim,
+                     best_psnr=e.best_psnr) for e in evals[:n_evals.value]]
+        return {"evals": recs, "lr_decay_iteration": decay.value, "final_count": final.value,
+                "log": log.value.decode()}
 
     # ---- BSP ------------------------------------------------------------------------------
     def partition_build(self, n_max: int):
