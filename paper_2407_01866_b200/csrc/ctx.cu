@@ -516,7 +516,7 @@ int igs_set_target(igs_ctx* ctx, const float* rgb, int width, int height) {
 
 static int allreduce_grads(igs_ctx* ctx, double* dev_loss) {
 #ifndef IGS_NO_NCCL
-    if (ctx->comm && ctx->nranks > 1) {
+    if (ctx->comm) {  // a 1-rank communicator still runs (exercises the path on one GPU)
         if (nccl().allReduce(ctx->grads, ctx->grads, (size_t)ctx->n * 8, ncclDouble, ncclSum, ctx->comm, ctx->stream) !=
             ncclSuccess)
             return igs_fail(ctx, IGS_E_CUDA, "ncclAllReduce(grads) failed");

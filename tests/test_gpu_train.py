@@ -166,3 +166,26 @@ def test_frozen_selection_finite_differences(gctx, port):
             fd = (loss(pp) - loss(pm)) / (2 * h)
             an = grads[gi, prm]
             assert abs(an - fd) / max(abs(an), abs(fd), 1e-6) < 1e-4
+
+
+def test_nccl_single_rank_allreduce_path(gctx, port):
+    """The NCCL gradient/loss all-reduce inside the train step, with a 1-rank
+    communicator (one GPU per gpurun box): results must equal the no-comm
+    path exactly.  The multi-rank decomposition is covered on CPU by
+    tests/test_dist.py (gloo, world size 2)."""
+    from paper_2407_01866_b200 import Context
+    target = synth.photo_like_image(96, 64, 31021)
+    params = port.initialize_set(target, 500, 0.3, 21)
+    sidx = synth.sample_indices(3000, 96, 64, seed=22)[0]
+    gctx.set_params(params)
+    gctx.set_target(target)
+    l0, g0 = gctx.train_step(sidx, 10)
+    with Context(0) as c2:
+        c2.comm_init(Context.comm_unique_id(), 1, 0)
+        c2.set_params(params)
+        c2.set_target(target)
+        l1, g1 = c2.train_step(sidx, 10)
+        assert l1 == l0 and np.array_equal(g1, g0)
+        c2.train_iteration(sidx, 10, LR, 1)
+        gctx.train_iteration(sidx, 10, LR, 1)
+        assert np.array_equal(c2.get_params(), gctx.get_params())
