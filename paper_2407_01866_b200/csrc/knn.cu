@@ -463,11 +463,16 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
                                                             int kk, Epi E, unsigned long long* __restrict__ pairs,
                                                             uint32_t* __restrict__ hard_count,
                                                             uint32_t* __restrict__ hard_list,
-                                                            unsigned long long* __restrict__ hard_stat) {
+                                                            unsigned long long* __restrict__ hard_stat,
+                                                            uint32_t* __restrict__ next_point) {
     __shared__ uint32_t queue[4][2][kQueue];
     const int warp = threadIdx.x >> 5;
-    const uint32_t pt = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
+    // persistent warps: pull points until none are left (no wave tail)
+    for (;;) {
+    uint32_t pt = 0;
+    if (lane == 0) pt = atomicAdd(next_point, 1u);
+    pt = __shfl_sync(0xffffffffu, pt, 0);
     if (pt >= npts) return;  // warp-uniform
     double px, py;
     point_of(uv, E, W, H, pt, px, py);
@@ -567,7 +572,7 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
         slot = __shfl_sync(0xffffffffu, slot, 0);
         if (slot < kHardCap) {
             if (lane == 0) hard_list[slot] = pt;
-            return;
+            continue;
         }
         t.init(kk, lane);
         for (uint32_t base = 0; base < n; base += 32) {
@@ -590,6 +595,7 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
     }
     if (pairs && lane == 0) atomicAdd(pairs, evaluated);
     warp_epilogue(E, scan, pt, kk, lane, t.q, t.i, px, py);
+    }  // persistent loop
 }
 
 // Hard points (frontier overflow) are resolved by an exact split scan:
@@ -711,6 +717,7 @@ __global__ void __launch_bounds__(128) hard_merge_kernel(const ScanRec* __restri
 
 struct KnnBufs {
     DevBuf cnt, off, key, mem, own, sub, cub_tmp, hard, ticket, part, lcount;
+    int knn_blocks = 0;  // resident CTAs for the persistent query kernel
     uint64_t version = ~0ull;
     Lq lq{};
 };
@@ -788,16 +795,22 @@ int knn_build(igs_ctx* ctx) {
 template <int KCAP>
 int launch_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int kk, const Epi& E) {
     KnnBufs& b = *static_cast<KnnBufs*>(ctx->knn);
-    if (!grow(b.hard, (kHardCap + 1) * 4)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
-    uint32_t* hard_count = (uint32_t*)b.hard.p;
-    uint32_t* hard_list = hard_count + 1;
+    if (!grow(b.hard, (2 * kHardCap + 2) * 4)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
+    uint32_t* hard_count = (uint32_t*)b.hard.p;  // [0] hard-point count, [1] point cursor, [2..] list
+    uint32_t* cursor = hard_count + 1;
+    uint32_t* hard_list = hard_count + 2;
     igs_prof_begin(ctx, IGS_PROF_SCAN);
-    IGS_CUDA(ctx, cudaMemsetAsync(hard_count, 0, 4, ctx->stream));
-    const uint64_t threads = (uint64_t)npts * 32;
-    knn_points_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, ctx->stream>>>(
+    IGS_CUDA(ctx, cudaMemsetAsync(hard_count, 0, 8, ctx->stream));  // hard count + point cursor
+    if (b.knn_blocks == 0) {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, knn_points_kernel, 128, 0);
+        b.knn_blocks = std::max(1, per_sm) * ctx->sm_count;
+    }
+    const unsigned blocks = (unsigned)std::min<uint64_t>(b.knn_blocks, ((uint64_t)npts + 3) / 4);
+    knn_points_kernel<<<blocks, 128, 0, ctx->stream>>>(
         ctx->scan, ctx->n, b.lq, (const Sum*)b.own.p, (const Sum*)b.sub.p, (const uint32_t*)b.off.p,
         (const uint32_t*)b.mem.p, uv, W, H, npts, kk, E, igs_prof_counter(ctx, IGS_PROF_SCAN), hard_count,
-        hard_list, igs_prof_counter(ctx, IGS_PROF_KNN_HARD));
+        hard_list, igs_prof_counter(ctx, IGS_PROF_KNN_HARD), cursor);
     IGS_LAUNCHED(ctx);
     const size_t pitems = (size_t)kHardCap * kHardSplit * kk;
     if (!grow(b.part, pitems * 12)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
