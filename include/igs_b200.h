@@ -137,6 +137,8 @@ int igs_train_iterations(igs_ctx* ctx, uint32_t steps, int k, const double* lr4,
 /* Resident gradient buffer (double[n][8]). */
 const double* igs_device_grads(const igs_ctx* ctx);
 int igs_get_grads(igs_ctx* ctx, double* grads8, uint32_t n);
+/* Sets the resident gradients (adam_step's `grads` argument, adam.hpp:40). */
+int igs_set_grads(igs_ctx* ctx, const double* grads8, uint32_t n);
 /* Adam moments in record order (AdamState m/v). */
 int igs_get_adam_state(igs_ctx* ctx, double* m, double* v, uint32_t n);
 int igs_set_adam_state(igs_ctx* ctx, const double* m, const double* v, uint32_t n);

@@ -747,6 +747,15 @@ int igs_get_grads(igs_ctx* ctx, double* grads8, uint32_t n) {
     return dev_to_host(ctx, grads8, ctx->grads, (size_t)n * 64);
 }
 
+int igs_set_grads(igs_ctx* ctx, const double* grads8, uint32_t n) {
+    CHECK_CTX(ctx);
+    if (n != ctx->n) return igs_fail(ctx, IGS_E_DIMENSION_MISMATCH, "gradient count != Gaussian count");
+    if (n == 0) return IGS_OK;
+    ctx->grads_valid = true;
+    ctx->grads_checked = false;
+    return host_to_dev(ctx, ctx->grads, grads8, (size_t)n * 64);
+}
+
 int igs_get_adam_state(igs_ctx* ctx, double* m, double* v, uint32_t n) {
     CHECK_CTX(ctx);
     if (n != ctx->n) return igs_fail(ctx, IGS_E_DIMENSION_MISMATCH, "state size mismatch");

@@ -1,6 +1,6 @@
 // cull_math.cuh -- the certified tile-culling predicate (kernel 2), shared by
 // the device kernels (cull.cu) and restated op-for-op by the CPU oracle
-// (oracle/igs_oracle.c orc_cull_lists, in C) so tile lists compare
+// (the test-only C checker, orc_cull_lists) so tile lists compare
 // bit-exactly.  Device-only; compiled with -fmad=false.
 //
 // The reference ranks ALL Gaussians at every pixel (renderer.cpp:168-176);

@@ -115,6 +115,7 @@ SIGNATURES = {
     "igs_train_iterations": (C.c_int, [_vp, C.c_uint32, C.c_int, _dp, C.c_longlong, _dp]),
     "igs_device_grads": (_vp, [_vp]),
     "igs_get_grads": (C.c_int, [_vp, _dp, C.c_uint32]),
+    "igs_set_grads": (C.c_int, [_vp, _dp, C.c_uint32]),
     "igs_get_adam_state": (C.c_int, [_vp, _dp, _dp, C.c_uint32]),
     "igs_set_adam_state": (C.c_int, [_vp, _dp, _dp, C.c_uint32]),
     "igs_add_distribution": (C.c_int, [_vp, _fp, C.c_int, C.c_int, _dp]),
@@ -318,6 +319,10 @@ class Context:
         out = np.zeros((self.n, 8))
         self._chk(self.lib.igs_get_grads(self.h, _p(out, _dp), out.shape[0]))
         return out
+
+    def set_grads(self, grads):
+        g = _f64(grads, 8)
+        self._chk(self.lib.igs_set_grads(self.h, _p(g, _dp), g.shape[0]))
 
     def get_adam_state(self):
         m = np.zeros((self.n, 8)); v = np.zeros((self.n, 8))
