@@ -99,12 +99,52 @@ __global__ void lq_count(const ScanRec* __restrict__ scan, uint32_t n, Lq L, uin
     if (l >= 0 && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(lcount + l, (unsigned)__popc(same));
 }
 
-__global__ void lq_fill(uint32_t n, const uint32_t* __restrict__ key, const uint32_t* __restrict__ off,
-                        uint32_t* __restrict__ cur, uint32_t* __restrict__ mem) {
+// Own-cell summaries are accumulated with order-preserving 64-bit atomics
+// while the members are scattered (no per-cell member loop): a double's bit
+// pattern, sign-flipped, orders like the double itself.
+struct Acc {
+    unsigned long long x0, y0, x1, y1, lmin, aniso;
+};
+
+__device__ __forceinline__ unsigned long long okey(double d) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double odec(unsigned long long k) {
+    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k));
+}
+
+// One launch clears everything a build accumulates into.
+__global__ void lq_clear(uint32_t cells, uint32_t* __restrict__ cnt2, Acc* __restrict__ acc,
+                         uint32_t* __restrict__ lcount) {
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += gridDim.x * blockDim.x) {
+        cnt2[c] = 0;
+        cnt2[cells + c] = 0;
+        acc[c] = Acc{okey(inf), okey(inf), okey(-inf), okey(-inf), okey(inf), okey(1.0)};
+        if (c < kMaxLv) lcount[c] = 0;
+    }
+}
+
+__global__ void lq_fill(const ScanRec* __restrict__ scan, uint32_t n, const uint32_t* __restrict__ key,
+                        const uint32_t* __restrict__ off, uint32_t* __restrict__ cur, uint32_t* __restrict__ mem,
+                        Acc* __restrict__ acc) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t k = key[i];
     mem[off[k] + atomicAdd(cur + k, 1u)] = i;
+    const ScanRec r = scan[i];
+    const double lo = fmin(r.inv_a, r.inv_b), hi = fmax(r.inv_a, r.inv_b);
+    double aniso = hi / lo;
+    if (!(lo > 0.0) || !isfinite(hi) || !isfinite(r.mu_x) || !isfinite(r.mu_y))
+        aniso = __longlong_as_double(0x7ff0000000000000LL);
+    Acc* a = acc + k;
+    atomicMin(&a->x0, okey(r.mu_x));
+    atomicMin(&a->y0, okey(r.mu_y));
+    atomicMax(&a->x1, okey(r.mu_x));
+    atomicMax(&a->y1, okey(r.mu_y));
+    atomicMin(&a->lmin, okey(lo));
+    atomicMax(&a->aniso, okey(aniso));
 }
 
 __device__ __forceinline__ Sum empty_sum() {
@@ -126,23 +166,18 @@ __device__ __forceinline__ void merge(Sum& a, const Sum& b) {
     a.count += b.count;
 }
 
-// Own summary of cell c: reduce its members.
-__device__ __forceinline__ Sum own_of(const ScanRec* __restrict__ scan, const uint32_t* __restrict__ cnt,
-                                      const uint32_t* __restrict__ off, const uint32_t* __restrict__ mem, uint32_t c) {
+// Own summary of cell c from its accumulator.
+__device__ __forceinline__ Sum own_of(const Acc* __restrict__ acc, const uint32_t* __restrict__ cnt, uint32_t c) {
     Sum s = empty_sum();
-    double aniso = 1.0;
-    const uint32_t o = off[c], m = cnt[c];
-    for (uint32_t j = 0; j < m; ++j) {
-        const ScanRec r = scan[mem[o + j]];
-        s.x0 = fmin(s.x0, r.mu_x); s.x1 = fmax(s.x1, r.mu_x);
-        s.y0 = fmin(s.y0, r.mu_y); s.y1 = fmax(s.y1, r.mu_y);
-        const double lo = fmin(r.inv_a, r.inv_b), hi = fmax(r.inv_a, r.inv_b);
-        s.lmin = fmin(s.lmin, lo);
-        aniso = fmax(aniso, hi / lo);
-        if (!(lo > 0.0) || !isfinite(hi) || !isfinite(r.mu_x) || !isfinite(r.mu_y))
-            aniso = __longlong_as_double(0x7ff0000000000000LL);
-    }
-    s.slack = slack_for(aniso);
+    const uint32_t m = cnt[c];
+    if (m == 0) return s;
+    const Acc a = acc[c];
+    s.x0 = odec(a.x0);
+    s.y0 = odec(a.y0);
+    s.x1 = odec(a.x1);
+    s.y1 = odec(a.y1);
+    s.lmin = odec(a.lmin);
+    s.slack = slack_for(odec(a.aniso));
     s.count = m;
     return s;
 }
@@ -153,10 +188,8 @@ __device__ __forceinline__ Sum own_of(const ScanRec* __restrict__ scan, const ui
 // ticket after a fence) builds the levels above from global memory.
 constexpr int kBlk = 16;
 
-__global__ void __launch_bounds__(256) lq_tree_kernel(const ScanRec* __restrict__ scan, Lq L,
-                                                      const uint32_t* __restrict__ cnt,
-                                                      const uint32_t* __restrict__ off,
-                                                      const uint32_t* __restrict__ mem, Sum* __restrict__ own,
+__global__ void __launch_bounds__(256) lq_tree_kernel(const Acc* __restrict__ acc, Lq L,
+                                                      const uint32_t* __restrict__ cnt, Sum* __restrict__ own,
                                                       Sum* __restrict__ sub, unsigned int* __restrict__ ticket) {
     __shared__ Sum sm[2][kBlk * kBlk];
     const int t = threadIdx.x;
@@ -172,7 +205,7 @@ __global__ void __launch_bounds__(256) lq_tree_kernel(const ScanRec* __restrict_
             Sum s = empty_sum();
             if (x < G && y < G) {
                 const uint32_t c = (uint32_t)(L.loff[l] + y * G + x);
-                const Sum o = own_of(scan, cnt, off, mem, c);
+                const Sum o = own_of(acc, cnt, c);
                 own[c] = o;
                 s = o;
                 if (l > 0) {
@@ -200,7 +233,7 @@ __global__ void __launch_bounds__(256) lq_tree_kernel(const ScanRec* __restrict_
         for (int i = t; i < G * G; i += 256) {
             const int x = i % G, y = i / G;
             const uint32_t c = (uint32_t)(L.loff[l] + i);
-            Sum s = own_of(scan, cnt, off, mem, c);
+            Sum s = own_of(acc, cnt, c);
             own[c] = s;
             for (int dy = 0; dy < 2; ++dy)
                 for (int dx = 0; dx < 2; ++dx) {
@@ -716,7 +749,7 @@ __global__ void __launch_bounds__(128) hard_merge_kernel(const ScanRec* __restri
 }
 
 struct KnnBufs {
-    DevBuf cnt, off, key, mem, own, sub, cub_tmp, hard, ticket, part, lcount;
+    DevBuf cnt, off, key, mem, own, sub, cub_tmp, hard, ticket, part, lcount, acc;
     int knn_blocks = 0;  // resident CTAs for the persistent query kernel
     uint64_t version = ~0ull;
     Lq lq{};
@@ -764,14 +797,15 @@ int knn_build(igs_ctx* ctx) {
         if (!grow(b.ticket, 16)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
         IGS_CUDA(ctx, cudaMemsetAsync(b.ticket.p, 0, 16, ctx->stream));
     }
-    if (!grow(b.lcount, kMaxLv * 4)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
+    if (!grow(b.lcount, kMaxLv * 4) || !grow(b.acc, (size_t)cells * sizeof(Acc)))
+        return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
     L.lcount = (const uint32_t*)b.lcount.p;
-    IGS_CUDA(ctx, cudaMemsetAsync(b.lcount.p, 0, kMaxLv * 4, ctx->stream));
     uint32_t* cnt = (uint32_t*)b.cnt.p;
     uint32_t* cur = cnt + cells;
     uint32_t* off = (uint32_t*)b.off.p;
     igs_prof_begin(ctx, IGS_PROF_CULL);
-    IGS_CUDA(ctx, cudaMemsetAsync(cnt, 0, (size_t)cells * 8, ctx->stream));
+    lq_clear<<<2 * ctx->sm_count, 256, 0, ctx->stream>>>(cells, cnt, (Acc*)b.acc.p, (uint32_t*)b.lcount.p);
+    IGS_LAUNCHED(ctx);
     lq_count<<<(n + 255) / 256, 256, 0, ctx->stream>>>(ctx->scan, n, L, cnt, (uint32_t*)b.key.p,
                                                        (uint32_t*)b.lcount.p);
     IGS_LAUNCHED(ctx);
@@ -780,11 +814,12 @@ int knn_build(igs_ctx* ctx) {
     if (!grow(b.cub_tmp, tb)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn scan)");
     IGS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(b.cub_tmp.p, tb, cnt, off, (int)cells, ctx->stream));
     ctx->launches += 2;
-    lq_fill<<<(n + 255) / 256, 256, 0, ctx->stream>>>(n, (const uint32_t*)b.key.p, off, cur, (uint32_t*)b.mem.p);
+    lq_fill<<<(n + 255) / 256, 256, 0, ctx->stream>>>(ctx->scan, n, (const uint32_t*)b.key.p, off, cur,
+                                                      (uint32_t*)b.mem.p, (Acc*)b.acc.p);
     IGS_LAUNCHED(ctx);
     const int nb = (G0 + kBlk - 1) / kBlk;
-    lq_tree_kernel<<<nb * nb, 256, 0, ctx->stream>>>(ctx->scan, L, cnt, off, (const uint32_t*)b.mem.p,
-                                                     (Sum*)b.own.p, (Sum*)b.sub.p, (unsigned int*)b.ticket.p);
+    lq_tree_kernel<<<nb * nb, 256, 0, ctx->stream>>>((const Acc*)b.acc.p, L, cnt, (Sum*)b.own.p, (Sum*)b.sub.p,
+                                                     (unsigned int*)b.ticket.p);
     IGS_LAUNCHED(ctx);
     igs_prof_end(ctx, IGS_PROF_CULL, 0.0);
     b.lq = L;
@@ -842,7 +877,7 @@ void igs_knn_free(igs_ctx* ctx) {
     if (!ctx->knn) return;
     KnnBufs* b = static_cast<KnnBufs*>(ctx->knn);
     for (DevBuf* d : {&b->cnt, &b->off, &b->key, &b->mem, &b->own, &b->sub, &b->cub_tmp, &b->hard, &b->ticket,
-                      &b->part, &b->lcount})
+                      &b->part, &b->lcount, &b->acc})
         cudaFree(d->p);
     delete b;
     ctx->knn = nullptr;
