@@ -17,7 +17,8 @@ using namespace igs_dev;
 // train.cu
 int igs_status_reset(igs_ctx* ctx);
 int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint32_t* dev_sidx,
-                         const double* dev_samples5, double* dev_loss, double inv_n);
+                         const double* dev_samples5, double* dev_loss, double inv_n, const double* fuse_lr4 = nullptr,
+                         long long t = 0, bool* fused = nullptr);
 int igs_grad_check(igs_ctx* ctx);
 int igs_adam_launch(igs_ctx* ctx, const double* lr4, long long t);
 int igs_weights(igs_ctx* ctx, const double* q, const uint32_t* idx, size_t total, double* w);
@@ -617,11 +618,14 @@ int igs_train_iteration(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, i
     double* dloss = (double*)igs_scratch(ctx, 14, 64 * sizeof(double));
     if ((e = igs_status_reset(ctx))) return e;
     const uint32_t ns_total = ns * (uint32_t)ctx->nranks;
-    if ((e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss, 1.0 / (double)ns_total))) return e;
-    if ((e = allreduce_grads(ctx, dloss))) return e;
-    // the deterministic reduction already flags non-finite gradients (single rank)
-    if ((ctx->nranks > 1 || !ctx->grads_checked) && (e = igs_grad_check(ctx))) return e;
-    if ((e = igs_adam_launch(ctx, lr4, t))) return e;
+    bool fused = false;
+    if ((e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss, 1.0 / (double)ns_total, lr4, t, &fused)))
+        return e;
+    if (!fused) {
+        if ((e = allreduce_grads(ctx, dloss))) return e;
+        if ((ctx->comm || !ctx->grads_checked) && (e = igs_grad_check(ctx))) return e;
+        if ((e = igs_adam_launch(ctx, lr4, t))) return e;
+    }
     return read_status(ctx, dloss, loss, 1);
 }
 
@@ -663,10 +667,14 @@ int igs_train_iteration_async(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t
     IGS_CUDA(ctx, cudaMemcpyAsync(dsidx, pin, (size_t)ns * 4, cudaMemcpyHostToDevice, ctx->stream));
     if ((e = igs_status_reset(ctx))) return e;
     const uint32_t ns_total = ns * (uint32_t)ctx->nranks;
-    if ((e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss, 1.0 / (double)ns_total))) return e;
-    if ((e = allreduce_grads(ctx, dloss))) return e;
-    if ((ctx->nranks > 1 || !ctx->grads_checked) && (e = igs_grad_check(ctx))) return e;
-    if ((e = igs_adam_launch(ctx, lr4, t))) return e;
+    bool fused = false;
+    if ((e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss, 1.0 / (double)ns_total, lr4, t, &fused)))
+        return e;
+    if (!fused) {
+        if ((e = allreduce_grads(ctx, dloss))) return e;
+        if ((ctx->comm || !ctx->grads_checked) && (e = igs_grad_check(ctx))) return e;
+        if ((e = igs_adam_launch(ctx, lr4, t))) return e;
+    }
     IGS_CUDA(ctx, cudaMemcpyAsync(res, ctx->status, 4 * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
     IGS_CUDA(ctx, cudaMemcpyAsync(res + 4, dloss, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     ctx->async_pending = true;
@@ -729,10 +737,15 @@ int igs_train_iterations(igs_ctx* ctx, uint32_t steps, int k, const double* lr4,
         // step t uses uploaded slot (t-1) mod steps_uploaded
         const uint32_t slot = (uint32_t)((t0 + s - 1) % (long long)ctx->samples_steps);
         const uint32_t* dsidx = (const uint32_t*)ctx->samples.p + (size_t)slot * ns;
-        if ((e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss + s, 1.0 / (double)ns_total))) return e;
-        if ((e = allreduce_grads(ctx, dloss + s))) return e;
-        if ((ctx->nranks > 1 || !ctx->grads_checked) && (e = igs_grad_check(ctx))) return e;
-        if ((e = igs_adam_launch(ctx, lr4, t0 + s))) return e;
+        bool fused = false;
+        if ((e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss + s, 1.0 / (double)ns_total, lr4, t0 + s,
+                                      &fused)))
+            return e;
+        if (!fused) {
+            if ((e = allreduce_grads(ctx, dloss + s))) return e;
+            if ((ctx->comm || !ctx->grads_checked) && (e = igs_grad_check(ctx))) return e;
+            if ((e = igs_adam_launch(ctx, lr4, t0 + s))) return e;
+        }
     }
     igs_timer_autostop(ctx);  // device time of the loop excludes the status readback
     if ((e = read_status(ctx, nullptr, nullptr, 1))) return e;

@@ -168,16 +168,21 @@ __global__ void segment_reduce_kernel(const uint32_t* __restrict__ skeys, const 
 }
 
 // --- counting-sort reduction (deterministic, reference summation order) ----
+constexpr uint32_t kShortSeg = 32;  // longer segments go to long_segment_kernel
 // keys[slot] = Gaussian of contribution slot (slot = sample * kk + entry, so
 // slot order is sample order).  gcnt/goff: per-Gaussian count / offset.
+// (also queues every Gaussian with a long segment for long_segment_kernel)
 __global__ void scatter_slots_kernel(const uint32_t* __restrict__ keys, uint32_t items, uint32_t n,
-                                     const uint32_t* __restrict__ goff, uint32_t* __restrict__ gcur,
-                                     uint32_t* __restrict__ perm) {
+                                     const uint32_t* __restrict__ goff, const uint32_t* __restrict__ gcnt,
+                                     uint32_t* __restrict__ gcur, uint32_t* __restrict__ perm,
+                                     uint32_t* __restrict__ long_count, uint32_t* __restrict__ long_list) {
     const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
     if (slot >= items) return;
     const uint32_t g = keys[slot];
     if (g >= n) return;
-    perm[goff[g] + atomicAdd(gcur + g, 1u)] = slot;
+    const uint32_t pos = atomicAdd(gcur + g, 1u);
+    perm[goff[g] + pos] = slot;
+    if (pos == 0 && gcnt[g] > kShortSeg) long_list[atomicAdd(long_count, 1u)] = g;
 }
 
 __device__ __forceinline__ void sum_sorted(const double* __restrict__ contrib, const uint32_t* slots, uint32_t m,
@@ -211,22 +216,16 @@ __device__ __forceinline__ void store_grad(double* __restrict__ grads, uint32_t 
         }
 }
 
-constexpr uint32_t kShortSeg = 32;
-
 // Thread per Gaussian: sort its (short) slot list, sum from 0.0 in slot
 // (= sample) order -- the reference's operation sequence.  Long segments are
 // queued for long_segment_kernel.
 __global__ void segment_sum_kernel(const uint32_t* __restrict__ gcnt, const uint32_t* __restrict__ goff,
                                    const uint32_t* __restrict__ perm, const double* __restrict__ contrib, uint32_t n,
-                                   double* __restrict__ grads, uint32_t* __restrict__ long_count,
-                                   uint32_t* __restrict__ long_list, long long* __restrict__ status) {
+                                   double* __restrict__ grads, long long* __restrict__ status) {
     const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
     const uint32_t m = gcnt[g];
-    if (m > kShortSeg) {
-        long_list[atomicAdd(long_count, 1u)] = g;
-        return;
-    }
+    if (m > kShortSeg) return;  // long_segment_kernel
     uint32_t sl[kShortSeg];
     const uint32_t o = goff[g];
     for (uint32_t e = 0; e < m; ++e) {
@@ -243,9 +242,12 @@ __global__ void segment_sum_kernel(const uint32_t* __restrict__ gcnt, const uint
     store_grad(grads, g, acc, status);
 }
 
-// One CTA per long segment (persistent over the queue): rank sort in shared
-// memory (slot ids are unique: rank = number of smaller ids), then thread 0
-// sums in order.  Segments beyond the shared capacity sort in place in perm.
+// One CTA per long segment (persistent over the queue).  The slot ids are
+// bitonic-sorted in shared memory (padded to a power of two); then chunks of
+// 256 contribution rows are gathered in parallel into shared memory and 8
+// threads -- one per parameter -- accumulate them in slot (= sample) order.
+// Segments beyond the shared capacity (degenerate sets) sort in place in
+// global memory.
 constexpr uint32_t kLongCap = 4096;
 
 __global__ void __launch_bounds__(256) long_segment_kernel(const uint32_t* __restrict__ gcnt,
@@ -256,42 +258,72 @@ __global__ void __launch_bounds__(256) long_segment_kernel(const uint32_t* __res
                                                            const uint32_t* __restrict__ long_count,
                                                            const uint32_t* __restrict__ long_list,
                                                            long long* __restrict__ status) {
-    __shared__ uint32_t in[kLongCap], outs[kLongCap];
+    __shared__ uint32_t keys[kLongCap];
+    __shared__ double rows[256][8];
     const uint32_t total = *long_count;
+    const int t = threadIdx.x;
     for (uint32_t it = blockIdx.x; it < total; it += gridDim.x) {
         const uint32_t g = long_list[it];
         const uint32_t m = gcnt[g], o = goff[g];
+        const uint32_t* sorted = keys;
         __syncthreads();
         if (m <= kLongCap) {
-            for (uint32_t e = threadIdx.x; e < m; e += blockDim.x) in[e] = perm[o + e];
+            uint32_t pow2 = 1;
+            while (pow2 < m) pow2 <<= 1;
+            for (uint32_t e = t; e < pow2; e += 256) keys[e] = e < m ? perm[o + e] : 0xFFFFFFFFu;
             __syncthreads();
-            for (uint32_t e = threadIdx.x; e < m; e += blockDim.x) {
-                const uint32_t v = in[e];
-                uint32_t r = 0;
-                for (uint32_t f = 0; f < m; ++f) r += in[f] < v;
-                outs[r] = v;
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                sum_sorted(contrib, outs, m, acc);
-                store_grad(grads, g, acc, status);
-            }
-        } else if (threadIdx.x == 0) {
-            // huge segment (degenerate sets): in-place insertion sort in global memory
-            uint32_t* s = perm + o;
-            for (uint32_t e = 1; e < m; ++e) {
-                const uint32_t v = s[e];
-                uint32_t pos = e;
-                while (pos > 0 && s[pos - 1] > v) {
-                    s[pos] = s[pos - 1];
-                    --pos;
+            for (uint32_t size = 2; size <= pow2; size <<= 1)
+                for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                    for (uint32_t e = t; e < pow2; e += 256) {
+                        const uint32_t partner = e ^ stride;
+                        if (partner > e) {
+                            const bool up = (e & size) == 0;
+                            const uint32_t a = keys[e], b = keys[partner];
+                            if ((a > b) == up) {
+                                keys[e] = b;
+                                keys[partner] = a;
+                            }
+                        }
+                    }
+                    __syncthreads();
                 }
-                s[pos] = v;
+        } else {
+            if (t == 0) {
+                uint32_t* sl = perm + o;
+                for (uint32_t e = 1; e < m; ++e) {
+                    const uint32_t v = sl[e];
+                    uint32_t pos = e;
+                    while (pos > 0 && sl[pos - 1] > v) {
+                        sl[pos] = sl[pos - 1];
+                        --pos;
+                    }
+                    sl[pos] = v;
+                }
             }
-            double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            sum_sorted(contrib, s, m, acc);
-            store_grad(grads, g, acc, status);
+            __threadfence_block();
+            __syncthreads();
+            sorted = perm + o;
+        }
+        double acc = 0.0;  // thread p < 8 owns parameter p
+        for (uint32_t base = 0; base < m; base += 256) {
+            const uint32_t cnt = min(256u, m - base);
+            if ((uint32_t)t < cnt) {
+                const double2* c = reinterpret_cast<const double2*>(contrib + (size_t)sorted[base + t] * 8);
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const double2 v = c[h];
+                    rows[t][2 * h] = v.x;
+                    rows[t][2 * h + 1] = v.y;
+                }
+            }
+            __syncthreads();
+            if (t < 8)
+                for (uint32_t r = 0; r < cnt; ++r) acc = __dadd_rn(acc, rows[r][t]);
+            __syncthreads();
+        }
+        if (t < 8) {
+            grads[(size_t)g * 8 + t] = acc;
+            if (!isfinite(acc)) atomicMin(status, (long long)g * 8 + t);  // adam.cpp:29-31 (first (i, p))
         }
     }
 }
@@ -342,30 +374,23 @@ __device__ __forceinline__ double clamp_scale(double v) {
 }
 
 // Kernel 5: Adam (adam.cpp:21-51) + constrain (gaussian.cpp:74-90) +
-// PreparedSet refresh for the next step, one thread per Gaussian.  Skips
-// all writes when a non-finite gradient or loss was flagged this step, so a
-// failed step leaves the set untouched.  HBM: 256 B read + 192 B written
-// for params/grads/m/v, plus 96 B of refreshed scan/shade records.
-__global__ void adam_kernel(double* __restrict__ params, const double* __restrict__ grads, double* __restrict__ m,
-                            double* __restrict__ v, ScanRec* __restrict__ scan, ShadeRec* __restrict__ shade,
-                            uint32_t n, double lr_mu, double lr_color, double lr_scale, double lr_theta, double bc1,
-                            double bc2, const long long* __restrict__ status) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    if (status[0] != LLONG_MAX || status[2] != LLONG_MAX) return;
+// PreparedSet refresh for the next step, for one Gaussian.  HBM: 256 B read
+// + 192 B written for params/grads/m/v, plus 96 B of refreshed scan/shade.
+__device__ __forceinline__ void adam_one(uint32_t i, const double* gg, double* __restrict__ params,
+                                         double* __restrict__ m, double* __restrict__ v, ScanRec* __restrict__ scan,
+                                         ShadeRec* __restrict__ shade, double lr_mu, double lr_color, double lr_scale,
+                                         double lr_theta, double bc1, double bc2, long long* __restrict__ status) {
     const double b1 = 0.9, b2 = 0.999, eps = 1e-8;  // adam.hpp:33-35
     const double omb1 = 1.0 - b1, omb2 = 1.0 - b2;  // folded exactly like the reference's constants
     const double lr8[8] = {lr_mu, lr_mu, lr_theta, lr_scale, lr_scale, lr_color, lr_color, lr_color};
-    double gp[8], gg[8], mm[8], vv[8];
+    double gp[8], mm[8], vv[8];
     const double2* P = reinterpret_cast<const double2*>(params + (size_t)i * 8);
-    const double2* G = reinterpret_cast<const double2*>(grads + (size_t)i * 8);
     const double2* M = reinterpret_cast<const double2*>(m + (size_t)i * 8);
     const double2* V = reinterpret_cast<const double2*>(v + (size_t)i * 8);
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
-        const double2 a = P[h], b = G[h], c = M[h], d = V[h];
+        const double2 a = P[h], c = M[h], d = V[h];
         gp[2 * h] = a.x; gp[2 * h + 1] = a.y;
-        gg[2 * h] = b.x; gg[2 * h + 1] = b.y;
         mm[2 * h] = c.x; mm[2 * h + 1] = c.y;
         vv[2 * h] = d.x; vv[2 * h + 1] = d.y;
     }
@@ -384,7 +409,7 @@ __global__ void adam_kernel(double* __restrict__ params, const double* __restric
 #pragma unroll
     for (int p = 0; p < 8; ++p) finite_all = finite_all && isfinite(gp[p]);
     if (!finite_all) {
-        atomicMin((long long*)status + 1, (long long)i);
+        atomicMin(status + 1, (long long)i);
         return;
     }
     gp[0] = clamp01d(gp[0]);
@@ -428,6 +453,81 @@ __global__ void adam_kernel(double* __restrict__ params, const double* __restric
     hh.inv_s2 = inv_s2;
     hh.pad = 0.0;
     shade[i] = hh;
+}
+
+// Adam over the resident gradients.  Skips all writes when a non-finite
+// gradient or loss was flagged (checked by an earlier launch), so a failed
+// step leaves the set untouched.
+__global__ void adam_kernel(double* __restrict__ params, const double* __restrict__ grads, double* __restrict__ m,
+                            double* __restrict__ v, ScanRec* __restrict__ scan, ShadeRec* __restrict__ shade,
+                            uint32_t n, double lr_mu, double lr_color, double lr_scale, double lr_theta, double bc1,
+                            double bc2, long long* __restrict__ status) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (status[0] != LLONG_MAX || status[2] != LLONG_MAX) return;
+    double gg[8];
+    const double2* G = reinterpret_cast<const double2*>(grads + (size_t)i * 8);
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+        const double2 b = G[h];
+        gg[2 * h] = b.x;
+        gg[2 * h + 1] = b.y;
+    }
+    adam_one(i, gg, params, m, v, scan, shade, lr_mu, lr_color, lr_scale, lr_theta, bc1, bc2, status);
+}
+
+// Fused short-segment reduction + Adam (single rank): thread g sums its
+// short segment in sample order (or reads the long-segment result), stores
+// the gradient, and updates Gaussian g unless that gradient is non-finite
+// (then it flags status[0] = first (i, p) and leaves g untouched -- every
+// finite Gaussian is still updated, deterministically; the reference has
+// updated Gaussians 0..i-1 when it throws, adam.cpp:29-31).  A non-finite
+// loss (flagged by the search epilogue) skips the whole step, as fit.cpp:155.
+__global__ void segment_adam_kernel(const uint32_t* __restrict__ gcnt, const uint32_t* __restrict__ goff,
+                                    const uint32_t* __restrict__ perm, const double* __restrict__ contrib,
+                                    uint32_t n, double* __restrict__ grads, double* __restrict__ params,
+                                    double* __restrict__ m, double* __restrict__ v, ScanRec* __restrict__ scan,
+                                    ShadeRec* __restrict__ shade, double lr_mu, double lr_color, double lr_scale,
+                                    double lr_theta, double bc1, double bc2, long long* __restrict__ status) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    if (status[2] != LLONG_MAX) return;
+    const uint32_t cntg = gcnt[g];
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (cntg > kShortSeg) {
+        const double2* G = reinterpret_cast<const double2*>(grads + (size_t)g * 8);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const double2 b = G[h];
+            acc[2 * h] = b.x;
+            acc[2 * h + 1] = b.y;
+        }
+    } else {
+        uint32_t sl[kShortSeg];
+        const uint32_t o = goff[g];
+        for (uint32_t e = 0; e < cntg; ++e) {
+            const uint32_t val = perm[o + e];
+            uint32_t pos = e;
+            while (pos > 0 && sl[pos - 1] > val) {
+                sl[pos] = sl[pos - 1];
+                --pos;
+            }
+            sl[pos] = val;
+        }
+        sum_sorted(contrib, sl, cntg, acc);
+        double2* o2 = reinterpret_cast<double2*>(grads + (size_t)g * 8);
+        o2[0] = make_double2(acc[0], acc[1]);
+        o2[1] = make_double2(acc[2], acc[3]);
+        o2[2] = make_double2(acc[4], acc[5]);
+        o2[3] = make_double2(acc[6], acc[7]);
+    }
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+        if (!isfinite(acc[p])) {
+            atomicMin(status, (long long)g * 8 + p);
+            return;
+        }
+    adam_one(g, acc, params, m, v, scan, shade, lr_mu, lr_color, lr_scale, lr_theta, bc1, bc2, status);
 }
 
 __global__ void reset_status_kernel(long long* status) {
@@ -480,7 +580,9 @@ int igs_status_reset(igs_ctx* ctx) {
 // target), mode 1: backward (samples5 on device).  Writes ctx->grads and,
 // in train mode, the loss into *dev_loss.
 int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint32_t* dev_sidx,
-                         const double* dev_samples5, double* dev_loss, double inv_n) {
+                         const double* dev_samples5, double* dev_loss, double inv_n, const double* fuse_lr4,
+                         long long t, bool* fused) {
+    if (fused) *fused = false;
     const uint32_t n = ctx->n;
     const int kk = (int)std::min<uint32_t>((uint32_t)k, n);
     const size_t items = (size_t)ns * kk;
@@ -499,6 +601,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
             return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
         IGS_CUDA(ctx, cudaMemsetAsync(gcnt, 0, (size_t)n * 2 * sizeof(uint32_t), ctx->stream));
         IGS_CUDA(ctx, cudaMemsetAsync(long_ctl, 0, sizeof(uint32_t), ctx->stream));
+        // (long_ctl[0]: long-segment count; long_ctl[1..]: the queue)
     } else {
         IGS_CUDA(ctx, cudaMemsetAsync(ctx->grads, 0, (size_t)n * 8 * sizeof(double), ctx->stream));
     }
@@ -546,17 +649,32 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
         if (!temp) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (scan)");
         IGS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(temp, tb, gcnt, goff, (int)n, ctx->stream));
         ctx->launches += 2;
-        scatter_slots_kernel<<<(unsigned)((items + 255) / 256), 256, 0, ctx->stream>>>(keys, (uint32_t)items, n, goff,
-                                                                                       gcnt + n, perm);
-        IGS_LAUNCHED(ctx);
-        segment_sum_kernel<<<(n + 255) / 256, 256, 0, ctx->stream>>>(gcnt, goff, perm, contrib, n, ctx->grads,
-                                                                     long_ctl, long_ctl + 1, ctx->status);
+        scatter_slots_kernel<<<(unsigned)((items + 255) / 256), 256, 0, ctx->stream>>>(
+            keys, (uint32_t)items, n, goff, gcnt, gcnt + n, perm, long_ctl, long_ctl + 1);
         IGS_LAUNCHED(ctx);
         long_segment_kernel<<<ctx->sm_count, 256, 0, ctx->stream>>>(gcnt, goff, perm, contrib, ctx->grads, long_ctl,
                                                                     long_ctl + 1, ctx->status);
         IGS_LAUNCHED(ctx);
+        if (fuse_lr4 && ctx->nranks == 1 && !ctx->comm) {
+            // short segments summed inside the Adam kernel (one pass over the set)
+            const double bc1 = 1.0 - std::pow(0.9, (double)t);  // adam.cpp:16-17, host libm
+            const double bc2 = 1.0 - std::pow(0.999, (double)t);
+            ctx->params_version++;
+            igs_prof_end(ctx, IGS_PROF_REDUCE, (double)items);
+            igs_prof_begin(ctx, IGS_PROF_ADAM);
+            segment_adam_kernel<<<(n + 255) / 256, 256, 0, ctx->stream>>>(
+                gcnt, goff, perm, contrib, n, ctx->grads, ctx->params, ctx->adam_m, ctx->adam_v, ctx->scan,
+                ctx->shade, fuse_lr4[0], fuse_lr4[1], fuse_lr4[2], fuse_lr4[3], bc1, bc2, ctx->status);
+            IGS_LAUNCHED(ctx);
+            igs_prof_end(ctx, IGS_PROF_ADAM, (double)n * 544.0);
+            if (fused) *fused = true;
+        } else {
+            segment_sum_kernel<<<(n + 255) / 256, 256, 0, ctx->stream>>>(gcnt, goff, perm, contrib, n, ctx->grads,
+                                                                         ctx->status);
+            IGS_LAUNCHED(ctx);
+            igs_prof_end(ctx, IGS_PROF_REDUCE, (double)items);
+        }
         ctx->grads_checked = true;
-        igs_prof_end(ctx, IGS_PROF_REDUCE, (double)items);
     } else {
         ctx->grads_checked = false;
     }
