@@ -283,18 +283,28 @@ struct WarpTopK {
     // warp-uniform (cq, ci); no effect unless it beats the threshold
     __device__ __forceinline__ void offer(double cq, uint32_t ci) {
         if (!beats(cq, ci)) return;
+        push(cq, ci);
+        refresh();
+    }
+    // insertion without the threshold broadcast: a candidate that beats no
+    // entry (ballot empty) is dropped, so a stale threshold only costs time;
+    // call refresh() before tq()/beats() are used again
+    __device__ __forceinline__ void push(double cq, uint32_t ci) {
         const bool gt = lane < kk && (cq < q || (cq == q && ci < i));
         const unsigned m = __ballot_sync(0xffffffffu, gt);
+        if (m == 0) return;  // warp-uniform
         const int pos = __ffs(m) - 1;
         const double pq = __shfl_up_sync(0xffffffffu, q, 1);
         const uint32_t pi = __shfl_up_sync(0xffffffffu, i, 1);
         if (lane == pos) {
             q = cq;
             i = ci;
-        } else if (lane > pos && lane < kk) {
+        } else if (lane > pos) {  // lanes >= kk never satisfy gt, so their ballot bit is clear
             q = pq;
             i = pi;
         }
+    }
+    __device__ __forceinline__ void refresh() {
         tq_ = __shfl_sync(0xffffffffu, q, kk - 1);
         ti = __shfl_sync(0xffffffffu, i, kk - 1);
     }
@@ -336,20 +346,19 @@ __device__ __forceinline__ void eval_members(TK& t, uint32_t o_mine, uint32_t m_
             cand = t.beats(q, gi);
         }
         unsigned msk = __ballot_sync(0xffffffffu, cand);
-        while (msk) {
-            const int src = __ffs(msk) - 1;
-            msk &= msk - 1;
-            const double qq = __shfl_sync(0xffffffffu, q, src);
-            const uint32_t ii = __shfl_sync(0xffffffffu, gi, src);
-            t.offer(qq, ii);
+        if (msk) {
+            do {
+                const int src = __ffs(msk) - 1;
+                msk &= msk - 1;
+                const double qq = __shfl_sync(0xffffffffu, q, src);
+                const uint32_t ii = __shfl_sync(0xffffffffu, gi, src);
+                t.push(qq, ii);
+            } while (msk);
+            t.refresh();
         }
     }
 }
 
-__device__ __forceinline__ bool in_seed(const Lq& L, int l, int x, int y, double px, double py) {
-    const int sx = cell_of(px, L.lw[l]), sy = cell_of(py, L.lw[l]);
-    return x >= sx - 1 && x <= sx + 1 && y >= sy - 1 && y <= sy + 1;
-}
 
 // One warp per point.
 constexpr uint32_t kHardCap = 256;
@@ -499,8 +508,23 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
                                                             unsigned long long* __restrict__ hard_stat,
                                                             uint32_t* __restrict__ next_point) {
     __shared__ uint32_t queue[4][2][kQueue];
+    __shared__ int s_loff[kMaxLv];  // level tables (a dynamic index into the
+    __shared__ int s_lg[kMaxLv];    // kernel parameters would go to local memory)
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int l = 0; l < kMaxLv; ++l) {
+            s_loff[l] = L.loff[l];
+            s_lg[l] = 31 - __clz(max(L.lw[l], 1));
+        }
+    }
+    __syncthreads();
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    // per-level population, one bit per level (same for every point)
+    unsigned lvmask = 0;
+    if (lane < L.levels && L.lcount[lane] > 0) lvmask = 1u;
+    lvmask = __ballot_sync(0xffffffffu, lvmask);
+    const int npop = __popc(lvmask);
     // persistent warps: pull points until none are left (no wave tail)
     for (;;) {
     uint32_t pt = 0;
@@ -514,10 +538,6 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
     unsigned long long evaluated = 0;
 
     // (1) seeds: own members of the 3x3 window at every populated level
-    unsigned lvmask = 0;
-    if (lane < L.levels && L.lcount[lane] > 0) lvmask = 1u;
-    lvmask = __ballot_sync(0xffffffffu, lvmask);
-    const int npop = __popc(lvmask);
     const int nseed = npop * 9;
     for (int base = 0; base < nseed; base += 32) {
         const int it = base + lane;
@@ -526,10 +546,10 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
             // it-th populated level
             unsigned mm = lvmask;
             for (int skip = it / 9; skip > 0; --skip) mm &= mm - 1;
-            const int l = __ffs(mm) - 1, d = it % 9, G = L.lw[l];
+            const int l = __ffs(mm) - 1, d = it % 9, lg = s_lg[l], G = 1 << lg;
             const int x = cell_of(px, G) + d % 3 - 1, y = cell_of(py, G) + d / 3 - 1;
             if (x >= 0 && x < G && y >= 0 && y < G) {
-                const uint32_t c = (uint32_t)(L.loff[l] + y * G + x);
+                const uint32_t c = (uint32_t)(s_loff[l] + (y << lg) + x);
                 o = off[c];
                 m = own[c].count;
             }
@@ -539,22 +559,26 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
 
     bool overflow = false;
     // (2) descent: evaluate own members of frontier nodes, expand children
+    // (G_l = G0 >> l is a power of two, so the child grid is exactly 2x)
     uint32_t* cur = queue[warp][0];
     uint32_t* nxt = queue[warp][1];
     int ncur = 1;
     if (lane == 0) cur[0] = 0;  // root cell of the top level
     __syncwarp();
     for (int l = L.levels - 1; l >= 0 && ncur > 0; --l) {
-        const int w = L.lw[l];
+        const int lg = s_lg[l];
+        const int wmask = (1 << lg) - 1;
+        const int sx = cell_of(px, 1 << lg), sy = cell_of(py, 1 << lg);  // seed window centre
+        const uint32_t lo = (uint32_t)s_loff[l];
         // own members of the frontier (outside the seed window)
         for (int base = 0; base < ncur; base += 32) {
             const int i = base + lane;
             uint32_t o = 0, m = 0;
             if (i < ncur) {
                 const uint32_t node = cur[i];
-                const int x = node % w, y = node / w;
-                const uint32_t c = (uint32_t)L.loff[l] + node;
-                if (!in_seed(L, l, x, y, px, py)) {
+                const int x = (int)node & wmask, y = (int)(node >> lg);
+                if (abs(x - sx) > 1 || abs(y - sy) > 1) {
+                    const uint32_t c = lo + node;
                     const Sum so = own[c];
                     if (so.count && sum_lb(so, px, py) <= t.tq()) {
                         o = off[c];
@@ -565,7 +589,8 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
             eval_members(t, o, m, lane, scan, mem, px, py, evaluated);
         }
         if (l == 0) break;
-        const int cw = L.lw[l - 1];
+        const uint32_t clo = (uint32_t)s_loff[l - 1];
+        const int clg = lg + 1;
         int nnext = 0;
         for (int base = 0; base < ncur * 4; base += 32) {
             const int item = base + lane;
@@ -573,12 +598,9 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
             uint32_t child = 0;
             if (item < ncur * 4) {
                 const uint32_t node = cur[item >> 2];
-                const int x = node % w, y = node / w;
-                const int ccx = 2 * x + (item & 1), ccy = 2 * y + ((item >> 1) & 1);
-                if (ccx < cw && ccy < cw) {
-                    child = (uint32_t)(ccy * cw + ccx);
-                    keep = sum_lb(sub[L.loff[l - 1] + child], px, py) <= t.tq();
-                }
+                const uint32_t x = node & (uint32_t)wmask, y = node >> lg;
+                child = ((2 * y + ((item >> 1) & 1)) << clg) + 2 * x + (item & 1);
+                keep = sum_lb(sub[clo + child], px, py) <= t.tq();
             }
             const unsigned msk = __ballot_sync(0xffffffffu, keep);
             const int pos = nnext + __popc(msk & ((1u << lane) - 1));

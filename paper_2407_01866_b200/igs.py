@@ -28,11 +28,14 @@ extension raises, and every call runs on the GPU.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libigs_b200.so"
+# IGS_B200_LIB: an alternative build of the same library (kernel-tuning
+# experiments); it must exist -- there is no fallback.
+LIB_PATH = Path(os.environ.get("IGS_B200_LIB") or Path(__file__).resolve().parent / "libigs_b200.so")
 
 ERROR_KINDS = {
     1: "invalid_parameter",
