@@ -236,6 +236,9 @@ int igs_ctx_create(int device, igs_ctx** out) {
     ctx->device = device;
     cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
     if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
         cudaMalloc(&ctx->status, 4 * sizeof(long long)) != cudaSuccess) {
         delete ctx;
         return IGS_E_CUDA;
@@ -275,6 +278,10 @@ void igs_ctx_destroy(igs_ctx* ctx) {
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     for (auto& b : ctx->async_pin)
         if (b.p) cudaFreeHost(b.p);
+    cudaStreamSynchronize(ctx->side);
+    cudaEventDestroy(ctx->ev_fork);
+    cudaEventDestroy(ctx->ev_join);
+    cudaStreamDestroy(ctx->side);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -552,6 +559,7 @@ static int read_status(igs_ctx* ctx, double* dev_loss, double* loss_out, int che
     if ((e = dev_to_host(ctx, h.st, ctx->status, sizeof(h.st)))) return e;
     h.loss = 0.0;
     if (dev_loss && (e = dev_to_host(ctx, &h.loss, dev_loss, sizeof(double)))) return e;
+    ctx->knn_grown = h.st[3];
     if (h.st[2] != LLONG_MAX) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "training loss became non-finite");
     if (check_grads && h.st[0] != LLONG_MAX) {
         static const char* names[8] = {"mu_u", "mu_v", "theta", "s1", "s2", "r", "g", "b"};
@@ -688,6 +696,7 @@ int igs_train_wait(igs_ctx* ctx, double* loss) {
     ctx->async_pending = false;
     IGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     const long long* st = (const long long*)ctx->async_pin[1].p;
+    ctx->knn_grown = st[3];
     if (st[2] != LLONG_MAX) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "training loss became non-finite");
     if (st[0] != LLONG_MAX) {
         static const char* names[8] = {"mu_u", "mu_v", "theta", "s1", "s2", "r", "g", "b"};
@@ -737,6 +746,7 @@ int igs_train_iterations(igs_ctx* ctx, uint32_t steps, int k, const double* lr4,
         // step t uses uploaded slot (t-1) mod steps_uploaded
         const uint32_t slot = (uint32_t)((t0 + s - 1) % (long long)ctx->samples_steps);
         const uint32_t* dsidx = (const uint32_t*)ctx->samples.p + (size_t)slot * ns;
+        if (s > 0) ctx->knn_grown = -1;  // no read-back inside the device loop: re-bucket
         bool fused = false;
         if ((e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss + s, 1.0 / (double)ns_total, lr4, t0 + s,
                                       &fused)))

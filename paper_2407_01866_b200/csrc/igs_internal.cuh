@@ -151,6 +151,8 @@ struct PartitionDev;  // bsp.cu
 struct igs_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;                   // off-critical-path work (loss sum)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::string err;
     uint64_t launches = 0;
     int sm_count = 148;
@@ -198,6 +200,9 @@ struct igs_ctx {
     void* cull = nullptr;            // CullBufs (cull.cu)
     void* knn = nullptr;             // KnnBufs (knn.cu)
     uint64_t params_version = 0;     // bumped on every change of the set
+    long long knn_grown = -1;        // status[3] of the last step read back (-1: unknown)
+    const void* gcnt_clean = nullptr;  // deterministic-reduction counters left zeroed (for this n)
+    uint32_t gcnt_clean_n = 0;
 
     // profiling (igs_profile_*)
     bool prof_on = false;

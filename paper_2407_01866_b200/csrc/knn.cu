@@ -35,15 +35,25 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "igs_internal.cuh"
+#include "knn_tree.cuh"
 
 using namespace igs_dev;
 
 namespace {
 
-constexpr int kMaxLv = 13;
 constexpr int kQueue = 512;  // per-warp frontier capacity
+// Builds between full re-bucketings (in between, the summaries are refit
+// from the Adam kernels' accumulation; exact either way, only the tightness
+// of the bounds drifts as Gaussians move and change scale).
+constexpr int kRefitPeriod = 16;
+#ifndef IGS_GROW_SHIFT
+#define IGS_GROW_SHIFT 3
+#endif
+constexpr int kGrowShift = IGS_GROW_SHIFT;  // re-bucket when more than n >> kGrowShift Gaussians grew
 
 struct Sum {
     double x0, y0, x1, y1;  // centre bbox (empty: +inf/-inf)
@@ -52,35 +62,14 @@ struct Sum {
     uint32_t count;
 };
 
-struct Lq {
-    int G0, levels;
-    int lw[kMaxLv];    // cells per side
-    int loff[kMaxLv];  // first cell id of the level
-    const uint32_t* lcount;  // Gaussians stored per level (device)
-};
 
-__device__ __forceinline__ int cell_of(double v, int G) {
-    const double f = floor(v * (double)G);
-    return isfinite(f) ? (int)fmin(fmax(f, 0.0), (double)(G - 1)) : 0;
-}
 
 __device__ __forceinline__ float slack_for(double aniso) {
     const double s = 1.0 - (9.5367431640625e-07 + 256.0 * 1.1102230246251565e-16 * (1.0 + aniso));
     return s > 0.5 ? (float)(s - 1e-7) : 0.0f;
 }
 
-// Level whose cell (1/G_l) is >= 2 sigma_max: 4 G_l^2 <= lmin.
-__device__ __forceinline__ int level_of(const Lq& L, double lmin) {
-    int l = 0;
-    while (l < L.levels - 1 && !(4.0 * (double)L.lw[l] * (double)L.lw[l] <= lmin)) ++l;
-    return l;
-}
 
-__device__ __forceinline__ uint32_t key_of(const Lq& L, const ScanRec& r) {
-    const int l = level_of(L, fmin(r.inv_a, r.inv_b));
-    const int G = L.lw[l];
-    return (uint32_t)(L.loff[l] + cell_of(r.mu_y, G) * G + cell_of(r.mu_x, G));
-}
 
 __global__ void lq_count(const ScanRec* __restrict__ scan, uint32_t n, Lq L, uint32_t* __restrict__ cnt,
                          uint32_t* __restrict__ key, uint32_t* __restrict__ lcount) {
@@ -99,20 +88,6 @@ __global__ void lq_count(const ScanRec* __restrict__ scan, uint32_t n, Lq L, uin
     if (l >= 0 && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(lcount + l, (unsigned)__popc(same));
 }
 
-// Own-cell summaries are accumulated with order-preserving 64-bit atomics
-// while the members are scattered (no per-cell member loop): a double's bit
-// pattern, sign-flipped, orders like the double itself.
-struct Acc {
-    unsigned long long x0, y0, x1, y1, lmin, aniso;
-};
-
-__device__ __forceinline__ unsigned long long okey(double d) {
-    const unsigned long long b = (unsigned long long)__double_as_longlong(d);
-    return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
-}
-__device__ __forceinline__ double odec(unsigned long long k) {
-    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k));
-}
 
 // One launch clears everything a build accumulates into.
 __global__ void lq_clear(uint32_t cells, uint32_t* __restrict__ cnt2, Acc* __restrict__ acc,
@@ -121,7 +96,7 @@ __global__ void lq_clear(uint32_t cells, uint32_t* __restrict__ cnt2, Acc* __res
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += gridDim.x * blockDim.x) {
         cnt2[c] = 0;
         cnt2[cells + c] = 0;
-        acc[c] = Acc{okey(inf), okey(inf), okey(-inf), okey(-inf), okey(inf), okey(1.0)};
+        acc[c] = acc_empty();
         if (c < kMaxLv) lcount[c] = 0;
     }
 }
@@ -133,18 +108,7 @@ __global__ void lq_fill(const ScanRec* __restrict__ scan, uint32_t n, const uint
     if (i >= n) return;
     const uint32_t k = key[i];
     mem[off[k] + atomicAdd(cur + k, 1u)] = i;
-    const ScanRec r = scan[i];
-    const double lo = fmin(r.inv_a, r.inv_b), hi = fmax(r.inv_a, r.inv_b);
-    double aniso = hi / lo;
-    if (!(lo > 0.0) || !isfinite(hi) || !isfinite(r.mu_x) || !isfinite(r.mu_y))
-        aniso = __longlong_as_double(0x7ff0000000000000LL);
-    Acc* a = acc + k;
-    atomicMin(&a->x0, okey(r.mu_x));
-    atomicMin(&a->y0, okey(r.mu_y));
-    atomicMax(&a->x1, okey(r.mu_x));
-    atomicMax(&a->y1, okey(r.mu_y));
-    atomicMin(&a->lmin, okey(lo));
-    atomicMax(&a->aniso, okey(aniso));
+    acc_add(acc + k, scan[i]);
 }
 
 __device__ __forceinline__ Sum empty_sum() {
@@ -166,12 +130,14 @@ __device__ __forceinline__ void merge(Sum& a, const Sum& b) {
     a.count += b.count;
 }
 
-// Own summary of cell c from its accumulator.
-__device__ __forceinline__ Sum own_of(const Acc* __restrict__ acc, const uint32_t* __restrict__ cnt, uint32_t c) {
+// Own summary of cell c from its accumulator, which is reset for the next
+// round of accumulation (lq_fill or the Adam kernels).
+__device__ __forceinline__ Sum own_of(Acc* __restrict__ acc, const uint32_t* __restrict__ cnt, uint32_t c) {
     Sum s = empty_sum();
     const uint32_t m = cnt[c];
     if (m == 0) return s;
     const Acc a = acc[c];
+    acc[c] = acc_empty();
     s.x0 = odec(a.x0);
     s.y0 = odec(a.y0);
     s.x1 = odec(a.x1);
@@ -185,42 +151,101 @@ __device__ __forceinline__ Sum own_of(const Acc* __restrict__ acc, const uint32_
 // All own + subtree summaries in one launch.  CTA (bx, by) owns a 16 x 16
 // block of level-0 cells and builds levels 0..4 of that block in shared
 // memory (subtree = own + the four children); the last CTA to finish (atomic
-// ticket after a fence) builds the levels above from global memory.
+// ticket after a fence) builds the levels above.  Every own summary a
+// thread needs is fetched up front (all levels at once), so a CTA waits on
+// memory twice rather than twice per level.
 constexpr int kBlk = 16;
+constexpr int kInLv = 5;     // levels 0..4 live inside a block
+constexpr int kUpCells = 341;  // 16^2 + 8^2 + 4^2 + 2^2 + 1: upper levels kept in shared memory
 
-__global__ void __launch_bounds__(256) lq_tree_kernel(const Acc* __restrict__ acc, Lq L,
+// own summary from prefetched (count, accumulator); resets the accumulator
+__device__ __forceinline__ Sum own_from(uint32_t m, const Acc& a) {
+    Sum s = empty_sum();
+    if (m == 0) return s;
+    s.x0 = odec(a.x0);
+    s.y0 = odec(a.y0);
+    s.x1 = odec(a.x1);
+    s.y1 = odec(a.y1);
+    s.lmin = odec(a.lmin);
+    s.slack = slack_for(odec(a.aniso));
+    s.count = m;
+    return s;
+}
+
+__global__ void __launch_bounds__(256) lq_tree_kernel(Acc* __restrict__ acc, Lq L,
                                                       const uint32_t* __restrict__ cnt, Sum* __restrict__ own,
                                                       Sum* __restrict__ sub, unsigned int* __restrict__ ticket) {
     __shared__ Sum sm[2][kBlk * kBlk];
+    __shared__ Sum up[kUpCells];
+    __shared__ int s_loff[kMaxLv];
     const int t = threadIdx.x;
-    const int nb = (L.G0 + kBlk - 1) / kBlk;
+    if (t == 0) {
+#pragma unroll
+        for (int l = 0; l < kMaxLv; ++l) s_loff[l] = L.loff[l];
+    }
+    const int nb = L.G0 / kBlk;  // G0 is a power of two >= 16
     const int bx = blockIdx.x % nb, by = blockIdx.x / nb;
-    int cur = 0;
-    const int inlv = min(L.levels, 5);  // levels 0..4 live inside a block
-    for (int l = 0; l < inlv; ++l) {
-        const int side = kBlk >> l;  // this block's cells per side at level l
-        const int G = L.lw[l];
+    // prefetch: the cell this thread owns at each in-block level
+    uint32_t cell[kInLv], m[kInLv];
+    Acc a[kInLv];
+#pragma unroll
+    for (int l = 0; l < kInLv; ++l) {
+        const int side = kBlk >> l, G = L.G0 >> l;
+        cell[l] = ~0u;
+        m[l] = 0;
         if (t < side * side) {
             const int x = bx * side + t % side, y = by * side + t / side;
-            Sum s = empty_sum();
-            if (x < G && y < G) {
-                const uint32_t c = (uint32_t)(L.loff[l] + y * G + x);
-                const Sum o = own_of(acc, cnt, c);
-                own[c] = o;
-                s = o;
-                if (l > 0) {
-                    const int cs = side * 2;
-                    for (int dy = 0; dy < 2; ++dy)
-                        for (int dx = 0; dx < 2; ++dx) merge(s, sm[cur][(2 * (t / side) + dy) * cs + 2 * (t % side) + dx]);
-                }
-                sub[c] = s;
+            cell[l] = (uint32_t)(L.loff[l] + y * G + x);
+            m[l] = cnt[cell[l]];
+        }
+    }
+#pragma unroll
+    for (int l = 0; l < kInLv; ++l)
+        if (m[l]) a[l] = acc[cell[l]];
+#pragma unroll
+    for (int l = 0; l < kInLv; ++l)
+        if (m[l]) acc[cell[l]] = acc_empty();  // ready for the next accumulation
+    int cur = 0;
+#pragma unroll
+    for (int l = 0; l < kInLv; ++l) {
+        const int side = kBlk >> l;
+        if (t < side * side) {
+            const Sum o = own_from(m[l], a[l]);
+            own[cell[l]] = o;
+            Sum s = o;
+            if (l > 0) {
+                const int cs = side * 2;
+                for (int dy = 0; dy < 2; ++dy)
+                    for (int dx = 0; dx < 2; ++dx) merge(s, sm[cur][(2 * (t / side) + dy) * cs + 2 * (t % side) + dx]);
             }
+            sub[cell[l]] = s;
             sm[cur ^ 1][t] = s;
         }
         __syncthreads();
         cur ^= 1;
     }
-    if (L.levels <= 5) return;
+    if (L.levels <= kInLv) return;
+    // upper levels: the first level from which every level fits in shared
+    // memory (<= 16 x 16 cells), and the cells from there to the root
+    int l0 = kInLv;
+    while (l0 < L.levels && (L.G0 >> l0) > kBlk) ++l0;
+    int ncell = 0;
+    for (int j = l0; j < L.levels; ++j) ncell += (L.G0 >> j) * (L.G0 >> j);
+    // speculative prefetch (every CTA; L2 hits after the first): the own
+    // data of the shared-memory levels, so the last CTA does not wait for it
+    uint32_t um[2] = {0, 0}, uc[2] = {0, 0};
+    Acc ua[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int i = t + 256 * r;
+        if (i < ncell) {
+            uc[r] = (uint32_t)(s_loff[l0] + i);  // levels are contiguous in the cell numbering
+            um[r] = cnt[uc[r]];
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+        if (um[r]) ua[r] = acc[uc[r]];
     __shared__ bool last;
     __threadfence();
     __syncthreads();
@@ -228,22 +253,56 @@ __global__ void __launch_bounds__(256) lq_tree_kernel(const Acc* __restrict__ ac
     __syncthreads();
     if (!last) return;
     __threadfence();
-    for (int l = 5; l < L.levels; ++l) {
-        const int G = L.lw[l], cw = L.lw[l - 1];
+    // upper levels too large for shared memory (G0 >= 1024): level by level
+    // through global memory
+    for (int l = kInLv; l < l0; ++l) {
+        const int G = L.G0 >> l, cw = G * 2;
         for (int i = t; i < G * G; i += 256) {
             const int x = i % G, y = i / G;
-            const uint32_t c = (uint32_t)(L.loff[l] + i);
+            const uint32_t c = (uint32_t)(s_loff[l] + i);
             Sum s = own_of(acc, cnt, c);
             own[c] = s;
             for (int dy = 0; dy < 2; ++dy)
-                for (int dx = 0; dx < 2; ++dx) {
-                    const int cx = 2 * x + dx, cy = 2 * y + dy;
-                    if (cx < cw && cy < cw) merge(s, sub[L.loff[l - 1] + cy * cw + cx]);
-                }
+                for (int dx = 0; dx < 2; ++dx) merge(s, sub[s_loff[l - 1] + (2 * y + dy) * cw + 2 * x + dx]);
             sub[c] = s;
         }
         __threadfence();
         __syncthreads();
+    }
+    // the shared-memory levels: own summaries from the prefetch, children of
+    // level l0 from global memory, the rest merged in shared memory
+    {
+        const int G = L.G0 >> l0, cw = G * 2;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int i = t + 256 * r;
+            if (i >= ncell) continue;
+            if (um[r]) acc[uc[r]] = acc_empty();
+            const Sum o = own_from(um[r], ua[r]);
+            own[uc[r]] = o;
+            Sum s = o;
+            if (i < G * G) {
+                const int x = i % G, y = i / G;
+                for (int dy = 0; dy < 2; ++dy)
+                    for (int dx = 0; dx < 2; ++dx) merge(s, sub[s_loff[l0 - 1] + (2 * y + dy) * cw + 2 * x + dx]);
+                sub[uc[r]] = s;
+            }
+            up[i] = s;  // level l0: subtree; above: own (merged below)
+        }
+    }
+    __syncthreads();
+    for (int j = l0 + 1, b0 = 0; j < L.levels; ++j) {
+        const int G = L.G0 >> j, cw = G * 2, b1 = b0 + cw * cw;  // b0: first cell of level j-1 in up[]
+        for (int i = t; i < G * G; i += 256) {
+            const int x = i % G, y = i / G;
+            Sum s = up[b1 + i];
+            for (int dy = 0; dy < 2; ++dy)
+                for (int dx = 0; dx < 2; ++dx) merge(s, up[b0 + (2 * y + dy) * cw + 2 * x + dx]);
+            up[b1 + i] = s;
+            sub[s_loff[j] + i] = s;
+        }
+        __syncthreads();
+        b0 = b1;
     }
     if (t == 0) *ticket = 0;  // ready for the next build
 }
@@ -773,7 +832,14 @@ __global__ void __launch_bounds__(128) hard_merge_kernel(const ScanRec* __restri
 struct KnnBufs {
     DevBuf cnt, off, key, mem, own, sub, cub_tmp, hard, ticket, part, lcount, acc;
     int knn_blocks = 0;  // resident CTAs for the persistent query kernel
-    uint64_t version = ~0ull;
+    uint64_t version = ~0ull;  // params_version the summaries describe
+    // refit chain: Adam launches accumulated every Gaussian into acc (by its
+    // cell at the last rebuild) for each params version up to `chain`
+    bool acc_ok = false;
+    uint64_t chain = ~0ull;
+    uint32_t built_n = 0;
+    int since_build = 0;
+    uint64_t builds = 0, refits = 0;
     Lq lq{};
 };
 
@@ -795,6 +861,23 @@ int knn_build(igs_ctx* ctx) {
     if (!ctx->knn) ctx->knn = new KnnBufs();
     KnnBufs& b = *static_cast<KnnBufs*>(ctx->knn);
     if (b.version == ctx->params_version) return IGS_OK;
+    // ctx->knn_grown: the last Adam's count of Gaussians grown past their
+    // level, read back with the step's status (-1: unknown)
+    if (b.acc_ok && b.chain == ctx->params_version && b.built_n == ctx->n && b.since_build < kRefitPeriod &&
+        ctx->knn_grown >= 0 && ctx->knn_grown <= (long long)(ctx->n >> kGrowShift)) {
+        b.refits++;
+        // every Gaussian was accumulated into its (old) cell by the Adam
+        // launches since the last build: re-derive the summaries only
+        const int nb = (b.lq.G0 + kBlk - 1) / kBlk;
+        igs_prof_begin(ctx, IGS_PROF_CULL);
+        lq_tree_kernel<<<nb * nb, 256, 0, ctx->stream>>>((Acc*)b.acc.p, b.lq, (const uint32_t*)b.cnt.p,
+                                                         (Sum*)b.own.p, (Sum*)b.sub.p, (unsigned int*)b.ticket.p);
+        IGS_LAUNCHED(ctx);
+        igs_prof_end(ctx, IGS_PROF_CULL, 0.0);
+        b.since_build++;
+        b.version = b.chain = ctx->params_version;
+        return IGS_OK;
+    }
     const uint32_t n = ctx->n;
     int G0 = 16;  // finest grid: about 2 centres per cell
     while (G0 < 4096 && (uint64_t)G0 * G0 * 2 < n) G0 *= 2;
@@ -840,12 +923,16 @@ int knn_build(igs_ctx* ctx) {
                                                       (uint32_t*)b.mem.p, (Acc*)b.acc.p);
     IGS_LAUNCHED(ctx);
     const int nb = (G0 + kBlk - 1) / kBlk;
-    lq_tree_kernel<<<nb * nb, 256, 0, ctx->stream>>>((const Acc*)b.acc.p, L, cnt, (Sum*)b.own.p, (Sum*)b.sub.p,
+    lq_tree_kernel<<<nb * nb, 256, 0, ctx->stream>>>((Acc*)b.acc.p, L, cnt, (Sum*)b.own.p, (Sum*)b.sub.p,
                                                      (unsigned int*)b.ticket.p);
     IGS_LAUNCHED(ctx);
     igs_prof_end(ctx, IGS_PROF_CULL, 0.0);
     b.lq = L;
-    b.version = ctx->params_version;
+    b.builds++;
+    b.version = b.chain = ctx->params_version;
+    b.acc_ok = true;
+    b.built_n = n;
+    b.since_build = 0;
     return IGS_OK;
 }
 
@@ -895,9 +982,27 @@ int run_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int kk,
 
 }  // namespace
 
+// Called by an Adam launch right before it bumps params_version by one.
+TreeAcc igs_knn_tree_acc(igs_ctx* ctx) {
+    if (!ctx->knn) return TreeAcc{nullptr, nullptr};
+    KnnBufs& b = *static_cast<KnnBufs*>(ctx->knn);
+    TreeAcc ta{};
+    if (b.acc_ok && b.chain == ctx->params_version && b.built_n == ctx->n) {
+        b.chain = ctx->params_version + 1;
+        ta.acc = (Acc*)b.acc.p;
+        ta.key = (const uint32_t*)b.key.p;
+        ta.grown = (unsigned long long*)(ctx->status + 3);
+        ta.L = b.lq;
+        return ta;
+    }
+    b.acc_ok = false;
+    return ta;
+}
+
 void igs_knn_free(igs_ctx* ctx) {
     if (!ctx->knn) return;
     KnnBufs* b = static_cast<KnnBufs*>(ctx->knn);
+    if (getenv("IGS_KNN_STATS")) fprintf(stderr, "knn tree: %llu builds, %llu refits\n", (unsigned long long)b->builds, (unsigned long long)b->refits);
     for (DevBuf* d : {&b->cnt, &b->off, &b->key, &b->mem, &b->own, &b->sub, &b->cub_tmp, &b->hard, &b->ticket,
                       &b->part, &b->lcount, &b->acc})
         cudaFree(d->p);

@@ -1,0 +1,109 @@
+// knn_tree.cuh -- the loose-quadtree pieces shared by the kNN search
+// (knn.cu) and the Adam kernels (train.cu), which accumulate each updated
+// Gaussian into its cell's summary accumulator so the next search only
+// re-derives the summaries (no re-bucketing) -- see knn.cu for the
+// structure and the certified bound.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "igs_internal.cuh"
+
+namespace igs_dev {
+
+constexpr int kMaxLv = 13;
+
+struct Lq {
+    int G0, levels;
+    int lw[kMaxLv];    // cells per side
+    int loff[kMaxLv];  // first cell id of the level
+    const uint32_t* lcount;  // Gaussians stored per level (device)
+};
+
+__device__ __forceinline__ int cell_of(double v, int G) {
+    const double f = floor(v * (double)G);
+    return isfinite(f) ? (int)fmin(fmax(f, 0.0), (double)(G - 1)) : 0;
+}
+
+// Level whose cell (1/G_l) is >= 2 sigma_max: 4 G_l^2 <= lmin.
+__device__ __forceinline__ int level_of(const Lq& L, double lmin) {
+    int l = 0;
+    while (l < L.levels - 1 && !(4.0 * (double)L.lw[l] * (double)L.lw[l] <= lmin)) ++l;
+    return l;
+}
+
+__device__ __forceinline__ uint32_t key_of(const Lq& L, const ScanRec& r) {
+    const int l = level_of(L, fmin(r.inv_a, r.inv_b));
+    const int G = L.lw[l];
+    return (uint32_t)(L.loff[l] + cell_of(r.mu_y, G) * G + cell_of(r.mu_x, G));
+}
+
+// Own-cell summaries are accumulated with order-preserving 64-bit atomics
+// while the members are scattered (no per-cell member loop): a double's bit
+// pattern, sign-flipped, orders like the double itself.
+struct Acc {
+    unsigned long long x0, y0, x1, y1, lmin, aniso;
+};
+
+__device__ __forceinline__ unsigned long long okey(double d) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double odec(unsigned long long k) {
+    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k));
+}
+
+// Adds Gaussian r to a cell accumulator.  A non-finite or degenerate record
+// gets aniso = inf, whose slack 0 makes the cell never prunable.
+__device__ __forceinline__ void acc_add(Acc* a, const ScanRec& r) {
+    const double lo = fmin(r.inv_a, r.inv_b), hi = fmax(r.inv_a, r.inv_b);
+    double aniso = hi / lo;
+    if (!(lo > 0.0) || !isfinite(hi) || !isfinite(r.mu_x) || !isfinite(r.mu_y))
+        aniso = __longlong_as_double(0x7ff0000000000000LL);
+    atomicMin(&a->x0, okey(r.mu_x));
+    atomicMin(&a->y0, okey(r.mu_y));
+    atomicMax(&a->x1, okey(r.mu_x));
+    atomicMax(&a->y1, okey(r.mu_y));
+    atomicMin(&a->lmin, okey(lo));
+    atomicMax(&a->aniso, okey(aniso));
+}
+
+__device__ __forceinline__ Acc acc_empty() {
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    return Acc{okey(inf), okey(inf), okey(-inf), okey(-inf), okey(inf), okey(1.0)};
+}
+
+// What an Adam launch needs to keep the tree refittable: acc == nullptr
+// means "do not accumulate" (the next search rebuilds).
+struct TreeAcc {
+    Acc* acc;
+    const uint32_t* key;            // cell of every Gaussian at the last rebuild
+    unsigned long long* grown;      // Gaussians now too large for their level
+    Lq L;
+};
+
+__device__ __forceinline__ int level_of_cell(const Lq& L, uint32_t c) {
+    int l = 0;
+    while (l + 1 < L.levels && (uint32_t)L.loff[l + 1] <= c) ++l;
+    return l;
+}
+
+// Accumulates Gaussian i (record r) into its stored cell and counts it in
+// *grown when its scale now calls for a coarser level than the one it is
+// stored at: such a Gaussian weakens the bounds of its cell and every
+// ancestor, so the host re-buckets before the next search (knn_build).
+__device__ __forceinline__ void tree_acc_add(const TreeAcc& ta, uint32_t i, const ScanRec& r) {
+    if (!ta.acc) return;
+    const uint32_t c = ta.key[i];
+    acc_add(ta.acc + c, r);
+    const bool grew = level_of(ta.L, fmin(r.inv_a, r.inv_b)) > level_of_cell(ta.L, c);
+    const unsigned act = __activemask();
+    const unsigned m = __ballot_sync(act, grew);
+    if (m && (threadIdx.x & 31) == __ffs(act) - 1) atomicAdd(ta.grown, (unsigned long long)__popc(m));
+}
+
+}  // namespace igs_dev
+
+// knn.cu: the accumulation target for an Adam launch that is about to bump
+// params_version by exactly one ({nullptr, nullptr}: do not accumulate).
+igs_dev::TreeAcc igs_knn_tree_acc(igs_ctx* ctx);

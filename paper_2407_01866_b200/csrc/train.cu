@@ -23,6 +23,7 @@
 #include <cmath>
 
 #include "igs_internal.cuh"
+#include "knn_tree.cuh"
 
 using namespace igs_dev;
 
@@ -185,20 +186,51 @@ __global__ void scatter_slots_kernel(const uint32_t* __restrict__ keys, uint32_t
     if (pos == 0 && gcnt[g] > kShortSeg) long_list[atomicAdd(long_count, 1u)] = g;
 }
 
+__device__ __forceinline__ void sum_row(const double* __restrict__ contrib, uint32_t slot, double* acc) {
+    const double2* c = reinterpret_cast<const double2*>(contrib + (size_t)slot * 8);
+    const double2 a = c[0], b = c[1], cc = c[2], d = c[3];
+    acc[0] = __dadd_rn(acc[0], a.x);
+    acc[1] = __dadd_rn(acc[1], a.y);
+    acc[2] = __dadd_rn(acc[2], b.x);
+    acc[3] = __dadd_rn(acc[3], b.y);
+    acc[4] = __dadd_rn(acc[4], cc.x);
+    acc[5] = __dadd_rn(acc[5], cc.y);
+    acc[6] = __dadd_rn(acc[6], d.x);
+    acc[7] = __dadd_rn(acc[7], d.y);
+}
+
 __device__ __forceinline__ void sum_sorted(const double* __restrict__ contrib, const uint32_t* slots, uint32_t m,
                                            double* acc) {
-    for (uint32_t e = 0; e < m; ++e) {
-        const double2* c = reinterpret_cast<const double2*>(contrib + (size_t)slots[e] * 8);
-        const double2 a = c[0], b = c[1], cc = c[2], d = c[3];
-        acc[0] = __dadd_rn(acc[0], a.x);
-        acc[1] = __dadd_rn(acc[1], a.y);
-        acc[2] = __dadd_rn(acc[2], b.x);
-        acc[3] = __dadd_rn(acc[3], b.y);
-        acc[4] = __dadd_rn(acc[4], cc.x);
-        acc[5] = __dadd_rn(acc[5], cc.y);
-        acc[6] = __dadd_rn(acc[6], d.x);
-        acc[7] = __dadd_rn(acc[7], d.y);
+    for (uint32_t e = 0; e < m; ++e) sum_row(contrib, slots[e], acc);
+}
+
+// Sums segment [o, o + m) of perm (m <= kShortSeg) in ascending slot order.
+// m <= 2 -- nearly every Gaussian -- stays in registers.
+__device__ __forceinline__ void sum_segment(const double* __restrict__ contrib, const uint32_t* __restrict__ perm,
+                                            uint32_t o, uint32_t m, double* acc) {
+    if (m == 0) return;
+    if (m <= 2) {
+        uint32_t a = perm[o], b = m == 2 ? perm[o + 1] : 0u;
+        if (m == 2 && b < a) {
+            const uint32_t t = a;
+            a = b;
+            b = t;
+        }
+        sum_row(contrib, a, acc);
+        if (m == 2) sum_row(contrib, b, acc);
+        return;
     }
+    uint32_t sl[kShortSeg];
+    for (uint32_t e = 0; e < m; ++e) {
+        const uint32_t val = perm[o + e];
+        uint32_t pos = e;
+        while (pos > 0 && sl[pos - 1] > val) {
+            sl[pos] = sl[pos - 1];
+            --pos;
+        }
+        sl[pos] = val;
+    }
+    sum_sorted(contrib, sl, m, acc);
 }
 
 __device__ __forceinline__ void store_grad(double* __restrict__ grads, uint32_t g, const double* acc,
@@ -226,19 +258,8 @@ __global__ void segment_sum_kernel(const uint32_t* __restrict__ gcnt, const uint
     if (g >= n) return;
     const uint32_t m = gcnt[g];
     if (m > kShortSeg) return;  // long_segment_kernel
-    uint32_t sl[kShortSeg];
-    const uint32_t o = goff[g];
-    for (uint32_t e = 0; e < m; ++e) {
-        const uint32_t v = perm[o + e];
-        uint32_t pos = e;
-        while (pos > 0 && sl[pos - 1] > v) {
-            sl[pos] = sl[pos - 1];
-            --pos;
-        }
-        sl[pos] = v;
-    }
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    sum_sorted(contrib, sl, m, acc);
+    sum_segment(contrib, perm, goff[g], m, acc);
     store_grad(grads, g, acc, status);
 }
 
@@ -368,6 +389,14 @@ __global__ void grad_check_kernel(const double* __restrict__ grads, uint32_t n, 
         }
 }
 
+// a / b correctly rounded; a zero dividend (every parameter of a Gaussian no
+// sample selected) skips __ddiv_rn's slow path: 0 / b == 0 * b for finite
+// nonzero b, sign included.
+__device__ __forceinline__ double div_rn(double a, double b) {
+    return (a == 0.0 && b != 0.0 && fabs(b) < __longlong_as_double(0x7ff0000000000000LL)) ? __dmul_rn(a, b)
+                                                                                         : __ddiv_rn(a, b);
+}
+
 __device__ __forceinline__ double clamp01d(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
 __device__ __forceinline__ double clamp_scale(double v) {
     return v < kScaleMin ? kScaleMin : (v > kScaleMax ? kScaleMax : v);
@@ -376,14 +405,8 @@ __device__ __forceinline__ double clamp_scale(double v) {
 // Kernel 5: Adam (adam.cpp:21-51) + constrain (gaussian.cpp:74-90) +
 // PreparedSet refresh for the next step, for one Gaussian.  HBM: 256 B read
 // + 192 B written for params/grads/m/v, plus 96 B of refreshed scan/shade.
-__device__ __forceinline__ void adam_one(uint32_t i, const double* gg, double* __restrict__ params,
-                                         double* __restrict__ m, double* __restrict__ v, ScanRec* __restrict__ scan,
-                                         ShadeRec* __restrict__ shade, double lr_mu, double lr_color, double lr_scale,
-                                         double lr_theta, double bc1, double bc2, long long* __restrict__ status) {
-    const double b1 = 0.9, b2 = 0.999, eps = 1e-8;  // adam.hpp:33-35
-    const double omb1 = 1.0 - b1, omb2 = 1.0 - b2;  // folded exactly like the reference's constants
-    const double lr8[8] = {lr_mu, lr_mu, lr_theta, lr_scale, lr_scale, lr_color, lr_color, lr_color};
-    double gp[8], mm[8], vv[8];
+__device__ __forceinline__ void adam_load(uint32_t i, const double* __restrict__ params, const double* __restrict__ m,
+                                          const double* __restrict__ v, double* gp, double* mm, double* vv) {
     const double2* P = reinterpret_cast<const double2*>(params + (size_t)i * 8);
     const double2* M = reinterpret_cast<const double2*>(m + (size_t)i * 8);
     const double2* V = reinterpret_cast<const double2*>(v + (size_t)i * 8);
@@ -394,14 +417,25 @@ __device__ __forceinline__ void adam_one(uint32_t i, const double* gg, double* _
         mm[2 * h] = c.x; mm[2 * h + 1] = c.y;
         vv[2 * h] = d.x; vv[2 * h + 1] = d.y;
     }
+}
+
+// gp/mm/vv: Gaussian i's parameters and moments (adam_load), updated in place.
+__device__ __forceinline__ void adam_one(uint32_t i, const double* gg, double* gp, double* mm, double* vv,
+                                         double* __restrict__ params, double* __restrict__ m, double* __restrict__ v,
+                                         ScanRec* __restrict__ scan, ShadeRec* __restrict__ shade, double lr_mu,
+                                         double lr_color, double lr_scale, double lr_theta, double bc1, double bc2,
+                                         long long* __restrict__ status, const TreeAcc& ta) {
+    const double b1 = 0.9, b2 = 0.999, eps = 1e-8;  // adam.hpp:33-35
+    const double omb1 = 1.0 - b1, omb2 = 1.0 - b2;  // folded exactly like the reference's constants
+    const double lr8[8] = {lr_mu, lr_mu, lr_theta, lr_scale, lr_scale, lr_color, lr_color, lr_color};
 #pragma unroll
     for (int p = 0; p < 8; ++p) {
         const double g = gg[p];
         mm[p] = __dadd_rn(__dmul_rn(b1, mm[p]), __dmul_rn(omb1, g));
         vv[p] = __dadd_rn(__dmul_rn(b2, vv[p]), __dmul_rn(__dmul_rn(omb2, g), g));
-        const double m_hat = __ddiv_rn(mm[p], bc1);
-        const double v_hat = __ddiv_rn(vv[p], bc2);
-        const double upd = __ddiv_rn(__dmul_rn(lr8[p], m_hat), __dadd_rn(__dsqrt_rn(v_hat), eps));
+        const double m_hat = div_rn(mm[p], bc1);
+        const double v_hat = div_rn(vv[p], bc2);
+        const double upd = div_rn(__dmul_rn(lr8[p], m_hat), __dadd_rn(__dsqrt_rn(v_hat), eps));
         gp[p] = __dsub_rn(gp[p], upd);
     }
     // constrain (gaussian.cpp:74-90); a non-finite result raises there.
@@ -410,6 +444,7 @@ __device__ __forceinline__ void adam_one(uint32_t i, const double* gg, double* _
     for (int p = 0; p < 8; ++p) finite_all = finite_all && isfinite(gp[p]);
     if (!finite_all) {
         atomicMin(status + 1, (long long)i);
+        tree_acc_add(ta, i, scan[i]);  // unchanged
         return;
     }
     gp[0] = clamp01d(gp[0]);
@@ -445,6 +480,7 @@ __device__ __forceinline__ void adam_one(uint32_t i, const double* gg, double* _
     r.inv_a = __dmul_rn(inv_s1, inv_s1);
     r.inv_b = __dmul_rn(inv_s2, inv_s2);
     scan[i] = r;
+    tree_acc_add(ta, i, r);
     ShadeRec hh;
     hh.r = gp[5];
     hh.g = gp[6];
@@ -461,11 +497,14 @@ __device__ __forceinline__ void adam_one(uint32_t i, const double* gg, double* _
 __global__ void adam_kernel(double* __restrict__ params, const double* __restrict__ grads, double* __restrict__ m,
                             double* __restrict__ v, ScanRec* __restrict__ scan, ShadeRec* __restrict__ shade,
                             uint32_t n, double lr_mu, double lr_color, double lr_scale, double lr_theta, double bc1,
-                            double bc2, long long* __restrict__ status) {
+                            double bc2, long long* __restrict__ status, TreeAcc ta) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    if (status[0] != LLONG_MAX || status[2] != LLONG_MAX) return;
-    double gg[8];
+    if (status[0] != LLONG_MAX || status[2] != LLONG_MAX) {
+        tree_acc_add(ta, i, scan[i]);  // every Gaussian is accumulated, updated or not
+        return;
+    }
+    double gg[8], gp[8], mm[8], vv[8];
     const double2* G = reinterpret_cast<const double2*>(grads + (size_t)i * 8);
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
@@ -473,7 +512,8 @@ __global__ void adam_kernel(double* __restrict__ params, const double* __restric
         gg[2 * h] = b.x;
         gg[2 * h + 1] = b.y;
     }
-    adam_one(i, gg, params, m, v, scan, shade, lr_mu, lr_color, lr_scale, lr_theta, bc1, bc2, status);
+    adam_load(i, params, m, v, gp, mm, vv);
+    adam_one(i, gg, gp, mm, vv, params, m, v, scan, shade, lr_mu, lr_color, lr_scale, lr_theta, bc1, bc2, status, ta);
 }
 
 // Fused short-segment reduction + Adam (single rank): thread g sums its
@@ -483,16 +523,26 @@ __global__ void adam_kernel(double* __restrict__ params, const double* __restric
 // finite Gaussian is still updated, deterministically; the reference has
 // updated Gaussians 0..i-1 when it throws, adam.cpp:29-31).  A non-finite
 // loss (flagged by the search epilogue) skips the whole step, as fit.cpp:155.
-__global__ void segment_adam_kernel(const uint32_t* __restrict__ gcnt, const uint32_t* __restrict__ goff,
+__global__ void segment_adam_kernel(uint32_t* __restrict__ gcnt, const uint32_t* __restrict__ goff,
                                     const uint32_t* __restrict__ perm, const double* __restrict__ contrib,
                                     uint32_t n, double* __restrict__ grads, double* __restrict__ params,
                                     double* __restrict__ m, double* __restrict__ v, ScanRec* __restrict__ scan,
                                     ShadeRec* __restrict__ shade, double lr_mu, double lr_color, double lr_scale,
-                                    double lr_theta, double bc1, double bc2, long long* __restrict__ status) {
+                                    double lr_theta, double bc1, double bc2, long long* __restrict__ status,
+                                    TreeAcc ta) {
     const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
-    if (status[2] != LLONG_MAX) return;
-    const uint32_t cntg = gcnt[g];
+    // the parameter/moment loads do not depend on the reduction: issue first
+    double gp[8], mm[8], vv[8];
+    adam_load(g, params, m, v, gp, mm, vv);
+    const uint32_t cntg = gcnt[g], og = goff[g];
+    // last reader of the counters/cursors: leave them zeroed for the next step
+    gcnt[g] = 0;
+    gcnt[n + g] = 0;
+    if (status[2] != LLONG_MAX) {
+        tree_acc_add(ta, g, scan[g]);  // every Gaussian is accumulated, updated or not
+        return;
+    }
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (cntg > kShortSeg) {
         const double2* G = reinterpret_cast<const double2*>(grads + (size_t)g * 8);
@@ -503,18 +553,7 @@ __global__ void segment_adam_kernel(const uint32_t* __restrict__ gcnt, const uin
             acc[2 * h + 1] = b.y;
         }
     } else {
-        uint32_t sl[kShortSeg];
-        const uint32_t o = goff[g];
-        for (uint32_t e = 0; e < cntg; ++e) {
-            const uint32_t val = perm[o + e];
-            uint32_t pos = e;
-            while (pos > 0 && sl[pos - 1] > val) {
-                sl[pos] = sl[pos - 1];
-                --pos;
-            }
-            sl[pos] = val;
-        }
-        sum_sorted(contrib, sl, cntg, acc);
+        sum_segment(contrib, perm, og, cntg, acc);
         double2* o2 = reinterpret_cast<double2*>(grads + (size_t)g * 8);
         o2[0] = make_double2(acc[0], acc[1]);
         o2[1] = make_double2(acc[2], acc[3]);
@@ -525,13 +564,15 @@ __global__ void segment_adam_kernel(const uint32_t* __restrict__ gcnt, const uin
     for (int p = 0; p < 8; ++p)
         if (!isfinite(acc[p])) {
             atomicMin(status, (long long)g * 8 + p);
+            tree_acc_add(ta, g, scan[g]);
             return;
         }
-    adam_one(g, acc, params, m, v, scan, shade, lr_mu, lr_color, lr_scale, lr_theta, bc1, bc2, status);
+    adam_one(g, acc, gp, mm, vv, params, m, v, scan, shade, lr_mu, lr_color, lr_scale, lr_theta, bc1, bc2, status, ta);
 }
 
 __global__ void reset_status_kernel(long long* status) {
-    if (threadIdx.x < 4) status[threadIdx.x] = LLONG_MAX;
+    if (threadIdx.x < 3) status[threadIdx.x] = LLONG_MAX;
+    if (threadIdx.x == 3) status[3] = 0;  // a count (kNN tree growth)
 }
 
 __global__ void weights_kernel(const double* __restrict__ q, const uint32_t* __restrict__ idx, size_t total,
@@ -599,7 +640,10 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
         long_ctl = (uint32_t*)igs_scratch(ctx, 24, ((size_t)n + 1) * sizeof(uint32_t));
         if (!contrib || !keys || !gcnt || !goff || !perm || !long_ctl)
             return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
-        IGS_CUDA(ctx, cudaMemsetAsync(gcnt, 0, (size_t)n * 2 * sizeof(uint32_t), ctx->stream));
+        // counters | cursors: the fused Adam leaves them zeroed for the next step
+        if (ctx->gcnt_clean != gcnt || ctx->gcnt_clean_n != n)
+            IGS_CUDA(ctx, cudaMemsetAsync(gcnt, 0, (size_t)n * 2 * sizeof(uint32_t), ctx->stream));
+        ctx->gcnt_clean = nullptr;
         IGS_CUDA(ctx, cudaMemsetAsync(long_ctl, 0, sizeof(uint32_t), ctx->stream));
         // (long_ctl[0]: long-segment count; long_ctl[1..]: the queue)
     } else {
@@ -635,6 +679,16 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
         IGS_LAUNCHED(ctx);
         igs_prof_end(ctx, IGS_PROF_FINISH, (double)items);
     }
+    // the loss sum needs only the per-sample losses: it runs on the side
+    // stream, overlapping the reduction and Adam, and is joined below
+    const bool loss_side = mode == 0 && dev_loss;
+    if (loss_side) {
+        IGS_CUDA(ctx, cudaEventRecord(ctx->ev_fork, ctx->stream));
+        IGS_CUDA(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+        loss_reduce_kernel<<<1, 1024, 0, ctx->side>>>(losses, ns, inv_n, dev_loss);
+        IGS_LAUNCHED(ctx);
+        IGS_CUDA(ctx, cudaEventRecord(ctx->ev_join, ctx->side));
+    }
     if (ctx->opt_deterministic) {
         igs_prof_begin(ctx, IGS_PROF_REDUCE);
         if (!gcnt_filled) {
@@ -659,14 +713,17 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
             // short segments summed inside the Adam kernel (one pass over the set)
             const double bc1 = 1.0 - std::pow(0.9, (double)t);  // adam.cpp:16-17, host libm
             const double bc2 = 1.0 - std::pow(0.999, (double)t);
+            const TreeAcc ta = igs_knn_tree_acc(ctx);
             ctx->params_version++;
             igs_prof_end(ctx, IGS_PROF_REDUCE, (double)items);
             igs_prof_begin(ctx, IGS_PROF_ADAM);
             segment_adam_kernel<<<(n + 255) / 256, 256, 0, ctx->stream>>>(
                 gcnt, goff, perm, contrib, n, ctx->grads, ctx->params, ctx->adam_m, ctx->adam_v, ctx->scan,
-                ctx->shade, fuse_lr4[0], fuse_lr4[1], fuse_lr4[2], fuse_lr4[3], bc1, bc2, ctx->status);
+                ctx->shade, fuse_lr4[0], fuse_lr4[1], fuse_lr4[2], fuse_lr4[3], bc1, bc2, ctx->status, ta);
             IGS_LAUNCHED(ctx);
             igs_prof_end(ctx, IGS_PROF_ADAM, (double)n * 544.0);
+            ctx->gcnt_clean = gcnt;
+            ctx->gcnt_clean_n = n;
             if (fused) *fused = true;
         } else {
             segment_sum_kernel<<<(n + 255) / 256, 256, 0, ctx->stream>>>(gcnt, goff, perm, contrib, n, ctx->grads,
@@ -678,10 +735,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
     } else {
         ctx->grads_checked = false;
     }
-    if (mode == 0 && dev_loss) {
-        loss_reduce_kernel<<<1, 1024, 0, ctx->stream>>>(losses, ns, inv_n, dev_loss);
-        IGS_LAUNCHED(ctx);
-    }
+    if (loss_side) IGS_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
     ctx->grads_valid = true;
     return IGS_OK;
 }
@@ -696,11 +750,12 @@ int igs_adam_launch(igs_ctx* ctx, const double* lr4, long long t) {
     // Bias corrections with the host libm pow, as adam.cpp:16-17.
     const double bc1 = 1.0 - std::pow(0.9, (double)t);
     const double bc2 = 1.0 - std::pow(0.999, (double)t);
+    const TreeAcc ta = igs_knn_tree_acc(ctx);
     ctx->params_version++;
     igs_prof_begin(ctx, IGS_PROF_ADAM);
     adam_kernel<<<(ctx->n + 255) / 256, 256, 0, ctx->stream>>>(ctx->params, ctx->grads, ctx->adam_m, ctx->adam_v,
                                                                ctx->scan, ctx->shade, ctx->n, lr4[0], lr4[1], lr4[2],
-                                                               lr4[3], bc1, bc2, ctx->status);
+                                                               lr4[3], bc1, bc2, ctx->status, ta);
     IGS_LAUNCHED(ctx);
     // algorithmic bytes: read params/grads/m/v (256 B), write params/m/v
     // (192 B) and the refreshed 96 B of scan+shade records

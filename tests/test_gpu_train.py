@@ -189,3 +189,30 @@ def test_nccl_single_rank_allreduce_path(gctx, port):
         c2.train_iteration(sidx, 10, LR, 1)
         gctx.train_iteration(sidx, 10, LR, 1)
         assert np.array_equal(c2.get_params(), gctx.get_params())
+
+
+def test_knn_refit_stays_exact_over_many_steps(gctx, port):
+    """Between full re-bucketings the kNN tree is refit from the Adam
+    kernels' accumulation (knn.cu kRefitPeriod).  After 24 fused iterations
+    with a large learning rate (Gaussians cross cells and change level), one
+    more step through the unfused Adam, the exact top-K at 3000 pixel centres
+    must still equal the oracle's on the device's current parameters."""
+    W, H = 128, 96
+    target = synth.photo_like_image(W, H, 31007)
+    params = port.initialize_set(target, 2500, 0.3, 17)
+    steps = synth.sample_indices(2000, W, H, seed=19, steps=24)
+    gctx.set_params(params)
+    gctx.set_target(target)
+    gctx.upload_samples(steps)
+    gctx.train_iterations(24, 10, LR * 10, 1)
+    gctx.train_step(steps[0], 10)
+    gctx.adam_step(LR * 10, 25)
+    p = gctx.get_params()
+    _, topk = port.render_image(p, W, H, 10, want_topk=True)
+    rng = np.random.default_rng(3)
+    xs = rng.integers(0, W, 3000)
+    ys = rng.integers(0, H, 3000)
+    uv = np.stack([(xs + 0.5) / W, (ys + 0.5) / H], axis=1)
+    idx, w, cnt = gctx.select_top_k(uv, 10)
+    assert np.all(cnt == 10)
+    assert np.array_equal(idx, topk[ys, xs])
