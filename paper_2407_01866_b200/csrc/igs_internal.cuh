@@ -236,6 +236,35 @@ int igs_ensure_image(igs_ctx* ctx, int w, int h);
         if (_e != cudaSuccess) return igs_cuda_check((ctx), _e, "launch");  \
     } while (0)
 
+// Programmatic dependent launch: a kernel launched with IGS_PDL may be
+// scheduled while its stream predecessor drains (hiding launch latency); it
+// must execute pdl_wait() before it reads or writes any memory a
+// predecessor touches.  Without the launch attribute pdl_wait is a no-op.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t igs_launch_pdl(cudaStream_t st, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                  Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
+#define IGS_PDL(ctx, kernel, grid, block, smem, ...)                                                        \
+    do {                                                                                                    \
+        cudaError_t _e = igs_launch_pdl((ctx)->stream, kernel, dim3(grid), dim3(block), (smem), __VA_ARGS__); \
+        (ctx)->launches++;                                                                                  \
+        if (_e != cudaSuccess) return igs_cuda_check((ctx), _e, #kernel);                                   \
+    } while (0)
+
 #define IGS_CUDA(ctx, call)                                                 \
     do {                                                                    \
         cudaError_t _e = (call);                                            \
@@ -259,7 +288,7 @@ void igs_knn_free(igs_ctx* ctx);
 int igs_topk_knn(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq);
 int igs_knn_forward_backward(igs_ctx* ctx, int mode, const uint32_t* sidx, const double* samples5, uint32_t npts,
                              int kk, double inv_n, double* losses, double* contrib, uint32_t* keys, uint32_t* gcnt,
-                             double* grads_atomic);
+                             double* grads_atomic, uint32_t* zero_word = nullptr);
 int igs_topk_samples_culled(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq);
 int igs_topk_pixels_culled(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq, int W,
                            int H);

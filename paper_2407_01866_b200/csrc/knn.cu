@@ -73,6 +73,7 @@ __device__ __forceinline__ float slack_for(double aniso) {
 
 __global__ void lq_count(const ScanRec* __restrict__ scan, uint32_t n, Lq L, uint32_t* __restrict__ cnt,
                          uint32_t* __restrict__ key, uint32_t* __restrict__ lcount) {
+    pdl_wait();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     int l = -1;
     if (i < n) {
@@ -92,7 +93,7 @@ __global__ void lq_count(const ScanRec* __restrict__ scan, uint32_t n, Lq L, uin
 // One launch clears everything a build accumulates into.
 __global__ void lq_clear(uint32_t cells, uint32_t* __restrict__ cnt2, Acc* __restrict__ acc,
                          uint32_t* __restrict__ lcount) {
-    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    pdl_wait();
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += gridDim.x * blockDim.x) {
         cnt2[c] = 0;
         cnt2[cells + c] = 0;
@@ -104,6 +105,7 @@ __global__ void lq_clear(uint32_t cells, uint32_t* __restrict__ cnt2, Acc* __res
 __global__ void lq_fill(const ScanRec* __restrict__ scan, uint32_t n, const uint32_t* __restrict__ key,
                         const uint32_t* __restrict__ off, uint32_t* __restrict__ cur, uint32_t* __restrict__ mem,
                         Acc* __restrict__ acc) {
+    pdl_wait();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t k = key[i];
@@ -185,6 +187,7 @@ __global__ void __launch_bounds__(256) lq_tree_kernel(Acc* __restrict__ acc, Lq 
     }
     const int nb = L.G0 / kBlk;  // G0 is a power of two >= 16
     const int bx = blockIdx.x % nb, by = blockIdx.x / nb;
+    pdl_wait();
     // prefetch: the cell this thread owns at each in-block level
     uint32_t cell[kInLv], m[kInLv];
     Acc a[kInLv];
@@ -439,6 +442,7 @@ struct Epi {
     double* oq;                  // mode 2
     uint32_t* oi;                // mode 2
     uint32_t n;
+    uint32_t* zero_word;         // zeroed at the start of the search (or null)
 };
 
 // Query point: the centre of target pixel sidx[pt] (mode 0; pixel_center,
@@ -565,7 +569,8 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
                                                             uint32_t* __restrict__ hard_count,
                                                             uint32_t* __restrict__ hard_list,
                                                             unsigned long long* __restrict__ hard_stat,
-                                                            uint32_t* __restrict__ next_point) {
+                                                            uint32_t* __restrict__ next_point,
+                                                            uint32_t* __restrict__ zero_next) {
     __shared__ uint32_t queue[4][2][kQueue];
     __shared__ int s_loff[kMaxLv];  // level tables (a dynamic index into the
     __shared__ int s_lg[kMaxLv];    // kernel parameters would go to local memory)
@@ -577,6 +582,11 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
         }
     }
     __syncthreads();
+    pdl_wait();
+    // the other counter pair (hard count, point cursor) and the caller's
+    // word are zeroed for the next search: nothing reads them before it
+    if (blockIdx.x == 0 && threadIdx.x < 2) zero_next[threadIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 2 && E.zero_word) *E.zero_word = 0;
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     // per-level population, one bit per level (same for every point)
@@ -730,6 +740,7 @@ __global__ void __launch_bounds__(kHardThreads) hard_scan_kernel(const ScanRec* 
                                                                  uint32_t* __restrict__ part_i) {
     __shared__ double sq[kHardThreads * KCAP];
     __shared__ uint32_t si[kHardThreads * KCAP];
+    pdl_wait();
     const uint32_t cnt = min(*hard_count, kHardCap);
     const uint32_t per = (n + kHardSplit - 1) / kHardSplit;
     for (uint32_t item = blockIdx.x; item < cnt * kHardSplit; item += gridDim.x) {
@@ -808,6 +819,7 @@ __global__ void __launch_bounds__(128) hard_merge_kernel(const ScanRec* __restri
                                                          unsigned long long* __restrict__ pairs) {
     const uint32_t slot = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
+    pdl_wait();
     if (slot >= min(*hard_count, kHardCap)) return;
     const uint32_t pt = hard_list[slot];
     double px, py;
@@ -831,6 +843,7 @@ __global__ void __launch_bounds__(128) hard_merge_kernel(const ScanRec* __restri
 
 struct KnnBufs {
     DevBuf cnt, off, key, mem, own, sub, cub_tmp, hard, ticket, part, lcount, acc;
+    int hard_phase = 0;  // which (hard count, cursor) pair the next search uses
     int knn_blocks = 0;  // resident CTAs for the persistent query kernel
     uint64_t version = ~0ull;  // params_version the summaries describe
     // refit chain: Adam launches accumulated every Gaussian into acc (by its
@@ -870,9 +883,8 @@ int knn_build(igs_ctx* ctx) {
         // launches since the last build: re-derive the summaries only
         const int nb = (b.lq.G0 + kBlk - 1) / kBlk;
         igs_prof_begin(ctx, IGS_PROF_CULL);
-        lq_tree_kernel<<<nb * nb, 256, 0, ctx->stream>>>((Acc*)b.acc.p, b.lq, (const uint32_t*)b.cnt.p,
-                                                         (Sum*)b.own.p, (Sum*)b.sub.p, (unsigned int*)b.ticket.p);
-        IGS_LAUNCHED(ctx);
+        IGS_PDL(ctx, lq_tree_kernel, nb * nb, 256, 0, (Acc*)b.acc.p, b.lq, (const uint32_t*)b.cnt.p, (Sum*)b.own.p,
+                (Sum*)b.sub.p, (unsigned int*)b.ticket.p);
         igs_prof_end(ctx, IGS_PROF_CULL, 0.0);
         b.since_build++;
         b.version = b.chain = ctx->params_version;
@@ -909,23 +921,19 @@ int knn_build(igs_ctx* ctx) {
     uint32_t* cur = cnt + cells;
     uint32_t* off = (uint32_t*)b.off.p;
     igs_prof_begin(ctx, IGS_PROF_CULL);
-    lq_clear<<<2 * ctx->sm_count, 256, 0, ctx->stream>>>(cells, cnt, (Acc*)b.acc.p, (uint32_t*)b.lcount.p);
-    IGS_LAUNCHED(ctx);
-    lq_count<<<(n + 255) / 256, 256, 0, ctx->stream>>>(ctx->scan, n, L, cnt, (uint32_t*)b.key.p,
-                                                       (uint32_t*)b.lcount.p);
-    IGS_LAUNCHED(ctx);
+    IGS_PDL(ctx, lq_clear, 2 * ctx->sm_count, 256, 0, cells, cnt, (Acc*)b.acc.p, (uint32_t*)b.lcount.p);
+    IGS_PDL(ctx, lq_count, (n + 255) / 256, 256, 0, (const ScanRec*)ctx->scan, n, L, cnt, (uint32_t*)b.key.p,
+            (uint32_t*)b.lcount.p);
     size_t tb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, (int)cells, ctx->stream);
     if (!grow(b.cub_tmp, tb)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn scan)");
     IGS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(b.cub_tmp.p, tb, cnt, off, (int)cells, ctx->stream));
     ctx->launches += 2;
-    lq_fill<<<(n + 255) / 256, 256, 0, ctx->stream>>>(ctx->scan, n, (const uint32_t*)b.key.p, off, cur,
-                                                      (uint32_t*)b.mem.p, (Acc*)b.acc.p);
-    IGS_LAUNCHED(ctx);
+    IGS_PDL(ctx, lq_fill, (n + 255) / 256, 256, 0, (const ScanRec*)ctx->scan, n, (const uint32_t*)b.key.p,
+            (const uint32_t*)off, cur, (uint32_t*)b.mem.p, (Acc*)b.acc.p);
     const int nb = (G0 + kBlk - 1) / kBlk;
-    lq_tree_kernel<<<nb * nb, 256, 0, ctx->stream>>>((Acc*)b.acc.p, L, cnt, (Sum*)b.own.p, (Sum*)b.sub.p,
-                                                     (unsigned int*)b.ticket.p);
-    IGS_LAUNCHED(ctx);
+    IGS_PDL(ctx, lq_tree_kernel, nb * nb, 256, 0, (Acc*)b.acc.p, L, (const uint32_t*)cnt, (Sum*)b.own.p,
+            (Sum*)b.sub.p, (unsigned int*)b.ticket.p);
     igs_prof_end(ctx, IGS_PROF_CULL, 0.0);
     b.lq = L;
     b.builds++;
@@ -939,34 +947,37 @@ int knn_build(igs_ctx* ctx) {
 template <int KCAP>
 int launch_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int kk, const Epi& E) {
     KnnBufs& b = *static_cast<KnnBufs*>(ctx->knn);
-    if (!grow(b.hard, (2 * kHardCap + 2) * 4)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
-    uint32_t* hard_count = (uint32_t*)b.hard.p;  // [0] hard-point count, [1] point cursor, [2..] list
+    if (!b.hard.p) {
+        if (!grow(b.hard, (kHardCap + 4) * 4)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
+        IGS_CUDA(ctx, cudaMemsetAsync(b.hard.p, 0, 16, ctx->stream));
+    }
+    // [0,1] and [2,3]: two (hard-point count, point cursor) pairs used by
+    // alternate searches -- each search zeroes the other pair; [4..] list
+    uint32_t* hard_count = (uint32_t*)b.hard.p + 2 * b.hard_phase;
     uint32_t* cursor = hard_count + 1;
-    uint32_t* hard_list = hard_count + 2;
+    uint32_t* zero_next = (uint32_t*)b.hard.p + 2 * (b.hard_phase ^ 1);
+    uint32_t* hard_list = (uint32_t*)b.hard.p + 4;
+    b.hard_phase ^= 1;
     igs_prof_begin(ctx, IGS_PROF_SCAN);
-    IGS_CUDA(ctx, cudaMemsetAsync(hard_count, 0, 8, ctx->stream));  // hard count + point cursor
     if (b.knn_blocks == 0) {
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, knn_points_kernel, 128, 0);
         b.knn_blocks = std::max(1, per_sm) * ctx->sm_count;
     }
     const unsigned blocks = (unsigned)std::min<uint64_t>(b.knn_blocks, ((uint64_t)npts + 3) / 4);
-    knn_points_kernel<<<blocks, 128, 0, ctx->stream>>>(
-        ctx->scan, ctx->n, b.lq, (const Sum*)b.own.p, (const Sum*)b.sub.p, (const uint32_t*)b.off.p,
-        (const uint32_t*)b.mem.p, uv, W, H, npts, kk, E, igs_prof_counter(ctx, IGS_PROF_SCAN), hard_count,
-        hard_list, igs_prof_counter(ctx, IGS_PROF_KNN_HARD), cursor);
-    IGS_LAUNCHED(ctx);
+    IGS_PDL(ctx, knn_points_kernel, blocks, 128, 0, (const ScanRec*)ctx->scan, ctx->n, b.lq, (const Sum*)b.own.p,
+            (const Sum*)b.sub.p, (const uint32_t*)b.off.p, (const uint32_t*)b.mem.p, uv, W, H, npts, kk, E,
+            igs_prof_counter(ctx, IGS_PROF_SCAN), hard_count, hard_list, igs_prof_counter(ctx, IGS_PROF_KNN_HARD),
+            cursor, zero_next);
     const size_t pitems = (size_t)kHardCap * kHardSplit * kk;
     if (!grow(b.part, pitems * 12)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
     double* part_q = (double*)b.part.p;
     uint32_t* part_i = (uint32_t*)(part_q + pitems);
-    hard_scan_kernel<KCAP><<<2 * ctx->sm_count, kHardThreads, 0, ctx->stream>>>(
-        ctx->scan, ctx->n, uv, W, H, kk, hard_count, hard_list, E, part_q, part_i);
-    IGS_LAUNCHED(ctx);
-    hard_merge_kernel<<<kHardCap * 32 / 128, 128, 0, ctx->stream>>>(ctx->scan, ctx->n, uv, W, H, kk, hard_count,
-                                                                    hard_list, E, part_q, part_i,
-                                                                    igs_prof_counter(ctx, IGS_PROF_SCAN));
-    IGS_LAUNCHED(ctx);
+    IGS_PDL(ctx, hard_scan_kernel<KCAP>, 2 * ctx->sm_count, kHardThreads, 0, (const ScanRec*)ctx->scan, ctx->n, uv,
+            W, H, kk, (const uint32_t*)hard_count, (const uint32_t*)hard_list, E, part_q, part_i);
+    IGS_PDL(ctx, hard_merge_kernel, kHardCap * 32 / 128, 128, 0, (const ScanRec*)ctx->scan, ctx->n, uv, W, H, kk,
+            (const uint32_t*)hard_count, (const uint32_t*)hard_list, E, (const double*)part_q,
+            (const uint32_t*)part_i, igs_prof_counter(ctx, IGS_PROF_SCAN));
     igs_prof_end(ctx, IGS_PROF_SCAN, 0.0);
     return IGS_OK;
 }
@@ -1029,8 +1040,9 @@ int igs_topk_knn(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t*
 // grads_atomic.
 int igs_knn_forward_backward(igs_ctx* ctx, int mode, const uint32_t* sidx, const double* samples5, uint32_t npts,
                              int kk, double inv_n, double* losses, double* contrib, uint32_t* keys, uint32_t* gcnt,
-                             double* grads_atomic) {
+                             double* grads_atomic, uint32_t* zero_word) {
     Epi E{};
+    E.zero_word = zero_word;
     E.gcnt = gcnt;
     E.mode = mode;
     E.sidx = sidx;

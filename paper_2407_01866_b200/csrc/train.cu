@@ -177,6 +177,7 @@ __global__ void scatter_slots_kernel(const uint32_t* __restrict__ keys, uint32_t
                                      const uint32_t* __restrict__ goff, const uint32_t* __restrict__ gcnt,
                                      uint32_t* __restrict__ gcur, uint32_t* __restrict__ perm,
                                      uint32_t* __restrict__ long_count, uint32_t* __restrict__ long_list) {
+    pdl_wait();
     const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
     if (slot >= items) return;
     const uint32_t g = keys[slot];
@@ -254,6 +255,7 @@ __device__ __forceinline__ void store_grad(double* __restrict__ grads, uint32_t 
 __global__ void segment_sum_kernel(const uint32_t* __restrict__ gcnt, const uint32_t* __restrict__ goff,
                                    const uint32_t* __restrict__ perm, const double* __restrict__ contrib, uint32_t n,
                                    double* __restrict__ grads, long long* __restrict__ status) {
+    pdl_wait();
     const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
     const uint32_t m = gcnt[g];
@@ -279,6 +281,7 @@ __global__ void __launch_bounds__(256) long_segment_kernel(const uint32_t* __res
                                                            const uint32_t* __restrict__ long_count,
                                                            const uint32_t* __restrict__ long_list,
                                                            long long* __restrict__ status) {
+    pdl_wait();
     __shared__ uint32_t keys[kLongCap];
     __shared__ double rows[256][8];
     const uint32_t total = *long_count;
@@ -379,6 +382,7 @@ __global__ void loss_reduce_kernel(const double* __restrict__ losses, uint32_t n
 
 // Non-finite gradient scan: status[0] <- first bad slot i*8+p (min).
 __global__ void grad_check_kernel(const double* __restrict__ grads, uint32_t n, long long* __restrict__ status) {
+    pdl_wait();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
 #pragma unroll
@@ -498,6 +502,7 @@ __global__ void adam_kernel(double* __restrict__ params, const double* __restric
                             double* __restrict__ v, ScanRec* __restrict__ scan, ShadeRec* __restrict__ shade,
                             uint32_t n, double lr_mu, double lr_color, double lr_scale, double lr_theta, double bc1,
                             double bc2, long long* __restrict__ status, TreeAcc ta) {
+    pdl_wait();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     if (status[0] != LLONG_MAX || status[2] != LLONG_MAX) {
@@ -530,6 +535,7 @@ __global__ void segment_adam_kernel(uint32_t* __restrict__ gcnt, const uint32_t*
                                     ShadeRec* __restrict__ shade, double lr_mu, double lr_color, double lr_scale,
                                     double lr_theta, double bc1, double bc2, long long* __restrict__ status,
                                     TreeAcc ta) {
+    pdl_wait();
     const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
     // the parameter/moment loads do not depend on the reduction: issue first
@@ -571,6 +577,7 @@ __global__ void segment_adam_kernel(uint32_t* __restrict__ gcnt, const uint32_t*
 }
 
 __global__ void reset_status_kernel(long long* status) {
+    pdl_wait();
     if (threadIdx.x < 3) status[threadIdx.x] = LLONG_MAX;
     if (threadIdx.x == 3) status[3] = 0;  // a count (kNN tree growth)
 }
@@ -612,8 +619,7 @@ __global__ void blend_points_kernel(const double* __restrict__ lq, const uint32_
 // 24 long-segment queue.
 
 int igs_status_reset(igs_ctx* ctx) {
-    reset_status_kernel<<<1, 32, 0, ctx->stream>>>(ctx->status);
-    IGS_LAUNCHED(ctx);
+    IGS_PDL(ctx, reset_status_kernel, 1, 32, 0, ctx->status);
     return IGS_OK;
 }
 
@@ -644,8 +650,9 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
         if (ctx->gcnt_clean != gcnt || ctx->gcnt_clean_n != n)
             IGS_CUDA(ctx, cudaMemsetAsync(gcnt, 0, (size_t)n * 2 * sizeof(uint32_t), ctx->stream));
         ctx->gcnt_clean = nullptr;
-        IGS_CUDA(ctx, cudaMemsetAsync(long_ctl, 0, sizeof(uint32_t), ctx->stream));
-        // (long_ctl[0]: long-segment count; long_ctl[1..]: the queue)
+        // (long_ctl[0]: long-segment count, zeroed by the search kernel on the
+        // fused path; long_ctl[1..]: the queue)
+        if (!(ctx->opt_cull && kk <= 32)) IGS_CUDA(ctx, cudaMemsetAsync(long_ctl, 0, sizeof(uint32_t), ctx->stream));
     } else {
         IGS_CUDA(ctx, cudaMemsetAsync(ctx->grads, 0, (size_t)n * 8 * sizeof(double), ctx->stream));
     }
@@ -654,7 +661,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
     if (ctx->opt_cull && kk <= 32) {
         // fused: exact top-K search + blend / loss / gradient epilogue per warp
         e = igs_knn_forward_backward(ctx, mode, dev_sidx, dev_samples5, ns, kk, inv_n, losses, contrib, keys, gcnt,
-                                     ctx->opt_deterministic ? nullptr : ctx->grads);
+                                     ctx->opt_deterministic ? nullptr : ctx->grads, long_ctl);
         if (e) return e;
         gcnt_filled = true;
     } else {
@@ -703,12 +710,12 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
         if (!temp) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (scan)");
         IGS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(temp, tb, gcnt, goff, (int)n, ctx->stream));
         ctx->launches += 2;
-        scatter_slots_kernel<<<(unsigned)((items + 255) / 256), 256, 0, ctx->stream>>>(
-            keys, (uint32_t)items, n, goff, gcnt, gcnt + n, perm, long_ctl, long_ctl + 1);
-        IGS_LAUNCHED(ctx);
-        long_segment_kernel<<<ctx->sm_count, 256, 0, ctx->stream>>>(gcnt, goff, perm, contrib, ctx->grads, long_ctl,
-                                                                    long_ctl + 1, ctx->status);
-        IGS_LAUNCHED(ctx);
+        IGS_PDL(ctx, scatter_slots_kernel, (unsigned)((items + 255) / 256), 256, 0, (const uint32_t*)keys,
+                (uint32_t)items, n, (const uint32_t*)goff, (const uint32_t*)gcnt, gcnt + n, perm, long_ctl,
+                long_ctl + 1);
+        IGS_PDL(ctx, long_segment_kernel, ctx->sm_count, 256, 0, (const uint32_t*)gcnt, (const uint32_t*)goff, perm,
+                (const double*)contrib, ctx->grads, (const uint32_t*)long_ctl, (const uint32_t*)(long_ctl + 1),
+                ctx->status);
         if (fuse_lr4 && ctx->nranks == 1 && !ctx->comm) {
             // short segments summed inside the Adam kernel (one pass over the set)
             const double bc1 = 1.0 - std::pow(0.9, (double)t);  // adam.cpp:16-17, host libm
@@ -717,18 +724,17 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
             ctx->params_version++;
             igs_prof_end(ctx, IGS_PROF_REDUCE, (double)items);
             igs_prof_begin(ctx, IGS_PROF_ADAM);
-            segment_adam_kernel<<<(n + 255) / 256, 256, 0, ctx->stream>>>(
-                gcnt, goff, perm, contrib, n, ctx->grads, ctx->params, ctx->adam_m, ctx->adam_v, ctx->scan,
-                ctx->shade, fuse_lr4[0], fuse_lr4[1], fuse_lr4[2], fuse_lr4[3], bc1, bc2, ctx->status, ta);
-            IGS_LAUNCHED(ctx);
+            IGS_PDL(ctx, segment_adam_kernel, (n + 255) / 256, 256, 0, gcnt, (const uint32_t*)goff,
+                    (const uint32_t*)perm, (const double*)contrib, n, ctx->grads, ctx->params, ctx->adam_m,
+                    ctx->adam_v, ctx->scan, ctx->shade, fuse_lr4[0], fuse_lr4[1], fuse_lr4[2], fuse_lr4[3], bc1, bc2,
+                    ctx->status, ta);
             igs_prof_end(ctx, IGS_PROF_ADAM, (double)n * 544.0);
             ctx->gcnt_clean = gcnt;
             ctx->gcnt_clean_n = n;
             if (fused) *fused = true;
         } else {
-            segment_sum_kernel<<<(n + 255) / 256, 256, 0, ctx->stream>>>(gcnt, goff, perm, contrib, n, ctx->grads,
-                                                                         ctx->status);
-            IGS_LAUNCHED(ctx);
+            IGS_PDL(ctx, segment_sum_kernel, (n + 255) / 256, 256, 0, (const uint32_t*)gcnt, (const uint32_t*)goff,
+                    (const uint32_t*)perm, (const double*)contrib, n, ctx->grads, ctx->status);
             igs_prof_end(ctx, IGS_PROF_REDUCE, (double)items);
         }
         ctx->grads_checked = true;
@@ -741,8 +747,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
 }
 
 int igs_grad_check(igs_ctx* ctx) {
-    grad_check_kernel<<<(ctx->n + 255) / 256, 256, 0, ctx->stream>>>(ctx->grads, ctx->n, ctx->status);
-    IGS_LAUNCHED(ctx);
+    IGS_PDL(ctx, grad_check_kernel, (ctx->n + 255) / 256, 256, 0, (const double*)ctx->grads, ctx->n, ctx->status);
     return IGS_OK;
 }
 
@@ -753,10 +758,8 @@ int igs_adam_launch(igs_ctx* ctx, const double* lr4, long long t) {
     const TreeAcc ta = igs_knn_tree_acc(ctx);
     ctx->params_version++;
     igs_prof_begin(ctx, IGS_PROF_ADAM);
-    adam_kernel<<<(ctx->n + 255) / 256, 256, 0, ctx->stream>>>(ctx->params, ctx->grads, ctx->adam_m, ctx->adam_v,
-                                                               ctx->scan, ctx->shade, ctx->n, lr4[0], lr4[1], lr4[2],
-                                                               lr4[3], bc1, bc2, ctx->status, ta);
-    IGS_LAUNCHED(ctx);
+    IGS_PDL(ctx, adam_kernel, (ctx->n + 255) / 256, 256, 0, ctx->params, (const double*)ctx->grads, ctx->adam_m,
+            ctx->adam_v, ctx->scan, ctx->shade, ctx->n, lr4[0], lr4[1], lr4[2], lr4[3], bc1, bc2, ctx->status, ta);
     // algorithmic bytes: read params/grads/m/v (256 B), write params/m/v
     // (192 B) and the refreshed 96 B of scan+shade records
     igs_prof_end(ctx, IGS_PROF_ADAM, (double)ctx->n * 544.0);
