@@ -141,6 +141,60 @@ IGS_HD void dd_sincos_reduced(dd r, dd* s, dd* c) {
     *c = pc;
 }
 
+// dd + dd where |a| >= |b| is known (Horner steps c_k + z*S with the
+// coefficient dominating): cheaper than the general dd_add.
+IGS_HD dd dd_add_big(dd a, dd b) {
+    const double s = a.hi + b.hi;
+    const double e = ((a.hi - s) + b.hi) + (a.lo + b.lo);
+    return quick_two_sum(s, e);
+}
+
+// Fast path (Ziv): sin(r), cos(r) for the reduced r with the three leading
+// Taylor coefficients in double-double and the tail -- below 2^-14 (sin) /
+// 2^-18 (cos) of the result -- in double.  The evaluation error is below
+// 2^-66 relative (largest seen against the full series over 2M angles:
+// 2^-70 for cos, 2^-73 for sin); the doubles are accepted only when
+// rounding is the same at both ends of a 2^-65 relative interval,
+// otherwise (about 1 in 2^11 values) the caller runs the full series.
+IGS_HD bool fast_sincos_reduced(dd r, double* sh_out, double* ch_out) {
+    const dd z = dd_mul(r, r);
+    const double zd = z.hi;
+    // sin(r) = r (1 + z P),  P = -1/3! + z/5! - z^2/7! + z^3 Ts
+    double ts = -3.868170170630684e-23;  // -1/23!
+    ts = ts * zd + 1.9572941063391263e-20;   // 1/21!
+    ts = ts * zd - 8.22063524662433e-18;     // -1/19!
+    ts = ts * zd + 2.8114572543455206e-15;   // 1/17!
+    ts = ts * zd - 7.647163731819816e-13;    // -1/15!
+    ts = ts * zd + 1.6059043836821613e-10;   // 1/13!
+    ts = ts * zd - 2.505210838544172e-08;    // -1/11!
+    ts = ts * zd + 2.7557319223985893e-06;   // 1/9!
+    dd ps = dd_add_big(dd{-0.0001984126984126984, -1.7209558293420705e-22}, two_prod(zd, ts));  // -1/7!
+    ps = dd_add_big(dd{0.008333333333333333, 1.1564823173178714e-19}, dd_mul(z, ps));          // 1/5!
+    ps = dd_add_big(dd{-0.16666666666666666, -9.25185853854297e-18}, dd_mul(z, ps));           // -1/3!
+    const dd s = dd_add(r, dd_mul(r, dd_mul(z, ps)));
+    // cos(r) = 1 + z Q,  Q = -1/2! + z/4! - z^2/6! + z^3 Tc
+    double tc = 1.6117375710961184e-24;      // 1/24!
+    tc = tc * zd - 8.896791392450574e-22;    // -1/22!
+    tc = tc * zd + 4.110317623312165e-19;    // 1/20!
+    tc = tc * zd - 1.5619206968586225e-16;   // -1/18!
+    tc = tc * zd + 4.779477332387385e-14;    // 1/16!
+    tc = tc * zd - 1.1470745597729725e-11;   // -1/14!
+    tc = tc * zd + 2.08767569878681e-09;     // 1/12!
+    tc = tc * zd - 2.755731922398589e-07;    // -1/10!
+    tc = tc * zd + 2.48015873015873e-05;     // 1/8!
+    dd pc = dd_add_big(dd{-0.001388888888888889, 5.300543954373577e-20}, two_prod(zd, tc));    // -1/6!
+    pc = dd_add_big(dd{0.041666666666666664, 2.3129646346357427e-18}, dd_mul(z, pc));         // 1/4!
+    pc = dd_add_big(dd{-0.5, 0.0}, dd_mul(z, pc));                                            // -1/2!
+    const dd c = dd_add_big(dd{1.0, 0.0}, dd_mul(z, pc));
+    // rounding test at +-2^-65 relative
+    const double es = fabs(s.hi) * 0x1p-65, ec = fabs(c.hi) * 0x1p-65;
+    const double s0 = s.hi + (s.lo - es), s1 = s.hi + (s.lo + es);
+    const double c0 = c.hi + (c.lo - ec), c1 = c.hi + (c.lo + ec);
+    *sh_out = s0;
+    *ch_out = c0;
+    return s0 == s1 && c0 == c1;
+}
+
 // Correctly rounded (except on hard cases) sin and cos of x.
 IGS_HD void cr_sincos(double x, double* sin_out, double* cos_out) {
     if (!(fabs(x) < 524288.0)) {  // huge or non-finite: libm semantics
@@ -155,6 +209,29 @@ IGS_HD void cr_sincos(double x, double* sin_out, double* cos_out) {
     }
     int q;
     const dd r = reduce_pio2(x, &q);
+    double sh, ch;
+    if (!fast_sincos_reduced(r, &sh, &ch)) {
+        dd s, c;
+        dd_sincos_reduced(r, &s, &c);
+        sh = s.hi + s.lo;
+        ch = c.hi + c.lo;
+    }
+    switch (q) {
+        case 0: *sin_out = sh; *cos_out = ch; break;
+        case 1: *sin_out = ch; *cos_out = -sh; break;
+        case 2: *sin_out = -sh; *cos_out = -ch; break;
+        default: *sin_out = -ch; *cos_out = sh; break;
+    }
+}
+
+// The full series only (tests compare the fast path against it).
+IGS_HD void cr_sincos_full(double x, double* sin_out, double* cos_out) {
+    if (!(fabs(x) < 524288.0) || x == 0.0) {
+        cr_sincos(x, sin_out, cos_out);
+        return;
+    }
+    int q;
+    const dd r = reduce_pio2(x, &q);
     dd s, c;
     dd_sincos_reduced(r, &s, &c);
     const double sh = s.hi + s.lo, ch = c.hi + c.lo;
@@ -164,6 +241,22 @@ IGS_HD void cr_sincos(double x, double* sin_out, double* cos_out) {
         case 2: *sin_out = -sh; *cos_out = -ch; break;
         default: *sin_out = -ch; *cos_out = sh; break;
     }
+}
+
+// a / b correctly rounded, from y = RN(1/b) computed once for many a (the
+// Adam bias corrections are per-step constants): q0 = a*y is within 1.5 ulp
+// of a/b; one Markstein correction q + (a - b q) y brings it within 1 ulp,
+// and a second one -- Markstein's theorem: y = RN(1/b) and q within 1 ulp
+// => RN(q + r y) = RN(a/b) -- rounds correctly.  Requires normal operands
+// away from the exponent limits (the caller checks 2^-960 <= |a| <= 2^1000,
+// 2^-20 <= b <= 2^20); tests/test_math_host.py checks it against IEEE
+// division on random, per-step and near-midpoint operands.
+IGS_HD double div_by_recip(double a, double b, double y) {
+    double q = a * y;
+    double r = fma(-b, q, a);
+    q = fma(r, y, q);
+    r = fma(-b, q, a);
+    return fma(r, y, q);
 }
 
 }  // namespace igs_math

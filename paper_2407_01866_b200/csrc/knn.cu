@@ -81,7 +81,7 @@ __global__ void lq_count(const ScanRec* __restrict__ scan, uint32_t n, Lq L, uin
         l = level_of(L, fmin(r.inv_a, r.inv_b));
         const int G = L.lw[l];
         const uint32_t k = (uint32_t)(L.loff[l] + cell_of(r.mu_y, G) * G + cell_of(r.mu_x, G));
-        key[i] = k;
+        key[i] = k | ((uint32_t)l << kKeyLevelShift);
         atomicAdd(cnt + k, 1u);
     }
     // per-level population, warp-aggregated (13 addresses would serialise)
@@ -108,7 +108,7 @@ __global__ void lq_fill(const ScanRec* __restrict__ scan, uint32_t n, const uint
     pdl_wait();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const uint32_t k = key[i];
+    const uint32_t k = key[i] & kKeyCellMask;
     mem[off[k] + atomicAdd(cur + k, 1u)] = i;
     acc_add(acc + k, scan[i]);
 }

@@ -12,6 +12,9 @@
 namespace igs_dev {
 
 constexpr int kMaxLv = 13;
+// key[i] = cell | level << 27 (cells < 2^25 for G0 <= 4096)
+constexpr int kKeyLevelShift = 27;
+constexpr uint32_t kKeyCellMask = (1u << kKeyLevelShift) - 1;
 
 struct Lq {
     int G0, levels;
@@ -82,21 +85,19 @@ struct TreeAcc {
     Lq L;
 };
 
-__device__ __forceinline__ int level_of_cell(const Lq& L, uint32_t c) {
-    int l = 0;
-    while (l + 1 < L.levels && (uint32_t)L.loff[l + 1] <= c) ++l;
-    return l;
-}
-
 // Accumulates Gaussian i (record r) into its stored cell and counts it in
 // *grown when its scale now calls for a coarser level than the one it is
 // stored at: such a Gaussian weakens the bounds of its cell and every
-// ancestor, so the host re-buckets before the next search (knn_build).
+// ancestor, so the host re-buckets before the next search (knn_build).  The
+// level here is a float estimate of level_of: it only steers that decision.
 __device__ __forceinline__ void tree_acc_add(const TreeAcc& ta, uint32_t i, const ScanRec& r) {
     if (!ta.acc) return;
-    const uint32_t c = ta.key[i];
-    acc_add(ta.acc + c, r);
-    const bool grew = level_of(ta.L, fmin(r.inv_a, r.inv_b)) > level_of_cell(ta.L, c);
+    const uint32_t k = ta.key[i];
+    acc_add(ta.acc + (k & kKeyCellMask), r);
+    // level_of: smallest l with cell 2^l / G0 >= 2 sigma_max = 2 / sqrt(lmin)
+    const float lmin = (float)fmin(r.inv_a, r.inv_b);
+    const float l = fminf(ceilf(log2f(2.0f * (float)ta.L.G0 * rsqrtf(lmin))), (float)(ta.L.levels - 1));
+    const bool grew = l > (float)(k >> kKeyLevelShift);  // NaN compares false
     const unsigned act = __activemask();
     const unsigned m = __ballot_sync(act, grew);
     if (m && (threadIdx.x & 31) == __ffs(act) - 1) atomicAdd(ta.grown, (unsigned long long)__popc(m));

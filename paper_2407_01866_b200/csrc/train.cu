@@ -401,6 +401,15 @@ __device__ __forceinline__ double div_rn(double a, double b) {
                                                                                          : __ddiv_rn(a, b);
 }
 
+// a / b for the per-step constants b = bc1, bc2 with y = RN(1/b) from the
+// host: two Markstein corrections (igs_math::div_by_recip), exact IEEE
+// division outside its operand range (zero, tiny, huge, non-finite).
+__device__ __forceinline__ double div_const(double a, double b, double y) {
+    const double aa = fabs(a);
+    if (aa >= 0x1p-960 && aa <= 0x1p1000) return igs_math::div_by_recip(a, b, y);
+    return div_rn(a, b);
+}
+
 __device__ __forceinline__ double clamp01d(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
 __device__ __forceinline__ double clamp_scale(double v) {
     return v < kScaleMin ? kScaleMin : (v > kScaleMax ? kScaleMax : v);
@@ -428,7 +437,8 @@ __device__ __forceinline__ void adam_one(uint32_t i, const double* gg, double* g
                                          double* __restrict__ params, double* __restrict__ m, double* __restrict__ v,
                                          ScanRec* __restrict__ scan, ShadeRec* __restrict__ shade, double lr_mu,
                                          double lr_color, double lr_scale, double lr_theta, double bc1, double bc2,
-                                         long long* __restrict__ status, const TreeAcc& ta) {
+                                         double ibc1, double ibc2, long long* __restrict__ status,
+                                         const TreeAcc& ta) {
     const double b1 = 0.9, b2 = 0.999, eps = 1e-8;  // adam.hpp:33-35
     const double omb1 = 1.0 - b1, omb2 = 1.0 - b2;  // folded exactly like the reference's constants
     const double lr8[8] = {lr_mu, lr_mu, lr_theta, lr_scale, lr_scale, lr_color, lr_color, lr_color};
@@ -437,8 +447,8 @@ __device__ __forceinline__ void adam_one(uint32_t i, const double* gg, double* g
         const double g = gg[p];
         mm[p] = __dadd_rn(__dmul_rn(b1, mm[p]), __dmul_rn(omb1, g));
         vv[p] = __dadd_rn(__dmul_rn(b2, vv[p]), __dmul_rn(__dmul_rn(omb2, g), g));
-        const double m_hat = div_rn(mm[p], bc1);
-        const double v_hat = div_rn(vv[p], bc2);
+        const double m_hat = div_const(mm[p], bc1, ibc1);
+        const double v_hat = div_const(vv[p], bc2, ibc2);
         const double upd = div_rn(__dmul_rn(lr8[p], m_hat), __dadd_rn(__dsqrt_rn(v_hat), eps));
         gp[p] = __dsub_rn(gp[p], upd);
     }
@@ -501,7 +511,7 @@ __device__ __forceinline__ void adam_one(uint32_t i, const double* gg, double* g
 __global__ void adam_kernel(double* __restrict__ params, const double* __restrict__ grads, double* __restrict__ m,
                             double* __restrict__ v, ScanRec* __restrict__ scan, ShadeRec* __restrict__ shade,
                             uint32_t n, double lr_mu, double lr_color, double lr_scale, double lr_theta, double bc1,
-                            double bc2, long long* __restrict__ status, TreeAcc ta) {
+                            double bc2, double ibc1, double ibc2, long long* __restrict__ status, TreeAcc ta) {
     pdl_wait();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -518,7 +528,8 @@ __global__ void adam_kernel(double* __restrict__ params, const double* __restric
         gg[2 * h + 1] = b.y;
     }
     adam_load(i, params, m, v, gp, mm, vv);
-    adam_one(i, gg, gp, mm, vv, params, m, v, scan, shade, lr_mu, lr_color, lr_scale, lr_theta, bc1, bc2, status, ta);
+    adam_one(i, gg, gp, mm, vv, params, m, v, scan, shade, lr_mu, lr_color, lr_scale, lr_theta, bc1, bc2, ibc1, ibc2,
+             status, ta);
 }
 
 // Fused short-segment reduction + Adam (single rank): thread g sums its
@@ -528,13 +539,16 @@ __global__ void adam_kernel(double* __restrict__ params, const double* __restric
 // finite Gaussian is still updated, deterministically; the reference has
 // updated Gaussians 0..i-1 when it throws, adam.cpp:29-31).  A non-finite
 // loss (flagged by the search epilogue) skips the whole step, as fit.cpp:155.
-__global__ void segment_adam_kernel(uint32_t* __restrict__ gcnt, const uint32_t* __restrict__ goff,
+#ifndef IGS_ADAM_MINB
+#define IGS_ADAM_MINB 3
+#endif
+__global__ void __launch_bounds__(256, IGS_ADAM_MINB) segment_adam_kernel(uint32_t* __restrict__ gcnt, const uint32_t* __restrict__ goff,
                                     const uint32_t* __restrict__ perm, const double* __restrict__ contrib,
                                     uint32_t n, double* __restrict__ grads, double* __restrict__ params,
                                     double* __restrict__ m, double* __restrict__ v, ScanRec* __restrict__ scan,
                                     ShadeRec* __restrict__ shade, double lr_mu, double lr_color, double lr_scale,
-                                    double lr_theta, double bc1, double bc2, long long* __restrict__ status,
-                                    TreeAcc ta) {
+                                    double lr_theta, double bc1, double bc2, double ibc1, double ibc2,
+                                    long long* __restrict__ status, TreeAcc ta) {
     pdl_wait();
     const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
@@ -573,7 +587,8 @@ __global__ void segment_adam_kernel(uint32_t* __restrict__ gcnt, const uint32_t*
             tree_acc_add(ta, g, scan[g]);
             return;
         }
-    adam_one(g, acc, gp, mm, vv, params, m, v, scan, shade, lr_mu, lr_color, lr_scale, lr_theta, bc1, bc2, status, ta);
+    adam_one(g, acc, gp, mm, vv, params, m, v, scan, shade, lr_mu, lr_color, lr_scale, lr_theta, bc1, bc2, ibc1, ibc2,
+             status, ta);
 }
 
 __global__ void reset_status_kernel(long long* status) {
@@ -727,7 +742,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
             IGS_PDL(ctx, segment_adam_kernel, (n + 255) / 256, 256, 0, gcnt, (const uint32_t*)goff,
                     (const uint32_t*)perm, (const double*)contrib, n, ctx->grads, ctx->params, ctx->adam_m,
                     ctx->adam_v, ctx->scan, ctx->shade, fuse_lr4[0], fuse_lr4[1], fuse_lr4[2], fuse_lr4[3], bc1, bc2,
-                    ctx->status, ta);
+                    1.0 / bc1, 1.0 / bc2, ctx->status, ta);
             igs_prof_end(ctx, IGS_PROF_ADAM, (double)n * 544.0);
             ctx->gcnt_clean = gcnt;
             ctx->gcnt_clean_n = n;
@@ -759,7 +774,8 @@ int igs_adam_launch(igs_ctx* ctx, const double* lr4, long long t) {
     ctx->params_version++;
     igs_prof_begin(ctx, IGS_PROF_ADAM);
     IGS_PDL(ctx, adam_kernel, (ctx->n + 255) / 256, 256, 0, ctx->params, (const double*)ctx->grads, ctx->adam_m,
-            ctx->adam_v, ctx->scan, ctx->shade, ctx->n, lr4[0], lr4[1], lr4[2], lr4[3], bc1, bc2, ctx->status, ta);
+            ctx->adam_v, ctx->scan, ctx->shade, ctx->n, lr4[0], lr4[1], lr4[2], lr4[3], bc1, bc2, 1.0 / bc1,
+            1.0 / bc2, ctx->status, ta);
     // algorithmic bytes: read params/grads/m/v (256 B), write params/m/v
     // (192 B) and the refreshed 96 B of scan+shade records
     igs_prof_end(ctx, IGS_PROF_ADAM, (double)ctx->n * 544.0);

@@ -68,3 +68,106 @@ def test_glibc_disagreement_rate(harness):
     ms, mc = map(int, subprocess.run([str(harness), str(n)], capture_output=True, text=True,
                                      check=True).stdout.split())
     assert ms / n < 0.005 and mc / n < 0.005
+
+
+DIV_HARNESS = r"""
+#include "HDR"
+#include <cstdio>
+#include <cstdlib>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+static uint64_t x = 88172645463325252ull;
+static uint64_t nxt() { x ^= x << 13; x ^= x >> 7; x ^= x << 17; return x; }
+static double unif() { return (nxt() >> 11) * 0x1.0p-53; }
+int main() {
+  long bad = 0, n = 0;
+  // Adam's bias corrections for t = 1..20000 against moments over many scales
+  for (int t = 1; t <= 20000; ++t) {
+    const double bs[2] = {1.0 - pow(0.9, (double)t), 1.0 - pow(0.999, (double)t)};
+    for (double b : bs) {
+      const double y = 1.0 / b;
+      for (int j = 0; j < 200; ++j) {
+        double a = ldexp(1.0 + unif(), (int)(nxt() % 1400) - 700);
+        if (nxt() & 1) a = -a;
+        ++n; bad += igs_math::div_by_recip(a, b, y) != a / b;
+      }
+    }
+  }
+  // random divisors
+  for (int j = 0; j < 3000000; ++j) {
+    const double b = ldexp(1.0 + unif(), (int)(nxt() % 40) - 20);
+    const double a = ldexp(1.0 + unif(), (int)(nxt() % 1400) - 700);
+    ++n; bad += igs_math::div_by_recip(a, b, 1.0 / b) != a / b;
+  }
+  // near-midpoint quotients: a = RN(b * m) for m a midpoint between doubles
+  for (int j = 0; j < 3000000; ++j) {
+    const double b = ldexp(1.0 + unif(), (int)(nxt() % 40) - 20);
+    const double q = ldexp(1.0 + unif(), (int)(nxt() % 200) - 100);
+    const double m = q + 0.5 * (nextafter(q, INFINITY) - q);  // rounds; use long double for the product
+    long double mm = (long double)q + 0.5L * ((long double)nextafter(q, INFINITY) - (long double)q);
+    const double a = (double)((long double)b * mm);
+    (void)m;
+    ++n; bad += igs_math::div_by_recip(a, b, 1.0 / b) != a / b;
+    const double a2 = nextafter(a, INFINITY), a3 = nextafter(a, -INFINITY);
+    n += 2; bad += (igs_math::div_by_recip(a2, b, 1.0 / b) != a2 / b) + (igs_math::div_by_recip(a3, b, 1.0 / b) != a3 / b);
+  }
+  printf("%ld %ld\n", bad, n);
+}
+"""
+
+
+def test_div_by_recip_correctly_rounded(tmp_path):
+    src = tmp_path / "d.cpp"
+    src.write_text(DIV_HARNESS.replace("HDR", str(HDR)))
+    exe = tmp_path / "d"
+    subprocess.run(["g++", "-O2", "-ffp-contract=off", "-std=c++17", str(src), "-o", str(exe)], check=True)
+    bad, n = map(int, subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split())
+    assert n > 10_000_000
+    assert bad == 0
+
+
+FAST_HARNESS = r"""
+#include "HDR"
+#include <cstdio>
+#include <cstdint>
+#include <cmath>
+static uint64_t x = 0x9E3779B97F4A7C15ull;
+static uint64_t nxt() { x ^= x << 13; x ^= x >> 7; x ^= x << 17; return x; }
+int main() {
+  long n = 0, diff = 0, slow = 0;
+  for (int j = 0; j < 4000000; ++j) {
+    double th;
+    switch (j & 3) {
+      case 0: th = (nxt() >> 11) * 0x1.0p-53 * 3.141592653589793; break;   // constrain's range
+      case 1: th = ((nxt() >> 11) * 0x1.0p-53 - 0.5) * 2000.0; break;     // wide
+      case 2: th = ldexp((nxt() >> 11) * 0x1.0p-53, -(int)(nxt() % 60)); break;  // tiny
+      default: {  // next to multiples of pi/2
+        const int k = (int)(nxt() % 5);
+        th = k * 1.5707963267948966;
+        for (int s = (int)(nxt() % 9); s > 0; --s) th = nextafter(th, (nxt() & 1) ? INFINITY : -INFINITY);
+      }
+    }
+    int q; const igs_math::dd r = igs_math::reduce_pio2(th, &q);
+    double a, b; slow += !igs_math::fast_sincos_reduced(r, &a, &b);
+    double s1, c1, s2, c2;
+    igs_math::cr_sincos(th, &s1, &c1);
+    igs_math::cr_sincos_full(th, &s2, &c2);
+    ++n; diff += (s1 != s2 || c1 != c2) && th != 0.0;
+  }
+  printf("%ld %ld %ld\n", diff, slow, n);
+}
+"""
+
+
+def test_fast_sincos_path_matches_full_series(tmp_path):
+    """The Ziv fast path (three leading terms in double-double, tail in
+    double, rounding test at 2^-65) returns exactly what the full
+    double-double series rounds to, and falls back rarely."""
+    src = tmp_path / "f.cpp"
+    src.write_text(FAST_HARNESS.replace("HDR", str(HDR)))
+    exe = tmp_path / "f"
+    subprocess.run(["g++", "-O2", "-ffp-contract=off", "-std=c++17", str(src), "-o", str(exe)], check=True)
+    diff, slow, n = map(int, subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split())
+    assert diff == 0
+    assert slow / n < 0.002, slow / n
