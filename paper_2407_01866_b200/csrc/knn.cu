@@ -606,24 +606,39 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
     t.init(kk, lane);
     unsigned long long evaluated = 0;
 
-    // (1) seeds: own members of the 3x3 window at every populated level
+    // (1) seeds: the 3x3 cells around the point at every populated level.
+    // Pass 0 evaluates the point's own cell at each level and the whole
+    // window at the finest populated level (a tight threshold at once);
+    // pass 1 evaluates the other window cells whose own bound survives it.
     const int nseed = npop * 9;
-    for (int base = 0; base < nseed; base += 32) {
-        const int it = base + lane;
-        uint32_t o = 0, m = 0;
-        if (it < nseed) {
-            // it-th populated level
-            unsigned mm = lvmask;
-            for (int skip = it / 9; skip > 0; --skip) mm &= mm - 1;
-            const int l = __ffs(mm) - 1, d = it % 9, lg = s_lg[l], G = 1 << lg;
-            const int x = cell_of(px, G) + d % 3 - 1, y = cell_of(py, G) + d / 3 - 1;
-            if (x >= 0 && x < G && y >= 0 && y < G) {
-                const uint32_t c = (uint32_t)(s_loff[l] + (y << lg) + x);
-                o = off[c];
-                m = own[c].count;
+    const int lfine = __ffs(lvmask) - 1;
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int base = 0; base < nseed; base += 32) {
+            const int it = base + lane;
+            uint32_t o = 0, m = 0;
+            if (it < nseed) {
+                // it-th populated level
+                unsigned mm = lvmask;
+                for (int skip = it / 9; skip > 0; --skip) mm &= mm - 1;
+                const int l = __ffs(mm) - 1, d = it % 9, lg = s_lg[l], G = 1 << lg;
+                const int x = cell_of(px, G) + d % 3 - 1, y = cell_of(py, G) + d / 3 - 1;
+                const bool primary = d == 4 || l == lfine;
+                if (x >= 0 && x < G && y >= 0 && y < G && primary == (pass == 0)) {
+                    const uint32_t c = (uint32_t)(s_loff[l] + (y << lg) + x);
+                    if (primary) {
+                        o = off[c];
+                        m = own[c].count;
+                    } else {
+                        const Sum so = own[c];
+                        if (so.count && sum_lb(so, px, py) <= t.tq()) {
+                            o = off[c];
+                            m = so.count;
+                        }
+                    }
+                }
             }
+            eval_members(t, o, m, lane, scan, mem, px, py, evaluated);
         }
-        eval_members(t, o, m, lane, scan, mem, px, py, evaluated);
     }
 
     bool overflow = false;
