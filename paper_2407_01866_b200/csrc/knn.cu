@@ -378,6 +378,7 @@ template <class TK>
 __device__ __forceinline__ void eval_members(TK& t, uint32_t o_mine, uint32_t m_mine, int lane,
                                              const ScanRec* __restrict__ scan, const uint32_t* __restrict__ mem,
                                              double px, double py, unsigned long long& evaluated) {
+    if (__ballot_sync(0xffffffffu, m_mine != 0) == 0) return;  // nothing to evaluate (common)
     uint32_t incl = m_mine;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
