@@ -595,6 +595,9 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
     if (lane < L.levels && L.lcount[lane] > 0) lvmask = 1u;
     lvmask = __ballot_sync(0xffffffffu, lvmask);
     const int npop = __popc(lvmask);
+    // lane j < npop: the j-th populated level (seed item it -> level of lane it / 9)
+    const int my_pop = lane < npop ? __fns(lvmask, 0, lane + 1) : 0;
+    const int lg0 = s_lg[0];
     // persistent warps: pull points until none are left (no wave tail)
     for (;;) {
     uint32_t pt = 0;
@@ -613,16 +616,17 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
     // pass 1 evaluates the other window cells whose own bound survives it.
     const int nseed = npop * 9;
     const int lfine = __ffs(lvmask) - 1;
+    // the point's cell at level 0; at level l it is (cx0 >> l, cy0 >> l)
+    // (G_l = G0 >> l, so floor(v G_l) = floor(v G0) >> l)
+    const int cx0 = cell_of(px, 1 << lg0), cy0 = cell_of(py, 1 << lg0);
     for (int pass = 0; pass < 2; ++pass) {
         for (int base = 0; base < nseed; base += 32) {
             const int it = base + lane;
+            const int l = __shfl_sync(0xffffffffu, my_pop, min(it / 9, 31));
             uint32_t o = 0, m = 0;
             if (it < nseed) {
-                // it-th populated level
-                unsigned mm = lvmask;
-                for (int skip = it / 9; skip > 0; --skip) mm &= mm - 1;
-                const int l = __ffs(mm) - 1, d = it % 9, lg = s_lg[l], G = 1 << lg;
-                const int x = cell_of(px, G) + d % 3 - 1, y = cell_of(py, G) + d / 3 - 1;
+                const int d = it % 9, lg = s_lg[l], G = 1 << lg;
+                const int x = (cx0 >> l) + d % 3 - 1, y = (cy0 >> l) + d / 3 - 1;
                 const bool primary = d == 4 || l == lfine;
                 if (x >= 0 && x < G && y >= 0 && y < G && primary == (pass == 0)) {
                     const uint32_t c = (uint32_t)(s_loff[l] + (y << lg) + x);
@@ -653,7 +657,7 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
     for (int l = L.levels - 1; l >= 0 && ncur > 0; --l) {
         const int lg = s_lg[l];
         const int wmask = (1 << lg) - 1;
-        const int sx = cell_of(px, 1 << lg), sy = cell_of(py, 1 << lg);  // seed window centre
+        const int sx = cx0 >> l, sy = cy0 >> l;  // seed window centre
         const uint32_t lo = (uint32_t)s_loff[l];
         // own members of the frontier (outside the seed window)
         for (int base = 0; base < ncur; base += 32) {
