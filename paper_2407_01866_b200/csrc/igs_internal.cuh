@@ -41,6 +41,35 @@ struct __align__(16) ShadeRec {
 static_assert(sizeof(ScanRec) == 48, "ScanRec");
 static_assert(sizeof(ShadeRec) == 48, "ShadeRec");
 
+// PreparedSet entry of Gaussian i (renderer.cpp:37-50): correctly rounded
+// sincos, IEEE reciprocals; writes both records and returns the scan one.
+__device__ __forceinline__ ScanRec prepare_one(const double* __restrict__ params, uint32_t i,
+                                               ScanRec* __restrict__ scan, ShadeRec* __restrict__ shade) {
+    const double2* p2 = reinterpret_cast<const double2*>(params + (size_t)i * 8);
+    const double2 a = p2[0], b = p2[1], c = p2[2], d = p2[3];
+    double s, co;
+    igs_math::cr_sincos(b.x, &s, &co);
+    const double inv_s1 = __ddiv_rn(1.0, b.y);
+    const double inv_s2 = __ddiv_rn(1.0, c.x);
+    ScanRec r;
+    r.mu_x = a.x;
+    r.mu_y = a.y;
+    r.cos_t = co;
+    r.sin_t = s;
+    r.inv_a = __dmul_rn(inv_s1, inv_s1);
+    r.inv_b = __dmul_rn(inv_s2, inv_s2);
+    scan[i] = r;
+    ShadeRec h;
+    h.r = c.y;
+    h.g = d.x;
+    h.b = d.y;
+    h.inv_s1 = inv_s1;
+    h.inv_s2 = inv_s2;
+    h.pad = 0.0;
+    shade[i] = h;
+    return r;
+}
+
 // renderer.cpp:17-23 mahalanobis_sq, each op rounded separately (no FMA).
 __device__ __forceinline__ double maha(const ScanRec& g, double x, double y) {
     const double dx = __dsub_rn(x, g.mu_x);

@@ -21,28 +21,7 @@ __global__ void prepare_kernel(const double* __restrict__ params, ScanRec* __res
                                ShadeRec* __restrict__ shade, uint32_t first, uint32_t n) {
     const uint32_t i = first + blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const double2* p2 = reinterpret_cast<const double2*>(params + (size_t)i * 8);
-    const double2 a = p2[0], b = p2[1], c = p2[2], d = p2[3];
-    double s, co;
-    igs_math::cr_sincos(b.x, &s, &co);
-    const double inv_s1 = __ddiv_rn(1.0, b.y);
-    const double inv_s2 = __ddiv_rn(1.0, c.x);
-    ScanRec r;
-    r.mu_x = a.x;
-    r.mu_y = a.y;
-    r.cos_t = co;
-    r.sin_t = s;
-    r.inv_a = __dmul_rn(inv_s1, inv_s1);
-    r.inv_b = __dmul_rn(inv_s2, inv_s2);
-    scan[i] = r;
-    ShadeRec h;
-    h.r = c.y;
-    h.g = d.x;
-    h.b = d.y;
-    h.inv_s1 = inv_s1;
-    h.inv_s2 = inv_s2;
-    h.pad = 0.0;
-    shade[i] = h;
+    prepare_one(params, i, scan, shade);
 }
 
 constexpr int kTile = 16;      // 16x16 pixel tile per CTA (256 threads)
