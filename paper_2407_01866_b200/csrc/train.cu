@@ -458,9 +458,7 @@ __device__ __forceinline__ void adam_one(uint32_t i, const double* gg, double* g
     for (int p = 0; p < 8; ++p) finite_all = finite_all && isfinite(gp[p]);
     if (!finite_all) {
         atomicMin(status + 1, (long long)i);
-#ifndef IGS_SPLIT_PREP
         tree_acc_add(ta, i, scan[i]);  // unchanged
-#endif
         return;
     }
     gp[0] = clamp01d(gp[0]);
@@ -483,9 +481,6 @@ __device__ __forceinline__ void adam_one(uint32_t i, const double* gg, double* g
         Mw[h] = make_double2(mm[2 * h], mm[2 * h + 1]);
         Vw[h] = make_double2(vv[2 * h], vv[2 * h + 1]);
     }
-#ifdef IGS_SPLIT_PREP
-    return;  // prepare_acc_kernel refreshes the records
-#endif
     // refresh the prepared records (renderer.cpp:37-50) for the next step
     double s, co;
     igs_math::cr_sincos(gp[2], &s, &co);
@@ -521,9 +516,7 @@ __global__ void adam_kernel(double* __restrict__ params, const double* __restric
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     if (status[0] != LLONG_MAX || status[2] != LLONG_MAX) {
-#ifndef IGS_SPLIT_PREP
         tree_acc_add(ta, i, scan[i]);  // every Gaussian is accumulated, updated or not
-#endif
         return;
     }
     double gg[8], gp[8], mm[8], vv[8];
@@ -564,9 +557,7 @@ __global__ void __launch_bounds__(256, IGS_ADAM_MINB) segment_adam_kernel(uint32
     gcnt[g] = 0;
     gcnt[n + g] = 0;
     if (status[2] != LLONG_MAX) {
-#ifndef IGS_SPLIT_PREP
         tree_acc_add(ta, g, scan[g]);  // every Gaussian is accumulated, updated or not
-#endif
         return;
     }
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -590,9 +581,7 @@ __global__ void __launch_bounds__(256, IGS_ADAM_MINB) segment_adam_kernel(uint32
     for (int p = 0; p < 8; ++p)
         if (!isfinite(acc[p])) {
             atomicMin(status, (long long)g * 8 + p);
-#ifndef IGS_SPLIT_PREP
             tree_acc_add(ta, g, scan[g]);
-#endif
             return;
         }
     // (loading the parameters and moments only now keeps the register
@@ -601,20 +590,6 @@ __global__ void __launch_bounds__(256, IGS_ADAM_MINB) segment_adam_kernel(uint32
     adam_load(g, params, m, v, gp, mm, vv);
     adam_one(g, acc, gp, mm, vv, params, m, v, scan, shade, lr_mu, lr_color, lr_scale, lr_theta, bc1, bc2, ibc1, ibc2,
              status, ta);
-}
-
-// PreparedSet refresh after Adam (renderer.cpp:37-50) plus the kNN tree
-// accumulation, for every Gaussian (updated or not: a skipped one gets its
-// unchanged record back).  Few registers, so the long double-double sincos
-// chains of many warps overlap.
-__global__ void __launch_bounds__(256) prepare_acc_kernel(const double* __restrict__ params,
-                                                          ScanRec* __restrict__ scan, ShadeRec* __restrict__ shade,
-                                                          uint32_t n, TreeAcc ta) {
-    pdl_wait();
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const ScanRec r = prepare_one(params, i, scan, shade);
-    tree_acc_add(ta, i, r);
 }
 
 __global__ void reset_status_kernel(long long* status) {
@@ -769,10 +744,6 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
                     (const uint32_t*)perm, (const double*)contrib, n, ctx->grads, ctx->params, ctx->adam_m,
                     ctx->adam_v, ctx->scan, ctx->shade, fuse_lr4[0], fuse_lr4[1], fuse_lr4[2], fuse_lr4[3], bc1, bc2,
                     1.0 / bc1, 1.0 / bc2, ctx->status, ta);
-#ifdef IGS_SPLIT_PREP
-            IGS_PDL(ctx, prepare_acc_kernel, (n + 255) / 256, 256, 0, (const double*)ctx->params, ctx->scan,
-                    ctx->shade, n, ta);
-#endif
             igs_prof_end(ctx, IGS_PROF_ADAM, (double)n * 544.0);
             ctx->gcnt_clean = gcnt;
             ctx->gcnt_clean_n = n;
@@ -806,10 +777,6 @@ int igs_adam_launch(igs_ctx* ctx, const double* lr4, long long t) {
     IGS_PDL(ctx, adam_kernel, (ctx->n + 255) / 256, 256, 0, ctx->params, (const double*)ctx->grads, ctx->adam_m,
             ctx->adam_v, ctx->scan, ctx->shade, ctx->n, lr4[0], lr4[1], lr4[2], lr4[3], bc1, bc2, 1.0 / bc1,
             1.0 / bc2, ctx->status, ta);
-#ifdef IGS_SPLIT_PREP
-    IGS_PDL(ctx, prepare_acc_kernel, (ctx->n + 255) / 256, 256, 0, (const double*)ctx->params, ctx->scan,
-            ctx->shade, ctx->n, ta);
-#endif
     // algorithmic bytes: read params/grads/m/v (256 B), write params/m/v
     // (192 B) and the refreshed 96 B of scan+shade records
     igs_prof_end(ctx, IGS_PROF_ADAM, (double)ctx->n * 544.0);
