@@ -172,7 +172,6 @@ def run_ours(args, rank, world, local_rank, dist):
     ctx.sync()
     clocks.start()
     launches0 = ctx.kernel_launches
-    ctx.profile_enable(True)
     step_ms = []
     for s in range(args.steps):
         ctx.flush_l2(FLUSH_BYTES)
@@ -182,7 +181,14 @@ def run_ours(args, rank, world, local_rank, dist):
     ctx.sync()
     barrier()
     clk = clocks.stop()
-    launches = ctx.kernel_launches - launches0 - 0  # includes the flush memsets? no: memsets are not kernels we count
+    launches = ctx.kernel_launches - launches0  # our kernels only (the L2 flush is a memset)
+    # per-family breakdown: a separate pass over the next `steps` iterations
+    # (profiling inserts events between the families, so it is not timed above)
+    ctx.profile_enable(True)
+    for s in range(args.steps):
+        ctx.flush_l2(FLUSH_BYTES)
+        ctx.train_iterations(1, K, LR, args.warmup + args.steps + 1 + s, want_losses=False)
+    ctx.sync()
     prof = {PROF_NAMES[f]: ctx.profile_read(f) for f in range(len(PROF_NAMES))}
     ctx.profile_enable(False)
     total_ms = max_over_ranks(sum(step_ms))
@@ -190,16 +196,24 @@ def run_ours(args, rank, world, local_rank, dist):
     value = args.steps / (total_ms / 1e3)
 
     # ---- e2e through the public host-buffer call --------------------------------
+    # igs_train_iteration_async / igs_train_wait pipelined two deep, as igs_fit
+    # drives it: every step copies its sample indices from pinned host memory
+    # and reads its loss + status back.  Device marks bracket each step (after
+    # its L2 flush, through its D2H read); the host enqueue of step s+1
+    # overlaps step s.
     ctx.set_params(params)  # fresh state: moments zero, same trajectory start
     for s in range(args.warmup):
         ctx.train_iteration(mine[s], K, LR, s + 1)
     barrier()
-    e2e_ms = []
     for s in range(args.steps):
         ctx.flush_l2(FLUSH_BYTES)
-        ctx.timer_begin()
-        ctx.train_iteration(mine[args.warmup + s], K, LR, args.warmup + 1 + s)
-        e2e_ms.append(ctx.timer_end())
+        ctx.timer_mark(2 * s)
+        ctx.train_iteration_async(mine[args.warmup + s], K, LR, args.warmup + 1 + s)
+        ctx.timer_mark(2 * s + 1)
+        if s > 0:
+            ctx.train_wait()
+    ctx.train_wait()
+    e2e_ms = [ctx.timer_between(2 * s, 2 * s + 1) for s in range(args.steps)]
     barrier()
     e2e_total = max_over_ranks(sum(e2e_ms))
     e2e_value = args.steps / (e2e_total / 1e3)
@@ -213,7 +227,7 @@ def run_ours(args, rank, world, local_rank, dist):
         achieved = scan_pairs * OPS_PER_PAIR / (scan_ms * 1e-3)
         roof = {"kernel": "top-K candidate scan (IGS_PROF_SCAN)", "bound": "fp64",
                 "achieved": achieved / 1e9, "peak": fp64_peak / 1e9, "unit": "Gop/s (fp64 add/mul pipe)",
-                "frac": achieved / fp64_peak, "traffic": None,
+                "frac": achieved / fp64_peak, "traffic": ncu_traffic("knn_points_kernel"),
                 "work_per_launch": f"{scan_pairs / max(scan_launches, 1):.4g} (pixel, candidate) pairs x "
                                    f"{OPS_PER_PAIR} fp64 ops",
                 "peak_source": "measured in this run (igs_fp64_peak: independent DMUL/DADD chains, all SMs); "
@@ -229,7 +243,8 @@ def run_ours(args, rank, world, local_rank, dist):
     if adam_ms > 0 and hbm:
         gbs = adam_bytes / (adam_ms * 1e-3) / 1e9
         adam_roof = {"kernel": "fused Adam+constrain+prepare", "bound": "hbm", "achieved": gbs, "peak": hbm,
-                     "unit": "GB/s", "frac": gbs / hbm, "traffic": None, "bytes_per_gaussian": 544}
+                     "unit": "GB/s", "frac": gbs / hbm, "traffic": ncu_traffic("segment_adam_kernel"),
+                     "bytes_per_gaussian": 544}
 
     # ---- culling statistics of the last state (target raster, K) -----------------------
     cull_stats = None
@@ -266,7 +281,8 @@ def run_ours(args, rank, world, local_rank, dist):
                    "cull": ctx.get_option(1), "deterministic_reduction": ctx.get_option(2)},
         "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": int(mine.shape[1]) * 4,
                 "d2h_bytes_per_step": 8 + 32,
-                "call": "igs_train_iteration (host sample indices in, host loss out)"},
+                "call": "igs_train_iteration_async + igs_train_wait, pipelined two deep (host sample indices in, "
+                        "host loss + status out every step)"},
         "roofline": roof, "roofline_adam": adam_roof,
         "profile_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
         "knn_hard_points_per_step": prof["knn_hard"][2] / args.steps,
@@ -277,6 +293,16 @@ def run_ours(args, rank, world, local_rank, dist):
         "render": render,
     }
     return out, ctx
+
+
+def ncu_traffic(kernel: str):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed
+    `ncu --set full` capture summary (profiles/r1_traffic.json), or None."""
+    try:
+        d = json.loads((ROOT / "profiles" / "r1_traffic.json").read_text())
+        return d[kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
 
 
 # ---------------------------------------------------------------------- reference

@@ -123,8 +123,10 @@ int igs_train_iteration(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, i
                         long long t, double* loss);
 /* Asynchronous form for pipelined drivers: enqueues the iteration (the
  * sample indices are staged through pinned memory; returns immediately) --
- * igs_train_wait() then waits, checks the step's status and reports its
- * loss.  At most one iteration may be outstanding. */
+ * igs_train_wait() then waits for the oldest outstanding iteration, checks
+ * its status and reports its loss.  At most two iterations may be
+ * outstanding: enqueueing t+1 before waiting on t overlaps the host's
+ * enqueue with the device's work (the iterations still run in order). */
 int igs_train_iteration_async(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, int k, const double* lr4,
                               long long t);
 int igs_train_wait(igs_ctx* ctx, double* loss);
@@ -219,6 +221,11 @@ int igs_timer_begin(igs_ctx* ctx);
 /* Records the stop event (unless igs_train_iterations already recorded it
  * right after its last kernel), waits for it, returns elapsed ms. */
 int igs_timer_end(igs_ctx* ctx, float* ms);
+/* Numbered timing marks for pipelined loops: records event `idx` on the
+ * stream without waiting; igs_timer_between waits for mark b and returns the
+ * elapsed ms from mark a to mark b. */
+int igs_timer_mark(igs_ctx* ctx, uint32_t idx);
+int igs_timer_between(igs_ctx* ctx, uint32_t a, uint32_t b, float* ms);
 /* Overwrites a scratch buffer of `bytes` (choose > 126 MB L2) on the stream. */
 int igs_flush_l2(igs_ctx* ctx, size_t bytes);
 /* Microbenchmarks the FP64 add/mul pipe (independent DADD/DMUL chains,

@@ -273,11 +273,14 @@ void igs_ctx_destroy(igs_ctx* ctx) {
     for (auto& v : ctx->prof_ev)
         for (auto e : v) cudaEventDestroy(e);
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    for (auto e : ctx->marks) cudaEventDestroy(e);
     for (auto e : ctx->timer)
         if (e) cudaEventDestroy(e);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     for (auto& b : ctx->async_pin)
         if (b.p) cudaFreeHost(b.p);
+    for (auto e : ctx->async_ev)
+        if (e) cudaEventDestroy(e);
     cudaStreamSynchronize(ctx->side);
     cudaEventDestroy(ctx->ev_fork);
     cudaEventDestroy(ctx->ev_join);
@@ -639,8 +642,8 @@ int igs_train_iteration(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, i
 
 static int stage_rendered(igs_ctx* ctx, const float* rendered, int W, int H, const float** dev);
 
-// Pinned staging for the async iteration: [0] sample buffer, [1] result
-// block {status[4], loss}.
+// Pinned staging for the async iterations: [slot] sample buffer, [2 + slot]
+// result block {status[4], loss}.
 static void* async_pinned(igs_ctx* ctx, int which, size_t bytes) {
     DevBuf& b = ctx->async_pin[which];
     if (b.bytes >= bytes) return b.p;
@@ -660,17 +663,22 @@ int igs_train_iteration_async(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t
     CHECK_CTX(ctx);
     cudaSetDevice(ctx->device);
     int e;
-    if (ctx->async_pending) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "an iteration is already outstanding");
+    if (ctx->async_count >= 2) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "two iterations are already outstanding");
     if ((e = train_checks(ctx, ns, k))) return e;
     if (t < 1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "Adam step index must be >= 1");
     const uint64_t npx = (uint64_t)ctx->tgt_w * ctx->tgt_h;
     for (uint32_t i = 0; i < ns; ++i)
         if (sample_idx[i] >= npx) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "sample index outside the target");
-    uint32_t* pin = (uint32_t*)async_pinned(ctx, 0, (size_t)ns * 4);
-    long long* res = (long long*)async_pinned(ctx, 1, 64);
+    const int slot = (ctx->async_head + ctx->async_count) & 1;
+    uint32_t* pin = (uint32_t*)async_pinned(ctx, slot, (size_t)ns * 4);
+    long long* res = (long long*)async_pinned(ctx, 2 + slot, 64);
+    // the device sample buffer is shared: the next iteration's copy into it
+    // is ordered after this iteration's kernels on the stream
     uint32_t* dsidx = (uint32_t*)igs_scratch(ctx, 21, (size_t)ns * sizeof(uint32_t));
     double* dloss = (double*)igs_scratch(ctx, 14, 64 * sizeof(double));
     if (!pin || !res || !dsidx || !dloss) return igs_fail(ctx, IGS_E_CUDA, "out of memory (async iteration)");
+    if (!ctx->async_ev[slot]) IGS_CUDA(ctx, cudaEventCreateWithFlags(&ctx->async_ev[slot], cudaEventDisableTiming));
+    dloss += slot;
     std::memcpy(pin, sample_idx, (size_t)ns * 4);
     IGS_CUDA(ctx, cudaMemcpyAsync(dsidx, pin, (size_t)ns * 4, cudaMemcpyHostToDevice, ctx->stream));
     if ((e = igs_status_reset(ctx))) return e;
@@ -685,17 +693,20 @@ int igs_train_iteration_async(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t
     }
     IGS_CUDA(ctx, cudaMemcpyAsync(res, ctx->status, 4 * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
     IGS_CUDA(ctx, cudaMemcpyAsync(res + 4, dloss, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    ctx->async_pending = true;
+    IGS_CUDA(ctx, cudaEventRecord(ctx->async_ev[slot], ctx->stream));
+    ctx->async_count++;
     return IGS_OK;
 }
 
 int igs_train_wait(igs_ctx* ctx, double* loss) {
     CHECK_CTX(ctx);
     cudaSetDevice(ctx->device);
-    if (!ctx->async_pending) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "no outstanding iteration");
-    ctx->async_pending = false;
-    IGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    const long long* st = (const long long*)ctx->async_pin[1].p;
+    if (ctx->async_count == 0) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "no outstanding iteration");
+    const int slot = ctx->async_head;
+    ctx->async_head ^= 1;
+    ctx->async_count--;
+    IGS_CUDA(ctx, cudaEventSynchronize(ctx->async_ev[slot]));
+    const long long* st = (const long long*)ctx->async_pin[2 + slot].p;
     ctx->knn_grown = st[3];
     if (st[2] != LLONG_MAX) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "training loss became non-finite");
     if (st[0] != LLONG_MAX) {

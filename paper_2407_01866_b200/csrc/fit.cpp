@@ -250,15 +250,29 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
         return igs_render_image_blocked(ctx, W, H, c.k, nullptr);
     };
 
+    // drains an enqueued iteration after a failure, keeping the first error
+    auto drain = [&](int code) {
+        const std::string keep = igs_last_error(ctx);
+        igs_train_wait(ctx, nullptr);
+        return igs_internal_fail(ctx, code, keep.c_str());
+    };
+    // Iterations are pipelined two deep: while the device runs iteration t,
+    // the host draws t+1's samples and enqueues it (unless t evaluates or
+    // densifies, which needs the set after t), then waits on t.
     draw(cur);
+    if (c.iterations >= 1 && (e = igs_train_iteration_async(ctx, cur.data(), (uint32_t)cur.size(), c.k, lr, 1)))
+        return e;
     for (int iter = 1; iter <= c.iterations; ++iter) {
-        if ((e = igs_train_iteration_async(ctx, cur.data(), (uint32_t)cur.size(), c.k, lr, iter))) return e;
         const bool do_eval = iter % c.eval_interval == 0 || iter == c.iterations;
         const bool do_densify = stage < 4 && iter == c.warmup_iters + stage * c.densify_interval;
         double loss = 0.0;
         if (!do_eval && !do_densify) {
-            if (iter < c.iterations) draw(next);  // overlaps the device step
-            if ((e = igs_train_wait(ctx, &loss))) return e;
+            if (iter < c.iterations) {
+                draw(next);  // overlaps the device step
+                if ((e = igs_train_iteration_async(ctx, next.data(), (uint32_t)next.size(), c.k, lr, iter + 1)))
+                    return drain(e);  // t is still outstanding
+            }
+            if ((e = igs_train_wait(ctx, &loss))) return iter < c.iterations ? drain(e) : e;  // t+1 outstanding
             std::swap(cur, next);
             continue;
         }
@@ -297,8 +311,11 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
             if (add_count > 0 && (e = igs_append_params(ctx, fresh.data(), (uint32_t)add_count))) return e;
             ++stage;
         }
-        if (iter < c.iterations) draw(next);
-        std::swap(cur, next);
+        if (iter < c.iterations) {
+            draw(next);
+            std::swap(cur, next);
+            if ((e = igs_train_iteration_async(ctx, cur.data(), (uint32_t)cur.size(), c.k, lr, iter + 1))) return e;
+        }
     }
     if ((e = emit_checkpoint(c.iterations))) return e;
 

@@ -218,8 +218,10 @@ struct igs_ctx {
     long long* status = nullptr;
 
     // pinned staging of the async iteration (igs_train_iteration_async)
-    DevBuf async_pin[2];
-    bool async_pending = false;
+    // (two slots: samples, result block and completion event per slot)
+    DevBuf async_pin[4];
+    cudaEvent_t async_ev[2] = {nullptr, nullptr};
+    int async_head = 0, async_count = 0;
 
     // uploaded samples for device-resident training
     DevBuf samples;
@@ -244,6 +246,7 @@ struct igs_ctx {
     DevBuf flush;
     int flush_salt = 0;
     std::vector<cudaEvent_t> ev_pool;
+    std::vector<cudaEvent_t> marks;  // igs_timer_mark
 
 #ifndef IGS_NO_NCCL
     ncclComm_t comm = nullptr;

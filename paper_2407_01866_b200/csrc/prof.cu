@@ -90,6 +90,26 @@ int igs_timer_end(igs_ctx* ctx, float* ms) {
     return IGS_OK;
 }
 
+int igs_timer_mark(igs_ctx* ctx, uint32_t idx) {
+    if (!ctx || idx > (1u << 20)) return IGS_E_INVALID_PARAMETER;
+    cudaSetDevice(ctx->device);
+    while (ctx->marks.size() <= idx) {
+        cudaEvent_t e;
+        IGS_CUDA(ctx, cudaEventCreate(&e));
+        ctx->marks.push_back(e);
+    }
+    IGS_CUDA(ctx, cudaEventRecord(ctx->marks[idx], ctx->stream));
+    return IGS_OK;
+}
+
+int igs_timer_between(igs_ctx* ctx, uint32_t a, uint32_t b, float* ms) {
+    if (!ctx || !ms || a >= ctx->marks.size() || b >= ctx->marks.size()) return IGS_E_INVALID_PARAMETER;
+    cudaSetDevice(ctx->device);
+    IGS_CUDA(ctx, cudaEventSynchronize(ctx->marks[b]));
+    IGS_CUDA(ctx, cudaEventElapsedTime(ms, ctx->marks[a], ctx->marks[b]));
+    return IGS_OK;
+}
+
 int igs_flush_l2(igs_ctx* ctx, size_t bytes) {
     if (!ctx) return IGS_E_INVALID_PARAMETER;
     cudaSetDevice(ctx->device);

@@ -134,6 +134,8 @@ SIGNATURES = {
     "igs_tile_lists": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _up, _u64p, _up, _up, _dp]),
     "igs_timer_begin": (C.c_int, [_vp]),
     "igs_timer_end": (C.c_int, [_vp, C.POINTER(C.c_float)]),
+    "igs_timer_mark": (C.c_int, [_vp, C.c_uint32]),
+    "igs_timer_between": (C.c_int, [_vp, C.c_uint32, C.c_uint32, C.POINTER(C.c_float)]),
     "igs_flush_l2": (C.c_int, [_vp, C.c_size_t]),
     "igs_fp64_peak": (C.c_int, [_vp, _dp]),
     "igs_profile_enable": (C.c_int, [_vp, C.c_int]),
@@ -460,6 +462,14 @@ class Context:
     def timer_end(self) -> float:
         ms = C.c_float(0)
         self._chk(self.lib.igs_timer_end(self.h, C.byref(ms)))
+        return ms.value
+
+    def timer_mark(self, idx: int):
+        self._chk(self.lib.igs_timer_mark(self.h, idx))
+
+    def timer_between(self, a: int, b: int) -> float:
+        ms = C.c_float(0)
+        self._chk(self.lib.igs_timer_between(self.h, a, b, C.byref(ms)))
         return ms.value
 
     def flush_l2(self, nbytes: int = 512 << 20):

@@ -216,3 +216,30 @@ def test_knn_refit_stays_exact_over_many_steps(gctx, port):
     idx, w, cnt = gctx.select_top_k(uv, 10)
     assert np.all(cnt == 10)
     assert np.array_equal(idx, topk[ys, xs])
+
+
+def test_async_pipelined_iterations_match_sync(gctx, port):
+    """Two-deep pipelined igs_train_iteration_async / igs_train_wait gives the
+    synchronous trajectory bit for bit; a third outstanding iteration and a
+    wait with none outstanding are rejected."""
+    target = synth.photo_like_image(96, 64, 31011)
+    params = port.initialize_set(target, 700, 0.3, 23)
+    steps = synth.sample_indices(2500, 96, 64, seed=29, steps=6)
+    gctx.set_params(params)
+    gctx.set_target(target)
+    want = [gctx.train_iteration(steps[s], 10, LR, s + 1) for s in range(6)]
+    p_sync = gctx.get_params()
+    gctx.set_params(params)
+    got = []
+    gctx.train_iteration_async(steps[0], 10, LR, 1)
+    for s in range(1, 6):
+        gctx.train_iteration_async(steps[s], 10, LR, s + 1)
+        if s == 1:
+            with pytest.raises(IgsError, match="outstanding"):
+                gctx.train_iteration_async(steps[2], 10, LR, 3)
+        got.append(gctx.train_wait())
+    got.append(gctx.train_wait())
+    with pytest.raises(IgsError, match="no outstanding"):
+        gctx.train_wait()
+    assert got == want
+    assert np.array_equal(gctx.get_params(), p_sync)
