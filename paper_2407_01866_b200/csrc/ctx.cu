@@ -16,6 +16,8 @@ using namespace igs_dev;
 
 // train.cu
 int igs_status_reset(igs_ctx* ctx);
+int igs_stage_samples(igs_ctx* ctx, const uint32_t* host_pinned, uint32_t* dsidx, uint32_t ns);
+int igs_publish(igs_ctx* ctx, const double* dloss, long long* host_res);
 int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint32_t* dev_sidx,
                          const double* dev_samples5, double* dev_loss, double inv_n, const double* fuse_lr4 = nullptr,
                          long long t = 0, bool* fused = nullptr);
@@ -620,24 +622,12 @@ int igs_adam_step(igs_ctx* ctx, const double* lr4, long long t) {
 int igs_train_iteration(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, int k, const double* lr4,
                         long long t, double* loss) {
     CHECK_CTX(ctx);
-    cudaSetDevice(ctx->device);
+    // = the asynchronous form plus its wait (after any outstanding ones)
+    if (ctx->async_count)
+        return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "asynchronous iterations are outstanding (igs_train_wait)");
     int e;
-    if ((e = train_checks(ctx, ns, k))) return e;
-    if (t < 1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "Adam step index must be >= 1");
-    uint32_t* dsidx;
-    if ((e = upload_sidx(ctx, sample_idx, ns, &dsidx))) return e;
-    double* dloss = (double*)igs_scratch(ctx, 14, 64 * sizeof(double));
-    if ((e = igs_status_reset(ctx))) return e;
-    const uint32_t ns_total = ns * (uint32_t)ctx->nranks;
-    bool fused = false;
-    if ((e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss, 1.0 / (double)ns_total, lr4, t, &fused)))
-        return e;
-    if (!fused) {
-        if ((e = allreduce_grads(ctx, dloss))) return e;
-        if ((ctx->comm || !ctx->grads_checked) && (e = igs_grad_check(ctx))) return e;
-        if ((e = igs_adam_launch(ctx, lr4, t))) return e;
-    }
-    return read_status(ctx, dloss, loss, 1);
+    if ((e = igs_train_iteration_async(ctx, sample_idx, ns, k, lr4, t))) return e;
+    return igs_train_wait(ctx, loss);
 }
 
 static int stage_rendered(igs_ctx* ctx, const float* rendered, int W, int H, const float** dev);
@@ -680,8 +670,7 @@ int igs_train_iteration_async(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t
     if (!ctx->async_ev[slot]) IGS_CUDA(ctx, cudaEventCreateWithFlags(&ctx->async_ev[slot], cudaEventDisableTiming));
     dloss += slot;
     std::memcpy(pin, sample_idx, (size_t)ns * 4);
-    IGS_CUDA(ctx, cudaMemcpyAsync(dsidx, pin, (size_t)ns * 4, cudaMemcpyHostToDevice, ctx->stream));
-    if ((e = igs_status_reset(ctx))) return e;
+    if ((e = igs_stage_samples(ctx, pin, dsidx, ns))) return e;  // status reset + H2D
     const uint32_t ns_total = ns * (uint32_t)ctx->nranks;
     bool fused = false;
     if ((e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss, 1.0 / (double)ns_total, lr4, t, &fused)))
@@ -691,8 +680,7 @@ int igs_train_iteration_async(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t
         if ((ctx->comm || !ctx->grads_checked) && (e = igs_grad_check(ctx))) return e;
         if ((e = igs_adam_launch(ctx, lr4, t))) return e;
     }
-    IGS_CUDA(ctx, cudaMemcpyAsync(res, ctx->status, 4 * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
-    IGS_CUDA(ctx, cudaMemcpyAsync(res + 4, dloss, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    if ((e = igs_publish(ctx, dloss, res))) return e;  // D2H of status + loss
     IGS_CUDA(ctx, cudaEventRecord(ctx->async_ev[slot], ctx->stream));
     ctx->async_count++;
     return IGS_OK;

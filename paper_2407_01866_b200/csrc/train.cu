@@ -592,6 +592,26 @@ __global__ void __launch_bounds__(256, IGS_ADAM_MINB) segment_adam_kernel(uint32
              status, ta);
 }
 
+// Start of an iteration fed from host memory: resets the status block and
+// copies the sample indices straight from the pinned (device-mapped) host
+// buffer -- a kernel rather than a copy-engine transfer, so the step's
+// kernels stay one programmatic-dependent-launch chain.
+__global__ void stage_kernel(long long* __restrict__ status, const uint32_t* __restrict__ host_sidx,
+                             uint32_t* __restrict__ dsidx, uint32_t ns) {
+    pdl_wait();
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (blockIdx.x == 0 && threadIdx.x < 4) status[threadIdx.x] = threadIdx.x == 3 ? 0 : LLONG_MAX;
+    if (i < ns) dsidx[i] = host_sidx[i];
+}
+
+// End of an iteration: status block + loss into the pinned result block.
+__global__ void publish_kernel(const long long* __restrict__ status, const double* __restrict__ dloss,
+                               long long* __restrict__ host_res) {
+    pdl_wait();
+    if (threadIdx.x < 4) host_res[threadIdx.x] = status[threadIdx.x];
+    if (threadIdx.x == 4) host_res[4] = __double_as_longlong(*dloss);
+}
+
 __global__ void reset_status_kernel(long long* status) {
     pdl_wait();
     if (threadIdx.x < 3) status[threadIdx.x] = LLONG_MAX;
@@ -633,6 +653,16 @@ __global__ void blend_points_kernel(const double* __restrict__ lq, const uint32_
 // 4 keys, 5 keys sorted, 6 vals, 7 vals sorted, 8 cub temp, 9 losses,
 // 10/11 point partials, 12/13 generic lists, 14 loss out, 15 upstream samples,
 // 24 long-segment queue.
+
+int igs_stage_samples(igs_ctx* ctx, const uint32_t* host_pinned, uint32_t* dsidx, uint32_t ns) {
+    IGS_PDL(ctx, stage_kernel, (ns + 255) / 256 + (ns == 0), 256, 0, ctx->status, host_pinned, dsidx, ns);
+    return IGS_OK;
+}
+
+int igs_publish(igs_ctx* ctx, const double* dloss, long long* host_res) {
+    IGS_PDL(ctx, publish_kernel, 1, 32, 0, (const long long*)ctx->status, dloss, host_res);
+    return IGS_OK;
+}
 
 int igs_status_reset(igs_ctx* ctx) {
     IGS_PDL(ctx, reset_status_kernel, 1, 32, 0, ctx->status);
