@@ -268,6 +268,28 @@ int igs_ensure_image(igs_ctx* ctx, int w, int h);
         if (_e != cudaSuccess) return igs_cuda_check((ctx), _e, "launch");  \
     } while (0)
 
+// L2 prefetch of data a LATER kernel of the same step reads: a kernel that is
+// itself latency-bound spreads fire-and-forget prefetches over its threads
+// so the follower's first touch hits L2 instead of DRAM.
+struct L2Prefetch {
+    const char* p[4];
+    uint32_t lines[4];  // 128-byte lines per range
+    int nr;
+};
+
+inline void l2pf_add(L2Prefetch& pf, const void* p, size_t bytes) {
+    if (!p || !bytes || pf.nr >= 4) return;
+    pf.p[pf.nr] = static_cast<const char*>(p);
+    pf.lines[pf.nr] = (uint32_t)((bytes + 127) / 128);
+    pf.nr++;
+}
+
+__device__ __forceinline__ void prefetch_l2(const L2Prefetch& pf, uint32_t tid, uint32_t nthr) {
+    for (int r = 0; r < pf.nr; ++r)
+        for (uint32_t l = tid; l < pf.lines[r]; l += nthr)
+            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(pf.p[r] + (size_t)l * 128));
+}
+
 // Programmatic dependent launch: a kernel launched with IGS_PDL may be
 // scheduled while its stream predecessor drains (hiding launch latency); it
 // must execute pdl_wait() before it reads or writes any memory a
@@ -320,7 +342,9 @@ void igs_knn_free(igs_ctx* ctx);
 int igs_topk_knn(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq);
 int igs_knn_forward_backward(igs_ctx* ctx, int mode, const uint32_t* sidx, const double* samples5, uint32_t npts,
                              int kk, double inv_n, double* losses, double* contrib, uint32_t* keys, uint32_t* gcnt,
-                             double* grads_atomic, uint32_t* zero_word = nullptr);
+                             double* grads_atomic, uint32_t* zero_word = nullptr,
+                             const L2Prefetch* pf = nullptr);
+L2Prefetch igs_knn_tree_inputs(igs_ctx* ctx);
 int igs_topk_samples_culled(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq);
 int igs_topk_pixels_culled(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq, int W,
                            int H);

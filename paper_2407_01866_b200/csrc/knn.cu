@@ -176,7 +176,8 @@ __device__ __forceinline__ Sum own_from(uint32_t m, const Acc& a) {
 
 __global__ void __launch_bounds__(256) lq_tree_kernel(Acc* __restrict__ acc, Lq L,
                                                       const uint32_t* __restrict__ cnt, Sum* __restrict__ own,
-                                                      Sum* __restrict__ sub, unsigned int* __restrict__ ticket) {
+                                                      Sum* __restrict__ sub, unsigned int* __restrict__ ticket,
+                                                      L2Prefetch pf) {
     __shared__ Sum sm[2][kBlk * kBlk];
     __shared__ Sum up[kUpCells];
     __shared__ int s_loff[kMaxLv];
@@ -188,6 +189,7 @@ __global__ void __launch_bounds__(256) lq_tree_kernel(Acc* __restrict__ acc, Lq 
     const int nb = L.G0 / kBlk;  // G0 is a power of two >= 16
     const int bx = blockIdx.x % nb, by = blockIdx.x / nb;
     pdl_wait();
+    prefetch_l2(pf, blockIdx.x * 256 + t, gridDim.x * 256);  // the search's inputs
     // prefetch: the cell this thread owns at each in-block level
     uint32_t cell[kInLv], m[kInLv];
     Acc a[kInLv];
@@ -444,6 +446,7 @@ struct Epi {
     uint32_t* oi;                // mode 2
     uint32_t n;
     uint32_t* zero_word;         // zeroed at the start of the search (or null)
+    L2Prefetch pf;               // what the kernels after the search read (Adam's rows)
 };
 
 // Query point: the centre of target pixel sidx[pt] (mode 0; pixel_center,
@@ -588,6 +591,7 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
     // word are zeroed for the next search: nothing reads them before it
     if (blockIdx.x == 0 && threadIdx.x < 2) zero_next[threadIdx.x] = 0;
     if (blockIdx.x == 0 && threadIdx.x == 2 && E.zero_word) *E.zero_word = 0;
+    prefetch_l2(E.pf, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     // per-level population, one bit per level (same for every point)
@@ -890,6 +894,15 @@ void* grow(DevBuf& b, size_t bytes) {
     return b.p;
 }
 
+// What knn_points_kernel reads besides the tree: the scan records and the
+// member lists.
+L2Prefetch search_inputs(igs_ctx* ctx, const KnnBufs& b) {
+    L2Prefetch pf{};
+    l2pf_add(pf, ctx->scan, (size_t)ctx->n * sizeof(ScanRec));
+    l2pf_add(pf, b.mem.p, (size_t)ctx->n * 4);
+    return pf;
+}
+
 int knn_build(igs_ctx* ctx) {
     if (!ctx->knn) ctx->knn = new KnnBufs();
     KnnBufs& b = *static_cast<KnnBufs*>(ctx->knn);
@@ -904,7 +917,7 @@ int knn_build(igs_ctx* ctx) {
         const int nb = (b.lq.G0 + kBlk - 1) / kBlk;
         igs_prof_begin(ctx, IGS_PROF_CULL);
         IGS_PDL(ctx, lq_tree_kernel, nb * nb, 256, 0, (Acc*)b.acc.p, b.lq, (const uint32_t*)b.cnt.p, (Sum*)b.own.p,
-                (Sum*)b.sub.p, (unsigned int*)b.ticket.p);
+                (Sum*)b.sub.p, (unsigned int*)b.ticket.p, search_inputs(ctx, b));
         igs_prof_end(ctx, IGS_PROF_CULL, 0.0);
         b.since_build++;
         b.version = b.chain = ctx->params_version;
@@ -953,7 +966,7 @@ int knn_build(igs_ctx* ctx) {
             (const uint32_t*)off, cur, (uint32_t*)b.mem.p, (Acc*)b.acc.p);
     const int nb = (G0 + kBlk - 1) / kBlk;
     IGS_PDL(ctx, lq_tree_kernel, nb * nb, 256, 0, (Acc*)b.acc.p, L, (const uint32_t*)cnt, (Sum*)b.own.p,
-            (Sum*)b.sub.p, (unsigned int*)b.ticket.p);
+            (Sum*)b.sub.p, (unsigned int*)b.ticket.p, search_inputs(ctx, b));
     igs_prof_end(ctx, IGS_PROF_CULL, 0.0);
     b.lq = L;
     b.builds++;
@@ -1013,6 +1026,19 @@ int run_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int kk,
 
 }  // namespace
 
+// The refit's inputs (cell accumulators and counts), for the step's first
+// kernel to prefetch; empty unless the next search can refit.
+L2Prefetch igs_knn_tree_inputs(igs_ctx* ctx) {
+    L2Prefetch pf{};
+    if (!ctx->knn) return pf;
+    KnnBufs& b = *static_cast<KnnBufs*>(ctx->knn);
+    if (!b.acc_ok || b.version == ctx->params_version) return pf;
+    const size_t cells = (size_t)b.lq.loff[b.lq.levels - 1] + 1;
+    l2pf_add(pf, b.acc.p, cells * sizeof(Acc));
+    l2pf_add(pf, b.cnt.p, cells * 4);
+    return pf;
+}
+
 // Called by an Adam launch right before it bumps params_version by one.
 TreeAcc igs_knn_tree_acc(igs_ctx* ctx) {
     if (!ctx->knn) return TreeAcc{nullptr, nullptr};
@@ -1060,9 +1086,10 @@ int igs_topk_knn(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t*
 // grads_atomic.
 int igs_knn_forward_backward(igs_ctx* ctx, int mode, const uint32_t* sidx, const double* samples5, uint32_t npts,
                              int kk, double inv_n, double* losses, double* contrib, uint32_t* keys, uint32_t* gcnt,
-                             double* grads_atomic, uint32_t* zero_word) {
+                             double* grads_atomic, uint32_t* zero_word, const L2Prefetch* pf) {
     Epi E{};
     E.zero_word = zero_word;
+    if (pf) E.pf = *pf;
     E.gcnt = gcnt;
     E.mode = mode;
     E.sidx = sidx;

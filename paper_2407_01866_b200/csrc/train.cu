@@ -597,9 +597,10 @@ __global__ void __launch_bounds__(256, IGS_ADAM_MINB) segment_adam_kernel(uint32
 // buffer -- a kernel rather than a copy-engine transfer, so the step's
 // kernels stay one programmatic-dependent-launch chain.
 __global__ void stage_kernel(long long* __restrict__ status, const uint32_t* __restrict__ host_sidx,
-                             uint32_t* __restrict__ dsidx, uint32_t ns) {
+                             uint32_t* __restrict__ dsidx, uint32_t ns, L2Prefetch pf) {
     pdl_wait();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    prefetch_l2(pf, i, gridDim.x * blockDim.x);  // the tree refit's inputs
     if (blockIdx.x == 0 && threadIdx.x < 4) status[threadIdx.x] = threadIdx.x == 3 ? 0 : LLONG_MAX;
     if (i < ns) dsidx[i] = host_sidx[i];
 }
@@ -612,8 +613,10 @@ __global__ void publish_kernel(const long long* __restrict__ status, const doubl
     if (threadIdx.x == 4) host_res[4] = __double_as_longlong(*dloss);
 }
 
-__global__ void reset_status_kernel(long long* status) {
+__global__ void reset_status_kernel(long long* status, L2Prefetch pf) {
     pdl_wait();
+    prefetch_l2(pf, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+    if (blockIdx.x) return;
     if (threadIdx.x < 3) status[threadIdx.x] = LLONG_MAX;
     if (threadIdx.x == 3) status[3] = 0;  // a count (kNN tree growth)
 }
@@ -655,7 +658,9 @@ __global__ void blend_points_kernel(const double* __restrict__ lq, const uint32_
 // 24 long-segment queue.
 
 int igs_stage_samples(igs_ctx* ctx, const uint32_t* host_pinned, uint32_t* dsidx, uint32_t ns) {
-    IGS_PDL(ctx, stage_kernel, (ns + 255) / 256 + (ns == 0), 256, 0, ctx->status, host_pinned, dsidx, ns);
+    const L2Prefetch pf = igs_knn_tree_inputs(ctx);
+    const unsigned blocks = std::max((ns + 255) / 256 + (ns == 0), (unsigned)ctx->sm_count);
+    IGS_PDL(ctx, stage_kernel, blocks, 256, 0, ctx->status, host_pinned, dsidx, ns, pf);
     return IGS_OK;
 }
 
@@ -665,7 +670,8 @@ int igs_publish(igs_ctx* ctx, const double* dloss, long long* host_res) {
 }
 
 int igs_status_reset(igs_ctx* ctx) {
-    IGS_PDL(ctx, reset_status_kernel, 1, 32, 0, ctx->status);
+    const L2Prefetch pf = igs_knn_tree_inputs(ctx);
+    IGS_PDL(ctx, reset_status_kernel, pf.nr ? ctx->sm_count : 1, pf.nr ? 256 : 32, 0, ctx->status, pf);
     return IGS_OK;
 }
 
@@ -706,8 +712,15 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
     int e;
     if (ctx->opt_cull && kk <= 32) {
         // fused: exact top-K search + blend / loss / gradient epilogue per warp
+        // the fused Adam's parameter rows and moments, prefetched during the search
+        L2Prefetch pf{};
+        if (fuse_lr4) {
+            l2pf_add(pf, ctx->params, (size_t)n * 64);
+            l2pf_add(pf, ctx->adam_m, (size_t)n * 64);
+            l2pf_add(pf, ctx->adam_v, (size_t)n * 64);
+        }
         e = igs_knn_forward_backward(ctx, mode, dev_sidx, dev_samples5, ns, kk, inv_n, losses, contrib, keys, gcnt,
-                                     ctx->opt_deterministic ? nullptr : ctx->grads, long_ctl);
+                                     ctx->opt_deterministic ? nullptr : ctx->grads, long_ctl, &pf);
         if (e) return e;
         gcnt_filled = true;
     } else {
