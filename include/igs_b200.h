@@ -67,6 +67,8 @@ uint64_t igs_kernel_launches(const igs_ctx* ctx);
 #define IGS_OPT_CULL 1          /* 1 = certified tile culling for global top-K (default), 0 = brute force */
 #define IGS_OPT_DETERMINISTIC 2 /* 1 = sample-ordered gradient reduction, bit-exact (default); 0 = fp64 atomics */
 #define IGS_OPT_TILE 3          /* tile edge in pixels for culling (default 16) */
+#define IGS_OPT_RASTER 4        /* culled global render: 0 = loose-quadtree patch search (default, k <= 32),
+                                   1 = certified per-tile candidate lists */
 int igs_set_option(igs_ctx* ctx, int option, int64_t value);
 int64_t igs_get_option(const igs_ctx* ctx, int option);
 

@@ -451,6 +451,258 @@ int check_partition(igs_ctx* ctx) {
     return IGS_OK;
 }
 
+// --- device tree build (bsp.cpp:27-118 on the GPU) --------------------------
+// Level-synchronous restatement of Builder::build.  Once: every point's key
+// along x and along y, radix-sorted with the index as the stable tie-break
+// -- the (coord, idx) order the reference's comparator defines.  Per level:
+// a stable radix sort of that global order by the point's current node
+// yields every active node's members in (coord, idx) order as one
+// contiguous segment; one thread per node applies the tie-aware split rule
+// (pos, line); points move to their child.  The host (a few thousand nodes)
+// turns the level records into the reference's DFS numbering of nodes and
+// blocks and the block rectangles.
+__device__ __forceinline__ unsigned long long coord_key(double v) {
+    if (v == 0.0) v = 0.0;  // -0 and +0 compare equal in the reference
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+
+__global__ void gb_keys_kernel(const ScanRec* __restrict__ scan, uint32_t n, unsigned long long* __restrict__ kx,
+                               unsigned long long* __restrict__ ky, uint32_t* __restrict__ iota,
+                               uint32_t* __restrict__ node_of) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    kx[i] = coord_key(scan[i].mu_x);
+    ky[i] = coord_key(scan[i].mu_y);
+    iota[i] = i;
+    node_of[i] = 0;
+}
+
+// node key of the j-th point in the global (coord, idx) order
+__global__ void gb_gather_kernel(const uint32_t* __restrict__ ord, const uint32_t* __restrict__ node_of, uint32_t n,
+                                 uint32_t* __restrict__ key) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n) key[j] = node_of[ord[j]];
+}
+
+__device__ __forceinline__ double coord_of(const ScanRec* __restrict__ scan, uint32_t i, int axis) {
+    return axis == 0 ? scan[i].mu_x : scan[i].mu_y;
+}
+
+// bsp.cpp:54-95 for active node k: members seg[start[k] .. start[k]+size[k])
+__global__ void gb_split_kernel(const ScanRec* __restrict__ scan, const uint32_t* __restrict__ seg,
+                                const uint32_t* __restrict__ start, const uint32_t* __restrict__ size, uint32_t na,
+                                int axis, uint32_t* __restrict__ pos_out, double* __restrict__ line_out) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= na) return;
+    const uint32_t* m = seg + start[k];
+    const size_t n = size[k], half = n / 2;
+    auto c = [&](size_t j) { return coord_of(scan, m[j], axis); };
+    size_t pos = 0;
+    double line = 0.0;
+    bool forced = false;
+    if (c(half - 1) < c(half)) {
+        pos = half;
+    } else {
+        size_t lo = 0, hi = 0;
+        bool has_lo = false, has_hi = false;
+        for (size_t j = half; j-- > 1;)
+            if (c(j - 1) < c(j)) {
+                lo = j;
+                has_lo = true;
+                break;
+            }
+        for (size_t j = half + 1; j < n; ++j)
+            if (c(j - 1) < c(j)) {
+                hi = j;
+                has_hi = true;
+                break;
+            }
+        if (has_lo && (!has_hi || half - lo <= hi - half)) pos = lo;
+        else if (has_hi) pos = hi;
+        else forced = true;
+    }
+    if (forced) {
+        pos = half;
+        line = c(0);
+    } else {
+        const double lo_c = c(pos - 1), hi_c = c(pos);
+        line = __dmul_rn(0.5, __dadd_rn(lo_c, hi_c));
+        if (!(line > lo_c)) line = hi_c;
+    }
+    pos_out[k] = (uint32_t)pos;
+    line_out[k] = line;
+}
+
+// Moves the points of active nodes to their children (next-level active
+// rank, or `inactive` once the child is a leaf).
+__global__ void gb_move_kernel(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ seg_node, uint32_t cnt,
+                               const uint32_t* __restrict__ start, const uint32_t* __restrict__ pos,
+                               const uint32_t* __restrict__ child, uint32_t* __restrict__ node_of) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= cnt) return;
+    const uint32_t k = seg_node[j];
+    node_of[seg[j]] = child[2 * k + (j - start[k] < pos[k] ? 0 : 1)];
+}
+
+struct GbLevelNode {
+    uint32_t size;
+    bool leaf;
+    uint32_t pos = 0;
+    double line = 0.0;
+    uint32_t low = 0, high = 0;  // indices into the next level
+    RectD rect;
+};
+
+// Builds p->nodes / p->blocks / p->root exactly like Builder on the device.
+int build_tree_device(igs_ctx* ctx, PartitionDev* p, int n_max) {
+    const uint32_t n = ctx->n;
+    const size_t tb_n = ((size_t)n + 255) / 256;
+    // scratch: kx, ky (u64); ordX, ordY, iota, node_of, key, key_sorted, seg (u32)
+    // (active nodes hold > n_max >= 1 points each: at most n / 2 of them)
+    uint32_t* s32 = (uint32_t*)igs_scratch(ctx, 29, ((size_t)n * 7 + 5 * ((size_t)n / 2 + 1)) * 4);
+    unsigned long long* s64 = (unsigned long long*)igs_scratch(ctx, 30, (size_t)n * 8 * 4);
+    if (!s32 || !s64) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (bsp build)");
+    unsigned long long *kx = s64, *ky = s64 + n, *ks = s64 + 2 * (size_t)n;
+    uint32_t *ordX = s32, *ordY = s32 + n, *iota = s32 + 2 * (size_t)n, *node_of = s32 + 3 * (size_t)n,
+             *key = s32 + 4 * (size_t)n, *key_sorted = s32 + 5 * (size_t)n, *seg = s32 + 6 * (size_t)n;
+    uint32_t* small = s32 + 7 * (size_t)n;  // per-level node arrays (start | size | pos | child...)
+    double* line_d = (double*)(s64 + 3 * (size_t)n);
+    gb_keys_kernel<<<(unsigned)tb_n, 256, 0, ctx->stream>>>(ctx->scan, n, kx, ky, iota, node_of);
+    IGS_LAUNCHED(ctx);
+    size_t tb = 0, tb2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, kx, ks, iota, ordX, (int)n, 0, 64, ctx->stream);
+    cub::DeviceRadixSort::SortPairs(nullptr, tb2, key, key_sorted, ordX, seg, (int)n, 0, 32, ctx->stream);
+    void* temp = igs_scratch(ctx, 31, std::max(tb, tb2));
+    if (!temp) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (bsp build)");
+    const size_t tcap = std::max(tb, tb2);
+    tb = tcap;
+    IGS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(temp, tb, kx, ks, iota, ordX, (int)n, 0, 64, ctx->stream));
+    tb = tcap;
+    IGS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(temp, tb, ky, ks, iota, ordY, (int)n, 0, 64, ctx->stream));
+    ctx->launches += 8;
+
+    std::vector<std::vector<GbLevelNode>> levels(1);
+    levels[0].push_back(GbLevelNode{n, (long long)n <= (long long)n_max, 0, 0.0, 0, 0, RectD{0.0, 0.0, 1.0, 1.0}});
+    for (int d = 0;; ++d) {
+        std::vector<GbLevelNode>& lv = levels[d];
+        // active nodes of this level in order, their starts
+        std::vector<uint32_t> act;
+        for (uint32_t k = 0; k < lv.size(); ++k)
+            if (!lv[k].leaf) act.push_back(k);
+        const uint32_t na = (uint32_t)act.size();
+        if (na == 0) break;
+        std::vector<uint32_t> hs(3 * (size_t)na);  // start | size | (pos)
+        uint32_t total = 0;
+        for (uint32_t a = 0; a < na; ++a) {
+            hs[a] = total;
+            hs[na + a] = lv[act[a]].size;
+            total += lv[act[a]].size;
+        }
+        uint32_t *d_start = small, *d_size = small + na, *d_pos = small + 2 * (size_t)na,
+                 *d_child = small + 3 * (size_t)na;  // 2 na entries
+        IGS_CUDA(ctx, cudaMemcpyAsync(d_start, hs.data(), 2 * (size_t)na * 4, cudaMemcpyHostToDevice, ctx->stream));
+        const int axis = d % 2;
+        const uint32_t* ord = axis == 0 ? ordX : ordY;
+        // node key per point in the global order; inactive points sort last
+        gb_gather_kernel<<<(unsigned)tb_n, 256, 0, ctx->stream>>>(ord, node_of, n, key);
+        IGS_LAUNCHED(ctx);
+        int bits = 1;
+        while (bits < 32 && (1u << bits) <= na) ++bits;
+        tb = tcap;
+        IGS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(temp, tb, key, key_sorted, ord, seg, (int)n, 0, bits,
+                                                      ctx->stream));
+        ctx->launches += 2 * ((bits + 7) / 8) + 1;
+        gb_split_kernel<<<(na + 127) / 128, 128, 0, ctx->stream>>>(ctx->scan, seg, d_start, d_size, na, axis, d_pos,
+                                                                  line_d);
+        IGS_LAUNCHED(ctx);
+        std::vector<double> hl(na);
+        IGS_CUDA(ctx, cudaMemcpyAsync(hs.data() + 2 * (size_t)na, d_pos, (size_t)na * 4, cudaMemcpyDeviceToHost,
+                                      ctx->stream));
+        IGS_CUDA(ctx, cudaMemcpyAsync(hl.data(), line_d, (size_t)na * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        IGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        // children (bsp.cpp:96-117): low = [0, pos), high = [pos, n)
+        levels.emplace_back();
+        std::vector<GbLevelNode>& nx = levels[d + 1];
+        std::vector<GbLevelNode>& cur = levels[d];  // (levels may have reallocated)
+        std::vector<uint32_t> child(2 * (size_t)na);
+        uint32_t next_active = 0;
+        for (uint32_t a = 0; a < na; ++a) {
+            GbLevelNode& nd = cur[act[a]];
+            nd.pos = hs[2 * (size_t)na + a];
+            nd.line = hl[a];
+            RectD lr = nd.rect, hr = nd.rect;
+            if (axis == 0) {
+                lr.x2 = nd.line;
+                hr.x1 = nd.line;
+            } else {
+                lr.y2 = nd.line;
+                hr.y1 = nd.line;
+            }
+            const uint32_t sz[2] = {nd.pos, nd.size - nd.pos};
+            const RectD rc[2] = {lr, hr};
+            for (int h = 0; h < 2; ++h) {
+                const bool leaf = (long long)sz[h] <= (long long)n_max;
+                (h == 0 ? nd.low : nd.high) = (uint32_t)nx.size();
+                child[2 * (size_t)a + h] = leaf ? 0xFFFFFFFFu : next_active++;
+                nx.push_back(GbLevelNode{sz[h], leaf, 0, 0.0, 0, 0, rc[h]});
+            }
+        }
+        IGS_CUDA(ctx, cudaMemcpyAsync(d_child, child.data(), child.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+        gb_move_kernel<<<(total + 255) / 256, 256, 0, ctx->stream>>>(seg, key_sorted, total, d_start, d_pos, d_child,
+                                                                    node_of);
+        IGS_LAUNCHED(ctx);
+        // (the next level's host staging reuses `small`; order the copies)
+        IGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    // DFS numbering (bsp.cpp:32-118): preorder node ids, leaves in visit order
+    const int D = (int)levels.size();
+    std::vector<std::vector<uint32_t>> cnt(D), leaves(D);
+    for (int d = D - 1; d >= 0; --d) {
+        cnt[d].resize(levels[d].size());
+        leaves[d].resize(levels[d].size());
+        for (size_t k = 0; k < levels[d].size(); ++k) {
+            const GbLevelNode& nd = levels[d][k];
+            if (nd.leaf) {
+                cnt[d][k] = 1;
+                leaves[d][k] = 1;
+            } else {
+                cnt[d][k] = 1 + cnt[d + 1][nd.low] + cnt[d + 1][nd.high];
+                leaves[d][k] = leaves[d + 1][nd.low] + leaves[d + 1][nd.high];
+            }
+        }
+    }
+    p->nodes.assign(cnt[0][0], NodeD{0, 0.0, -1, -1, -1});
+    p->blocks.assign(leaves[0][0], RectD{});
+    std::vector<std::vector<int32_t>> id(D), boff(D);
+    for (int d = 0; d < D; ++d) {
+        id[d].resize(levels[d].size());
+        boff[d].resize(levels[d].size());
+    }
+    id[0][0] = 0;
+    boff[0][0] = 0;
+    for (int d = 0; d < D; ++d)
+        for (size_t k = 0; k < levels[d].size(); ++k) {
+            const GbLevelNode& nd = levels[d][k];
+            NodeD& out = p->nodes[id[d][k]];
+            if (nd.leaf) {
+                out.block = boff[d][k];
+                p->blocks[boff[d][k]] = nd.rect;
+                continue;
+            }
+            out.axis = d % 2;
+            out.line = nd.line;
+            id[d + 1][nd.low] = id[d][k] + 1;
+            id[d + 1][nd.high] = id[d][k] + 1 + (int32_t)cnt[d + 1][nd.low];
+            boff[d + 1][nd.low] = boff[d][k];
+            boff[d + 1][nd.high] = boff[d][k] + (int32_t)leaves[d + 1][nd.low];
+            out.low = id[d + 1][nd.low];
+            out.high = id[d + 1][nd.high];
+        }
+    p->root = 0;
+    return IGS_OK;
+}
+
 int download_centres(igs_ctx* ctx, std::vector<double>& mx, std::vector<double>& my) {
     std::vector<double> p((size_t)ctx->n * 8);
     if (ctx->n) {
@@ -485,17 +737,15 @@ int igs_partition_build(igs_ctx* ctx, int n_max) {
     cudaSetDevice(ctx->device);
     if (ctx->n == 0) return igs_fail(ctx, IGS_E_EMPTY_SET, "build_partition requires a non-empty GaussianSet");
     if (n_max < 1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "n_max must be >= 1");
-    std::vector<double> mx, my;
-    int e = download_centres(ctx, mx, my);
-    if (e) return e;
     auto* p = new PartitionDev();
     p->tree = true;
     p->n_max = n_max;
     p->source_size = ctx->n;
-    std::vector<uint32_t> all(ctx->n);
-    for (uint32_t i = 0; i < ctx->n; ++i) all[i] = i;
-    Builder b{mx, my, n_max, *p};
-    p->root = b.build(RectD{0.0, 0.0, 1.0, 1.0}, std::move(all), 0);
+    int e = build_tree_device(ctx, p, n_max);
+    if (e) {
+        delete p;
+        return e;
+    }
     igs_partition_free(ctx);
     ctx->part = p;
     if ((e = finish_partition(ctx, p))) {

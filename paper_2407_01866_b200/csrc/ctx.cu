@@ -17,6 +17,7 @@ using namespace igs_dev;
 // train.cu
 int igs_status_reset(igs_ctx* ctx);
 int igs_stage_samples(igs_ctx* ctx, const uint32_t* host_pinned, uint32_t* dsidx, uint32_t ns);
+int igs_stage_draws(igs_ctx* ctx, const unsigned long long* host_raw, uint32_t* dsidx, uint32_t ns);
 int igs_publish(igs_ctx* ctx, const double* dloss, long long* host_res);
 int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint32_t* dev_sidx,
                          const double* dev_samples5, double* dev_loss, double inv_n, const double* fuse_lr4 = nullptr,
@@ -268,6 +269,8 @@ void igs_ctx_destroy(igs_ctx* ctx) {
     cudaFree(ctx->image.p);
     cudaFree(ctx->target.p);
     cudaFree(ctx->samples.p);
+    cudaFree(ctx->alias_prob.p);
+    cudaFree(ctx->alias_idx.p);
     cudaFree(ctx->status);
     cudaFree(ctx->flush.p);
     cudaFree(ctx->prof_dev_work);
@@ -306,6 +309,7 @@ int igs_set_option(igs_ctx* ctx, int option, int64_t value) {
     switch (option) {
         case IGS_OPT_CULL: ctx->opt_cull = value ? 1 : 0; return IGS_OK;
         case IGS_OPT_DETERMINISTIC: ctx->opt_deterministic = value ? 1 : 0; return IGS_OK;
+        case IGS_OPT_RASTER: ctx->opt_raster = value ? 1 : 0; return IGS_OK;
         case IGS_OPT_TILE:
             if (value != 8 && value != 16 && value != 32)
                 return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "tile must be 8, 16 or 32");
@@ -320,6 +324,7 @@ int64_t igs_get_option(const igs_ctx* ctx, int option) {
     switch (option) {
         case IGS_OPT_CULL: return ctx->opt_cull;
         case IGS_OPT_DETERMINISTIC: return ctx->opt_deterministic;
+        case IGS_OPT_RASTER: return ctx->opt_raster;
         case IGS_OPT_TILE: return ctx->opt_tile;
     }
     return -1;
@@ -403,7 +408,8 @@ static int render_rows(igs_ctx* ctx, int W, int H, int k, int row0, int row1, fl
         if (!dtopk) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (top-k dump)");
     }
     float* dout = (float*)ctx->image.p;
-    if (ctx->opt_cull) e = igs_raster_culled(ctx, W, H, k, row0, row1, dout, dtopk);
+    if (ctx->opt_cull && ctx->opt_raster == 0 && kk <= 32) e = igs_raster_knn(ctx, W, H, k, row0, row1, dout, dtopk);
+    else if (ctx->opt_cull) e = igs_raster_culled(ctx, W, H, k, row0, row1, dout, dtopk);
     else e = igs_raster_global(ctx, W, H, k, row0, row1, dout, dtopk);
     if (e) return e;
     if (out_rgb && (e = dev_to_host(ctx, out_rgb, dout, (size_t)W * (row1 - row0) * 3 * sizeof(float)))) return e;
@@ -648,19 +654,26 @@ static void* async_pinned(igs_ctx* ctx, int which, size_t bytes) {
     return b.p;
 }
 
-int igs_train_iteration_async(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, int k, const double* lr4,
-                              long long t) {
-    CHECK_CTX(ctx);
-    cudaSetDevice(ctx->device);
+// One enqueued iteration; the samples are either indices (sample_idx) or
+// raw engine outputs to draw from the uploaded alias table (raw2: 2 per
+// sample, the fit driver).
+static int train_iteration_enqueue(igs_ctx* ctx, const uint32_t* sample_idx, const unsigned long long* raw2,
+                                   uint32_t ns, int k, const double* lr4, long long t) {
     int e;
     if (ctx->async_count >= 2) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "two iterations are already outstanding");
     if ((e = train_checks(ctx, ns, k))) return e;
     if (t < 1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "Adam step index must be >= 1");
-    const uint64_t npx = (uint64_t)ctx->tgt_w * ctx->tgt_h;
-    for (uint32_t i = 0; i < ns; ++i)
-        if (sample_idx[i] >= npx) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "sample index outside the target");
+    if (sample_idx) {
+        const uint64_t npx = (uint64_t)ctx->tgt_w * ctx->tgt_h;
+        for (uint32_t i = 0; i < ns; ++i)
+            if (sample_idx[i] >= npx)
+                return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "sample index outside the target");
+    } else if (ctx->alias_n != (uint64_t)ctx->tgt_w * ctx->tgt_h) {
+        return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "no sampling table for the target");
+    }
     const int slot = (ctx->async_head + ctx->async_count) & 1;
-    uint32_t* pin = (uint32_t*)async_pinned(ctx, slot, (size_t)ns * 4);
+    const size_t in_bytes = sample_idx ? (size_t)ns * 4 : (size_t)ns * 16;
+    void* pin = async_pinned(ctx, slot, in_bytes);
     long long* res = (long long*)async_pinned(ctx, 2 + slot, 64);
     // the device sample buffer is shared: the next iteration's copy into it
     // is ordered after this iteration's kernels on the stream
@@ -669,8 +682,11 @@ int igs_train_iteration_async(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t
     if (!pin || !res || !dsidx || !dloss) return igs_fail(ctx, IGS_E_CUDA, "out of memory (async iteration)");
     if (!ctx->async_ev[slot]) IGS_CUDA(ctx, cudaEventCreateWithFlags(&ctx->async_ev[slot], cudaEventDisableTiming));
     dloss += slot;
-    std::memcpy(pin, sample_idx, (size_t)ns * 4);
-    if ((e = igs_stage_samples(ctx, pin, dsidx, ns))) return e;  // status reset + H2D
+    std::memcpy(pin, sample_idx ? (const void*)sample_idx : (const void*)raw2, in_bytes);
+    // status reset + H2D (or device draws)
+    if (sample_idx) e = igs_stage_samples(ctx, (const uint32_t*)pin, dsidx, ns);
+    else e = igs_stage_draws(ctx, (const unsigned long long*)pin, dsidx, ns);
+    if (e) return e;
     const uint32_t ns_total = ns * (uint32_t)ctx->nranks;
     bool fused = false;
     if ((e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss, 1.0 / (double)ns_total, lr4, t, &fused)))
@@ -684,6 +700,36 @@ int igs_train_iteration_async(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t
     IGS_CUDA(ctx, cudaEventRecord(ctx->async_ev[slot], ctx->stream));
     ctx->async_count++;
     return IGS_OK;
+}
+
+int igs_train_iteration_async(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, int k, const double* lr4,
+                              long long t) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    if (!sample_idx) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "null sample indices");
+    return train_iteration_enqueue(ctx, sample_idx, nullptr, ns, k, lr4, t);
+}
+
+// fit driver (fit.cpp), not part of the public header: the sampling table
+// on the device, and iterations whose samples are drawn there
+int igs_internal_set_sampler(igs_ctx* ctx, const double* prob, const uint32_t* alias, uint64_t n) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    ctx->alias_n = 0;
+    if (!grow(ctx->alias_prob, n * 8) || !grow(ctx->alias_idx, n * 4))
+        return igs_fail(ctx, IGS_E_CUDA, "out of device memory (sampler)");
+    int e;
+    if ((e = host_to_dev(ctx, ctx->alias_prob.p, prob, n * 8))) return e;
+    if ((e = host_to_dev(ctx, ctx->alias_idx.p, alias, n * 4))) return e;
+    ctx->alias_n = n;
+    return IGS_OK;
+}
+
+int igs_internal_train_iteration_async_raw(igs_ctx* ctx, const unsigned long long* raw2, uint32_t ns, int k,
+                                           const double* lr4, long long t) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    return train_iteration_enqueue(ctx, nullptr, raw2, ns, k, lr4, t);
 }
 
 int igs_train_wait(igs_ctx* ctx, double* loss) {

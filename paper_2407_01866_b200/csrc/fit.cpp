@@ -16,6 +16,8 @@
 // does that work first and then draws (the reference's RNG order: samples_t,
 // densification draws at t, samples_{t+1}).
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -28,6 +30,9 @@
 
 // ctx.cu: records the message returned by igs_last_error
 extern "C" int igs_internal_fail(igs_ctx* ctx, int code, const char* msg);
+extern "C" int igs_internal_set_sampler(igs_ctx* ctx, const double* prob, const uint32_t* alias, uint64_t n);
+extern "C" int igs_internal_train_iteration_async_raw(igs_ctx* ctx, const unsigned long long* raw2, uint32_t ns,
+                                                      int k, const double* lr4, long long t);
 
 namespace {
 
@@ -198,6 +203,13 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
                   c.densify_interval, (unsigned long long)c.seed);
     text += line;
 
+    // IGS_FIT_TRACE=1: wall time per phase on stderr (init, iterations,
+    // evaluation renders, densification)
+    const bool trace = std::getenv("IGS_FIT_TRACE") != nullptr;
+    using clk = std::chrono::steady_clock;
+    double t_init = 0, t_eval = 0, t_densify = 0, t_render = 0, t_metric = 0;
+    const auto t_start = clk::now();
+    auto since = [](clk::time_point a) { return std::chrono::duration<double, std::milli>(clk::now() - a).count(); };
     Rng rng(c.seed);
     // initialize_set(target, budget/2, lambda_init, rng) (sampling.cpp:154-174)
     const int init_count = c.budget / 2;
@@ -213,6 +225,10 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
     if (!opt.ok) return bad("alias table weights must have positive sum");
     if ((e = igs_set_target(ctx, target, W, H))) return e;
     if ((e = igs_set_params(ctx, set.data(), (uint32_t)init_count))) return e;
+    // the per-iteration draws from `opt` happen on the device (the host only
+    // advances the engine): the table goes up once
+    if ((e = igs_internal_set_sampler(ctx, opt.prob.data(), opt.alias.data(), opt.prob.size()))) return e;
+    t_init = since(t_start);
 
     double lr[4] = {c.lr[0], c.lr[1], c.lr[2], c.lr[3]};
     bool decayed = false;
@@ -226,10 +242,13 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
     std::vector<std::string> checkpoints;
     std::vector<float> rendered((size_t)W * H * 3);
     std::vector<double> dist((size_t)W * H);
-    std::vector<uint32_t> cur((size_t)c.samples_per_iter), next((size_t)c.samples_per_iter);
-    auto draw = [&](std::vector<uint32_t>& s) {
-        for (auto& v : s) v = opt.sample(rng);
+    // one sample = opt.sample(rng) = next_index (one engine output) then
+    // next_double (one more): the raw outputs, in that order
+    std::vector<unsigned long long> cur(2 * (size_t)c.samples_per_iter), next(2 * (size_t)c.samples_per_iter);
+    auto draw = [&](std::vector<unsigned long long>& s) {
+        for (auto& v : s) v = rng.e();
     };
+    const uint32_t ns = (uint32_t)c.samples_per_iter;
     auto emit_checkpoint = [&](int iteration) -> int {
         const uint32_t n = igs_num_gaussians(ctx);
         char id[64];
@@ -260,8 +279,7 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
     // the host draws t+1's samples and enqueues it (unless t evaluates or
     // densifies, which needs the set after t), then waits on t.
     draw(cur);
-    if (c.iterations >= 1 && (e = igs_train_iteration_async(ctx, cur.data(), (uint32_t)cur.size(), c.k, lr, 1)))
-        return e;
+    if (c.iterations >= 1 && (e = igs_internal_train_iteration_async_raw(ctx, cur.data(), ns, c.k, lr, 1))) return e;
     for (int iter = 1; iter <= c.iterations; ++iter) {
         const bool do_eval = iter % c.eval_interval == 0 || iter == c.iterations;
         const bool do_densify = stage < 4 && iter == c.warmup_iters + stage * c.densify_interval;
@@ -269,7 +287,7 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
         if (!do_eval && !do_densify) {
             if (iter < c.iterations) {
                 draw(next);  // overlaps the device step
-                if ((e = igs_train_iteration_async(ctx, next.data(), (uint32_t)next.size(), c.k, lr, iter + 1)))
+                if ((e = igs_internal_train_iteration_async_raw(ctx, next.data(), ns, c.k, lr, iter + 1)))
                     return drain(e);  // t is still outstanding
             }
             if ((e = igs_train_wait(ctx, &loss))) return iter < c.iterations ? drain(e) : e;  // t+1 outstanding
@@ -278,12 +296,18 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
         }
         if ((e = igs_train_wait(ctx, &loss))) return e;
         bool have_render = false;
+        const auto t_post = clk::now();
         if (do_eval) {
+            const auto t_r = clk::now();
             if ((e = render_current())) return e;
+            igs_sync(ctx);
+            t_render += since(t_r);
+            const auto t_m = clk::now();
             have_render = true;
             double p = 0.0, s = 0.0;
             if ((e = igs_psnr(ctx, nullptr, W, H, &p))) return e;
             if (c.compute_ssim && (e = igs_ssim(ctx, nullptr, W, H, &s))) return e;
+            t_metric += since(t_m);
             if (p >= best_psnr + 0.01) {
                 best_psnr = p;
                 streak = 0;
@@ -298,6 +322,8 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
             }
             recs.push_back({iter, (int)igs_num_gaussians(ctx), loss, p, s, best_psnr});
         }
+        t_eval += since(t_post);
+        const auto t_dens = clk::now();
         if (do_densify) {
             if ((e = emit_checkpoint(iter))) return e;
             if (!have_render && (e = render_current())) return e;
@@ -311,13 +337,20 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
             if (add_count > 0 && (e = igs_append_params(ctx, fresh.data(), (uint32_t)add_count))) return e;
             ++stage;
         }
+        t_densify += since(t_dens);
         if (iter < c.iterations) {
             draw(next);
             std::swap(cur, next);
-            if ((e = igs_train_iteration_async(ctx, cur.data(), (uint32_t)cur.size(), c.k, lr, iter + 1))) return e;
+            if ((e = igs_internal_train_iteration_async_raw(ctx, cur.data(), ns, c.k, lr, iter + 1))) return e;
         }
     }
     if ((e = emit_checkpoint(c.iterations))) return e;
+    if (trace) {
+        const double total = since(t_start);
+        std::fprintf(stderr, "igs_fit: %.1f ms total: init %.1f, evaluation %.1f (render %.1f, metrics %.1f), "
+                     "densification %.1f, iterations %.1f (%d)\n", total, t_init, t_eval, t_render, t_metric,
+                     t_densify, total - t_init - t_eval - t_densify, c.iterations);
+    }
 
     // FitReport::write (fit.cpp:209-231)
     for (const auto& r : recs) {

@@ -190,6 +190,7 @@ struct igs_ctx {
     int opt_cull = 1;
     int opt_deterministic = 1;
     int opt_tile = 16;
+    int opt_raster = 0;  // IGS_OPT_RASTER
 
     // set
     uint32_t n = 0;
@@ -222,6 +223,10 @@ struct igs_ctx {
     DevBuf async_pin[4];
     cudaEvent_t async_ev[2] = {nullptr, nullptr};
     int async_head = 0, async_count = 0;
+
+    // the fit driver's sampling distribution (alias table) on the device
+    DevBuf alias_prob, alias_idx;
+    uint64_t alias_n = 0;
 
     // uploaded samples for device-resident training
     DevBuf samples;
@@ -340,6 +345,7 @@ int igs_partition_free(igs_ctx* ctx);
 void igs_cull_free(igs_ctx* ctx);
 void igs_knn_free(igs_ctx* ctx);
 int igs_topk_knn(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq);
+int igs_raster_knn(igs_ctx* ctx, int W, int H, int k, int row0, int row1, float* out, uint32_t* topk);
 int igs_knn_forward_backward(igs_ctx* ctx, int mode, const uint32_t* sidx, const double* samples5, uint32_t npts,
                              int kk, double inv_n, double* losses, double* contrib, uint32_t* keys, uint32_t* gcnt,
                              double* grads_atomic, uint32_t* zero_word = nullptr,

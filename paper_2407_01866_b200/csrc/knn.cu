@@ -1024,6 +1024,267 @@ int run_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int kk,
     return launch_knn<32>(ctx, uv, W, H, npts, kk, E);
 }
 
+// ---------------------------------------------------------------------------
+// Global render through the loose quadtree (renderer.cpp:161-191): one warp
+// per 8 x 4 pixel patch, lane = pixel, a register top-K per lane (the
+// reference's per-pixel selection), one shared candidate search per patch.
+// A tree node or cell is skipped only when its certified bound over the
+// patch's pixel-centre box, lambda_min * dist(box, bbox)^2 * slack, exceeds
+// T = the largest kk-th best q over the lanes -- then none of its members
+// can enter any lane's top-K (strictly, so index ties are never pruned).
+// Members are staged 32 at a time in shared memory and every lane scans
+// them; the epilogue is raster_global_kernel's (blend, clamp, float32).
+// ---------------------------------------------------------------------------
+constexpr int kPatchW = 8, kPatchH = 4;
+
+__device__ __forceinline__ double box_lb(const Sum& s, double bx0, double by0, double bx1, double by1) {
+    if (s.count == 0) return __longlong_as_double(0x7ff0000000000000LL);
+    const double dx = fmax(fmax(s.x0 - bx1, bx0 - s.x1), 0.0);
+    const double dy = fmax(fmax(s.y0 - by1, by0 - s.y1), 0.0);
+    return s.lmin * (dx * dx + dy * dy) * (double)s.slack;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, d));
+    return v;
+}
+
+// Every lane offers the members of up to 32 cells (lane i: [o_i, o_i + m_i))
+// for its own pixel; returns the refreshed warp threshold.
+template <int KCAP>
+__device__ __forceinline__ double raster_members(TopK<KCAP>& t, uint32_t o_mine, uint32_t m_mine, int lane,
+                                                 const ScanRec* __restrict__ scan, const uint32_t* __restrict__ mem,
+                                                 ScanRec* stage, uint32_t* stage_i, double px, double py,
+                                                 double T, unsigned long long& evaluated) {
+    if (__ballot_sync(0xffffffffu, m_mine != 0) == 0) return T;
+    uint32_t incl = m_mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += v;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t excl = incl - m_mine;
+    evaluated += total;
+    for (uint32_t base = 0; base < total; base += 32) {
+        const uint32_t f = base + lane;
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const uint32_t ex = __shfl_sync(0xffffffffu, excl, lo + step);
+            if (ex <= f) lo += step;
+        }
+        const uint32_t lo_ex = __shfl_sync(0xffffffffu, excl, lo);
+        const uint32_t lo_o = __shfl_sync(0xffffffffu, o_mine, lo);
+        __syncwarp();
+        if (f < total) {
+            const uint32_t gi = __ldg(mem + lo_o + (f - lo_ex));
+            stage[lane] = scan[gi];
+            stage_i[lane] = gi;
+        }
+        __syncwarp();
+        const uint32_t cnt = min(32u, total - base);
+#pragma unroll 1
+        for (uint32_t c = 0; c < cnt; ++c) {
+            const double q = maha(stage[c], px, py);
+            if (__any_sync(0xffffffffu, q <= t.tq()))
+                if (q <= t.tq()) t.offer(q, stage_i[c]);
+        }
+        T = warp_max(t.tq());
+    }
+    return T;
+}
+
+template <int KCAP>
+__global__ void __launch_bounds__(128) knn_raster_kernel(const ScanRec* __restrict__ scan,
+                                                            const ShadeRec* __restrict__ shade, uint32_t n, Lq L,
+                                                            const Sum* __restrict__ own, const Sum* __restrict__ sub,
+                                                            const uint32_t* __restrict__ off,
+                                                            const uint32_t* __restrict__ mem, int W, int H, int row0,
+                                                            int row1, int kk, float* __restrict__ out,
+                                                            uint32_t* __restrict__ topk, uint32_t npx_patch,
+                                                            uint32_t npatch, uint32_t* __restrict__ next_patch,
+                                                            unsigned long long* __restrict__ pairs) {
+    __shared__ uint32_t queue[4][2][kQueue];
+    __shared__ ScanRec stage[4][32];
+    __shared__ uint32_t stage_i[4][32];
+    __shared__ int s_loff[kMaxLv];
+    __shared__ int s_lg[kMaxLv];
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int l = 0; l < kMaxLv; ++l) {
+            s_loff[l] = L.loff[l];
+            s_lg[l] = 31 - __clz(max(L.lw[l], 1));
+        }
+    }
+    __syncthreads();
+    pdl_wait();
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    unsigned lvmask = 0;
+    if (lane < L.levels && L.lcount[lane] > 0) lvmask = 1u;
+    lvmask = __ballot_sync(0xffffffffu, lvmask);
+    const int npop = __popc(lvmask);
+    const int my_pop = lane < npop ? __fns(lvmask, 0, lane + 1) : 0;
+    const int lg0 = s_lg[0];
+    for (;;) {
+        uint32_t patch = 0;
+        if (lane == 0) patch = atomicAdd(next_patch, 1u);
+        patch = __shfl_sync(0xffffffffu, patch, 0);
+        if (patch >= npatch) return;
+        const int x0 = (int)(patch % npx_patch) * kPatchW, y0 = row0 + (int)(patch / npx_patch) * kPatchH;
+        const int x1 = min(x0 + kPatchW, W) - 1, y1 = min(y0 + kPatchH, row1) - 1;
+        const int xi = x0 + (lane % kPatchW), yi = y0 + (lane / kPatchW);
+        const bool live = xi <= x1 && yi <= y1;
+        // lanes past the edge work on a copy of an edge pixel (so the
+        // warp threshold stays finite) and write nothing
+        const double px = center(min(xi, x1), W), py = center(min(yi, y1), H);
+        const double bx0 = center(x0, W), bx1 = center(x1, W), by0 = center(y0, H), by1 = center(y1, H);
+        TopK<KCAP> t;
+        t.init(kk);
+        double T = __longlong_as_double(0x7ff0000000000000LL);
+        unsigned long long evaluated = 0;
+        const double cx = __dmul_rn(0.5, __dadd_rn(bx0, bx1)), cy = __dmul_rn(0.5, __dadd_rn(by0, by1));
+        const int cx0 = cell_of(cx, 1 << lg0), cy0 = cell_of(cy, 1 << lg0);
+
+        // (1) seeds around the patch centre's cell (see knn_points_kernel)
+        const int nseed = npop * 9;
+        const int lfine = __ffs(lvmask) - 1;
+        for (int pass = 0; pass < 2; ++pass) {
+            for (int b = 0; b < nseed; b += 32) {
+                const int it = b + lane;
+                const int l = __shfl_sync(0xffffffffu, my_pop, min(it / 9, 31));
+                uint32_t o = 0, m = 0;
+                if (it < nseed) {
+                    const int d = it % 9, lg = s_lg[l], G = 1 << lg;
+                    const int x = (cx0 >> l) + d % 3 - 1, y = (cy0 >> l) + d / 3 - 1;
+                    const bool primary = d == 4 || l == lfine;
+                    if (x >= 0 && x < G && y >= 0 && y < G && primary == (pass == 0)) {
+                        const uint32_t c = (uint32_t)(s_loff[l] + (y << lg) + x);
+                        const Sum so = own[c];
+                        if (so.count && (primary || box_lb(so, bx0, by0, bx1, by1) <= T)) {
+                            o = off[c];
+                            m = so.count;
+                        }
+                    }
+                }
+                T = raster_members(t, o, m, lane, scan, mem, stage[warp], stage_i[warp], px, py, T, evaluated);
+            }
+        }
+
+        // (2) descent from the root with box bounds
+        bool overflow = false;
+        uint32_t* cur = queue[warp][0];
+        uint32_t* nxt = queue[warp][1];
+        int ncur = 1;
+        if (lane == 0) cur[0] = 0;
+        __syncwarp();
+        for (int l = L.levels - 1; l >= 0 && ncur > 0; --l) {
+            const int lg = s_lg[l];
+            const int wmask = (1 << lg) - 1;
+            const int sx = cx0 >> l, sy = cy0 >> l;
+            const uint32_t lo = (uint32_t)s_loff[l];
+            for (int b = 0; b < ncur; b += 32) {
+                const int i = b + lane;
+                uint32_t o = 0, m = 0;
+                if (i < ncur) {
+                    const uint32_t node = cur[i];
+                    const int x = (int)node & wmask, y = (int)(node >> lg);
+                    if (abs(x - sx) > 1 || abs(y - sy) > 1) {
+                        const uint32_t c = lo + node;
+                        const Sum so = own[c];
+                        if (so.count && box_lb(so, bx0, by0, bx1, by1) <= T) {
+                            o = off[c];
+                            m = so.count;
+                        }
+                    }
+                }
+                T = raster_members(t, o, m, lane, scan, mem, stage[warp], stage_i[warp], px, py, T, evaluated);
+            }
+            if (l == 0) break;
+            const uint32_t clo = (uint32_t)s_loff[l - 1];
+            const int clg = lg + 1;
+            int nnext = 0;
+            for (int b = 0; b < ncur * 4; b += 32) {
+                const int item = b + lane;
+                bool keep = false;
+                uint32_t child = 0;
+                if (item < ncur * 4) {
+                    const uint32_t node = cur[item >> 2];
+                    const uint32_t x = node & (uint32_t)wmask, y = node >> lg;
+                    child = ((2 * y + ((item >> 1) & 1)) << clg) + 2 * x + (item & 1);
+                    keep = box_lb(sub[clo + child], bx0, by0, bx1, by1) <= T;
+                }
+                const unsigned msk = __ballot_sync(0xffffffffu, keep);
+                const int pos = nnext + __popc(msk & ((1u << lane) - 1));
+                if (keep && pos < kQueue) nxt[pos] = child;
+                nnext += __popc(msk);
+            }
+            __syncwarp();
+            if (nnext > kQueue) {
+                overflow = true;
+                break;
+            }
+            uint32_t* tmp = cur;
+            cur = nxt;
+            nxt = tmp;
+            ncur = nnext;
+        }
+        if (overflow) {
+            // the frontier outgrew the queue: every lane scans all N (exact)
+            t.init(kk);
+            for (uint32_t b = 0; b < n; b += 32) {
+                __syncwarp();
+                const uint32_t gi = b + lane;
+                if (gi < n) {
+                    stage[warp][lane] = scan[gi];
+                    stage_i[warp][lane] = gi;
+                }
+                __syncwarp();
+                const uint32_t cnt = min(32u, n - b);
+#pragma unroll 1
+                for (uint32_t c = 0; c < cnt; ++c) {
+                    const double q = maha(stage[warp][c], px, py);
+                    if (__any_sync(0xffffffffu, q <= t.tq()))
+                        if (q <= t.tq()) t.offer(q, stage_i[warp][c]);
+                }
+            }
+            evaluated += n;
+        }
+        if (pairs && lane == 0) atomicAdd(pairs, evaluated * 32ull);
+        if (!live) continue;
+        double col[3];
+        blend_topk(t, shade, col);
+        const size_t o = (size_t)(yi - row0) * W + xi;
+        out[o * 3 + 0] = clamp01f(col[0]);
+        out[o * 3 + 1] = clamp01f(col[1]);
+        out[o * 3 + 2] = clamp01f(col[2]);
+        if (topk) store_topk(t, (double*)nullptr, topk + ((size_t)yi * W + xi) * kk);
+    }
+}
+
+template <int KCAP>
+int launch_knn_raster(igs_ctx* ctx, int W, int H, int row0, int row1, int kk, float* out, uint32_t* topk) {
+    KnnBufs& b = *static_cast<KnnBufs*>(ctx->knn);
+    uint32_t* cursor = (uint32_t*)igs_scratch(ctx, 27, 16);
+    if (!cursor) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (raster)");
+    IGS_CUDA(ctx, cudaMemsetAsync(cursor, 0, 4, ctx->stream));
+    const uint32_t npx = (uint32_t)((W + kPatchW - 1) / kPatchW);
+    const uint32_t npy = (uint32_t)((row1 - row0 + kPatchH - 1) / kPatchH);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, knn_raster_kernel<KCAP>, 128, 0);
+    const unsigned blocks = (unsigned)std::min<uint64_t>((uint64_t)std::max(1, per_sm) * ctx->sm_count,
+                                                         ((uint64_t)npx * npy + 3) / 4);
+    igs_prof_begin(ctx, IGS_PROF_SCAN);
+    IGS_PDL(ctx, knn_raster_kernel<KCAP>, blocks, 128, 0, (const ScanRec*)ctx->scan, (const ShadeRec*)ctx->shade,
+            ctx->n, b.lq, (const Sum*)b.own.p, (const Sum*)b.sub.p, (const uint32_t*)b.off.p,
+            (const uint32_t*)b.mem.p, W, H, row0, row1, kk, out, topk, npx, npx * npy, cursor,
+            igs_prof_counter(ctx, IGS_PROF_SCAN));
+    igs_prof_end(ctx, IGS_PROF_SCAN, 0.0);
+    return IGS_OK;
+}
+
 }  // namespace
 
 // The refit's inputs (cell accumulators and counts), for the step's first
@@ -1065,6 +1326,17 @@ void igs_knn_free(igs_ctx* ctx) {
         cudaFree(d->p);
     delete b;
     ctx->knn = nullptr;
+}
+
+// Global render (kk <= 32) through the loose quadtree; rows [row0, row1).
+int igs_raster_knn(igs_ctx* ctx, int W, int H, int k, int row0, int row1, float* out, uint32_t* topk) {
+    const int kk = (int)std::min<uint32_t>((uint32_t)k, ctx->n);
+    int e = knn_build(ctx);
+    if (e) return e;
+    if (kk <= 4) return launch_knn_raster<4>(ctx, W, H, row0, row1, kk, out, topk);
+    if (kk <= 8) return launch_knn_raster<8>(ctx, W, H, row0, row1, kk, out, topk);
+    if (kk <= 16) return launch_knn_raster<16>(ctx, W, H, row0, row1, kk, out, topk);
+    return launch_knn_raster<32>(ctx, W, H, row0, row1, kk, out, topk);
 }
 
 // Exact top-K (q ascending, idx) at device points; kk = min(k, n).

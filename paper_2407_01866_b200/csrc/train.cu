@@ -605,6 +605,26 @@ __global__ void stage_kernel(long long* __restrict__ status, const uint32_t* __r
     if (i < ns) dsidx[i] = host_sidx[i];
 }
 
+// Same, drawing the samples on the device from raw engine outputs: sample j
+// is AliasTable::sample (sampling.cpp:126-133) with rng.next_index(n) =
+// raw[2j] % n and rng.next_double() = (raw[2j+1] >> 11) * 2^-53 -- the
+// reference's draw, bit for bit, with the table lookups (random accesses
+// into a W*H table) done here instead of on the host.
+__global__ void draw_stage_kernel(long long* __restrict__ status, const unsigned long long* __restrict__ host_raw,
+                                  const double* __restrict__ prob, const uint32_t* __restrict__ alias,
+                                  unsigned long long table_n, uint32_t* __restrict__ dsidx, uint32_t ns,
+                                  L2Prefetch pf) {
+    pdl_wait();
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    prefetch_l2(pf, i, gridDim.x * blockDim.x);
+    if (blockIdx.x == 0 && threadIdx.x < 4) status[threadIdx.x] = threadIdx.x == 3 ? 0 : LLONG_MAX;
+    if (i >= ns) return;
+    const unsigned long long r0 = host_raw[2 * (size_t)i], r1 = host_raw[2 * (size_t)i + 1];
+    const unsigned long long j = r0 % table_n;
+    const double coin = (double)(r1 >> 11) * 0x1.0p-53;
+    dsidx[i] = coin < prob[j] ? (uint32_t)j : alias[j];
+}
+
 // End of an iteration: status block + loss into the pinned result block.
 __global__ void publish_kernel(const long long* __restrict__ status, const double* __restrict__ dloss,
                                long long* __restrict__ host_res) {
@@ -661,6 +681,14 @@ int igs_stage_samples(igs_ctx* ctx, const uint32_t* host_pinned, uint32_t* dsidx
     const L2Prefetch pf = igs_knn_tree_inputs(ctx);
     const unsigned blocks = std::max((ns + 255) / 256 + (ns == 0), (unsigned)ctx->sm_count);
     IGS_PDL(ctx, stage_kernel, blocks, 256, 0, ctx->status, host_pinned, dsidx, ns, pf);
+    return IGS_OK;
+}
+
+int igs_stage_draws(igs_ctx* ctx, const unsigned long long* host_raw, uint32_t* dsidx, uint32_t ns) {
+    const L2Prefetch pf = igs_knn_tree_inputs(ctx);
+    const unsigned blocks = std::max((ns + 255) / 256 + (ns == 0), (unsigned)ctx->sm_count);
+    IGS_PDL(ctx, draw_stage_kernel, blocks, 256, 0, ctx->status, host_raw, (const double*)ctx->alias_prob.p,
+            (const uint32_t*)ctx->alias_idx.p, (unsigned long long)ctx->alias_n, dsidx, ns, pf);
     return IGS_OK;
 }
 

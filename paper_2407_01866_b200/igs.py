@@ -49,7 +49,7 @@ ERROR_KINDS = {
     100: "cuda",
 }
 
-OPT_CULL, OPT_DETERMINISTIC, OPT_TILE = 1, 2, 3
+OPT_CULL, OPT_DETERMINISTIC, OPT_TILE, OPT_RASTER = 1, 2, 3, 4
 PROF_SCAN, PROF_FINISH, PROF_REDUCE, PROF_ADAM, PROF_CULL, PROF_BLOCKED, PROF_KNN_HARD = range(7)
 PROF_NAMES = ["scan", "finish", "reduce", "adam", "cull", "blocked", "knn_hard"]
 

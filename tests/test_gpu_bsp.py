@@ -28,11 +28,24 @@ def test_golden_partition_and_blocked_render(gctx, golden):
                                atol=1e-14)
 
 
-@pytest.mark.parametrize("seed,n,n_max", [(1, 900, 16), (2, 2500, 64), (3, 40, 1), (4, 7, 8)])
+@pytest.mark.parametrize("seed,n,n_max", [(1, 900, 16), (2, 2500, 64), (3, 40, 1), (4, 7, 8), (5, 100_000, 64),
+                                          (6, 5000, 4), (7, 300, 8), (8, 2000, 16)])
 def test_partition_vs_oracle(gctx, port, seed, n, n_max):
+    """The device tree build (bsp.cu build_tree_device) against the reference's
+    recursive Builder: uniform sets, a coincident cluster, quantized
+    coordinates (ties everywhere), all points identical (forced splits), and
+    signed zeros (which the reference's comparator treats as equal)."""
     params = synth.random_set(n, 6000 + seed, 0.005, 0.06)
     if seed == 2:
         params[:600, 0:2] = params[0, 0:2]  # coincident cluster (tie-aware split)
+    if seed == 6:
+        params[:, 0:2] = np.floor(params[:, 0:2] * 16) / 16  # a 16 x 16 lattice
+    if seed == 7:
+        params[:, 0:2] = 0.25
+    if seed == 8:
+        params[:700, 0] = 0.0
+        params[300:700, 0] = -0.0
+        params[100:900, 1] = params[100, 1]
     gctx.set_params(params)
     gctx.partition_build(n_max)
     part = port.partition_build(params, n_max)

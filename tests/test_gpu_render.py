@@ -10,7 +10,7 @@ last-ulp decisions, so we also require >= 99.99 % exact pixels.
 import numpy as np
 import pytest
 
-from paper_2407_01866_b200 import OPT_CULL, IgsError, synth
+from paper_2407_01866_b200 import OPT_CULL, OPT_RASTER, IgsError, synth
 
 pytestmark = pytest.mark.gpu
 
@@ -29,11 +29,14 @@ def check_image(got, want):
     assert np.mean(got == want) >= 0.9999
 
 
-@pytest.fixture(params=[1, 0], ids=["cull", "brute"])
+@pytest.fixture(params=[(1, 0), (1, 1), (0, 0)], ids=["knn-patch", "tile-lists", "brute"])
 def mode(request, gctx):
-    gctx.set_option(OPT_CULL, request.param)
-    yield request.param
+    cull, raster = request.param
+    gctx.set_option(OPT_CULL, cull)
+    gctx.set_option(OPT_RASTER, raster)
+    yield cull
     gctx.set_option(OPT_CULL, 1)
+    gctx.set_option(OPT_RASTER, 0)
 
 
 def test_golden_render_topk(gctx, golden, mode):
@@ -173,3 +176,21 @@ def test_knn_hard_points_fallback(gctx, port):
             assert np.array_equal(idx[p, :cnt[p]], wi), (k, p)
         np.testing.assert_allclose(gctx.render_points(uv, k), port.render_topk(params, uv, k), rtol=1e-12,
                                    atol=1e-14)
+
+
+def test_patch_render_heterogeneous_set(gctx, port):
+    """The quadtree patch render on a trained-like set: scales from 0.2 px to
+    a quarter of the image, strong anisotropy, clusters -- top-K bit-exact
+    and pixels as the reference's, with image edges not multiples of the
+    8 x 4 patch."""
+    rng = np.random.default_rng(91)
+    n = 4000
+    params = synth.random_set(n, 92, 0.0005, 0.25)
+    params[:1500, 0:2] = 0.3 + 0.05 * rng.random((1500, 2))
+    params[:, 3] *= rng.uniform(0.05, 1.0, n)
+    gctx.set_params(params)
+    for (W, H, k) in ((61, 45, 10), (37, 70, 3), (50, 33, 32)):
+        want, wtk = port.render_image(params, W, H, k, want_topk=True)
+        got, gtk = gctx.render_image(W, H, k, want_topk=True)
+        assert np.array_equal(gtk, wtk), (W, H, k)
+        check_image(got, want)
