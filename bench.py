@@ -64,6 +64,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-render", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the C1/C3 secondary measurements")
     return ap.parse_args()
 
 
@@ -246,14 +247,6 @@ def run_ours(args, rank, world, local_rank, dist):
                      "unit": "GB/s", "frac": gbs / hbm, "traffic": ncu_traffic("segment_adam_kernel"),
                      "bytes_per_gaussian": 544}
 
-    # ---- culling statistics of the last state (target raster, K) -----------------------
-    cull_stats = None
-    if ctx.get_option(1):
-        off, mem, tau = ctx.tile_lists(W_IMG, H_IMG, K)
-        sizes = np.diff(off.astype(np.int64))
-        cull_stats = {"tiles": int(sizes.size), "mean_list": float(sizes.mean()), "max_list": int(sizes.max()),
-                      "tau_median": float(np.median(tau)), "pairs_vs_brute_force": float(sizes.mean() / N_GAUSS)}
-
     # ---- secondary: full render Mpix/s (the eval render of the same set) ------------
     render = None
     if not args.no_render:
@@ -266,9 +259,20 @@ def run_ours(args, rank, world, local_rank, dist):
             ctx.render_image(W_IMG, H_IMG, K, host=False)
             rms.append(ctx.timer_end())
         r_ms = max_over_ranks(min(rms))
+        ctx.profile_enable(True)
+        ctx.render_image(W_IMG, H_IMG, K, host=False)
+        ctx.sync()
+        r_pairs = ctx.profile_read(PROF_SCAN)[2]
+        ctx.profile_enable(False)
         render = {"metric": "global top-K render Mpix/s (render_image, 2048x2048, 100k G, K=10)",
                   "value": W_IMG * H_IMG / (r_ms * 1e-3) / 1e6, "unit": "Mpix/s", "ms": r_ms,
-                  "note": "every GPU renders the full image here; tile-row sharding splits rows (igs_render_image_rows)"}
+                  "pairs_per_pixel": r_pairs / (W_IMG * H_IMG),
+                  "state": f"the set after {args.warmup + 2 * args.steps} training steps",
+                  "note": "L2 flushed before each render; every GPU renders the full image here "
+                          "(tile-row sharding: igs_render_image_rows)"}
+        if world == 1 and not args.no_secondary:
+            render["c1"] = secondary_c1(ctx)
+            render["c3"] = secondary_c3(ctx)
 
     out = {
         "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
@@ -288,11 +292,66 @@ def run_ours(args, rank, world, local_rank, dist):
         "knn_hard_points_per_step": prof["knn_hard"][2] / args.steps,
         "pairs_per_sample": prof["scan"][2] / args.steps / NS,
         "dominant_family": dom,
-        "cull": cull_stats,
         "clocks": clk, "gpu_launches": int(launches),
         "render": render,
     }
     return out, ctx
+
+
+def _best_ms(ctx, f, reps=3):
+    best = 1e30
+    for _ in range(reps):
+        ctx.flush_l2(FLUSH_BYTES)
+        ctx.timer_begin()
+        f()
+        best = min(best, ctx.timer_end())
+    return best
+
+
+def secondary_c1(ctx):
+    """configs[0] (C1): 512x512, 10k Gaussians, K=10 -- one forward render and
+    one train step + Adam (the reference's CPU-runnable case)."""
+    from paper_2407_01866_b200 import synth
+    W = H = 512
+    ctx.set_params(synth.init_set(10_000, W, H, seed=5))
+    ctx.set_target(synth.photo_like_image(W, H, 777))
+    sidx = synth.sample_indices(NS, W, H, seed=8)[0]
+    ctx.render_image(W, H, K, host=False)
+    r_ms = _best_ms(ctx, lambda: ctx.render_image(W, H, K, host=False))
+    ctx.train_iteration(sidx, K, LR, 1)
+    t_ms = _best_ms(ctx, lambda: ctx.train_iteration(sidx, K, LR, 2))
+    return {"config": "C1: 512x512, 10k G, K=10", "render_ms": r_ms, "render_mpix_s": W * H / r_ms / 1e3,
+            "train_iteration_ms": t_ms}
+
+
+def secondary_c3(ctx):
+    """configs[2] (C3): 4096x4096 texture, 250k Gaussians (300 training
+    steps from the init state, for a heterogeneous set) -- BSP decode
+    (rebuild_partition from fp16 corners), blocked render, 1M random point
+    queries, and the global render."""
+    from paper_2407_01866_b200 import synth
+    W = H = 4096
+    ctx.set_params(synth.init_set(250_000, W, H, seed=17))
+    ctx.set_target(synth.texture_like_image(W, H, 5))
+    ctx.upload_samples(synth.sample_indices(NS, W, H, seed=3, steps=50))
+    ctx.train_iterations(300, K, LR, 1, want_losses=False)
+    ctx.partition_build(64)
+    build_ms = _best_ms(ctx, lambda: ctx.partition_build(64))
+    rects = ctx.partition_get()[0].astype(np.float16).astype(np.float64)
+    ctx.partition_rebuild(rects)
+    rebuild_ms = _best_ms(ctx, lambda: ctx.partition_rebuild(rects))
+    ctx.render_image_blocked(W, H, K, host=False)
+    blocked_ms = _best_ms(ctx, lambda: ctx.render_image_blocked(W, H, K, host=False))
+    uv = np.random.default_rng(1).random((1_000_000, 2))
+    ctx.render_points_blocked(uv, K)
+    pts_ms = _best_ms(ctx, lambda: ctx.render_points_blocked(uv, K))
+    ctx.render_image(W, H, K, host=False)
+    glob_ms = _best_ms(ctx, lambda: ctx.render_image(W, H, K, host=False))
+    return {"config": "C3: 4096x4096, 250k G, K=10, n_max=64 (4096 blocks)", "partition_build_ms": build_ms,
+            "rebuild_partition_ms": rebuild_ms, "blocked_render_ms": blocked_ms,
+            "blocked_render_mpix_s": W * H / blocked_ms / 1e3, "point_queries_1m_ms": pts_ms,
+            "global_render_ms": glob_ms, "global_render_mpix_s": W * H / glob_ms / 1e3,
+            "note": "point queries include the 16 MB host->device copy of (u, v) and the result copy back"}
 
 
 def ncu_traffic(kernel: str):

@@ -46,6 +46,17 @@ using namespace igs_dev;
 namespace {
 
 constexpr int kQueue = 512;  // per-warp frontier capacity
+constexpr int kSeedRMax = 8;  // widest seed window at the finest level: 17 x 17 cells
+
+// cell it (0 <= it < 8R) of the square ring at Chebyshev radius R
+__device__ __forceinline__ int ring_dx(int it, int R) {
+    const int side = it / (2 * R), t = it % (2 * R);
+    return side == 0 ? -R + t : (side == 1 ? R : (side == 2 ? R - t : -R));
+}
+__device__ __forceinline__ int ring_dy(int it, int R) {
+    const int side = it / (2 * R), t = it % (2 * R);
+    return side == 0 ? -R : (side == 1 ? -R + t : (side == 2 ? R : R - t));
+}
 // Builds between full re-bucketings (in between, the summaries are refit
 // from the Adam kernels' accumulation; exact either way, only the tightness
 // of the bounds drifts as Gaussians move and change scale).
@@ -650,6 +661,28 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
         }
     }
 
+    // (1b) fewer than kk candidates so far (sparse finest level): widen the
+    // window at the finest populated level ring by ring, so the descent
+    // starts with a finite threshold
+    int R = 1;
+    while (!(t.tq() < __longlong_as_double(0x7ff0000000000000LL)) && R < kSeedRMax) {
+        ++R;
+        const int lg = s_lg[lfine], G = 1 << lg, sx = cx0 >> lfine, sy = cy0 >> lfine;
+        for (int b = 0; b < 8 * R; b += 32) {
+            const int it = b + lane;
+            uint32_t o = 0, m = 0;
+            if (it < 8 * R) {
+                const int x = sx + ring_dx(it, R), y = sy + ring_dy(it, R);
+                if (x >= 0 && x < G && y >= 0 && y < G) {
+                    const uint32_t c = (uint32_t)(s_loff[lfine] + (y << lg) + x);
+                    o = off[c];
+                    m = own[c].count;
+                }
+            }
+            eval_members(t, o, m, lane, scan, mem, px, py, evaluated);
+        }
+    }
+
     bool overflow = false;
     // (2) descent: evaluate own members of frontier nodes, expand children
     // (G_l = G0 >> l is a power of two, so the child grid is exactly 2x)
@@ -670,7 +703,8 @@ __global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restri
             if (i < ncur) {
                 const uint32_t node = cur[i];
                 const int x = (int)node & wmask, y = (int)(node >> lg);
-                if (abs(x - sx) > 1 || abs(y - sy) > 1) {
+                const int Rl = l == lfine ? R : 1;  // the seed window at this level
+                if (abs(x - sx) > Rl || abs(y - sy) > Rl) {
                     const uint32_t c = lo + node;
                     const Sum so = own[c];
                     if (so.count && sum_lb(so, px, py) <= t.tq()) {
@@ -1173,6 +1207,26 @@ __global__ void __launch_bounds__(128) knn_raster_kernel(const ScanRec* __restri
             }
         }
 
+        // (1b) widen the finest-level window while some lane has < kk
+        int R = 1;
+        while (!(T < __longlong_as_double(0x7ff0000000000000LL)) && R < kSeedRMax) {
+            ++R;
+            const int lg = s_lg[lfine], G = 1 << lg, sx = cx0 >> lfine, sy = cy0 >> lfine;
+            for (int b = 0; b < 8 * R; b += 32) {
+                const int it = b + lane;
+                uint32_t o = 0, m = 0;
+                if (it < 8 * R) {
+                    const int x = sx + ring_dx(it, R), y = sy + ring_dy(it, R);
+                    if (x >= 0 && x < G && y >= 0 && y < G) {
+                        const uint32_t c = (uint32_t)(s_loff[lfine] + (y << lg) + x);
+                        o = off[c];
+                        m = own[c].count;
+                    }
+                }
+                T = raster_members(t, o, m, lane, scan, mem, stage[warp], stage_i[warp], px, py, T, evaluated);
+            }
+        }
+
         // (2) descent from the root with box bounds
         bool overflow = false;
         uint32_t* cur = queue[warp][0];
@@ -1191,7 +1245,8 @@ __global__ void __launch_bounds__(128) knn_raster_kernel(const ScanRec* __restri
                 if (i < ncur) {
                     const uint32_t node = cur[i];
                     const int x = (int)node & wmask, y = (int)(node >> lg);
-                    if (abs(x - sx) > 1 || abs(y - sy) > 1) {
+                    const int Rl = l == lfine ? R : 1;  // the seed window at this level
+                    if (abs(x - sx) > Rl || abs(y - sy) > Rl) {
                         const uint32_t c = lo + node;
                         const Sum so = own[c];
                         if (so.count && box_lb(so, bx0, by0, bx1, by1) <= T) {

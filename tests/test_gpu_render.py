@@ -194,3 +194,23 @@ def test_patch_render_heterogeneous_set(gctx, port):
         got, gtk = gctx.render_image(W, H, k, want_topk=True)
         assert np.array_equal(gtk, wtk), (W, H, k)
         check_image(got, want)
+
+
+def test_sparse_finest_level_widened_seeds(gctx, port):
+    """A sparse set of small Gaussians (fewer than K in the 3 x 3 seed window
+    at the finest level): the seed window widens ring by ring (knn.cu
+    kSeedRMax) before the descent; points and the patch render stay exact."""
+    rng = np.random.default_rng(5)
+    n = 3000
+    params = synth.random_set(n, 6, 0.0008, 0.0016)
+    gctx.set_params(params)
+    uv = rng.random((400, 2))
+    for k in (10, 24):
+        idx, w, cnt = gctx.select_top_k(uv, k)
+        for p in range(0, uv.shape[0], 9):
+            wi, ww = port.select_top_k(params, uv[p, 0], uv[p, 1], k)
+            assert np.array_equal(idx[p, :cnt[p]], wi), (k, p)
+        want, wtk = port.render_image(params, 96, 80, k, want_topk=True)
+        got, gtk = gctx.render_image(96, 80, k, want_topk=True)
+        assert np.array_equal(gtk, wtk)
+        check_image(got, want)
