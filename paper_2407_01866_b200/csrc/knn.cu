@@ -383,7 +383,48 @@ struct WarpTopK {
         tq_ = __shfl_sync(0xffffffffu, q, kk - 1);
         ti = __shfl_sync(0xffffffffu, i, kk - 1);
     }
+    static __device__ __forceinline__ bool lt(double aq, uint32_t ai, double bq, uint32_t bi) {
+        return aq < bq || (aq == bq && ai < bi);
+    }
+    // compare-exchange with lane ^ j; keep_min: this lane keeps the smaller
+    static __device__ __forceinline__ void cx(double& cq, uint32_t& ci, int j, bool keep_min) {
+        const double oq = __shfl_xor_sync(0xffffffffu, cq, j);
+        const uint32_t oi = __shfl_xor_sync(0xffffffffu, ci, j);
+        if (lt(oq, oi, cq, ci) == keep_min) {
+            cq = oq;
+            ci = oi;
+        }
+    }
+    // Many candidates at once (each lane one, (inf, kNoIdx) for none): a
+    // bitonic sort of the batch, then the first step of a bitonic merge with
+    // the kept list (elementwise min against the reversed batch leaves the
+    // 32 smallest of the union as a bitonic sequence) and five half-cleaner
+    // stages: lane j ends with the j-th smallest, the list's own layout.
+    __device__ __forceinline__ void merge(double cq, uint32_t ci) {
+#pragma unroll
+        for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1) cx(cq, ci, j, ((lane & j) == 0) == ((lane & k) == 0));
+        const double rq = __shfl_sync(0xffffffffu, cq, 31 - lane);
+        const uint32_t ri = __shfl_sync(0xffffffffu, ci, 31 - lane);
+        double lq = lane < kk ? q : __longlong_as_double(0x7ff0000000000000LL);
+        uint32_t li = lane < kk ? i : kNoIdx;
+        if (lt(rq, ri, lq, li)) {
+            lq = rq;
+            li = ri;
+        }
+#pragma unroll
+        for (int j = 16; j > 0; j >>= 1) cx(lq, li, j, (lane & j) == 0);
+        q = lq;
+        i = li;
+        refresh();
+    }
 };
+
+#ifndef IGS_MERGE_MIN
+#define IGS_MERGE_MIN 8
+#endif
+constexpr int kMergeMin = IGS_MERGE_MIN;  // candidates per batch from which merge() beats sequential inserts
 
 // Evaluates the members of up to 32 cells (lane i: range [o_i, o_i + m_i)),
 // flattened so that all lanes work on members.
@@ -422,7 +463,9 @@ __device__ __forceinline__ void eval_members(TK& t, uint32_t o_mine, uint32_t m_
             cand = t.beats(q, gi);
         }
         unsigned msk = __ballot_sync(0xffffffffu, cand);
-        if (msk) {
+        if (__popc(msk) >= kMergeMin) {
+            t.merge(cand ? q : __longlong_as_double(0x7ff0000000000000LL), cand ? gi : kNoIdx);
+        } else if (msk) {
             do {
                 const int src = __ffs(msk) - 1;
                 msk &= msk - 1;
