@@ -211,7 +211,7 @@ struct igs_ctx {
     int tgt_w = 0, tgt_h = 0;
 
     // per-call scratch (grow-only), indexed by purpose
-    DevBuf scratch[32];
+    DevBuf scratch[40];
     // pinned host staging
     void* pinned = nullptr;
     size_t pinned_bytes = 0;

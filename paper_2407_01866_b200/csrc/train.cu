@@ -266,39 +266,54 @@ __global__ void segment_sum_kernel(const uint32_t* __restrict__ gcnt, const uint
 }
 
 // One CTA per long segment (persistent over the queue).  The slot ids are
-// bitonic-sorted in shared memory (padded to a power of two); then chunks of
-// 256 contribution rows are gathered in parallel into shared memory and 8
-// threads -- one per parameter -- accumulate them in slot (= sample) order.
-// Segments beyond the shared capacity (degenerate sets) sort in place in
+// put in slot (= sample) order in shared memory: up to 256 by counting ranks
+// (rank = number of smaller ids; ids are distinct -- two barriers), larger
+// by a bitonic sort; then 8 threads, one per parameter, accumulate the
+// contribution rows in that order with the row loads issued ahead of the
+// dependent adds.  Segments beyond the shared capacity rank straight from
 // global memory.
-constexpr uint32_t kLongCap = 4096;
+constexpr uint32_t kLongCap = 2048;
+constexpr uint32_t kLongRank = 256;  // up to here: rank by counting; above: bitonic sort
+constexpr int kLongThreads = 256;
 
-__global__ void __launch_bounds__(256) long_segment_kernel(const uint32_t* __restrict__ gcnt,
-                                                           const uint32_t* __restrict__ goff,
-                                                           uint32_t* __restrict__ perm,
-                                                           const double* __restrict__ contrib,
-                                                           double* __restrict__ grads,
-                                                           const uint32_t* __restrict__ long_count,
-                                                           const uint32_t* __restrict__ long_list,
-                                                           long long* __restrict__ status) {
+__global__ void __launch_bounds__(kLongThreads) long_segment_kernel(const uint32_t* __restrict__ gcnt,
+                                                                    const uint32_t* __restrict__ goff,
+                                                                    uint32_t* __restrict__ perm,
+                                                                    const double* __restrict__ contrib,
+                                                                    double* __restrict__ grads,
+                                                                    const uint32_t* __restrict__ long_count,
+                                                                    const uint32_t* __restrict__ long_list,
+                                                                    long long* __restrict__ status,
+                                                                    uint32_t* __restrict__ big) {
     pdl_wait();
     __shared__ uint32_t keys[kLongCap];
-    __shared__ double rows[256][8];
+    __shared__ uint32_t sorted[kLongCap];
+    __shared__ double rows[kLongThreads][8];
     const uint32_t total = *long_count;
     const int t = threadIdx.x;
     for (uint32_t it = blockIdx.x; it < total; it += gridDim.x) {
         const uint32_t g = long_list[it];
         const uint32_t m = gcnt[g], o = goff[g];
-        const uint32_t* sorted = keys;
+        const uint32_t* out = sorted;
         __syncthreads();
-        if (m <= kLongCap) {
+        if (m <= kLongRank) {
+            for (uint32_t e = t; e < m; e += kLongThreads) keys[e] = perm[o + e];
+            __syncthreads();
+            for (uint32_t e = t; e < m; e += kLongThreads) {
+                const uint32_t v = keys[e];
+                uint32_t r = 0;
+                for (uint32_t j = 0; j < m; ++j) r += keys[j] < v;
+                sorted[r] = v;
+            }
+        } else if (m <= kLongCap) {
+            // bitonic sort in shared memory, padded to a power of two
             uint32_t pow2 = 1;
             while (pow2 < m) pow2 <<= 1;
-            for (uint32_t e = t; e < pow2; e += 256) keys[e] = e < m ? perm[o + e] : 0xFFFFFFFFu;
+            for (uint32_t e = t; e < pow2; e += kLongThreads) keys[e] = e < m ? perm[o + e] : 0xFFFFFFFFu;
             __syncthreads();
             for (uint32_t size = 2; size <= pow2; size <<= 1)
                 for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-                    for (uint32_t e = t; e < pow2; e += 256) {
+                    for (uint32_t e = t; e < pow2; e += kLongThreads) {
                         const uint32_t partner = e ^ stride;
                         if (partner > e) {
                             const bool up = (e & size) == 0;
@@ -311,28 +326,26 @@ __global__ void __launch_bounds__(256) long_segment_kernel(const uint32_t* __res
                     }
                     __syncthreads();
                 }
+            out = keys;
         } else {
-            if (t == 0) {
-                uint32_t* sl = perm + o;
-                for (uint32_t e = 1; e < m; ++e) {
-                    const uint32_t v = sl[e];
-                    uint32_t pos = e;
-                    while (pos > 0 && sl[pos - 1] > v) {
-                        sl[pos] = sl[pos - 1];
-                        --pos;
-                    }
-                    sl[pos] = v;
-                }
+            // beyond shared memory (degenerate sets): rank from global
+            // memory into the same range of a second slot array
+            for (uint32_t e = t; e < m; e += kLongThreads) {
+                const uint32_t v = perm[o + e];
+                uint32_t r = 0;
+                for (uint32_t j = 0; j < m; ++j) r += perm[o + j] < v;
+                big[o + r] = v;
             }
-            __threadfence_block();
-            __syncthreads();
-            sorted = perm + o;
+            out = big + o;
         }
-        double acc = 0.0;  // thread p < 8 owns parameter p
-        for (uint32_t base = 0; base < m; base += 256) {
-            const uint32_t cnt = min(256u, m - base);
+        __syncthreads();
+        // chunks of rows gathered by all threads (loads in flight together),
+        // then summed in order by thread p < 8 (parameter p)
+        double acc = 0.0;
+        for (uint32_t base = 0; base < m; base += kLongThreads) {
+            const uint32_t cnt = min((uint32_t)kLongThreads, m - base);
             if ((uint32_t)t < cnt) {
-                const double2* c = reinterpret_cast<const double2*>(contrib + (size_t)sorted[base + t] * 8);
+                const double2* c = reinterpret_cast<const double2*>(contrib + (size_t)out[base + t] * 8);
 #pragma unroll
                 for (int h = 0; h < 4; ++h) {
                     const double2 v = c[h];
@@ -800,9 +813,11 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
         IGS_PDL(ctx, scatter_slots_kernel, (unsigned)((items + 255) / 256), 256, 0, (const uint32_t*)keys,
                 (uint32_t)items, n, (const uint32_t*)goff, (const uint32_t*)gcnt, gcnt + n, perm, long_ctl,
                 long_ctl + 1);
-        IGS_PDL(ctx, long_segment_kernel, ctx->sm_count, 256, 0, (const uint32_t*)gcnt, (const uint32_t*)goff, perm,
-                (const double*)contrib, ctx->grads, (const uint32_t*)long_ctl, (const uint32_t*)(long_ctl + 1),
-                ctx->status);
+        uint32_t* big = (uint32_t*)igs_scratch(ctx, 32, items * sizeof(uint32_t));
+        if (!big) return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
+        IGS_PDL(ctx, long_segment_kernel, 8 * ctx->sm_count, kLongThreads, 0, (const uint32_t*)gcnt,
+                (const uint32_t*)goff, perm, (const double*)contrib, ctx->grads, (const uint32_t*)long_ctl,
+                (const uint32_t*)(long_ctl + 1), ctx->status, big);
         if (fuse_lr4 && ctx->nranks == 1 && !ctx->comm) {
             // short segments summed inside the Adam kernel (one pass over the set)
             const double bc1 = 1.0 - std::pow(0.9, (double)t);  // adam.cpp:16-17, host libm

@@ -243,3 +243,21 @@ def test_async_pipelined_iterations_match_sync(gctx, port):
         gctx.train_wait()
     assert got == want
     assert np.array_equal(gctx.get_params(), p_sync)
+
+
+@pytest.mark.parametrize("n,ns", [(5, 5000), (40, 9000), (300, 9000)])
+def test_long_segments_reference_order(gctx, port, n, ns):
+    """Gaussians with hundreds to thousands of contributions: the long-segment
+    reduction (rank by counting, bitonic, and the beyond-shared-memory path)
+    still sums every Gaussian's contributions in sample order, so the
+    gradients agree with the reference's to 1e-12."""
+    target = synth.photo_like_image(64, 48, 31013)
+    params = port.initialize_set(target, n, 0.3, 41)
+    params[:, 3:5] = 0.3  # large: every sample sees most Gaussians
+    sidx = synth.sample_indices(ns, 64, 48, seed=43)[0]
+    gctx.set_params(params)
+    gctx.set_target(target)
+    loss, grads = gctx.train_step(sidx, 10)
+    wl, wg = port.train_step(params, target, sidx, 10)
+    assert abs(loss - wl) <= 1e-12 * abs(wl)
+    grad_close(grads, wg, 1e-12)
