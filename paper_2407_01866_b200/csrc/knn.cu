@@ -66,7 +66,7 @@ constexpr int kRefitPeriod = 16;
 #endif
 constexpr int kGrowShift = IGS_GROW_SHIFT;  // re-bucket when more than n >> kGrowShift Gaussians grew
 
-struct Sum {
+struct __align__(16) Sum {
     double x0, y0, x1, y1;  // centre bbox (empty: +inf/-inf)
     double lmin;            // smallest Sigma^-1 eigenvalue
     float slack;            // bound safety factor (0 = never prune)
