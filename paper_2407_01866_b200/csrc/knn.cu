@@ -618,7 +618,7 @@ __device__ __forceinline__ void warp_epilogue(const Epi& E, const ScanRec* __res
     }
 }
 
-__global__ void __launch_bounds__(128) knn_points_kernel(const ScanRec* __restrict__ scan, uint32_t n, Lq L,
+__global__ void __launch_bounds__(128, 9) knn_points_kernel(const ScanRec* __restrict__ scan, uint32_t n, Lq L,
                                                             const Sum* __restrict__ own, const Sum* __restrict__ sub,
                                                             const uint32_t* __restrict__ off,
                                                             const uint32_t* __restrict__ mem,
