@@ -552,10 +552,7 @@ __global__ void adam_kernel(double* __restrict__ params, const double* __restric
 // finite Gaussian is still updated, deterministically; the reference has
 // updated Gaussians 0..i-1 when it throws, adam.cpp:29-31).  A non-finite
 // loss (flagged by the search epilogue) skips the whole step, as fit.cpp:155.
-#ifndef IGS_ADAM_MINB
-#define IGS_ADAM_MINB 3
-#endif
-__global__ void __launch_bounds__(256, IGS_ADAM_MINB) segment_adam_kernel(uint32_t* __restrict__ gcnt, const uint32_t* __restrict__ goff,
+__global__ void __launch_bounds__(128, 6) segment_adam_kernel(uint32_t* __restrict__ gcnt, const uint32_t* __restrict__ goff,
                                     const uint32_t* __restrict__ perm, const double* __restrict__ contrib,
                                     uint32_t n, double* __restrict__ grads, double* __restrict__ params,
                                     double* __restrict__ m, double* __restrict__ v, ScanRec* __restrict__ scan,
@@ -565,6 +562,7 @@ __global__ void __launch_bounds__(256, IGS_ADAM_MINB) segment_adam_kernel(uint32
     pdl_wait();
     const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
+    if (ta.acc) asm volatile("prefetch.global.L1 [%0];" ::"l"(ta.key + g));  // read at the very end
     const uint32_t cntg = gcnt[g], og = goff[g];
     // last reader of the counters/cursors: leave them zeroed for the next step
     gcnt[g] = 0;
@@ -826,7 +824,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
             ctx->params_version++;
             igs_prof_end(ctx, IGS_PROF_REDUCE, (double)items);
             igs_prof_begin(ctx, IGS_PROF_ADAM);
-            IGS_PDL(ctx, segment_adam_kernel, (n + 255) / 256, 256, 0, gcnt, (const uint32_t*)goff,
+            IGS_PDL(ctx, segment_adam_kernel, (n + 127) / 128, 128, 0, gcnt, (const uint32_t*)goff,
                     (const uint32_t*)perm, (const double*)contrib, n, ctx->grads, ctx->params, ctx->adam_m,
                     ctx->adam_v, ctx->scan, ctx->shade, fuse_lr4[0], fuse_lr4[1], fuse_lr4[2], fuse_lr4[3], bc1, bc2,
                     1.0 / bc1, 1.0 / bc2, ctx->status, ta);
