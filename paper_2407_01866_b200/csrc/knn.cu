@@ -826,11 +826,39 @@ __global__ void __launch_bounds__(128, 9) knn_points_kernel(const ScanRec* __res
 // Hard points (frontier overflow) are resolved by an exact split scan:
 // hard_scan_kernel -- a persistent grid walks (point, split) items; each CTA
 // scans a contiguous 1/kHardSplit of the set with per-thread top-K lists and
-// folds them (warp 0) into one partial list; hard_merge_kernel -- one warp
-// per point offers the kHardSplit partial lists to a warp top-K (any order:
-// (q, idx) is a strict total order) and runs the epilogue.
+// folds them (warp 0) into one partial list; the CTA completing a point's
+// last split then offers the kHardSplit partial lists to a warp top-K (any
+// order: (q, idx) is a strict total order) and runs the epilogue.
 constexpr int kHardThreads = 128;
 constexpr int kHardSplit = 32;
+
+// The point of hard slot `slot`: merge its kHardSplit partial lists (any
+// order: (q, idx) is a strict total order) and run the epilogue -- one warp.
+__device__ __forceinline__ void hard_merge_point(const ScanRec* __restrict__ scan, uint32_t n,
+                                                 const double* __restrict__ uv, int W, int H, int kk,
+                                                 const uint32_t* __restrict__ hard_list, const Epi& E,
+                                                 const double* __restrict__ part_q,
+                                                 const uint32_t* __restrict__ part_i, uint32_t slot, int lane,
+                                                 unsigned long long* __restrict__ pairs) {
+    const uint32_t pt = hard_list[slot];
+    double px, py;
+    point_of(uv, E, W, H, pt, px, py);
+    WarpTopK t;
+    t.init(kk, lane);
+    for (int sp = 0; sp < kHardSplit; ++sp) {
+        const size_t o = ((size_t)slot * kHardSplit + sp) * kk;
+        const double q = lane < kk ? part_q[o + lane] : 0.0;
+        const uint32_t i = lane < kk ? part_i[o + lane] : kNoIdx;
+        for (int j = 0; j < kk; ++j) {
+            const uint32_t ij = __shfl_sync(0xffffffffu, i, j);
+            const double qj = __shfl_sync(0xffffffffu, q, j);
+            if (ij == kNoIdx) break;
+            t.offer(qj, ij);
+        }
+    }
+    if (pairs && lane == 0) atomicAdd(pairs, (unsigned long long)n);
+    warp_epilogue(E, scan, pt, kk, lane, t.q, t.i, px, py);
+}
 
 template <int KCAP>
 __global__ void __launch_bounds__(kHardThreads) hard_scan_kernel(const ScanRec* __restrict__ scan, uint32_t n,
@@ -838,7 +866,9 @@ __global__ void __launch_bounds__(kHardThreads) hard_scan_kernel(const ScanRec* 
                                                                  const uint32_t* __restrict__ hard_count,
                                                                  const uint32_t* __restrict__ hard_list, Epi E,
                                                                  double* __restrict__ part_q,
-                                                                 uint32_t* __restrict__ part_i) {
+                                                                 uint32_t* __restrict__ part_i,
+                                                                 unsigned int* __restrict__ point_done,
+                                                                 unsigned long long* __restrict__ pairs) {
     __shared__ double sq[kHardThreads * KCAP];
     __shared__ uint32_t si[kHardThreads * KCAP];
     pdl_wait();
@@ -907,40 +937,23 @@ __global__ void __launch_bounds__(kHardThreads) hard_scan_kernel(const ScanRec* 
                     part_i[(size_t)item * kk + r] = vi;
                 }
             }
+            // the CTA finishing a point's last split merges it (the partial
+            // writes are made visible before the count that publishes them)
+            unsigned last = 0;
+            if (lane == 0) {
+                __threadfence();
+                last = atomicAdd(point_done + slot, 1u) == (unsigned)(kHardSplit - 1);
+            }
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (last) {
+                __threadfence();
+                hard_merge_point(scan, n, uv, W, H, kk, hard_list, E, part_q, part_i, slot, lane, pairs);
+                if (lane == 0) point_done[slot] = 0;  // ready for the next search
+            }
         }
     }
 }
 
-__global__ void __launch_bounds__(128) hard_merge_kernel(const ScanRec* __restrict__ scan, uint32_t n,
-                                                         const double* __restrict__ uv, int W, int H, int kk,
-                                                         const uint32_t* __restrict__ hard_count,
-                                                         const uint32_t* __restrict__ hard_list, Epi E,
-                                                         const double* __restrict__ part_q,
-                                                         const uint32_t* __restrict__ part_i,
-                                                         unsigned long long* __restrict__ pairs) {
-    const uint32_t slot = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    pdl_wait();
-    if (slot >= min(*hard_count, kHardCap)) return;
-    const uint32_t pt = hard_list[slot];
-    double px, py;
-    point_of(uv, E, W, H, pt, px, py);
-    WarpTopK t;
-    t.init(kk, lane);
-    for (int sp = 0; sp < kHardSplit; ++sp) {
-        const size_t o = ((size_t)slot * kHardSplit + sp) * kk;
-        const double q = lane < kk ? part_q[o + lane] : 0.0;
-        const uint32_t i = lane < kk ? part_i[o + lane] : kNoIdx;
-        for (int j = 0; j < kk; ++j) {
-            const uint32_t ij = __shfl_sync(0xffffffffu, i, j);
-            const double qj = __shfl_sync(0xffffffffu, q, j);
-            if (ij == kNoIdx) break;
-            t.offer(qj, ij);
-        }
-    }
-    if (pairs && lane == 0) atomicAdd(pairs, (unsigned long long)n);
-    warp_epilogue(E, scan, pt, kk, lane, t.q, t.i, px, py);
-}
 
 struct KnnBufs {
     DevBuf cnt, off, key, mem, own, sub, cub_tmp, hard, ticket, part, lcount, acc;
@@ -1058,8 +1071,9 @@ template <int KCAP>
 int launch_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int kk, const Epi& E) {
     KnnBufs& b = *static_cast<KnnBufs*>(ctx->knn);
     if (!b.hard.p) {
-        if (!grow(b.hard, (kHardCap + 4) * 4)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
-        IGS_CUDA(ctx, cudaMemsetAsync(b.hard.p, 0, 16, ctx->stream));
+        // [0..3] counter pairs, [4..] hard list, [4 + kHardCap..] per-slot split counts
+        if (!grow(b.hard, (2 * kHardCap + 4) * 4)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
+        IGS_CUDA(ctx, cudaMemsetAsync(b.hard.p, 0, (2 * kHardCap + 4) * 4, ctx->stream));
     }
     // [0,1] and [2,3]: two (hard-point count, point cursor) pairs used by
     // alternate searches -- each search zeroes the other pair; [4..] list
@@ -1084,10 +1098,8 @@ int launch_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int 
     double* part_q = (double*)b.part.p;
     uint32_t* part_i = (uint32_t*)(part_q + pitems);
     IGS_PDL(ctx, hard_scan_kernel<KCAP>, 2 * ctx->sm_count, kHardThreads, 0, (const ScanRec*)ctx->scan, ctx->n, uv,
-            W, H, kk, (const uint32_t*)hard_count, (const uint32_t*)hard_list, E, part_q, part_i);
-    IGS_PDL(ctx, hard_merge_kernel, kHardCap * 32 / 128, 128, 0, (const ScanRec*)ctx->scan, ctx->n, uv, W, H, kk,
-            (const uint32_t*)hard_count, (const uint32_t*)hard_list, E, (const double*)part_q,
-            (const uint32_t*)part_i, igs_prof_counter(ctx, IGS_PROF_SCAN));
+            W, H, kk, (const uint32_t*)hard_count, (const uint32_t*)hard_list, E, part_q, part_i,
+            (unsigned int*)((uint32_t*)b.hard.p + 4 + kHardCap), igs_prof_counter(ctx, IGS_PROF_SCAN));
     igs_prof_end(ctx, IGS_PROF_SCAN, 0.0);
     return IGS_OK;
 }
