@@ -728,13 +728,54 @@ __global__ void __launch_bounds__(128, 9) knn_points_kernel(const ScanRec* __res
 
     bool overflow = false;
     // (2) descent: evaluate own members of frontier nodes, expand children
-    // (G_l = G0 >> l is a power of two, so the child grid is exactly 2x)
+    // (G_l = G0 >> l is a power of two, so the child grid is exactly 2x).
+    // Flat start: the levels above ls (at most 4 x 4 cells, 21 in all) are
+    // checked cell by cell -- own members whose own bound survives -- and
+    // the frontier at ls (8 x 8) is every cell whose subtree bound does;
+    // the same sets a descent from the root reaches (a subtree bound never
+    // exceeds an ancestor's), without its chain of dependent loads.
     uint32_t* cur = queue[warp][0];
     uint32_t* nxt = queue[warp][1];
-    int ncur = 1;
-    if (lane == 0) cur[0] = 0;  // root cell of the top level
-    __syncwarp();
-    for (int l = L.levels - 1; l >= 0 && ncur > 0; --l) {
+    const int ls = min(L.levels - 1, max(lg0 - 3, 0));
+    {
+        const uint32_t c0 = ls + 1 < L.levels ? (uint32_t)s_loff[ls + 1] : 0u;
+        const uint32_t nup = ls + 1 < L.levels ? (uint32_t)(s_loff[L.levels - 1] + 1) - c0 : 0u;
+        for (uint32_t b = 0; b < nup; b += 32) {
+            const uint32_t c = c0 + b + lane;
+            uint32_t o = 0, m = 0;
+            if (b + lane < nup) {
+                int l = ls + 1;
+                while (l + 1 < L.levels && (uint32_t)s_loff[l + 1] <= c) ++l;
+                const int lg = s_lg[l];
+                const int node = (int)(c - (uint32_t)s_loff[l]);
+                const int x = node & ((1 << lg) - 1), y = node >> lg;
+                const int Rl = l == lfine ? R : 1;  // the seed window at this level
+                if (abs(x - (cx0 >> l)) > Rl || abs(y - (cy0 >> l)) > Rl) {
+                    const Sum so = own[c];
+                    if (so.count && sum_lb(so, px, py) <= t.tq()) {
+                        o = off[c];
+                        m = so.count;
+                    }
+                }
+            }
+            eval_members(t, o, m, lane, scan, mem, px, py, evaluated);
+        }
+    }
+    int ncur = 0;
+    {
+        const int nls = 1 << (2 * s_lg[ls]);
+        const uint32_t lo = (uint32_t)s_loff[ls];
+        for (int b = 0; b < nls; b += 32) {
+            const int node = b + lane;
+            const bool keep = node < nls && sum_lb(sub[lo + node], px, py) <= t.tq();
+            const unsigned msk = __ballot_sync(0xffffffffu, keep);
+            const int pos = ncur + __popc(msk & ((1u << lane) - 1));
+            if (keep) cur[pos] = (uint32_t)node;  // (at most 64 <= kQueue)
+            ncur += __popc(msk);
+        }
+        __syncwarp();
+    }
+    for (int l = ls; l >= 0 && ncur > 0; --l) {
         const int lg = s_lg[l];
         const int wmask = (1 << lg) - 1;
         const int sx = cx0 >> l, sy = cy0 >> l;  // seed window centre
