@@ -24,6 +24,7 @@
 #include <limits>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "igs_b200.h"
@@ -56,13 +57,31 @@ double kahan_sum(const std::vector<double>& v) {
     return sum;
 }
 
-// sampling.cpp:44-67
+// Runs f(begin, end) over [0, n) on the host's cores (per-element work with
+// no cross-element arithmetic, so the split does not change any result).
+template <class F>
+void parallel_for(size_t n, F f) {
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const size_t parts = std::min<size_t>(hw, std::max<size_t>(1, n / 65536));
+    if (parts <= 1) {
+        f((size_t)0, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    const size_t step = (n + parts - 1) / parts;
+    for (size_t p = 1; p < parts; ++p) th.emplace_back(f, p * step, std::min(n, (p + 1) * step));
+    f((size_t)0, std::min(n, step));
+    for (auto& t : th) t.join();
+}
+
+// sampling.cpp:44-67 (rows in parallel)
 std::vector<double> gradient_magnitude(const float* img, int W, int H) {
     std::vector<double> mag((size_t)W * H);
     auto cl = [](int v, int hi) { return v < 0 ? 0 : (v > hi ? hi : v); };
     auto at = [&](int h, int w, int c) { return (double)img[((size_t)h * W + w) * 3 + c]; };
-    for (int h = 0; h < H; ++h)
-        for (int w = 0; w < W; ++w) {
+    parallel_for((size_t)H * W, [&](size_t b, size_t e) {
+    for (size_t f = b; f < e; ++f) {
+            const int h = (int)(f / W), w = (int)(f % W);
             const int hm = cl(h - 1, H - 1), hp = cl(h + 1, H - 1), wm = cl(w - 1, W - 1), wp = cl(w + 1, W - 1);
             double acc = 0.0;
             for (int c = 0; c < 3; ++c) {
@@ -74,18 +93,21 @@ std::vector<double> gradient_magnitude(const float* img, int W, int H) {
                 acc += gx * gx + gy * gy;
             }
             mag[(size_t)h * W + w] = std::sqrt(acc);
-        }
+    }
+    });
     return mag;
 }
 
 // sampling.cpp:25-40 gradient_mixture (init_distribution / opt_distribution)
-std::vector<double> gradient_mixture(const float* img, int W, int H, double lambda) {
-    std::vector<double> p = gradient_magnitude(img, W, H);
-    const double total = kahan_sum(p);
+// from a precomputed gradient magnitude and its Kahan total: the init and
+// optimisation distributions share both (only lambda differs), so the
+// Sobel pass and the sum run once.
+std::vector<double> gradient_mixture(const std::vector<double>& mag, double total, double lambda) {
+    std::vector<double> p(mag.size());
     const double uniform = 1.0 / (double)p.size();
     if (total > 0.0) {
         const double scale = (1.0 - lambda) / total;
-        for (double& v : p) v = v * scale + lambda * uniform;
+        for (size_t i = 0; i < p.size(); ++i) p[i] = mag[i] * scale + lambda * uniform;
     } else {
         std::fill(p.begin(), p.end(), uniform);
     }
@@ -103,28 +125,50 @@ struct Alias {
         if (n == 0) return;
         const double total = kahan_sum(w);
         if (!(total > 0.0)) return;
+        for (size_t i = 0; i < n; ++i)
+            if (w[i] < 0.0) return;
         prob.assign(n, 0.0);
         alias.assign(n, 0);
         std::vector<double> scaled(n);
+        parallel_for(n, [&](size_t b, size_t e) {
+            for (size_t i = b; i < e; ++i) scaled[i] = w[i] * n / total;
+        });
+        // small / large stacks in index order (branch-free partition)
+        std::vector<uint32_t> small(n), large(n);
+        size_t ns = 0, nl = 0;
         for (size_t i = 0; i < n; ++i) {
-            if (w[i] < 0.0) return;
-            scaled[i] = w[i] * n / total;
+            const bool sm = scaled[i] < 1.0;
+            small[ns] = (uint32_t)i;
+            large[nl] = (uint32_t)i;
+            ns += sm;
+            nl += !sm;
         }
-        std::vector<uint32_t> small, large;
-        small.reserve(n);
-        large.reserve(n);
-        for (size_t i = 0; i < n; ++i) (scaled[i] < 1.0 ? small : large).push_back((uint32_t)i);
-        while (!small.empty() && !large.empty()) {
-            const uint32_t s = small.back(), l = large.back();
-            small.pop_back();
-            large.pop_back();
-            prob[s] = scaled[s];
-            alias[s] = l;
-            scaled[l] = (scaled[l] + scaled[s]) - 1.0;
-            (scaled[l] < 1.0 ? small : large).push_back(l);
+        // Vose's loop, the reference's stack order: pop s and l; l takes
+        // s's deficit and goes back on top of the small or large stack.
+        // The large item stays in a register while it remains large (it
+        // would be popped again at once).
+        while (ns > 0 && nl > 0) {
+            uint32_t l = large[--nl];
+            double sl = scaled[l];
+            for (;;) {
+                const uint32_t s = small[--ns];
+                prob[s] = scaled[s];
+                alias[s] = l;
+                sl = (sl + scaled[s]) - 1.0;
+                if (sl < 1.0) {
+                    scaled[l] = sl;
+                    small[ns++] = l;  // l is the next s
+                    break;
+                }
+                if (ns == 0) {  // l stays large, the loop ends
+                    scaled[l] = sl;
+                    large[nl++] = l;
+                    break;
+                }
+            }
         }
-        for (uint32_t i : large) prob[i] = 1.0;
-        for (uint32_t i : small) prob[i] = 1.0;
+        for (size_t j = 0; j < nl; ++j) prob[large[j]] = 1.0;
+        for (size_t j = 0; j < ns; ++j) prob[small[j]] = 1.0;
         ok = true;
     }
     uint32_t sample(Rng& r) const {
@@ -214,14 +258,16 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
     // initialize_set(target, budget/2, lambda_init, rng) (sampling.cpp:154-174)
     const int init_count = c.budget / 2;
     std::vector<double> set;
+    const std::vector<double> mag = gradient_magnitude(target, W, H);
+    const double mag_total = kahan_sum(mag);
     {
-        const Alias init(gradient_mixture(target, W, H, c.lambda_init));
+        const Alias init(gradient_mixture(mag, mag_total, c.lambda_init));
         if (!init.ok) return bad("alias table weights must have positive sum");
         const double s0 = 2.0 / std::max(W, H);
         set.reserve((size_t)init_count * 8);
         for (int i = 0; i < init_count; ++i) add_gaussian(set, target, W, H, init.sample(rng), s0);
     }
-    const Alias opt(gradient_mixture(target, W, H, c.lambda_opt));
+    const Alias opt(gradient_mixture(mag, mag_total, c.lambda_opt));
     if (!opt.ok) return bad("alias table weights must have positive sum");
     if ((e = igs_set_target(ctx, target, W, H))) return e;
     if ((e = igs_set_params(ctx, set.data(), (uint32_t)init_count))) return e;
