@@ -275,7 +275,8 @@ def run_ours(args, rank, world, local_rank, dist):
                           "(tile-row sharding: igs_render_image_rows)"}
     secondary = None
     if world == 1 and not args.no_secondary:
-        secondary = {"c1": secondary_c1(ctx), "c3": secondary_c3(ctx), "fit_c2": secondary_fit(ctx)}
+        secondary = {"c1": secondary_c1(ctx), "c3": secondary_c3(ctx), "c4": secondary_c4(ctx),
+                     "c5": secondary_c5(ctx), "fit_c2": secondary_fit(ctx)}
 
     out = {
         "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
@@ -312,32 +313,34 @@ def _best_ms(ctx, f, reps=3):
 
 
 def secondary_c1(ctx):
-    """configs[0] (C1): 512x512, 10k Gaussians, K=10 -- one forward render and
-    one train step + Adam (the reference's CPU-runnable case)."""
+    """configs[0] (C1): random-local N = 10k at 512x512, K = 10 --
+    one global render, one train step (NS = 10k) + Adam (t = 1)."""
     from paper_2407_01866_b200 import synth
     W = H = 512
-    ctx.set_params(synth.init_set(10_000, W, H, seed=5))
-    ctx.set_target(synth.photo_like_image(W, H, 777))
-    sidx = synth.sample_indices(NS, W, H, seed=8)[0]
+    params = synth.random_local_set(10_000, W, H, seed=7)
+    ctx.set_params(params)
+    ctx.set_target(synth.photo_like_image(W, H, 31002))
+    sidx = synth.sample_indices(NS, W, H, seed=99)[0]
     ctx.render_image(W, H, K, host=False)
     r_ms = _best_ms(ctx, lambda: ctx.render_image(W, H, K, host=False))
-    ctx.train_iteration(sidx, K, LR, 1)
-    t_ms = _best_ms(ctx, lambda: ctx.train_iteration(sidx, K, LR, 2))
-    return {"config": "C1: 512x512, 10k G, K=10", "render_ms": r_ms, "render_mpix_s": W * H / r_ms / 1e3,
-            "train_iteration_ms": t_ms}
+
+    def step():
+        ctx.set_params(params)
+        ctx.train_iteration(sidx, K, LR, 1)
+    step()
+    t_ms = _best_ms(ctx, step)
+    return {"config": "C1: random-local 10k G at 512x512, K=10", "render_ms": r_ms,
+            "render_mpix_s": W * H / r_ms / 1e3, "train_step_plus_adam_ms": t_ms,
+            "note": "the train step time includes re-uploading the set (set_params) so every repetition is t = 1"}
 
 
 def secondary_c3(ctx):
-    """configs[2] (C3): 4096x4096 texture, 250k Gaussians (300 training
-    steps from the init state, for a heterogeneous set) -- BSP decode
-    (rebuild_partition from fp16 corners), blocked render, 1M random point
-    queries, and the global render."""
+    """configs[2] (C3): random-local N = 250k at 4096x4096 -- build_partition(64),
+    decode (rebuild_partition from the fp16-quantized corners the IGS2 codec
+    stores), blocked render, random point queries; and the global render."""
     from paper_2407_01866_b200 import synth
     W = H = 4096
-    ctx.set_params(synth.init_set(250_000, W, H, seed=17))
-    ctx.set_target(synth.texture_like_image(W, H, 5))
-    ctx.upload_samples(synth.sample_indices(NS, W, H, seed=3, steps=50))
-    ctx.train_iterations(300, K, LR, 1, want_losses=False)
+    ctx.set_params(synth.random_local_set(250_000, W, H, seed=7))
     ctx.partition_build(64)
     build_ms = _best_ms(ctx, lambda: ctx.partition_build(64))
     rects = ctx.partition_get()[0].astype(np.float16).astype(np.float64)
@@ -345,35 +348,85 @@ def secondary_c3(ctx):
     rebuild_ms = _best_ms(ctx, lambda: ctx.partition_rebuild(rects))
     ctx.render_image_blocked(W, H, K, host=False)
     blocked_ms = _best_ms(ctx, lambda: ctx.render_image_blocked(W, H, K, host=False))
-    uv = np.random.default_rng(1).random((1_000_000, 2))
-    ctx.render_points_blocked(uv, K)
-    pts_ms = _best_ms(ctx, lambda: ctx.render_points_blocked(uv, K))
+    rng = np.random.default_rng(1)
+    uv10k, uv1m = rng.random((10_000, 2)), rng.random((1_000_000, 2))
+    ctx.render_points_blocked(uv10k, K)
+    pts10k_ms = _best_ms(ctx, lambda: ctx.render_points_blocked(uv10k, K))
+    pts1m_ms = _best_ms(ctx, lambda: ctx.render_points_blocked(uv1m, K))
     ctx.render_image(W, H, K, host=False)
     glob_ms = _best_ms(ctx, lambda: ctx.render_image(W, H, K, host=False))
-    return {"config": "C3: 4096x4096, 250k G, K=10, n_max=64 (4096 blocks)", "partition_build_ms": build_ms,
+    return {"config": "C3: random-local 250k G at 4096x4096, K=10, n_max=64", "partition_build_ms": build_ms,
             "rebuild_partition_ms": rebuild_ms, "blocked_render_ms": blocked_ms,
-            "blocked_render_mpix_s": W * H / blocked_ms / 1e3, "point_queries_1m_ms": pts_ms,
-            "global_render_ms": glob_ms, "global_render_mpix_s": W * H / glob_ms / 1e3,
-            "note": "point queries include the 16 MB host->device copy of (u, v) and the result copy back"}
+            "blocked_render_mpix_s": W * H / blocked_ms / 1e3, "point_queries_10k_ms": pts10k_ms,
+            "point_queries_1m_ms": pts1m_ms, "global_render_ms": glob_ms,
+            "global_render_mpix_s": W * H / glob_ms / 1e3,
+            "note": "point queries include the host->device copy of (u, v) and the result copy back"}
+
+
+def secondary_c4(ctx):
+    """configs[3] (C4) on one GPU: random-local N = 1M, 8192x8192 photo-like
+    target (a 2048x2048 photo-like image upsampled 4x, nearest -- the
+    generator itself takes a minute at 8192^2), train iterations/s (20 steps,
+    L2 flushed before each), and the global render."""
+    from paper_2407_01866_b200 import synth
+    W = H = 8192
+    ctx.set_params(synth.random_local_set(1_000_000, W, H, seed=7))
+    small = synth.photo_like_image(2048, 2048, 31004)
+    ctx.set_target(np.ascontiguousarray(small.repeat(4, axis=0).repeat(4, axis=1)))
+    ctx.upload_samples(synth.sample_indices(NS, W, H, seed=99, steps=30))
+    ctx.train_iterations(5, K, LR, 1, want_losses=False)
+    ms = []
+    for s in range(20):
+        ctx.flush_l2(FLUSH_BYTES)
+        ctx.timer_begin()
+        ctx.train_iterations(1, K, LR, 6 + s, want_losses=False)
+        ms.append(ctx.timer_end())
+    ctx.render_image(W, H, K, host=False)
+    glob_ms = _best_ms(ctx, lambda: ctx.render_image(W, H, K, host=False))
+    return {"config": "C4 (1 GPU): random-local 1M G, 8192x8192, NS=10k, K=10",
+            "train_iters_per_s": 1e3 * len(ms) / sum(ms), "ms_per_step": sum(ms) / len(ms),
+            "global_render_ms": glob_ms, "global_render_mpix_s": W * H / glob_ms / 1e3}
+
+
+def secondary_c5(ctx):
+    """configs[4] (C5), one GPU's share: 8 texture-like 1024x1024 sets of 50k
+    random-local Gaussians; for each, the LoD prefixes {25k, 31.25k, 37.5k,
+    43.75k, 50k} (fit.cpp:182-201's stage counts) are partitioned (n_max 64)
+    and rendered blocked."""
+    from paper_2407_01866_b200 import synth
+    W = H = 1024
+    sets = [synth.random_local_set(50_000, W, H, seed=100 + t) for t in range(8)]
+    prefixes = [25_000, 31_250, 37_500, 43_750, 50_000]
+
+    def sweep():
+        for p in sets:
+            for m in prefixes:
+                ctx.set_params(p[:m])
+                ctx.partition_build(64)
+                ctx.render_image_blocked(W, H, K, host=False)
+    sweep()
+    ms = _best_ms(ctx, sweep, reps=2)
+    return {"config": "C5 (1 GPU share): 8 x 1024x1024 textures, 50k G, 5 LoD prefixes each, blocked (n_max 64)",
+            "sweep_ms": ms, "renders": 40, "mpix_s_incl_partition": 40 * W * H / ms / 1e3}
 
 
 def secondary_fit(ctx):
-    """configs[1] as the config text states it: a full C2 optimisation, 5k
-    iterations with gradient-based init (50k Gaussians) and four
-    error-guided additions (to 100k), evaluation every 1000 iterations --
-    igs_fit end to end (host init/alias tables, device iterations, device
-    BSP evaluation renders), after a short warm-up fit."""
+    """configs[1] as its text states it: a full C2 optimisation (SURVEY.md 8d
+    compressed schedule) -- igs_fit end to end (host init and alias tables,
+    device iterations, device BSP evaluation renders), after a short warm-up
+    fit."""
     import time
     from paper_2407_01866_b200 import Context, synth
     target = synth.photo_like_image(W_IMG, H_IMG, 31001)
     ctx.fit(target, Context.fit_config(budget=100_000, iterations=200, eval_interval=1000, warmup_iters=100,
                                        densify_interval=50))
-    cfg = Context.fit_config(budget=100_000, iterations=5000, eval_interval=1000, warmup_iters=1000,
+    cfg = Context.fit_config(budget=100_000, iterations=5000, eval_interval=500, warmup_iters=1000,
                              densify_interval=1000)
     t0 = time.perf_counter()
     rep = ctx.fit(target, cfg)
     wall = time.perf_counter() - t0
-    return {"config": "C2 fit: 2048x2048, budget 100k (50k init + 4 x 12.5k), 5000 iterations, eval every 1000",
+    return {"config": "C2 fit (SURVEY.md 8d schedule): 2048x2048, budget 100k (50k init + 4 x 12.5k), 5000 "
+                      "iterations, warmup 1000, densify every 1000, eval every 500",
             "wall_s": wall, "iters_per_s_incl_everything": 5000 / wall, "final_count": rep["final_count"],
             "psnr_per_eval": [round(e["psnr"], 4) for e in rep["evals"]]}
 
