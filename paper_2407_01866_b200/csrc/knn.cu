@@ -61,10 +61,7 @@ __device__ __forceinline__ int ring_dy(int it, int R) {
 // from the Adam kernels' accumulation; exact either way, only the tightness
 // of the bounds drifts as Gaussians move and change scale).
 constexpr int kRefitPeriod = 16;
-#ifndef IGS_GROW_SHIFT
-#define IGS_GROW_SHIFT 3
-#endif
-constexpr int kGrowShift = IGS_GROW_SHIFT;  // re-bucket when more than n >> kGrowShift Gaussians grew
+constexpr int kGrowShift = 3;  // re-bucket when more than n >> kGrowShift Gaussians grew
 
 struct __align__(16) Sum {
     double x0, y0, x1, y1;  // centre bbox (empty: +inf/-inf)
@@ -421,10 +418,7 @@ struct WarpTopK {
     }
 };
 
-#ifndef IGS_MERGE_MIN
-#define IGS_MERGE_MIN 8
-#endif
-constexpr int kMergeMin = IGS_MERGE_MIN;  // candidates per batch from which merge() beats sequential inserts
+constexpr int kMergeMin = 8;  // candidates per batch from which merge() beats sequential inserts
 
 // Evaluates the members of up to 32 cells (lane i: range [o_i, o_i + m_i)),
 // flattened so that all lanes work on members.

@@ -1,5 +1,6 @@
-// train.cu -- kernel 4 (backward with sample-ordered reduction) and
-// kernel 5 (fused Adam + constrain + re-prepare).
+// train.cu -- kernel 4 (backward with sample-ordered reduction), kernel 5
+// (fused short-segment sum + Adam + constrain + re-prepare + kNN tree
+// accumulation), and the iteration's staging / publication kernels.
 //
 // Reference: renderer.cpp:91-122 (sample_gradients), :193-252
 // (backward_into / ordered reduction), fit.cpp:51-106
@@ -10,12 +11,15 @@
 // order (renderer.cpp:251, fit.cpp:91-104).  Each sample contributes at most
 // once per Gaussian (its top-K indices are distinct), so the per-Gaussian
 // sum is the sequence of that Gaussian's contributions in ascending sample
-// index.  Deterministic mode (default) reproduces it bit for bit: a stable
-// radix sort of the NS*K contribution keys by Gaussian index keeps sample
-// order inside each key, then one thread per Gaussian sums its segment
-// sequentially starting from 0.0 -- the exact operation sequence of the
-// reference.  Fast mode accumulates with fp64 atomics instead
-// (order-nondeterministic, ~1e-16 relative).
+// index.  Deterministic mode (default) reproduces it bit for bit: the
+// search epilogue counts contributions per Gaussian, an exclusive scan gives
+// each Gaussian a segment, a scatter fills it with slot ids (slot = sample *
+// K + entry, so slot order is sample order), and each segment is put in slot
+// order and summed sequentially from 0.0 -- the exact operation sequence of
+// the reference: short segments inside the fused Adam kernel (one thread per
+// Gaussian), long ones by long_segment_kernel (a CTA each).  Fast mode
+// accumulates with fp64 atomics instead (order-nondeterministic, ~1e-16
+// relative).
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
@@ -133,39 +137,6 @@ __global__ void sample_finish_kernel(const ScanRec* __restrict__ scan, const Sha
             keys[slot] = ci;
         }
     }
-}
-
-// One thread per Gaussian: its contributions are the sorted segment
-// [lower_bound(g), lower_bound(g+1)); summed in sample order from 0.0.
-__global__ void segment_reduce_kernel(const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
-                                      uint32_t nitems, const double* __restrict__ contrib, uint32_t n,
-                                      double* __restrict__ grads) {
-    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= n) return;
-    uint32_t lo = 0, hi = nitems;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (skeys[mid] < g) lo = mid + 1;
-        else hi = mid;
-    }
-    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (uint32_t e = lo; e < nitems && skeys[e] == g; ++e) {
-        const double2* c = reinterpret_cast<const double2*>(contrib + (size_t)svals[e] * 8);
-        const double2 a = c[0], b = c[1], cc = c[2], d = c[3];
-        acc[0] = __dadd_rn(acc[0], a.x);
-        acc[1] = __dadd_rn(acc[1], a.y);
-        acc[2] = __dadd_rn(acc[2], b.x);
-        acc[3] = __dadd_rn(acc[3], b.y);
-        acc[4] = __dadd_rn(acc[4], cc.x);
-        acc[5] = __dadd_rn(acc[5], cc.y);
-        acc[6] = __dadd_rn(acc[6], d.x);
-        acc[7] = __dadd_rn(acc[7], d.y);
-    }
-    double2* o = reinterpret_cast<double2*>(grads + (size_t)g * 8);
-    o[0] = make_double2(acc[0], acc[1]);
-    o[1] = make_double2(acc[2], acc[3]);
-    o[2] = make_double2(acc[4], acc[5]);
-    o[3] = make_double2(acc[6], acc[7]);
 }
 
 // --- counting-sort reduction (deterministic, reference summation order) ----
@@ -371,11 +342,6 @@ __global__ void count_keys_kernel(const uint32_t* __restrict__ keys, uint32_t it
     if (slot >= items) return;
     const uint32_t g = keys[slot];
     if (g < n) atomicAdd(gcnt + g, 1u);
-}
-
-__global__ void iota_kernel(uint32_t* v, uint32_t n) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) v[i] = i;
 }
 
 // Deterministic loss sum (fixed tree order), times 1/ns.  One CTA.
