@@ -141,7 +141,8 @@ def run_ours(args, rank, world, local_rank, dist):
     params, target = workload()
     total_steps = args.warmup + args.steps
     samples = synth.sample_indices(NS, W_IMG, H_IMG, seed=99, steps=total_steps)
-    mine = np.ascontiguousarray(samples[:, rank::world])  # this rank's share of every step
+    from paper_2407_01866_b200 import dist as D
+    mine = D.shard(samples, rank, world)  # this rank's contiguous block of every step
     ctx = Context(local_rank)
     ctx.set_params(params)
     ctx.set_target(target)

@@ -50,6 +50,7 @@ struct NcclApi {
     ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
+    ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
 };
 NcclApi& nccl() {
     static NcclApi api;
@@ -64,7 +65,8 @@ NcclApi& nccl() {
     api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
     api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
     api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
-    api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce;
+    api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
+    api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce && api.allGather;
     return api;
 }
 }  // namespace
@@ -533,9 +535,33 @@ int igs_set_target(igs_ctx* ctx, const float* rgb, int width, int height) {
     return host_to_dev(ctx, ctx->target.p, rgb, bytes);
 }
 
+}  // extern "C"
+
+// In-place all-gather of `bytes` per rank: rank r's block sits at
+// buf + r * bytes (train.cu's sample-ordered exchange of contributions).
+int igs_comm_allgather(igs_ctx* ctx, void* buf, size_t bytes) {
+#ifndef IGS_NO_NCCL
+    if (!ctx->comm) return IGS_OK;
+    char* b = static_cast<char*>(buf);
+    if (nccl().allGather(b + (size_t)ctx->rank * bytes, b, bytes, ncclChar, ctx->comm, ctx->stream) != ncclSuccess)
+        return igs_fail(ctx, IGS_E_CUDA, "ncclAllGather failed");
+#else
+    (void)ctx;
+    (void)buf;
+    (void)bytes;
+#endif
+    return IGS_OK;
+}
+
+extern "C" {
+
+
+// Gradient + loss all-reduce, for the paths that do not exchange
+// contributions (fp64-atomics mode, the brute-force fallback); after an
+// exchange the gradients and the loss are already global.
 static int allreduce_grads(igs_ctx* ctx, double* dev_loss) {
 #ifndef IGS_NO_NCCL
-    if (ctx->comm) {  // a 1-rank communicator still runs (exercises the path on one GPU)
+    if (ctx->comm && !ctx->exchanged) {  // a 1-rank communicator still runs (exercises the path on one GPU)
         if (nccl().allReduce(ctx->grads, ctx->grads, (size_t)ctx->n * 8, ncclDouble, ncclSum, ctx->comm, ctx->stream) !=
             ncclSuccess)
             return igs_fail(ctx, IGS_E_CUDA, "ncclAllReduce(grads) failed");

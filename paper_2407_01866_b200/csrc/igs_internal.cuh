@@ -237,6 +237,7 @@ struct igs_ctx {
     void* knn = nullptr;             // KnnBufs (knn.cu)
     uint64_t params_version = 0;     // bumped on every change of the set
     long long knn_grown = -1;        // status[3] of the last step read back (-1: unknown)
+    bool exchanged = false;          // the last forward/backward gathered every rank's contributions
     const void* gcnt_clean = nullptr;  // deterministic-reduction counters left zeroed (for this n)
     uint32_t gcnt_clean_n = 0;
 
@@ -349,7 +350,8 @@ int igs_raster_knn(igs_ctx* ctx, int W, int H, int k, int row0, int row1, float*
 int igs_knn_forward_backward(igs_ctx* ctx, int mode, const uint32_t* sidx, const double* samples5, uint32_t npts,
                              int kk, double inv_n, double* losses, double* contrib, uint32_t* keys, uint32_t* gcnt,
                              double* grads_atomic, uint32_t* zero_word = nullptr,
-                             const L2Prefetch* pf = nullptr);
+                             const L2Prefetch* pf = nullptr, int defer_loss_check = 0);
+int igs_comm_allgather(igs_ctx* ctx, void* buf, size_t bytes);
 L2Prefetch igs_knn_tree_inputs(igs_ctx* ctx);
 int igs_topk_samples_culled(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq);
 int igs_topk_pixels_culled(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq, int W,

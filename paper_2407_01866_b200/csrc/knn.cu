@@ -494,6 +494,7 @@ struct Epi {
     uint32_t* oi;                // mode 2
     uint32_t n;
     uint32_t* zero_word;         // zeroed at the start of the search (or null)
+    int defer_loss_check;        // multi-rank: the non-finite loss check runs on the gathered losses
     L2Prefetch pf;               // what the kernels after the search read (Adam's rows)
 };
 
@@ -560,7 +561,7 @@ __device__ __forceinline__ void warp_epilogue(const Epi& E, const ScanRec* __res
         if (lane == 0) {
             const double l = __dadd_rn(__dadd_rn(fabs(d0), fabs(d1)), fabs(d2));
             E.losses[pt] = l;
-            if (!isfinite(l)) atomicMin(E.status + 2, (long long)pt);
+            if (!isfinite(l) && !E.defer_loss_check) atomicMin(E.status + 2, (long long)pt);
         }
         up0 = __dmul_rn(sign_of(d0), E.inv_n);
         up1 = __dmul_rn(sign_of(d1), E.inv_n);
@@ -608,7 +609,7 @@ __device__ __forceinline__ void warp_epilogue(const Epi& E, const ScanRec* __res
         o[2] = make_double2(d[4], d[5]);
         o[3] = make_double2(d[6], d[7]);
         E.keys[slot] = myi;
-        atomicAdd(E.gcnt + myi, 1u);
+        if (E.gcnt) atomicAdd(E.gcnt + myi, 1u);
     }
 }
 
@@ -1503,8 +1504,10 @@ int igs_topk_knn(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t*
 // grads_atomic.
 int igs_knn_forward_backward(igs_ctx* ctx, int mode, const uint32_t* sidx, const double* samples5, uint32_t npts,
                              int kk, double inv_n, double* losses, double* contrib, uint32_t* keys, uint32_t* gcnt,
-                             double* grads_atomic, uint32_t* zero_word, const L2Prefetch* pf) {
+                             double* grads_atomic, uint32_t* zero_word, const L2Prefetch* pf,
+                             int defer_loss_check) {
     Epi E{};
+    E.defer_loss_check = defer_loss_check;
     E.zero_word = zero_word;
     if (pf) E.pf = *pf;
     E.gcnt = gcnt;

@@ -336,6 +336,21 @@ __global__ void __launch_bounds__(kLongThreads) long_segment_kernel(const uint32
     }
 }
 
+// Multi-rank exchange: per-Gaussian counts over every rank's contributions,
+// and the non-finite loss check over the gathered losses (first global
+// sample index, as a single rank would flag it).
+__global__ void count_check_kernel(const uint32_t* __restrict__ keys, uint32_t items, uint32_t n,
+                                   uint32_t* __restrict__ gcnt, const double* __restrict__ losses, uint32_t ns,
+                                   long long* __restrict__ status) {
+    pdl_wait();
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < items) {
+        const uint32_t g = keys[i];
+        if (g < n) atomicAdd(gcnt + g, 1u);
+    }
+    if (losses && i < ns && !isfinite(losses[i])) atomicMin(status + 2, (long long)i);
+}
+
 __global__ void count_keys_kernel(const uint32_t* __restrict__ keys, uint32_t items, uint32_t n,
                                   uint32_t* __restrict__ gcnt) {
     const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
@@ -683,14 +698,28 @@ int igs_status_reset(igs_ctx* ctx) {
 // Shared forward/backward over ns device points.  mode 0: train (sidx +
 // target), mode 1: backward (samples5 on device).  Writes ctx->grads and,
 // in train mode, the loss into *dev_loss.
+// Multi-rank (a communicator attached), deterministic mode: every rank
+// computes the contributions of its contiguous share of the samples
+// (rank r: global samples [r ns, (r+1) ns)) into its block of the full
+// slot arrays, an in-place all-gather completes them, and every rank runs
+// the single-GPU reduction and Adam on all NS contributions -- the same
+// sample-ordered sums, so the result is bit-identical to one GPU's
+// (SURVEY.md 8e's all-gather alternative; fewer bytes than an all-reduce
+// of the gradients).
 int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint32_t* dev_sidx,
                          const double* dev_samples5, double* dev_loss, double inv_n, const double* fuse_lr4,
                          long long t, bool* fused) {
     if (fused) *fused = false;
     const uint32_t n = ctx->n;
     const int kk = (int)std::min<uint32_t>((uint32_t)k, n);
-    const size_t items = (size_t)ns * kk;
-    double* losses = (double*)igs_scratch(ctx, 9, (size_t)std::max<uint32_t>(ns, 1) * sizeof(double));
+    const bool knn_path = ctx->opt_cull && kk <= 32;
+    const bool exch = ctx->comm != nullptr && ctx->opt_deterministic && knn_path;
+    const uint32_t R = exch ? (uint32_t)ctx->nranks : 1u, rk = exch ? (uint32_t)ctx->rank : 0u;
+    ctx->exchanged = exch;
+    const size_t items_local = (size_t)ns * kk;
+    const size_t items = items_local * R;  // all ranks' contributions
+    const uint32_t ns_all = ns * R;
+    double* losses = (double*)igs_scratch(ctx, 9, (size_t)std::max<uint32_t>(ns_all, 1) * sizeof(double));
     double* contrib = nullptr;
     uint32_t *keys = nullptr, *gcnt = nullptr, *goff = nullptr, *perm = nullptr, *long_ctl = nullptr;
     bool gcnt_filled = false;
@@ -709,13 +738,13 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
         ctx->gcnt_clean = nullptr;
         // (long_ctl[0]: long-segment count, zeroed by the search kernel on the
         // fused path; long_ctl[1..]: the queue)
-        if (!(ctx->opt_cull && kk <= 32)) IGS_CUDA(ctx, cudaMemsetAsync(long_ctl, 0, sizeof(uint32_t), ctx->stream));
+        if (!knn_path) IGS_CUDA(ctx, cudaMemsetAsync(long_ctl, 0, sizeof(uint32_t), ctx->stream));
     } else {
         IGS_CUDA(ctx, cudaMemsetAsync(ctx->grads, 0, (size_t)n * 8 * sizeof(double), ctx->stream));
     }
     if (!losses) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (train)");
     int e;
-    if (ctx->opt_cull && kk <= 32) {
+    if (knn_path) {
         // fused: exact top-K search + blend / loss / gradient epilogue per warp
         // the fused Adam's parameter rows and moments, prefetched during the search
         L2Prefetch pf{};
@@ -724,10 +753,12 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
             l2pf_add(pf, ctx->adam_m, (size_t)n * 64);
             l2pf_add(pf, ctx->adam_v, (size_t)n * 64);
         }
-        e = igs_knn_forward_backward(ctx, mode, dev_sidx, dev_samples5, ns, kk, inv_n, losses, contrib, keys, gcnt,
-                                     ctx->opt_deterministic ? nullptr : ctx->grads, long_ctl, &pf);
+        e = igs_knn_forward_backward(ctx, mode, dev_sidx, dev_samples5, ns, kk, inv_n, losses + (size_t)rk * ns,
+                                     contrib ? contrib + rk * items_local * 8 : nullptr,
+                                     keys ? keys + rk * items_local : nullptr, exch ? nullptr : gcnt,
+                                     ctx->opt_deterministic ? nullptr : ctx->grads, long_ctl, &pf, exch ? 1 : 0);
         if (e) return e;
-        gcnt_filled = true;
+        gcnt_filled = !exch;
     } else {
         double* uv = (double*)igs_scratch(ctx, 0, (size_t)ns * 2 * sizeof(double));
         double* lq = (double*)igs_scratch(ctx, 1, (size_t)ns * kk * sizeof(double));
@@ -750,13 +781,23 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
         IGS_LAUNCHED(ctx);
         igs_prof_end(ctx, IGS_PROF_FINISH, (double)items);
     }
+    if (exch) {
+        // every rank's contributions (and losses) in global slot order
+        if ((e = igs_comm_allgather(ctx, keys, items_local * sizeof(uint32_t)))) return e;
+        if ((e = igs_comm_allgather(ctx, contrib, items_local * 8 * sizeof(double)))) return e;
+        if (mode == 0 && (e = igs_comm_allgather(ctx, losses, (size_t)ns * sizeof(double)))) return e;
+        IGS_PDL(ctx, count_check_kernel, (unsigned)((std::max<size_t>(items, ns_all) + 255) / 256), 256, 0,
+                (const uint32_t*)keys, (uint32_t)items, n, gcnt, mode == 0 ? (const double*)losses : nullptr, ns_all,
+                ctx->status);
+        gcnt_filled = true;
+    }
     // the loss sum needs only the per-sample losses: it runs on the side
     // stream, overlapping the reduction and Adam, and is joined below
     const bool loss_side = mode == 0 && dev_loss;
     if (loss_side) {
         IGS_CUDA(ctx, cudaEventRecord(ctx->ev_fork, ctx->stream));
         IGS_CUDA(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
-        loss_reduce_kernel<<<1, 1024, 0, ctx->side>>>(losses, ns, inv_n, dev_loss);
+        loss_reduce_kernel<<<1, 1024, 0, ctx->side>>>(losses, ns_all, inv_n, dev_loss);
         IGS_LAUNCHED(ctx);
         IGS_CUDA(ctx, cudaEventRecord(ctx->ev_join, ctx->side));
     }
@@ -782,7 +823,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
         IGS_PDL(ctx, long_segment_kernel, 8 * ctx->sm_count, kLongThreads, 0, (const uint32_t*)gcnt,
                 (const uint32_t*)goff, perm, (const double*)contrib, ctx->grads, (const uint32_t*)long_ctl,
                 (const uint32_t*)(long_ctl + 1), ctx->status, big);
-        if (fuse_lr4 && ctx->nranks == 1 && !ctx->comm) {
+        if (fuse_lr4 && (exch || (ctx->nranks == 1 && !ctx->comm))) {
             // short segments summed inside the Adam kernel (one pass over the set)
             const double bc1 = 1.0 - std::pow(0.9, (double)t);  // adam.cpp:16-17, host libm
             const double bc2 = 1.0 - std::pow(0.999, (double)t);

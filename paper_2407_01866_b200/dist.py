@@ -1,11 +1,13 @@
 """Multi-GPU decomposition of the hot path.
 
-* Training: one iteration's samples are split across ranks (strided shard);
-  every rank runs the exact global top-K + backward on its share with the
-  upstream scaled by 1 / (total samples), the per-Gaussian gradients and the
-  loss are summed with one NCCL all-reduce over NVLink (inside the C-ABI,
-  igs_comm_init), and every rank applies the identical Adam step -- the
-  replicated sets stay bit-identical across ranks.
+* Training: one iteration's samples are split across ranks in contiguous
+  equal blocks (rank r: samples [r ns, (r+1) ns)); every rank runs the exact
+  global top-K + contribution epilogue on its block with the upstream scaled
+  by 1 / (total samples), one in-place NCCL all-gather over NVLink (inside
+  the C-ABI, igs_comm_init) completes the contribution and loss arrays in
+  global sample order, and every rank runs the single-GPU sample-ordered
+  reduction and Adam on all of them -- the result is bit-identical to one
+  GPU's, and the replicated sets stay identical across ranks.
 * Rendering: pixels are independent; rank r renders the band of tile rows
   [row0, row1) (igs_render_image_rows) with no communication.
 
@@ -21,8 +23,16 @@ TILE = 16
 
 
 def shard(sample_idx: np.ndarray, rank: int, world: int) -> np.ndarray:
-    """This rank's samples of one iteration (strided: balanced for any count)."""
-    return np.ascontiguousarray(np.asarray(sample_idx)[..., rank::world])
+    """This rank's samples of one iteration: the contiguous block
+    [rank * ns, (rank + 1) * ns) of the last axis, ns = count / world (the
+    device path gathers the blocks back in this order, so the count must
+    divide evenly)."""
+    a = np.asarray(sample_idx)
+    total = a.shape[-1]
+    if total % world:
+        raise ValueError(f"{total} samples do not split evenly over {world} ranks")
+    ns = total // world
+    return np.ascontiguousarray(a[..., rank * ns:(rank + 1) * ns])
 
 
 def row_band(height: int, rank: int, world: int, tile: int = TILE) -> tuple[int, int]:

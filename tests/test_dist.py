@@ -36,8 +36,11 @@ def _worker(rank, world, port, q):
         target = synth.photo_like_image(W, H, 31011)
         params = P.initialize_set(target, 300, 0.3, 4)
         params[:, 3:5] *= 3
-        sidx = synth.sample_indices(1001, W, H, seed=12)[0]  # odd count: uneven shards
+        sidx = synth.sample_indices(1000, W, H, seed=12)[0]
         mine = D.shard(sidx, rank, world)
+        blocks = [None] * world
+        dist.all_gather_object(blocks, mine)
+        assert np.array_equal(np.concatenate(blocks), sidx)  # gathered blocks = the sample order
         # the oracle scales by its own shard size; rescale to 1/NS_total like the device path
         loss, g = P.train_step(params, target, mine, 10)
         scale = mine.shape[0] / sidx.shape[0]
@@ -72,7 +75,7 @@ def test_sharded_train_step_and_row_bands(port):
     target = synth.photo_like_image(W, H, 31011)
     params = port.initialize_set(target, 300, 0.3, 4)
     params[:, 3:5] *= 3
-    sidx = synth.sample_indices(1001, W, H, seed=12)[0]
+    sidx = synth.sample_indices(1000, W, H, seed=12)[0]
     loss, g = port.train_step(params, target, sidx, 10)
     np.testing.assert_allclose(red[:-1].reshape(g.shape), g, rtol=1e-12, atol=1e-18)
     assert abs(red[-1] - loss) <= 1e-12 * loss
@@ -89,3 +92,11 @@ def test_row_bands_cover_and_align():
             assert bands[0][0] == 0 and bands[-1][1] == H
             for (a0, a1), (b0, b1) in zip(bands, bands[1:]):
                 assert a1 == b0 and a0 % 16 == 0
+
+
+def test_shard_blocks_and_uneven_count():
+    from paper_2407_01866_b200 import dist as D
+    s = np.arange(24).reshape(2, 12)
+    assert np.array_equal(np.concatenate([D.shard(s, r, 4) for r in range(4)], axis=1), s)
+    with pytest.raises(ValueError):
+        D.shard(np.arange(10), 0, 4)

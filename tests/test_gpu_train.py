@@ -168,11 +168,13 @@ def test_frozen_selection_finite_differences(gctx, port):
             assert abs(an - fd) / max(abs(an), abs(fd), 1e-6) < 1e-4
 
 
-def test_nccl_single_rank_allreduce_path(gctx, port):
-    """The NCCL gradient/loss all-reduce inside the train step, with a 1-rank
-    communicator (one GPU per gpurun box): results must equal the no-comm
-    path exactly.  The multi-rank decomposition is covered on CPU by
-    tests/test_dist.py (gloo, world size 2)."""
+def test_nccl_single_rank_exchange_path(gctx, port):
+    """The multi-rank train step with a 1-rank communicator (one GPU per
+    gpurun box): the in-place all-gather of contributions and losses, the
+    counts and the loss check on the gathered arrays, then the single-GPU
+    reduction and Adam -- results must equal the no-comm path exactly (with
+    R ranks every rank reproduces the 1-GPU result the same way).  The
+    sample sharding is covered on CPU by tests/test_dist.py (gloo)."""
     from paper_2407_01866_b200 import Context
     target = synth.photo_like_image(96, 64, 31021)
     params = port.initialize_set(target, 500, 0.3, 21)
@@ -186,9 +188,15 @@ def test_nccl_single_rank_allreduce_path(gctx, port):
         c2.set_target(target)
         l1, g1 = c2.train_step(sidx, 10)
         assert l1 == l0 and np.array_equal(g1, g0)
-        c2.train_iteration(sidx, 10, LR, 1)
-        gctx.train_iteration(sidx, 10, LR, 1)
+        l2 = c2.train_iteration(sidx, 10, LR, 1)
+        l3 = gctx.train_iteration(sidx, 10, LR, 1)
+        assert l2 == l3
         assert np.array_equal(c2.get_params(), gctx.get_params())
+        c2.set_option(OPT_DETERMINISTIC, 0)  # fp64-atomics mode keeps the all-reduce
+        c2.set_params(params)
+        l4, g4 = c2.train_step(sidx, 10)
+        assert abs(l4 - l0) <= 1e-12 * abs(l0)
+        grad_close(g4, g0, 1e-12)
 
 
 def test_knn_refit_stays_exact_over_many_steps(gctx, port):
