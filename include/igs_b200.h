@@ -218,6 +218,20 @@ int igs_get_prepared(igs_ctx* ctx, double* scan6, uint32_t n);
 int igs_tile_lists(igs_ctx* ctx, int width, int height, int k, uint32_t* ntiles, uint64_t* total,
                    uint32_t* offsets, uint32_t* members, double* tau);
 
+/* ---- IGS2 container (codec.hpp:46-57, codec.cpp:141-224) ------------------- */
+/* encode(set, partition?, width, height, k): the resident set (and, with
+ * with_partition, the resident partition's blocks) as IGS2 bytes -- binary16
+ * packing on the device.  out == NULL or cap too small: *size only. */
+int igs_encode(igs_ctx* ctx, int with_partition, uint32_t width, uint32_t height, int k, uint8_t* out, size_t cap,
+               size_t* size);
+/* decode(bytes): validates like the reference, unpacks + constrains the set on
+ * the device (it becomes the resident set), and rebuilds the partition from
+ * the stored block corners when there are any (rebuild_partition). */
+int igs_decode(igs_ctx* ctx, const uint8_t* bytes, size_t size, uint32_t* width, uint32_t* height, int* k,
+               uint32_t* n_blocks);
+/* quantize_set (codec.cpp:69-81) in place: every parameter through binary16, re-constrained. */
+int igs_quantize_set(igs_ctx* ctx);
+
 /* ---- benchmark support (device timing on the context's stream) ----------- */
 int igs_timer_begin(igs_ctx* ctx);
 /* Records the stop event (unless igs_train_iterations already recorded it

@@ -184,6 +184,44 @@ class Oracle:
             f.restype = res
             f.argtypes = args
 
+
+    # ---- IGS2 codec (reference library only) ------------------------------------------
+    def encode(self, params, width, height, k, part=None):
+        params = np.ascontiguousarray(params, np.float64)
+        size = C.c_size_t(0)
+        f = self.lib.ref_encode
+        f.restype = C.c_int
+        f.argtypes = [_dp, C.c_uint32, C.c_void_p, C.c_uint32, C.c_uint32, C.c_int, C.POINTER(C.c_uint8), C.c_size_t,
+                      C.POINTER(C.c_size_t)]
+        code = f(_ptr(params, _dp), params.shape[0], part.h if part is not None else None, width, height, k, None, 0,
+                 C.byref(size))
+        self._chk(code, "encode")
+        out = np.zeros(size.value, np.uint8)
+        self._chk(f(_ptr(params, _dp), params.shape[0], part.h if part is not None else None, width, height, k,
+                    out.ctypes.data_as(C.POINTER(C.c_uint8)), out.size, C.byref(size)), "encode")
+        return out.tobytes()
+
+    def decode(self, data, max_n=1 << 24):
+        buf = np.frombuffer(bytes(data), np.uint8).copy()
+        f = self.lib.ref_decode
+        f.restype = C.c_int
+        f.argtypes = [C.POINTER(C.c_uint8), C.c_size_t, _dp, C.c_uint32, _up, _up, _up, _ip, C.POINTER(C.c_void_p)]
+        n = C.c_uint32(0); w = C.c_uint32(0); h = C.c_uint32(0); k = C.c_int(0); part = C.c_void_p()
+        n_hdr = int.from_bytes(bytes(data)[12:16], "little") if len(data) >= 16 else 0
+        out = np.zeros((max(min(n_hdr, max_n), 1), 8))
+        self._chk(f(buf.ctypes.data_as(C.POINTER(C.c_uint8)), buf.size, _ptr(out, _dp), out.shape[0], C.byref(n),
+                    C.byref(w), C.byref(h), C.byref(k), C.byref(part)), "decode")
+        p = Partition(self.lib, part.value, self.p) if part.value else None
+        return out[:n.value], w.value, h.value, k.value, p
+
+    def quantize_set(self, params):
+        p = np.ascontiguousarray(params, np.float64).copy()
+        f = self.lib.ref_quantize_set
+        f.restype = C.c_int
+        f.argtypes = [_dp, C.c_uint32]
+        self._chk(f(_ptr(p, _dp), p.shape[0]), "quantize_set")
+        return p
+
     def _f(self, name):
         return getattr(self.lib, self.p + name)
 

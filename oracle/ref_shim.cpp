@@ -13,6 +13,7 @@
 
 #include "igs/adam.hpp"
 #include "igs/bsp.hpp"
+#include "igs/codec.hpp"
 #include "igs/error.hpp"
 #include "igs/fit.hpp"
 #include "igs/metrics.hpp"
@@ -431,6 +432,49 @@ int ref_train_iteration(double* p8, uint32_t n, double* m, double* v, const floa
     int e = ref_train_step(p8, n, target, W, H, sidx, ns, k, loss, grads.data());
     if (e) return e;
     return ref_adam_step(p8, grads.data(), m, v, n, lr4, t, nullptr);
+}
+
+
+// ---- IGS2 codec (codec.cpp) --------------------------------------------------
+// encode(set, partition?, W, H, k) into out (cap bytes); *size = full length
+int ref_encode(const double* p8, uint32_t n, const ref_partition* part, uint32_t W, uint32_t H, int k, uint8_t* out,
+               size_t cap, size_t* size) {
+    try {
+        const std::vector<uint8_t> b = encode(to_set(p8, n), part ? &part->p : nullptr, W, H, k);
+        *size = b.size();
+        if (out && cap >= b.size()) std::memcpy(out, b.data(), b.size());
+        return 0;
+    } catch (const Error& e) {
+        return code_of(e);
+    }
+}
+
+// decode(bytes): the set (<= max_n records), header fields, and the rebuilt
+// partition (null when the file has no blocks)
+int ref_decode(const uint8_t* bytes, size_t size, double* out8, uint32_t max_n, uint32_t* n, uint32_t* W,
+               uint32_t* H, int* k, ref_partition** part) {
+    try {
+        Decoded d = decode(std::vector<uint8_t>(bytes, bytes + size));
+        *n = static_cast<uint32_t>(d.set.size());
+        if (out8 && d.set.size() <= max_n) std::memcpy(out8, d.set.gaussians.data(), 64 * d.set.size());
+        *W = d.width;
+        *H = d.height;
+        *k = d.k;
+        *part = d.partition ? new ref_partition{std::move(*d.partition)} : nullptr;
+        return 0;
+    } catch (const Error& e) {
+        return code_of(e);
+    }
+}
+
+int ref_quantize_set(double* p8, uint32_t n) {
+    try {
+        const GaussianSet q = quantize_set(to_set(p8, n));
+        std::memcpy(p8, q.gaussians.data(), 64 * static_cast<size_t>(n));
+        return 0;
+    } catch (const Error& e) {
+        return code_of(e);
+    }
 }
 
 }  // extern "C"

@@ -773,6 +773,8 @@ int igs_partition_rebuild(igs_ctx* ctx, const double* rects4, uint32_t n_blocks)
     return e;
 }
 
+uint32_t igs_partition_source_size(igs_ctx* ctx) { return ctx->part ? ctx->part->source_size : 0; }
+
 int igs_partition_info(igs_ctx* ctx, uint32_t* n_blocks, uint64_t* shell_total) {
     if (!ctx) return IGS_E_INVALID_PARAMETER;
     if (!ctx->part) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "no partition");

@@ -19,6 +19,12 @@ int igs_status_reset(igs_ctx* ctx);
 int igs_stage_samples(igs_ctx* ctx, const uint32_t* host_pinned, uint32_t* dsidx, uint32_t ns);
 int igs_stage_draws(igs_ctx* ctx, const unsigned long long* host_raw, uint32_t* dsidx, uint32_t ns);
 int igs_publish(igs_ctx* ctx, const double* dloss, long long* host_res);
+int igs_codec_pack(igs_ctx* ctx, uint16_t* dev_out);
+int igs_codec_unpack(igs_ctx* ctx, const uint16_t* dev_in, uint32_t n);
+uint16_t igs_host_double_to_half(double d);
+double igs_host_half_to_double(uint16_t h);
+bool igs_host_encodable(double v);
+extern "C" uint32_t igs_partition_source_size(igs_ctx* ctx);
 int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint32_t* dev_sidx,
                          const double* dev_samples5, double* dev_loss, double inv_n, const double* fuse_lr4 = nullptr,
                          long long t = 0, bool* fused = nullptr);
@@ -918,6 +924,137 @@ int igs_tile_lists(igs_ctx* ctx, int width, int height, int k, uint32_t* ntiles,
     if (width < 1 || height < 1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "render target must be at least 1x1");
     if ((e = require_k(ctx, k))) return e;
     return igs_cull_lists(ctx, width, height, k, ntiles, total, offsets, members, tau);
+}
+
+
+// ---- IGS2 container (codec.cpp) ------------------------------------------------
+static void put16(uint8_t* b, uint16_t v) {
+    b[0] = (uint8_t)(v & 0xff);
+    b[1] = (uint8_t)(v >> 8);
+}
+static void put32(uint8_t* b, uint32_t v) {
+    for (int i = 0; i < 4; ++i) b[i] = (uint8_t)((v >> (8 * i)) & 0xff);
+}
+static uint16_t get16(const uint8_t* b) { return (uint16_t)(b[0] | (b[1] << 8)); }
+static uint32_t get32(const uint8_t* b) {
+    uint32_t v = 0;
+    for (int i = 0; i < 4; ++i) v |= (uint32_t)b[i] << (8 * i);
+    return v;
+}
+
+int igs_encode(igs_ctx* ctx, int with_partition, uint32_t width, uint32_t height, int k, uint8_t* out, size_t cap,
+               size_t* size_out) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    // codec.cpp:142-154 validation, in the reference's order
+    if (ctx->n == 0) return igs_fail(ctx, IGS_E_EMPTY_SET, "cannot encode an empty GaussianSet");
+    if (width == 0 || height == 0) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "encoded dimensions must be positive");
+    if (width > 0xffff || height > 0xffff)
+        return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "encoded dimensions exceed the u16 header fields");
+    if (k < 1 || k > 0xffff) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "k out of range for the header");
+    if (with_partition && !ctx->part) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "no partition");
+    if (with_partition && igs_partition_source_size(ctx) != ctx->n)
+        return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "partition was not built over this set");
+    uint32_t nb = 0;
+    int e;
+    if (with_partition && (e = igs_partition_info(ctx, &nb, nullptr))) return e;
+    const uint32_t n = ctx->n;
+    const size_t total = 20 + 16ull * n + 8ull * nb;
+    if (size_out) *size_out = total;
+    if (!out || cap < total) return IGS_OK;  // size query
+    uint16_t* dev = (uint16_t*)igs_scratch(ctx, 33, (size_t)n * 16);
+    if (!dev) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (encode)");
+    if ((e = igs_status_reset(ctx))) return e;
+    if ((e = igs_codec_pack(ctx, dev))) return e;
+    long long st[4];
+    if ((e = dev_to_host(ctx, st, ctx->status, sizeof(st)))) return e;
+    if (st[1] != LLONG_MAX)
+        return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "value of Gaussian parameter outside binary16 finite range");
+    std::memcpy(out, "IGS2", 4);
+    out[4] = 1;  // version
+    out[5] = 0;  // flags
+    put16(out + 6, (uint16_t)k);
+    put16(out + 8, (uint16_t)width);
+    put16(out + 10, (uint16_t)height);
+    put32(out + 12, n);
+    put32(out + 16, nb);
+    if ((e = dev_to_host(ctx, out + 20, dev, (size_t)n * 16))) return e;  // little-endian halves
+    if (nb) {
+        std::vector<double> rects((size_t)nb * 4);
+        if ((e = igs_partition_get(ctx, rects.data(), nullptr, nullptr, nullptr))) return e;
+        uint8_t* b = out + 20 + 16ull * n;
+        for (size_t i = 0; i < rects.size(); ++i) {
+            if (!igs_host_encodable(rects[i]))
+                return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "value of block corner outside binary16 finite range");
+            put16(b + 2 * i, igs_host_double_to_half(rects[i]));
+        }
+    }
+    return IGS_OK;
+}
+
+int igs_decode(igs_ctx* ctx, const uint8_t* bytes, size_t size, uint32_t* width, uint32_t* height, int* k,
+               uint32_t* n_blocks) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    // codec.cpp:186-224, the reference's checks and messages
+    if (!bytes || size < 20) return igs_fail(ctx, IGS_E_TRUNCATED, "file shorter than the 20-byte header");
+    if (std::memcmp(bytes, "IGS2", 4) != 0) return igs_fail(ctx, IGS_E_BAD_MAGIC, "not an IGS2 file");
+    if (bytes[4] != 1)
+        return igs_fail(ctx, IGS_E_BAD_VERSION, "unsupported IGS2 version " + std::to_string((int)bytes[4]));
+    const int kk = get16(bytes + 6);
+    const uint32_t w = get16(bytes + 8), h = get16(bytes + 10), n = get32(bytes + 12), nb = get32(bytes + 16);
+    if (n == 0) return igs_fail(ctx, IGS_E_EMPTY_SET, "IGS2 file contains zero Gaussians");
+    const size_t expected = 20 + 16ull * n + 8ull * nb;
+    if (size != expected)
+        return igs_fail(ctx, IGS_E_TRUNCATED,
+                        "file length " + std::to_string(size) + " != expected " + std::to_string(expected));
+    if (kk < 1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "header k must be >= 1");
+    if (w == 0 || h == 0) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "header dimensions must be positive");
+    int e = ensure_capacity(ctx, n, false);
+    if (e) return e;
+    uint16_t* dev = (uint16_t*)igs_scratch(ctx, 33, (size_t)n * 16);
+    if (!dev) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (decode)");
+    if ((e = host_to_dev(ctx, dev, bytes + 20, (size_t)n * 16))) return e;
+    if ((e = igs_status_reset(ctx))) return e;
+    if ((e = igs_codec_unpack(ctx, dev, n))) return e;
+    long long st[4];
+    if ((e = dev_to_host(ctx, st, ctx->status, sizeof(st)))) return e;
+    if (st[1] != LLONG_MAX) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "non-finite Gaussian parameters");
+    // a new set: fresh moments and gradients, as igs_set_params
+    ctx->n = n;
+    ctx->grads_valid = false;
+    ctx->params_version++;
+    const size_t rb = (size_t)n * 8 * sizeof(double);
+    IGS_CUDA(ctx, cudaMemsetAsync(ctx->adam_m, 0, rb, ctx->stream));
+    IGS_CUDA(ctx, cudaMemsetAsync(ctx->adam_v, 0, rb, ctx->stream));
+    IGS_CUDA(ctx, cudaMemsetAsync(ctx->grads, 0, rb, ctx->stream));
+    if ((e = igs_prepare_all(ctx, 0))) return e;
+    if (nb) {
+        // codec.cpp:213-223: stored corners -> rebuild_partition over the set
+        std::vector<double> rects((size_t)nb * 4);
+        const uint8_t* b = bytes + 20 + 16ull * n;
+        for (size_t i = 0; i < rects.size(); ++i) rects[i] = igs_host_half_to_double(get16(b + 2 * i));
+        if ((e = igs_partition_rebuild(ctx, rects.data(), nb))) return e;
+    }
+    if (width) *width = w;
+    if (height) *height = h;
+    if (k) *k = kk;
+    if (n_blocks) *n_blocks = nb;
+    return IGS_OK;
+}
+
+int igs_quantize_set(igs_ctx* ctx) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    if (ctx->n == 0) return IGS_OK;
+    int e;
+    if ((e = igs_status_reset(ctx))) return e;
+    if ((e = igs_codec_unpack(ctx, nullptr, ctx->n))) return e;
+    long long st[4];
+    if ((e = dev_to_host(ctx, st, ctx->status, sizeof(st)))) return e;
+    if (st[1] != LLONG_MAX) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "non-finite Gaussian parameters");
+    ctx->params_version++;
+    return igs_prepare_all(ctx, 0);
 }
 
 // ---- multi-GPU -------------------------------------------------------------------

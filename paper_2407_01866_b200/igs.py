@@ -127,6 +127,10 @@ SIGNATURES = {
     "igs_partition_rebuild": (C.c_int, [_vp, _dp, C.c_uint32]),
     "igs_partition_info": (C.c_int, [_vp, _up, _u64p]),
     "igs_partition_get": (C.c_int, [_vp, _dp, _dp, _up, _up]),
+    "igs_encode": (C.c_int, [_vp, C.c_int, C.c_uint32, C.c_uint32, C.c_int, _u8p, C.c_size_t,
+                             C.POINTER(C.c_size_t)]),
+    "igs_decode": (C.c_int, [_vp, _u8p, C.c_size_t, _up, _up, C.POINTER(C.c_int), _up]),
+    "igs_quantize_set": (C.c_int, [_vp]),
     "igs_locate_blocks": (C.c_int, [_vp, _dp, C.c_uint32, _i32p]),
     "igs_render_image_blocked": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _fp]),
     "igs_render_points_blocked": (C.c_int, [_vp, _dp, C.c_uint32, C.c_int, _dp]),
@@ -422,6 +426,27 @@ class Context:
         off = np.zeros(nb + 1, np.uint32); mem = np.zeros(max(tot, 1), np.uint32)
         self._chk(self.lib.igs_partition_get(self.h, _p(b, _dp), _p(s, _dp), _p(off, _up), _p(mem, _up)))
         return b, s, off, mem[:tot]
+
+    # ---- IGS2 container (codec.cpp) ---------------------------------------------------------
+    def encode(self, width: int, height: int, k: int = DEFAULT_K, with_partition: bool = False) -> bytes:
+        size = C.c_size_t(0)
+        self._chk(self.lib.igs_encode(self.h, int(with_partition), width, height, k, None, 0, C.byref(size)))
+        out = np.zeros(size.value, np.uint8)
+        self._chk(self.lib.igs_encode(self.h, int(with_partition), width, height, k, _p(out, _u8p), out.size,
+                                      C.byref(size)))
+        return out.tobytes()
+
+    def decode(self, data: bytes) -> dict:
+        """The set becomes the resident set (and the partition, if the file has
+        blocks); returns the header fields."""
+        buf = np.frombuffer(bytes(data), np.uint8).copy()
+        w = C.c_uint32(0); h = C.c_uint32(0); k = C.c_int(0); nb = C.c_uint32(0)
+        self._chk(self.lib.igs_decode(self.h, _p(buf, _u8p) if buf.size else None, buf.size, C.byref(w), C.byref(h),
+                                      C.byref(k), C.byref(nb)))
+        return {"width": w.value, "height": h.value, "k": k.value, "n_blocks": nb.value}
+
+    def quantize_set(self):
+        self._chk(self.lib.igs_quantize_set(self.h))
 
     def locate_blocks(self, uv):
         uv = _f64(uv, 2)
