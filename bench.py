@@ -237,7 +237,12 @@ def run_ours(args, rank, world, local_rank, dist):
                                    f"{OPS_PER_PAIR} fp64 ops",
                 "peak_source": "measured in this run (igs_fp64_peak: independent DMUL/DADD chains, all SMs); "
                                "MEASURED_PEAKS.json has no fp64 figure",
-                "avg_launch_us": scan_ms * 1e3 / max(scan_launches, 1)}
+                "avg_launch_us": scan_ms * 1e3 / max(scan_launches, 1),
+                # the fraction uses executed pairs; the reference's
+                # own work (its global scan) is NS x N pairs per iteration
+                "reference_equivalent_pairs_per_launch": float(NS) * N_GAUSS,
+                "reference_equivalent_gop_s": float(NS) * N_GAUSS * OPS_PER_PAIR / (
+                    scan_ms * 1e-3 / max(scan_launches, 1)) / 1e9}
     adam_ms, adam_launches, adam_bytes = prof["adam"]
     hbm = None
     try:
@@ -271,6 +276,10 @@ def run_ours(args, rank, world, local_rank, dist):
         render = {"metric": "global top-K render Mpix/s (render_image, 2048x2048, 100k G, K=10)",
                   "value": W_IMG * H_IMG / (r_ms * 1e-3) / 1e6, "unit": "Mpix/s", "ms": r_ms,
                   "pairs_per_pixel": r_pairs / (W_IMG * H_IMG),
+                  "roofline": {"bound": "fp64", "achieved": r_pairs * OPS_PER_PAIR / (r_ms * 1e-3) / 1e9,
+                               "peak": fp64_peak / 1e9, "unit": "Gop/s",
+                               "frac": r_pairs * OPS_PER_PAIR / (r_ms * 1e-3) / fp64_peak,
+                               "work": "executed (pixel, candidate) pairs x 14 fp64 ops"},
                   "state": f"the set after {args.warmup + args.steps} training steps",
                   "note": "L2 flushed before each render; every GPU renders the full image here "
                           "(tile-row sharding: igs_render_image_rows)"}
