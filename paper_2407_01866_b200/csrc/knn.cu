@@ -260,9 +260,13 @@ __global__ void __launch_bounds__(256) lq_tree_kernel(Acc* __restrict__ acc, Lq 
     for (int r = 0; r < 2; ++r)
         if (um[r]) ua[r] = acc[uc[r]];
     __shared__ bool last;
-    __threadfence();
+    // the block's stores are ordered before thread 0's fence by the barrier
+    // (the cooperative-groups grid-barrier pattern): one fence per block
     __syncthreads();
-    if (t == 0) last = atomicAdd(ticket, 1u) == (unsigned)(nb * nb - 1);
+    if (t == 0) {
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == (unsigned)(nb * nb - 1);
+    }
     __syncthreads();
     if (!last) return;
     __threadfence();
