@@ -778,7 +778,8 @@ int igs_train_wait(igs_ctx* ctx, double* loss) {
     if (st[0] != LLONG_MAX) {
         static const char* names[8] = {"mu_u", "mu_v", "theta", "s1", "s2", "r", "g", "b"};
         return igs_fail(ctx, IGS_E_INVALID_PARAMETER,
-                        "non-finite gradient for Gaussian " + std::to_string(st[0] / 8) + " parameter " + names[st[0] % 8]);
+                        "non-finite gradient for Gaussian " + std::to_string(st[0] / 8) + " parameter " +
+                            names[st[0] % 8]);
     }
     if (st[1] != LLONG_MAX) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "non-finite Gaussian parameters");
     if (loss) std::memcpy(loss, st + 4, sizeof(double));

@@ -1470,7 +1470,10 @@ TreeAcc igs_knn_tree_acc(igs_ctx* ctx) {
 void igs_knn_free(igs_ctx* ctx) {
     if (!ctx->knn) return;
     KnnBufs* b = static_cast<KnnBufs*>(ctx->knn);
-    if (getenv("IGS_KNN_STATS")) fprintf(stderr, "knn tree: %llu builds, %llu refits\n", (unsigned long long)b->builds, (unsigned long long)b->refits);
+    // IGS_KNN_STATS=1: how often the tree was re-bucketed vs refit (diagnostics)
+    if (getenv("IGS_KNN_STATS"))
+        fprintf(stderr, "knn tree: %llu builds, %llu refits\n", (unsigned long long)b->builds,
+                (unsigned long long)b->refits);
     for (DevBuf* d : {&b->cnt, &b->off, &b->key, &b->mem, &b->own, &b->sub, &b->cub_tmp, &b->hard, &b->ticket,
                       &b->part, &b->lcount, &b->acc})
         cudaFree(d->p);

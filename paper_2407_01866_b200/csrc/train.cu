@@ -533,7 +533,8 @@ __global__ void adam_kernel(double* __restrict__ params, const double* __restric
 // finite Gaussian is still updated, deterministically; the reference has
 // updated Gaussians 0..i-1 when it throws, adam.cpp:29-31).  A non-finite
 // loss (flagged by the search epilogue) skips the whole step, as fit.cpp:155.
-__global__ void __launch_bounds__(128, 6) segment_adam_kernel(uint32_t* __restrict__ gcnt, const uint32_t* __restrict__ goff,
+__global__ void __launch_bounds__(128, 6) segment_adam_kernel(uint32_t* __restrict__ gcnt,
+                                                              const uint32_t* __restrict__ goff,
                                     const uint32_t* __restrict__ perm, const double* __restrict__ contrib,
                                     uint32_t n, double* __restrict__ grads, double* __restrict__ params,
                                     double* __restrict__ m, double* __restrict__ v, ScanRec* __restrict__ scan,
