@@ -526,64 +526,187 @@ __global__ void adam_kernel(double* __restrict__ params, const double* __restric
              status, ta);
 }
 
-// Fused short-segment reduction + Adam (single rank): thread g sums its
+__device__ __forceinline__ double shx(double v) { return __shfl_xor_sync(0xffffffffu, v, 1); }
+
+// Fused short-segment reduction + Adam: a lane pair per Gaussian sums its
 // short segment in sample order (or reads the long-segment result), stores
 // the gradient, and updates Gaussian g unless that gradient is non-finite
 // (then it flags status[0] = first (i, p) and leaves g untouched -- every
 // finite Gaussian is still updated, deterministically; the reference has
 // updated Gaussians 0..i-1 when it throws, adam.cpp:29-31).  A non-finite
 // loss (flagged by the search epilogue) skips the whole step, as fit.cpp:155.
-__global__ void __launch_bounds__(128, 6) segment_adam_kernel(uint32_t* __restrict__ gcnt,
-                                                              const uint32_t* __restrict__ goff,
-                                    const uint32_t* __restrict__ perm, const double* __restrict__ contrib,
-                                    uint32_t n, double* __restrict__ grads, double* __restrict__ params,
-                                    double* __restrict__ m, double* __restrict__ v, ScanRec* __restrict__ scan,
-                                    ShadeRec* __restrict__ shade, double lr_mu, double lr_color, double lr_scale,
-                                    double lr_theta, double bc1, double bc2, double ibc1, double ibc2,
-                                    long long* __restrict__ status, TreeAcc ta) {
+// Two lanes per Gaussian: lane h = 0 owns parameters 0-3 (mu, theta, s1),
+// h = 1 owns 4-7 (s2, colour); the Adam chains split in half, lane 1 forms
+// sin/cos while lane 0 forms both reciprocals.
+__global__ void __launch_bounds__(128, 8) segment_adam_kernel(
+    uint32_t* __restrict__ gcnt, const uint32_t* __restrict__ goff, const uint32_t* __restrict__ perm,
+    const double* __restrict__ contrib, uint32_t n, double* __restrict__ grads, double* __restrict__ params,
+    double* __restrict__ m, double* __restrict__ v, ScanRec* __restrict__ scan, ShadeRec* __restrict__ shade,
+    double lr_mu, double lr_color, double lr_scale, double lr_theta, double bc1, double bc2, double ibc1, double ibc2,
+    long long* __restrict__ status, TreeAcc ta) {
     pdl_wait();
-    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= n) return;
-    if (ta.acc) asm volatile("prefetch.global.L1 [%0];" ::"l"(ta.key + g));  // read at the very end
-    const uint32_t cntg = gcnt[g], og = goff[g];
-    // last reader of the counters/cursors: leave them zeroed for the next step
-    gcnt[g] = 0;
-    gcnt[n + g] = 0;
-    if (status[2] != LLONG_MAX) {
-        tree_acc_add(ta, g, scan[g]);  // every Gaussian is accumulated, updated or not
+    const uint32_t g0 = blockIdx.x * (blockDim.x / 2) + (threadIdx.x >> 1);
+    const int h = threadIdx.x & 1;
+    const bool live = g0 < n;
+    const uint32_t g = live ? g0 : n - 1;  // dead pairs shadow a live one (no writes) to keep shuffles full
+    uint32_t cntg = 0, og = 0;
+    if (h == 0) {
+        cntg = gcnt[g];
+        og = goff[g];
+    }
+    cntg = __shfl_sync(0xffffffffu, cntg, threadIdx.x & ~1);
+    og = __shfl_sync(0xffffffffu, og, threadIdx.x & ~1);
+    __syncwarp();
+    if (live && h == 0) {
+        gcnt[g] = 0;
+        gcnt[n + g] = 0;
+    }
+    const bool skip_all = status[2] != LLONG_MAX;
+    // gradient components 4h .. 4h+3
+    double G[4] = {0, 0, 0, 0};
+    if (!skip_all) {
+        if (cntg > kShortSeg) {
+            const double2* src = reinterpret_cast<const double2*>(grads + (size_t)g * 8 + 4 * h);
+            const double2 a = src[0], b = src[1];
+            G[0] = a.x; G[1] = a.y; G[2] = b.x; G[3] = b.y;
+        } else if (cntg > 0) {
+            uint32_t sl[kShortSeg];
+            uint32_t mseg = cntg;
+            for (uint32_t e = 0; e < mseg; ++e) {
+                const uint32_t val = perm[og + e];
+                uint32_t pos = e;
+                while (pos > 0 && sl[pos - 1] > val) {
+                    sl[pos] = sl[pos - 1];
+                    --pos;
+                }
+                sl[pos] = val;
+            }
+            for (uint32_t e = 0; e < mseg; ++e) {
+                const double2* c = reinterpret_cast<const double2*>(contrib + (size_t)sl[e] * 8 + 4 * h);
+                const double2 a = c[0], b = c[1];
+                G[0] = __dadd_rn(G[0], a.x);
+                G[1] = __dadd_rn(G[1], a.y);
+                G[2] = __dadd_rn(G[2], b.x);
+                G[3] = __dadd_rn(G[3], b.y);
+            }
+            if (live) {
+                double2* o2 = reinterpret_cast<double2*>(grads + (size_t)g * 8 + 4 * h);
+                o2[0] = make_double2(G[0], G[1]);
+                o2[1] = make_double2(G[2], G[3]);
+            }
+        } else if (live) {
+            double2* o2 = reinterpret_cast<double2*>(grads + (size_t)g * 8 + 4 * h);
+            o2[0] = make_double2(0.0, 0.0);
+            o2[1] = make_double2(0.0, 0.0);
+        }
+    }
+    // first non-finite gradient component of the pair (h = 0's first)
+    int badp = 8;
+    for (int j = 3; j >= 0; --j)
+        if (!isfinite(G[j])) badp = 4 * h + j;
+    const int other = __shfl_xor_sync(0xffffffffu, badp, 1);
+    const int firstbad = min(badp, other);
+    if (skip_all || firstbad < 8) {
+        if (live && h == 0) {
+            if (!skip_all) atomicMin(status, (long long)g * 8 + firstbad);
+            tree_acc_add(ta, g, scan[g]);
+        }
+        return;  // pair-uniform
+    }
+    const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
+    const double omb1 = 1.0 - b1, omb2 = 1.0 - b2;
+    const double2* P2 = reinterpret_cast<const double2*>(params + (size_t)g * 8 + 4 * h);
+    const double2* M2 = reinterpret_cast<const double2*>(m + (size_t)g * 8 + 4 * h);
+    const double2* V2 = reinterpret_cast<const double2*>(v + (size_t)g * 8 + 4 * h);
+    double gp[4], mm[4], vv[4];
+    {
+        const double2 p0 = P2[0], p1 = P2[1], m0 = M2[0], m1 = M2[1], v0 = V2[0], v1 = V2[1];
+        gp[0] = p0.x; gp[1] = p0.y; gp[2] = p1.x; gp[3] = p1.y;
+        mm[0] = m0.x; mm[1] = m0.y; mm[2] = m1.x; mm[3] = m1.y;
+        vv[0] = v0.x; vv[1] = v0.y; vv[2] = v1.x; vv[3] = v1.y;
+    }
+    const double lrh[4] = {h ? lr_scale : lr_mu, h ? lr_color : lr_mu, h ? lr_color : lr_theta,
+                           h ? lr_color : lr_scale};
+    bool fin = true;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        mm[j] = __dadd_rn(__dmul_rn(b1, mm[j]), __dmul_rn(omb1, G[j]));
+        vv[j] = __dadd_rn(__dmul_rn(b2, vv[j]), __dmul_rn(__dmul_rn(omb2, G[j]), G[j]));
+        const double m_hat = div_const(mm[j], bc1, ibc1);
+        const double v_hat = div_const(vv[j], bc2, ibc2);
+        const double upd = div_rn(__dmul_rn(lrh[j], m_hat), __dadd_rn(__dsqrt_rn(v_hat), eps));
+        gp[j] = __dsub_rn(gp[j], upd);
+        fin = fin && isfinite(gp[j]);
+    }
+    const bool fin_pair = __shfl_xor_sync(0xffffffffu, fin ? 1 : 0, 1) && fin;
+    if (!fin_pair) {
+        if (live && h == 0) {
+            atomicMin(status + 1, (long long)g);
+            tree_acc_add(ta, g, scan[g]);
+        }
         return;
     }
-    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (cntg > kShortSeg) {
-        const double2* G = reinterpret_cast<const double2*>(grads + (size_t)g * 8);
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-            const double2 b = G[h];
-            acc[2 * h] = b.x;
-            acc[2 * h + 1] = b.y;
-        }
+    // constrain (gaussian.cpp:74-90)
+    if (h == 0) {
+        gp[0] = clamp01d(gp[0]);
+        gp[1] = clamp01d(gp[1]);
+        double th = fmod(gp[2], kPi);
+        if (th < 0.0) th = __dadd_rn(th, kPi);
+        if (th >= kPi) th = 0.0;
+        gp[2] = th;
+        gp[3] = clamp_scale(gp[3]);
     } else {
-        sum_segment(contrib, perm, og, cntg, acc);
-        double2* o2 = reinterpret_cast<double2*>(grads + (size_t)g * 8);
-        o2[0] = make_double2(acc[0], acc[1]);
-        o2[1] = make_double2(acc[2], acc[3]);
-        o2[2] = make_double2(acc[4], acc[5]);
-        o2[3] = make_double2(acc[6], acc[7]);
+        gp[0] = clamp_scale(gp[0]);
+        gp[1] = clamp01d(gp[1]);
+        gp[2] = clamp01d(gp[2]);
+        gp[3] = clamp01d(gp[3]);
     }
-#pragma unroll
-    for (int p = 0; p < 8; ++p)
-        if (!isfinite(acc[p])) {
-            atomicMin(status, (long long)g * 8 + p);
-            tree_acc_add(ta, g, scan[g]);
-            return;
-        }
-    // (loading the parameters and moments only now keeps the register
-    // footprint of the reduction small: 3 CTAs per SM without spills in it)
-    double gp[8], mm[8], vv[8];
-    adam_load(g, params, m, v, gp, mm, vv);
-    adam_one(g, acc, gp, mm, vv, params, m, v, scan, shade, lr_mu, lr_color, lr_scale, lr_theta, bc1, bc2, ibc1, ibc2,
-             status, ta);
+    if (live) {
+        double2* Pw = reinterpret_cast<double2*>(params + (size_t)g * 8 + 4 * h);
+        double2* Mw = reinterpret_cast<double2*>(m + (size_t)g * 8 + 4 * h);
+        double2* Vw = reinterpret_cast<double2*>(v + (size_t)g * 8 + 4 * h);
+        Pw[0] = make_double2(gp[0], gp[1]);
+        Pw[1] = make_double2(gp[2], gp[3]);
+        Mw[0] = make_double2(mm[0], mm[1]);
+        Mw[1] = make_double2(mm[2], mm[3]);
+        Vw[0] = make_double2(vv[0], vv[1]);
+        Vw[1] = make_double2(vv[2], vv[3]);
+    }
+    // prepared records: h = 1 gets theta and forms sin/cos; h = 0 gets s2
+    // and forms both reciprocals
+    const double theta = shx(gp[2]);  // on h = 1: lane 0's theta
+    const double s2 = shx(gp[0]);     // on h = 0: lane 1's s2
+    double a = 0.0, b = 0.0;          // h = 0: inv_s1, inv_s2; h = 1: sin, cos
+    if (h == 0) {
+        a = __ddiv_rn(1.0, gp[3]);
+        b = __ddiv_rn(1.0, s2);
+    } else {
+        igs_math::cr_sincos(theta, &a, &b);
+    }
+    const double oa = shx(a), ob = shx(b);
+    if (!live) return;
+    if (h == 0) {
+        ScanRec r;
+        r.mu_x = gp[0];
+        r.mu_y = gp[1];
+        r.cos_t = ob;
+        r.sin_t = oa;
+        r.inv_a = __dmul_rn(a, a);
+        r.inv_b = __dmul_rn(b, b);
+        scan[g] = r;
+        tree_acc_add(ta, g, r);
+    } else {
+        ShadeRec hh;
+        hh.r = gp[1];
+        hh.g = gp[2];
+        hh.b = gp[3];
+        hh.inv_s1 = oa;
+        hh.inv_s2 = ob;
+        hh.pad = 0.0;
+        shade[g] = hh;
+    }
 }
+
 
 // Start of an iteration fed from host memory: resets the status block and
 // copies the sample indices straight from the pinned (device-mapped) host
@@ -832,7 +955,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
             ctx->params_version++;
             igs_prof_end(ctx, IGS_PROF_REDUCE, (double)items);
             igs_prof_begin(ctx, IGS_PROF_ADAM);
-            IGS_PDL(ctx, segment_adam_kernel, (n + 127) / 128, 128, 0, gcnt, (const uint32_t*)goff,
+            IGS_PDL(ctx, segment_adam_kernel, (n + 63) / 64, 128, 0, gcnt, (const uint32_t*)goff,
                     (const uint32_t*)perm, (const double*)contrib, n, ctx->grads, ctx->params, ctx->adam_m,
                     ctx->adam_v, ctx->scan, ctx->shade, fuse_lr4[0], fuse_lr4[1], fuse_lr4[2], fuse_lr4[3], bc1, bc2,
                     1.0 / bc1, 1.0 / bc2, ctx->status, ta);
