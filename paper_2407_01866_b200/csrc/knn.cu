@@ -1137,7 +1137,7 @@ int launch_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int 
     if (!grow(b.part, pitems * 12)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
     double* part_q = (double*)b.part.p;
     uint32_t* part_i = (uint32_t*)(part_q + pitems);
-    IGS_PDL(ctx, hard_scan_kernel<KCAP>, 2 * ctx->sm_count, kHardThreads, 0, (const ScanRec*)ctx->scan, ctx->n, uv,
+    IGS_PDL(ctx, hard_scan_kernel<KCAP>, ctx->sm_count, kHardThreads, 0, (const ScanRec*)ctx->scan, ctx->n, uv,
             W, H, kk, (const uint32_t*)hard_count, (const uint32_t*)hard_list, E, part_q, part_i,
             (unsigned int*)((uint32_t*)b.hard.p + 4 + kHardCap), igs_prof_counter(ctx, IGS_PROF_SCAN));
     igs_prof_end(ctx, IGS_PROF_SCAN, 0.0);
