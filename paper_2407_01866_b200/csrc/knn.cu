@@ -760,62 +760,70 @@ __global__ void __launch_bounds__(128, 9) knn_points_kernel(const ScanRec* __res
             eval_members(t, o, m, lane, scan, mem, px, py, evaluated);
         }
     }
+    // Each visited cell c: its subtree bound decides whether its children
+    // are visited (and it joins the frontier), its own bound -- when c lies
+    // outside the seed window at its level -- whether its own members are
+    // evaluated, in the same pass (a pruned subtree prunes its own members:
+    // own bound >= subtree bound).
     int ncur = 0;
     {
-        const int nls = 1 << (2 * s_lg[ls]);
+        const int lg = s_lg[ls], nls = 1 << (2 * lg);
         const uint32_t lo = (uint32_t)s_loff[ls];
+        const int sx = cx0 >> ls, sy = cy0 >> ls, Rl = ls == lfine ? R : 1;
         for (int b = 0; b < nls; b += 32) {
             const int node = b + lane;
-            const bool keep = node < nls && sum_lb(sub[lo + node], px, py) <= t.tq();
-            const unsigned msk = __ballot_sync(0xffffffffu, keep);
-            const int pos = ncur + __popc(msk & ((1u << lane) - 1));
-            if (keep) cur[pos] = (uint32_t)node;  // (at most 64 <= kQueue)
-            ncur += __popc(msk);
-        }
-        __syncwarp();
-    }
-    for (int l = ls; l >= 0 && ncur > 0; --l) {
-        const int lg = s_lg[l];
-        const int wmask = (1 << lg) - 1;
-        const int sx = cx0 >> l, sy = cy0 >> l;  // seed window centre
-        const uint32_t lo = (uint32_t)s_loff[l];
-        // own members of the frontier (outside the seed window)
-        for (int base = 0; base < ncur; base += 32) {
-            const int i = base + lane;
+            bool keep = false;
             uint32_t o = 0, m = 0;
-            if (i < ncur) {
-                const uint32_t node = cur[i];
-                const int x = (int)node & wmask, y = (int)(node >> lg);
-                const int Rl = l == lfine ? R : 1;  // the seed window at this level
-                if (abs(x - sx) > Rl || abs(y - sy) > Rl) {
-                    const uint32_t c = lo + node;
-                    const Sum so = own[c];
+            if (node < nls) {
+                keep = sum_lb(sub[lo + node], px, py) <= t.tq();
+                const int x = node & ((1 << lg) - 1), y = node >> lg;
+                if (keep && (abs(x - sx) > Rl || abs(y - sy) > Rl)) {
+                    const Sum so = own[lo + node];
                     if (so.count && sum_lb(so, px, py) <= t.tq()) {
-                        o = off[c];
+                        o = off[lo + node];
                         m = so.count;
                     }
                 }
             }
+            const unsigned msk = __ballot_sync(0xffffffffu, keep);
+            const int pos = ncur + __popc(msk & ((1u << lane) - 1));
+            if (keep) cur[pos] = (uint32_t)node;  // (at most 64 <= kQueue)
+            ncur += __popc(msk);
             eval_members(t, o, m, lane, scan, mem, px, py, evaluated);
         }
-        if (l == 0) break;
+        __syncwarp();
+    }
+    for (int l = ls; l > 0 && ncur > 0; --l) {
+        const int lg = s_lg[l];
+        const int wmask = (1 << lg) - 1;
         const uint32_t clo = (uint32_t)s_loff[l - 1];
         const int clg = lg + 1;
+        const int csx = cx0 >> (l - 1), csy = cy0 >> (l - 1);  // the children's seed window
+        const int cR = l - 1 == lfine ? R : 1;
         int nnext = 0;
         for (int base = 0; base < ncur * 4; base += 32) {
             const int item = base + lane;
             bool keep = false;
-            uint32_t child = 0;
+            uint32_t child = 0, o = 0, m = 0;
             if (item < ncur * 4) {
                 const uint32_t node = cur[item >> 2];
                 const uint32_t x = node & (uint32_t)wmask, y = node >> lg;
-                child = ((2 * y + ((item >> 1) & 1)) << clg) + 2 * x + (item & 1);
+                const uint32_t cx = 2 * x + (item & 1), cy = 2 * y + ((item >> 1) & 1);
+                child = (cy << clg) + cx;
                 keep = sum_lb(sub[clo + child], px, py) <= t.tq();
+                if (keep && (abs((int)cx - csx) > cR || abs((int)cy - csy) > cR)) {
+                    const Sum so = own[clo + child];
+                    if (so.count && sum_lb(so, px, py) <= t.tq()) {
+                        o = off[clo + child];
+                        m = so.count;
+                    }
+                }
             }
             const unsigned msk = __ballot_sync(0xffffffffu, keep);
             const int pos = nnext + __popc(msk & ((1u << lane) - 1));
             if (keep && pos < kQueue) nxt[pos] = child;
             nnext += __popc(msk);
+            eval_members(t, o, m, lane, scan, mem, px, py, evaluated);
         }
         __syncwarp();
         if (nnext > kQueue) {
