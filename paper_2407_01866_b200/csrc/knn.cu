@@ -655,12 +655,16 @@ __global__ void __launch_bounds__(128, 9) knn_points_kernel(const ScanRec* __res
     // lane j < npop: the j-th populated level (seed item it -> level of lane it / 9)
     const int my_pop = lane < npop ? __fns(lvmask, 0, lane + 1) : 0;
     const int lg0 = s_lg[0];
-    // persistent warps: pull points until none are left (no wave tail)
+    // persistent warps: pull points until none are left (no wave tail).
+    // Each warp's first point is its global warp index; later ones come from
+    // the cursor (offset by the warp count), claimed one point ahead so the
+    // atomic's latency overlaps the current point's search.
+    const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+    uint32_t claim = blockIdx.x * (blockDim.x >> 5) + warp;
     for (;;) {
-    uint32_t pt = 0;
-    if (lane == 0) pt = atomicAdd(next_point, 1u);
-    pt = __shfl_sync(0xffffffffu, pt, 0);
+    const uint32_t pt = __shfl_sync(0xffffffffu, claim, 0);
     if (pt >= npts) return;  // warp-uniform
+    if (lane == 0) claim = nwarps + atomicAdd(next_point, 1u);
     double px, py;
     point_of(uv, E, W, H, pt, px, py);
     WarpTopK t;
