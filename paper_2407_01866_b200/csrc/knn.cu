@@ -525,16 +525,21 @@ __device__ __forceinline__ double sign_of(double v) { return v > 0.0 ? 1.0 : (v 
 // + sample_gradients (renderer.cpp:91-122), one lane per selected entry.  The
 // blend sums run in entry order through a shuffle chain so every lane holds
 // the reference's exact sequential totals.
-__device__ __forceinline__ void warp_epilogue(const Epi& E, const ScanRec* __restrict__ scan, uint32_t pt, int kk,
-                                              int lane, double myq, uint32_t myi, double px, double py) {
+// WIDTH lanes per point (32, or 16 for two points per warp: the shuffles
+// stay inside each half); an inactive group (no point, or one handed to the
+// hard-point scan) joins the shuffles and writes nothing.
+template <int WIDTH>
+__device__ __forceinline__ void warp_epilogue(const Epi& E, const ScanRec* __restrict__ scan, uint32_t pt,
+                                              bool active, int kk, int lane, double myq, uint32_t myi, double px,
+                                              double py) {
     if (E.mode == 2) {
-        if (lane < kk) {
+        if (active && lane < kk) {
             E.oq[(size_t)pt * kk + lane] = myq;
             E.oi[(size_t)pt * kk + lane] = myi;
         }
         return;
     }
-    const bool live = lane < kk && myi != kNoIdx;
+    const bool live = active && lane < kk && myi != kNoIdx;
     double w = 0.0;
     ShadeRec h{};
     if (live) {
@@ -543,11 +548,11 @@ __device__ __forceinline__ void warp_epilogue(const Epi& E, const ScanRec* __res
     }
     double total = 0.0, ar = 0.0, ag = 0.0, ab = 0.0;
     for (int j = 0; j < kk; ++j) {
-        const double wj = __shfl_sync(0xffffffffu, w, j);
-        const double rj = __shfl_sync(0xffffffffu, h.r, j);
-        const double gj = __shfl_sync(0xffffffffu, h.g, j);
-        const double bj = __shfl_sync(0xffffffffu, h.b, j);
-        if (__shfl_sync(0xffffffffu, live ? 1 : 0, j)) {
+        const double wj = __shfl_sync(0xffffffffu, w, j, WIDTH);
+        const double rj = __shfl_sync(0xffffffffu, h.r, j, WIDTH);
+        const double gj = __shfl_sync(0xffffffffu, h.g, j, WIDTH);
+        const double bj = __shfl_sync(0xffffffffu, h.b, j, WIDTH);
+        if (__shfl_sync(0xffffffffu, live ? 1 : 0, j, WIDTH)) {
             total = __dadd_rn(total, wj);
             ar = __dadd_rn(ar, __dmul_rn(wj, rj));
             ag = __dadd_rn(ag, __dmul_rn(wj, gj));
@@ -558,11 +563,17 @@ __device__ __forceinline__ void warp_epilogue(const Epi& E, const ScanRec* __res
     const double c0 = __dmul_rn(ar, inv_denom), c1 = __dmul_rn(ag, inv_denom), c2 = __dmul_rn(ab, inv_denom);
     double up0, up1, up2;
     if (E.mode == 0) {
-        const float* t = E.target + (size_t)E.sidx[pt] * 3;
-        const double d0 = __dsub_rn(c0, (double)t[0]);
-        const double d1 = __dsub_rn(c1, (double)t[1]);
-        const double d2 = __dsub_rn(c2, (double)t[2]);
-        if (lane == 0) {
+        float t0 = 0.0f, t1 = 0.0f, t2 = 0.0f;
+        if (active) {
+            const float* t = E.target + (size_t)E.sidx[pt] * 3;
+            t0 = t[0];
+            t1 = t[1];
+            t2 = t[2];
+        }
+        const double d0 = __dsub_rn(c0, (double)t0);
+        const double d1 = __dsub_rn(c1, (double)t1);
+        const double d2 = __dsub_rn(c2, (double)t2);
+        if (active && lane == 0) {
             const double l = __dadd_rn(__dadd_rn(fabs(d0), fabs(d1)), fabs(d2));
             E.losses[pt] = l;
             if (!isfinite(l) && !E.defer_loss_check) atomicMin(E.status + 2, (long long)pt);
@@ -571,11 +582,12 @@ __device__ __forceinline__ void warp_epilogue(const Epi& E, const ScanRec* __res
         up1 = __dmul_rn(sign_of(d1), E.inv_n);
         up2 = __dmul_rn(sign_of(d2), E.inv_n);
     } else {
+        if (!active) return;  // nothing below is warp-collective
         up0 = E.samples5[(size_t)pt * 5 + 2];
         up1 = E.samples5[(size_t)pt * 5 + 3];
         up2 = E.samples5[(size_t)pt * 5 + 4];
     }
-    if (lane >= kk) return;
+    if (!active || lane >= kk) return;
     const size_t slot = (size_t)pt * kk + lane;
     if (!live) {
         if (E.keys) E.keys[slot] = E.n;  // sorts past every real index
@@ -871,7 +883,402 @@ __global__ void __launch_bounds__(128, 9) knn_points_kernel(const ScanRec* __res
         evaluated += n;
     }
     if (pairs && lane == 0) atomicAdd(pairs, evaluated);
-    warp_epilogue(E, scan, pt, kk, lane, t.q, t.i, px, py);
+    warp_epilogue<32>(E, scan, pt, true, kk, lane, t.q, t.i, px, py);
+    }  // persistent loop
+}
+
+// ---------------------------------------------------------------------------
+// Two points per warp (kk <= 16): each half-warp runs the search above for
+// its own point in 16-lane batches.  Every loop runs the larger of the two
+// halves' trip counts so the warp-wide votes and shuffles stay converged; a
+// half with nothing left feeds no-ops ((inf, kNoIdx) candidates, empty
+// cells).  Per point this halves the batch bookkeeping (votes, scans,
+// shuffles, the epilogue's blend chain), and a batch merge sorts 16
+// candidates instead of 32.  The selection is the same exact (q, idx) top-K.
+constexpr int kQueue16 = 256;   // per-half frontier capacity
+constexpr int kMergeMin16 = 8;  // candidates per half-batch from which merge() is used
+
+__device__ __forceinline__ unsigned half_bits(unsigned ballot) { return (ballot >> (threadIdx.x & 16)) & 0xffffu; }
+__device__ __forceinline__ int other_half(int v) { return __shfl_xor_sync(0xffffffffu, v, 16); }
+
+// WarpTopK on 16 lanes: lane hl < kk holds entry hl of its half's point
+struct HalfTopK {
+    double q;
+    uint32_t i;
+    double tq_;
+    uint32_t ti;
+    int kk, hl;
+
+    __device__ __forceinline__ void init(int kk_, int hl_) {
+        kk = kk_;
+        hl = hl_;
+        q = __longlong_as_double(0x7ff0000000000000LL);
+        i = kNoIdx;
+        tq_ = q;
+        ti = kNoIdx;
+    }
+    __device__ __forceinline__ double tq() const { return tq_; }
+    __device__ __forceinline__ bool beats(double cq, uint32_t ci) const {
+        return cq < tq_ || (cq == tq_ && ci < ti);
+    }
+    // (cq, ci) uniform within the half; one that beats no entry (including
+    // (inf, kNoIdx)) changes nothing; refresh() before tq()/beats()
+    __device__ __forceinline__ void push(double cq, uint32_t ci) {
+        const bool gt = hl < kk && (cq < q || (cq == q && ci < i));
+        const unsigned m = half_bits(__ballot_sync(0xffffffffu, gt));
+        const int pos = m ? __ffs(m) - 1 : 16;
+        const double pq = __shfl_up_sync(0xffffffffu, q, 1, 16);
+        const uint32_t pi = __shfl_up_sync(0xffffffffu, i, 1, 16);
+        if (hl == pos) {
+            q = cq;
+            i = ci;
+        } else if (hl > pos) {
+            q = pq;
+            i = pi;
+        }
+    }
+    __device__ __forceinline__ void refresh() {
+        tq_ = __shfl_sync(0xffffffffu, q, kk - 1, 16);
+        ti = __shfl_sync(0xffffffffu, i, kk - 1, 16);
+    }
+    // a half-batch (one candidate per lane, (inf, kNoIdx) for none): bitonic
+    // sort of 16, elementwise min against the reversed batch, four
+    // half-cleaner stages (WarpTopK::merge on 16 lanes)
+    __device__ __forceinline__ void merge(double cq, uint32_t ci) {
+#pragma unroll
+        for (int k = 2; k <= 16; k <<= 1)
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1) WarpTopK::cx(cq, ci, j, ((hl & j) == 0) == ((hl & k) == 0));
+        const double rq = __shfl_sync(0xffffffffu, cq, 15 - hl, 16);
+        const uint32_t ri = __shfl_sync(0xffffffffu, ci, 15 - hl, 16);
+        double lq = hl < kk ? q : __longlong_as_double(0x7ff0000000000000LL);
+        uint32_t li = hl < kk ? i : kNoIdx;
+        if (WarpTopK::lt(rq, ri, lq, li)) {
+            lq = rq;
+            li = ri;
+        }
+#pragma unroll
+        for (int j = 8; j > 0; j >>= 1) WarpTopK::cx(lq, li, j, (hl & j) == 0);
+        q = lq;
+        i = li;
+        refresh();
+    }
+};
+
+// eval_members on 16 lanes per point (lane hl: cell range [o, o + m))
+__device__ __forceinline__ void eval_members16(HalfTopK& t, uint32_t o_mine, uint32_t m_mine, int hl,
+                                               const ScanRec* __restrict__ scan, const uint32_t* __restrict__ mem,
+                                               double px, double py, unsigned long long& evaluated) {
+    if (__ballot_sync(0xffffffffu, m_mine != 0) == 0) return;  // nothing in either half (common)
+    uint32_t incl = m_mine;
+#pragma unroll
+    for (int d = 1; d < 16; d <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d, 16);
+        if (hl >= d) incl += v;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 15, 16);
+    const uint32_t excl = incl - m_mine;
+    evaluated += total;
+    const uint32_t tmax = max(total, (uint32_t)other_half((int)total));
+    for (uint32_t base = 0; base < tmax; base += 16) {
+        const uint32_t f = base + hl;
+        int lo = 0;
+#pragma unroll
+        for (int step = 8; step > 0; step >>= 1) {
+            const uint32_t ex = __shfl_sync(0xffffffffu, excl, lo + step, 16);
+            if (ex <= f) lo += step;
+        }
+        const uint32_t lo_ex = __shfl_sync(0xffffffffu, excl, lo, 16);
+        const uint32_t lo_o = __shfl_sync(0xffffffffu, o_mine, lo, 16);
+        double q = __longlong_as_double(0x7ff0000000000000LL);
+        uint32_t gi = kNoIdx;
+        bool cand = false;
+        if (f < total) {
+            gi = __ldg(mem + lo_o + (f - lo_ex));
+            q = maha(scan[gi], px, py);
+            cand = t.beats(q, gi);
+        }
+        unsigned mh = half_bits(__ballot_sync(0xffffffffu, cand));
+        const int np = __popc(mh), npmax = max(np, other_half(np));
+        if (npmax >= kMergeMin16) {
+            t.merge(cand ? q : __longlong_as_double(0x7ff0000000000000LL), cand ? gi : kNoIdx);
+        } else if (npmax) {
+            for (int r = 0; r < npmax; ++r) {
+                const int src = mh ? __ffs(mh) - 1 : 0;
+                mh &= mh - 1;
+                double qq = __shfl_sync(0xffffffffu, q, src, 16);
+                uint32_t ii = __shfl_sync(0xffffffffu, gi, src, 16);
+                if (r >= np) {
+                    qq = __longlong_as_double(0x7ff0000000000000LL);
+                    ii = kNoIdx;
+                }
+                t.push(qq, ii);
+            }
+            t.refresh();
+        }
+    }
+}
+
+__global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __restrict__ scan, uint32_t n, Lq L,
+                                                              const Sum* __restrict__ own,
+                                                              const Sum* __restrict__ sub,
+                                                              const uint32_t* __restrict__ off,
+                                                              const uint32_t* __restrict__ mem,
+                                                              const double* __restrict__ uv, int W, int H,
+                                                              uint32_t npts, int kk, Epi E,
+                                                              unsigned long long* __restrict__ pairs,
+                                                              uint32_t* __restrict__ hard_count,
+                                                              uint32_t* __restrict__ hard_list,
+                                                              unsigned long long* __restrict__ hard_stat,
+                                                              uint32_t* __restrict__ next_point,
+                                                              uint32_t* __restrict__ zero_next) {
+    __shared__ uint32_t queue[4][2][2][kQueue16];
+    __shared__ int s_loff[kMaxLv];
+    __shared__ int s_lg[kMaxLv];
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int l = 0; l < kMaxLv; ++l) {
+            s_loff[l] = L.loff[l];
+            s_lg[l] = 31 - __clz(max(L.lw[l], 1));
+        }
+    }
+    __syncthreads();
+    pdl_wait();
+    if (blockIdx.x == 0 && threadIdx.x < 2) zero_next[threadIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 2 && E.zero_word) *E.zero_word = 0;
+    prefetch_l2(E.pf, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int hl = lane & 15, hh = lane >> 4;
+    unsigned lvmask = 0;
+    if (lane < L.levels && L.lcount[lane] > 0) lvmask = 1u;
+    lvmask = __ballot_sync(0xffffffffu, lvmask);
+    const int npop = __popc(lvmask);
+    const int my_pop = hl < npop ? __fns(lvmask, 0, hl + 1) : 0;
+    const int lg0 = s_lg[0];
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    // persistent warps over point pairs (2c, 2c + 1), claimed as in
+    // knn_points_kernel
+    const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+    uint32_t claim = blockIdx.x * (blockDim.x >> 5) + warp;
+    for (;;) {
+    const uint32_t pair = __shfl_sync(0xffffffffu, claim, 0);
+    if (pair >= (npts + 1) / 2) return;  // warp-uniform
+    if (lane == 0) claim = nwarps + atomicAdd(next_point, 1u);
+    const uint32_t pt = 2 * pair + hh;
+    const bool active = pt < npts;  // the second half of an odd tail searches a dummy point
+    double px = 0.5, py = 0.5;
+    if (active) point_of(uv, E, W, H, pt, px, py);
+    HalfTopK t;
+    t.init(kk, hl);
+    unsigned long long evaluated = 0;
+
+    // (1) seeds, as knn_points_kernel
+    const int nseed = npop * 9;
+    const int lfine = __ffs(lvmask) - 1;
+    const int cx0 = cell_of(px, 1 << lg0), cy0 = cell_of(py, 1 << lg0);
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int base = 0; base < nseed; base += 16) {
+            const int it = base + hl;
+            const int l = __shfl_sync(0xffffffffu, my_pop, min(it / 9, 15), 16);
+            uint32_t o = 0, m = 0;
+            if (it < nseed) {
+                const int d = it % 9, lg = s_lg[l], G = 1 << lg;
+                const int x = (cx0 >> l) + d % 3 - 1, y = (cy0 >> l) + d / 3 - 1;
+                const bool primary = d == 4 || l == lfine;
+                if (x >= 0 && x < G && y >= 0 && y < G && primary == (pass == 0)) {
+                    const uint32_t c = (uint32_t)(s_loff[l] + (y << lg) + x);
+                    if (primary) {
+                        o = off[c];
+                        m = own[c].count;
+                    } else {
+                        const Sum so = own[c];
+                        if (so.count && sum_lb(so, px, py) <= t.tq()) {
+                            o = off[c];
+                            m = so.count;
+                        }
+                    }
+                }
+            }
+            eval_members16(t, o, m, hl, scan, mem, px, py, evaluated);
+        }
+    }
+
+    // (1b) ring widening at the finest level while a half has no threshold
+    int R = 1;
+    for (;;) {
+        const bool need = !(t.tq() < inf) && R < kSeedRMax;
+        if (__ballot_sync(0xffffffffu, need) == 0) break;
+        if (need) ++R;
+        const int nring = need ? 8 * R : 0;
+        const int nmax = max(nring, other_half(nring));
+        const int lg = s_lg[lfine], G = 1 << lg, sx = cx0 >> lfine, sy = cy0 >> lfine;
+        for (int b = 0; b < nmax; b += 16) {
+            const int it = b + hl;
+            uint32_t o = 0, m = 0;
+            if (it < nring) {
+                const int x = sx + ring_dx(it, R), y = sy + ring_dy(it, R);
+                if (x >= 0 && x < G && y >= 0 && y < G) {
+                    const uint32_t c = (uint32_t)(s_loff[lfine] + (y << lg) + x);
+                    o = off[c];
+                    m = own[c].count;
+                }
+            }
+            eval_members16(t, o, m, hl, scan, mem, px, py, evaluated);
+        }
+    }
+
+    // (2) descent, as knn_points_kernel (flat start at ls, one pass per level)
+    bool overflow = false;
+    uint32_t* cur = queue[warp][hh][0];
+    uint32_t* nxt = queue[warp][hh][1];
+    const int ls = min(L.levels - 1, max(lg0 - 3, 0));
+    {
+        const uint32_t c0 = ls + 1 < L.levels ? (uint32_t)s_loff[ls + 1] : 0u;
+        const uint32_t nup = ls + 1 < L.levels ? (uint32_t)(s_loff[L.levels - 1] + 1) - c0 : 0u;
+        for (uint32_t b = 0; b < nup; b += 16) {
+            const uint32_t c = c0 + b + hl;
+            uint32_t o = 0, m = 0;
+            if (b + hl < nup) {
+                int l = ls + 1;
+                while (l + 1 < L.levels && (uint32_t)s_loff[l + 1] <= c) ++l;
+                const int lg = s_lg[l];
+                const int node = (int)(c - (uint32_t)s_loff[l]);
+                const int x = node & ((1 << lg) - 1), y = node >> lg;
+                const int Rl = l == lfine ? R : 1;
+                if (abs(x - (cx0 >> l)) > Rl || abs(y - (cy0 >> l)) > Rl) {
+                    const Sum so = own[c];
+                    if (so.count && sum_lb(so, px, py) <= t.tq()) {
+                        o = off[c];
+                        m = so.count;
+                    }
+                }
+            }
+            eval_members16(t, o, m, hl, scan, mem, px, py, evaluated);
+        }
+    }
+    int ncur = 0;
+    {
+        const int lg = s_lg[ls], nls = 1 << (2 * lg);
+        const uint32_t lo = (uint32_t)s_loff[ls];
+        const int sx = cx0 >> ls, sy = cy0 >> ls, Rl = ls == lfine ? R : 1;
+        for (int b = 0; b < nls; b += 16) {
+            const int node = b + hl;
+            bool keep = false;
+            uint32_t o = 0, m = 0;
+            if (node < nls) {
+                keep = sum_lb(sub[lo + node], px, py) <= t.tq();
+                const int x = node & ((1 << lg) - 1), y = node >> lg;
+                if (keep && (abs(x - sx) > Rl || abs(y - sy) > Rl)) {
+                    const Sum so = own[lo + node];
+                    if (so.count && sum_lb(so, px, py) <= t.tq()) {
+                        o = off[lo + node];
+                        m = so.count;
+                    }
+                }
+            }
+            const unsigned mh = half_bits(__ballot_sync(0xffffffffu, keep));
+            const int pos = ncur + __popc(mh & ((1u << hl) - 1));
+            if (keep) cur[pos] = (uint32_t)node;  // (at most 64 <= kQueue16)
+            ncur += __popc(mh);
+            eval_members16(t, o, m, hl, scan, mem, px, py, evaluated);
+        }
+        __syncwarp();
+    }
+    for (int l = ls; l > 0; --l) {
+        if (__ballot_sync(0xffffffffu, ncur > 0) == 0) break;
+        const int lg = s_lg[l];
+        const int wmask = (1 << lg) - 1;
+        const uint32_t clo = (uint32_t)s_loff[l - 1];
+        const int clg = lg + 1;
+        const int csx = cx0 >> (l - 1), csy = cy0 >> (l - 1);
+        const int cR = l - 1 == lfine ? R : 1;
+        int nnext = 0;
+        const int items = ncur * 4, imax = max(items, other_half(items));
+        for (int base = 0; base < imax; base += 16) {
+            const int item = base + hl;
+            bool keep = false;
+            uint32_t child = 0, o = 0, m = 0;
+            if (item < items) {
+                const uint32_t node = cur[item >> 2];
+                const uint32_t x = node & (uint32_t)wmask, y = node >> lg;
+                const uint32_t cx = 2 * x + (item & 1), cy = 2 * y + ((item >> 1) & 1);
+                child = (cy << clg) + cx;
+                keep = sum_lb(sub[clo + child], px, py) <= t.tq();
+                if (keep && (abs((int)cx - csx) > cR || abs((int)cy - csy) > cR)) {
+                    const Sum so = own[clo + child];
+                    if (so.count && sum_lb(so, px, py) <= t.tq()) {
+                        o = off[clo + child];
+                        m = so.count;
+                    }
+                }
+            }
+            const unsigned mh = half_bits(__ballot_sync(0xffffffffu, keep));
+            const int pos = nnext + __popc(mh & ((1u << hl) - 1));
+            if (keep && pos < kQueue16) nxt[pos] = child;
+            nnext += __popc(mh);
+            eval_members16(t, o, m, hl, scan, mem, px, py, evaluated);
+        }
+        __syncwarp();
+        if (nnext > kQueue16) {  // this half stops; the other goes on
+            overflow = true;
+            nnext = 0;
+        }
+        uint32_t* tmp = cur;
+        cur = nxt;
+        nxt = tmp;
+        ncur = nnext;
+    }
+
+    // frontier overflow: the hard-point scan, or (beyond its capacity) all N here
+    bool handed = false;
+    if (__ballot_sync(0xffffffffu, overflow && active)) {
+        const bool mine = overflow && active;
+        uint32_t slot = 0;
+        if (mine && hl == 0) {
+            slot = atomicAdd(hard_count, 1u);
+            if (hard_stat) atomicAdd(hard_stat, 1ull);
+        }
+        slot = __shfl_sync(0xffffffffu, slot, 0, 16);
+        bool brute = false;
+        if (mine) {
+            if (slot < kHardCap) {
+                if (hl == 0) hard_list[slot] = pt;
+                handed = true;
+            } else {
+                brute = true;
+                t.init(kk, hl);
+            }
+        }
+        if (__ballot_sync(0xffffffffu, brute)) {
+            for (uint32_t base = 0; base < n; base += 16) {
+                const uint32_t gi = base + hl;
+                double q = inf;
+                bool cand = false;
+                if (brute && gi < n) {
+                    q = maha(scan[gi], px, py);
+                    cand = t.beats(q, gi);
+                }
+                unsigned mh = half_bits(__ballot_sync(0xffffffffu, cand));
+                const int np = __popc(mh), npmax = max(np, other_half(np));
+                for (int r = 0; r < npmax; ++r) {
+                    const int src = mh ? __ffs(mh) - 1 : 0;
+                    mh &= mh - 1;
+                    double qq = __shfl_sync(0xffffffffu, q, src, 16);
+                    uint32_t ii = base + src;
+                    if (r >= np || !t.beats(qq, ii)) {
+                        qq = inf;
+                        ii = kNoIdx;
+                    }
+                    t.push(qq, ii);
+                    t.refresh();
+                }
+            }
+            if (brute) evaluated += n;
+        }
+    }
+    if (pairs && active && hl == 0) atomicAdd(pairs, evaluated);
+    warp_epilogue<16>(E, scan, pt, active && !handed, kk, hl, t.q, t.i, px, py);
     }  // persistent loop
 }
 
@@ -909,7 +1316,7 @@ __device__ __forceinline__ void hard_merge_point(const ScanRec* __restrict__ sca
         }
     }
     if (pairs && lane == 0) atomicAdd(pairs, (unsigned long long)n);
-    warp_epilogue(E, scan, pt, kk, lane, t.q, t.i, px, py);
+    warp_epilogue<32>(E, scan, pt, true, kk, lane, t.q, t.i, px, py);
 }
 
 template <int KCAP>
@@ -1010,7 +1417,7 @@ __global__ void __launch_bounds__(kHardThreads) hard_scan_kernel(const ScanRec* 
 struct KnnBufs {
     DevBuf cnt, off, key, mem, own, sub, cub_tmp, hard, ticket, part, lcount, acc;
     int hard_phase = 0;  // which (hard count, cursor) pair the next search uses
-    int knn_blocks = 0;  // resident CTAs for the persistent query kernel
+    int knn_blocks[2] = {0, 0};  // resident CTAs for the persistent query kernels (full warp, halves)
     uint64_t version = ~0ull;  // params_version the summaries describe
     // refit chain: Adam launches accumulated every Gaussian into acc (by its
     // cell at the last rebuild) for each params version up to `chain`
@@ -1135,16 +1542,21 @@ int launch_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int 
     uint32_t* hard_list = (uint32_t*)b.hard.p + 4;
     b.hard_phase ^= 1;
     igs_prof_begin(ctx, IGS_PROF_SCAN);
-    if (b.knn_blocks == 0) {
+    // kk <= 16: two points per warp (knn_points16_kernel)
+    const bool halves = kk <= 16 && !getenv("IGS_KNN_FULLWARP");  // (A/B switch for tests and profiling)
+    if (b.knn_blocks[halves] == 0) {
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, knn_points_kernel, 128, 0);
-        b.knn_blocks = std::max(1, per_sm) * ctx->sm_count;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, halves ? knn_points16_kernel : knn_points_kernel,
+                                                      128, 0);
+        b.knn_blocks[halves] = std::max(1, per_sm) * ctx->sm_count;
     }
-    const unsigned blocks = (unsigned)std::min<uint64_t>(b.knn_blocks, ((uint64_t)npts + 3) / 4);
-    IGS_PDL(ctx, knn_points_kernel, blocks, 128, 0, (const ScanRec*)ctx->scan, ctx->n, b.lq, (const Sum*)b.own.p,
-            (const Sum*)b.sub.p, (const uint32_t*)b.off.p, (const uint32_t*)b.mem.p, uv, W, H, npts, kk, E,
-            igs_prof_counter(ctx, IGS_PROF_SCAN), hard_count, hard_list, igs_prof_counter(ctx, IGS_PROF_KNN_HARD),
-            cursor, zero_next);
+    const uint64_t per_block = halves ? 8 : 4;
+    const unsigned blocks =
+        (unsigned)std::min<uint64_t>(b.knn_blocks[halves], ((uint64_t)npts + per_block - 1) / per_block);
+    IGS_PDL(ctx, halves ? knn_points16_kernel : knn_points_kernel, blocks, 128, 0, (const ScanRec*)ctx->scan, ctx->n,
+            b.lq, (const Sum*)b.own.p, (const Sum*)b.sub.p, (const uint32_t*)b.off.p, (const uint32_t*)b.mem.p, uv,
+            W, H, npts, kk, E, igs_prof_counter(ctx, IGS_PROF_SCAN), hard_count, hard_list,
+            igs_prof_counter(ctx, IGS_PROF_KNN_HARD), cursor, zero_next);
     const size_t pitems = (size_t)kHardCap * kHardSplit * kk;
     if (!grow(b.part, pitems * 12)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
     double* part_q = (double*)b.part.p;
