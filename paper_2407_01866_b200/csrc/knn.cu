@@ -687,23 +687,32 @@ __global__ void __launch_bounds__(128, 9) knn_points_kernel(const ScanRec* __res
     // Pass 0 evaluates the point's own cell at each level and the whole
     // window at the finest populated level (a tight threshold at once);
     // pass 1 evaluates the other window cells whose own bound survives it.
-    const int nseed = npop * 9;
     const int lfine = __ffs(lvmask) - 1;
     // the point's cell at level 0; at level l it is (cx0 >> l, cy0 >> l)
     // (G_l = G0 >> l, so floor(v G_l) = floor(v G0) >> l)
     const int cx0 = cell_of(px, 1 << lg0), cy0 = cell_of(py, 1 << lg0);
     for (int pass = 0; pass < 2; ++pass) {
-        for (int base = 0; base < nseed; base += 32) {
+        // pass 0: the 9 finest-level cells, then the own cell at each other
+        // populated level; pass 1: the 8 other window cells at those levels
+        const int nitems = pass == 0 ? 8 + npop : 8 * (npop - 1);
+        for (int base = 0; base < nitems; base += 32) {
             const int it = base + lane;
-            const int l = __shfl_sync(0xffffffffu, my_pop, min(it / 9, 31));
+            int k, d;
+            if (pass == 0) {
+                k = it < 9 ? 0 : it - 8;
+                d = it < 9 ? it : 4;
+            } else {
+                k = 1 + it / 8;
+                d = it % 8 + (it % 8 >= 4);
+            }
+            const int l = __shfl_sync(0xffffffffu, my_pop, min(k, 31));
             uint32_t o = 0, m = 0;
-            if (it < nseed) {
-                const int d = it % 9, lg = s_lg[l], G = 1 << lg;
+            if (it < nitems) {
+                const int lg = s_lg[l], G = 1 << lg;
                 const int x = (cx0 >> l) + d % 3 - 1, y = (cy0 >> l) + d / 3 - 1;
-                const bool primary = d == 4 || l == lfine;
-                if (x >= 0 && x < G && y >= 0 && y < G && primary == (pass == 0)) {
+                if (x >= 0 && x < G && y >= 0 && y < G) {
                     const uint32_t c = (uint32_t)(s_loff[l] + (y << lg) + x);
-                    if (primary) {
+                    if (pass == 0) {
                         o = off[c];
                         m = own[c].count;
                     } else {
@@ -896,7 +905,7 @@ __global__ void __launch_bounds__(128, 9) knn_points_kernel(const ScanRec* __res
 // shuffles, the epilogue's blend chain), and a batch merge sorts 16
 // candidates instead of 32.  The selection is the same exact (q, idx) top-K.
 constexpr int kQueue16 = 256;   // per-half frontier capacity
-constexpr int kMergeMin16 = 8;  // candidates per half-batch from which merge() is used
+constexpr int kMergeMin16 = 5;  // candidates per half-batch from which merge() is used
 
 __device__ __forceinline__ unsigned half_bits(unsigned ballot) { return (ballot >> (threadIdx.x & 16)) & 0xffffu; }
 __device__ __forceinline__ int other_half(int v) { return __shfl_xor_sync(0xffffffffu, v, 16); }
@@ -1069,26 +1078,37 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
     const bool active = pt < npts;  // the second half of an odd tail searches a dummy point
     double px = 0.5, py = 0.5;
     if (active) point_of(uv, E, W, H, pt, px, py);
+    if (active && E.mode == 0) {  // the target pixel the epilogue reads
+        const float* tp = E.target + (size_t)E.sidx[pt] * 3;
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(tp));
+    }
     HalfTopK t;
     t.init(kk, hl);
     unsigned long long evaluated = 0;
 
     // (1) seeds, as knn_points_kernel
-    const int nseed = npop * 9;
     const int lfine = __ffs(lvmask) - 1;
     const int cx0 = cell_of(px, 1 << lg0), cy0 = cell_of(py, 1 << lg0);
     for (int pass = 0; pass < 2; ++pass) {
-        for (int base = 0; base < nseed; base += 16) {
+        const int nitems = pass == 0 ? 8 + npop : 8 * (npop - 1);
+        for (int base = 0; base < nitems; base += 16) {
             const int it = base + hl;
-            const int l = __shfl_sync(0xffffffffu, my_pop, min(it / 9, 15), 16);
+            int k, d;
+            if (pass == 0) {
+                k = it < 9 ? 0 : it - 8;
+                d = it < 9 ? it : 4;
+            } else {
+                k = 1 + it / 8;
+                d = it % 8 + (it % 8 >= 4);
+            }
+            const int l = __shfl_sync(0xffffffffu, my_pop, min(k, 15), 16);
             uint32_t o = 0, m = 0;
-            if (it < nseed) {
-                const int d = it % 9, lg = s_lg[l], G = 1 << lg;
+            if (it < nitems) {
+                const int lg = s_lg[l], G = 1 << lg;
                 const int x = (cx0 >> l) + d % 3 - 1, y = (cy0 >> l) + d / 3 - 1;
-                const bool primary = d == 4 || l == lfine;
-                if (x >= 0 && x < G && y >= 0 && y < G && primary == (pass == 0)) {
+                if (x >= 0 && x < G && y >= 0 && y < G) {
                     const uint32_t c = (uint32_t)(s_loff[l] + (y << lg) + x);
-                    if (primary) {
+                    if (pass == 0) {
                         o = off[c];
                         m = own[c].count;
                     } else {
@@ -1132,7 +1152,7 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
     bool overflow = false;
     uint32_t* cur = queue[warp][hh][0];
     uint32_t* nxt = queue[warp][hh][1];
-    const int ls = min(L.levels - 1, max(lg0 - 3, 0));
+    const int ls = min(L.levels - 1, max(lg0 - 2, 0));
     {
         const uint32_t c0 = ls + 1 < L.levels ? (uint32_t)s_loff[ls + 1] : 0u;
         const uint32_t nup = ls + 1 < L.levels ? (uint32_t)(s_loff[L.levels - 1] + 1) - c0 : 0u;
@@ -1179,7 +1199,7 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
             }
             const unsigned mh = half_bits(__ballot_sync(0xffffffffu, keep));
             const int pos = ncur + __popc(mh & ((1u << hl) - 1));
-            if (keep) cur[pos] = (uint32_t)node;  // (at most 64 <= kQueue16)
+            if (keep) cur[pos] = (uint32_t)node;  // (at most 16 <= kQueue16)
             ncur += __popc(mh);
             eval_members16(t, o, m, hl, scan, mem, px, py, evaluated);
         }
