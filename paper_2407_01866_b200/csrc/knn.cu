@@ -112,13 +112,17 @@ __global__ void lq_clear(uint32_t cells, uint32_t* __restrict__ cnt2, Acc* __res
 
 __global__ void lq_fill(const ScanRec* __restrict__ scan, uint32_t n, const uint32_t* __restrict__ key,
                         const uint32_t* __restrict__ off, uint32_t* __restrict__ cur, uint32_t* __restrict__ mem,
-                        Acc* __restrict__ acc) {
+                        ScanRec* __restrict__ mrec, uint32_t* __restrict__ minv, Acc* __restrict__ acc) {
     pdl_wait();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t k = key[i] & kKeyCellMask;
-    mem[off[k] + atomicAdd(cur + k, 1u)] = i;
-    acc_add(acc + k, scan[i]);
+    const uint32_t pos = off[k] + atomicAdd(cur + k, 1u);
+    const ScanRec r = scan[i];
+    mem[pos] = i;
+    mrec[pos] = r;  // the records in member order (the searches' evaluation stream)
+    minv[i] = pos;
+    acc_add(acc + k, r);
 }
 
 __device__ __forceinline__ Sum empty_sum() {
@@ -428,7 +432,7 @@ constexpr int kMergeMin = 8;  // candidates per batch from which merge() beats s
 // flattened so that all lanes work on members.
 template <class TK>
 __device__ __forceinline__ void eval_members(TK& t, uint32_t o_mine, uint32_t m_mine, int lane,
-                                             const ScanRec* __restrict__ scan, const uint32_t* __restrict__ mem,
+                                             const ScanRec* __restrict__ mrec, const uint32_t* __restrict__ mem,
                                              double px, double py, unsigned long long& evaluated) {
     if (__ballot_sync(0xffffffffu, m_mine != 0) == 0) return;  // nothing to evaluate (common)
     uint32_t incl = m_mine;
@@ -456,8 +460,9 @@ __device__ __forceinline__ void eval_members(TK& t, uint32_t o_mine, uint32_t m_
         uint32_t gi = kNoIdx;
         bool cand = false;
         if (f < total) {
-            gi = __ldg(mem + lo_o + (f - lo_ex));
-            q = maha(scan[gi], px, py);
+            const uint32_t p = lo_o + (f - lo_ex);  // records in member order: no dependent gather
+            gi = __ldg(mem + p);
+            q = maha(mrec[p], px, py);
             cand = t.beats(q, gi);
         }
         unsigned msk = __ballot_sync(0xffffffffu, cand);
@@ -632,7 +637,7 @@ __device__ __forceinline__ void warp_epilogue(const Epi& E, const ScanRec* __res
 __global__ void __launch_bounds__(128, 9) knn_points_kernel(const ScanRec* __restrict__ scan, uint32_t n, Lq L,
                                                             const Sum* __restrict__ own, const Sum* __restrict__ sub,
                                                             const uint32_t* __restrict__ off,
-                                                            const uint32_t* __restrict__ mem,
+                                                            const uint32_t* __restrict__ mem, const ScanRec* __restrict__ mrec,
                                                             const double* __restrict__ uv, int W, int H, uint32_t npts,
                                                             int kk, Epi E, unsigned long long* __restrict__ pairs,
                                                             uint32_t* __restrict__ hard_count,
@@ -724,7 +729,7 @@ __global__ void __launch_bounds__(128, 9) knn_points_kernel(const ScanRec* __res
                     }
                 }
             }
-            eval_members(t, o, m, lane, scan, mem, px, py, evaluated);
+            eval_members(t, o, m, lane, mrec, mem, px, py, evaluated);
         }
     }
 
@@ -746,7 +751,7 @@ __global__ void __launch_bounds__(128, 9) knn_points_kernel(const ScanRec* __res
                     m = own[c].count;
                 }
             }
-            eval_members(t, o, m, lane, scan, mem, px, py, evaluated);
+            eval_members(t, o, m, lane, mrec, mem, px, py, evaluated);
         }
     }
 
@@ -782,7 +787,7 @@ __global__ void __launch_bounds__(128, 9) knn_points_kernel(const ScanRec* __res
                     }
                 }
             }
-            eval_members(t, o, m, lane, scan, mem, px, py, evaluated);
+            eval_members(t, o, m, lane, mrec, mem, px, py, evaluated);
         }
     }
     // Each visited cell c: its subtree bound decides whether its children
@@ -814,7 +819,7 @@ __global__ void __launch_bounds__(128, 9) knn_points_kernel(const ScanRec* __res
             const int pos = ncur + __popc(msk & ((1u << lane) - 1));
             if (keep) cur[pos] = (uint32_t)node;  // (at most 64 <= kQueue)
             ncur += __popc(msk);
-            eval_members(t, o, m, lane, scan, mem, px, py, evaluated);
+            eval_members(t, o, m, lane, mrec, mem, px, py, evaluated);
         }
         __syncwarp();
     }
@@ -848,7 +853,7 @@ __global__ void __launch_bounds__(128, 9) knn_points_kernel(const ScanRec* __res
             const int pos = nnext + __popc(msk & ((1u << lane) - 1));
             if (keep && pos < kQueue) nxt[pos] = child;
             nnext += __popc(msk);
-            eval_members(t, o, m, lane, scan, mem, px, py, evaluated);
+            eval_members(t, o, m, lane, mrec, mem, px, py, evaluated);
         }
         __syncwarp();
         if (nnext > kQueue) {
@@ -976,7 +981,7 @@ struct HalfTopK {
 
 // eval_members on 16 lanes per point (lane hl: cell range [o, o + m))
 __device__ __forceinline__ void eval_members16(HalfTopK& t, uint32_t o_mine, uint32_t m_mine, int hl,
-                                               const ScanRec* __restrict__ scan, const uint32_t* __restrict__ mem,
+                                               const ScanRec* __restrict__ mrec, const uint32_t* __restrict__ mem,
                                                double px, double py, unsigned long long& evaluated) {
     if (__ballot_sync(0xffffffffu, m_mine != 0) == 0) return;  // nothing in either half (common)
     uint32_t incl = m_mine;
@@ -1003,8 +1008,9 @@ __device__ __forceinline__ void eval_members16(HalfTopK& t, uint32_t o_mine, uin
         uint32_t gi = kNoIdx;
         bool cand = false;
         if (f < total) {
-            gi = __ldg(mem + lo_o + (f - lo_ex));
-            q = maha(scan[gi], px, py);
+            const uint32_t p = lo_o + (f - lo_ex);  // records in member order: no dependent gather
+            gi = __ldg(mem + p);
+            q = maha(mrec[p], px, py);
             cand = t.beats(q, gi);
         }
         unsigned mh = half_bits(__ballot_sync(0xffffffffu, cand));
@@ -1032,7 +1038,7 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
                                                               const Sum* __restrict__ own,
                                                               const Sum* __restrict__ sub,
                                                               const uint32_t* __restrict__ off,
-                                                              const uint32_t* __restrict__ mem,
+                                                              const uint32_t* __restrict__ mem, const ScanRec* __restrict__ mrec,
                                                               const double* __restrict__ uv, int W, int H,
                                                               uint32_t npts, int kk, Epi E,
                                                               unsigned long long* __restrict__ pairs,
@@ -1120,7 +1126,7 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
                     }
                 }
             }
-            eval_members16(t, o, m, hl, scan, mem, px, py, evaluated);
+            eval_members16(t, o, m, hl, mrec, mem, px, py, evaluated);
         }
     }
 
@@ -1144,7 +1150,7 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
                     m = own[c].count;
                 }
             }
-            eval_members16(t, o, m, hl, scan, mem, px, py, evaluated);
+            eval_members16(t, o, m, hl, mrec, mem, px, py, evaluated);
         }
     }
 
@@ -1174,7 +1180,7 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
                     }
                 }
             }
-            eval_members16(t, o, m, hl, scan, mem, px, py, evaluated);
+            eval_members16(t, o, m, hl, mrec, mem, px, py, evaluated);
         }
     }
     int ncur = 0;
@@ -1201,7 +1207,7 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
             const int pos = ncur + __popc(mh & ((1u << hl) - 1));
             if (keep) cur[pos] = (uint32_t)node;  // (at most 16 <= kQueue16)
             ncur += __popc(mh);
-            eval_members16(t, o, m, hl, scan, mem, px, py, evaluated);
+            eval_members16(t, o, m, hl, mrec, mem, px, py, evaluated);
         }
         __syncwarp();
     }
@@ -1237,7 +1243,7 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
             const int pos = nnext + __popc(mh & ((1u << hl) - 1));
             if (keep && pos < kQueue16) nxt[pos] = child;
             nnext += __popc(mh);
-            eval_members16(t, o, m, hl, scan, mem, px, py, evaluated);
+            eval_members16(t, o, m, hl, mrec, mem, px, py, evaluated);
         }
         __syncwarp();
         if (nnext > kQueue16) {  // this half stops; the other goes on
@@ -1436,6 +1442,7 @@ __global__ void __launch_bounds__(kHardThreads) hard_scan_kernel(const ScanRec* 
 
 struct KnnBufs {
     DevBuf cnt, off, key, mem, own, sub, cub_tmp, hard, ticket, part, lcount, acc;
+    DevBuf mrec, minv;  // records in member order, and each Gaussian's position there
     int hard_phase = 0;  // which (hard count, cursor) pair the next search uses
     int knn_blocks[2] = {0, 0};  // resident CTAs for the persistent query kernels (full warp, halves)
     uint64_t version = ~0ull;  // params_version the summaries describe
@@ -1469,6 +1476,7 @@ L2Prefetch search_inputs(igs_ctx* ctx, const KnnBufs& b) {
     L2Prefetch pf{};
     l2pf_add(pf, ctx->scan, (size_t)ctx->n * sizeof(ScanRec));
     l2pf_add(pf, b.mem.p, (size_t)ctx->n * 4);
+    l2pf_add(pf, b.mrec.p, (size_t)ctx->n * sizeof(ScanRec));
     return pf;
 }
 
@@ -1509,7 +1517,7 @@ int knn_build(igs_ctx* ctx) {
     L.levels = l;
     const uint32_t cells = (uint32_t)o;
     if (!grow(b.cnt, (size_t)cells * 8) || !grow(b.off, (size_t)cells * 4) || !grow(b.key, (size_t)n * 4) ||
-        !grow(b.mem, (size_t)n * 4) || !grow(b.own, (size_t)cells * sizeof(Sum)) ||
+        !grow(b.mem, (size_t)n * 4) || !grow(b.mrec, (size_t)n * sizeof(ScanRec)) || !grow(b.minv, (size_t)n * 4) || !grow(b.own, (size_t)cells * sizeof(Sum)) ||
         !grow(b.sub, (size_t)cells * sizeof(Sum)))
         return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
     if (!b.ticket.p) {
@@ -1532,7 +1540,7 @@ int knn_build(igs_ctx* ctx) {
     IGS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(b.cub_tmp.p, tb, cnt, off, (int)cells, ctx->stream));
     ctx->launches += 2;
     IGS_PDL(ctx, lq_fill, (n + 255) / 256, 256, 0, (const ScanRec*)ctx->scan, n, (const uint32_t*)b.key.p,
-            (const uint32_t*)off, cur, (uint32_t*)b.mem.p, (Acc*)b.acc.p);
+            (const uint32_t*)off, cur, (uint32_t*)b.mem.p, (ScanRec*)b.mrec.p, (uint32_t*)b.minv.p, (Acc*)b.acc.p);
     const int nb = (G0 + kBlk - 1) / kBlk;
     IGS_PDL(ctx, lq_tree_kernel, nb * nb, 256, 0, (Acc*)b.acc.p, L, (const uint32_t*)cnt, (Sum*)b.own.p,
             (Sum*)b.sub.p, (unsigned int*)b.ticket.p, search_inputs(ctx, b));
@@ -1574,7 +1582,8 @@ int launch_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int 
     const unsigned blocks =
         (unsigned)std::min<uint64_t>(b.knn_blocks[halves], ((uint64_t)npts + per_block - 1) / per_block);
     IGS_PDL(ctx, halves ? knn_points16_kernel : knn_points_kernel, blocks, 128, 0, (const ScanRec*)ctx->scan, ctx->n,
-            b.lq, (const Sum*)b.own.p, (const Sum*)b.sub.p, (const uint32_t*)b.off.p, (const uint32_t*)b.mem.p, uv,
+            b.lq, (const Sum*)b.own.p, (const Sum*)b.sub.p, (const uint32_t*)b.off.p, (const uint32_t*)b.mem.p,
+            (const ScanRec*)b.mrec.p, uv,
             W, H, npts, kk, E, igs_prof_counter(ctx, IGS_PROF_SCAN), hard_count, hard_list,
             igs_prof_counter(ctx, IGS_PROF_KNN_HARD), cursor, zero_next);
     const size_t pitems = (size_t)kHardCap * kHardSplit * kk;
@@ -1627,7 +1636,7 @@ __device__ __forceinline__ double warp_max(double v) {
 // for its own pixel; returns the refreshed warp threshold.
 template <int KCAP>
 __device__ __forceinline__ double raster_members(TopK<KCAP>& t, uint32_t o_mine, uint32_t m_mine, int lane,
-                                                 const ScanRec* __restrict__ scan, const uint32_t* __restrict__ mem,
+                                                 const ScanRec* __restrict__ mrec, const uint32_t* __restrict__ mem,
                                                  ScanRec* stage, uint32_t* stage_i, double px, double py,
                                                  double T, unsigned long long& evaluated) {
     if (__ballot_sync(0xffffffffu, m_mine != 0) == 0) return T;
@@ -1652,8 +1661,9 @@ __device__ __forceinline__ double raster_members(TopK<KCAP>& t, uint32_t o_mine,
         const uint32_t lo_o = __shfl_sync(0xffffffffu, o_mine, lo);
         __syncwarp();
         if (f < total) {
-            const uint32_t gi = __ldg(mem + lo_o + (f - lo_ex));
-            stage[lane] = scan[gi];
+            const uint32_t p = lo_o + (f - lo_ex);
+            const uint32_t gi = __ldg(mem + p);
+            stage[lane] = mrec[p];
             stage_i[lane] = gi;
         }
         __syncwarp();
@@ -1674,7 +1684,7 @@ __global__ void __launch_bounds__(128, 5) knn_raster_kernel(const ScanRec* __res
                                                             const ShadeRec* __restrict__ shade, uint32_t n, Lq L,
                                                             const Sum* __restrict__ own, const Sum* __restrict__ sub,
                                                             const uint32_t* __restrict__ off,
-                                                            const uint32_t* __restrict__ mem, int W, int H, int row0,
+                                                            const uint32_t* __restrict__ mem, const ScanRec* __restrict__ mrec, int W, int H, int row0,
                                                             int row1, int kk, float* __restrict__ out,
                                                             uint32_t* __restrict__ topk, uint32_t npx_patch,
                                                             uint32_t npatch, uint32_t* __restrict__ next_patch,
@@ -1742,7 +1752,7 @@ __global__ void __launch_bounds__(128, 5) knn_raster_kernel(const ScanRec* __res
                         }
                     }
                 }
-                T = raster_members(t, o, m, lane, scan, mem, stage[warp], stage_i[warp], px, py, T, evaluated);
+                T = raster_members(t, o, m, lane, mrec, mem, stage[warp], stage_i[warp], px, py, T, evaluated);
             }
         }
 
@@ -1762,7 +1772,7 @@ __global__ void __launch_bounds__(128, 5) knn_raster_kernel(const ScanRec* __res
                         m = own[c].count;
                     }
                 }
-                T = raster_members(t, o, m, lane, scan, mem, stage[warp], stage_i[warp], px, py, T, evaluated);
+                T = raster_members(t, o, m, lane, mrec, mem, stage[warp], stage_i[warp], px, py, T, evaluated);
             }
         }
 
@@ -1794,7 +1804,7 @@ __global__ void __launch_bounds__(128, 5) knn_raster_kernel(const ScanRec* __res
                         }
                     }
                 }
-                T = raster_members(t, o, m, lane, scan, mem, stage[warp], stage_i[warp], px, py, T, evaluated);
+                T = raster_members(t, o, m, lane, mrec, mem, stage[warp], stage_i[warp], px, py, T, evaluated);
             }
             if (l == 0) break;
             const uint32_t clo = (uint32_t)s_loff[l - 1];
@@ -1873,7 +1883,7 @@ int launch_knn_raster(igs_ctx* ctx, int W, int H, int row0, int row1, int kk, fl
     igs_prof_begin(ctx, IGS_PROF_SCAN);
     IGS_PDL(ctx, knn_raster_kernel<KCAP>, blocks, 128, 0, (const ScanRec*)ctx->scan, (const ShadeRec*)ctx->shade,
             ctx->n, b.lq, (const Sum*)b.own.p, (const Sum*)b.sub.p, (const uint32_t*)b.off.p,
-            (const uint32_t*)b.mem.p, W, H, row0, row1, kk, out, topk, npx, npx * npy, cursor,
+            (const uint32_t*)b.mem.p, (const ScanRec*)b.mrec.p, W, H, row0, row1, kk, out, topk, npx, npx * npy, cursor,
             igs_prof_counter(ctx, IGS_PROF_SCAN));
     igs_prof_end(ctx, IGS_PROF_SCAN, 0.0);
     return IGS_OK;
@@ -1903,6 +1913,8 @@ TreeAcc igs_knn_tree_acc(igs_ctx* ctx) {
         b.chain = ctx->params_version + 1;
         ta.acc = (Acc*)b.acc.p;
         ta.key = (const uint32_t*)b.key.p;
+        ta.mrec = (ScanRec*)b.mrec.p;
+        ta.minv = (const uint32_t*)b.minv.p;
         ta.grown = (unsigned long long*)(ctx->status + 3);
         ta.L = b.lq;
         return ta;
@@ -1918,7 +1930,7 @@ void igs_knn_free(igs_ctx* ctx) {
     if (getenv("IGS_KNN_STATS"))
         fprintf(stderr, "knn tree: %llu builds, %llu refits\n", (unsigned long long)b->builds,
                 (unsigned long long)b->refits);
-    for (DevBuf* d : {&b->cnt, &b->off, &b->key, &b->mem, &b->own, &b->sub, &b->cub_tmp, &b->hard, &b->ticket,
+    for (DevBuf* d : {&b->mrec, &b->minv, &b->cnt, &b->off, &b->key, &b->mem, &b->own, &b->sub, &b->cub_tmp, &b->hard, &b->ticket,
                       &b->part, &b->lcount, &b->acc})
         cudaFree(d->p);
     delete b;

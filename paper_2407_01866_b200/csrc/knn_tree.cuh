@@ -83,6 +83,8 @@ struct TreeAcc {
     const uint32_t* key;            // cell of every Gaussian at the last rebuild
     unsigned long long* grown;      // Gaussians now too large for their level
     Lq L;
+    ScanRec* mrec;                  // the records in member order (kept current)
+    const uint32_t* minv;           // position of every Gaussian there
 };
 
 // Accumulates Gaussian i (record r) into its stored cell and counts it in
@@ -93,6 +95,7 @@ struct TreeAcc {
 __device__ __forceinline__ void tree_acc_add(const TreeAcc& ta, uint32_t i, const ScanRec& r) {
     if (!ta.acc) return;
     const uint32_t k = ta.key[i];
+    ta.mrec[ta.minv[i]] = r;
     acc_add(ta.acc + (k & kKeyCellMask), r);
     // level_of: smallest l with cell 2^l / G0 >= 2 sigma_max = 2 / sqrt(lmin)
     const float lmin = (float)fmin(r.inv_a, r.inv_b);
