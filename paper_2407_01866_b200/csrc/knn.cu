@@ -63,11 +63,15 @@ __device__ __forceinline__ int ring_dy(int it, int R) {
 constexpr int kRefitPeriod = 16;
 constexpr int kGrowShift = 3;  // re-bucket when more than n >> kGrowShift Gaussians grew
 
-struct __align__(16) Sum {
-    double x0, y0, x1, y1;  // centre bbox (empty: +inf/-inf)
-    double lmin;            // smallest Sigma^-1 eigenvalue
-    float slack;            // bound safety factor (0 = never prune)
+// 32 bytes (one sector).  The bbox is rounded outward and lambda_min down
+// to float: a box that contains the true one and a smaller eigenvalue only
+// lower the (monotonically evaluated) bound, so it stays certified.
+struct __align__(32) Sum {
+    float x0, y0, x1, y1;  // centre bbox, rounded outward (empty: +inf/-inf)
+    float lmin;            // smallest Sigma^-1 eigenvalue, rounded down
+    float slack;           // bound safety factor (0 = never prune)
     uint32_t count;
+    uint32_t pad;
 };
 
 
@@ -126,20 +130,21 @@ __global__ void lq_fill(const ScanRec* __restrict__ scan, uint32_t n, const uint
 }
 
 __device__ __forceinline__ Sum empty_sum() {
-    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    const float inf = __int_as_float(0x7f800000);
     Sum s;
     s.x0 = inf; s.y0 = inf; s.x1 = -inf; s.y1 = -inf;
     s.lmin = inf;
     s.slack = 1.0f;
     s.count = 0;
+    s.pad = 0;
     return s;
 }
 
 __device__ __forceinline__ void merge(Sum& a, const Sum& b) {
     if (b.count == 0) return;
-    a.x0 = fmin(a.x0, b.x0); a.x1 = fmax(a.x1, b.x1);
-    a.y0 = fmin(a.y0, b.y0); a.y1 = fmax(a.y1, b.y1);
-    a.lmin = fmin(a.lmin, b.lmin);
+    a.x0 = fminf(a.x0, b.x0); a.x1 = fmaxf(a.x1, b.x1);
+    a.y0 = fminf(a.y0, b.y0); a.y1 = fmaxf(a.y1, b.y1);
+    a.lmin = fminf(a.lmin, b.lmin);
     a.slack = fminf(a.slack, b.slack);
     a.count += b.count;
 }
@@ -152,11 +157,11 @@ __device__ __forceinline__ Sum own_of(Acc* __restrict__ acc, const uint32_t* __r
     if (m == 0) return s;
     const Acc a = acc[c];
     acc[c] = acc_empty();
-    s.x0 = odec(a.x0);
-    s.y0 = odec(a.y0);
-    s.x1 = odec(a.x1);
-    s.y1 = odec(a.y1);
-    s.lmin = odec(a.lmin);
+    s.x0 = __double2float_rd(odec(a.x0));
+    s.y0 = __double2float_rd(odec(a.y0));
+    s.x1 = __double2float_ru(odec(a.x1));
+    s.y1 = __double2float_ru(odec(a.y1));
+    s.lmin = __double2float_rd(odec(a.lmin));
     s.slack = slack_for(odec(a.aniso));
     s.count = m;
     return s;
@@ -176,11 +181,11 @@ constexpr int kUpCells = 341;  // 16^2 + 8^2 + 4^2 + 2^2 + 1: upper levels kept 
 __device__ __forceinline__ Sum own_from(uint32_t m, const Acc& a) {
     Sum s = empty_sum();
     if (m == 0) return s;
-    s.x0 = odec(a.x0);
-    s.y0 = odec(a.y0);
-    s.x1 = odec(a.x1);
-    s.y1 = odec(a.y1);
-    s.lmin = odec(a.lmin);
+    s.x0 = __double2float_rd(odec(a.x0));
+    s.y0 = __double2float_rd(odec(a.y0));
+    s.x1 = __double2float_ru(odec(a.x1));
+    s.y1 = __double2float_ru(odec(a.y1));
+    s.lmin = __double2float_rd(odec(a.lmin));
     s.slack = slack_for(odec(a.aniso));
     s.count = m;
     return s;
@@ -330,9 +335,9 @@ __global__ void __launch_bounds__(256) lq_tree_kernel(Acc* __restrict__ acc, Lq 
 
 __device__ __forceinline__ double sum_lb(const Sum& s, double px, double py) {
     if (s.count == 0) return __longlong_as_double(0x7ff0000000000000LL);
-    const double dx = fmax(fmax(s.x0 - px, px - s.x1), 0.0);
-    const double dy = fmax(fmax(s.y0 - py, py - s.y1), 0.0);
-    return s.lmin * (dx * dx + dy * dy) * (double)s.slack;
+    const double dx = fmax(fmax((double)s.x0 - px, px - (double)s.x1), 0.0);
+    const double dy = fmax(fmax((double)s.y0 - py, py - (double)s.y1), 0.0);
+    return (double)s.lmin * (dx * dx + dy * dy) * (double)s.slack;
 }
 
 // Warp-distributed top-K: lane j holds the j-th best (q, idx) for j < kk,
@@ -1621,9 +1626,9 @@ constexpr int kPatchW = 8, kPatchH = 4;
 
 __device__ __forceinline__ double box_lb(const Sum& s, double bx0, double by0, double bx1, double by1) {
     if (s.count == 0) return __longlong_as_double(0x7ff0000000000000LL);
-    const double dx = fmax(fmax(s.x0 - bx1, bx0 - s.x1), 0.0);
-    const double dy = fmax(fmax(s.y0 - by1, by0 - s.y1), 0.0);
-    return s.lmin * (dx * dx + dy * dy) * (double)s.slack;
+    const double dx = fmax(fmax((double)s.x0 - bx1, bx0 - (double)s.x1), 0.0);
+    const double dy = fmax(fmax((double)s.y0 - by1, by0 - (double)s.y1), 0.0);
+    return (double)s.lmin * (dx * dx + dy * dy) * (double)s.slack;
 }
 
 __device__ __forceinline__ double warp_max(double v) {
