@@ -157,12 +157,12 @@ __device__ __forceinline__ Sum own_of(Acc* __restrict__ acc, const uint32_t* __r
     if (m == 0) return s;
     const Acc a = acc[c];
     acc[c] = acc_empty();
-    s.x0 = __double2float_rd(odec(a.x0));
-    s.y0 = __double2float_rd(odec(a.y0));
-    s.x1 = __double2float_ru(odec(a.x1));
-    s.y1 = __double2float_ru(odec(a.y1));
-    s.lmin = __double2float_rd(odec(a.lmin));
-    s.slack = slack_for(odec(a.aniso));
+    s.x0 = odec(a.x0);
+    s.y0 = odec(a.y0);
+    s.x1 = odec(a.x1);
+    s.y1 = odec(a.y1);
+    s.lmin = odec(a.lmin);
+    s.slack = slack_for((double)odec(a.aniso));
     s.count = m;
     return s;
 }
@@ -181,12 +181,12 @@ constexpr int kUpCells = 341;  // 16^2 + 8^2 + 4^2 + 2^2 + 1: upper levels kept 
 __device__ __forceinline__ Sum own_from(uint32_t m, const Acc& a) {
     Sum s = empty_sum();
     if (m == 0) return s;
-    s.x0 = __double2float_rd(odec(a.x0));
-    s.y0 = __double2float_rd(odec(a.y0));
-    s.x1 = __double2float_ru(odec(a.x1));
-    s.y1 = __double2float_ru(odec(a.y1));
-    s.lmin = __double2float_rd(odec(a.lmin));
-    s.slack = slack_for(odec(a.aniso));
+    s.x0 = odec(a.x0);
+    s.y0 = odec(a.y0);
+    s.x1 = odec(a.x1);
+    s.y1 = odec(a.y1);
+    s.lmin = odec(a.lmin);
+    s.slack = slack_for((double)odec(a.aniso));
     s.count = m;
     return s;
 }

@@ -41,20 +41,20 @@ __device__ __forceinline__ uint32_t key_of(const Lq& L, const ScanRec& r) {
     return (uint32_t)(L.loff[l] + cell_of(r.mu_y, G) * G + cell_of(r.mu_x, G));
 }
 
-// Own-cell summaries are accumulated with order-preserving 64-bit atomics
-// while the members are scattered (no per-cell member loop): a double's bit
-// pattern, sign-flipped, orders like the double itself.
+// Own-cell summaries are accumulated with order-preserving 32-bit atomics
+// while the members are scattered (no per-cell member loop): a float's bit
+// pattern, sign-flipped, orders like the float itself.  Values are rounded
+// in the direction that keeps the summary conservative (bbox outward,
+// lambda_min down, anisotropy up), as the 32-byte Sum stores them.
 struct Acc {
-    unsigned long long x0, y0, x1, y1, lmin, aniso;
+    unsigned x0, y0, x1, y1, lmin, aniso;
 };
 
-__device__ __forceinline__ unsigned long long okey(double d) {
-    const unsigned long long b = (unsigned long long)__double_as_longlong(d);
-    return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+__device__ __forceinline__ unsigned okey(float f) {
+    const unsigned b = __float_as_uint(f);
+    return (b >> 31) ? ~b : (b | 0x80000000u);
 }
-__device__ __forceinline__ double odec(unsigned long long k) {
-    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k));
-}
+__device__ __forceinline__ float odec(unsigned k) { return __uint_as_float((k >> 31) ? (k & 0x7fffffffu) : ~k); }
 
 // Adds Gaussian r to a cell accumulator.  A non-finite or degenerate record
 // gets aniso = inf, whose slack 0 makes the cell never prunable.
@@ -63,17 +63,17 @@ __device__ __forceinline__ void acc_add(Acc* a, const ScanRec& r) {
     double aniso = hi / lo;
     if (!(lo > 0.0) || !isfinite(hi) || !isfinite(r.mu_x) || !isfinite(r.mu_y))
         aniso = __longlong_as_double(0x7ff0000000000000LL);
-    atomicMin(&a->x0, okey(r.mu_x));
-    atomicMin(&a->y0, okey(r.mu_y));
-    atomicMax(&a->x1, okey(r.mu_x));
-    atomicMax(&a->y1, okey(r.mu_y));
-    atomicMin(&a->lmin, okey(lo));
-    atomicMax(&a->aniso, okey(aniso));
+    atomicMin(&a->x0, okey(__double2float_rd(r.mu_x)));
+    atomicMin(&a->y0, okey(__double2float_rd(r.mu_y)));
+    atomicMax(&a->x1, okey(__double2float_ru(r.mu_x)));
+    atomicMax(&a->y1, okey(__double2float_ru(r.mu_y)));
+    atomicMin(&a->lmin, okey(__double2float_rd(lo)));
+    atomicMax(&a->aniso, okey(__double2float_ru(aniso)));
 }
 
 __device__ __forceinline__ Acc acc_empty() {
-    const double inf = __longlong_as_double(0x7ff0000000000000LL);
-    return Acc{okey(inf), okey(inf), okey(-inf), okey(-inf), okey(inf), okey(1.0)};
+    const float inf = __int_as_float(0x7f800000);
+    return Acc{okey(inf), okey(inf), okey(-inf), okey(-inf), okey(inf), okey(1.0f)};
 }
 
 // What an Adam launch needs to keep the tree refittable: acc == nullptr
