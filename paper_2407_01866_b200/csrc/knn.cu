@@ -221,9 +221,11 @@ __global__ void __launch_bounds__(256) lq_tree_kernel(Acc* __restrict__ acc, Lq 
             m[l] = cnt[cell[l]];
         }
     }
+    // (an empty cell's accumulator holds acc_empty(): loaded unconditionally,
+    // the counts and accumulators arrive in one round trip)
 #pragma unroll
     for (int l = 0; l < kInLv; ++l)
-        if (m[l]) a[l] = acc[cell[l]];
+        if (cell[l] != ~0u) a[l] = acc[cell[l]];
 #pragma unroll
     for (int l = 0; l < kInLv; ++l)
         if (m[l]) acc[cell[l]] = acc_empty();  // ready for the next accumulation
@@ -267,7 +269,7 @@ __global__ void __launch_bounds__(256) lq_tree_kernel(Acc* __restrict__ acc, Lq 
     }
 #pragma unroll
     for (int r = 0; r < 2; ++r)
-        if (um[r]) ua[r] = acc[uc[r]];
+        if (t + 256 * r < ncell) ua[r] = acc[uc[r]];
     __shared__ bool last;
     // the block's stores are ordered before thread 0's fence by the barrier
     // (the cooperative-groups grid-barrier pattern): one fence per block
