@@ -222,6 +222,8 @@ struct igs_ctx {
     // (two slots: samples, result block and completion event per slot)
     DevBuf async_pin[4];
     cudaEvent_t async_ev[2] = {nullptr, nullptr};
+    int off_blocks = 0;          // offsets_scatter_kernel grid (co-resident)
+    bool off_ctl_ready = false;  // its barrier counters zeroed (scratch 34)
     int async_head = 0, async_count = 0;
 
     // the fit driver's sampling distribution (alias table) on the device

@@ -158,6 +158,106 @@ __global__ void scatter_slots_kernel(const uint32_t* __restrict__ keys, uint32_t
     if (pos == 0 && gcnt[g] > kShortSeg) long_list[atomicAdd(long_count, 1u)] = g;
 }
 
+// Segment offsets (exclusive scan of the per-Gaussian counts) and the slot
+// scatter in one persistent launch: every CTA scans its chunk of the counts,
+// a grid barrier publishes the chunk totals, each CTA adds its base and
+// writes the offsets, a second barrier, then scatter_slots_kernel's work.
+// The grid is sized to be co-resident (a few CTAs per SM), so the spinning
+// barrier cannot wait on a CTA that is not running; bar[0] counts arrivals,
+// bar[1] exits, and the last CTA out resets both for the next launch.
+constexpr int kOffThreads = 256;
+constexpr int kOffPer = 4;  // counts per thread and chunk pass
+
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1u);
+        while (*(volatile unsigned*)bar < target) __nanosleep(20);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kOffThreads) offsets_scatter_kernel(
+    const uint32_t* __restrict__ gcnt, uint32_t n, uint32_t* __restrict__ goff, uint32_t* __restrict__ chunk_sum,
+    const uint32_t* __restrict__ keys, uint32_t items, uint32_t* __restrict__ gcur, uint32_t* __restrict__ perm,
+    uint32_t* __restrict__ long_count, uint32_t* __restrict__ long_list, unsigned* __restrict__ bar) {
+    using BlockScan = cub::BlockScan<uint32_t, kOffThreads>;
+    __shared__ typename BlockScan::TempStorage tmp;
+    __shared__ uint32_t s_base;
+    pdl_wait();
+    const uint32_t G = gridDim.x;
+    // chunk of CTA b: [b * per_cta, (b + 1) * per_cta), per_cta a multiple of kOffThreads * kOffPer
+    const uint32_t tile = kOffThreads * kOffPer;
+    const uint32_t per_cta = ((n + G - 1) / G + tile - 1) / tile * tile;
+    const uint32_t c0 = blockIdx.x * per_cta, c1 = min(n, c0 + per_cta);
+    // pass 1: chunk total
+    uint32_t total = 0;
+    for (uint32_t b = c0; b < c1; b += tile) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int j = 0; j < kOffPer; ++j) {
+            const uint32_t i = b + threadIdx.x * kOffPer + j;
+            if (i < c1) v += gcnt[i];
+        }
+        total += v;
+    }
+    {
+        using BlockReduce = cub::BlockReduce<uint32_t, kOffThreads>;
+        __shared__ typename BlockReduce::TempStorage rtmp;
+        const uint32_t agg = BlockReduce(rtmp).Sum(total);
+        if (threadIdx.x == 0) chunk_sum[blockIdx.x] = agg;
+    }
+    grid_sync(bar, G);
+    // the chunk's base: the totals of the chunks before it
+    uint32_t mine = 0;
+    for (uint32_t b = threadIdx.x; b < blockIdx.x; b += kOffThreads) mine += *(volatile uint32_t*)(chunk_sum + b);
+    {
+        using BlockReduce = cub::BlockReduce<uint32_t, kOffThreads>;
+        __shared__ typename BlockReduce::TempStorage rtmp2;
+        const uint32_t base = BlockReduce(rtmp2).Sum(mine);
+        if (threadIdx.x == 0) s_base = base;
+    }
+    __syncthreads();
+    uint32_t run = s_base;
+    // pass 2: offsets
+    for (uint32_t b = c0; b < c1; b += tile) {
+        uint32_t v[kOffPer], sum = 0;
+#pragma unroll
+        for (int j = 0; j < kOffPer; ++j) {
+            const uint32_t i = b + threadIdx.x * kOffPer + j;
+            v[j] = i < c1 ? gcnt[i] : 0u;
+            sum += v[j];
+        }
+        uint32_t excl, agg;
+        BlockScan(tmp).ExclusiveSum(sum, excl, agg);
+        __syncthreads();  // tmp reused next pass
+        uint32_t o = run + excl;
+#pragma unroll
+        for (int j = 0; j < kOffPer; ++j) {
+            const uint32_t i = b + threadIdx.x * kOffPer + j;
+            if (i < c1) goff[i] = o;
+            o += v[j];
+        }
+        run += agg;
+    }
+    grid_sync(bar, 2 * G);
+    // scatter (scatter_slots_kernel)
+    for (uint32_t slot = blockIdx.x * kOffThreads + threadIdx.x; slot < items; slot += G * kOffThreads) {
+        const uint32_t g = keys[slot];
+        if (g >= n) continue;
+        const uint32_t pos = atomicAdd(gcur + g, 1u);
+        perm[__ldcg(goff + g) + pos] = slot;  // (written by other CTAs: read through L2)
+        if (pos == 0 && gcnt[g] > kShortSeg) long_list[atomicAdd(long_count, 1u)] = g;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(bar + 1, 1u) == G - 1) {
+        bar[0] = 0;
+        bar[1] = 0;
+    }
+}
+
 __device__ __forceinline__ void sum_row(const double* __restrict__ contrib, uint32_t slot, double* acc) {
     const double2* c = reinterpret_cast<const double2*>(contrib + (size_t)slot * 8);
     const double2 a = c[0], b = c[1], cc = c[2], d = c[3];
@@ -933,15 +1033,33 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
                                                                                         gcnt);
             IGS_LAUNCHED(ctx);
         }
-        size_t tb = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tb, gcnt, goff, (int)n, ctx->stream);
-        void* temp = igs_scratch(ctx, 8, tb);
-        if (!temp) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (scan)");
-        IGS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(temp, tb, gcnt, goff, (int)n, ctx->stream));
-        ctx->launches += 2;
-        IGS_PDL(ctx, scatter_slots_kernel, (unsigned)((items + 255) / 256), 256, 0, (const uint32_t*)keys,
-                (uint32_t)items, n, (const uint32_t*)goff, (const uint32_t*)gcnt, gcnt + n, perm, long_ctl,
-                long_ctl + 1);
+        if (!getenv("IGS_CUB_SCAN")) {
+            // offsets + scatter in one persistent launch (two grid barriers)
+            if (!ctx->off_blocks) {
+                int per_sm = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, offsets_scatter_kernel, kOffThreads, 0);
+                ctx->off_blocks = std::max(1, std::min(per_sm, 2)) * ctx->sm_count;
+            }
+            uint32_t* ctl = (uint32_t*)igs_scratch(ctx, 34, ((size_t)ctx->off_blocks + 2) * sizeof(uint32_t));
+            if (!ctl) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (scan)");
+            if (!ctx->off_ctl_ready) {
+                IGS_CUDA(ctx, cudaMemsetAsync(ctl, 0, 2 * sizeof(uint32_t), ctx->stream));
+                ctx->off_ctl_ready = true;
+            }
+            IGS_PDL(ctx, offsets_scatter_kernel, (unsigned)ctx->off_blocks, kOffThreads, 0, (const uint32_t*)gcnt, n,
+                    goff, ctl + 2, (const uint32_t*)keys, (uint32_t)items, gcnt + n, perm, long_ctl, long_ctl + 1,
+                    (unsigned*)ctl);
+        } else {
+            size_t tb = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, tb, gcnt, goff, (int)n, ctx->stream);
+            void* temp = igs_scratch(ctx, 8, tb);
+            if (!temp) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (scan)");
+            IGS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(temp, tb, gcnt, goff, (int)n, ctx->stream));
+            ctx->launches += 2;
+            IGS_PDL(ctx, scatter_slots_kernel, (unsigned)((items + 255) / 256), 256, 0, (const uint32_t*)keys,
+                    (uint32_t)items, n, (const uint32_t*)goff, (const uint32_t*)gcnt, gcnt + n, perm, long_ctl,
+                    long_ctl + 1);
+        }
         uint32_t* big = (uint32_t*)igs_scratch(ctx, 32, items * sizeof(uint32_t));
         if (!big) return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
         IGS_PDL(ctx, long_segment_kernel, 8 * ctx->sm_count, kLongThreads, 0, (const uint32_t*)gcnt,
