@@ -269,3 +269,29 @@ def test_long_segments_reference_order(gctx, port, n, ns):
     wl, wg = port.train_step(params, target, sidx, 10)
     assert abs(loss - wl) <= 1e-12 * abs(wl)
     grad_close(grads, wg, 1e-12)
+
+
+@pytest.mark.parametrize("k", [10, 24])
+def test_alternate_kernels_bit_identical(gctx, port, monkeypatch, k):
+    """The K <= 16 search runs two points per warp (knn_points16_kernel) and
+    the reduction's offsets + scatter run as one persistent launch; the
+    one-point-per-warp search (IGS_KNN_FULLWARP) and the CUB scan + scatter
+    (IGS_CUB_SCAN) select and sum identically, so 8 iterations give the same
+    losses and parameters bit for bit (K = 24 takes the full-warp search
+    either way)."""
+    target = synth.photo_like_image(160, 120, 31013)
+    params = port.initialize_set(target, 3000, 0.3, 31)
+    steps = synth.sample_indices(3001, 160, 120, seed=37, steps=8)  # odd: a half-empty last warp
+
+    def run():
+        gctx.set_params(params)
+        gctx.set_target(target)
+        losses = [gctx.train_iteration(steps[s], k, LR * 5, s + 1) for s in range(8)]
+        return losses, gctx.get_params()
+
+    l0, p0 = run()
+    monkeypatch.setenv("IGS_KNN_FULLWARP", "1")
+    monkeypatch.setenv("IGS_CUB_SCAN", "1")
+    l1, p1 = run()
+    assert l0 == l1
+    assert np.array_equal(p0, p1)
