@@ -355,13 +355,30 @@ __global__ void __launch_bounds__(kLongThreads) long_segment_kernel(const uint32
                                                                     const uint32_t* __restrict__ long_count,
                                                                     const uint32_t* __restrict__ long_list,
                                                                     long long* __restrict__ status,
-                                                                    uint32_t* __restrict__ big) {
+                                                                    uint32_t* __restrict__ big,
+                                                                    const double* __restrict__ losses,
+                                                                    uint32_t ns, double inv_n,
+                                                                    double* __restrict__ dloss) {
     pdl_wait();
     __shared__ uint32_t keys[kLongCap];
     __shared__ uint32_t sorted[kLongCap];
     __shared__ double rows[kLongThreads][8];
     const uint32_t total = *long_count;
     const int t = threadIdx.x;
+    if (dloss && blockIdx.x == gridDim.x - 1) {
+        // the loss (fit.cpp:87-89: mean of the per-sample L1 losses), by the
+        // last CTA while the others take the long segments
+        double acc = 0.0;
+        for (uint32_t i = t; i < ns; i += kLongThreads) acc = __dadd_rn(acc, losses[i]);
+        double* sm = &rows[0][0];
+        sm[t] = acc;
+        __syncthreads();
+        for (int s = kLongThreads / 2; s > 0; s >>= 1) {
+            if (t < s) sm[t] = __dadd_rn(sm[t], sm[t + s]);
+            __syncthreads();
+        }
+        if (t == 0) *dloss = __dmul_rn(sm[0], inv_n);
+    }
     for (uint32_t it = blockIdx.x; it < total; it += gridDim.x) {
         const uint32_t g = long_list[it];
         const uint32_t m = gcnt[g], o = goff[g];
@@ -1017,7 +1034,9 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
     }
     // the loss sum needs only the per-sample losses: it runs on the side
     // stream, overlapping the reduction and Adam, and is joined below
-    const bool loss_side = mode == 0 && dev_loss;
+    // the loss sum rides in long_segment_kernel (deterministic mode), else on
+    // the side stream
+    const bool loss_side = mode == 0 && dev_loss && !ctx->opt_deterministic;
     if (loss_side) {
         IGS_CUDA(ctx, cudaEventRecord(ctx->ev_fork, ctx->stream));
         IGS_CUDA(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
@@ -1064,7 +1083,8 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
         if (!big) return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
         IGS_PDL(ctx, long_segment_kernel, 8 * ctx->sm_count, kLongThreads, 0, (const uint32_t*)gcnt,
                 (const uint32_t*)goff, perm, (const double*)contrib, ctx->grads, (const uint32_t*)long_ctl,
-                (const uint32_t*)(long_ctl + 1), ctx->status, big);
+                (const uint32_t*)(long_ctl + 1), ctx->status, big, (const double*)losses, ns_all, inv_n,
+                mode == 0 ? dev_loss : nullptr);
         if (fuse_lr4 && (exch || (ctx->nranks == 1 && !ctx->comm))) {
             // short segments summed inside the Adam kernel (one pass over the set)
             const double bc1 = 1.0 - std::pow(0.9, (double)t);  // adam.cpp:16-17, host libm
