@@ -831,11 +831,14 @@ __global__ void __launch_bounds__(128, 7) segment_adam_kernel(
 // kernels stay one programmatic-dependent-launch chain.
 __global__ void stage_kernel(long long* __restrict__ status, const uint32_t* __restrict__ host_sidx,
                              uint32_t* __restrict__ dsidx, uint32_t ns, L2Prefetch pf) {
-    pdl_wait();
+    // the host buffer was filled before the launch and the prefetch is a
+    // hint: both overlap the previous kernel; the writes wait for it
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     prefetch_l2(pf, i, gridDim.x * blockDim.x);  // the tree refit's inputs
+    const uint32_t v = i < ns ? host_sidx[i] : 0u;
+    pdl_wait();
     if (blockIdx.x == 0 && threadIdx.x < 4) status[threadIdx.x] = threadIdx.x == 3 ? 0 : LLONG_MAX;
-    if (i < ns) dsidx[i] = host_sidx[i];
+    if (i < ns) dsidx[i] = v;
 }
 
 // Same, drawing the samples on the device from raw engine outputs: sample j
@@ -847,15 +850,19 @@ __global__ void draw_stage_kernel(long long* __restrict__ status, const unsigned
                                   const double* __restrict__ prob, const uint32_t* __restrict__ alias,
                                   unsigned long long table_n, uint32_t* __restrict__ dsidx, uint32_t ns,
                                   L2Prefetch pf) {
-    pdl_wait();
+    // reads (host buffer, the fixed sampling table) before the wait, as stage_kernel
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     prefetch_l2(pf, i, gridDim.x * blockDim.x);
+    uint32_t v = 0;
+    if (i < ns) {
+        const unsigned long long r0 = host_raw[2 * (size_t)i], r1 = host_raw[2 * (size_t)i + 1];
+        const unsigned long long j = r0 % table_n;
+        const double coin = (double)(r1 >> 11) * 0x1.0p-53;
+        v = coin < prob[j] ? (uint32_t)j : alias[j];
+    }
+    pdl_wait();
     if (blockIdx.x == 0 && threadIdx.x < 4) status[threadIdx.x] = threadIdx.x == 3 ? 0 : LLONG_MAX;
-    if (i >= ns) return;
-    const unsigned long long r0 = host_raw[2 * (size_t)i], r1 = host_raw[2 * (size_t)i + 1];
-    const unsigned long long j = r0 % table_n;
-    const double coin = (double)(r1 >> 11) * 0x1.0p-53;
-    dsidx[i] = coin < prob[j] ? (uint32_t)j : alias[j];
+    if (i < ns) dsidx[i] = v;
 }
 
 // End of an iteration: status block + loss into the pinned result block.
