@@ -232,7 +232,7 @@ def run_ours(args, rank, world, local_rank, dist):
         achieved = scan_pairs * OPS_PER_PAIR / (scan_ms * 1e-3)
         roof = {"kernel": "top-K candidate scan (IGS_PROF_SCAN)", "bound": "fp64",
                 "achieved": achieved / 1e9, "peak": fp64_peak / 1e9, "unit": "Gop/s (fp64 add/mul pipe)",
-                "frac": achieved / fp64_peak, "traffic": ncu_traffic("knn_points_kernel"),
+                "frac": achieved / fp64_peak, "traffic": ncu_traffic("knn_points16_kernel"),
                 "work_per_launch": f"{scan_pairs / max(scan_launches, 1):.4g} (pixel, candidate) pairs x "
                                    f"{OPS_PER_PAIR} fp64 ops",
                 "peak_source": "measured in this run (igs_fp64_peak: independent DMUL/DADD chains, all SMs); "

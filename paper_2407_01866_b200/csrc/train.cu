@@ -169,12 +169,13 @@ constexpr int kOffThreads = 256;
 constexpr int kOffPer = 4;  // counts per thread and chunk pass
 
 __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned target) {
-    __syncthreads();
+    __syncthreads();  // the CTA's writes are ordered before thread 0's release
     if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(bar, 1u);
-        while (*(volatile unsigned*)bar < target) __nanosleep(20);
-        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+        } while (v < target);
     }
     __syncthreads();
 }
@@ -1064,7 +1065,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
             if (!ctx->off_blocks) {
                 int per_sm = 0;
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, offsets_scatter_kernel, kOffThreads, 0);
-                ctx->off_blocks = std::max(1, std::min(per_sm, 2)) * ctx->sm_count;
+                ctx->off_blocks = std::max(1, std::min(per_sm, 1)) * ctx->sm_count;
             }
             uint32_t* ctl = (uint32_t*)igs_scratch(ctx, 34, ((size_t)ctx->off_blocks + 2) * sizeof(uint32_t));
             if (!ctl) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (scan)");
