@@ -254,7 +254,7 @@ def run_ours(args, rank, world, local_rank, dist):
         gbs = adam_bytes / (adam_ms * 1e-3) / 1e9
         adam_roof = {"kernel": "fused Adam+constrain+prepare", "bound": "hbm", "achieved": gbs, "peak": hbm,
                      "unit": "GB/s", "frac": gbs / hbm, "traffic": ncu_traffic("segment_adam_kernel"),
-                     "bytes_per_gaussian": 544}
+                     "bytes_per_gaussian": 596}
 
     # ---- secondary: full render Mpix/s (the eval render of the same set) ------------
     render = None

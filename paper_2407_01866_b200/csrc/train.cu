@@ -1105,7 +1105,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
                     (const uint32_t*)perm, (const double*)contrib, n, ctx->grads, ctx->params, ctx->adam_m,
                     ctx->adam_v, ctx->scan, ctx->shade, fuse_lr4[0], fuse_lr4[1], fuse_lr4[2], fuse_lr4[3], bc1, bc2,
                     1.0 / bc1, 1.0 / bc2, ctx->status, ta);
-            igs_prof_end(ctx, IGS_PROF_ADAM, (double)n * 544.0);
+            igs_prof_end(ctx, IGS_PROF_ADAM, (double)n * 596.0);
             ctx->gcnt_clean = gcnt;
             ctx->gcnt_clean_n = n;
             if (fused) *fused = true;
