@@ -27,7 +27,7 @@ bool igs_host_encodable(double v);
 extern "C" uint32_t igs_partition_source_size(igs_ctx* ctx);
 int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint32_t* dev_sidx,
                          const double* dev_samples5, double* dev_loss, double inv_n, const double* fuse_lr4 = nullptr,
-                         long long t = 0, bool* fused = nullptr);
+                         long long t = 0, bool* fused = nullptr, const StageJob* job = nullptr);
 int igs_grad_check(igs_ctx* ctx);
 int igs_adam_launch(igs_ctx* ctx, const double* lr4, long long t);
 int igs_weights(igs_ctx* ctx, const double* q, const uint32_t* idx, size_t total, double* w);
@@ -715,13 +715,20 @@ static int train_iteration_enqueue(igs_ctx* ctx, const uint32_t* sample_idx, con
     if (!ctx->async_ev[slot]) IGS_CUDA(ctx, cudaEventCreateWithFlags(&ctx->async_ev[slot], cudaEventDisableTiming));
     dloss += slot;
     std::memcpy(pin, sample_idx ? (const void*)sample_idx : (const void*)raw2, in_bytes);
-    // status reset + H2D (or device draws)
-    if (sample_idx) e = igs_stage_samples(ctx, (const uint32_t*)pin, dsidx, ns);
-    else e = igs_stage_draws(ctx, (const unsigned long long*)pin, dsidx, ns);
-    if (e) return e;
+    // status reset + H2D (or device draws): run by the step's first kernel
+    StageJob job;
+    job.kind = sample_idx ? 2 : 3;
+    job.status = ctx->status;
+    job.host = pin;
+    job.dsidx = dsidx;
+    job.ns = ns;
+    job.prob = (const double*)ctx->alias_prob.p;
+    job.alias = (const uint32_t*)ctx->alias_idx.p;
+    job.table_n = ctx->alias_n;
     const uint32_t ns_total = ns * (uint32_t)ctx->nranks;
     bool fused = false;
-    if ((e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss, 1.0 / (double)ns_total, lr4, t, &fused)))
+    if ((e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss, 1.0 / (double)ns_total, lr4, t, &fused,
+                                  &job)))
         return e;
     if (!fused) {
         if ((e = allreduce_grads(ctx, dloss))) return e;
@@ -818,7 +825,9 @@ int igs_train_iterations(igs_ctx* ctx, uint32_t steps, int k, const double* lr4,
     if (ctx->samples_steps == 0) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "no uploaded samples");
     if (t0 < 1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "Adam step index must be >= 1");
     double* dloss = (double*)igs_scratch(ctx, 22, (size_t)std::max<uint32_t>(steps, 1) * sizeof(double));
-    if ((e = igs_status_reset(ctx))) return e;
+    StageJob reset;  // the status reset, run by the first step's first kernel
+    reset.kind = 1;
+    reset.status = ctx->status;
     const uint32_t ns_total = ns * (uint32_t)ctx->nranks;
     for (uint32_t s = 0; s < steps; ++s) {
         // step t uses uploaded slot (t-1) mod steps_uploaded
@@ -827,7 +836,7 @@ int igs_train_iterations(igs_ctx* ctx, uint32_t steps, int k, const double* lr4,
         if (s > 0) ctx->knn_grown = -1;  // no read-back inside the device loop: re-bucket
         bool fused = false;
         if ((e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss + s, 1.0 / (double)ns_total, lr4, t0 + s,
-                                      &fused)))
+                                      &fused, s == 0 ? &reset : nullptr)))
             return e;
         if (!fused) {
             if ((e = allreduce_grads(ctx, dloss + s))) return e;

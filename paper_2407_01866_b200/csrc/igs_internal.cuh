@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <climits>
+
 #include <string>
 #include <vector>
 
@@ -177,6 +179,44 @@ struct DevBuf {
 
 struct PartitionDev;  // bsp.cu
 
+// The start of a training iteration -- status reset, plus the sample
+// indices copied from pinned host memory or drawn from raw engine outputs --
+// run by the first kernel of the step (the kNN tree refit) instead of a
+// launch of its own; igs_stage_launch runs it standalone when no such kernel
+// follows.
+struct StageJob {
+    int kind = 0;  // 0 none, 1 status reset, 2 + copy host indices, 3 + draw from host raw outputs
+    long long* status = nullptr;
+    const void* host = nullptr;
+    uint32_t* dsidx = nullptr;
+    uint32_t ns = 0;
+    const double* prob = nullptr;
+    const uint32_t* alias = nullptr;
+    unsigned long long table_n = 0;
+};
+
+#ifdef __CUDACC__
+__device__ __forceinline__ void stage_job_run(const StageJob& J, uint32_t tid, uint32_t nthr) {
+    if (J.kind == 0) return;
+    if (tid < 4) J.status[tid] = tid == 3 ? 0 : LLONG_MAX;  // status[3]: a count (kNN tree growth)
+    if (J.kind == 1) return;
+    for (uint32_t i = tid; i < J.ns; i += nthr) {
+        uint32_t v;
+        if (J.kind == 2) {
+            v = static_cast<const uint32_t*>(J.host)[i];
+        } else {
+            // AliasTable::sample (sampling.cpp:126-133), as draw_stage_kernel
+            const unsigned long long* raw = static_cast<const unsigned long long*>(J.host);
+            const unsigned long long r0 = raw[2 * (size_t)i], r1 = raw[2 * (size_t)i + 1];
+            const unsigned long long j = r0 % J.table_n;
+            const double coin = (double)(r1 >> 11) * 0x1.0p-53;
+            v = coin < J.prob[j] ? (uint32_t)j : J.alias[j];
+        }
+        J.dsidx[i] = v;
+    }
+}
+#endif
+
 struct igs_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -222,6 +262,7 @@ struct igs_ctx {
     // (two slots: samples, result block and completion event per slot)
     DevBuf async_pin[4];
     cudaEvent_t async_ev[2] = {nullptr, nullptr};
+    StageJob stage_job;          // handed from igs_forward_backward to knn_build (see StageJob)
     int off_blocks = 0;          // offsets_scatter_kernel grid (co-resident)
     bool off_ctl_ready = false;  // its barrier counters zeroed (scratch 34)
     int async_head = 0, async_count = 0;
@@ -275,6 +316,9 @@ int igs_ensure_image(igs_ctx* ctx, int w, int h);
         cudaError_t _e = cudaGetLastError();                                \
         if (_e != cudaSuccess) return igs_cuda_check((ctx), _e, "launch");  \
     } while (0)
+
+// train.cu: a StageJob as its own launch
+int igs_stage_launch(igs_ctx* ctx, const StageJob& J);
 
 // L2 prefetch of data a LATER kernel of the same step reads: a kernel that is
 // itself latency-bound spreads fire-and-forget prefetches over its threads

@@ -194,7 +194,7 @@ __device__ __forceinline__ Sum own_from(uint32_t m, const Acc& a) {
 __global__ void __launch_bounds__(256) lq_tree_kernel(Acc* __restrict__ acc, Lq L,
                                                       const uint32_t* __restrict__ cnt, Sum* __restrict__ own,
                                                       Sum* __restrict__ sub, unsigned int* __restrict__ ticket,
-                                                      L2Prefetch pf) {
+                                                      L2Prefetch pf, StageJob job) {
     __shared__ Sum sm[2][kBlk * kBlk];
     __shared__ Sum up[kUpCells];
     __shared__ int s_loff[kMaxLv];
@@ -206,6 +206,7 @@ __global__ void __launch_bounds__(256) lq_tree_kernel(Acc* __restrict__ acc, Lq 
     const int nb = L.G0 / kBlk;  // G0 is a power of two >= 16
     const int bx = blockIdx.x % nb, by = blockIdx.x / nb;
     pdl_wait();
+    stage_job_run(job, blockIdx.x * 256 + t, gridDim.x * 256);  // the iteration's start (StageJob)
     prefetch_l2(pf, blockIdx.x * 256 + t, gridDim.x * 256);  // the search's inputs
     // prefetch: the cell this thread owns at each in-block level
     uint32_t cell[kInLv], m[kInLv];
@@ -1490,7 +1491,9 @@ L2Prefetch search_inputs(igs_ctx* ctx, const KnnBufs& b) {
 int knn_build(igs_ctx* ctx) {
     if (!ctx->knn) ctx->knn = new KnnBufs();
     KnnBufs& b = *static_cast<KnnBufs*>(ctx->knn);
-    if (b.version == ctx->params_version) return IGS_OK;
+    const StageJob job = ctx->stage_job;  // run by lq_tree_kernel below, or standalone
+    ctx->stage_job = StageJob{};
+    if (b.version == ctx->params_version) return igs_stage_launch(ctx, job);
     // ctx->knn_grown: the last Adam's count of Gaussians grown past their
     // level, read back with the step's status (-1: unknown)
     if (b.acc_ok && b.chain == ctx->params_version && b.built_n == ctx->n && b.since_build < kRefitPeriod &&
@@ -1501,7 +1504,7 @@ int knn_build(igs_ctx* ctx) {
         const int nb = (b.lq.G0 + kBlk - 1) / kBlk;
         igs_prof_begin(ctx, IGS_PROF_CULL);
         IGS_PDL(ctx, lq_tree_kernel, nb * nb, 256, 0, (Acc*)b.acc.p, b.lq, (const uint32_t*)b.cnt.p, (Sum*)b.own.p,
-                (Sum*)b.sub.p, (unsigned int*)b.ticket.p, search_inputs(ctx, b));
+                (Sum*)b.sub.p, (unsigned int*)b.ticket.p, search_inputs(ctx, b), job);
         igs_prof_end(ctx, IGS_PROF_CULL, 0.0);
         b.since_build++;
         b.version = b.chain = ctx->params_version;
@@ -1550,7 +1553,7 @@ int knn_build(igs_ctx* ctx) {
             (const uint32_t*)off, cur, (uint32_t*)b.mem.p, (ScanRec*)b.mrec.p, (uint32_t*)b.minv.p, (Acc*)b.acc.p);
     const int nb = (G0 + kBlk - 1) / kBlk;
     IGS_PDL(ctx, lq_tree_kernel, nb * nb, 256, 0, (Acc*)b.acc.p, L, (const uint32_t*)cnt, (Sum*)b.own.p,
-            (Sum*)b.sub.p, (unsigned int*)b.ticket.p, search_inputs(ctx, b));
+            (Sum*)b.sub.p, (unsigned int*)b.ticket.p, search_inputs(ctx, b), job);
     igs_prof_end(ctx, IGS_PROF_CULL, 0.0);
     b.lq = L;
     b.builds++;

@@ -938,6 +938,15 @@ int igs_publish(igs_ctx* ctx, const double* dloss, long long* host_res) {
     return IGS_OK;
 }
 
+int igs_status_reset(igs_ctx* ctx);
+
+int igs_stage_launch(igs_ctx* ctx, const StageJob& J) {
+    if (J.kind == 1) return igs_status_reset(ctx);
+    if (J.kind == 2) return igs_stage_samples(ctx, (const uint32_t*)J.host, J.dsidx, J.ns);
+    if (J.kind == 3) return igs_stage_draws(ctx, (const unsigned long long*)J.host, J.dsidx, J.ns);
+    return IGS_OK;
+}
+
 int igs_status_reset(igs_ctx* ctx) {
     const L2Prefetch pf = igs_knn_tree_inputs(ctx);
     IGS_PDL(ctx, reset_status_kernel, pf.nr ? ctx->sm_count : 1, pf.nr ? 256 : 32, 0, ctx->status, pf);
@@ -957,11 +966,16 @@ int igs_status_reset(igs_ctx* ctx) {
 // of the gradients).
 int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint32_t* dev_sidx,
                          const double* dev_samples5, double* dev_loss, double inv_n, const double* fuse_lr4,
-                         long long t, bool* fused) {
+                         long long t, bool* fused, const StageJob* job) {
     if (fused) *fused = false;
     const uint32_t n = ctx->n;
     const int kk = (int)std::min<uint32_t>((uint32_t)k, n);
     const bool knn_path = ctx->opt_cull && kk <= 32;
+    // the iteration's staging: absorbed by the kNN tree launch, else its own
+    if (job && job->kind && !knn_path) {
+        const int es = igs_stage_launch(ctx, *job);
+        if (es) return es;
+    }
     const bool exch = ctx->comm != nullptr && ctx->opt_deterministic && knn_path;
     const uint32_t R = exch ? (uint32_t)ctx->nranks : 1u, rk = exch ? (uint32_t)ctx->rank : 0u;
     ctx->exchanged = exch;
@@ -1002,10 +1016,12 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
             l2pf_add(pf, ctx->adam_m, (size_t)n * 64);
             l2pf_add(pf, ctx->adam_v, (size_t)n * 64);
         }
+        ctx->stage_job = job ? *job : StageJob{};  // knn_build runs it (or launches it) first
         e = igs_knn_forward_backward(ctx, mode, dev_sidx, dev_samples5, ns, kk, inv_n, losses + (size_t)rk * ns,
                                      contrib ? contrib + rk * items_local * 8 : nullptr,
                                      keys ? keys + rk * items_local : nullptr, exch ? nullptr : gcnt,
                                      ctx->opt_deterministic ? nullptr : ctx->grads, long_ctl, &pf, exch ? 1 : 0);
+        ctx->stage_job = StageJob{};
         if (e) return e;
         gcnt_filled = !exch;
     } else {
