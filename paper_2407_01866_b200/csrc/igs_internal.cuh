@@ -265,6 +265,7 @@ struct igs_ctx {
     StageJob stage_job;          // handed from igs_forward_backward to knn_build (see StageJob)
     int off_blocks = 0;          // offsets_scatter_kernel grid (co-resident)
     bool off_ctl_ready = false;  // its barrier counters zeroed (scratch 34)
+    bool loss_ticket_ready = false;  // long_segment_kernel's loss ticket zeroed (scratch 35)
     int async_head = 0, async_count = 0;
 
     // the fit driver's sampling distribution (alias table) on the device

@@ -347,6 +347,7 @@ __global__ void segment_sum_kernel(const uint32_t* __restrict__ gcnt, const uint
 constexpr uint32_t kLongCap = 2048;
 constexpr uint32_t kLongRank = 256;  // up to here: rank by counting; above: bitonic sort
 constexpr int kLongThreads = 256;
+constexpr uint32_t kLossCtas = 8;  // long_segment_kernel CTAs that form the loss
 
 __global__ void __launch_bounds__(kLongThreads) long_segment_kernel(const uint32_t* __restrict__ gcnt,
                                                                     const uint32_t* __restrict__ goff,
@@ -359,18 +360,24 @@ __global__ void __launch_bounds__(kLongThreads) long_segment_kernel(const uint32
                                                                     uint32_t* __restrict__ big,
                                                                     const double* __restrict__ losses,
                                                                     uint32_t ns, double inv_n,
-                                                                    double* __restrict__ dloss) {
+                                                                    double* __restrict__ dloss,
+                                                                    double* __restrict__ loss_part,
+                                                                    unsigned* __restrict__ loss_ticket) {
     pdl_wait();
     __shared__ uint32_t keys[kLongCap];
     __shared__ uint32_t sorted[kLongCap];
     __shared__ double rows[kLongThreads][8];
     const uint32_t total = *long_count;
     const int t = threadIdx.x;
-    if (dloss && blockIdx.x == gridDim.x - 1) {
-        // the loss (fit.cpp:87-89: mean of the per-sample L1 losses), by the
-        // last CTA while the others take the long segments
+    if (dloss && blockIdx.x >= gridDim.x - kLossCtas) {
+        // the loss (fit.cpp:87-89: mean of the per-sample L1 losses) by the
+        // last kLossCtas CTAs while the others take the long segments: chunk
+        // c summed by CTA c (a fixed tree), the chunks combined in order by
+        // whichever finishes last
+        const uint32_t c = blockIdx.x - (gridDim.x - kLossCtas);
+        const uint32_t per = (ns + kLossCtas - 1) / kLossCtas, l0 = c * per, l1 = min(ns, l0 + per);
         double acc = 0.0;
-        for (uint32_t i = t; i < ns; i += kLongThreads) acc = __dadd_rn(acc, losses[i]);
+        for (uint32_t i = l0 + t; i < l1; i += kLongThreads) acc = __dadd_rn(acc, losses[i]);
         double* sm = &rows[0][0];
         sm[t] = acc;
         __syncthreads();
@@ -378,7 +385,17 @@ __global__ void __launch_bounds__(kLongThreads) long_segment_kernel(const uint32
             if (t < s) sm[t] = __dadd_rn(sm[t], sm[t + s]);
             __syncthreads();
         }
-        if (t == 0) *dloss = __dmul_rn(sm[0], inv_n);
+        if (t == 0) {
+            loss_part[c] = sm[0];
+            __threadfence();
+            if (atomicAdd(loss_ticket, 1u) == kLossCtas - 1) {
+                __threadfence();
+                double l = 0.0;
+                for (uint32_t k = 0; k < kLossCtas; ++k) l = __dadd_rn(l, __ldcg(loss_part + k));
+                *dloss = __dmul_rn(l, inv_n);
+                *loss_ticket = 0;
+            }
+        }
     }
     for (uint32_t it = blockIdx.x; it < total; it += gridDim.x) {
         const uint32_t g = long_list[it];
@@ -1105,10 +1122,17 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
         }
         uint32_t* big = (uint32_t*)igs_scratch(ctx, 32, items * sizeof(uint32_t));
         if (!big) return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
+        // loss partials + the combining ticket (zeroed once; the last CTA re-zeroes it)
+        double* loss_part = (double*)igs_scratch(ctx, 35, kLossCtas * sizeof(double) + 16);
+        if (!loss_part) return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
+        if (!ctx->loss_ticket_ready) {
+            IGS_CUDA(ctx, cudaMemsetAsync(loss_part + kLossCtas, 0, 16, ctx->stream));
+            ctx->loss_ticket_ready = true;
+        }
         IGS_PDL(ctx, long_segment_kernel, 8 * ctx->sm_count, kLongThreads, 0, (const uint32_t*)gcnt,
                 (const uint32_t*)goff, perm, (const double*)contrib, ctx->grads, (const uint32_t*)long_ctl,
                 (const uint32_t*)(long_ctl + 1), ctx->status, big, (const double*)losses, ns_all, inv_n,
-                mode == 0 ? dev_loss : nullptr);
+                mode == 0 ? dev_loss : nullptr, loss_part, (unsigned*)(loss_part + kLossCtas));
         if (fuse_lr4 && (exch || (ctx->nranks == 1 && !ctx->comm))) {
             // short segments summed inside the Adam kernel (one pass over the set)
             const double bc1 = 1.0 - std::pow(0.9, (double)t);  // adam.cpp:16-17, host libm
