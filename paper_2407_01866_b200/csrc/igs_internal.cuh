@@ -318,6 +318,23 @@ int igs_ensure_image(igs_ctx* ctx, int w, int h);
         if (_e != cudaSuccess) return igs_cuda_check((ctx), _e, "launch");  \
     } while (0)
 
+#ifdef __CUDACC__
+// Grid-wide barrier for a persistent launch whose CTAs are all co-resident
+// (one per SM): arrivals counted in *bar (release), spun on (acquire) until
+// `target`; callers count targets G, 2G, ... and reset *bar at the end.
+__device__ __forceinline__ void igs_grid_sync(unsigned* bar, unsigned target) {
+    __syncthreads();  // the CTA's writes are ordered before thread 0's release
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+        } while (v < target);
+    }
+    __syncthreads();
+}
+#endif
+
 // train.cu: a StageJob as its own launch
 int igs_stage_launch(igs_ctx* ctx, const StageJob& J);
 

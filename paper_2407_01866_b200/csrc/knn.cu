@@ -129,6 +129,117 @@ __global__ void lq_fill(const ScanRec* __restrict__ scan, uint32_t n, const uint
     acc_add(acc + k, r);
 }
 
+// A full re-bucketing in one persistent launch (one CTA per SM, all
+// co-resident; grid barriers as offsets_scatter_kernel): clear -> level,
+// cell and count per Gaussian (lq_count) -> cell offsets (exclusive scan:
+// chunk totals, barrier, chunk base + block scan) -> member lists, the
+// member-ordered records and the accumulators (lq_fill).  The summaries
+// follow in lq_tree_kernel.  bar[0] arrivals, bar[1] exits, then the chunk
+// totals; the last CTA out resets the counters.
+constexpr int kBuildThreads = 256;
+constexpr int kBuildPer = 4;  // cell counts per thread and scan pass
+
+__global__ void __launch_bounds__(kBuildThreads) lq_build_kernel(
+    const ScanRec* __restrict__ scan, uint32_t n, Lq L, uint32_t cells, uint32_t* __restrict__ cnt,
+    uint32_t* __restrict__ cur, uint32_t* __restrict__ off, uint32_t* __restrict__ key, uint32_t* __restrict__ mem,
+    ScanRec* __restrict__ mrec, uint32_t* __restrict__ minv, Acc* __restrict__ acc, uint32_t* __restrict__ lcount,
+    unsigned* __restrict__ bar) {
+    using BlockScan = cub::BlockScan<uint32_t, kBuildThreads>;
+    using BlockReduce = cub::BlockReduce<uint32_t, kBuildThreads>;
+    __shared__ union {
+        typename BlockScan::TempStorage scan;
+        typename BlockReduce::TempStorage red;
+    } tmp;
+    __shared__ uint32_t s_base;
+    uint32_t* chunk_sum = bar + 2;
+    pdl_wait();
+    const uint32_t G = gridDim.x, tid = blockIdx.x * kBuildThreads + threadIdx.x, nth = G * kBuildThreads;
+    // 1. clear
+    for (uint32_t c = tid; c < cells; c += nth) {
+        cnt[c] = 0;
+        cur[c] = 0;
+        acc[c] = acc_empty();
+    }
+    if (tid < kMaxLv) lcount[tid] = 0;
+    igs_grid_sync(bar, G);
+    // 2. level, cell and count (lq_count)
+    for (uint32_t base = blockIdx.x * kBuildThreads; base < n; base += nth) {
+        const uint32_t i = base + threadIdx.x;
+        int l = -1;
+        if (i < n) {
+            const ScanRec r = scan[i];
+            l = level_of(L, fmin(r.inv_a, r.inv_b));
+            const int Gl = L.lw[l];
+            const uint32_t k = (uint32_t)(L.loff[l] + cell_of(r.mu_y, Gl) * Gl + cell_of(r.mu_x, Gl));
+            key[i] = k | ((uint32_t)l << kKeyLevelShift);
+            atomicAdd(cnt + k, 1u);
+        }
+        const unsigned same = __match_any_sync(0xffffffffu, l);
+        if (l >= 0 && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(lcount + l, (unsigned)__popc(same));
+    }
+    igs_grid_sync(bar, 2 * G);
+    // 3. cell offsets: chunk totals, barrier, chunk base + block scan
+    const uint32_t tile = kBuildThreads * kBuildPer;
+    const uint32_t per_cta = ((cells + G - 1) / G + tile - 1) / tile * tile;
+    const uint32_t c0 = blockIdx.x * per_cta, c1 = min(cells, c0 + per_cta);
+    uint32_t total = 0;
+    for (uint32_t b = c0; b < c1; b += tile)
+#pragma unroll
+        for (int j = 0; j < kBuildPer; ++j) {
+            const uint32_t c = b + threadIdx.x * kBuildPer + j;
+            if (c < c1) total += __ldcg(cnt + c);
+        }
+    {
+        const uint32_t agg = BlockReduce(tmp.red).Sum(total);
+        if (threadIdx.x == 0) chunk_sum[blockIdx.x] = agg;
+    }
+    igs_grid_sync(bar, 3 * G);
+    uint32_t mine = 0;
+    for (uint32_t b = threadIdx.x; b < blockIdx.x; b += kBuildThreads) mine += __ldcg(chunk_sum + b);
+    {
+        const uint32_t base = BlockReduce(tmp.red).Sum(mine);
+        if (threadIdx.x == 0) s_base = base;
+    }
+    __syncthreads();
+    uint32_t run = s_base;
+    for (uint32_t b = c0; b < c1; b += tile) {
+        uint32_t v[kBuildPer], sum = 0;
+#pragma unroll
+        for (int j = 0; j < kBuildPer; ++j) {
+            const uint32_t c = b + threadIdx.x * kBuildPer + j;
+            v[j] = c < c1 ? __ldcg(cnt + c) : 0u;
+            sum += v[j];
+        }
+        uint32_t excl, agg;
+        BlockScan(tmp.scan).ExclusiveSum(sum, excl, agg);
+        __syncthreads();
+        uint32_t o = run + excl;
+#pragma unroll
+        for (int j = 0; j < kBuildPer; ++j) {
+            const uint32_t c = b + threadIdx.x * kBuildPer + j;
+            if (c < c1) off[c] = o;
+            o += v[j];
+        }
+        run += agg;
+    }
+    igs_grid_sync(bar, 4 * G);
+    // 4. member lists, member-ordered records, accumulators (lq_fill)
+    for (uint32_t i = tid; i < n; i += nth) {
+        const uint32_t k = key[i] & kKeyCellMask;  // (this thread wrote key[i] in step 2)
+        const uint32_t pos = __ldcg(off + k) + atomicAdd(cur + k, 1u);
+        const ScanRec r = scan[i];
+        mem[pos] = i;
+        mrec[pos] = r;
+        minv[i] = pos;
+        acc_add(acc + k, r);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(bar + 1, 1u) == G - 1) {
+        bar[0] = 0;
+        bar[1] = 0;
+    }
+}
+
 __device__ __forceinline__ Sum empty_sum() {
     const float inf = __int_as_float(0x7f800000);
     Sum s;
@@ -1451,6 +1562,7 @@ __global__ void __launch_bounds__(kHardThreads) hard_scan_kernel(const ScanRec* 
 struct KnnBufs {
     DevBuf cnt, off, key, mem, own, sub, cub_tmp, hard, ticket, part, lcount, acc;
     DevBuf mrec, minv;  // records in member order, and each Gaussian's position there
+    DevBuf bctl;        // lq_build_kernel: barrier counters + chunk totals
     int hard_phase = 0;  // which (hard count, cursor) pair the next search uses
     int knn_blocks[2] = {0, 0};  // resident CTAs for the persistent query kernels (full warp, halves)
     uint64_t version = ~0ull;  // params_version the summaries describe
@@ -1541,16 +1653,29 @@ int knn_build(igs_ctx* ctx) {
     uint32_t* cur = cnt + cells;
     uint32_t* off = (uint32_t*)b.off.p;
     igs_prof_begin(ctx, IGS_PROF_CULL);
-    IGS_PDL(ctx, lq_clear, 2 * ctx->sm_count, 256, 0, cells, cnt, (Acc*)b.acc.p, (uint32_t*)b.lcount.p);
-    IGS_PDL(ctx, lq_count, (n + 255) / 256, 256, 0, (const ScanRec*)ctx->scan, n, L, cnt, (uint32_t*)b.key.p,
-            (uint32_t*)b.lcount.p);
-    size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, (int)cells, ctx->stream);
-    if (!grow(b.cub_tmp, tb)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn scan)");
-    IGS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(b.cub_tmp.p, tb, cnt, off, (int)cells, ctx->stream));
-    ctx->launches += 2;
-    IGS_PDL(ctx, lq_fill, (n + 255) / 256, 256, 0, (const ScanRec*)ctx->scan, n, (const uint32_t*)b.key.p,
-            (const uint32_t*)off, cur, (uint32_t*)b.mem.p, (ScanRec*)b.mrec.p, (uint32_t*)b.minv.p, (Acc*)b.acc.p);
+    if (!getenv("IGS_KNN_BUILD_LAUNCHES")) {
+        // one persistent launch (lq_build_kernel): [0, 2) barrier counters, then chunk totals
+        if (!b.bctl.p) {
+            if (!grow(b.bctl, (2 + (size_t)ctx->sm_count) * 4))
+                return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
+            IGS_CUDA(ctx, cudaMemsetAsync(b.bctl.p, 0, 8, ctx->stream));
+        }
+        IGS_PDL(ctx, lq_build_kernel, ctx->sm_count, kBuildThreads, 0, (const ScanRec*)ctx->scan, n, L, cells, cnt,
+                cur, off, (uint32_t*)b.key.p, (uint32_t*)b.mem.p, (ScanRec*)b.mrec.p, (uint32_t*)b.minv.p,
+                (Acc*)b.acc.p, (uint32_t*)b.lcount.p, (unsigned*)b.bctl.p);
+    } else {
+        IGS_PDL(ctx, lq_clear, 2 * ctx->sm_count, 256, 0, cells, cnt, (Acc*)b.acc.p, (uint32_t*)b.lcount.p);
+        IGS_PDL(ctx, lq_count, (n + 255) / 256, 256, 0, (const ScanRec*)ctx->scan, n, L, cnt, (uint32_t*)b.key.p,
+                (uint32_t*)b.lcount.p);
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, (int)cells, ctx->stream);
+        if (!grow(b.cub_tmp, tb)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn scan)");
+        IGS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(b.cub_tmp.p, tb, cnt, off, (int)cells, ctx->stream));
+        ctx->launches += 2;
+        IGS_PDL(ctx, lq_fill, (n + 255) / 256, 256, 0, (const ScanRec*)ctx->scan, n, (const uint32_t*)b.key.p,
+                (const uint32_t*)off, cur, (uint32_t*)b.mem.p, (ScanRec*)b.mrec.p, (uint32_t*)b.minv.p,
+                (Acc*)b.acc.p);
+    }
     const int nb = (G0 + kBlk - 1) / kBlk;
     IGS_PDL(ctx, lq_tree_kernel, nb * nb, 256, 0, (Acc*)b.acc.p, L, (const uint32_t*)cnt, (Sum*)b.own.p,
             (Sum*)b.sub.p, (unsigned int*)b.ticket.p, search_inputs(ctx, b), job);
@@ -1940,7 +2065,7 @@ void igs_knn_free(igs_ctx* ctx) {
     if (getenv("IGS_KNN_STATS"))
         fprintf(stderr, "knn tree: %llu builds, %llu refits\n", (unsigned long long)b->builds,
                 (unsigned long long)b->refits);
-    for (DevBuf* d : {&b->mrec, &b->minv, &b->cnt, &b->off, &b->key, &b->mem, &b->own, &b->sub, &b->cub_tmp, &b->hard, &b->ticket,
+    for (DevBuf* d : {&b->bctl, &b->mrec, &b->minv, &b->cnt, &b->off, &b->key, &b->mem, &b->own, &b->sub, &b->cub_tmp, &b->hard, &b->ticket,
                       &b->part, &b->lcount, &b->acc})
         cudaFree(d->p);
     delete b;

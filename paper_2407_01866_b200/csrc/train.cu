@@ -168,17 +168,6 @@ __global__ void scatter_slots_kernel(const uint32_t* __restrict__ keys, uint32_t
 constexpr int kOffThreads = 256;
 constexpr int kOffPer = 4;  // counts per thread and chunk pass
 
-__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned target) {
-    __syncthreads();  // the CTA's writes are ordered before thread 0's release
-    if (threadIdx.x == 0) {
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-        unsigned v;
-        do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-        } while (v < target);
-    }
-    __syncthreads();
-}
 
 __global__ void __launch_bounds__(kOffThreads) offsets_scatter_kernel(
     const uint32_t* __restrict__ gcnt, uint32_t n, uint32_t* __restrict__ goff, uint32_t* __restrict__ chunk_sum,
@@ -210,7 +199,7 @@ __global__ void __launch_bounds__(kOffThreads) offsets_scatter_kernel(
         const uint32_t agg = BlockReduce(rtmp).Sum(total);
         if (threadIdx.x == 0) chunk_sum[blockIdx.x] = agg;
     }
-    grid_sync(bar, G);
+    igs_grid_sync(bar, G);
     // the chunk's base: the totals of the chunks before it
     uint32_t mine = 0;
     for (uint32_t b = threadIdx.x; b < blockIdx.x; b += kOffThreads) mine += *(volatile uint32_t*)(chunk_sum + b);
@@ -243,7 +232,7 @@ __global__ void __launch_bounds__(kOffThreads) offsets_scatter_kernel(
         }
         run += agg;
     }
-    grid_sync(bar, 2 * G);
+    igs_grid_sync(bar, 2 * G);
     // scatter (scatter_slots_kernel)
     for (uint32_t slot = blockIdx.x * kOffThreads + threadIdx.x; slot < items; slot += G * kOffThreads) {
         const uint32_t g = keys[slot];

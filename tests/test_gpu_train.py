@@ -275,8 +275,9 @@ def test_long_segments_reference_order(gctx, port, n, ns):
 def test_alternate_kernels_bit_identical(gctx, port, monkeypatch, k):
     """The K <= 16 search runs two points per warp (knn_points16_kernel) and
     the reduction's offsets + scatter run as one persistent launch; the
-    one-point-per-warp search (IGS_KNN_FULLWARP) and the CUB scan + scatter
-    (IGS_CUB_SCAN) select and sum identically, so 8 iterations give the same
+    one-point-per-warp search (IGS_KNN_FULLWARP), the CUB scan + scatter
+    (IGS_CUB_SCAN) and the five-launch tree build (IGS_KNN_BUILD_LAUNCHES)
+    select and sum identically, so 8 iterations give the same
     losses and parameters bit for bit (K = 24 takes the full-warp search
     either way)."""
     target = synth.photo_like_image(160, 120, 31013)
@@ -292,6 +293,7 @@ def test_alternate_kernels_bit_identical(gctx, port, monkeypatch, k):
     l0, p0 = run()
     monkeypatch.setenv("IGS_KNN_FULLWARP", "1")
     monkeypatch.setenv("IGS_CUB_SCAN", "1")
+    monkeypatch.setenv("IGS_KNN_BUILD_LAUNCHES", "1")
     l1, p1 = run()
     assert l0 == l1
     assert np.array_equal(p0, p1)
