@@ -1165,7 +1165,7 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
                                                               uint32_t* __restrict__ hard_list,
                                                               unsigned long long* __restrict__ hard_stat,
                                                               uint32_t* __restrict__ next_point,
-                                                              uint32_t* __restrict__ zero_next) {
+                                                              uint32_t* __restrict__ zero_next, int hand_off) {
     __shared__ uint32_t queue[4][2][2][kQueue16];
     __shared__ int s_loff[kMaxLv];
     __shared__ int s_lg[kMaxLv];
@@ -1375,7 +1375,9 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
         ncur = nnext;
     }
 
-    // frontier overflow: the hard-point scan, or (beyond its capacity) all N here
+    // frontier overflow (rare: the first steps from an initial set): all N
+    // scanned here by this half-warp -- or, with hand_off, handed to the
+    // split hard-point scan up to its capacity
     bool handed = false;
     if (__ballot_sync(0xffffffffu, overflow && active)) {
         const bool mine = overflow && active;
@@ -1387,7 +1389,7 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
         slot = __shfl_sync(0xffffffffu, slot, 0, 16);
         bool brute = false;
         if (mine) {
-            if (slot < kHardCap) {
+            if (hand_off && slot < kHardCap) {
                 if (hl == 0) hard_list[slot] = pt;
                 handed = true;
             } else {
@@ -1709,14 +1711,27 @@ int launch_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int 
     const bool halves = kk <= 16 && !getenv("IGS_KNN_FULLWARP");  // (A/B switch for tests and profiling)
     if (b.knn_blocks[halves] == 0) {
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, halves ? knn_points16_kernel : knn_points_kernel,
-                                                      128, 0);
+        if (halves)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, knn_points16_kernel, 128, 0);
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, knn_points_kernel, 128, 0);
         b.knn_blocks[halves] = std::max(1, per_sm) * ctx->sm_count;
     }
     const uint64_t per_block = halves ? 8 : 4;
     const unsigned blocks =
         (unsigned)std::min<uint64_t>(b.knn_blocks[halves], ((uint64_t)npts + per_block - 1) / per_block);
-    IGS_PDL(ctx, halves ? knn_points16_kernel : knn_points_kernel, blocks, 128, 0, (const ScanRec*)ctx->scan, ctx->n,
+    // the split hard-point scan (a launch of its own, even when empty) only
+    // for the full-warp search or on request; the half-warp search scans an
+    // overflowing point's whole set itself
+    const bool hand_off = !halves || getenv("IGS_KNN_HARD_SPLIT") != nullptr;
+    if (halves)
+        IGS_PDL(ctx, knn_points16_kernel, blocks, 128, 0, (const ScanRec*)ctx->scan, ctx->n,
+                b.lq, (const Sum*)b.own.p, (const Sum*)b.sub.p, (const uint32_t*)b.off.p, (const uint32_t*)b.mem.p,
+            (const ScanRec*)b.mrec.p, uv,
+            W, H, npts, kk, E, igs_prof_counter(ctx, IGS_PROF_SCAN), hard_count, hard_list,
+            igs_prof_counter(ctx, IGS_PROF_KNN_HARD), cursor, zero_next, (int)hand_off);
+    else
+        IGS_PDL(ctx, knn_points_kernel, blocks, 128, 0, (const ScanRec*)ctx->scan, ctx->n,
             b.lq, (const Sum*)b.own.p, (const Sum*)b.sub.p, (const uint32_t*)b.off.p, (const uint32_t*)b.mem.p,
             (const ScanRec*)b.mrec.p, uv,
             W, H, npts, kk, E, igs_prof_counter(ctx, IGS_PROF_SCAN), hard_count, hard_list,
@@ -1725,7 +1740,7 @@ int launch_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int 
     if (!grow(b.part, pitems * 12)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
     double* part_q = (double*)b.part.p;
     uint32_t* part_i = (uint32_t*)(part_q + pitems);
-    IGS_PDL(ctx, hard_scan_kernel<KCAP>, ctx->sm_count, kHardThreads, 0, (const ScanRec*)ctx->scan, ctx->n, uv,
+    if (hand_off) IGS_PDL(ctx, hard_scan_kernel<KCAP>, ctx->sm_count, kHardThreads, 0, (const ScanRec*)ctx->scan, ctx->n, uv,
             W, H, kk, (const uint32_t*)hard_count, (const uint32_t*)hard_list, E, part_q, part_i,
             (unsigned int*)((uint32_t*)b.hard.p + 4 + kHardCap), igs_prof_counter(ctx, IGS_PROF_SCAN));
     igs_prof_end(ctx, IGS_PROF_SCAN, 0.0);

@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 from paper_2407_01866_b200 import synth
+from paper_2407_01866_b200.igs import PROF_KNN_HARD
 
 pytestmark = pytest.mark.gpu
 
@@ -46,6 +47,36 @@ def test_fuzz_points_and_render(gctx, port, seed):
     got, gtk = gctx.render_image(W, H, k, want_topk=True)
     assert np.array_equal(gtk, wtk), (seed, n, k, W, H)
     assert np.max(np.abs(got.astype(np.float64) - want)) <= 1e-4
+
+
+@pytest.mark.parametrize("seed", [0, 3, 5, 8])
+def test_fuzz_points_hard_split(gctx, port, monkeypatch, seed):
+    """The same sweep with frontier overflows handed to the split hard-point
+    scan (IGS_KNN_HARD_SPLIT) instead of scanned by the overflowing warp."""
+    monkeypatch.setenv("IGS_KNN_HARD_SPLIT", "1")
+    test_fuzz_points_and_render(gctx, port, seed)
+
+
+@pytest.mark.parametrize("seed,k", [(9, 10), (26, 16), (27, 16)])
+def test_frontier_overflow_both_paths(gctx, port, monkeypatch, seed, k):
+    """Sweep cases whose search frontier overflows at some points (counted by
+    the device): both overflow paths -- the whole set scanned by the
+    overflowing half-warp (default), the split hard-point scan
+    (IGS_KNN_HARD_SPLIT) -- return the oracle's top-K."""
+    params = random_case(np.random.default_rng(1000 + seed))
+    gctx.set_params(params)
+    uv = np.random.default_rng(seed).random((300, 2))
+    for split in (False, True):
+        if split:
+            monkeypatch.setenv("IGS_KNN_HARD_SPLIT", "1")
+        gctx.profile_enable(True)
+        idx, w, cnt = gctx.select_top_k(uv, k)
+        hard = gctx.profile_read(PROF_KNN_HARD)[2]
+        gctx.profile_enable(False)
+        assert hard > 0  # the case does overflow
+        for p in range(uv.shape[0]):
+            wi, _ = port.select_top_k(params, uv[p, 0], uv[p, 1], k)
+            assert np.array_equal(idx[p, :cnt[p]], wi), (split, p)
 
 
 @pytest.mark.parametrize("seed", range(4))
