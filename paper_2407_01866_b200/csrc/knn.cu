@@ -1375,9 +1375,9 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
         ncur = nnext;
     }
 
-    // frontier overflow (rare: the first steps from an initial set): all N
-    // scanned here by this half-warp -- or, with hand_off, handed to the
-    // split hard-point scan up to its capacity
+    // frontier overflow (rare: the first steps from an initial set): handed
+    // to the split hard-point scan up to its capacity (hand_off), else all N
+    // scanned here by this half-warp
     bool handed = false;
     if (__ballot_sync(0xffffffffu, overflow && active)) {
         const bool mine = overflow && active;
@@ -1720,10 +1720,12 @@ int launch_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int 
     const uint64_t per_block = halves ? 8 : 4;
     const unsigned blocks =
         (unsigned)std::min<uint64_t>(b.knn_blocks[halves], ((uint64_t)npts + per_block - 1) / per_block);
-    // the split hard-point scan (a launch of its own, even when empty) only
-    // for the full-warp search or on request; the half-warp search scans an
-    // overflowing point's whole set itself
-    const bool hand_off = !halves || getenv("IGS_KNN_HARD_SPLIT") != nullptr;
+    // frontier overflows go to the split hard-point scan (a launch of its
+    // own, ~1.4 us per step even when empty); IGS_KNN_HARD_INWARP: the
+    // half-warp search scans an overflowing point's whole set itself and the
+    // launch is skipped -- cheaper when nothing overflows, but a half-warp
+    // scanning all N serially takes milliseconds when something does
+    const bool hand_off = !halves || getenv("IGS_KNN_HARD_INWARP") == nullptr;
     if (halves)
         IGS_PDL(ctx, knn_points16_kernel, blocks, 128, 0, (const ScanRec*)ctx->scan, ctx->n,
                 b.lq, (const Sum*)b.own.p, (const Sum*)b.sub.p, (const uint32_t*)b.off.p, (const uint32_t*)b.mem.p,

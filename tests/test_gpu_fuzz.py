@@ -50,25 +50,25 @@ def test_fuzz_points_and_render(gctx, port, seed):
 
 
 @pytest.mark.parametrize("seed", [0, 3, 5, 8])
-def test_fuzz_points_hard_split(gctx, port, monkeypatch, seed):
-    """The same sweep with frontier overflows handed to the split hard-point
-    scan (IGS_KNN_HARD_SPLIT) instead of scanned by the overflowing warp."""
-    monkeypatch.setenv("IGS_KNN_HARD_SPLIT", "1")
+def test_fuzz_points_hard_inwarp(gctx, port, monkeypatch, seed):
+    """The same sweep with frontier overflows scanned by the overflowing
+    half-warp (IGS_KNN_HARD_INWARP) instead of the split hard-point scan."""
+    monkeypatch.setenv("IGS_KNN_HARD_INWARP", "1")
     test_fuzz_points_and_render(gctx, port, seed)
 
 
 @pytest.mark.parametrize("seed,k", [(9, 10), (26, 16), (27, 16)])
 def test_frontier_overflow_both_paths(gctx, port, monkeypatch, seed, k):
     """Sweep cases whose search frontier overflows at some points (counted by
-    the device): both overflow paths -- the whole set scanned by the
-    overflowing half-warp (default), the split hard-point scan
-    (IGS_KNN_HARD_SPLIT) -- return the oracle's top-K."""
+    the device): both overflow paths -- the split hard-point scan
+    (default), the whole set scanned by the overflowing half-warp
+    (IGS_KNN_HARD_INWARP) -- return the oracle's top-K."""
     params = random_case(np.random.default_rng(1000 + seed))
     gctx.set_params(params)
     uv = np.random.default_rng(seed).random((300, 2))
-    for split in (False, True):
-        if split:
-            monkeypatch.setenv("IGS_KNN_HARD_SPLIT", "1")
+    for inwarp in (False, True):
+        if inwarp:
+            monkeypatch.setenv("IGS_KNN_HARD_INWARP", "1")
         gctx.profile_enable(True)
         idx, w, cnt = gctx.select_top_k(uv, k)
         hard = gctx.profile_read(PROF_KNN_HARD)[2]
@@ -76,7 +76,7 @@ def test_frontier_overflow_both_paths(gctx, port, monkeypatch, seed, k):
         assert hard > 0  # the case does overflow
         for p in range(uv.shape[0]):
             wi, _ = port.select_top_k(params, uv[p, 0], uv[p, 1], k)
-            assert np.array_equal(idx[p, :cnt[p]], wi), (split, p)
+            assert np.array_equal(idx[p, :cnt[p]], wi), (inwarp, p)
 
 
 @pytest.mark.parametrize("seed", range(4))
