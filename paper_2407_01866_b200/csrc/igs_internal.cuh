@@ -167,6 +167,21 @@ __device__ __forceinline__ float clamp01f(double v) { return (float)(v < 0.0 ? 0
 // pixel_center (image.hpp:18-20)
 __device__ __forceinline__ double center(int i, int n) { return __ddiv_rn(__dadd_rn((double)i, 0.5), (double)n); }
 
+// Arguments of the deterministic reduction's offsets + slot scatter (reduce.cuh).
+struct OffArgs {
+    const uint32_t* gcnt;  // per-Gaussian counts | [n, 2n) cursors
+    uint32_t n;
+    uint32_t* goff;
+    uint32_t* chunk_sum;   // gridDim.x entries
+    const uint32_t* keys;
+    uint32_t items;
+    uint32_t* gcur;
+    uint32_t* perm;
+    uint32_t* long_count;
+    uint32_t* long_list;
+    unsigned* bar;         // [0] arrivals, [1] exits
+};
+
 }  // namespace igs_dev
 
 // ---------------------------------------------------------------------------
@@ -263,7 +278,10 @@ struct igs_ctx {
     DevBuf async_pin[4];
     cudaEvent_t async_ev[2] = {nullptr, nullptr};
     StageJob stage_job;          // handed from igs_forward_backward to knn_build (see StageJob)
-    int off_blocks = 0;          // offsets_scatter_kernel grid (co-resident)
+    struct {
+        igs_dev::OffArgs args;   // reduce.cuh: offsets + scatter the kNN launch may take over
+        bool ready = false, done = false;
+    } fuse_off;
     bool off_ctl_ready = false;  // its barrier counters zeroed (scratch 34)
     bool loss_ticket_ready = false;  // long_segment_kernel's loss ticket zeroed (scratch 35)
     int async_head = 0, async_count = 0;

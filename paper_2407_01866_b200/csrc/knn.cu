@@ -40,6 +40,7 @@
 
 #include "igs_internal.cuh"
 #include "knn_tree.cuh"
+#include "reduce.cuh"
 
 using namespace igs_dev;
 
@@ -1466,19 +1467,17 @@ __device__ __forceinline__ void hard_merge_point(const ScanRec* __restrict__ sca
     warp_epilogue<32>(E, scan, pt, true, kk, lane, t.q, t.i, px, py);
 }
 
+// The (point, split) items of the hard points (cnt of them) for a CTA of
+// at least kHardThreads threads, item = blockIdx.x, += gridDim.x.
 template <int KCAP>
-__global__ void __launch_bounds__(kHardThreads) hard_scan_kernel(const ScanRec* __restrict__ scan, uint32_t n,
-                                                                 const double* __restrict__ uv, int W, int H, int kk,
-                                                                 const uint32_t* __restrict__ hard_count,
-                                                                 const uint32_t* __restrict__ hard_list, Epi E,
-                                                                 double* __restrict__ part_q,
-                                                                 uint32_t* __restrict__ part_i,
-                                                                 unsigned int* __restrict__ point_done,
-                                                                 unsigned long long* __restrict__ pairs) {
+__device__ __forceinline__ void hard_scan_items(const ScanRec* __restrict__ scan, uint32_t n,
+                                                const double* __restrict__ uv, int W, int H, int kk, uint32_t cnt,
+                                                const uint32_t* __restrict__ hard_list, const Epi& E,
+                                                double* __restrict__ part_q, uint32_t* __restrict__ part_i,
+                                                unsigned int* __restrict__ point_done,
+                                                unsigned long long* __restrict__ pairs) {
     __shared__ double sq[kHardThreads * KCAP];
     __shared__ uint32_t si[kHardThreads * KCAP];
-    pdl_wait();
-    const uint32_t cnt = min(*hard_count, kHardCap);
     const uint32_t per = (n + kHardSplit - 1) / kHardSplit;
     for (uint32_t item = blockIdx.x; item < cnt * kHardSplit; item += gridDim.x) {
         const uint32_t slot = item / kHardSplit, split = item % kHardSplit;
@@ -1490,7 +1489,8 @@ __global__ void __launch_bounds__(kHardThreads) hard_scan_kernel(const ScanRec* 
         t.init(kk);
         // 4 independent records in flight per thread; the (rare) insertion
         // sits behind a warp vote so it stays a branch, not predicated code
-        for (uint32_t base = g0; base < g1; base += 4 * kHardThreads) {
+        // (threads past kHardThreads, in a wider CTA, only join the barriers)
+        for (uint32_t base = g0 + (threadIdx.x < kHardThreads ? 0u : g1 - g0); base < g1; base += 4 * kHardThreads) {
             double q[4];
             uint32_t gi[4];
 #pragma unroll
@@ -1506,7 +1506,7 @@ __global__ void __launch_bounds__(kHardThreads) hard_scan_kernel(const ScanRec* 
             }
         }
         __syncthreads();
-        store_topk(t, sq + threadIdx.x * KCAP, si + threadIdx.x * KCAP);
+        if (threadIdx.x < kHardThreads) store_topk(t, sq + threadIdx.x * KCAP, si + threadIdx.x * KCAP);
         __syncthreads();
         if (threadIdx.x < 32) {
             const int lane = threadIdx.x;
@@ -1558,6 +1558,45 @@ __global__ void __launch_bounds__(kHardThreads) hard_scan_kernel(const ScanRec* 
             }
         }
     }
+}
+
+template <int KCAP>
+__global__ void __launch_bounds__(kHardThreads) hard_scan_kernel(const ScanRec* __restrict__ scan, uint32_t n,
+                                                                 const double* __restrict__ uv, int W, int H, int kk,
+                                                                 const uint32_t* __restrict__ hard_count,
+                                                                 const uint32_t* __restrict__ hard_list, Epi E,
+                                                                 double* __restrict__ part_q,
+                                                                 uint32_t* __restrict__ part_i,
+                                                                 unsigned int* __restrict__ point_done,
+                                                                 unsigned long long* __restrict__ pairs) {
+    pdl_wait();
+    hard_scan_items<KCAP>(scan, n, uv, W, H, kk, min(*hard_count, kHardCap), hard_list, E, part_q, part_i, point_done,
+                          pairs);
+}
+
+// The hard-point scan and the reduction's offsets + scatter in one persistent
+// launch (one CTA per SM): the hard points' contributions (when there are
+// any) land before a grid barrier, then offsets_scatter_body.  Saves the
+// hard-point scan's own launch, which the chain pays even when it is empty.
+template <int KCAP>
+__global__ void __launch_bounds__(kOffThreads) hard_offsets_kernel(const ScanRec* __restrict__ scan, uint32_t n,
+                                                                   const double* __restrict__ uv, int W, int H, int kk,
+                                                                   const uint32_t* __restrict__ hard_count,
+                                                                   const uint32_t* __restrict__ hard_list, Epi E,
+                                                                   double* __restrict__ part_q,
+                                                                   uint32_t* __restrict__ part_i,
+                                                                   unsigned int* __restrict__ point_done,
+                                                                   unsigned long long* __restrict__ pairs,
+                                                                   OffArgs A) {
+    pdl_wait();
+    const uint32_t cnt = min(*hard_count, kHardCap);
+    unsigned base = 0;
+    if (cnt) {  // (uniform: every CTA read the same count)
+        hard_scan_items<KCAP>(scan, n, uv, W, H, kk, cnt, hard_list, E, part_q, part_i, point_done, pairs);
+        igs_grid_sync(A.bar, gridDim.x);
+        base = gridDim.x;
+    }
+    offsets_scatter_body(A, base);
 }
 
 
@@ -1742,9 +1781,24 @@ int launch_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int 
     if (!grow(b.part, pitems * 12)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
     double* part_q = (double*)b.part.p;
     uint32_t* part_i = (uint32_t*)(part_q + pitems);
-    if (hand_off) IGS_PDL(ctx, hard_scan_kernel<KCAP>, ctx->sm_count, kHardThreads, 0, (const ScanRec*)ctx->scan, ctx->n, uv,
-            W, H, kk, (const uint32_t*)hard_count, (const uint32_t*)hard_list, E, part_q, part_i,
-            (unsigned int*)((uint32_t*)b.hard.p + 4 + kHardCap), igs_prof_counter(ctx, IGS_PROF_SCAN));
+    bool fused_off = false;
+    if constexpr (KCAP <= 16) {
+        if (hand_off && ctx->fuse_off.ready) {
+            // the reduction's offsets + scatter ride in the same launch
+            ctx->fuse_off.ready = false;
+            ctx->fuse_off.done = true;
+            fused_off = true;
+            IGS_PDL(ctx, hard_offsets_kernel<KCAP>, ctx->sm_count, kOffThreads, 0, (const ScanRec*)ctx->scan, ctx->n,
+                    uv, W, H, kk, (const uint32_t*)hard_count, (const uint32_t*)hard_list, E, part_q, part_i,
+                    (unsigned int*)((uint32_t*)b.hard.p + 4 + kHardCap), igs_prof_counter(ctx, IGS_PROF_SCAN),
+                    ctx->fuse_off.args);
+        }
+    }
+    if (hand_off && !fused_off) {
+        IGS_PDL(ctx, hard_scan_kernel<KCAP>, ctx->sm_count, kHardThreads, 0, (const ScanRec*)ctx->scan, ctx->n, uv,
+                W, H, kk, (const uint32_t*)hard_count, (const uint32_t*)hard_list, E, part_q, part_i,
+                (unsigned int*)((uint32_t*)b.hard.p + 4 + kHardCap), igs_prof_counter(ctx, IGS_PROF_SCAN));
+    }
     igs_prof_end(ctx, IGS_PROF_SCAN, 0.0);
     return IGS_OK;
 }

@@ -1,0 +1,112 @@
+// reduce.cuh -- the deterministic reduction's offsets + slot scatter as a
+// device body, shared by offsets_scatter_kernel (train.cu) and the fused
+// hard-point scan + offsets launch (knn.cu).
+#pragma once
+
+#include <cub/cub.cuh>
+
+#include "igs_internal.cuh"
+
+namespace igs_dev {
+
+constexpr uint32_t kShortSeg = 32;  // longer segments go to long_segment_kernel
+constexpr int kOffThreads = 256;
+constexpr int kOffPer = 4;  // counts per thread and chunk pass
+
+// (OffArgs: igs_internal.cuh)
+
+// Segment offsets (exclusive scan of the per-Gaussian counts) and the slot
+// scatter for a persistent, co-resident grid of kOffThreads-thread CTAs:
+// every CTA scans its chunk of the counts, a grid barrier publishes the
+// chunk totals, each CTA adds its base and writes the offsets, a second
+// barrier, then the scatter (slot ids at offset + arrival rank; every
+// Gaussian with more than kShortSeg contributions queued once).  Barrier
+// targets start at bar_base (arrivals already counted by the caller); the
+// last CTA out resets the counters for the next launch.
+__device__ __forceinline__ void offsets_scatter_body(const OffArgs& A, unsigned bar_base) {
+    using BlockScan = cub::BlockScan<uint32_t, kOffThreads>;
+    __shared__ typename BlockScan::TempStorage tmp;
+    __shared__ uint32_t s_base;
+    const uint32_t* __restrict__ gcnt = A.gcnt;
+    const uint32_t n = A.n;
+    uint32_t* __restrict__ goff = A.goff;
+    uint32_t* __restrict__ chunk_sum = A.chunk_sum;
+    const uint32_t* __restrict__ keys = A.keys;
+    const uint32_t items = A.items;
+    uint32_t* __restrict__ gcur = A.gcur;
+    uint32_t* __restrict__ perm = A.perm;
+    uint32_t* __restrict__ long_count = A.long_count;
+    uint32_t* __restrict__ long_list = A.long_list;
+    unsigned* __restrict__ bar = A.bar;
+    const uint32_t G = gridDim.x;
+    // chunk of CTA b: [b * per_cta, (b + 1) * per_cta), per_cta a multiple of kOffThreads * kOffPer
+    const uint32_t tile = kOffThreads * kOffPer;
+    const uint32_t per_cta = ((n + G - 1) / G + tile - 1) / tile * tile;
+    const uint32_t c0 = blockIdx.x * per_cta, c1 = min(n, c0 + per_cta);
+    // pass 1: chunk total
+    uint32_t total = 0;
+    for (uint32_t b = c0; b < c1; b += tile) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int j = 0; j < kOffPer; ++j) {
+            const uint32_t i = b + threadIdx.x * kOffPer + j;
+            if (i < c1) v += gcnt[i];
+        }
+        total += v;
+    }
+    {
+        using BlockReduce = cub::BlockReduce<uint32_t, kOffThreads>;
+        __shared__ typename BlockReduce::TempStorage rtmp;
+        const uint32_t agg = BlockReduce(rtmp).Sum(total);
+        if (threadIdx.x == 0) chunk_sum[blockIdx.x] = agg;
+    }
+    igs_grid_sync(A.bar, bar_base + G);
+    // the chunk's base: the totals of the chunks before it
+    uint32_t mine = 0;
+    for (uint32_t b = threadIdx.x; b < blockIdx.x; b += kOffThreads) mine += *(volatile uint32_t*)(chunk_sum + b);
+    {
+        using BlockReduce = cub::BlockReduce<uint32_t, kOffThreads>;
+        __shared__ typename BlockReduce::TempStorage rtmp2;
+        const uint32_t base = BlockReduce(rtmp2).Sum(mine);
+        if (threadIdx.x == 0) s_base = base;
+    }
+    __syncthreads();
+    uint32_t run = s_base;
+    // pass 2: offsets
+    for (uint32_t b = c0; b < c1; b += tile) {
+        uint32_t v[kOffPer], sum = 0;
+#pragma unroll
+        for (int j = 0; j < kOffPer; ++j) {
+            const uint32_t i = b + threadIdx.x * kOffPer + j;
+            v[j] = i < c1 ? gcnt[i] : 0u;
+            sum += v[j];
+        }
+        uint32_t excl, agg;
+        BlockScan(tmp).ExclusiveSum(sum, excl, agg);
+        __syncthreads();  // tmp reused next pass
+        uint32_t o = run + excl;
+#pragma unroll
+        for (int j = 0; j < kOffPer; ++j) {
+            const uint32_t i = b + threadIdx.x * kOffPer + j;
+            if (i < c1) goff[i] = o;
+            o += v[j];
+        }
+        run += agg;
+    }
+    igs_grid_sync(A.bar, bar_base + 2 * G);
+    // scatter (scatter_slots_kernel)
+    for (uint32_t slot = blockIdx.x * kOffThreads + threadIdx.x; slot < items; slot += G * kOffThreads) {
+        const uint32_t g = keys[slot];
+        if (g >= n) continue;
+        const uint32_t pos = atomicAdd(gcur + g, 1u);
+        perm[__ldcg(goff + g) + pos] = slot;  // (written by other CTAs: read through L2)
+        if (pos == 0 && gcnt[g] > kShortSeg) long_list[atomicAdd(long_count, 1u)] = g;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(bar + 1, 1u) == G - 1) {
+        bar[0] = 0;
+        bar[1] = 0;
+    }
+}
+
+}  // namespace igs_dev

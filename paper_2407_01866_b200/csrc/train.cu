@@ -28,6 +28,7 @@
 
 #include "igs_internal.cuh"
 #include "knn_tree.cuh"
+#include "reduce.cuh"
 
 using namespace igs_dev;
 
@@ -140,7 +141,6 @@ __global__ void sample_finish_kernel(const ScanRec* __restrict__ scan, const Sha
 }
 
 // --- counting-sort reduction (deterministic, reference summation order) ----
-constexpr uint32_t kShortSeg = 32;  // longer segments go to long_segment_kernel
 // keys[slot] = Gaussian of contribution slot (slot = sample * kk + entry, so
 // slot order is sample order).  gcnt/goff: per-Gaussian count / offset.
 // (also queues every Gaussian with a long segment for long_segment_kernel)
@@ -165,87 +165,11 @@ __global__ void scatter_slots_kernel(const uint32_t* __restrict__ keys, uint32_t
 // The grid is sized to be co-resident (a few CTAs per SM), so the spinning
 // barrier cannot wait on a CTA that is not running; bar[0] counts arrivals,
 // bar[1] exits, and the last CTA out resets both for the next launch.
-constexpr int kOffThreads = 256;
-constexpr int kOffPer = 4;  // counts per thread and chunk pass
 
 
-__global__ void __launch_bounds__(kOffThreads) offsets_scatter_kernel(
-    const uint32_t* __restrict__ gcnt, uint32_t n, uint32_t* __restrict__ goff, uint32_t* __restrict__ chunk_sum,
-    const uint32_t* __restrict__ keys, uint32_t items, uint32_t* __restrict__ gcur, uint32_t* __restrict__ perm,
-    uint32_t* __restrict__ long_count, uint32_t* __restrict__ long_list, unsigned* __restrict__ bar) {
-    using BlockScan = cub::BlockScan<uint32_t, kOffThreads>;
-    __shared__ typename BlockScan::TempStorage tmp;
-    __shared__ uint32_t s_base;
+__global__ void __launch_bounds__(kOffThreads) offsets_scatter_kernel(OffArgs A) {
     pdl_wait();
-    const uint32_t G = gridDim.x;
-    // chunk of CTA b: [b * per_cta, (b + 1) * per_cta), per_cta a multiple of kOffThreads * kOffPer
-    const uint32_t tile = kOffThreads * kOffPer;
-    const uint32_t per_cta = ((n + G - 1) / G + tile - 1) / tile * tile;
-    const uint32_t c0 = blockIdx.x * per_cta, c1 = min(n, c0 + per_cta);
-    // pass 1: chunk total
-    uint32_t total = 0;
-    for (uint32_t b = c0; b < c1; b += tile) {
-        uint32_t v = 0;
-#pragma unroll
-        for (int j = 0; j < kOffPer; ++j) {
-            const uint32_t i = b + threadIdx.x * kOffPer + j;
-            if (i < c1) v += gcnt[i];
-        }
-        total += v;
-    }
-    {
-        using BlockReduce = cub::BlockReduce<uint32_t, kOffThreads>;
-        __shared__ typename BlockReduce::TempStorage rtmp;
-        const uint32_t agg = BlockReduce(rtmp).Sum(total);
-        if (threadIdx.x == 0) chunk_sum[blockIdx.x] = agg;
-    }
-    igs_grid_sync(bar, G);
-    // the chunk's base: the totals of the chunks before it
-    uint32_t mine = 0;
-    for (uint32_t b = threadIdx.x; b < blockIdx.x; b += kOffThreads) mine += *(volatile uint32_t*)(chunk_sum + b);
-    {
-        using BlockReduce = cub::BlockReduce<uint32_t, kOffThreads>;
-        __shared__ typename BlockReduce::TempStorage rtmp2;
-        const uint32_t base = BlockReduce(rtmp2).Sum(mine);
-        if (threadIdx.x == 0) s_base = base;
-    }
-    __syncthreads();
-    uint32_t run = s_base;
-    // pass 2: offsets
-    for (uint32_t b = c0; b < c1; b += tile) {
-        uint32_t v[kOffPer], sum = 0;
-#pragma unroll
-        for (int j = 0; j < kOffPer; ++j) {
-            const uint32_t i = b + threadIdx.x * kOffPer + j;
-            v[j] = i < c1 ? gcnt[i] : 0u;
-            sum += v[j];
-        }
-        uint32_t excl, agg;
-        BlockScan(tmp).ExclusiveSum(sum, excl, agg);
-        __syncthreads();  // tmp reused next pass
-        uint32_t o = run + excl;
-#pragma unroll
-        for (int j = 0; j < kOffPer; ++j) {
-            const uint32_t i = b + threadIdx.x * kOffPer + j;
-            if (i < c1) goff[i] = o;
-            o += v[j];
-        }
-        run += agg;
-    }
-    igs_grid_sync(bar, 2 * G);
-    // scatter (scatter_slots_kernel)
-    for (uint32_t slot = blockIdx.x * kOffThreads + threadIdx.x; slot < items; slot += G * kOffThreads) {
-        const uint32_t g = keys[slot];
-        if (g >= n) continue;
-        const uint32_t pos = atomicAdd(gcur + g, 1u);
-        perm[__ldcg(goff + g) + pos] = slot;  // (written by other CTAs: read through L2)
-        if (pos == 0 && gcnt[g] > kShortSeg) long_list[atomicAdd(long_count, 1u)] = g;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && atomicAdd(bar + 1, 1u) == G - 1) {
-        bar[0] = 0;
-        bar[1] = 0;
-    }
+    offsets_scatter_body(A, 0);
 }
 
 __device__ __forceinline__ void sum_row(const double* __restrict__ contrib, uint32_t slot, double* acc) {
@@ -970,10 +894,23 @@ int igs_status_reset(igs_ctx* ctx) {
 // sample-ordered sums, so the result is bit-identical to one GPU's
 // (SURVEY.md 8e's all-gather alternative; fewer bytes than an all-reduce
 // of the gradients).
+// barrier counters [0, 2) + chunk totals of the persistent offsets launch
+// (one CTA per SM), zeroed once
+static uint32_t* off_ctl(igs_ctx* ctx) {
+    uint32_t* ctl = (uint32_t*)igs_scratch(ctx, 34, ((size_t)ctx->sm_count + 2) * sizeof(uint32_t));
+    if (ctl && !ctx->off_ctl_ready) {
+        if (cudaMemsetAsync(ctl, 0, 2 * sizeof(uint32_t), ctx->stream) != cudaSuccess) return nullptr;
+        ctx->off_ctl_ready = true;
+    }
+    return ctl;
+}
+
 int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint32_t* dev_sidx,
                          const double* dev_samples5, double* dev_loss, double inv_n, const double* fuse_lr4,
                          long long t, bool* fused, const StageJob* job) {
     if (fused) *fused = false;
+    ctx->fuse_off.ready = false;
+    ctx->fuse_off.done = false;
     const uint32_t n = ctx->n;
     const int kk = (int)std::min<uint32_t>((uint32_t)k, n);
     const bool knn_path = ctx->opt_cull && kk <= 32;
@@ -1023,11 +960,23 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
             l2pf_add(pf, ctx->adam_v, (size_t)n * 64);
         }
         ctx->stage_job = job ? *job : StageJob{};  // knn_build runs it (or launches it) first
+        // single rank, deterministic: the search's hard-point launch may run
+        // the reduction's offsets + scatter too (hard_offsets_kernel)
+        ctx->fuse_off.ready = false;
+        ctx->fuse_off.done = false;
+        if (ctx->opt_deterministic && !exch && !getenv("IGS_CUB_SCAN")) {
+            uint32_t* ctl = off_ctl(ctx);
+            if (!ctl) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (scan)");
+            ctx->fuse_off.args = OffArgs{(const uint32_t*)gcnt, n, goff, ctl + 2, (const uint32_t*)keys, (uint32_t)items,
+                                         gcnt + n, perm, long_ctl, long_ctl + 1, (unsigned*)ctl};
+            ctx->fuse_off.ready = true;
+        }
         e = igs_knn_forward_backward(ctx, mode, dev_sidx, dev_samples5, ns, kk, inv_n, losses + (size_t)rk * ns,
                                      contrib ? contrib + rk * items_local * 8 : nullptr,
                                      keys ? keys + rk * items_local : nullptr, exch ? nullptr : gcnt,
                                      ctx->opt_deterministic ? nullptr : ctx->grads, long_ctl, &pf, exch ? 1 : 0);
         ctx->stage_job = StageJob{};
+        ctx->fuse_off.ready = false;
         if (e) return e;
         gcnt_filled = !exch;
     } else {
@@ -1082,22 +1031,15 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
                                                                                         gcnt);
             IGS_LAUNCHED(ctx);
         }
-        if (!getenv("IGS_CUB_SCAN")) {
+        if (ctx->fuse_off.done) {
+            // done by the search's hard_offsets_kernel
+        } else if (!getenv("IGS_CUB_SCAN")) {
             // offsets + scatter in one persistent launch (two grid barriers)
-            if (!ctx->off_blocks) {
-                int per_sm = 0;
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, offsets_scatter_kernel, kOffThreads, 0);
-                ctx->off_blocks = std::max(1, std::min(per_sm, 1)) * ctx->sm_count;
-            }
-            uint32_t* ctl = (uint32_t*)igs_scratch(ctx, 34, ((size_t)ctx->off_blocks + 2) * sizeof(uint32_t));
+            uint32_t* ctl = off_ctl(ctx);
             if (!ctl) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (scan)");
-            if (!ctx->off_ctl_ready) {
-                IGS_CUDA(ctx, cudaMemsetAsync(ctl, 0, 2 * sizeof(uint32_t), ctx->stream));
-                ctx->off_ctl_ready = true;
-            }
-            IGS_PDL(ctx, offsets_scatter_kernel, (unsigned)ctx->off_blocks, kOffThreads, 0, (const uint32_t*)gcnt, n,
-                    goff, ctl + 2, (const uint32_t*)keys, (uint32_t)items, gcnt + n, perm, long_ctl, long_ctl + 1,
-                    (unsigned*)ctl);
+            OffArgs A{(const uint32_t*)gcnt, n, goff, ctl + 2, (const uint32_t*)keys, (uint32_t)items, gcnt + n, perm,
+                      long_ctl, long_ctl + 1, (unsigned*)ctl};
+            IGS_PDL(ctx, offsets_scatter_kernel, (unsigned)ctx->sm_count, kOffThreads, 0, A);
         } else {
             size_t tb = 0;
             cub::DeviceScan::ExclusiveSum(nullptr, tb, gcnt, goff, (int)n, ctx->stream);
