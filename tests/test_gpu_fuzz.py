@@ -100,3 +100,25 @@ def test_fuzz_after_training(gctx, port, seed):
     for q in range(0, 200, 13):
         wi, ww = port.select_top_k(p, uv[q, 0], uv[q, 1], 10)
         assert np.array_equal(idx[q, :cnt[q]], wi)
+
+
+@pytest.mark.parametrize("seed", [9, 26])
+def test_frontier_overflow_in_training_step(gctx, port, seed):
+    """A training step whose samples overflow the search frontier: the hard
+    points go through the fused hard-point scan + reduction-offsets launch
+    (hard_offsets_kernel); loss and gradients match the oracle's train_step."""
+    params = random_case(np.random.default_rng(1000 + seed))
+    W, H = 96, 80
+    target = synth.photo_like_image(W, H, 31200 + seed)
+    sidx = synth.sample_indices(3000, W, H, seed=seed)[0]
+    gctx.set_params(params)
+    gctx.set_target(target)
+    gctx.profile_enable(True)
+    loss, grads = gctx.train_step(sidx, 10)
+    hard = gctx.profile_read(PROF_KNN_HARD)[2]
+    gctx.profile_enable(False)
+    assert hard > 0  # the step does overflow
+    wl, wg = port.train_step(params, target, sidx, 10)
+    assert abs(loss - wl) <= 1e-12 * abs(wl)
+    scale = np.maximum(np.abs(wg), np.max(np.abs(wg), axis=0) * 1e-3)
+    assert np.max(np.abs(grads - wg) / np.maximum(scale, 1e-300)) <= 1e-12
