@@ -1788,10 +1788,15 @@ int launch_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int 
             ctx->fuse_off.ready = false;
             ctx->fuse_off.done = true;
             fused_off = true;
+            // (profiled with the reduction: mostly its offsets + scatter)
+            igs_prof_end(ctx, IGS_PROF_SCAN, 0.0);
+            igs_prof_begin(ctx, IGS_PROF_REDUCE);
             IGS_PDL(ctx, hard_offsets_kernel<KCAP>, ctx->sm_count, kOffThreads, 0, (const ScanRec*)ctx->scan, ctx->n,
                     uv, W, H, kk, (const uint32_t*)hard_count, (const uint32_t*)hard_list, E, part_q, part_i,
                     (unsigned int*)((uint32_t*)b.hard.p + 4 + kHardCap), igs_prof_counter(ctx, IGS_PROF_SCAN),
                     ctx->fuse_off.args);
+            igs_prof_end(ctx, IGS_PROF_REDUCE, 0.0);
+            return IGS_OK;
         }
     }
     if (hand_off && !fused_off) {
