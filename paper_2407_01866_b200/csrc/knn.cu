@@ -1813,6 +1813,7 @@ int run_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int kk,
     if (e) return e;
     if (kk <= 4) return launch_knn<4>(ctx, uv, W, H, npts, kk, E);
     if (kk <= 8) return launch_knn<8>(ctx, uv, W, H, npts, kk, E);
+    if (kk <= 10) return launch_knn<10>(ctx, uv, W, H, npts, kk, E);
     if (kk <= 16) return launch_knn<16>(ctx, uv, W, H, npts, kk, E);
     return launch_knn<32>(ctx, uv, W, H, npts, kk, E);
 }
@@ -2155,6 +2156,7 @@ int igs_raster_knn(igs_ctx* ctx, int W, int H, int k, int row0, int row1, float*
     if (e) return e;
     if (kk <= 4) return launch_knn_raster<4>(ctx, W, H, row0, row1, kk, out, topk);
     if (kk <= 8) return launch_knn_raster<8>(ctx, W, H, row0, row1, kk, out, topk);
+    if (kk <= 10) return launch_knn_raster<10>(ctx, W, H, row0, row1, kk, out, topk);  // (the default K)
     if (kk <= 16) return launch_knn_raster<16>(ctx, W, H, row0, row1, kk, out, topk);
     return launch_knn_raster<32>(ctx, W, H, row0, row1, kk, out, topk);
 }
