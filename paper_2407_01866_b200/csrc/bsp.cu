@@ -837,6 +837,7 @@ int igs_render_image_blocked(igs_ctx* ctx, int width, int height, int k, float* 
                                                              ctx->part->d_shell_mem, width, height, kk, out, pairs)
     if (kk <= 4) LAUNCH(4);
     else if (kk <= 8) LAUNCH(8);
+    else if (kk <= 10) LAUNCH(10);
     else if (kk <= 16) LAUNCH(16);
     else LAUNCH(32);
 #undef LAUNCH
@@ -870,6 +871,7 @@ int igs_render_points_blocked(igs_ctx* ctx, const double* uv, uint32_t npts, int
         ctx->scan, ctx->shade, v, ctx->part->d_shell_off, ctx->part->d_shell_mem, duv, npts, kk, drgb)
     if (kk <= 4) LAUNCH(4);
     else if (kk <= 8) LAUNCH(8);
+    else if (kk <= 10) LAUNCH(10);
     else if (kk <= 16) LAUNCH(16);
     else LAUNCH(32);
 #undef LAUNCH

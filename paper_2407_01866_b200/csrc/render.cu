@@ -265,6 +265,7 @@ int igs_raster_global(igs_ctx* ctx, int W, int H, int k, int row0, int row1, flo
     const int kk = (int)std::min<uint32_t>((uint32_t)k, ctx->n);
     if (kk <= 4) return launch_raster<4>(ctx, W, H, row0, row1, kk, out, topk);
     if (kk <= 8) return launch_raster<8>(ctx, W, H, row0, row1, kk, out, topk);
+    if (kk <= 10) return launch_raster<10>(ctx, W, H, row0, row1, kk, out, topk);
     if (kk <= 16) return launch_raster<16>(ctx, W, H, row0, row1, kk, out, topk);
     if (kk <= 32) return launch_raster<32>(ctx, W, H, row0, row1, kk, out, topk);
     const uint32_t items = (uint32_t)W * (uint32_t)(row1 - row0);
@@ -286,6 +287,7 @@ int igs_topk_points(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32
     if (npts == 0) return IGS_OK;
     if (kk <= 4) return launch_points<4>(ctx, uv, npts, kk, oi, oq);
     if (kk <= 8) return launch_points<8>(ctx, uv, npts, kk, oi, oq);
+    if (kk <= 10) return launch_points<10>(ctx, uv, npts, kk, oi, oq);
     if (kk <= 16) return launch_points<16>(ctx, uv, npts, kk, oi, oq);
     if (kk <= 32) return launch_points<32>(ctx, uv, npts, kk, oi, oq);
     topk_generic_kernel<<<(npts + 127) / 128, 128, 0, ctx->stream>>>(ctx->scan, ctx->n, uv, npts, 0, 0, 0, kk, oq,
