@@ -1680,7 +1680,8 @@ int knn_build(igs_ctx* ctx) {
     L.levels = l;
     const uint32_t cells = (uint32_t)o;
     if (!grow(b.cnt, (size_t)cells * 8) || !grow(b.off, (size_t)cells * 4) || !grow(b.key, (size_t)n * 4) ||
-        !grow(b.mem, (size_t)n * 4) || !grow(b.mrec, (size_t)n * sizeof(ScanRec)) || !grow(b.minv, (size_t)n * 4) || !grow(b.own, (size_t)cells * sizeof(Sum)) ||
+        !grow(b.mem, (size_t)n * 4) || !grow(b.mrec, (size_t)n * sizeof(ScanRec)) || !grow(b.minv, (size_t)n * 4) ||
+        !grow(b.own, (size_t)cells * sizeof(Sum)) ||
         !grow(b.sub, (size_t)cells * sizeof(Sum)))
         return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
     if (!b.ticket.p) {
@@ -1896,7 +1897,8 @@ __global__ void __launch_bounds__(128, KCAP <= 10 ? 7 : 5) knn_raster_kernel(con
                                                             const ShadeRec* __restrict__ shade, uint32_t n, Lq L,
                                                             const Sum* __restrict__ own, const Sum* __restrict__ sub,
                                                             const uint32_t* __restrict__ off,
-                                                            const uint32_t* __restrict__ mem, const ScanRec* __restrict__ mrec, int W, int H, int row0,
+                                                            const uint32_t* __restrict__ mem,
+                                                            const ScanRec* __restrict__ mrec, int W, int H, int row0,
                                                             int row1, int kk, float* __restrict__ out,
                                                             uint32_t* __restrict__ topk, uint32_t npx_patch,
                                                             uint32_t npatch, uint32_t* __restrict__ next_patch,
@@ -2142,7 +2144,8 @@ void igs_knn_free(igs_ctx* ctx) {
     if (getenv("IGS_KNN_STATS"))
         fprintf(stderr, "knn tree: %llu builds, %llu refits\n", (unsigned long long)b->builds,
                 (unsigned long long)b->refits);
-    for (DevBuf* d : {&b->bctl, &b->mrec, &b->minv, &b->cnt, &b->off, &b->key, &b->mem, &b->own, &b->sub, &b->cub_tmp, &b->hard, &b->ticket,
+    for (DevBuf* d : {&b->bctl, &b->mrec, &b->minv, &b->cnt, &b->off, &b->key, &b->mem, &b->own, &b->sub, &b->cub_tmp,
+                      &b->hard, &b->ticket,
                       &b->part, &b->lcount, &b->acc})
         cudaFree(d->p);
     delete b;

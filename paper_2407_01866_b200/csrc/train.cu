@@ -846,7 +846,9 @@ __global__ void blend_points_kernel(const double* __restrict__ lq, const uint32_
 // Scratch slot map (igs_scratch): 0 uv, 1 list q, 2 list idx, 3 contrib,
 // 4 keys, 5 keys sorted, 6 vals, 7 vals sorted, 8 cub temp, 9 losses,
 // 10/11 point partials, 12/13 generic lists, 14 loss out, 15 upstream samples,
-// 24 long-segment queue.
+// 21 staged sample indices, 22 per-step losses (device loop), 24 long-segment
+// queue, 32 long-segment overflow ranks, 34 offsets launch barrier + chunk
+// totals, 35 loss partials + ticket.
 
 int igs_stage_samples(igs_ctx* ctx, const uint32_t* host_pinned, uint32_t* dsidx, uint32_t ns) {
     const L2Prefetch pf = igs_knn_tree_inputs(ctx);
