@@ -291,7 +291,7 @@ def run_ours(args, rank, world, local_rank, dist):
     out = {
         "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded mt19937_64 generators of the reference test suite)",
         "config": {"workload": WORKLOAD, "image": f"{W_IMG}x{H_IMG}", "gaussians": N_GAUSS, "samples_per_iter": NS,
                    "k": K, "parallelism": f"dp{world} (samples split across ranks, NCCL all-reduce of grads)",

@@ -3,6 +3,8 @@ widening, the flat-start descent, batch merges, hard points, the patch
 render, the refit after Adam): random set sizes, scale ranges, anisotropy,
 clusters, image shapes and K -- top-K indices bit-exact against the oracle,
 at sampled points and over whole renders."""
+import os
+
 import numpy as np
 import pytest
 
@@ -10,6 +12,9 @@ from paper_2407_01866_b200 import synth
 from paper_2407_01866_b200.igs import PROF_KNN_HARD
 
 pytestmark = pytest.mark.gpu
+
+# IGS_FUZZ_SEEDS widens the two random sweeps (default: the quick set)
+N_FUZZ = int(os.environ.get("IGS_FUZZ_SEEDS", "12"))
 
 LR = np.array([2e-4, 2e-3, 1e-3, 1e-3])
 
@@ -28,7 +33,7 @@ def random_case(rng):
     return params
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(N_FUZZ))
 def test_fuzz_points_and_render(gctx, port, seed):
     rng = np.random.default_rng(1000 + seed)
     params = random_case(rng)
@@ -79,7 +84,7 @@ def test_frontier_overflow_both_paths(gctx, port, monkeypatch, seed, k):
             assert np.array_equal(idx[p, :cnt[p]], wi), (inwarp, p)
 
 
-@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("seed", range(max(4, N_FUZZ // 3)))
 def test_fuzz_after_training(gctx, port, seed):
     """Searches after Adam steps (tree refits between re-bucketings)."""
     rng = np.random.default_rng(2000 + seed)
