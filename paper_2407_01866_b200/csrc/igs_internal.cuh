@@ -110,17 +110,22 @@ struct TopK {
     __device__ __forceinline__ bool beats(double cq, uint32_t ci) const {
         return cq < q[KCAP - 1] || (cq == q[KCAP - 1] && ci < i[KCAP - 1]);
     }
+    // The list is ascending in the (q, idx) order, so lt[j] = (cand < slot j)
+    // is monotone in j: slot j takes slot j-1 if the candidate went above it,
+    // else the candidate if it goes here, else keeps its own.  All compares
+    // read the old list and the slots update in place from the top down, so
+    // there is no carried value (no branches, no register rotation).
     __device__ __forceinline__ void insert(double cq, uint32_t ci) {
+        bool lt[KCAP];
 #pragma unroll
-        for (int j = 0; j < KCAP; ++j) {
-            const bool lt = cq < q[j] || (cq == q[j] && ci < i[j]);
-            const double tq2 = q[j];
-            const uint32_t ti2 = i[j];
-            q[j] = lt ? cq : tq2;
-            i[j] = lt ? ci : ti2;
-            cq = lt ? tq2 : cq;
-            ci = lt ? ti2 : ci;
+        for (int j = 0; j < KCAP; ++j) lt[j] = (cq < q[j]) | ((cq == q[j]) & (ci < i[j]));
+#pragma unroll
+        for (int j = KCAP - 1; j > 0; --j) {
+            q[j] = lt[j - 1] ? q[j - 1] : (lt[j] ? cq : q[j]);
+            i[j] = lt[j - 1] ? i[j - 1] : (lt[j] ? ci : i[j]);
         }
+        q[0] = lt[0] ? cq : q[0];
+        i[0] = lt[0] ? ci : i[0];
     }
     __device__ __forceinline__ void offer(double cq, uint32_t ci) {
         if (beats(cq, ci)) insert(cq, ci);
