@@ -294,7 +294,8 @@ def run_ours(args, rank, world, local_rank, dist):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded mt19937_64 generators of the reference test suite)",
         "config": {"workload": WORKLOAD, "image": f"{W_IMG}x{H_IMG}", "gaussians": N_GAUSS, "samples_per_iter": NS,
-                   "k": K, "parallelism": f"dp{world} (samples split across ranks, NCCL all-reduce of grads)",
+                   "k": K, "parallelism": f"dp{world} (samples split across ranks, NCCL all-gather of the "
+                                          "per-sample contributions, replicated sample-ordered reduction + Adam)",
                    "l2": "flushed before every timed step (512 MiB memset on the stream, outside the events)",
                    "cull": ctx.get_option(1), "deterministic_reduction": ctx.get_option(2)},
         "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": int(mine.shape[1]) * 4,
