@@ -1893,7 +1893,7 @@ __device__ __forceinline__ double raster_members(TopK<KCAP>& t, uint32_t o_mine,
 }
 
 template <int KCAP>
-__global__ void __launch_bounds__(128, 5) knn_raster_kernel(const ScanRec* __restrict__ scan,
+__global__ void __launch_bounds__(128, KCAP <= 16 ? 5 : 2) knn_raster_kernel(const ScanRec* __restrict__ scan,
                                                             const ShadeRec* __restrict__ shade, uint32_t n, Lq L,
                                                             const Sum* __restrict__ own, const Sum* __restrict__ sub,
                                                             const uint32_t* __restrict__ off,
