@@ -247,6 +247,9 @@ int igs_flush_l2(igs_ctx* ctx, size_t bytes);
 /* Microbenchmarks the FP64 add/mul pipe (independent DADD/DMUL chains,
  * every SM): returns operations per second. */
 int igs_fp64_peak(igs_ctx* ctx, double* ops_per_s);
+/* glibc-exact exp(x) and sincos(x) (csrc/glibc_math.cuh) evaluated on the
+ * device: out3[3i..3i+2] = exp, sin, cos of x[i] (parity diagnostics). */
+int igs_libm_eval(igs_ctx* ctx, const double* x, uint32_t n, double* out3);
 /* Per-kernel-family CUDA-event profiling of the launches the context issues. */
 #define IGS_PROF_SCAN 0    /* top-K candidate scans (raster, point/sample scans) */
 #define IGS_PROF_FINISH 1  /* per-sample blend + loss + contributions */

@@ -124,6 +124,7 @@ _REF_ONLY = [
     ("ssim", C.c_double, [_fp, _fp, C.c_int, C.c_int]),
     ("train_iteration", C.c_int, [_dp, C.c_uint32, _dp, _dp, _fp, C.c_int, C.c_int, _up, C.c_uint32,
                                   C.c_int, _dp, C.c_longlong, _dp]),
+    ("topk_points", C.c_int, [_dp, C.c_uint32, _dp, C.c_uint32, C.c_int, _up, _dp]),
 ]
 
 
@@ -265,6 +266,30 @@ class Oracle:
         self._chk(self._f("select_top_k")(_ptr(params, _dp), n, u, v, k, _ptr(idx, _up), _ptr(w, _dp),
                                           C.byref(cnt)), "select_top_k")
         return idx[:cnt.value], w[:cnt.value]
+
+    def topk_points(self, params, uv, k):
+        """(reference back-end) global top-K indices and q at many points, OpenMP."""
+        params = np.ascontiguousarray(params, np.float64)
+        uv = np.ascontiguousarray(uv, np.float64).reshape(-1, 2)
+        kk = max(1, min(k, params.shape[0]))
+        idx = np.zeros((uv.shape[0], kk), np.uint32); q = np.zeros((uv.shape[0], kk))
+        self._chk(self._f("topk_points")(_ptr(params, _dp), params.shape[0], _ptr(uv, _dp), uv.shape[0], k,
+                                         _ptr(idx, _up), _ptr(q, _dp)), "topk_points")
+        return idx, q
+
+    def train_iteration(self, params, m, v, target, sample_idx, k, lr4, t):
+        """(reference back-end) train_step_gradients + adam_step in place on params/m/v; returns the loss."""
+        for a in (params, m, v):
+            assert a.flags.c_contiguous and a.dtype == np.float64
+        target = np.ascontiguousarray(target, np.float32)
+        sidx = np.ascontiguousarray(sample_idx, np.uint32)
+        lr = np.ascontiguousarray(lr4, np.float64)
+        H, W, _ = target.shape
+        loss = C.c_double(0)
+        self._chk(self._f("train_iteration")(_ptr(params, _dp), params.shape[0], _ptr(m, _dp), _ptr(v, _dp),
+                                             _ptr(target, _fp), W, H, _ptr(sidx, _up), sidx.shape[0], k,
+                                             _ptr(lr, _dp), t, C.byref(loss)), "train_iteration")
+        return loss.value
 
     def render_topk(self, params, uv, k):
         params = np.ascontiguousarray(params, np.float64)

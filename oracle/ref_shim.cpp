@@ -97,6 +97,35 @@ int ref_render_topk(const double* p8, uint32_t n, const double* uv, uint32_t npt
     }
 }
 
+// Global top-K at npts points through one PreparedSet (select_top_k_entries
+// over all indices, renderer.cpp:53-74), OpenMP over points -- the batched
+// form of select_top_k for parity checks at the BASELINE sizes.  idx/q are
+// npts*min(k,n), best-first; unused slots 0xFFFFFFFF / +inf.
+int ref_topk_points(const double* p8, uint32_t n, const double* uv, uint32_t npts, int k, uint32_t* idx, double* q) {
+    try {
+        const GaussianSet set = to_set(p8, n);
+        if (set.empty()) raise(ErrorKind::empty_set, "empty Gaussian set");
+        if (k < 1) raise(ErrorKind::invalid_parameter, "k must be >= 1");
+        PreparedSet ps(set);
+        const int kk = static_cast<int>(std::min<size_t>(k, n));
+#pragma omp parallel
+        {
+            std::vector<TopKEntry> e(kk);
+#pragma omp for schedule(static)
+            for (int64_t i = 0; i < static_cast<int64_t>(npts); ++i) {
+                const int c = select_top_k_entries(ps, ps.all_indices(), {uv[2 * i], uv[2 * i + 1]}, kk, e.data());
+                for (int j = 0; j < kk; ++j) {
+                    idx[i * kk + j] = j < c ? e[j].idx : 0xFFFFFFFFu;
+                    q[i * kk + j] = j < c ? e[j].q : INFINITY;
+                }
+            }
+        }
+        return 0;
+    } catch (const Error& e) {
+        return code_of(e);
+    }
+}
+
 int ref_render_naive(const double* p8, uint32_t n, const double* uv, uint32_t npts, double* rgb) {
     try {
         const GaussianSet set = to_set(p8, n);

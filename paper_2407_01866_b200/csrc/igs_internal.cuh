@@ -21,6 +21,7 @@
 
 #include "../../include/igs_b200.h"
 #include "igs_math.cuh"
+#include "glibc_math.cuh"
 
 #ifndef IGS_NO_NCCL
 #include <nccl.h>
@@ -43,14 +44,15 @@ struct __align__(16) ShadeRec {
 static_assert(sizeof(ScanRec) == 48, "ScanRec");
 static_assert(sizeof(ShadeRec) == 48, "ShadeRec");
 
-// PreparedSet entry of Gaussian i (renderer.cpp:37-50): correctly rounded
-// sincos, IEEE reciprocals; writes both records and returns the scan one.
+// PreparedSet entry of Gaussian i (renderer.cpp:37-50): glibc's sincos
+// (glibc_math.cuh, bit-identical to the reference's std::cos/std::sin), IEEE
+// reciprocals; writes both records and returns the scan one.
 __device__ __forceinline__ ScanRec prepare_one(const double* __restrict__ params, uint32_t i,
                                                ScanRec* __restrict__ scan, ShadeRec* __restrict__ shade) {
     const double2* p2 = reinterpret_cast<const double2*>(params + (size_t)i * 8);
     const double2 a = p2[0], b = p2[1], c = p2[2], d = p2[3];
     double s, co;
-    igs_math::cr_sincos(b.x, &s, &co);
+    glibc_math::sincos(b.x, &s, &co);
     const double inv_s1 = __ddiv_rn(1.0, b.y);
     const double inv_s2 = __ddiv_rn(1.0, c.x);
     ScanRec r;
@@ -141,7 +143,7 @@ __device__ __forceinline__ double blend_topk(const TopK<KCAP>& t, const ShadeRec
 #pragma unroll
     for (int j = 0; j < KCAP; ++j) {
         if (t.live(j)) {
-            const double w = exp(__dmul_rn(-0.5, t.q[j]));
+            const double w = glibc_math::exp(__dmul_rn(-0.5, t.q[j]));
             const ShadeRec s = shade[t.i[j]];
             total = __dadd_rn(total, w);
             ar = __dadd_rn(ar, __dmul_rn(w, s.r));

@@ -668,7 +668,7 @@ __device__ __forceinline__ void warp_epilogue(const Epi& E, const ScanRec* __res
     double w = 0.0;
     ShadeRec h{};
     if (live) {
-        w = exp(__dmul_rn(-0.5, myq));
+        w = glibc_math::exp(__dmul_rn(-0.5, myq));
         h = E.shade[myi];
     }
     double total = 0.0, ar = 0.0, ag = 0.0, ab = 0.0;

@@ -128,6 +128,33 @@ int igs_flush_l2(igs_ctx* ctx, size_t bytes) {
     return IGS_OK;
 }
 
+// glibc-exact exp and sincos (glibc_math.cuh) evaluated on the device, so the
+// tests can compare the device build (nvcc -fmad=false) with the host libm.
+__global__ void libm_eval_kernel(const double* __restrict__ x, uint32_t n, double* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s, c;
+    glibc_math::sincos(x[i], &s, &c);
+    out[3 * (size_t)i] = glibc_math::exp(x[i]);
+    out[3 * (size_t)i + 1] = s;
+    out[3 * (size_t)i + 2] = c;
+}
+
+int igs_libm_eval(igs_ctx* ctx, const double* x, uint32_t n, double* out3) {
+    if (!ctx || (n && (!x || !out3))) return IGS_E_INVALID_PARAMETER;
+    if (n == 0) return IGS_OK;
+    cudaSetDevice(ctx->device);
+    double* dx = (double*)igs_scratch(ctx, 17, (size_t)n * 8);
+    double* dout = (double*)igs_scratch(ctx, 20, (size_t)n * 24);
+    if (!dx || !dout) return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
+    IGS_CUDA(ctx, cudaMemcpyAsync(dx, x, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    libm_eval_kernel<<<(n + 255) / 256, 256, 0, ctx->stream>>>(dx, n, dout);
+    IGS_LAUNCHED(ctx);
+    IGS_CUDA(ctx, cudaMemcpyAsync(out3, dout, (size_t)n * 24, cudaMemcpyDeviceToHost, ctx->stream));
+    IGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return IGS_OK;
+}
+
 int igs_fp64_peak(igs_ctx* ctx, double* ops_per_s) {
     if (!ctx || !ops_per_s) return IGS_E_INVALID_PARAMETER;
     cudaSetDevice(ctx->device);

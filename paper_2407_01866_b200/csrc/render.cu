@@ -14,7 +14,7 @@ using namespace igs_dev;
 namespace {
 
 // ---------------------------------------------------------------------------
-// Kernel 1: PreparedSet.  One thread per Gaussian: correctly-rounded sincos,
+// Kernel 1: PreparedSet.  One thread per Gaussian: glibc-exact sincos,
 // IEEE reciprocals, 2 x 48 B records written with 16-B stores.
 // ---------------------------------------------------------------------------
 __global__ void prepare_kernel(const double* __restrict__ params, ScanRec* __restrict__ scan,
@@ -193,7 +193,7 @@ __global__ void blend_list_image_kernel(const double* __restrict__ lq, const uin
     for (int j = 0; j < kk; ++j) {
         const uint32_t ci = li[(size_t)it * kk + j];
         if (ci == kNoIdx) break;
-        const double w = exp(__dmul_rn(-0.5, lq[(size_t)it * kk + j]));
+        const double w = glibc_math::exp(__dmul_rn(-0.5, lq[(size_t)it * kk + j]));
         const ShadeRec s = shade[ci];
         total = __dadd_rn(total, w);
         ar = __dadd_rn(ar, __dmul_rn(w, s.r));

@@ -68,7 +68,7 @@ __global__ void sample_finish_kernel(const ScanRec* __restrict__ scan, const Sha
     for (int j = 0; j < kk; ++j) {
         const uint32_t ci = ix[j];
         if (ci == kNoIdx) break;
-        const double w = exp(__dmul_rn(-0.5, q[j]));
+        const double w = glibc_math::exp(__dmul_rn(-0.5, q[j]));
         const ShadeRec h = shade[ci];
         total = __dadd_rn(total, w);
         ar = __dadd_rn(ar, __dmul_rn(w, h.r));
@@ -104,7 +104,7 @@ __global__ void sample_finish_kernel(const ScanRec* __restrict__ scan, const Sha
         const uint32_t ci = ix[j];
         const ScanRec g = scan[ci];
         const ShadeRec h = shade[ci];
-        const double w = exp(__dmul_rn(-0.5, q[j]));
+        const double w = glibc_math::exp(__dmul_rn(-0.5, q[j]));
         const double dL_dw = __dmul_rn(
             __dadd_rn(__dadd_rn(__dmul_rn(up0, __dsub_rn(h.r, c0)), __dmul_rn(up1, __dsub_rn(h.g, c1))),
                       __dmul_rn(up2, __dsub_rn(h.b, c2))),
@@ -525,7 +525,7 @@ __device__ __forceinline__ void adam_one(uint32_t i, const double* gg, double* g
     }
     // refresh the prepared records (renderer.cpp:37-50) for the next step
     double s, co;
-    igs_math::cr_sincos(gp[2], &s, &co);
+    glibc_math::sincos(gp[2], &s, &co);
     const double inv_s1 = __ddiv_rn(1.0, gp[3]);
     const double inv_s2 = __ddiv_rn(1.0, gp[4]);
     ScanRec r;
@@ -729,7 +729,7 @@ __global__ void __launch_bounds__(128, 7) segment_adam_kernel(
         a = __ddiv_rn(1.0, gp[3]);
         b = __ddiv_rn(1.0, s2);
     } else {
-        igs_math::cr_sincos(theta, &a, &b);
+        glibc_math::sincos(theta, &a, &b);
     }
     const double oa = shx(a), ob = shx(b);
     if (!live) return;
@@ -816,7 +816,7 @@ __global__ void weights_kernel(const double* __restrict__ q, const uint32_t* __r
                                double* __restrict__ w) {
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= total) return;
-    w[i] = idx[i] == kNoIdx ? 0.0 : exp(__dmul_rn(-0.5, q[i]));
+    w[i] = idx[i] == kNoIdx ? 0.0 : glibc_math::exp(__dmul_rn(-0.5, q[i]));
 }
 
 __global__ void blend_points_kernel(const double* __restrict__ lq, const uint32_t* __restrict__ li,
@@ -828,7 +828,7 @@ __global__ void blend_points_kernel(const double* __restrict__ lq, const uint32_
     for (int j = 0; j < kk; ++j) {
         const uint32_t ci = li[(size_t)p * kk + j];
         if (ci == kNoIdx) break;
-        const double w = exp(__dmul_rn(-0.5, lq[(size_t)p * kk + j]));
+        const double w = glibc_math::exp(__dmul_rn(-0.5, lq[(size_t)p * kk + j]));
         const ShadeRec s = shade[ci];
         total = __dadd_rn(total, w);
         ar = __dadd_rn(ar, __dmul_rn(w, s.r));

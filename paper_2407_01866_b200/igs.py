@@ -142,6 +142,7 @@ SIGNATURES = {
     "igs_timer_between": (C.c_int, [_vp, C.c_uint32, C.c_uint32, C.POINTER(C.c_float)]),
     "igs_flush_l2": (C.c_int, [_vp, C.c_size_t]),
     "igs_fp64_peak": (C.c_int, [_vp, _dp]),
+    "igs_libm_eval": (C.c_int, [_vp, _dp, C.c_uint32, _dp]),
     "igs_profile_enable": (C.c_int, [_vp, C.c_int]),
     "igs_profile_read": (C.c_int, [_vp, C.c_int, _dp, _u64p, _dp]),
     "igs_train_iteration_async": (C.c_int, [_vp, _up, C.c_uint32, C.c_int, _dp, C.c_longlong]),
@@ -504,6 +505,13 @@ class Context:
         out = C.c_double(0)
         self._chk(self.lib.igs_fp64_peak(self.h, C.byref(out)))
         return out.value
+
+    def libm_eval(self, x):
+        """Device glibc-exact (exp, sin, cos) of each x (parity diagnostics)."""
+        x = np.ascontiguousarray(x, np.float64).ravel()
+        out = np.zeros((x.size, 3))
+        self._chk(self.lib.igs_libm_eval(self.h, _p(x, _dp), x.size, _p(out, _dp)))
+        return out
 
     def profile_enable(self, on: bool = True):
         self._chk(self.lib.igs_profile_enable(self.h, 1 if on else 0))
