@@ -69,6 +69,9 @@ uint64_t igs_kernel_launches(const igs_ctx* ctx);
 #define IGS_OPT_TILE 3          /* tile edge in pixels for culling (default 16) */
 #define IGS_OPT_RASTER 4        /* culled global render: 0 = loose-quadtree patch search (default, k <= 32),
                                    1 = certified per-tile candidate lists */
+#define IGS_OPT_SHARD_ADAM 5    /* multi-rank fused iterations: 1 = each rank reduces + updates its 1/R slice of
+                                   the set and the parameters are all-gathered (default); 0 = every rank
+                                   updates the whole set (replicated).  Bit-identical either way. */
 int igs_set_option(igs_ctx* ctx, int option, int64_t value);
 int64_t igs_get_option(const igs_ctx* ctx, int option);
 
@@ -154,6 +157,15 @@ int igs_add_distribution(igs_ctx* ctx, const float* rendered, int width, int hei
 /* psnr(rendered, target); rendered nullable = last device image. */
 int igs_psnr(igs_ctx* ctx, const float* rendered, int width, int height, double* out);
 
+/* image_gradient_magnitude(img) (sampling.cpp:44-67) on the device: per-pixel
+ * L2 norm of the six Sobel responses, replicate padding; img nullable = the
+ * resident target; mag = H*W doubles (nullable: stays on the device). */
+int igs_image_gradient_magnitude(igs_ctx* ctx, const float* img, int width, int height, double* mag);
+/* init_distribution / opt_distribution (sampling.cpp:25-40): (1-lambda) *
+ * |grad| / Kahan-sum|grad| + lambda / (H*W), uniform when the gradient field
+ * is zero.  img nullable = the target; p = H*W doubles. */
+int igs_gradient_mixture(igs_ctx* ctx, const float* img, int width, int height, double lambda, double* p);
+
 /* ssim(rendered, target) (metrics.cpp:33-112); rendered nullable = last image. */
 int igs_ssim(igs_ctx* ctx, const float* rendered, int width, int height, double* out);
 
@@ -206,6 +218,20 @@ int igs_locate_blocks(igs_ctx* ctx, const double* uv, uint32_t npts, int32_t* bl
 int igs_render_image_blocked(igs_ctx* ctx, int width, int height, int k, float* out_rgb);
 /* render_topk_blocked at npts points (random-access decode queries). */
 int igs_render_points_blocked(igs_ctx* ctx, const double* uv, uint32_t npts, int k, double* rgb);
+
+/* bench_render (bsp.hpp:89-106, bsp.cpp:343-406): `pixels` random points
+ * from Rng(seed); rows[0] = the unpartitioned global top-K baseline
+ * (n_max 0, n_b 0, candidates = N), rows[1 + i] = n_max_values[i]:
+ * build_partition, then blocked queries.  Times are device time per trial
+ * (CUDA events), in ms per 10k points, mean and population std over
+ * `trials` after `warmup`; mean_candidates is the reference's count.  The
+ * last partition stays resident. */
+typedef struct {
+    int n_max, n_b;
+    double mean_ms_per_10k, std_ms, mean_candidates;
+} igs_bench_row;
+int igs_bench_render(igs_ctx* ctx, int pixels, const int* n_max_values, int n_values, uint64_t seed, int trials,
+                     int warmup, igs_bench_row* rows /* n_values + 1 */);
 
 /* The device's prepared scan records (mu_x, mu_y, cos, sin, 1/s1^2, 1/s2^2)
  * per Gaussian (PreparedSet::scan, renderer.hpp:31-34): n*6 doubles. */
@@ -265,11 +291,27 @@ int igs_profile_enable(igs_ctx* ctx, int on);
 int igs_profile_read(igs_ctx* ctx, int family, double* ms, uint64_t* launches, double* work);
 
 /* ---- multi-GPU (one context per GPU, one process or thread each) --------- */
+/* Training splits each iteration's samples into contiguous equal rank blocks;
+ * every rank searches its block, an in-place all-gather completes the
+ * per-sample contribution / key / loss arrays in global sample order, and
+ * the sample-ordered reduction + Adam follow (bit-identical to one GPU).
+ * The fp64-atomics mode (IGS_OPT_DETERMINISTIC 0) all-reduces the gradients
+ * instead.  Rendering needs no communication (igs_render_image_rows). */
 int igs_comm_unique_id(uint8_t id[128]);
-/* NCCL communicator over NVLink; training steps then all-reduce the
- * per-Gaussian gradients (sum) before Adam. */
+/* NCCL communicator over NVLink (one rank per context). */
 int igs_comm_init(igs_ctx* ctx, const uint8_t id[128], int nranks, int rank);
+/* In-process loopback group of nranks contexts (any devices, including one
+ * device for all ranks): the same collectives as cudaMemcpyAsync between the
+ * contexts' buffers, ordered by events; each rank must then be driven by
+ * its own host thread, as with NCCL.  For testing the R-rank exchange on
+ * one GPU (NCCL rejects two ranks on one device). */
+int igs_comm_init_loopback(igs_ctx** ctxs, int nranks);
 int igs_comm_destroy(igs_ctx* ctx);
+/* With IGS_OPT_SHARD_ADAM each rank keeps only its slice of the Adam
+ * moments current; this (collective: every rank calls it) all-gathers them,
+ * e.g. before igs_get_adam_state.  Calls that change the set (set_params,
+ * append_params, decode, adam_step) must be made on every rank alike. */
+int igs_comm_gather_moments(igs_ctx* ctx);
 
 #ifdef __cplusplus
 }

@@ -125,6 +125,7 @@ _REF_ONLY = [
     ("train_iteration", C.c_int, [_dp, C.c_uint32, _dp, _dp, _fp, C.c_int, C.c_int, _up, C.c_uint32,
                                   C.c_int, _dp, C.c_longlong, _dp]),
     ("topk_points", C.c_int, [_dp, C.c_uint32, _dp, C.c_uint32, C.c_int, _up, _dp]),
+    ("bench_render", C.c_int, [_dp, C.c_uint32, C.c_int, _ip, C.c_int, C.c_uint64, C.c_int, C.c_int, _dp]),
 ]
 
 
@@ -277,6 +278,17 @@ class Oracle:
                                          _ptr(idx, _up), _ptr(q, _dp)), "topk_points")
         return idx, q
 
+    def bench_render(self, params, pixels, n_max_values, seed, trials=20, warmup=3):
+        """(reference back-end) bench_render rows: [baseline] + one per n_max, each
+        (n_max, n_b, mean_ms_per_10k, std_ms, mean_candidates)."""
+        params = np.ascontiguousarray(params, np.float64)
+        nm = np.ascontiguousarray(n_max_values, np.int32)
+        out = np.zeros((len(nm) + 1, 5))
+        self._chk(self._f("bench_render")(_ptr(params, _dp), params.shape[0], pixels,
+                                          nm.ctypes.data_as(_ip), len(nm), seed, trials, warmup, _ptr(out, _dp)),
+                  "bench_render")
+        return out
+
     def train_iteration(self, params, m, v, target, sample_idx, k, lr4, t):
         """(reference back-end) train_step_gradients + adam_step in place on params/m/v; returns the loss."""
         for a in (params, m, v):
@@ -385,6 +397,13 @@ class Oracle:
         self._chk(self._f("initialize_set")(_ptr(img, _fp), W, H, count, lam, seed, _ptr(out, _dp)),
                   "initialize_set")
         return out
+
+    def ssim(self, a, b):
+        """(reference back-end) ssim(a, b) (metrics.cpp:71-112)."""
+        a = np.ascontiguousarray(a, np.float32)
+        b = np.ascontiguousarray(b, np.float32)
+        H, W, _ = a.shape
+        return float(self._f("ssim")(_ptr(a, _fp), _ptr(b, _fp), W, H))
 
     def psnr(self, a, b):
         a = np.ascontiguousarray(a, np.float32).ravel()

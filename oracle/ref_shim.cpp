@@ -453,6 +453,29 @@ int ref_fit(const float* target, int W, int H, const RefFitConfig* c, double* ou
     }
 }
 
+// bench_render (bsp.cpp:343-406) as the reference runs it: rows5 receives
+// (n_max, n_b, mean_ms_per_10k, std_ms, mean_candidates) for the baseline
+// and then each n_max.
+int ref_bench_render(const double* p8, uint32_t n, int pixels, const int* nmax, int nv, uint64_t seed, int trials,
+                     int warmup, double* rows5) {
+    try {
+        const GaussianSet set = to_set(p8, n);
+        const BenchResult r = bench_render(set, pixels, std::vector<int>(nmax, nmax + nv), seed, trials, warmup);
+        auto put = [&](int i, const BenchRow& b) {
+            rows5[5 * i] = b.n_max;
+            rows5[5 * i + 1] = b.n_b;
+            rows5[5 * i + 2] = b.mean_ms_per_10k;
+            rows5[5 * i + 3] = b.std_ms;
+            rows5[5 * i + 4] = b.mean_candidates;
+        };
+        put(0, r.baseline);
+        for (size_t i = 0; i < r.rows.size(); ++i) put(static_cast<int>(i) + 1, r.rows[i]);
+        return 0;
+    } catch (const Error& e) {
+        return code_of(e);
+    }
+}
+
 // One reference Adam step over an already-built set (used by the CPU
 // baseline timing of a full train iteration).
 int ref_train_iteration(double* p8, uint32_t n, double* m, double* v, const float* target, int W, int H,

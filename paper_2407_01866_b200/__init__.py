@@ -6,8 +6,9 @@ reference's igs:: C++ API; ``synth`` generates the reference test-suite's
 seeded synthetic inputs; ``fit`` is the host-side encoder loop driving the
 device through the ABI.
 """
-from .igs import (DEFAULT_K, DEFAULT_LR, OPT_CULL, OPT_DETERMINISTIC, OPT_TILE, OPT_RASTER, Context, IgsError,  # noqa: F401
+from .igs import (DEFAULT_K, DEFAULT_LR, OPT_CULL, OPT_DETERMINISTIC, OPT_TILE, OPT_RASTER, OPT_SHARD_ADAM, Context,  # noqa: F401
+                  IgsError,
                   LIB_PATH, load_library)
 
 __all__ = ["Context", "IgsError", "load_library", "LIB_PATH", "DEFAULT_K", "DEFAULT_LR", "OPT_CULL", "OPT_RASTER",
-           "OPT_DETERMINISTIC", "OPT_TILE"]
+           "OPT_DETERMINISTIC", "OPT_TILE", "OPT_SHARD_ADAM"]

@@ -850,6 +850,26 @@ int igs_render_image_blocked(igs_ctx* ctx, int width, int height, int k, float* 
     return IGS_OK;
 }
 
+}  // extern "C"
+
+// blocked_pixel at npts device points (validated partition, kk <= 32)
+int igs_blocked_points_dev(igs_ctx* ctx, const double* duv, uint32_t npts, int kk, double* drgb) {
+    const LocView v = view_of(ctx->part);
+#define LAUNCH(KC)                                                                                    \
+    blocked_points_kernel<KC><<<(npts + 127) / 128, 128, 0, ctx->stream>>>(                          \
+        ctx->scan, ctx->shade, v, ctx->part->d_shell_off, ctx->part->d_shell_mem, duv, npts, kk, drgb)
+    if (kk <= 4) LAUNCH(4);
+    else if (kk <= 8) LAUNCH(8);
+    else if (kk <= 10) LAUNCH(10);
+    else if (kk <= 16) LAUNCH(16);
+    else LAUNCH(32);
+#undef LAUNCH
+    IGS_LAUNCHED(ctx);
+    return IGS_OK;
+}
+
+extern "C" {
+
 // bsp.cpp:321-332 render_topk_blocked at many points
 int igs_render_points_blocked(igs_ctx* ctx, const double* uv, uint32_t npts, int k, double* rgb) {
     if (!ctx) return IGS_E_INVALID_PARAMETER;
@@ -865,17 +885,7 @@ int igs_render_points_blocked(igs_ctx* ctx, const double* uv, uint32_t npts, int
     double* drgb = (double*)igs_scratch(ctx, 20, (size_t)npts * 24);
     if (!duv || !drgb) return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
     IGS_CUDA(ctx, cudaMemcpyAsync(duv, uv, (size_t)npts * 16, cudaMemcpyHostToDevice, ctx->stream));
-    const LocView v = view_of(ctx->part);
-#define LAUNCH(KC)                                                                                    \
-    blocked_points_kernel<KC><<<(npts + 127) / 128, 128, 0, ctx->stream>>>(                          \
-        ctx->scan, ctx->shade, v, ctx->part->d_shell_off, ctx->part->d_shell_mem, duv, npts, kk, drgb)
-    if (kk <= 4) LAUNCH(4);
-    else if (kk <= 8) LAUNCH(8);
-    else if (kk <= 10) LAUNCH(10);
-    else if (kk <= 16) LAUNCH(16);
-    else LAUNCH(32);
-#undef LAUNCH
-    IGS_LAUNCHED(ctx);
+    if ((e = igs_blocked_points_dev(ctx, duv, npts, kk, drgb))) return e;
     if (rgb) {
         IGS_CUDA(ctx, cudaMemcpyAsync(rgb, drgb, (size_t)npts * 24, cudaMemcpyDeviceToHost, ctx->stream));
         IGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));

@@ -135,11 +135,14 @@ int igs_codec_pack(igs_ctx* ctx, uint16_t* dev_out) {
     return IGS_OK;
 }
 
-// in == nullptr: quantize the resident parameters in place
-int igs_codec_unpack(igs_ctx* ctx, const uint16_t* dev_in, uint32_t n) {
+// binary16 -> double + constrain into dev_out (n records): from packed
+// halves (dev_in, decode) or by rounding doubles through binary16 (dev_src,
+// quantize_set).  status[1] <- first record with a non-finite value; the
+// caller commits dev_out only when it is clear.
+int igs_codec_unpack(igs_ctx* ctx, const uint16_t* dev_in, const double* dev_src, uint32_t n, double* dev_out) {
     const size_t count = (size_t)n * 8;
-    unpack_kernel<<<(unsigned)((count + 255) / 256), 256, 0, ctx->stream>>>(dev_in, dev_in ? nullptr : ctx->params,
-                                                                           count, ctx->params, ctx->status);
+    unpack_kernel<<<(unsigned)((count + 255) / 256), 256, 0, ctx->stream>>>(dev_in, dev_src, count, dev_out,
+                                                                           ctx->status);
     IGS_LAUNCHED(ctx);
     return IGS_OK;
 }

@@ -8,6 +8,7 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <random>
 #include <string>
 
 #include "igs_internal.cuh"
@@ -20,7 +21,7 @@ int igs_stage_samples(igs_ctx* ctx, const uint32_t* host_pinned, uint32_t* dsidx
 int igs_stage_draws(igs_ctx* ctx, const unsigned long long* host_raw, uint32_t* dsidx, uint32_t ns);
 int igs_publish(igs_ctx* ctx, const double* dloss, long long* host_res);
 int igs_codec_pack(igs_ctx* ctx, uint16_t* dev_out);
-int igs_codec_unpack(igs_ctx* ctx, const uint16_t* dev_in, uint32_t n);
+int igs_codec_unpack(igs_ctx* ctx, const uint16_t* dev_in, const double* dev_src, uint32_t n, double* dev_out);
 uint16_t igs_host_double_to_half(double d);
 double igs_host_half_to_double(uint16_t h);
 bool igs_host_encodable(double v);
@@ -37,46 +38,13 @@ int igs_raster_culled(igs_ctx* ctx, int W, int H, int k, int row0, int row1, flo
 int igs_cull_lists(igs_ctx* ctx, int W, int H, int k, uint32_t* ntiles, uint64_t* total, uint32_t* offsets,
                    uint32_t* members, double* tau);
 // metrics.cu
-int igs_error_map(igs_ctx* ctx, const float* dev_rendered, int W, int H, double* dev_p);
+int igs_error_map(igs_ctx* ctx, const float* dev_rendered, int W, int H, double* dev_p, int normalize);
+extern "C" void igs_internal_kahan_normalize(double* p, size_t n);
 int igs_psnr_dev(igs_ctx* ctx, const float* dev_a, const float* dev_b, size_t count, double* out);
 int igs_ssim_dev(igs_ctx* ctx, const float* a, const float* b, int W, int H, double* out);
+int igs_sobel_dev(igs_ctx* ctx, const float* img, int W, int H, double* dev_mag);
+extern "C" void igs_internal_gradient_mixture(const double* mag, size_t n, double lambda, double* p);
 
-
-// ---------------------------------------------------------------------------
-// NCCL, resolved at first use with dlopen: the process may already hold a
-// libnccl.so.2 (e.g. torch's bundled 2.28 when torch.distributed is the
-// plumbing); linking the system one at load time would shadow it.
-// ---------------------------------------------------------------------------
-#ifndef IGS_NO_NCCL
-namespace {
-struct NcclApi {
-    bool ok = false;
-    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
-    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
-    ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
-                              cudaStream_t) = nullptr;
-    ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
-};
-NcclApi& nccl() {
-    static NcclApi api;
-    static bool tried = false;
-    if (tried) return api;
-    tried = true;
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
-    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) return api;
-    api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
-    api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
-    api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
-    api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
-    api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
-    api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce && api.allGather;
-    return api;
-}
-}  // namespace
-#endif
 
 // ---------------------------------------------------------------------------
 // plumbing
@@ -150,15 +118,23 @@ int igs_ensure_image(igs_ctx* ctx, int w, int h) {
 static int ensure_capacity(igs_ctx* ctx, uint32_t n, bool keep) {
     if (n <= ctx->cap) return IGS_OK;
     uint32_t cap = std::max<uint32_t>(n, ctx->cap + ctx->cap / 2);
-    cap = std::max<uint32_t>(cap, 64);
-    double *p, *g, *m, *v;
-    ScanRec* s;
-    ShadeRec* h;
+    // slack: the sharded Adam's all-gather moves ceil(n/R) * R records
+    cap = std::max<uint32_t>(cap, n + 64);
+    double *p = nullptr, *g = nullptr, *m = nullptr, *v = nullptr;
+    ScanRec* s = nullptr;
+    ShadeRec* h = nullptr;
     const size_t rb = (size_t)cap * 8 * sizeof(double);
     if (cudaMalloc(&p, rb) != cudaSuccess || cudaMalloc(&g, rb) != cudaSuccess || cudaMalloc(&m, rb) != cudaSuccess ||
         cudaMalloc(&v, rb) != cudaSuccess || cudaMalloc(&s, (size_t)cap * sizeof(ScanRec)) != cudaSuccess ||
         cudaMalloc(&h, (size_t)cap * sizeof(ShadeRec)) != cudaSuccess) {
         cudaGetLastError();
+        // release whatever this call did get; the resident set is untouched
+        cudaFree(p);
+        cudaFree(g);
+        cudaFree(m);
+        cudaFree(v);
+        cudaFree(s);
+        cudaFree(h);
         return igs_fail(ctx, IGS_E_CUDA, "out of device memory (Gaussian set)");
     }
     if (keep && ctx->n) {
@@ -265,9 +241,7 @@ void igs_ctx_destroy(igs_ctx* ctx) {
     igs_partition_free(ctx);
     igs_cull_free(ctx);
     igs_knn_free(ctx);
-#ifndef IGS_NO_NCCL
-    if (ctx->comm) nccl().commDestroy(ctx->comm);
-#endif
+    igs_comm_release(ctx);
     cudaFree(ctx->params);
     cudaFree(ctx->grads);
     cudaFree(ctx->adam_m);
@@ -318,6 +292,7 @@ int igs_set_option(igs_ctx* ctx, int option, int64_t value) {
         case IGS_OPT_CULL: ctx->opt_cull = value ? 1 : 0; return IGS_OK;
         case IGS_OPT_DETERMINISTIC: ctx->opt_deterministic = value ? 1 : 0; return IGS_OK;
         case IGS_OPT_RASTER: ctx->opt_raster = value ? 1 : 0; return IGS_OK;
+        case IGS_OPT_SHARD_ADAM: ctx->opt_shard_adam = value ? 1 : 0; return IGS_OK;
         case IGS_OPT_TILE:
             if (value != 8 && value != 16 && value != 32)
                 return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "tile must be 8, 16 or 32");
@@ -333,14 +308,34 @@ int64_t igs_get_option(const igs_ctx* ctx, int option) {
         case IGS_OPT_CULL: return ctx->opt_cull;
         case IGS_OPT_DETERMINISTIC: return ctx->opt_deterministic;
         case IGS_OPT_RASTER: return ctx->opt_raster;
+        case IGS_OPT_SHARD_ADAM: return ctx->opt_shard_adam;
         case IGS_OPT_TILE: return ctx->opt_tile;
     }
     return -1;
 }
 
 // ---- Gaussian set ----------------------------------------------------------
+// (collective) every rank's slice of the Adam moments to every rank, after
+// sharded updates (IGS_OPT_SHARD_ADAM); a no-op otherwise
+static int gather_moments(igs_ctx* ctx) {
+    if (!ctx->moments_local) return IGS_OK;
+    const uint32_t R = (uint32_t)ctx->nranks, B = (ctx->n + R - 1) / R;
+    int e;
+    if ((e = igs_comm_allgather(ctx, ctx->adam_m, (size_t)B * 64))) return e;
+    if ((e = igs_comm_allgather(ctx, ctx->adam_v, (size_t)B * 64))) return e;
+    ctx->moments_local = false;
+    return IGS_OK;
+}
+
+int igs_comm_gather_moments(igs_ctx* ctx) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    return gather_moments(ctx);
+}
+
 int igs_set_params(igs_ctx* ctx, const double* params8, uint32_t n) {
     CHECK_CTX(ctx);
+    ctx->moments_local = false;  // fresh (zero) moments everywhere
     if (n && !params8) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "null params");
     cudaSetDevice(ctx->device);
     int e = ensure_capacity(ctx, n, false);
@@ -365,7 +360,10 @@ int igs_append_params(igs_ctx* ctx, const double* params8, uint32_t n) {
     if (!params8) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "null params");
     cudaSetDevice(ctx->device);
     const uint32_t old = ctx->n;
-    int e = ensure_capacity(ctx, old + n, true);
+    // the slices move with n: re-replicate sharded moments first (collective)
+    int e = gather_moments(ctx);
+    if (e) return e;
+    e = ensure_capacity(ctx, old + n, true);
     if (e) return e;
     const size_t rb = (size_t)n * 8 * sizeof(double);
     if ((e = host_to_dev(ctx, ctx->params + (size_t)old * 8, params8, rb))) return e;
@@ -545,20 +543,6 @@ int igs_set_target(igs_ctx* ctx, const float* rgb, int width, int height) {
 
 // In-place all-gather of `bytes` per rank: rank r's block sits at
 // buf + r * bytes (train.cu's sample-ordered exchange of contributions).
-int igs_comm_allgather(igs_ctx* ctx, void* buf, size_t bytes) {
-#ifndef IGS_NO_NCCL
-    if (!ctx->comm) return IGS_OK;
-    char* b = static_cast<char*>(buf);
-    if (nccl().allGather(b + (size_t)ctx->rank * bytes, b, bytes, ncclChar, ctx->comm, ctx->stream) != ncclSuccess)
-        return igs_fail(ctx, IGS_E_CUDA, "ncclAllGather failed");
-#else
-    (void)ctx;
-    (void)buf;
-    (void)bytes;
-#endif
-    return IGS_OK;
-}
-
 extern "C" {
 
 
@@ -566,19 +550,11 @@ extern "C" {
 // contributions (fp64-atomics mode, the brute-force fallback); after an
 // exchange the gradients and the loss are already global.
 static int allreduce_grads(igs_ctx* ctx, double* dev_loss) {
-#ifndef IGS_NO_NCCL
-    if (ctx->comm && !ctx->exchanged) {  // a 1-rank communicator still runs (exercises the path on one GPU)
-        if (nccl().allReduce(ctx->grads, ctx->grads, (size_t)ctx->n * 8, ncclDouble, ncclSum, ctx->comm, ctx->stream) !=
-            ncclSuccess)
-            return igs_fail(ctx, IGS_E_CUDA, "ncclAllReduce(grads) failed");
-        if (dev_loss &&
-            nccl().allReduce(dev_loss, dev_loss, 1, ncclDouble, ncclSum, ctx->comm, ctx->stream) != ncclSuccess)
-            return igs_fail(ctx, IGS_E_CUDA, "ncclAllReduce(loss) failed");
+    if (igs_has_comm(ctx) && !ctx->exchanged) {  // a 1-rank communicator still runs (exercises the path on one GPU)
+        int e;
+        if ((e = igs_comm_allreduce_sum(ctx, ctx->grads, (size_t)ctx->n * 8))) return e;
+        if (dev_loss && (e = igs_comm_allreduce_sum(ctx, dev_loss, 1))) return e;
     }
-#else
-    (void)ctx;
-    (void)dev_loss;
-#endif
     return IGS_OK;
 }
 
@@ -616,6 +592,30 @@ static int read_status(igs_ctx* ctx, double* dev_loss, double* loss_out, int che
     return IGS_OK;
 }
 
+// fit.cpp:87-89: the loss is the per-sample L1 losses summed in sample
+// order, times 1/ns.  A sequential sum has no exact parallel form (and one
+// device thread takes ~60 us for 10k terms), so the per-sample losses come
+// to the host -- mirrored by the search epilogue into mapped memory on the
+// asynchronous path -- and are summed here exactly as the reference does.
+static double sequential_loss(const double* l, uint32_t n) {
+    double s = 0.0;
+    for (uint32_t i = 0; i < n; ++i) s += l[i];
+    return s * (1.0 / (double)n);
+}
+
+// the per-sample losses of the last forward/backward are on the device for
+// every rank's samples (single rank, or the deterministic exchange)
+static bool losses_complete(const igs_ctx* ctx) { return !igs_has_comm(ctx) || ctx->exchanged; }
+
+static int host_loss_from_device(igs_ctx* ctx, uint32_t ns_total, double* loss) {
+    std::vector<double> l(ns_total);
+    const double* dl = (const double*)igs_scratch(ctx, 9, (size_t)std::max<uint32_t>(ns_total, 1) * sizeof(double));
+    int e;
+    if ((e = dev_to_host(ctx, l.data(), dl, (size_t)ns_total * sizeof(double)))) return e;
+    *loss = sequential_loss(l.data(), ns_total);
+    return IGS_OK;
+}
+
 static int upload_sidx(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, uint32_t** dev) {
     const uint64_t npx = (uint64_t)ctx->tgt_w * ctx->tgt_h;
     for (uint32_t i = 0; i < ns; ++i)
@@ -640,6 +640,7 @@ int igs_train_step(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, int k,
     if ((e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss, 1.0 / (double)ns_total))) return e;
     if ((e = allreduce_grads(ctx, dloss))) return e;
     if ((e = read_status(ctx, dloss, loss, 0))) return e;
+    if (loss && losses_complete(ctx) && (e = host_loss_from_device(ctx, ns_total, loss))) return e;
     if (grads8) return dev_to_host(ctx, grads8, ctx->grads, (size_t)ctx->n * 64);
     return IGS_OK;
 }
@@ -651,6 +652,7 @@ int igs_adam_step(igs_ctx* ctx, const double* lr4, long long t) {
     if (!lr4) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "null learning rates");
     if (ctx->n == 0) return IGS_OK;
     int e;
+    if ((e = gather_moments(ctx))) return e;
     if ((e = igs_status_reset(ctx))) return e;
     if ((e = igs_grad_check(ctx))) return e;
     if ((e = igs_adam_launch(ctx, lr4, t))) return e;
@@ -726,13 +728,25 @@ static int train_iteration_enqueue(igs_ctx* ctx, const uint32_t* sample_idx, con
     job.alias = (const uint32_t*)ctx->alias_idx.p;
     job.table_n = ctx->alias_n;
     const uint32_t ns_total = ns * (uint32_t)ctx->nranks;
+    double* hl = (double*)async_pinned(ctx, 4 + slot, (size_t)std::max<uint32_t>(ns_total, 1) * sizeof(double));
+    if (!hl) return igs_fail(ctx, IGS_E_CUDA, "out of memory (async iteration)");
+    ctx->async_ns[slot] = ns_total;
     bool fused = false;
-    if ((e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss, 1.0 / (double)ns_total, lr4, t, &fused,
-                                  &job)))
-        return e;
+    ctx->loss_mirror = hl;
+    ctx->loss_mirrored = false;
+    e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss, 1.0 / (double)ns_total, lr4, t, &fused, &job);
+    ctx->loss_mirror = nullptr;
+    if (e) return e;
+    if (!ctx->loss_mirrored && losses_complete(ctx)) {
+        // the search did not mirror them (other search paths, or the
+        // multi-rank exchange, whose gathered array holds every rank's)
+        const double* dl = (const double*)igs_scratch(ctx, 9, (size_t)ns_total * sizeof(double));
+        IGS_CUDA(ctx, cudaMemcpyAsync(hl, dl, (size_t)ns_total * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    if (!losses_complete(ctx)) ctx->async_ns[slot] = 0;  // fp64-atomics multi-rank: the device's loss
     if (!fused) {
         if ((e = allreduce_grads(ctx, dloss))) return e;
-        if ((ctx->comm || !ctx->grads_checked) && (e = igs_grad_check(ctx))) return e;
+        if ((igs_has_comm(ctx) || !ctx->grads_checked) && (e = igs_grad_check(ctx))) return e;
         if ((e = igs_adam_launch(ctx, lr4, t))) return e;
     }
     if ((e = igs_publish(ctx, dloss, res))) return e;  // D2H of status + loss
@@ -789,7 +803,12 @@ int igs_train_wait(igs_ctx* ctx, double* loss) {
                             names[st[0] % 8]);
     }
     if (st[1] != LLONG_MAX) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "non-finite Gaussian parameters");
-    if (loss) std::memcpy(loss, st + 4, sizeof(double));
+    if (loss) {
+        if (ctx->async_ns[slot])
+            *loss = sequential_loss((const double*)ctx->async_pin[4 + slot].p, ctx->async_ns[slot]);
+        else
+            std::memcpy(loss, st + 4, sizeof(double));
+    }
     return IGS_OK;
 }
 
@@ -829,6 +848,12 @@ int igs_train_iterations(igs_ctx* ctx, uint32_t steps, int k, const double* lr4,
     reset.kind = 1;
     reset.status = ctx->status;
     const uint32_t ns_total = ns * (uint32_t)ctx->nranks;
+    // per-step per-sample losses (only when the caller wants the losses)
+    double* step_losses = nullptr;
+    if (losses) {
+        step_losses = (double*)igs_scratch(ctx, 37, (size_t)std::max<uint32_t>(steps, 1) * ns_total * sizeof(double));
+        if (!step_losses) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (losses)");
+    }
     for (uint32_t s = 0; s < steps; ++s) {
         // step t uses uploaded slot (t-1) mod steps_uploaded
         const uint32_t slot = (uint32_t)((t0 + s - 1) % (long long)ctx->samples_steps);
@@ -838,15 +863,26 @@ int igs_train_iterations(igs_ctx* ctx, uint32_t steps, int k, const double* lr4,
         if ((e = igs_forward_backward(ctx, ns, k, 0, dsidx, nullptr, dloss + s, 1.0 / (double)ns_total, lr4, t0 + s,
                                       &fused, s == 0 ? &reset : nullptr)))
             return e;
+        if (step_losses && losses_complete(ctx)) {
+            const double* dl = (const double*)igs_scratch(ctx, 9, (size_t)ns_total * sizeof(double));
+            IGS_CUDA(ctx, cudaMemcpyAsync(step_losses + (size_t)s * ns_total, dl, (size_t)ns_total * sizeof(double),
+                                          cudaMemcpyDeviceToDevice, ctx->stream));
+        }
         if (!fused) {
             if ((e = allreduce_grads(ctx, dloss + s))) return e;
-            if ((ctx->comm || !ctx->grads_checked) && (e = igs_grad_check(ctx))) return e;
+            if ((igs_has_comm(ctx) || !ctx->grads_checked) && (e = igs_grad_check(ctx))) return e;
             if ((e = igs_adam_launch(ctx, lr4, t0 + s))) return e;
         }
     }
     igs_timer_autostop(ctx);  // device time of the loop excludes the status readback
     if ((e = read_status(ctx, nullptr, nullptr, 1))) return e;
-    if (losses) return dev_to_host(ctx, losses, dloss, (size_t)steps * sizeof(double));
+    if (!losses) return IGS_OK;
+    if ((e = dev_to_host(ctx, losses, dloss, (size_t)steps * sizeof(double)))) return e;
+    if (losses_complete(ctx)) {
+        std::vector<double> l((size_t)steps * ns_total);
+        if ((e = dev_to_host(ctx, l.data(), step_losses, l.size() * sizeof(double)))) return e;
+        for (uint32_t s = 0; s < steps; ++s) losses[s] = sequential_loss(l.data() + (size_t)s * ns_total, ns_total);
+    }
     return IGS_OK;
 }
 
@@ -869,6 +905,9 @@ int igs_set_grads(igs_ctx* ctx, const double* grads8, uint32_t n) {
 int igs_get_adam_state(igs_ctx* ctx, double* m, double* v, uint32_t n) {
     CHECK_CTX(ctx);
     if (n != ctx->n) return igs_fail(ctx, IGS_E_DIMENSION_MISMATCH, "state size mismatch");
+    if (ctx->moments_local)
+        return igs_fail(ctx, IGS_E_INVALID_PARAMETER,
+                        "Adam moments are sharded across ranks: call igs_comm_gather_moments on every rank first");
     if (n == 0) return IGS_OK;
     int e;
     if (m && (e = dev_to_host(ctx, m, ctx->adam_m, (size_t)n * 64))) return e;
@@ -878,6 +917,7 @@ int igs_get_adam_state(igs_ctx* ctx, double* m, double* v, uint32_t n) {
 
 int igs_set_adam_state(igs_ctx* ctx, const double* m, const double* v, uint32_t n) {
     CHECK_CTX(ctx);
+    ctx->moments_local = false;
     if (n != ctx->n) return igs_fail(ctx, IGS_E_DIMENSION_MISMATCH, "state size mismatch");
     if (n == 0) return IGS_OK;
     int e;
@@ -911,8 +951,12 @@ int igs_add_distribution(igs_ctx* ctx, const float* rendered, int width, int hei
     if ((e = stage_rendered(ctx, rendered, width, height, &dr))) return e;
     double* dp = (double*)igs_scratch(ctx, 12, (size_t)width * height * sizeof(double));
     if (!dp) return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
-    if ((e = igs_error_map(ctx, dr, width, height, dp))) return e;
-    if (p) return dev_to_host(ctx, p, dp, (size_t)width * height * sizeof(double));
+    if ((e = igs_error_map(ctx, dr, width, height, dp, p == nullptr))) return e;
+    if (!p) return IGS_OK;
+    // sampling.cpp:84-93: the raw L1 map comes back and is normalised by the
+    // reference's sequential Kahan total on the host (bit-identical table)
+    if ((e = dev_to_host(ctx, p, dp, (size_t)width * height * sizeof(double)))) return e;
+    igs_internal_kahan_normalize(p, (size_t)width * height);
     return IGS_OK;
 }
 
@@ -923,6 +967,130 @@ int igs_psnr(igs_ctx* ctx, const float* rendered, int width, int height, double*
     int e;
     if ((e = stage_rendered(ctx, rendered, width, height, &dr))) return e;
     return igs_psnr_dev(ctx, dr, (const float*)ctx->target.p, (size_t)width * height * 3, out);
+}
+
+// ---- sampling tables (sampling.cpp:25-75) ----------------------------------------
+
+// device copy of an arbitrary float image (img == nullptr: the target)
+static int stage_image(igs_ctx* ctx, const float* img, int W, int H, const float** dev) {
+    if (W < 1 || H < 1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "image must be at least 1x1");
+    if (!img) {
+        if (!ctx->target.p || ctx->tgt_w != W || ctx->tgt_h != H)
+            return igs_fail(ctx, IGS_E_DIMENSION_MISMATCH, "no target image of these dimensions");
+        *dev = (const float*)ctx->target.p;
+        return IGS_OK;
+    }
+    const size_t bytes = (size_t)W * H * 3 * sizeof(float);
+    float* d = (float*)igs_scratch(ctx, 23, bytes);
+    if (!d) return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
+    *dev = d;
+    return host_to_dev(ctx, d, img, bytes);
+}
+
+int igs_image_gradient_magnitude(igs_ctx* ctx, const float* img, int width, int height, double* mag) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    const float* di;
+    int e;
+    if ((e = stage_image(ctx, img, width, height, &di))) return e;
+    const size_t npx = (size_t)width * height;
+    double* dm = (double*)igs_scratch(ctx, 12, npx * sizeof(double));
+    if (!dm) return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
+    if ((e = igs_sobel_dev(ctx, di, width, height, dm))) return e;
+    if (mag) return dev_to_host(ctx, mag, dm, npx * sizeof(double));
+    return IGS_OK;
+}
+
+int igs_gradient_mixture(igs_ctx* ctx, const float* img, int width, int height, double lambda, double* p) {
+    CHECK_CTX(ctx);
+    if (lambda < 0.0 || lambda > 1.0) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "lambda must lie in [0,1]");
+    if (!p) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "null output table");
+    int e;
+    // the magnitude on the device, the Kahan total and mixture on the host
+    if ((e = igs_image_gradient_magnitude(ctx, img, width, height, p))) return e;
+    igs_internal_gradient_mixture(p, (size_t)width * height, lambda, p);
+    return IGS_OK;
+}
+
+// bsp.cpp:343-406 bench_render: random continuous points (Rng(seed), two
+// next_double() per point), the global top-K baseline, then per n_max a
+// build_partition and the blocked point query.  Device time per trial
+// (CUDA events around the launch), scaled to ms per 10k points; mean and
+// population std over the trials as the reference computes them.
+// Candidates per point = |shell_members[locate_block(x)]| (the reference's
+// count, bit-identical); the baseline row reports N (its global scan).
+// The partition of the last n_max stays resident.
+int igs_bench_render(igs_ctx* ctx, int pixels, const int* n_max_values, int n_values, uint64_t seed, int trials,
+                     int warmup, igs_bench_row* rows) {
+    CHECK_CTX(ctx);
+    cudaSetDevice(ctx->device);
+    if (ctx->n == 0) return igs_fail(ctx, IGS_E_EMPTY_SET, "bench requires a non-empty GaussianSet");
+    if (pixels < 1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "pixel count must be >= 1");
+    if (trials < 1 || warmup < 0 || n_values < 0 || (n_values && !n_max_values) || !rows)
+        return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "bench needs trials >= 1 and a row buffer");
+    std::mt19937_64 rng(seed);
+    std::vector<double> uv((size_t)pixels * 2);
+    for (auto& x : uv) x = (double)(rng() >> 11) * 0x1.0p-53;  // rng.hpp next_double, u then v
+    const uint32_t npts = (uint32_t)pixels;
+    const int kk = (int)std::min<uint32_t>(10u, ctx->n);  // kDefaultTopK
+    double* duv = (double*)igs_scratch(ctx, 38, (size_t)npts * 16);
+    double* drgb = (double*)igs_scratch(ctx, 39, (size_t)npts * 24);
+    uint32_t* li = (uint32_t*)igs_scratch(ctx, 18, (size_t)npts * kk * sizeof(uint32_t));
+    double* lq = (double*)igs_scratch(ctx, 19, (size_t)npts * kk * sizeof(double));
+    if (!duv || !drgb || !li || !lq) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (bench)");
+    int e;
+    if ((e = host_to_dev(ctx, duv, uv.data(), uv.size() * sizeof(double)))) return e;
+    cudaEvent_t a, b;
+    IGS_CUDA(ctx, cudaEventCreate(&a));
+    IGS_CUDA(ctx, cudaEventCreate(&b));
+    const double to_10k = 10000.0 / pixels;
+    auto time_trials = [&](auto&& body, double* mean_out, double* sd_out) -> int {
+        std::vector<double> ms(trials);
+        int e2;
+        for (int t = 0; t < warmup; ++t)
+            if ((e2 = body())) return e2;
+        for (int t = 0; t < trials; ++t) {
+            IGS_CUDA(ctx, cudaEventRecord(a, ctx->stream));
+            if ((e2 = body())) return e2;
+            IGS_CUDA(ctx, cudaEventRecord(b, ctx->stream));
+            IGS_CUDA(ctx, cudaEventSynchronize(b));
+            float f = 0.0f;
+            IGS_CUDA(ctx, cudaEventElapsedTime(&f, a, b));
+            ms[t] = f * to_10k;
+        }
+        double mean = 0.0;
+        for (double v : ms) mean += v;
+        mean /= trials;
+        double var = 0.0;
+        for (double v : ms) var += (v - mean) * (v - mean);
+        *mean_out = mean;
+        *sd_out = std::sqrt(var / trials);
+        return IGS_OK;
+    };
+    rows[0] = {0, 0, 0.0, 0.0, (double)ctx->n};
+    e = time_trials([&]() -> int {
+        const int e2 = ctx->opt_cull && kk <= 32 ? igs_topk_knn(ctx, duv, npts, kk, li, lq)
+                                                 : igs_topk_points(ctx, duv, npts, kk, li, lq);
+        return e2 ? e2 : igs_blend_points(ctx, lq, li, npts, kk, drgb);
+    }, &rows[0].mean_ms_per_10k, &rows[0].std_ms);
+    for (int r = 0; !e && r < n_values; ++r) {
+        if ((e = igs_partition_build(ctx, n_max_values[r]))) break;
+        uint32_t nb = 0;
+        uint64_t tot = 0;
+        if ((e = igs_partition_info(ctx, &nb, &tot))) break;
+        std::vector<uint32_t> off(nb + 1);
+        std::vector<int32_t> blk(npts);
+        if ((e = igs_partition_get(ctx, nullptr, nullptr, off.data(), nullptr))) break;
+        if ((e = igs_locate_blocks(ctx, uv.data(), npts, blk.data()))) break;
+        double cand = 0.0;
+        for (uint32_t i = 0; i < npts; ++i) cand += (double)(off[blk[i] + 1] - off[blk[i]]);
+        rows[r + 1] = {n_max_values[r], (int)nb, 0.0, 0.0, cand / pixels};
+        e = time_trials([&]() { return igs_blocked_points_dev(ctx, duv, npts, kk, drgb); },
+                        &rows[r + 1].mean_ms_per_10k, &rows[r + 1].std_ms);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return e;
 }
 
 int igs_tile_lists(igs_ctx* ctx, int width, int height, int k, uint32_t* ntiles, uint64_t* total, uint32_t* offsets,
@@ -1020,21 +1188,27 @@ int igs_decode(igs_ctx* ctx, const uint8_t* bytes, size_t size, uint32_t* width,
                         "file length " + std::to_string(size) + " != expected " + std::to_string(expected));
     if (kk < 1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "header k must be >= 1");
     if (w == 0 || h == 0) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "header dimensions must be positive");
-    int e = ensure_capacity(ctx, n, false);
-    if (e) return e;
+    // decode() is a pure function in the reference: a file that fails
+    // validation leaves the caller's set untouched.  Unpack into scratch,
+    // check, and only then replace the resident set.
     uint16_t* dev = (uint16_t*)igs_scratch(ctx, 33, (size_t)n * 16);
-    if (!dev) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (decode)");
+    double* staged = (double*)igs_scratch(ctx, 36, (size_t)n * 8 * sizeof(double));
+    if (!dev || !staged) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (decode)");
+    int e;
     if ((e = host_to_dev(ctx, dev, bytes + 20, (size_t)n * 16))) return e;
     if ((e = igs_status_reset(ctx))) return e;
-    if ((e = igs_codec_unpack(ctx, dev, n))) return e;
+    if ((e = igs_codec_unpack(ctx, dev, nullptr, n, staged))) return e;
     long long st[4];
     if ((e = dev_to_host(ctx, st, ctx->status, sizeof(st)))) return e;
     if (st[1] != LLONG_MAX) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "non-finite Gaussian parameters");
+    if ((e = ensure_capacity(ctx, n, false))) return e;
+    const size_t rb = (size_t)n * 8 * sizeof(double);
+    IGS_CUDA(ctx, cudaMemcpyAsync(ctx->params, staged, rb, cudaMemcpyDeviceToDevice, ctx->stream));
     // a new set: fresh moments and gradients, as igs_set_params
+    ctx->moments_local = false;
     ctx->n = n;
     ctx->grads_valid = false;
     ctx->params_version++;
-    const size_t rb = (size_t)n * 8 * sizeof(double);
     IGS_CUDA(ctx, cudaMemsetAsync(ctx->adam_m, 0, rb, ctx->stream));
     IGS_CUDA(ctx, cudaMemsetAsync(ctx->adam_v, 0, rb, ctx->stream));
     IGS_CUDA(ctx, cudaMemsetAsync(ctx->grads, 0, rb, ctx->stream));
@@ -1058,61 +1232,19 @@ int igs_quantize_set(igs_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->n == 0) return IGS_OK;
     int e;
+    // quantize_set returns a new set (codec.cpp:69-81): round into scratch and
+    // commit only when every record is finite
+    double* staged = (double*)igs_scratch(ctx, 36, (size_t)ctx->n * 8 * sizeof(double));
+    if (!staged) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (quantize)");
     if ((e = igs_status_reset(ctx))) return e;
-    if ((e = igs_codec_unpack(ctx, nullptr, ctx->n))) return e;
+    if ((e = igs_codec_unpack(ctx, nullptr, ctx->params, ctx->n, staged))) return e;
     long long st[4];
     if ((e = dev_to_host(ctx, st, ctx->status, sizeof(st)))) return e;
     if (st[1] != LLONG_MAX) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "non-finite Gaussian parameters");
+    IGS_CUDA(ctx, cudaMemcpyAsync(ctx->params, staged, (size_t)ctx->n * 8 * sizeof(double), cudaMemcpyDeviceToDevice,
+                                  ctx->stream));
     ctx->params_version++;
     return igs_prepare_all(ctx, 0);
-}
-
-// ---- multi-GPU -------------------------------------------------------------------
-int igs_comm_unique_id(uint8_t id[128]) {
-#ifndef IGS_NO_NCCL
-    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
-    ncclUniqueId u;
-    if (!nccl().ok || nccl().getUniqueId(&u) != ncclSuccess) return IGS_E_CUDA;
-    std::memcpy(id, &u, 128);
-    return IGS_OK;
-#else
-    (void)id;
-    return IGS_E_CUDA;
-#endif
-}
-
-int igs_comm_init(igs_ctx* ctx, const uint8_t id[128], int nranks, int rank) {
-    CHECK_CTX(ctx);
-    cudaSetDevice(ctx->device);
-    if (nranks < 1 || rank < 0 || rank >= nranks) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "bad rank");
-#ifndef IGS_NO_NCCL
-    if (!nccl().ok) return igs_fail(ctx, IGS_E_CUDA, "libnccl.so.2 not found");
-    if (ctx->comm) {
-        nccl().commDestroy(ctx->comm);
-        ctx->comm = nullptr;
-    }
-    ncclUniqueId u;
-    std::memcpy(&u, id, 128);
-    if (nccl().commInitRank(&ctx->comm, nranks, u, rank) != ncclSuccess)
-        return igs_fail(ctx, IGS_E_CUDA, "ncclCommInitRank failed");
-    ctx->nranks = nranks;
-    ctx->rank = rank;
-    return IGS_OK;
-#else
-    (void)id;
-    return igs_fail(ctx, IGS_E_CUDA, "built without NCCL");
-#endif
-}
-
-int igs_comm_destroy(igs_ctx* ctx) {
-    CHECK_CTX(ctx);
-#ifndef IGS_NO_NCCL
-    if (ctx->comm) nccl().commDestroy(ctx->comm);
-    ctx->comm = nullptr;
-#endif
-    ctx->nranks = 1;
-    ctx->rank = 0;
-    return IGS_OK;
 }
 
 }  // extern "C"

@@ -74,29 +74,43 @@ void parallel_for(size_t n, F f) {
     for (auto& t : th) t.join();
 }
 
-// sampling.cpp:44-67 (rows in parallel)
-std::vector<double> gradient_magnitude(const float* img, int W, int H) {
-    std::vector<double> mag((size_t)W * H);
-    auto cl = [](int v, int hi) { return v < 0 ? 0 : (v > hi ? hi : v); };
-    auto at = [&](int h, int w, int c) { return (double)img[((size_t)h * W + w) * 3 + c]; };
-    parallel_for((size_t)H * W, [&](size_t b, size_t e) {
-    for (size_t f = b; f < e; ++f) {
-            const int h = (int)(f / W), w = (int)(f % W);
-            const int hm = cl(h - 1, H - 1), hp = cl(h + 1, H - 1), wm = cl(w - 1, W - 1), wp = cl(w + 1, W - 1);
-            double acc = 0.0;
-            for (int c = 0; c < 3; ++c) {
-                const double tl = at(hm, wm, c), tc = at(hm, w, c), tr = at(hm, wp, c);
-                const double ml = at(h, wm, c), mr = at(h, wp, c);
-                const double bl = at(hp, wm, c), bc = at(hp, w, c), br = at(hp, wp, c);
-                const double gx = (tr + 2.0 * mr + br) - (tl + 2.0 * ml + bl);
-                const double gy = (bl + 2.0 * bc + br) - (tl + 2.0 * tc + tr);
-                acc += gx * gx + gy * gy;
-            }
-            mag[(size_t)h * W + w] = std::sqrt(acc);
+}  // namespace
+
+// sampling.cpp:84-93 add_distribution's normalisation: Kahan total in index
+// order, then v *= 1/total (elementwise, any split), uniform when zero.
+extern "C" void igs_internal_kahan_normalize(double* p, size_t n) {
+    double sum = 0.0, comp = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+        const double y = p[i] - comp;
+        const double t = sum + y;
+        comp = (t - sum) - y;
+        sum = t;
     }
-    });
-    return mag;
+    if (sum > 0.0) {
+        const double inv = 1.0 / sum;
+        parallel_for(n, [&](size_t b, size_t e) {
+            for (size_t i = b; i < e; ++i) p[i] *= inv;
+        });
+    } else {
+        const double u = 1.0 / (double)n;
+        for (size_t i = 0; i < n; ++i) p[i] = u;
+    }
 }
+
+namespace {
+double kahan_sum(const std::vector<double>& v);
+std::vector<double> gradient_mixture(const std::vector<double>& mag, double total, double lambda);
+}  // namespace
+
+// sampling.cpp:25-40 gradient_mixture from a magnitude table (in place
+// allowed): Kahan total in index order, then the elementwise mixture.
+extern "C" void igs_internal_gradient_mixture(const double* mag, size_t n, double lambda, double* p) {
+    std::vector<double> m(mag, mag + n);
+    const std::vector<double> q = gradient_mixture(m, kahan_sum(m), lambda);
+    std::memcpy(p, q.data(), n * sizeof(double));
+}
+
+namespace {
 
 // sampling.cpp:25-40 gradient_mixture (init_distribution / opt_distribution)
 // from a precomputed gradient magnitude and its Kahan total: the init and
@@ -258,7 +272,11 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
     // initialize_set(target, budget/2, lambda_init, rng) (sampling.cpp:154-174)
     const int init_count = c.budget / 2;
     std::vector<double> set;
-    const std::vector<double> mag = gradient_magnitude(target, W, H);
+    // image_gradient_magnitude on the device (sobel_kernel, bit-identical),
+    // its Kahan total and the mixtures here
+    if ((e = igs_set_target(ctx, target, W, H))) return e;
+    std::vector<double> mag((size_t)W * H);
+    if ((e = igs_image_gradient_magnitude(ctx, nullptr, W, H, mag.data()))) return e;
     const double mag_total = kahan_sum(mag);
     {
         const Alias init(gradient_mixture(mag, mag_total, c.lambda_init));
@@ -269,7 +287,6 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
     }
     const Alias opt(gradient_mixture(mag, mag_total, c.lambda_opt));
     if (!opt.ok) return bad("alias table weights must have positive sum");
-    if ((e = igs_set_target(ctx, target, W, H))) return e;
     if ((e = igs_set_params(ctx, set.data(), (uint32_t)init_count))) return e;
     // the per-iteration draws from `opt` happen on the device (the host only
     // advances the engine): the table goes up once

@@ -251,6 +251,7 @@ struct igs_ctx {
     // options
     int opt_cull = 1;
     int opt_deterministic = 1;
+    int opt_shard_adam = 1;  // multi-rank exchange: each rank updates its slice of the set, then an all-gather
     int opt_tile = 16;
     int opt_raster = 0;  // IGS_OPT_RASTER
 
@@ -273,7 +274,7 @@ struct igs_ctx {
     int tgt_w = 0, tgt_h = 0;
 
     // per-call scratch (grow-only), indexed by purpose
-    DevBuf scratch[40];
+    DevBuf scratch[48];
     // pinned host staging
     void* pinned = nullptr;
     size_t pinned_bytes = 0;
@@ -281,8 +282,15 @@ struct igs_ctx {
     long long* status = nullptr;
 
     // pinned staging of the async iteration (igs_train_iteration_async)
-    // (two slots: samples, result block and completion event per slot)
-    DevBuf async_pin[4];
+    // (two slots: [slot] samples, [2 + slot] result block, [4 + slot] the
+    // per-sample losses, and a completion event per slot)
+    DevBuf async_pin[6];
+    uint32_t async_ns[2] = {0, 0};  // samples (all ranks) of the iteration in each slot
+    // host-mapped buffer the search epilogue mirrors the per-sample losses
+    // into (set around one igs_forward_backward call; loss_mirrored reports
+    // whether that call's search wrote it)
+    double* loss_mirror = nullptr;
+    bool loss_mirrored = false;
     cudaEvent_t async_ev[2] = {nullptr, nullptr};
     StageJob stage_job;          // handed from igs_forward_backward to knn_build (see StageJob)
     struct {
@@ -326,8 +334,21 @@ struct igs_ctx {
 #ifndef IGS_NO_NCCL
     ncclComm_t comm = nullptr;
 #endif
+    struct igs_loop_group* loop = nullptr;  // in-process loopback group (comm.cu)
+    bool moments_local = false;  // sharded update: only this rank's slice of adam_m/adam_v is current
     int nranks = 1, rank = 0;
 };
+
+// comm.cu: the multi-rank transport (NCCL or the in-process loopback group)
+inline bool igs_has_comm(const igs_ctx* ctx) {
+#ifndef IGS_NO_NCCL
+    if (ctx->comm) return true;
+#endif
+    return ctx->loop != nullptr;
+}
+int igs_comm_allgather(igs_ctx* ctx, void* buf, size_t bytes);
+int igs_comm_allreduce_sum(igs_ctx* ctx, double* buf, size_t count);
+void igs_comm_release(igs_ctx* ctx);
 
 // helpers implemented in ctx.cu
 int igs_fail(igs_ctx* ctx, int code, const std::string& msg);
@@ -392,24 +413,38 @@ __device__ __forceinline__ void prefetch_l2(const L2Prefetch& pf, uint32_t tid, 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 template <typename... KArgs, typename... Args>
-inline cudaError_t igs_launch_pdl(cudaStream_t st, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+inline cudaError_t igs_launch_pdl(cudaStream_t st, bool coop, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
                                   Args... args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
+    // kernels with grid barriers (igs_grid_sync) launch cooperatively: the
+    // driver then guarantees every CTA is co-resident or fails the launch
+    // (cudaErrorCooperativeLaunchTooLarge) instead of letting it spin forever
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = coop ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
 #define IGS_PDL(ctx, kernel, grid, block, smem, ...)                                                        \
     do {                                                                                                    \
-        cudaError_t _e = igs_launch_pdl((ctx)->stream, kernel, dim3(grid), dim3(block), (smem), __VA_ARGS__); \
+        cudaError_t _e =                                                                                    \
+            igs_launch_pdl((ctx)->stream, false, kernel, dim3(grid), dim3(block), (smem), __VA_ARGS__);     \
+        (ctx)->launches++;                                                                                  \
+        if (_e != cudaSuccess) return igs_cuda_check((ctx), _e, #kernel);                                   \
+    } while (0)
+// a persistent launch with grid barriers: cooperative + PDL
+#define IGS_PDL_COOP(ctx, kernel, grid, block, smem, ...)                                                   \
+    do {                                                                                                    \
+        cudaError_t _e =                                                                                    \
+            igs_launch_pdl((ctx)->stream, true, kernel, dim3(grid), dim3(block), (smem), __VA_ARGS__);      \
         (ctx)->launches++;                                                                                  \
         if (_e != cudaSuccess) return igs_cuda_check((ctx), _e, #kernel);                                   \
     } while (0)
@@ -431,6 +466,8 @@ void igs_timer_autostop(igs_ctx* ctx);
 int igs_prepare_all(igs_ctx* ctx, uint32_t first);
 int igs_raster_global(igs_ctx* ctx, int W, int H, int k, int row0, int row1, float* dev_out, uint32_t* dev_topk);
 int igs_topk_points(igs_ctx* ctx, const double* dev_uv, uint32_t npts, int k, uint32_t* dev_idx, double* dev_q);
+int igs_blocked_points_dev(igs_ctx* ctx, const double* duv, uint32_t npts, int kk, double* drgb);
+
 int igs_partition_free(igs_ctx* ctx);
 void igs_cull_free(igs_ctx* ctx);
 void igs_knn_free(igs_ctx* ctx);

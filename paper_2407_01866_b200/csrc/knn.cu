@@ -614,6 +614,7 @@ struct Epi {
     double inv_n;                // mode 0: 1 / (total samples over all ranks)
     const ShadeRec* shade;
     double* losses;              // mode 0: per point
+    double* host_losses;         // mode 0: host-mapped copy of losses (the host sums them in sample order) or null
     double* contrib;             // modes 0/1: [pt][kk][8] (deterministic reduction) or null
     uint32_t* keys;              // modes 0/1: [pt][kk] Gaussian index, n for empty slots
     uint32_t* gcnt;              // modes 0/1 (deterministic): contributions per Gaussian
@@ -701,6 +702,7 @@ __device__ __forceinline__ void warp_epilogue(const Epi& E, const ScanRec* __res
         if (active && lane == 0) {
             const double l = __dadd_rn(__dadd_rn(fabs(d0), fabs(d1)), fabs(d2));
             E.losses[pt] = l;
+            if (E.host_losses) E.host_losses[pt] = l;
             if (!isfinite(l) && !E.defer_loss_check) atomicMin(E.status + 2, (long long)pt);
         }
         up0 = __dmul_rn(sign_of(d0), E.inv_n);
@@ -1702,7 +1704,7 @@ int knn_build(igs_ctx* ctx) {
                 return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
             IGS_CUDA(ctx, cudaMemsetAsync(b.bctl.p, 0, 8, ctx->stream));
         }
-        IGS_PDL(ctx, lq_build_kernel, ctx->sm_count, kBuildThreads, 0, (const ScanRec*)ctx->scan, n, L, cells, cnt,
+        IGS_PDL_COOP(ctx, lq_build_kernel, ctx->sm_count, kBuildThreads, 0, (const ScanRec*)ctx->scan, n, L, cells, cnt,
                 cur, off, (uint32_t*)b.key.p, (uint32_t*)b.mem.p, (ScanRec*)b.mrec.p, (uint32_t*)b.minv.p,
                 (Acc*)b.acc.p, (uint32_t*)b.lcount.p, (unsigned*)b.bctl.p);
     } else {
@@ -1792,7 +1794,7 @@ int launch_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int 
             // (profiled with the reduction: mostly its offsets + scatter)
             igs_prof_end(ctx, IGS_PROF_SCAN, 0.0);
             igs_prof_begin(ctx, IGS_PROF_REDUCE);
-            IGS_PDL(ctx, hard_offsets_kernel<KCAP>, ctx->sm_count, kOffThreads, 0, (const ScanRec*)ctx->scan, ctx->n,
+            IGS_PDL_COOP(ctx, hard_offsets_kernel<KCAP>, ctx->sm_count, kOffThreads, 0, (const ScanRec*)ctx->scan, ctx->n,
                     uv, W, H, kk, (const uint32_t*)hard_count, (const uint32_t*)hard_list, E, part_q, part_i,
                     (unsigned int*)((uint32_t*)b.hard.p + 4 + kHardCap), igs_prof_counter(ctx, IGS_PROF_SCAN),
                     ctx->fuse_off.args);
@@ -2197,6 +2199,8 @@ int igs_knn_forward_backward(igs_ctx* ctx, int mode, const uint32_t* sidx, const
     E.inv_n = inv_n;
     E.shade = ctx->shade;
     E.losses = losses;
+    E.host_losses = mode == 0 && !defer_loss_check ? ctx->loss_mirror : nullptr;
+    ctx->loss_mirrored = E.host_losses != nullptr;
     E.contrib = contrib;
     E.keys = keys;
     E.grads_atomic = grads_atomic;

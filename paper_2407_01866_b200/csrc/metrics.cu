@@ -2,16 +2,21 @@
 // error-guided Gaussian addition (sampling.cpp:77-94 add_distribution) and
 // PSNR (metrics.cpp:12-27).
 //
-// The reference normalises with a sequential Kahan sum.  On the device the
-// total is a fixed-order tree of error-free double-double additions
-// (TwoSum), i.e. the (nearly) exact sum rounded once -- which is what a
-// Kahan sum of well-conditioned positive terms returns, so the normalised
-// table matches the reference bit for bit in practice and always within
-// 1 ulp.  HBM-bound: 24 B/px read + 8 B/px written.
+// The reference normalises with a sequential Kahan sum (sampling.cpp:14-23,
+// 86).  A sequential recurrence has no exact parallel form, and one ulp of
+// the total moves every normalised entry and with them the alias table's
+// `scaled < 1.0` splits (sampling.cpp:114), so when the table goes to the
+// host (igs_add_distribution with a host buffer, and every densification of
+// igs_fit) the device writes the raw map and the host sums it in the
+// reference's order (fit.cpp igs_internal_kahan_normalize).  The device-only
+// form normalises by a fixed-order tree of error-free double-double
+// additions (the nearly exact sum rounded once; within 1 ulp of Kahan's).
+// HBM-bound: 24 B/px read + 8 B/px written.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
+#include <thread>
 
 #include "igs_internal.cuh"
 
@@ -101,7 +106,7 @@ __global__ void normalize_kernel(double* __restrict__ p, size_t npx, const doubl
 
 }  // namespace
 
-int igs_error_map(igs_ctx* ctx, const float* dev_rendered, int W, int H, double* dev_p) {
+int igs_error_map(igs_ctx* ctx, const float* dev_rendered, int W, int H, double* dev_p, int normalize) {
     const size_t npx = (size_t)W * H;
     const int blocks = (int)std::min<size_t>(4 * ctx->sm_count, (npx + kRedThreads - 1) / kRedThreads);
     double* part = (double*)igs_scratch(ctx, 13, (size_t)(2 * blocks + 2) * sizeof(double));
@@ -109,6 +114,7 @@ int igs_error_map(igs_ctx* ctx, const float* dev_rendered, int W, int H, double*
     error_map_kernel<<<blocks, kRedThreads, 0, ctx->stream>>>(dev_rendered, (const float*)ctx->target.p, npx, dev_p,
                                                               part);
     IGS_LAUNCHED(ctx);
+    if (!normalize) return IGS_OK;  // the host normalises with the reference's Kahan total
     double* total = part + 2 * blocks;
     finish_sum_kernel<<<1, kRedThreads, 0, ctx->stream>>>(part, blocks, total);
     IGS_LAUNCHED(ctx);
@@ -176,13 +182,13 @@ __global__ void ssim_h_kernel(const float* __restrict__ a, const float* __restri
     for (int m = 0; m < 5; ++m) tmp[m * n + p] = s[m];
 }
 
-// vertical pass + SSIM map + per-block double-double partial sums
-__global__ void __launch_bounds__(kRedThreads) ssim_v_kernel(const double* __restrict__ tmp, int W, int H, Win11 win,
-                                                            double* __restrict__ part) {
+// vertical pass + the SSIM map (metrics.cpp:95-103, op for op); the
+// per-channel mean is summed on the host in pixel order (the reference's
+// plain sequential `acc += num / den`)
+__global__ void ssim_v_kernel(const double* __restrict__ tmp, int W, int H, Win11 win, double* __restrict__ map) {
     const size_t n = (size_t)W * H;
     const double c1 = 0.01 * 0.01, c2 = 0.03 * 0.03;
-    DD acc = {0.0, 0.0};
-    for (size_t p = (size_t)blockIdx.x * kRedThreads + threadIdx.x; p < n; p += (size_t)gridDim.x * kRedThreads) {
+    for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (size_t)gridDim.x * blockDim.x) {
         const int h = (int)(p / W), w = (int)(p % W);
         double s[5] = {0, 0, 0, 0, 0};
         for (int i = 0; i < 11; ++i) {
@@ -198,13 +204,31 @@ __global__ void __launch_bounds__(kRedThreads) ssim_v_kernel(const double* __res
         const double num = __dmul_rn(__dadd_rn(__dmul_rn(__dmul_rn(2.0, mx), my), c1), __dadd_rn(__dmul_rn(2.0, cov), c2));
         const double den = __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(mx, mx), __dmul_rn(my, my)), c1),
                                      __dadd_rn(__dadd_rn(var_x, var_y), c2));
-        acc = dd_add(acc, {__ddiv_rn(num, den), 0.0});
+        map[p] = __ddiv_rn(num, den);
     }
-    const DD r = block_reduce(acc);
-    if (threadIdx.x == 0) {
-        part[2 * blockIdx.x] = r.hi;
-        part[2 * blockIdx.x + 1] = r.lo;
+}
+
+// sampling.cpp:44-67 image_gradient_magnitude: six Sobel responses with
+// replicate padding, L2 norm, op for op (no FMA, IEEE sqrt).  One thread
+// per pixel; 12 B/px read (neighbours from L1/L2), 8 B/px written.
+__global__ void sobel_kernel(const float* __restrict__ img, int W, int H, double* __restrict__ mag) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x, h = blockIdx.y * blockDim.y + threadIdx.y;
+    if (w >= W || h >= H) return;
+    const int hm = clampi(h - 1, H - 1), hp = clampi(h + 1, H - 1), wm = clampi(w - 1, W - 1), wp = clampi(w + 1, W - 1);
+    auto at = [&](int y, int x, int c) { return (double)__ldg(img + ((size_t)y * W + x) * 3 + c); };
+    double acc = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double tl = at(hm, wm, c), tc = at(hm, w, c), tr = at(hm, wp, c);
+        const double ml = at(h, wm, c), mr = at(h, wp, c);
+        const double bl = at(hp, wm, c), bc = at(hp, w, c), br = at(hp, wp, c);
+        const double gx = __dsub_rn(__dadd_rn(__dadd_rn(tr, __dmul_rn(2.0, mr)), br),
+                                    __dadd_rn(__dadd_rn(tl, __dmul_rn(2.0, ml)), bl));
+        const double gy = __dsub_rn(__dadd_rn(__dadd_rn(bl, __dmul_rn(2.0, bc)), br),
+                                    __dadd_rn(__dadd_rn(tl, __dmul_rn(2.0, tc)), tr));
+        acc = __dadd_rn(acc, __dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)));
     }
+    mag[(size_t)h * W + w] = __dsqrt_rn(acc);
 }
 
 }  // namespace
@@ -221,22 +245,40 @@ int igs_ssim_dev(igs_ctx* ctx, const float* a, const float* b, int W, int H, dou
     for (double& v : win.w) v /= sum;
     const size_t n = (size_t)W * H;
     double* tmp = (double*)igs_scratch(ctx, 27, 5 * n * sizeof(double));
-    const int blocks = (int)std::min<size_t>(4 * ctx->sm_count, (n + kRedThreads - 1) / kRedThreads);
-    double* part = (double*)igs_scratch(ctx, 28, (size_t)(2 * blocks + 2) * sizeof(double));
-    if (!tmp || !part) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (ssim)");
-    double channel_sum = 0.0;
+    double* map = (double*)igs_scratch(ctx, 28, 3 * n * sizeof(double));
+    double* host = (double*)igs_pinned(ctx, 3 * n * sizeof(double));
+    if (!tmp || !map || !host) return igs_fail(ctx, IGS_E_CUDA, "out of memory (ssim)");
+    const int blocks = (int)std::min<size_t>(8 * ctx->sm_count, (n + 255) / 256);
     for (int c = 0; c < 3; ++c) {
         ssim_h_kernel<<<dim3((W + 127) / 128, H), 128, 0, ctx->stream>>>(a, b, W, H, c, win, tmp);
         IGS_LAUNCHED(ctx);
-        ssim_v_kernel<<<blocks, kRedThreads, 0, ctx->stream>>>(tmp, W, H, win, part);
+        ssim_v_kernel<<<blocks, 256, 0, ctx->stream>>>(tmp, W, H, win, map + c * n);
         IGS_LAUNCHED(ctx);
-        finish_sum_kernel<<<1, kRedThreads, 0, ctx->stream>>>(part, blocks, part + 2 * blocks);
-        IGS_LAUNCHED(ctx);
-        double acc = 0.0;
-        IGS_CUDA(ctx, cudaMemcpyAsync(&acc, part + 2 * blocks, 8, cudaMemcpyDeviceToHost, ctx->stream));
-        IGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-        channel_sum += acc / (double)n;
     }
+    IGS_CUDA(ctx, cudaMemcpyAsync(host, map, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    IGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    // metrics.cpp:95-106: acc += num / den in pixel order per channel (the
+    // three channels are independent sums: one host thread each)
+    double acc[3];
+    auto channel = [&](int c) {
+        double s2 = 0.0;
+        const double* m = host + c * n;
+        for (size_t i = 0; i < n; ++i) s2 += m[i];
+        acc[c] = s2;
+    };
+    std::thread t1(channel, 1), t2(channel, 2);
+    channel(0);
+    t1.join();
+    t2.join();
+    double channel_sum = 0.0;
+    for (int c = 0; c < 3; ++c) channel_sum += acc[c] / (double)n;
     *out = channel_sum / 3.0;
+    return IGS_OK;
+}
+
+// image_gradient_magnitude of a device image into dev_mag (H*W doubles)
+int igs_sobel_dev(igs_ctx* ctx, const float* img, int W, int H, double* dev_mag) {
+    sobel_kernel<<<dim3((W + 31) / 32, (H + 7) / 8), dim3(32, 8), 0, ctx->stream>>>(img, W, H, dev_mag);
+    IGS_LAUNCHED(ctx);
     return IGS_OK;
 }

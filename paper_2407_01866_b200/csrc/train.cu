@@ -591,12 +591,14 @@ __global__ void __launch_bounds__(128, 7) segment_adam_kernel(
     const double* __restrict__ contrib, uint32_t n, double* __restrict__ grads, double* __restrict__ params,
     double* __restrict__ m, double* __restrict__ v, ScanRec* __restrict__ scan, ShadeRec* __restrict__ shade,
     double lr_mu, double lr_color, double lr_scale, double lr_theta, double bc1, double bc2, double ibc1, double ibc2,
-    long long* __restrict__ status, TreeAcc ta) {
+    long long* __restrict__ status, TreeAcc ta, uint32_t g_begin, uint32_t g_end) {
     pdl_wait();
-    const uint32_t g0 = blockIdx.x * (blockDim.x / 2) + (threadIdx.x >> 1);
+    // Gaussians [g_begin, g_end): the whole set, or this rank's slice when
+    // the multi-rank update is sharded (n stays the set size: gcnt is [2n])
+    const uint32_t g0 = g_begin + blockIdx.x * (blockDim.x / 2) + (threadIdx.x >> 1);
     const int h = threadIdx.x & 1;
-    const bool live = g0 < n;
-    const uint32_t g = live ? g0 : n - 1;  // dead pairs shadow a live one (no writes) to keep shuffles full
+    const bool live = g0 < g_end;
+    const uint32_t g = live ? g0 : g_end - 1;  // dead pairs shadow a live one (no writes) to keep shuffles full
     uint32_t cntg = 0, og = 0;
     if (h == 0) {
         cntg = gcnt[g];
@@ -755,6 +757,34 @@ __global__ void __launch_bounds__(128, 7) segment_adam_kernel(
     }
 }
 
+
+// Sharded multi-rank update, after the parameter all-gather: the Gaussians
+// outside this rank's slice get their prepared records (kernel 1), their
+// tree accumulation (as the Adam kernel does for its own) and their
+// contribution counters cleared for the next step.
+__global__ void complement_prepare_kernel(const double* __restrict__ params, uint32_t n, uint32_t lo, uint32_t hi,
+                                          ScanRec* __restrict__ scan, ShadeRec* __restrict__ shade,
+                                          uint32_t* __restrict__ gcnt, TreeAcc ta) {
+    pdl_wait();
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n - (hi - lo)) return;
+    const uint32_t g = j < lo ? j : j + (hi - lo);
+    const ScanRec r = prepare_one(params, g, scan, shade);
+    tree_acc_add(ta, g, r);
+    gcnt[g] = 0;
+    gcnt[n + g] = 0;
+}
+
+// status words [0..2] = the first flagged slot over all ranks (each rank
+// flagged only its own slice); [3] (a count) stays per rank
+__global__ void status_fold_kernel(const long long* __restrict__ gathered, int nranks, long long* __restrict__ status) {
+    pdl_wait();
+    const int j = threadIdx.x;
+    if (j >= 3) return;
+    long long v = gathered[j];
+    for (int r = 1; r < nranks; ++r) v = min(v, gathered[4 * r + j]);
+    status[j] = v;
+}
 
 // Start of an iteration fed from host memory: resets the status block and
 // copies the sample indices straight from the pinned (device-mapped) host
@@ -921,7 +951,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
         const int es = igs_stage_launch(ctx, *job);
         if (es) return es;
     }
-    const bool exch = ctx->comm != nullptr && ctx->opt_deterministic && knn_path;
+    const bool exch = igs_has_comm(ctx) && ctx->opt_deterministic && knn_path;
     const uint32_t R = exch ? (uint32_t)ctx->nranks : 1u, rk = exch ? (uint32_t)ctx->rank : 0u;
     ctx->exchanged = exch;
     const size_t items_local = (size_t)ns * kk;
@@ -1041,7 +1071,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
             if (!ctl) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (scan)");
             OffArgs A{(const uint32_t*)gcnt, n, goff, ctl + 2, (const uint32_t*)keys, (uint32_t)items, gcnt + n, perm,
                       long_ctl, long_ctl + 1, (unsigned*)ctl};
-            IGS_PDL(ctx, offsets_scatter_kernel, (unsigned)ctx->sm_count, kOffThreads, 0, A);
+            IGS_PDL_COOP(ctx, offsets_scatter_kernel, (unsigned)ctx->sm_count, kOffThreads, 0, A);
         } else {
             size_t tb = 0;
             cub::DeviceScan::ExclusiveSum(nullptr, tb, gcnt, goff, (int)n, ctx->stream);
@@ -1066,7 +1096,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
                 (const uint32_t*)goff, perm, (const double*)contrib, ctx->grads, (const uint32_t*)long_ctl,
                 (const uint32_t*)(long_ctl + 1), ctx->status, big, (const double*)losses, ns_all, inv_n,
                 mode == 0 ? dev_loss : nullptr, loss_part, (unsigned*)(loss_part + kLossCtas));
-        if (fuse_lr4 && (exch || (ctx->nranks == 1 && !ctx->comm))) {
+        if (fuse_lr4 && (exch || !igs_has_comm(ctx))) {
             // short segments summed inside the Adam kernel (one pass over the set)
             const double bc1 = 1.0 - std::pow(0.9, (double)t);  // adam.cpp:16-17, host libm
             const double bc2 = 1.0 - std::pow(0.999, (double)t);
@@ -1074,11 +1104,31 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
             ctx->params_version++;
             igs_prof_end(ctx, IGS_PROF_REDUCE, (double)items);
             igs_prof_begin(ctx, IGS_PROF_ADAM);
-            IGS_PDL(ctx, segment_adam_kernel, (n + 63) / 64, 128, 0, gcnt, (const uint32_t*)goff,
-                    (const uint32_t*)perm, (const double*)contrib, n, ctx->grads, ctx->params, ctx->adam_m,
-                    ctx->adam_v, ctx->scan, ctx->shade, fuse_lr4[0], fuse_lr4[1], fuse_lr4[2], fuse_lr4[3], bc1, bc2,
-                    1.0 / bc1, 1.0 / bc2, ctx->status, ta);
-            igs_prof_end(ctx, IGS_PROF_ADAM, (double)n * 596.0);
+            // multi-rank: this rank's slice [lo, hi) of ceil(n/R)-record blocks
+            const uint32_t B = (n + R - 1) / R;
+            const bool shard = exch && R > 1 && ctx->opt_shard_adam && (size_t)B * R <= ctx->cap;
+            const uint32_t lo = shard ? std::min(n, rk * B) : 0u, hi = shard ? std::min(n, lo + B) : n;
+            if (hi > lo)
+                IGS_PDL(ctx, segment_adam_kernel, (hi - lo + 63) / 64, 128, 0, gcnt, (const uint32_t*)goff,
+                        (const uint32_t*)perm, (const double*)contrib, n, ctx->grads, ctx->params, ctx->adam_m,
+                        ctx->adam_v, ctx->scan, ctx->shade, fuse_lr4[0], fuse_lr4[1], fuse_lr4[2], fuse_lr4[3], bc1,
+                        bc2, 1.0 / bc1, 1.0 / bc2, ctx->status, ta, lo, hi);
+            if (shard) {
+                // flags of every slice, then every slice's parameters, then
+                // the records + tree accumulation of the other slices here
+                long long* st = (long long*)igs_scratch(ctx, 40, (size_t)R * 4 * sizeof(long long));
+                if (!st) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (shard)");
+                IGS_CUDA(ctx, cudaMemcpyAsync(st + 4 * rk, ctx->status, 4 * sizeof(long long),
+                                              cudaMemcpyDeviceToDevice, ctx->stream));
+                if ((e = igs_comm_allgather(ctx, st, 4 * sizeof(long long)))) return e;
+                IGS_PDL(ctx, status_fold_kernel, 1, 32, 0, (const long long*)st, (int)R, ctx->status);
+                if ((e = igs_comm_allgather(ctx, ctx->params, (size_t)B * 8 * sizeof(double)))) return e;
+                if (n > hi - lo)
+                    IGS_PDL(ctx, complement_prepare_kernel, (n - (hi - lo) + 255) / 256, 256, 0,
+                            (const double*)ctx->params, n, lo, hi, ctx->scan, ctx->shade, gcnt, ta);
+                ctx->moments_local = true;
+            }
+            igs_prof_end(ctx, IGS_PROF_ADAM, (double)(hi - lo) * 596.0);
             ctx->gcnt_clean = gcnt;
             ctx->gcnt_clean_n = n;
             if (fused) *fused = true;

@@ -49,7 +49,7 @@ ERROR_KINDS = {
     100: "cuda",
 }
 
-OPT_CULL, OPT_DETERMINISTIC, OPT_TILE, OPT_RASTER = 1, 2, 3, 4
+OPT_CULL, OPT_DETERMINISTIC, OPT_TILE, OPT_RASTER, OPT_SHARD_ADAM = 1, 2, 3, 4, 5
 PROF_SCAN, PROF_FINISH, PROF_REDUCE, PROF_ADAM, PROF_CULL, PROF_BLOCKED, PROF_KNN_HARD = range(7)
 PROF_NAMES = ["scan", "finish", "reduce", "adam", "cull", "blocked", "knn_hard"]
 
@@ -73,6 +73,11 @@ class EvalRecord(C.Structure):
 
 
 CHECKPOINT_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.c_int, C.c_char_p, C.POINTER(C.c_double), C.c_uint32)
+
+
+class BenchRow(C.Structure):
+    _fields_ = [("n_max", C.c_int), ("n_b", C.c_int), ("mean_ms_per_10k", C.c_double), ("std_ms", C.c_double),
+                ("mean_candidates", C.c_double)]
 
 
 class IgsError(RuntimeError):
@@ -143,11 +148,15 @@ SIGNATURES = {
     "igs_flush_l2": (C.c_int, [_vp, C.c_size_t]),
     "igs_fp64_peak": (C.c_int, [_vp, _dp]),
     "igs_libm_eval": (C.c_int, [_vp, _dp, C.c_uint32, _dp]),
+    "igs_bench_render": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_int), C.c_int, C.c_uint64, C.c_int, C.c_int,
+                                   C.POINTER(BenchRow)]),
     "igs_profile_enable": (C.c_int, [_vp, C.c_int]),
     "igs_profile_read": (C.c_int, [_vp, C.c_int, _dp, _u64p, _dp]),
     "igs_train_iteration_async": (C.c_int, [_vp, _up, C.c_uint32, C.c_int, _dp, C.c_longlong]),
     "igs_train_wait": (C.c_int, [_vp, _dp]),
     "igs_ssim": (C.c_int, [_vp, _fp, C.c_int, C.c_int, _dp]),
+    "igs_image_gradient_magnitude": (C.c_int, [_vp, _fp, C.c_int, C.c_int, _dp]),
+    "igs_gradient_mixture": (C.c_int, [_vp, _fp, C.c_int, C.c_int, C.c_double, _dp]),
     "igs_fit_config_default": (None, [C.POINTER(FitConfig)]),
     "igs_fit": (C.c_int, [_vp, _fp, C.c_int, C.c_int, C.POINTER(FitConfig), CHECKPOINT_FN, C.c_void_p,
                           C.POINTER(EvalRecord), C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
@@ -155,6 +164,8 @@ SIGNATURES = {
     "igs_comm_unique_id": (C.c_int, [_u8p]),
     "igs_comm_init": (C.c_int, [_vp, _u8p, C.c_int, C.c_int]),
     "igs_comm_destroy": (C.c_int, [_vp]),
+    "igs_comm_init_loopback": (C.c_int, [C.POINTER(_vp), C.c_int]),
+    "igs_comm_gather_moments": (C.c_int, [_vp]),
 }
 
 _lib = None
@@ -362,6 +373,23 @@ class Context:
         self._chk(self.lib.igs_ssim(self.h, _p(r, _fp), width, height, C.byref(out)))
         return out.value
 
+    def image_gradient_magnitude(self, img=None, width: int = 0, height: int = 0):
+        """sampling.cpp:44-67 on the device; img None = the resident target."""
+        if img is not None:
+            img = np.ascontiguousarray(img, np.float32)
+            height, width = img.shape[:2]
+        out = np.zeros((height, width))
+        self._chk(self.lib.igs_image_gradient_magnitude(self.h, _p(img, _fp), width, height, _p(out, _dp)))
+        return out
+
+    def gradient_mixture(self, img, lam: float):
+        """init/opt_distribution (sampling.cpp:25-40)."""
+        img = np.ascontiguousarray(img, np.float32)
+        H, W = img.shape[:2]
+        out = np.zeros((H, W))
+        self._chk(self.lib.igs_gradient_mixture(self.h, _p(img, _fp), W, H, lam, _p(out, _dp)))
+        return out
+
     def train_iteration_async(self, sample_idx, k: int = DEFAULT_K, lr=DEFAULT_LR, t: int = 1):
         self._async_keep = np.ascontiguousarray(sample_idx, np.uint32)
         lr = np.ascontiguousarray(lr, np.float64)
@@ -506,6 +534,13 @@ class Context:
         self._chk(self.lib.igs_fp64_peak(self.h, C.byref(out)))
         return out.value
 
+    def bench_render(self, pixels: int, n_max_values, seed: int, trials: int = 20, warmup: int = 3):
+        """bench_render (bsp.cpp:343-406): [baseline] + one row per n_max as dicts."""
+        nm = (C.c_int * max(len(n_max_values), 1))(*n_max_values)
+        rows = (BenchRow * (len(n_max_values) + 1))()
+        self._chk(self.lib.igs_bench_render(self.h, pixels, nm, len(n_max_values), seed, trials, warmup, rows))
+        return [{f: getattr(r, f) for f, _ in BenchRow._fields_} for r in rows]
+
     def libm_eval(self, x):
         """Device glibc-exact (exp, sin, cos) of each x (parity diagnostics)."""
         x = np.ascontiguousarray(x, np.float64).ravel()
@@ -534,6 +569,19 @@ class Context:
     def comm_init(self, uid: bytes, nranks: int, rank: int):
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
         self._chk(self.lib.igs_comm_init(self.h, buf, nranks, rank))
+
+    @staticmethod
+    def comm_init_loopback(ctxs):
+        """Joins the contexts into one in-process loopback group (rank = list
+        position); drive each from its own thread afterwards."""
+        arr = (_vp * len(ctxs))(*[c.h for c in ctxs])
+        code = load_library().igs_comm_init_loopback(arr, len(ctxs))
+        if code:
+            raise IgsError(code, ctxs[0].lib.igs_last_error(ctxs[0].h).decode() if ctxs else "")
+
+    def comm_gather_moments(self):
+        """(collective) re-replicate the sharded Adam moments on every rank."""
+        self._chk(self.lib.igs_comm_gather_moments(self.h))
 
     def comm_destroy(self):
         self._chk(self.lib.igs_comm_destroy(self.h))

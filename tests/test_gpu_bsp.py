@@ -99,3 +99,18 @@ def test_stale_partition_rejected(gctx):
     assert e.value.kind == "invalid_parameter" and "stale" in str(e.value)
     with pytest.raises(IgsError):
         gctx.render_points_blocked([[0.5, 0.5]], 10)
+
+
+def test_bench_render_rows_match_reference(gctx, ref):
+    """a18: bench_render (bsp.cpp:343-406) -- the same random points, the same
+    partitions per n_max, so N_b and the mean candidate count per point
+    equal the reference's exactly; the times are device times."""
+    params = synth.random_local_set(20_000, 1024, 1024, seed=7)
+    n_max = [8, 32, 64, 128]
+    gctx.set_params(params)
+    rows = gctx.bench_render(10_000, n_max, seed=5, trials=5, warmup=1)
+    want = ref.bench_render(params, 10_000, n_max, seed=5, trials=1, warmup=0)
+    assert [r["n_max"] for r in rows] == [0] + n_max
+    assert [r["n_b"] for r in rows] == [int(w) for w in want[:, 1]]
+    assert [r["mean_candidates"] for r in rows] == list(want[:, 4])
+    assert all(r["mean_ms_per_10k"] > 0 and r["std_ms"] >= 0 for r in rows)

@@ -120,7 +120,7 @@ def train_compare(gctx, ref, params, target, sidx, tag):
                adam_params_differing=int((p1 != wp).sum()), adam_m_differing=int((m1 != wm).sum()),
                adam_v_differing=int((v1 != wv).sum()), seconds_gpu_call=t_gpu, seconds_ref=t_ref)
     record(tag, **rec)
-    assert abs(loss - wl) <= 1e-12 * abs(wl)
+    assert loss == wl
     check_grads(gs)
     assert rec["adam_params_differing"] == 0 and rec["adam_m_differing"] == 0 and rec["adam_v_differing"] == 0
 
@@ -189,7 +189,7 @@ def test_c2_trajectory_10_iterations(gctx, ref, c2):
                v_differing=int((gv != v).sum()),
                max_param_abs_diff=float(np.max(np.abs(got - p))), loss_last=losses[-1], loss_last_ref=wlosses[-1])
     record("c2_trajectory", **rec)
-    np.testing.assert_allclose(losses, wlosses, rtol=1e-10)
+    assert losses == wlosses
     assert rec["params_differing"] == 0 and rec["m_differing"] == 0 and rec["v_differing"] == 0
 
 
