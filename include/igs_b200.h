@@ -216,6 +216,9 @@ int igs_partition_get(igs_ctx* ctx, double* blocks4, double* shells4, uint32_t* 
 int igs_locate_blocks(igs_ctx* ctx, const double* uv, uint32_t npts, int32_t* blocks);
 /* render_image_blocked (bsp.cpp:334) through the resident partition. */
 int igs_render_image_blocked(igs_ctx* ctx, int width, int height, int k, float* out_rgb);
+/* Rows [row0, row1) of the blocked render (tile-row sharding of the decode /
+ * evaluation render); out_rgb receives (row1-row0)*W*3 floats (nullable). */
+int igs_render_image_blocked_rows(igs_ctx* ctx, int width, int height, int k, int row0, int row1, float* out_rgb);
 /* render_topk_blocked at npts points (random-access decode queries). */
 int igs_render_points_blocked(igs_ctx* ctx, const double* uv, uint32_t npts, int k, double* rgb);
 

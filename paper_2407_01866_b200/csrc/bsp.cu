@@ -262,14 +262,15 @@ __global__ void __launch_bounds__(256) blocked_raster_kernel(const ScanRec* __re
                                                              const ShadeRec* __restrict__ shade, LocView v,
                                                              const uint32_t* __restrict__ shell_off,
                                                              const uint32_t* __restrict__ shell_mem, int W, int H,
-                                                             int kk, float* __restrict__ out,
+                                                             int row0, int row1, int kk, float* __restrict__ out,
                                                              unsigned long long* __restrict__ pairs) {
     __shared__ ScanRec sm[kChunk];
     __shared__ uint32_t sidx[kChunk];
     __shared__ int cur_block;
     const int tid = threadIdx.y * kTile + threadIdx.x;
-    const int px = blockIdx.x * kTile + threadIdx.x, py = blockIdx.y * kTile + threadIdx.y;
-    const bool live = px < W && py < H;
+    // rows [row0, row1) of the W x H raster, written at their place in `out`
+    const int px = blockIdx.x * kTile + threadIdx.x, py = row0 + blockIdx.y * kTile + threadIdx.y;
+    const bool live = px < W && py < row1;
     const double x = center(px, W), y = center(py, H);
     const int myb = live ? locate(v, x, y) : 0x7fffffff;
     bool done = !live;
@@ -815,26 +816,31 @@ int igs_locate_blocks(igs_ctx* ctx, const double* uv, uint32_t npts, int32_t* bl
     return IGS_OK;
 }
 
-// bsp.cpp:334 render_image_blocked
-int igs_render_image_blocked(igs_ctx* ctx, int width, int height, int k, float* out_rgb) {
+// bsp.cpp:334 render_image_blocked, rows [row0, row1) (tile-row sharding of
+// the evaluation / decode render); the rows land at their place in the
+// context's W x H image
+int igs_blocked_render_rows(igs_ctx* ctx, int width, int height, int k, int row0, int row1) {
     if (!ctx) return IGS_E_INVALID_PARAMETER;
     cudaSetDevice(ctx->device);
     if (ctx->n == 0) return igs_fail(ctx, IGS_E_EMPTY_SET, "render requires a non-empty GaussianSet");
     if (width < 1 || height < 1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "render target must be at least 1x1");
     if (k < 1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "k must be >= 1");
+    if (row0 < 0 || row1 > height || row0 > row1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "bad row range");
     int e;
     if ((e = check_partition(ctx))) return e;
     if ((e = igs_ensure_image(ctx, width, height))) return e;
     const int kk = (int)std::min<uint32_t>((uint32_t)k, ctx->n);
     if (kk > 32) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "blocked render supports k <= 32");
+    if (row1 == row0) return IGS_OK;
     const LocView v = view_of(ctx->part);
-    dim3 grid((width + kTile - 1) / kTile, (height + kTile - 1) / kTile), blk(kTile, kTile);
+    dim3 grid((width + kTile - 1) / kTile, (row1 - row0 + kTile - 1) / kTile), blk(kTile, kTile);
     float* out = (float*)ctx->image.p;
     unsigned long long* pairs = igs_prof_counter(ctx, IGS_PROF_BLOCKED);
     igs_prof_begin(ctx, IGS_PROF_BLOCKED);
 #define LAUNCH(KC)                                                                                          \
     blocked_raster_kernel<KC><<<grid, blk, 0, ctx->stream>>>(ctx->scan, ctx->shade, v, ctx->part->d_shell_off, \
-                                                             ctx->part->d_shell_mem, width, height, kk, out, pairs)
+                                                             ctx->part->d_shell_mem, width, height, row0, row1, kk, \
+                                                             out, pairs)
     if (kk <= 4) LAUNCH(4);
     else if (kk <= 8) LAUNCH(8);
     else if (kk <= 10) LAUNCH(10);
@@ -843,8 +849,26 @@ int igs_render_image_blocked(igs_ctx* ctx, int width, int height, int k, float* 
 #undef LAUNCH
     IGS_LAUNCHED(ctx);
     igs_prof_end(ctx, IGS_PROF_BLOCKED, 0.0);
+    return IGS_OK;
+}
+
+int igs_render_image_blocked(igs_ctx* ctx, int width, int height, int k, float* out_rgb) {
+    int e = igs_blocked_render_rows(ctx, width, height, k, 0, height);
+    if (e) return e;
     if (out_rgb) {
-        IGS_CUDA(ctx, cudaMemcpyAsync(out_rgb, out, (size_t)width * height * 12, cudaMemcpyDeviceToHost, ctx->stream));
+        IGS_CUDA(ctx, cudaMemcpyAsync(out_rgb, ctx->image.p, (size_t)width * height * 12, cudaMemcpyDeviceToHost,
+                                      ctx->stream));
+        IGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    return IGS_OK;
+}
+
+int igs_render_image_blocked_rows(igs_ctx* ctx, int width, int height, int k, int row0, int row1, float* out_rgb) {
+    int e = igs_blocked_render_rows(ctx, width, height, k, row0, row1);
+    if (e) return e;
+    if (out_rgb && row1 > row0) {
+        IGS_CUDA(ctx, cudaMemcpyAsync(out_rgb, (const float*)ctx->image.p + (size_t)row0 * width * 3,
+                                      (size_t)width * (row1 - row0) * 12, cudaMemcpyDeviceToHost, ctx->stream));
         IGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     }
     return IGS_OK;

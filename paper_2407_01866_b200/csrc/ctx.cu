@@ -969,6 +969,30 @@ int igs_psnr(igs_ctx* ctx, const float* rendered, int width, int height, double*
     return igs_psnr_dev(ctx, dr, (const float*)ctx->target.p, (size_t)width * height * 3, out);
 }
 
+// ---- the fit driver's multi-rank pieces (fit.cpp) ------------------------------
+extern "C" void igs_internal_ranks(const igs_ctx* ctx, int* rank, int* nranks) {
+    *rank = ctx->rank;
+    *nranks = ctx->nranks;
+}
+
+// fit.cpp:34-37 render_current: build_partition(set, 64) + render_image_blocked
+// into the context's image.  With R ranks every rank renders its band of
+// ceil(H/R) rows and an in-place all-gather assembles the image on every
+// rank, so the metrics and the densification table that follow are computed
+// from the same image everywhere (replicated, identical bits).
+extern "C" int igs_internal_eval_render(igs_ctx* ctx, int W, int H, int k) {
+    int e;
+    if ((e = igs_partition_build(ctx, 64))) return e;
+    const int R = ctx->nranks;
+    if (R == 1 || !igs_has_comm(ctx)) return igs_blocked_render_rows(ctx, W, H, k, 0, H);
+    const int hb = (H + R - 1) / R;
+    const int r0 = std::min(H, ctx->rank * hb), r1 = std::min(H, r0 + hb);
+    if (!grow(ctx->image, (size_t)W * hb * R * 3 * sizeof(float)))
+        return igs_fail(ctx, IGS_E_CUDA, "out of device memory (image)");
+    if ((e = igs_blocked_render_rows(ctx, W, H, k, r0, r1))) return e;
+    return igs_comm_allgather(ctx, ctx->image.p, (size_t)W * hb * 3 * sizeof(float));
+}
+
 // ---- sampling tables (sampling.cpp:25-75) ----------------------------------------
 
 // device copy of an arbitrary float image (img == nullptr: the target)

@@ -32,6 +32,8 @@
 // ctx.cu: records the message returned by igs_last_error
 extern "C" int igs_internal_fail(igs_ctx* ctx, int code, const char* msg);
 extern "C" int igs_internal_set_sampler(igs_ctx* ctx, const double* prob, const uint32_t* alias, uint64_t n);
+extern "C" void igs_internal_ranks(const igs_ctx* ctx, int* rank, int* nranks);
+extern "C" int igs_internal_eval_render(igs_ctx* ctx, int W, int H, int k);
 extern "C" int igs_internal_train_iteration_async_raw(igs_ctx* ctx, const unsigned long long* raw2, uint32_t ns,
                                                       int k, const double* lr4, long long t);
 
@@ -248,6 +250,13 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
     if (c.lr[0] <= 0.0 || c.lr[1] <= 0.0 || c.lr[2] <= 0.0 || c.lr[3] <= 0.0 || c.lr_decay <= 0.0)
         return bad("rates must be positive");
     if (W < 1 || H < 1) return bad("image dimensions must be positive");
+    // multi-rank (a communicator attached): every rank runs this same driver
+    // with the same config and target; rank r trains on samples
+    // [r ns/R, (r+1) ns/R) of every iteration's draw, renders its band of the
+    // evaluation image, and all host-side decisions are replicated
+    int rank = 0, nranks = 1;
+    igs_internal_ranks(ctx, &rank, &nranks);
+    if (c.samples_per_iter % nranks) return bad("samples_per_iter must divide evenly over the ranks");
 
     int e;
     std::string text;
@@ -311,7 +320,8 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
     auto draw = [&](std::vector<unsigned long long>& s) {
         for (auto& v : s) v = rng.e();
     };
-    const uint32_t ns = (uint32_t)c.samples_per_iter;
+    const uint32_t ns = (uint32_t)(c.samples_per_iter / nranks);  // this rank's block
+    const size_t raw0 = 2 * (size_t)rank * ns;                      // its first raw output
     auto emit_checkpoint = [&](int iteration) -> int {
         const uint32_t n = igs_num_gaussians(ctx);
         char id[64];
@@ -326,11 +336,8 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
         return IGS_OK;
     };
     // fit.cpp:34-37 render_current: build_partition(set, 64) + render_image_blocked
-    auto render_current = [&]() -> int {
-        int ee = igs_partition_build(ctx, 64);
-        if (ee) return ee;
-        return igs_render_image_blocked(ctx, W, H, c.k, nullptr);
-    };
+    // (band per rank + all-gather when there are several)
+    auto render_current = [&]() -> int { return igs_internal_eval_render(ctx, W, H, c.k); };
 
     // drains an enqueued iteration after a failure, keeping the first error
     auto drain = [&](int code) {
@@ -342,7 +349,7 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
     // the host draws t+1's samples and enqueues it (unless t evaluates or
     // densifies, which needs the set after t), then waits on t.
     draw(cur);
-    if (c.iterations >= 1 && (e = igs_internal_train_iteration_async_raw(ctx, cur.data(), ns, c.k, lr, 1))) return e;
+    if (c.iterations >= 1 && (e = igs_internal_train_iteration_async_raw(ctx, cur.data() + raw0, ns, c.k, lr, 1))) return e;
     for (int iter = 1; iter <= c.iterations; ++iter) {
         const bool do_eval = iter % c.eval_interval == 0 || iter == c.iterations;
         const bool do_densify = stage < 4 && iter == c.warmup_iters + stage * c.densify_interval;
@@ -350,7 +357,7 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
         if (!do_eval && !do_densify) {
             if (iter < c.iterations) {
                 draw(next);  // overlaps the device step
-                if ((e = igs_internal_train_iteration_async_raw(ctx, next.data(), ns, c.k, lr, iter + 1)))
+                if ((e = igs_internal_train_iteration_async_raw(ctx, next.data() + raw0, ns, c.k, lr, iter + 1)))
                     return drain(e);  // t is still outstanding
             }
             if ((e = igs_train_wait(ctx, &loss))) return iter < c.iterations ? drain(e) : e;  // t+1 outstanding
@@ -404,7 +411,7 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
         if (iter < c.iterations) {
             draw(next);
             std::swap(cur, next);
-            if ((e = igs_internal_train_iteration_async_raw(ctx, cur.data(), ns, c.k, lr, iter + 1))) return e;
+            if ((e = igs_internal_train_iteration_async_raw(ctx, cur.data() + raw0, ns, c.k, lr, iter + 1))) return e;
         }
     }
     if ((e = emit_checkpoint(c.iterations))) return e;

@@ -467,6 +467,7 @@ int igs_prepare_all(igs_ctx* ctx, uint32_t first);
 int igs_raster_global(igs_ctx* ctx, int W, int H, int k, int row0, int row1, float* dev_out, uint32_t* dev_topk);
 int igs_topk_points(igs_ctx* ctx, const double* dev_uv, uint32_t npts, int k, uint32_t* dev_idx, double* dev_q);
 int igs_blocked_points_dev(igs_ctx* ctx, const double* duv, uint32_t npts, int kk, double* drgb);
+extern "C" int igs_blocked_render_rows(igs_ctx* ctx, int width, int height, int k, int row0, int row1);
 
 int igs_partition_free(igs_ctx* ctx);
 void igs_cull_free(igs_ctx* ctx);

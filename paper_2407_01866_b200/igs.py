@@ -138,6 +138,7 @@ SIGNATURES = {
     "igs_quantize_set": (C.c_int, [_vp]),
     "igs_locate_blocks": (C.c_int, [_vp, _dp, C.c_uint32, _i32p]),
     "igs_render_image_blocked": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _fp]),
+    "igs_render_image_blocked_rows": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _fp]),
     "igs_render_points_blocked": (C.c_int, [_vp, _dp, C.c_uint32, C.c_int, _dp]),
     "igs_get_prepared": (C.c_int, [_vp, _dp, C.c_uint32]),
     "igs_tile_lists": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _up, _u64p, _up, _up, _dp]),
@@ -486,6 +487,11 @@ class Context:
     def render_image_blocked(self, width: int, height: int, k: int = DEFAULT_K, host: bool = True):
         out = np.zeros((height, width, 3), np.float32) if host else None
         self._chk(self.lib.igs_render_image_blocked(self.h, width, height, k, _p(out, _fp)))
+        return out
+
+    def render_image_blocked_rows(self, width: int, height: int, k: int, row0: int, row1: int):
+        out = np.zeros((row1 - row0, width, 3), np.float32)
+        self._chk(self.lib.igs_render_image_blocked_rows(self.h, width, height, k, row0, row1, _p(out, _fp)))
         return out
 
     def render_points_blocked(self, uv, k: int = DEFAULT_K):

@@ -189,3 +189,28 @@ def test_sharded_moments_gather_and_densify(problem):
         assert losses == want_l
         assert np.array_equal(p, want_p)
         assert np.array_equal(m, want_m) and np.array_equal(v, want_v)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_fit_multirank_log_identical(world):
+    """SURVEY.md 8e eval/densify split: igs_fit on R ranks (each trains on its
+    sample block, renders its band of every evaluation image, all-gathers the
+    image; metrics, alias tables and appends replicated) writes the same
+    FitReport log and ends with the same set as one context -- and so as the
+    reference's fit() (test_gpu_fit)."""
+    cfg = dict(budget=400, k=10, iterations=300, samples_per_iter=4000, eval_interval=50, warmup_iters=60,
+               densify_interval=40, seed=5, plateau_patience=2)
+    target = synth.photo_like_image(96, 80, 31031)
+    with Context(0) as c:
+        want = c.fit(target, Context.fit_config(**cfg))
+        want_p = c.get_params()
+    ctxs = [Context(0) for _ in range(world)]
+    try:
+        Context.comm_init_loopback(ctxs)
+        res = run_ranks(ctxs, lambda r, c: (c.fit(target, Context.fit_config(**cfg)), c.get_params()))
+    finally:
+        for c in ctxs:
+            c.close()
+    for rep, p in res:
+        assert rep["log"] == want["log"]
+        assert np.array_equal(p, want_p)
