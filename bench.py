@@ -1,12 +1,23 @@
 #!/usr/bin/env python
-"""bench.py -- Image-GS train iteration on B200 (BASELINE.json configs[1]).
+"""bench.py -- Image-GS train iteration on B200 (BASELINE.json configs[1]; configs[3] at N > 1).
 
 One step = one training iteration of the reference's fit loop
 (fit.cpp:149-157): 10k sampled pixel centres, exact global top-K (K=10) over
 the whole set, normalised blend, L1 loss, analytic backward with the
-sample-ordered gradient reduction, Adam + constrain -- on a 2048x2048
-photo-like target with 100k Gaussians (the C2 budget) in the fit-start
-state (sigma = 2 px, theta = 0), the worst case for candidate culling.
+sample-ordered gradient reduction, Adam + constrain.
+
+* N = 1: C2, a 2048x2048 photo-like target with 100k Gaussians (the C2
+  budget) in the fit-start state (sigma = 2 px, theta = 0), the worst case
+  for candidate culling.
+* N > 1: C4, an 8192x8192 photo-like target with 1M random-local Gaussians
+  (BASELINE.json configs[3]: "training ... at 2/4/8 GPUs").  One process per
+  GPU (launched under torch.distributed.run; `--gpus N` without WORLD_SIZE
+  re-executes itself that way); the step's samples are split into
+  contiguous rank blocks, an NCCL all-gather completes the per-sample
+  contributions in sample order, every rank reduces, rank r updates its
+  1/N slice of the set (sharded Adam) and an all-gather of the parameters
+  follows -- strong scaling, bit-identical to one GPU.  Rank 0 also times
+  the same C4 step on one GPU first (`scaling_baseline`).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -14,11 +25,10 @@ state (sigma = 2 px, theta = 0), the worst case for candidate culling.
           time from CUDA events on the library's stream, L2 flushed (512 MiB
           memset) before every timed step; max over ranks.
 * e2e     the same iteration through the public C-ABI call
-          igs_train_iteration with HOST buffers: every step copies its 10k
-          sample indices host->device and reads the loss (+ status) back.
-* N > 1   one process per GPU (torchrun); the step's 10k samples are split
-          across ranks and the per-Gaussian gradients are summed with an NCCL
-          all-reduce before the (replicated) Adam step: strong scaling.
+          igs_train_iteration_async/igs_train_wait with HOST buffers: every
+          step copies its sample indices host->device and reads the loss
+          (+ status) back; device marks per step, with the host wall clock of
+          the whole loop beside it.
 * --impl reference times the reference's own OpenMP implementation
           (oracle/_ref: the unmodified reference library, all host threads) on
           the same workload; rank 0 only.
@@ -42,15 +52,45 @@ sys.path.insert(0, str(ROOT))
 
 BASE = json.loads((ROOT / "BASELINE.json").read_text())
 METRIC = BASE["metric"]
-W_IMG = H_IMG = 2048
-N_GAUSS = 100_000
 NS = 10_000
 K = 10
 LR = (2e-4, 2e-3, 1e-3, 1e-3)
 FLUSH_BYTES = 512 << 20
-WORKLOAD = ("C2 train iteration: 2048x2048 photo-like target, 100k Gaussians (fit-start state: sigma 2 px, "
-            "theta 0, uniform centres), 10k sampled pixels, exact global top-K K=10, L1 loss + backward "
-            "(sample-ordered reduction) + Adam/constrain")
+C2 = {"name": "C2", "W": 2048, "H": 2048, "N": 100_000,
+      "workload": ("C2 train iteration: 2048x2048 photo-like target, 100k Gaussians (fit-start state: sigma 2 px, "
+                   "theta 0, uniform centres), 10k sampled pixels, exact global top-K K=10, L1 loss + backward "
+                   "(sample-ordered reduction) + Adam/constrain")}
+C4 = {"name": "C4", "W": 8192, "H": 8192, "N": 1_000_000,
+      "workload": ("C4 train iteration: 8192x8192 photo-like target (2048^2 photo-like upsampled 4x), 1M "
+                   "random-local Gaussians (sigma 2-16 px), 10k sampled pixels, exact global top-K K=10, L1 loss + "
+                   "backward (sample-ordered reduction) + Adam/constrain")}
+
+
+def workload_for(world: int) -> dict:
+    return C2 if world == 1 else C4
+
+
+def make_inputs(wl: dict):
+    from paper_2407_01866_b200 import synth
+    if wl["name"] == "C2":
+        params = synth.init_set(wl["N"], wl["W"], wl["H"], seed=11)
+        target = synth.photo_like_image(wl["W"], wl["H"], 31001)
+    else:
+        params = synth.random_local_set(wl["N"], wl["W"], wl["H"], seed=7)
+        small = synth.photo_like_image(2048, 2048, 31004)
+        target = np.ascontiguousarray(small.repeat(4, axis=0).repeat(4, axis=1))
+    return params, target
+
+
+def bench_config(wl: dict, world: int) -> dict:
+    """The workload description both arms print (same keys and values)."""
+    return {"workload": wl["workload"], "image": f"{wl['W']}x{wl['H']}", "gaussians": wl["N"],
+            "samples_per_iter": NS, "k": K,
+            "parallelism": "single GPU" if world == 1 else
+            f"dp{world}: sample blocks per rank, NCCL all-gather of the per-sample contributions, "
+            "sample-ordered reduction, sharded Adam + parameter all-gather"}
+
+
 # FP64 pipe ops per evaluated (pixel, candidate) pair: 13 arithmetic ops of
 # mahalanobis_sq (renderer.cpp:17-23) + the threshold compare.
 OPS_PER_PAIR = 14
@@ -66,13 +106,6 @@ def parse():
     ap.add_argument("--no-render", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the C1/C3 secondary measurements")
     return ap.parse_args()
-
-
-def workload():
-    from paper_2407_01866_b200 import synth
-    params = synth.init_set(N_GAUSS, W_IMG, H_IMG, seed=11)
-    target = synth.photo_like_image(W_IMG, H_IMG, 31001)
-    return params, target
 
 
 class Clocks:
@@ -134,22 +167,44 @@ def physical_gpu(local_rank: int) -> int:
 
 
 # --------------------------------------------------------------------------- ours
+def device_steps(ctx, args, t0: int, reps: int) -> list:
+    """`reps` device-resident iterations t0.. each bracketed by CUDA events
+    after an L2 flush; per-step ms."""
+    step_ms = []
+    for s in range(reps):
+        ctx.flush_l2(FLUSH_BYTES)
+        ctx.timer_begin()
+        ctx.train_iterations(1, K, LR, t0 + s, want_losses=False)
+        step_ms.append(ctx.timer_end())
+    return step_ms
+
+
+def single_gpu_baseline(ctx_dev: int, args, wl: dict, params, target, samples) -> dict:
+    """The same step on one GPU (a context without a communicator): the
+    denominator of the N > 1 scaling efficiency, measured in this run."""
+    from paper_2407_01866_b200 import Context
+    with Context(ctx_dev) as c:
+        c.set_params(params)
+        c.set_target(target)
+        c.upload_samples(samples)
+        c.train_iterations(args.warmup, K, LR, 1, want_losses=False)
+        ms = device_steps(c, args, args.warmup + 1, args.steps)
+    return {"n_gpus": 1, "value": 1e3 * len(ms) / sum(ms), "unit": "iters/s", "ms_per_step": sum(ms) / len(ms),
+            "note": f"{wl['name']} on rank 0's GPU alone (no communicator), same steps, before the {wl['name']} "
+                    "multi-rank run"}
+
+
 def run_ours(args, rank, world, local_rank, dist):
     from paper_2407_01866_b200 import Context, synth
-    from paper_2407_01866_b200.igs import PROF_NAMES, PROF_SCAN, PROF_ADAM
-
-    params, target = workload()
-    total_steps = args.warmup + args.steps
-    samples = synth.sample_indices(NS, W_IMG, H_IMG, seed=99, steps=total_steps)
     from paper_2407_01866_b200 import dist as D
+    from paper_2407_01866_b200.igs import PROF_NAMES, PROF_SCAN
+
+    wl = workload_for(world)
+    W, H, N = wl["W"], wl["H"], wl["N"]
+    params, target = make_inputs(wl)
+    total_steps = args.warmup + args.steps
+    samples = synth.sample_indices(NS, W, H, seed=99, steps=total_steps)
     mine = D.shard(samples, rank, world)  # this rank's contiguous block of every step
-    ctx = Context(local_rank)
-    ctx.set_params(params)
-    ctx.set_target(target)
-    if world > 1:
-        uid = [Context.comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        ctx.comm_init(uid[0], world, rank)
 
     def barrier():
         if world > 1:
@@ -163,6 +218,19 @@ def run_ours(args, rank, world, local_rank, dist):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    baseline = None
+    if world > 1:
+        if rank == 0:
+            baseline = single_gpu_baseline(local_rank, args, wl, params, target, samples)
+        barrier()
+    ctx = Context(local_rank)
+    ctx.set_params(params)
+    ctx.set_target(target)
+    if world > 1:
+        uid = [Context.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.comm_init(uid[0], world, rank)
+
     fp64_peak = ctx.fp64_peak()
 
     # ---- device-resident value ------------------------------------------------
@@ -174,12 +242,7 @@ def run_ours(args, rank, world, local_rank, dist):
     ctx.sync()
     clocks.start()
     launches0 = ctx.kernel_launches
-    step_ms = []
-    for s in range(args.steps):
-        ctx.flush_l2(FLUSH_BYTES)
-        ctx.timer_begin()
-        ctx.train_iterations(1, K, LR, args.warmup + 1 + s, want_losses=False)
-        step_ms.append(ctx.timer_end())
+    step_ms = device_steps(ctx, args, args.warmup + 1, args.steps)
     ctx.sync()
     barrier()
     clk = clocks.stop()
@@ -205,11 +268,14 @@ def run_ours(args, rank, world, local_rank, dist):
     # drives it: every step copies its sample indices from pinned host memory
     # and reads its loss + status back.  Device marks bracket each step (after
     # its L2 flush, through its D2H read); the host enqueue of step s+1
-    # overlaps step s.
+    # overlaps step s.  The host wall clock of the whole loop (flushes
+    # included) is reported beside it.
     ctx.set_params(params)  # fresh state: moments zero, same trajectory start
     for s in range(args.warmup):
         ctx.train_iteration(mine[s], K, LR, s + 1)
     barrier()
+    ctx.sync()
+    wall0 = time.perf_counter()
     for s in range(args.steps):
         ctx.flush_l2(FLUSH_BYTES)
         ctx.timer_mark(2 * s)
@@ -218,10 +284,12 @@ def run_ours(args, rank, world, local_rank, dist):
         if s > 0:
             ctx.train_wait()
     ctx.train_wait()
+    wall = time.perf_counter() - wall0
     e2e_ms = [ctx.timer_between(2 * s, 2 * s + 1) for s in range(args.steps)]
     barrier()
     e2e_total = max_over_ranks(sum(e2e_ms))
     e2e_value = args.steps / (e2e_total / 1e3)
+    wall = max_over_ranks(wall)
 
     # ---- roofline of the dominant kernel family ----------------------------------
     fam_ms = {k: v[0] for k, v in prof.items()}
@@ -240,8 +308,8 @@ def run_ours(args, rank, world, local_rank, dist):
                 "avg_launch_us": scan_ms * 1e3 / max(scan_launches, 1),
                 # the fraction uses executed pairs; the reference's
                 # own work (its global scan) is NS x N pairs per iteration
-                "reference_equivalent_pairs_per_launch": float(NS) * N_GAUSS,
-                "reference_equivalent_gop_s": float(NS) * N_GAUSS * OPS_PER_PAIR / (
+                "reference_equivalent_pairs_per_launch": float(NS) * N / world,
+                "reference_equivalent_gop_s": float(NS) * N / world * OPS_PER_PAIR / (
                     scan_ms * 1e-3 / max(scan_launches, 1)) / 1e9}
     adam_ms, adam_launches, adam_bytes = prof["adam"]
     hbm = None
@@ -256,33 +324,35 @@ def run_ours(args, rank, world, local_rank, dist):
                      "unit": "GB/s", "frac": gbs / hbm, "traffic": ncu_traffic("segment_adam_kernel"),
                      "bytes_per_gaussian": 596}
 
-    # ---- secondary: full render Mpix/s (the eval render of the same set) ------------
+    # ---- secondary: full render Mpix/s (tile-row bands across ranks) ---------------
     render = None
     if not args.no_render:
-        ctx.render_image(W_IMG, H_IMG, K, host=False)
+        r0, r1 = D.row_band(H, rank, world)
+        ctx.render_image_rows(W, H, K, r0, r1, host=False)
         ctx.sync()
         rms = []
         for _ in range(3):
             ctx.flush_l2(FLUSH_BYTES)
+            barrier()
             ctx.timer_begin()
-            ctx.render_image(W_IMG, H_IMG, K, host=False)
+            ctx.render_image_rows(W, H, K, r0, r1, host=False)
             rms.append(ctx.timer_end())
         r_ms = max_over_ranks(min(rms))
         ctx.profile_enable(True)
-        ctx.render_image(W_IMG, H_IMG, K, host=False)
+        ctx.render_image_rows(W, H, K, r0, r1, host=False)
         ctx.sync()
         r_pairs = ctx.profile_read(PROF_SCAN)[2]
         ctx.profile_enable(False)
-        render = {"metric": "global top-K render Mpix/s (render_image, 2048x2048, 100k G, K=10)",
-                  "value": W_IMG * H_IMG / (r_ms * 1e-3) / 1e6, "unit": "Mpix/s", "ms": r_ms,
-                  "pairs_per_pixel": r_pairs / (W_IMG * H_IMG),
+        render = {"metric": f"global top-K render Mpix/s (render_image, {W}x{H}, {N // 1000}k G, K=10)",
+                  "value": W * H / (r_ms * 1e-3) / 1e6, "unit": "Mpix/s", "ms": r_ms,
+                  "pairs_per_pixel": r_pairs / max(r1 - r0, 1) / W,
                   "roofline": {"bound": "fp64", "achieved": r_pairs * OPS_PER_PAIR / (r_ms * 1e-3) / 1e9,
                                "peak": fp64_peak / 1e9, "unit": "Gop/s",
                                "frac": r_pairs * OPS_PER_PAIR / (r_ms * 1e-3) / fp64_peak,
-                               "work": "executed (pixel, candidate) pairs x 14 fp64 ops"},
+                               "work": "executed (pixel, candidate) pairs x 14 fp64 ops (rank 0's band)"},
                   "state": f"the set after {args.warmup + args.steps} training steps",
-                  "note": "L2 flushed before each render; every GPU renders the full image here "
-                          "(tile-row sharding: igs_render_image_rows)"}
+                  "note": f"L2 flushed before each render; {world} rank(s), each renders its tile-row band "
+                          "(igs_render_image_rows, no communication); time = max over ranks"}
     secondary = None
     if world == 1 and not args.no_secondary:
         secondary = {"c1": secondary_c1(ctx), "c3": secondary_c3(ctx), "c4": secondary_c4(ctx),
@@ -293,23 +363,28 @@ def run_ours(args, rank, world, local_rank, dist):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded mt19937_64 generators of the reference test suite)",
-        "config": {"workload": WORKLOAD, "image": f"{W_IMG}x{H_IMG}", "gaussians": N_GAUSS, "samples_per_iter": NS,
-                   "k": K, "parallelism": f"dp{world} (samples split across ranks, NCCL all-gather of the "
-                                          "per-sample contributions, replicated sample-ordered reduction + Adam)",
-                   "l2": "flushed before every timed step (512 MiB memset on the stream, outside the events)",
-                   "cull": ctx.get_option(1), "deterministic_reduction": ctx.get_option(2)},
+        "config": bench_config(wl, world),
+        "options": {"l2": "flushed before every timed step (512 MiB memset on the stream, outside the events)",
+                    "cull": ctx.get_option(1), "deterministic_reduction": ctx.get_option(2),
+                    "shard_adam": ctx.get_option(5)},
         "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": int(mine.shape[1]) * 4,
-                "d2h_bytes_per_step": 8 + 32,
-                "call": "igs_train_iteration_async + igs_train_wait, pipelined two deep (host sample indices in, "
-                        "host loss + status out every step)"},
+                "d2h_bytes_per_step": 8 + 32 + int(mine.shape[1]) * 8 * world,
+                "wall_clock_value": args.steps / wall,
+                "call": "igs_train_iteration_async + igs_train_wait, pipelined two deep (host sample indices in; "
+                        "host status, loss and the per-sample losses the host sums in sample order out, every "
+                        "step)",
+                "wall_clock_note": "host perf_counter over the whole loop, including the L2 flush memsets "
+                                   "between steps"},
         "roofline": roof, "roofline_adam": adam_roof,
         "profile_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
         "knn_hard_points_per_step": prof["knn_hard"][2] / args.steps,
-        "pairs_per_sample": prof["scan"][2] / args.steps / NS,
+        "pairs_per_sample": prof["scan"][2] / args.steps / max(NS // world, 1),
         "dominant_family": dom,
         "clocks": clk, "gpu_launches": int(launches),
         "render": render, "secondary": secondary,
     }
+    if baseline:
+        out["scaling_baseline"] = baseline
     return out, ctx
 
 
@@ -433,7 +508,7 @@ def secondary_fit(ctx):
     fit."""
     import time
     from paper_2407_01866_b200 import Context, synth
-    target = synth.photo_like_image(W_IMG, H_IMG, 31001)
+    target = synth.photo_like_image(C2["W"], C2["H"], 31001)
     ctx.fit(target, Context.fit_config(budget=100_000, iterations=200, eval_interval=1000, warmup_iters=100,
                                        densify_interval=50))
     cfg = Context.fit_config(budget=100_000, iterations=5000, eval_interval=500, warmup_iters=1000,
@@ -465,14 +540,15 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
-def run_reference_steps(steps: int, warmup: int, budget_s: float):
+def run_reference_steps(steps: int, warmup: int, budget_s: float, wl: dict = C2):
     """The unmodified reference (oracle/_ref) fit iteration on the same workload."""
     import oracle
     from paper_2407_01866_b200 import synth
     if not oracle.available("reference"):
         return None
     R = oracle.get("reference")
-    params, target = workload()
+    params, target = make_inputs(wl)
+    W_IMG, H_IMG = wl["W"], wl["H"]
     samples = synth.sample_indices(NS, W_IMG, H_IMG, seed=99, steps=max(steps + warmup, 1))
     import ctypes as C
     p = np.ascontiguousarray(params.copy())
@@ -513,8 +589,23 @@ def cpu_baseline_block(budget_s=20.0):
                       f"(oracle/_ref, OpenMP, {cpu_threads()} threads) after 1 warm-up, ~{budget_s:.0f} s budget"}
 
 
+def relaunch_under_torchrun(args) -> int:
+    """`--gpus N` without a launcher: one process per GPU under
+    torch.distributed.run (the driver's own launch line), same arguments."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -522,8 +613,9 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
+        wl = workload_for(world)
         steps = args.steps
-        times = run_reference_steps(steps, args.warmup, budget_s=150.0)
+        times = run_reference_steps(steps, args.warmup, budget_s=150.0, wl=wl)
         if times is None:
             print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libigs_ref.so not built"}))
             return 0
@@ -531,10 +623,12 @@ def main():
         out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": world,
                "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-               "data": "synthetic", "config": {"workload": WORKLOAD, "image": f"{W_IMG}x{H_IMG}",
-                                               "gaussians": N_GAUSS, "samples_per_iter": NS, "k": K},
+               "data": "synthetic (seeded mt19937_64 generators of the reference test suite)",
+               "config": bench_config(wl, world),
                "cpu_baseline": {"value": v, "unit": "iters/s", "cores": cpu_threads(), "kind": "reference",
-                                "sample": f"{len(times)} of {steps} requested full iterations (150 s cap)"},
+                                "sample": f"{len(times)} of {steps} requested full {wl['name']} iterations of the "
+                                          f"unmodified reference (oracle/_ref, OpenMP, {cpu_threads()} threads; "
+                                          "150 s cap)"},
                "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(out))
         return 0

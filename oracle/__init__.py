@@ -106,6 +106,8 @@ _PORT_ONLY = [
     ("alias_build", C.c_int, [_dp, C.c_size_t, _dp, _up]),
     ("cull_lists", C.c_uint64, [_dp, C.c_uint32, C.c_int, C.c_int, C.c_int, C.c_int, _up, _up, _dp]),
     ("prepare_scan", None, [_dp, C.c_uint32, _dp]),
+    ("train_contribs", C.c_int, [_dp, C.c_uint32, _fp, C.c_int, C.c_int, _up, C.c_uint32, C.c_int, C.c_double, _dp,
+                                 _up, _dp]),
 ]
 
 class RefFitConfig(C.Structure):
@@ -338,6 +340,21 @@ class Oracle:
                                         _ptr(sidx, _up), sidx.shape[0], k, C.byref(loss), _ptr(g, _dp)),
                   "train_step")
         return loss.value, g
+
+    def train_contribs(self, params, target, sample_idx, k, inv_n):
+        """(port) per-sample losses, slot keys (n = empty) and [ns][kk][8]
+        contributions of a sample block, upstream scaled by inv_n."""
+        params = np.ascontiguousarray(params, np.float64)
+        target = np.ascontiguousarray(target, np.float32)
+        sidx = np.ascontiguousarray(sample_idx, np.uint32)
+        H, W, _ = target.shape
+        kk = max(1, min(k, params.shape[0]))
+        ns = sidx.shape[0]
+        losses = np.zeros(ns); keys = np.zeros((ns, kk), np.uint32); contrib = np.zeros((ns, kk, 8))
+        self._chk(self._f("train_contribs")(_ptr(params, _dp), params.shape[0], _ptr(target, _fp), W, H,
+                                            _ptr(sidx, _up), ns, k, inv_n, _ptr(losses, _dp), _ptr(keys, _up),
+                                            _ptr(contrib, _dp)), "train_contribs")
+        return losses, keys, contrib
 
     def adam_step(self, params, grads, m, v, lr4, t):
         """In-place on copies; returns (params, m, v) or raises with .bad set."""

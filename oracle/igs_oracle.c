@@ -503,6 +503,39 @@ int orc_train_step(const double* p8, uint32_t n, const float* target, int W, int
     return ORC_OK;
 }
 
+/* The map half of train_step_gradients (fit.cpp:65-84) for a block of
+ * samples, with a caller-given 1/NS (the multi-rank decomposition: a rank
+ * owns a contiguous block of the iteration's samples): per-sample loss,
+ * and per slot (sample, entry) the Gaussian index (n for an empty slot) and
+ * the 8 gradient partials.  The ordered reduction is the caller's. */
+int orc_train_contribs(const double* p8, uint32_t n, const float* target, int W, int H, const uint32_t* sidx,
+                       uint32_t ns, int k, double inv_n, double* losses, uint32_t* keys, double* contrib) {
+    if (n == 0) return ORC_E_EMPTY_SET;
+    if (k < 1) return ORC_E_INVALID_PARAMETER;
+    prep_t* ps = prepare(p8, n);
+    const int kk = (int)((uint32_t)k < n ? (uint32_t)k : n);
+    entry_t* e = (entry_t*)malloc(sizeof(entry_t) * kk);
+    for (uint32_t i = 0; i < ns; ++i) {
+        const int h = (int)sidx[i] / W;
+        const int w = (int)sidx[i] % W;
+        const double x = (w + 0.5) / W, y = (h + 0.5) / H;
+        const float* t = target + ((size_t)h * W + w) * 3;
+        const int cnt = select_topk(ps, NULL, n, x, y, kk, e);
+        double c[3];
+        const double total = blend(ps, e, cnt, c);
+        const double dr = c[0] - (double)t[0], dg = c[1] - (double)t[1], db = c[2] - (double)t[2];
+        losses[i] = fabs(dr) + fabs(dg) + fabs(db);
+        const double up[3] = {sign_of(dr) * inv_n, sign_of(dg) * inv_n, sign_of(db) * inv_n};
+        double* d = contrib + (size_t)i * kk * 8;
+        memset(d, 0, sizeof(double) * 8 * kk);
+        sample_grads(ps, x, y, e, cnt, up, c, total, d);
+        for (int j = 0; j < kk; ++j) keys[(size_t)i * kk + j] = j < cnt ? e[j].idx : n;
+    }
+    free(e);
+    free(ps);
+    return ORC_OK;
+}
+
 /* ======================================================================= */
 /* Adam: adam.cpp:10-52                                                     */
 /* ======================================================================= */

@@ -76,6 +76,9 @@ int orc_render_topk(const double* p8, uint32_t n, const double* uv, uint32_t npt
 int orc_render_naive(const double* p8, uint32_t n, const double* uv, uint32_t npts, double* rgb);
 int orc_backward(const double* p8, uint32_t n, const double* samples5, uint32_t ns, int k, double* grads8);
 /* fit.cpp:51-106 train_step_gradients (+ the sign/loss logic). */
+/* fit.cpp:65-84 map half for a sample block with a given 1/NS (multi-rank) */
+int orc_train_contribs(const double* p8, uint32_t n, const float* target, int W, int H, const uint32_t* sidx,
+                       uint32_t ns, int k, double inv_n, double* losses, uint32_t* keys, double* contrib);
 int orc_train_step(const double* p8, uint32_t n, const float* target, int W, int H, const uint32_t* sample_idx,
                    uint32_t ns, int k, double* loss, double* grads8);
 

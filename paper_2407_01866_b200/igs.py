@@ -274,8 +274,8 @@ class Context:
         self._chk(self.lib.igs_render_image(self.h, width, height, k, _p(out, _fp), _p(topk, _up)))
         return (out, topk) if want_topk else out
 
-    def render_image_rows(self, width: int, height: int, k: int, row0: int, row1: int):
-        out = np.zeros((row1 - row0, width, 3), np.float32)
+    def render_image_rows(self, width: int, height: int, k: int, row0: int, row1: int, host: bool = True):
+        out = np.zeros((row1 - row0, width, 3), np.float32) if host else None
         self._chk(self.lib.igs_render_image_rows(self.h, width, height, k, row0, row1, _p(out, _fp)))
         return out
 
