@@ -279,6 +279,12 @@ int igs_fp64_peak(igs_ctx* ctx, double* ops_per_s);
 /* glibc-exact exp(x) and sincos(x) (csrc/glibc_math.cuh) evaluated on the
  * device: out3[3i..3i+2] = exp, sin, cos of x[i] (parity diagnostics). */
 int igs_libm_eval(igs_ctx* ctx, const double* x, uint32_t n, double* out3);
+/* The hand-written device primitives of kernel 2 on host arrays (tests):
+ * exclusive scan of n u32, and the stable LSD radix sort of (key, value)
+ * pairs by the low `bits` key bits. */
+int igs_debug_scan(igs_ctx* ctx, const uint32_t* in, uint32_t n, uint32_t* out);
+int igs_debug_sort_pairs(igs_ctx* ctx, const uint64_t* keys, const uint32_t* vals, uint32_t n, int bits,
+                         uint64_t* keys_out, uint32_t* vals_out);
 /* Per-kernel-family CUDA-event profiling of the launches the context issues. */
 #define IGS_PROF_SCAN 0    /* top-K candidate scans (raster, point/sample scans) */
 #define IGS_PROF_FINISH 1  /* per-sample blend + loss + contributions */

@@ -242,6 +242,7 @@ void igs_ctx_destroy(igs_ctx* ctx) {
     igs_cull_free(ctx);
     igs_knn_free(ctx);
     igs_comm_release(ctx);
+    igs_scan_free(ctx);
     cudaFree(ctx->params);
     cudaFree(ctx->grads);
     cudaFree(ctx->adam_m);

@@ -336,6 +336,7 @@ struct igs_ctx {
 #endif
     struct igs_loop_group* loop = nullptr;  // in-process loopback group (comm.cu)
     bool moments_local = false;  // sharded update: only this rank's slice of adam_m/adam_v is current
+    struct igs_scan_state* scan_st = nullptr;  // scan.cu: device scan look-back state
     int nranks = 1, rank = 0;
 };
 
@@ -349,6 +350,7 @@ inline bool igs_has_comm(const igs_ctx* ctx) {
 int igs_comm_allgather(igs_ctx* ctx, void* buf, size_t bytes);
 int igs_comm_allreduce_sum(igs_ctx* ctx, double* buf, size_t count);
 void igs_comm_release(igs_ctx* ctx);
+void igs_scan_free(igs_ctx* ctx);
 
 // helpers implemented in ctx.cu
 int igs_fail(igs_ctx* ctx, int code, const std::string& msg);

@@ -149,6 +149,8 @@ SIGNATURES = {
     "igs_flush_l2": (C.c_int, [_vp, C.c_size_t]),
     "igs_fp64_peak": (C.c_int, [_vp, _dp]),
     "igs_libm_eval": (C.c_int, [_vp, _dp, C.c_uint32, _dp]),
+    "igs_debug_scan": (C.c_int, [_vp, _up, C.c_uint32, _up]),
+    "igs_debug_sort_pairs": (C.c_int, [_vp, _u64p, _up, C.c_uint32, C.c_int, _u64p, _up]),
     "igs_bench_render": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_int), C.c_int, C.c_uint64, C.c_int, C.c_int,
                                    C.POINTER(BenchRow)]),
     "igs_profile_enable": (C.c_int, [_vp, C.c_int]),
@@ -546,6 +548,22 @@ class Context:
         rows = (BenchRow * (len(n_max_values) + 1))()
         self._chk(self.lib.igs_bench_render(self.h, pixels, nm, len(n_max_values), seed, trials, warmup, rows))
         return [{f: getattr(r, f) for f, _ in BenchRow._fields_} for r in rows]
+
+    def debug_scan(self, a):
+        """Device exclusive scan (kernel 2's primitive) of a u32 array."""
+        a = np.ascontiguousarray(a, np.uint32)
+        out = np.zeros_like(a)
+        self._chk(self.lib.igs_debug_scan(self.h, _p(a, _up), a.size, _p(out, _up)))
+        return out
+
+    def debug_sort_pairs(self, keys, vals, bits: int = 64):
+        """Device stable LSD radix sort of (u64 key, u32 value) pairs."""
+        keys = np.ascontiguousarray(keys, np.uint64)
+        vals = np.ascontiguousarray(vals, np.uint32)
+        ko, vo = np.zeros_like(keys), np.zeros_like(vals)
+        self._chk(self.lib.igs_debug_sort_pairs(self.h, _p(keys, _u64p), _p(vals, _up), keys.size, bits,
+                                                _p(ko, _u64p), _p(vo, _up)))
+        return ko, vo
 
     def libm_eval(self, x):
         """Device glibc-exact (exp, sin, cos) of each x (parity diagnostics)."""
