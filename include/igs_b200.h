@@ -212,6 +212,22 @@ int igs_partition_rebuild(igs_ctx* ctx, const double* rects4, uint32_t n_blocks)
 int igs_partition_info(igs_ctx* ctx, uint32_t* n_blocks, uint64_t* shell_total);
 int igs_partition_get(igs_ctx* ctx, double* blocks4, double* shells4, uint32_t* shell_offsets /* nb+1 */,
                       uint32_t* shell_members);
+/* The rest of a BspPartition (bsp.hpp:44-66), for handing the resident
+ * partition to the reference's own struct: n_max, source_size, and either
+ * the split tree (root, n_nodes; nodes as axis, low, high, block + lines) or
+ * the grid locator (grid_dim, cell CSR).  Block members: the builder's leaf
+ * lists (built) or locate_block of each centre (rebuilt), ascending. */
+int igs_partition_export(igs_ctx* ctx, int* n_max, uint32_t* source_size, int32_t* root, uint32_t* n_nodes,
+                         int* grid_dim, uint32_t* grid_total);
+int igs_partition_get_tree(igs_ctx* ctx, int32_t* nodes4, double* lines);
+int igs_partition_get_grid(igs_ctx* ctx, uint32_t* cell_offsets /* grid_dim^2 + 1 */, uint32_t* cell_blocks);
+int igs_partition_block_members(igs_ctx* ctx, uint32_t* offsets /* nb + 1 */, uint32_t* members);
+/* Installs a caller-held partition (e.g. an igs::BspPartition): blocks, and
+ * the split tree when n_nodes > 0 (else the grid locator is derived); shells
+ * and shell members are re-derived from the resident set; source_size is
+ * kept for the stale-partition check (bsp.cpp:278-282). */
+int igs_partition_set(igs_ctx* ctx, const double* blocks4, uint32_t n_blocks, const int32_t* nodes4,
+                      const double* lines, uint32_t n_nodes, int32_t root, int n_max, uint32_t source_size);
 /* locate_block at npts points. */
 int igs_locate_blocks(igs_ctx* ctx, const double* uv, uint32_t npts, int32_t* blocks);
 /* render_image_blocked (bsp.cpp:334) through the resident partition. */

@@ -6,15 +6,17 @@
 // build_partition / collect_shell_members, :178-218 grid locator +
 // rebuild_partition, :220-264 locate_block, :268-341 blocked renders.
 //
-// The split tree is built on the host (a deterministic restatement of the
-// recursive alternating-axis median; it needs only the centres, downloaded
-// once).  Everything per-pixel or per-(shell, Gaussian) runs on the device:
+// Everything runs on the device with the repo's own scan and radix sort
+// (scan.cu); the host only turns the per-level node records into the
+// reference's DFS numbering at the end:
+//   * tree build: a level-synchronous restatement of the recursive
+//     alternating-axis median split (build_tree_device below);
 //   * shell binning: shell_members[b] = {i : mu_i in shell_b (closed)}, in
-//     ascending i -- a CTA per shell scans the centres in index order with a
-//     block-wide ordered compaction (count pass, exclusive scan, fill pass).
-//     This is exactly the set collect_shell_members gathers through the tree
-//     (its bbox pruning only skips non-members), and exactly the rectangle
-//     test rebuild_partition runs (bsp.cpp:214-216).
+//     ascending i -- a uniform cell grid narrows each Gaussian's candidate
+//     shells, (shell, index) pairs are emitted in index order and stably
+//     radix-sorted by shell.  This is exactly the set collect_shell_members
+//     gathers through the tree (its bbox pruning only skips non-members), and
+//     exactly the rectangle test rebuild_partition runs (bsp.cpp:214-216).
 //   * locate: the tree descent (c < line ? low : high) or, for partitions
 //     rebuilt from corners, the grid locator with its first-containing /
 //     nearest-Chebyshev / scan-all fallbacks, op for op.
@@ -22,7 +24,6 @@
 //     one or two blocks -- the CTA loops over the distinct blocks present,
 //     staging each shell list through shared memory for the pixels of that
 //     block (scan order is index order, as the reference's member lists).
-#include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -31,6 +32,7 @@
 #include <vector>
 
 #include "igs_internal.cuh"
+#include "scan.cuh"
 
 using namespace igs_dev;
 
@@ -53,6 +55,9 @@ struct PartitionDev {
     int32_t root = -1;
     int grid_dim = 0;
     uint64_t shell_total = 0;
+    std::vector<uint32_t> grid_off_h, grid_blk_h;  // the grid locator's cells (rebuilt partitions)
+    std::vector<int32_t> leaf_block;               // built partitions: pool node -> block (leaves)
+    uint32_t* d_leaf_of = nullptr;                 // built partitions: every Gaussian's leaf (pool node)
     // device
     RectD* d_blocks = nullptr;
     RectD* d_shells = nullptr;
@@ -61,6 +66,10 @@ struct PartitionDev {
     uint32_t* d_grid_blk = nullptr;
     uint32_t* d_shell_off = nullptr;  // nb + 1
     uint32_t* d_shell_mem = nullptr;
+    // capacities (bytes) of the device arrays above: a replaced partition's
+    // arrays are kept for the next one (ctx->part_spare), so a rebuild at
+    // every evaluation allocates nothing
+    size_t cap[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 };
 
 namespace {
@@ -76,80 +85,6 @@ RectD shell_of(const RectD& b) {
     s.y2 = std::min(s.y2, 1.0);
     return s;
 }
-
-// bsp.cpp:27-118: recursive alternating-axis median split; leaves numbered
-// in DFS (low-first) order; the tie-aware split position keeps coincident
-// coordinates on one side.
-struct Builder {
-    const std::vector<double>& mx;
-    const std::vector<double>& my;
-    int n_max;
-    PartitionDev& out;
-
-    int32_t build(RectD rect, std::vector<uint32_t> m, int depth) {
-        const int32_t id = (int32_t)out.nodes.size();
-        out.nodes.push_back(NodeD{0, 0.0, -1, -1, -1});
-        if ((long long)m.size() <= (long long)n_max) {
-            out.nodes[id].block = (int32_t)out.blocks.size();
-            out.blocks.push_back(rect);
-            return id;
-        }
-        const int axis = depth % 2;
-        const std::vector<double>& c = axis == 0 ? mx : my;
-        std::sort(m.begin(), m.end(), [&](uint32_t a, uint32_t b) { return c[a] < c[b] || (c[a] == c[b] && a < b); });
-        const size_t n = m.size(), half = n / 2;
-        size_t pos = 0;
-        double line = 0.0;
-        bool forced = false;
-        if (c[m[half - 1]] < c[m[half]]) {
-            pos = half;
-        } else {
-            size_t lo = 0, hi = 0;
-            bool has_lo = false, has_hi = false;
-            for (size_t j = half; j-- > 1;)
-                if (c[m[j - 1]] < c[m[j]]) {
-                    lo = j;
-                    has_lo = true;
-                    break;
-                }
-            for (size_t j = half + 1; j < n; ++j)
-                if (c[m[j - 1]] < c[m[j]]) {
-                    hi = j;
-                    has_hi = true;
-                    break;
-                }
-            if (has_lo && (!has_hi || half - lo <= hi - half)) pos = lo;
-            else if (has_hi) pos = hi;
-            else forced = true;
-        }
-        if (forced) {
-            pos = half;
-            line = c[m[0]];
-        } else {
-            const double lo_c = c[m[pos - 1]], hi_c = c[m[pos]];
-            line = 0.5 * (lo_c + hi_c);
-            if (!(line > lo_c)) line = hi_c;
-        }
-        std::vector<uint32_t> lower(m.begin(), m.begin() + pos), upper(m.begin() + pos, m.end());
-        m.clear();
-        m.shrink_to_fit();
-        RectD lr = rect, hr = rect;
-        if (axis == 0) {
-            lr.x2 = line;
-            hr.x1 = line;
-        } else {
-            lr.y2 = line;
-            hr.y1 = line;
-        }
-        out.nodes[id].axis = axis;
-        out.nodes[id].line = line;
-        const int32_t l = build(lr, std::move(lower), depth + 1);
-        out.nodes[id].low = l;
-        const int32_t h = build(hr, std::move(upper), depth + 1);
-        out.nodes[id].high = h;
-        return id;
-    }
-};
 
 // --- device helpers ----------------------------------------------------------
 __device__ __forceinline__ bool contains_closed(const RectD& r, double x, double y) {
@@ -218,33 +153,45 @@ __device__ int locate(const LocView& v, double x, double y) {
     return best;
 }
 
-// Shell binning, CTA per shell: Gaussians in index order, block-wide ordered
-// compaction.  pass 0 counts, pass 1 writes at shell_off[b].
-__global__ void __launch_bounds__(256) shell_bin_kernel(const ScanRec* __restrict__ scan, uint32_t n,
-                                                        const RectD* __restrict__ shells, int pass,
-                                                        uint32_t* __restrict__ counts,
-                                                        const uint32_t* __restrict__ off, uint32_t* __restrict__ mem) {
-    __shared__ uint32_t warp_tot[8];
-    const uint32_t b = blockIdx.x;
-    const RectD s = shells[b];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t written = 0;
-    for (uint32_t base = 0; base < n; base += 256) {
-        const uint32_t i = base + threadIdx.x;
-        const bool in = i < n && contains_closed(s, scan[i].mu_x, scan[i].mu_y);
-        const unsigned m = __ballot_sync(0xffffffffu, in);
-        if (lane == 0) warp_tot[warp] = __popc(m);
-        __syncthreads();
-        uint32_t before = 0, total = 0;
-        for (int w = 0; w < 8; ++w) {
-            if (w < warp) before += warp_tot[w];
-            total += warp_tot[w];
+// Shell binning (kernel 2, count -> scan -> sort): shell_members[b] = {i :
+// mu_i in shell_b (closed)} in ascending i -- the set collect_shell_members
+// gathers through the tree (bsp.cpp:132-143, its bbox pruning only skips
+// non-members) and exactly rebuild_partition's rectangle test
+// (bsp.cpp:214-216).  A uniform grid of G x G cells lists the shells that
+// overlap each cell (a superset: floor(x G) is monotone in x); every
+// Gaussian tests only its cell's shells, counts its memberships, and after
+// an exclusive scan emits (shell, index) pairs in index order; a stable
+// radix sort by shell then leaves each shell's members ascending.
+__device__ __forceinline__ uint32_t grid_cell(double x, double y, int G) {
+    int cx = (int)floor(x * G), cy = (int)floor(y * G);
+    cx = cx < 0 ? 0 : (cx > G - 1 ? G - 1 : cx);
+    cy = cy < 0 ? 0 : (cy > G - 1 ? G - 1 : cy);
+    return (uint32_t)(cy * G + cx);
+}
+
+// pass 0: memberships per Gaussian into cnt[i]; pass 1: the (shell, i)
+// pairs at off[i], and a count per shell
+__global__ void shell_pairs_kernel(const ScanRec* __restrict__ scan, uint32_t n, const RectD* __restrict__ shells,
+                                   const uint32_t* __restrict__ cell_off, const uint32_t* __restrict__ cell_shell,
+                                   int G, int pass, uint32_t* __restrict__ cnt, const uint32_t* __restrict__ off,
+                                   unsigned long long* __restrict__ pair_key, uint32_t* __restrict__ pair_val,
+                                   uint32_t* __restrict__ shell_cnt) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double x = scan[i].mu_x, y = scan[i].mu_y;
+    const uint32_t c = grid_cell(x, y, G);
+    uint32_t k = 0, o = pass ? off[i] : 0u;
+    for (uint32_t j = cell_off[c]; j < cell_off[c + 1]; ++j) {
+        const uint32_t b = cell_shell[j];
+        if (!contains_closed(shells[b], x, y)) continue;
+        if (pass) {
+            pair_key[o + k] = b;
+            pair_val[o + k] = i;
+            atomicAdd(shell_cnt + b, 1u);
         }
-        if (pass == 1 && in) mem[off[b] + written + before + __popc(m & ((1u << lane) - 1))] = i;
-        written += total;
-        __syncthreads();
+        ++k;
     }
-    if (pass == 0 && threadIdx.x == 0) counts[b] = written;
+    if (!pass) cnt[i] = k;
 }
 
 __global__ void locate_kernel(LocView v, const double* __restrict__ uv, uint32_t npts, int32_t* __restrict__ out) {
@@ -347,15 +294,28 @@ __global__ void blocked_points_kernel(const ScanRec* __restrict__ scan, const Sh
     rgb[3 * (size_t)p + 2] = col[2];
 }
 
-template <typename T>
-T* to_dev(igs_ctx* ctx, const std::vector<T>& v) {
-    T* d = nullptr;
-    if (cudaMalloc(&d, std::max<size_t>(v.size(), 1) * sizeof(T)) != cudaSuccess) {
+// grow-only device array: ptr keeps at least `bytes` (capacity in cap)
+template <class T>
+bool reserve_dev(T*& ptr, size_t& cap, size_t bytes) {
+    bytes = std::max<size_t>(bytes, 16);
+    if (cap >= bytes) return true;
+    cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+    if (cudaMalloc(&ptr, bytes) != cudaSuccess) {
         cudaGetLastError();
-        return nullptr;
+        ptr = nullptr;
+        return false;
     }
-    if (!v.empty()) cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, ctx->stream);
-    return d;
+    cap = bytes;
+    return true;
+}
+
+template <class T>
+bool to_dev(igs_ctx* ctx, T*& ptr, size_t& cap, const std::vector<T>& v) {
+    if (!reserve_dev(ptr, cap, v.size() * sizeof(T))) return false;
+    if (!v.empty()) cudaMemcpyAsync(ptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, ctx->stream);
+    return true;
 }
 
 void free_dev(PartitionDev* p) {
@@ -366,6 +326,26 @@ void free_dev(PartitionDev* p) {
     cudaFree(p->d_grid_blk);
     cudaFree(p->d_shell_off);
     cudaFree(p->d_shell_mem);
+    cudaFree(p->d_leaf_of);
+}
+
+// a new partition, inheriting the device arrays of the last replaced one
+PartitionDev* new_partition(igs_ctx* ctx) {
+    auto* p = new PartitionDev();
+    if (PartitionDev* s = ctx->part_spare) {
+        p->d_blocks = s->d_blocks;
+        p->d_shells = s->d_shells;
+        p->d_nodes = s->d_nodes;
+        p->d_grid_off = s->d_grid_off;
+        p->d_grid_blk = s->d_grid_blk;
+        p->d_shell_off = s->d_shell_off;
+        p->d_shell_mem = s->d_shell_mem;
+        p->d_leaf_of = s->d_leaf_of;
+        std::copy(s->cap, s->cap + 8, p->cap);
+        delete s;
+        ctx->part_spare = nullptr;
+    }
+    return p;
 }
 
 LocView view_of(const PartitionDev* p) {
@@ -386,10 +366,9 @@ int finish_partition(igs_ctx* ctx, PartitionDev* p) {
     p->nb = (uint32_t)p->blocks.size();
     p->shells.resize(p->nb);
     for (uint32_t b = 0; b < p->nb; ++b) p->shells[b] = shell_of(p->blocks[b]);
-    p->d_blocks = to_dev(ctx, p->blocks);
-    p->d_shells = to_dev(ctx, p->shells);
-    p->d_nodes = to_dev(ctx, p->nodes);
-    if (!p->d_blocks || !p->d_shells || !p->d_nodes) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (bsp)");
+    if (!to_dev(ctx, p->d_blocks, p->cap[0], p->blocks) || !to_dev(ctx, p->d_shells, p->cap[1], p->shells) ||
+        !to_dev(ctx, p->d_nodes, p->cap[2], p->nodes))
+        return igs_fail(ctx, IGS_E_CUDA, "out of device memory (bsp)");
     if (!p->tree) {
         // bsp.cpp:178-195 build_grid_locator
         const int nb = (int)p->nb;
@@ -414,33 +393,62 @@ int finish_partition(igs_ctx* ctx, PartitionDev* p) {
             blk.insert(blk.end(), cells[c].begin(), cells[c].end());
         }
         off[cells.size()] = (uint32_t)blk.size();
-        p->d_grid_off = to_dev(ctx, off);
-        p->d_grid_blk = to_dev(ctx, blk);
-        if (!p->d_grid_off || !p->d_grid_blk) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (bsp)");
+        if (!to_dev(ctx, p->d_grid_off, p->cap[3], off) || !to_dev(ctx, p->d_grid_blk, p->cap[4], blk))
+            return igs_fail(ctx, IGS_E_CUDA, "out of device memory (bsp)");
+        p->grid_off_h = std::move(off);
+        p->grid_blk_h = std::move(blk);
     }
-    uint32_t* counts = (uint32_t*)igs_scratch(ctx, 25, (size_t)(p->nb + 1) * 4);
-    if (cudaMalloc(&p->d_shell_off, (size_t)(p->nb + 1) * 4) != cudaSuccess || !counts)
+    // shell -> cell lists on the host (a few thousand shells)
+    const uint32_t nb = p->nb, n = ctx->n;
+    const int G = std::max(1, (int)std::ceil(2.0 * std::sqrt((double)nb)));
+    std::vector<std::vector<uint32_t>> cl((size_t)G * G);
+    auto cidx = [&](double v) { return std::clamp((int)std::floor(v * G), 0, G - 1); };
+    for (uint32_t b = 0; b < nb; ++b) {
+        const RectD& r = p->shells[b];
+        for (int cy = cidx(r.y1); cy <= cidx(r.y2); ++cy)
+            for (int cx = cidx(r.x1); cx <= cidx(r.x2); ++cx) cl[(size_t)cy * G + cx].push_back(b);
+    }
+    std::vector<uint32_t> coff(cl.size() + 1), cshell;
+    for (size_t c = 0; c < cl.size(); ++c) {
+        coff[c] = (uint32_t)cshell.size();
+        cshell.insert(cshell.end(), cl[c].begin(), cl[c].end());
+    }
+    coff[cl.size()] = (uint32_t)cshell.size();
+    uint32_t* d_coff = (uint32_t*)igs_scratch(ctx, 25, coff.size() * 4);
+    uint32_t* d_cshell = (uint32_t*)igs_scratch(ctx, 26, std::max<size_t>(cshell.size(), 1) * 4);
+    uint32_t* cnt = (uint32_t*)igs_scratch(ctx, 29, ((size_t)n + 1) * 4);
+    if (!reserve_dev(p->d_shell_off, p->cap[5], (size_t)(nb + 1) * 4) || !d_coff || !d_cshell || !cnt)
         return igs_fail(ctx, IGS_E_CUDA, "out of device memory (bsp)");
     igs_prof_begin(ctx, IGS_PROF_BLOCKED);
-    IGS_CUDA(ctx, cudaMemsetAsync(counts, 0, (size_t)(p->nb + 1) * 4, ctx->stream));
-    shell_bin_kernel<<<p->nb, 256, 0, ctx->stream>>>(ctx->scan, ctx->n, p->d_shells, 0, counts, nullptr, nullptr);
+    IGS_CUDA(ctx, cudaMemcpyAsync(d_coff, coff.data(), coff.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    IGS_CUDA(ctx, cudaMemcpyAsync(d_cshell, cshell.data(), cshell.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    const unsigned tb = (n + 255) / 256;
+    shell_pairs_kernel<<<tb, 256, 0, ctx->stream>>>(ctx->scan, n, p->d_shells, d_coff, d_cshell, G, 0, cnt, nullptr,
+                                                     nullptr, nullptr, nullptr);
     IGS_LAUNCHED(ctx);
-    size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, counts, p->d_shell_off, (int)p->nb + 1, ctx->stream);
-    void* temp = igs_scratch(ctx, 26, tb);
-    if (!temp) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (bsp)");
-    IGS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(temp, tb, counts, p->d_shell_off, (int)p->nb + 1, ctx->stream));
-    ctx->launches += 2;
+    IGS_CUDA(ctx, cudaMemsetAsync(cnt + n, 0, 4, ctx->stream));
+    int e;
+    if ((e = igs_scan_excl_u32(ctx, cnt, cnt, (size_t)n + 1))) return e;  // cnt[n] = pair total
     uint32_t total = 0;
-    IGS_CUDA(ctx, cudaMemcpyAsync(&total, p->d_shell_off + p->nb, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    IGS_CUDA(ctx, cudaMemcpyAsync(&total, cnt + n, 4, cudaMemcpyDeviceToHost, ctx->stream));
     IGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     p->shell_total = total;
-    if (cudaMalloc(&p->d_shell_mem, std::max<size_t>(total, 1) * 4) != cudaSuccess)
+    if (!reserve_dev(p->d_shell_mem, p->cap[6], (size_t)total * 4))
         return igs_fail(ctx, IGS_E_CUDA, "out of device memory (bsp shells)");
-    shell_bin_kernel<<<p->nb, 256, 0, ctx->stream>>>(ctx->scan, ctx->n, p->d_shells, 1, nullptr, p->d_shell_off,
-                                                     p->d_shell_mem);
+    unsigned long long* pk = (unsigned long long*)igs_scratch(ctx, 30, std::max<size_t>(total, 1) * 8 * 3);
+    uint32_t* pv = (uint32_t*)igs_scratch(ctx, 31, std::max<size_t>(total, 1) * 4 * 2);
+    if (!pk || !pv) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (bsp shells)");
+    IGS_CUDA(ctx, cudaMemsetAsync(p->d_shell_off, 0, (size_t)(nb + 1) * 4, ctx->stream));
+    shell_pairs_kernel<<<tb, 256, 0, ctx->stream>>>(ctx->scan, n, p->d_shells, d_coff, d_cshell, G, 1, nullptr, cnt,
+                                                     pk, pv, p->d_shell_off);
     IGS_LAUNCHED(ctx);
-    igs_prof_end(ctx, IGS_PROF_BLOCKED, (double)ctx->n * p->nb);
+    if ((e = igs_scan_excl_u32(ctx, p->d_shell_off, p->d_shell_off, (size_t)nb + 1))) return e;
+    int bits = 1;
+    while (bits < 32 && (1ull << bits) < nb) ++bits;
+    if ((e = igs_radix_sort_u64_u32(ctx, pk, pv, pk + total, p->d_shell_mem, pk + 2 * (size_t)total, pv + total,
+                                    total, bits)))
+        return e;
+    igs_prof_end(ctx, IGS_PROF_BLOCKED, (double)total);
     return IGS_OK;
 }
 
@@ -453,25 +461,53 @@ int check_partition(igs_ctx* ctx) {
 }
 
 // --- device tree build (bsp.cpp:27-118 on the GPU) --------------------------
-// Level-synchronous restatement of Builder::build.  Once: every point's key
-// along x and along y, radix-sorted with the index as the stable tie-break
-// -- the (coord, idx) order the reference's comparator defines.  Per level:
-// a stable radix sort of that global order by the point's current node
-// yields every active node's members in (coord, idx) order as one
-// contiguous segment; one thread per node applies the tie-aware split rule
-// (pos, line); points move to their child.  The host (a few thousand nodes)
-// turns the level records into the reference's DFS numbering of nodes and
-// blocks and the block rectangles.
+// Level-synchronous restatement of Builder::build, device-resident.
+// Invariant: every active node of the current level owns one contiguous
+// segment [start, start + size) of BOTH ordX and ordY, and within it ordX is
+// sorted by (x, idx) and ordY by (y, idx) -- the reference comparator's
+// order along either axis.  Set up once by two stable radix sorts of the
+// coordinate keys (indices in order).  Per level (axis a = depth % 2):
+//   1. node flags -> exclusive scan = active index of every node;
+//   2. one thread per active node applies the tie-aware split rule
+//      (bsp.cpp:54-95) to its ord_a segment -> (pos, line), and writes its
+//      two children (sizes pos / size - pos, starts, rects) to the next level
+//      at positions 2 a, 2 a + 1 (Builder's low-then-high order);
+//   3. the low child is the ord_a segment's first pos points (ord_a needs no
+//      change); ord_b is stably partitioned inside each segment by side
+//      (a flag scan over all positions gives each point's rank on its side),
+//      so both invariants hold for the children.
+// Nothing comes back to the host per level: levels run in batches of eight
+// (a level past the last active one costs a few empty launches) and one
+// readback decides whether another batch is needed.  The host then numbers
+// nodes and blocks in DFS order from the downloaded per-level records.
 __device__ __forceinline__ unsigned long long coord_key(double v) {
     if (v == 0.0) v = 0.0;  // -0 and +0 compare equal in the reference
     const unsigned long long b = (unsigned long long)__double_as_longlong(v);
     return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
 }
 
+constexpr uint32_t kInact = 0xFFFFFFFFu;
+
+struct BuildNodes {  // the node pool, all levels (<= 2n - 1 nodes)
+    uint32_t* size;
+    uint32_t* start;
+    uint32_t* act;  // active index within its level, kInact for a leaf
+    uint32_t* pos;
+    double* line;
+    RectD* rect;
+};
+
 __global__ void gb_keys_kernel(const ScanRec* __restrict__ scan, uint32_t n, unsigned long long* __restrict__ kx,
                                unsigned long long* __restrict__ ky, uint32_t* __restrict__ iota,
-                               uint32_t* __restrict__ node_of) {
+                               uint32_t* __restrict__ node_of, BuildNodes P, uint32_t* __restrict__ lvl) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) {  // the root: level 0 = node 0
+        P.size[0] = n;
+        P.start[0] = 0;
+        P.rect[0] = RectD{0.0, 0.0, 1.0, 1.0};
+        lvl[0] = 0;  // base of level 0
+        lvl[1] = 1;  // its node count
+    }
     if (i >= n) return;
     kx[i] = coord_key(scan[i].mu_x);
     ky[i] = coord_key(scan[i].mu_y);
@@ -479,26 +515,48 @@ __global__ void gb_keys_kernel(const ScanRec* __restrict__ scan, uint32_t n, uns
     node_of[i] = 0;
 }
 
-// node key of the j-th point in the global (coord, idx) order
-__global__ void gb_gather_kernel(const uint32_t* __restrict__ ord, const uint32_t* __restrict__ node_of, uint32_t n,
-                                 uint32_t* __restrict__ key) {
+// lvl[2 d] = pool base of level d, lvl[2 d + 1] = its node count
+__global__ void gb_flag_kernel(BuildNodes P, const uint32_t* __restrict__ lvl, int d, uint32_t bound, int n_max,
+                               uint32_t* __restrict__ flag) {
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < n) key[j] = node_of[ord[j]];
+    if (j >= bound) return;
+    const uint32_t cnt = lvl[2 * d + 1];
+    flag[j] = j < cnt && (long long)P.size[lvl[2 * d] + j] > (long long)n_max ? 1u : 0u;
 }
 
 __device__ __forceinline__ double coord_of(const ScanRec* __restrict__ scan, uint32_t i, int axis) {
     return axis == 0 ? scan[i].mu_x : scan[i].mu_y;
 }
 
-// bsp.cpp:54-95 for active node k: members seg[start[k] .. start[k]+size[k])
-__global__ void gb_split_kernel(const ScanRec* __restrict__ scan, const uint32_t* __restrict__ seg,
-                                const uint32_t* __restrict__ start, const uint32_t* __restrict__ size, uint32_t na,
-                                int axis, uint32_t* __restrict__ pos_out, double* __restrict__ line_out) {
-    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= na) return;
-    const uint32_t* m = seg + start[k];
-    const size_t n = size[k], half = n / 2;
-    auto c = [&](size_t j) { return coord_of(scan, m[j], axis); };
+// bsp.cpp:54-95 on node j's ord_a segment; children to level d + 1
+__global__ void gb_split_kernel(const ScanRec* __restrict__ scan, const uint32_t* __restrict__ ord_a, BuildNodes P,
+                                uint32_t* __restrict__ lvl, int d, uint32_t bound, int n_max,
+                                const uint32_t* __restrict__ flag, const uint32_t* __restrict__ aidx) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t base = lvl[2 * d], cnt = lvl[2 * d + 1];
+    if (cnt == 0) {  // past the last level: keep the (empty) level records defined
+        if (j == 0) {
+            lvl[2 * d + 2] = base;
+            lvl[2 * d + 3] = 0;
+        }
+        return;
+    }
+    if (j >= cnt || j >= bound) return;
+    const uint32_t g = base + j;
+    if (j == cnt - 1) {  // the next level: 2 x (active nodes here)
+        lvl[2 * d + 2] = base + cnt;
+        lvl[2 * d + 3] = 2 * (aidx[j] + flag[j]);
+    }
+    if (!flag[j]) {
+        P.act[g] = kInact;
+        return;
+    }
+    const uint32_t a = aidx[j];
+    P.act[g] = a;
+    const int axis = d % 2;
+    const uint32_t* m = ord_a + P.start[g];
+    const size_t n = P.size[g], half = n / 2;
+    auto c = [&](size_t k) { return coord_of(scan, m[k], axis); };
     size_t pos = 0;
     double line = 0.0;
     bool forced = false;
@@ -507,15 +565,15 @@ __global__ void gb_split_kernel(const ScanRec* __restrict__ scan, const uint32_t
     } else {
         size_t lo = 0, hi = 0;
         bool has_lo = false, has_hi = false;
-        for (size_t j = half; j-- > 1;)
-            if (c(j - 1) < c(j)) {
-                lo = j;
+        for (size_t k = half; k-- > 1;)
+            if (c(k - 1) < c(k)) {
+                lo = k;
                 has_lo = true;
                 break;
             }
-        for (size_t j = half + 1; j < n; ++j)
-            if (c(j - 1) < c(j)) {
-                hi = j;
+        for (size_t k = half + 1; k < n; ++k)
+            if (c(k - 1) < c(k)) {
+                hi = k;
                 has_hi = true;
                 break;
             }
@@ -531,203 +589,220 @@ __global__ void gb_split_kernel(const ScanRec* __restrict__ scan, const uint32_t
         line = __dmul_rn(0.5, __dadd_rn(lo_c, hi_c));
         if (!(line > lo_c)) line = hi_c;
     }
-    pos_out[k] = (uint32_t)pos;
-    line_out[k] = line;
+    P.pos[g] = (uint32_t)pos;
+    P.line[g] = line;
+    const RectD r = P.rect[g];
+    RectD lr = r, hr = r;
+    if (axis == 0) {
+        lr.x2 = line;
+        hr.x1 = line;
+    } else {
+        lr.y2 = line;
+        hr.y1 = line;
+    }
+    const uint32_t c0 = base + cnt + 2 * a;
+    P.size[c0] = (uint32_t)pos;
+    P.start[c0] = P.start[g];
+    P.rect[c0] = lr;
+    P.size[c0 + 1] = (uint32_t)(n - pos);
+    P.start[c0 + 1] = P.start[g] + (uint32_t)pos;
+    P.rect[c0 + 1] = hr;
 }
 
-// Moves the points of active nodes to their children (next-level active
-// rank, or `inactive` once the child is a leaf).
-__global__ void gb_move_kernel(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ seg_node, uint32_t cnt,
-                               const uint32_t* __restrict__ start, const uint32_t* __restrict__ pos,
-                               const uint32_t* __restrict__ child, uint32_t* __restrict__ node_of) {
-    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= cnt) return;
-    const uint32_t k = seg_node[j];
-    node_of[seg[j]] = child[2 * k + (j - start[k] < pos[k] ? 0 : 1)];
+// side of every point of an active node (position in its ord_a segment)
+__global__ void gb_side_kernel(const uint32_t* __restrict__ ord_a, uint32_t n, BuildNodes P,
+                               const uint32_t* __restrict__ node_of, uint8_t* __restrict__ side) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t p = ord_a[i], g = node_of[p];
+    if (g == kInact || P.act[g] == kInact) return;
+    side[p] = i - P.start[g] < P.pos[g] ? 0 : 1;
 }
 
-struct GbLevelNode {
-    uint32_t size;
-    bool leaf;
-    uint32_t pos = 0;
-    double line = 0.0;
-    uint32_t low = 0, high = 0;  // indices into the next level
-    RectD rect;
-};
+// flag0[i] = the point at ord_b[i] goes to its node's low child
+__global__ void gb_lowflag_kernel(const uint32_t* __restrict__ ord_b, uint32_t n, BuildNodes P,
+                                  const uint32_t* __restrict__ node_of, const uint8_t* __restrict__ side,
+                                  uint32_t* __restrict__ flag0) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t p = ord_b[i], g = node_of[p];
+    flag0[i] = (g != kInact && P.act[g] != kInact && side[p] == 0) ? 1u : 0u;
+}
 
-// Builds p->nodes / p->blocks / p->root exactly like Builder on the device.
+// stable partition of ord_b inside each active segment; points move to
+// their child (or out of the build once their node is a leaf)
+__global__ void gb_scatter_kernel(const uint32_t* __restrict__ ord_b, uint32_t n, BuildNodes P,
+                                  uint32_t* __restrict__ node_of, const uint8_t* __restrict__ side,
+                                  const uint32_t* __restrict__ s0, const uint32_t* __restrict__ lvl, int d,
+                                  uint32_t* __restrict__ ord_b_out, uint32_t* __restrict__ leaf_of) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t p = ord_b[i], g = node_of[p];
+    if (g == kInact) {
+        ord_b_out[i] = p;
+        return;
+    }
+    const uint32_t a = P.act[g];
+    if (a == kInact) {  // its node is a leaf: the point stays put for good
+        ord_b_out[i] = p;
+        node_of[p] = kInact;
+        leaf_of[p] = g;  // the block members (Builder's leaf lists)
+        return;
+    }
+    const uint32_t start = P.start[g], pos = P.pos[g];
+    const uint32_t r0 = s0[i] - s0[start];  // low-side points before i in the segment
+    const uint32_t sd = side[p];
+    ord_b_out[sd == 0 ? start + r0 : start + pos + (i - start - r0)] = p;
+    node_of[p] = lvl[2 * d] + lvl[2 * d + 1] + 2 * a + sd;
+}
+
+// Builds p->nodes / p->blocks / p->root exactly like Builder, on the device.
 int build_tree_device(igs_ctx* ctx, PartitionDev* p, int n_max) {
     const uint32_t n = ctx->n;
-    const size_t tb_n = ((size_t)n + 255) / 256;
-    // scratch: kx, ky (u64); ordX, ordY, iota, node_of, key, key_sorted, seg (u32)
-    // (active nodes hold > n_max >= 1 points each: at most n / 2 of them)
-    uint32_t* s32 = (uint32_t*)igs_scratch(ctx, 29, ((size_t)n * 7 + 5 * ((size_t)n / 2 + 1)) * 4);
-    unsigned long long* s64 = (unsigned long long*)igs_scratch(ctx, 30, (size_t)n * 8 * 4);
-    if (!s32 || !s64) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (bsp build)");
-    unsigned long long *kx = s64, *ky = s64 + n, *ks = s64 + 2 * (size_t)n;
-    uint32_t *ordX = s32, *ordY = s32 + n, *iota = s32 + 2 * (size_t)n, *node_of = s32 + 3 * (size_t)n,
-             *key = s32 + 4 * (size_t)n, *key_sorted = s32 + 5 * (size_t)n, *seg = s32 + 6 * (size_t)n;
-    uint32_t* small = s32 + 7 * (size_t)n;  // per-level node arrays (start | size | pos | child...)
-    double* line_d = (double*)(s64 + 3 * (size_t)n);
-    gb_keys_kernel<<<(unsigned)tb_n, 256, 0, ctx->stream>>>(ctx->scan, n, kx, ky, iota, node_of);
+    const unsigned tb_n = (unsigned)(((size_t)n + 255) / 256);
+    const size_t pool = 2 * (size_t)n + 2;  // nodes of all levels
+    // scratch: kx, ky, key tmp (u64); ordX, ordY, ord tmp, iota, node_of, flags, scan (u32); side (u8)
+    unsigned long long* s64 = (unsigned long long*)igs_scratch(ctx, 30, (size_t)n * 8 * 3);
+    uint32_t* s32 = (uint32_t*)igs_scratch(ctx, 29, ((size_t)n * 7 + 4) * 4);
+    uint8_t* side = (uint8_t*)igs_scratch(ctx, 31, (size_t)n + 16);
+    // node pool: size, start, act, pos (u32) | line (f64) | rect (4 f64) | levels
+    char* np = (char*)igs_scratch(ctx, 45, pool * (4 * 4 + 8 + 32) + 64 * 1024);
+    if (!s64 || !s32 || !side || !np) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (bsp build)");
+    unsigned long long *kx = s64, *ky = s64 + n, *kt = s64 + 2 * (size_t)n;
+    uint32_t *ordX = s32, *ordY = s32 + n, *ordT = s32 + 2 * (size_t)n, *iota = s32 + 3 * (size_t)n,
+             *node_of = s32 + 4 * (size_t)n, *flag = s32 + 5 * (size_t)n, *scan_o = s32 + 6 * (size_t)n;
+    BuildNodes P;
+    P.size = (uint32_t*)np;
+    P.start = P.size + pool;
+    P.act = P.start + pool;
+    P.pos = P.act + pool;
+    P.line = (double*)(P.pos + pool);
+    P.rect = (RectD*)(P.line + pool);
+    uint32_t* lvl = (uint32_t*)(P.rect + pool);  // 2 words per level (<= 8192 levels)
+    const int kMaxLevels = 8192;
+    if (!reserve_dev(p->d_leaf_of, p->cap[7], (size_t)n * 4))
+        return igs_fail(ctx, IGS_E_CUDA, "out of device memory (bsp build)");
+    gb_keys_kernel<<<std::max(tb_n, 1u), 256, 0, ctx->stream>>>(ctx->scan, n, kx, ky, iota, node_of, P, lvl);
     IGS_LAUNCHED(ctx);
-    size_t tb = 0, tb2 = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, kx, ks, iota, ordX, (int)n, 0, 64, ctx->stream);
-    cub::DeviceRadixSort::SortPairs(nullptr, tb2, key, key_sorted, ordX, seg, (int)n, 0, 32, ctx->stream);
-    void* temp = igs_scratch(ctx, 31, std::max(tb, tb2));
-    if (!temp) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (bsp build)");
-    const size_t tcap = std::max(tb, tb2);
-    tb = tcap;
-    IGS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(temp, tb, kx, ks, iota, ordX, (int)n, 0, 64, ctx->stream));
-    tb = tcap;
-    IGS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(temp, tb, ky, ks, iota, ordY, (int)n, 0, 64, ctx->stream));
-    ctx->launches += 8;
-
-    std::vector<std::vector<GbLevelNode>> levels(1);
-    levels[0].push_back(GbLevelNode{n, (long long)n <= (long long)n_max, 0, 0.0, 0, 0, RectD{0.0, 0.0, 1.0, 1.0}});
-    for (int d = 0;; ++d) {
-        std::vector<GbLevelNode>& lv = levels[d];
-        // active nodes of this level in order, their starts
-        std::vector<uint32_t> act;
-        for (uint32_t k = 0; k < lv.size(); ++k)
-            if (!lv[k].leaf) act.push_back(k);
-        const uint32_t na = (uint32_t)act.size();
-        if (na == 0) break;
-        std::vector<uint32_t> hs(3 * (size_t)na);  // start | size | (pos)
-        uint32_t total = 0;
-        for (uint32_t a = 0; a < na; ++a) {
-            hs[a] = total;
-            hs[na + a] = lv[act[a]].size;
-            total += lv[act[a]].size;
+    int e;
+    // the (coord, idx) orders: stable sorts of the coordinate keys, indices in order
+    if ((e = igs_radix_sort_u64_u32(ctx, kx, iota, kx, ordX, kt, ordT, n, 64))) return e;
+    if ((e = igs_radix_sort_u64_u32(ctx, ky, iota, ky, ordY, kt, ordT, n, 64))) return e;
+    uint32_t* ord[2] = {ordX, ordY};
+    uint32_t* spare = ordT;
+    int d = 0;
+    for (;;) {
+        for (int batch = 0; batch < 8; ++batch, ++d) {
+            if (d + 1 >= kMaxLevels) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "partition deeper than 8192 levels");
+            const int axis = d % 2;
+            // a level has at most min(2^d, n) nodes
+            const uint32_t bound = d < 31 ? std::min<uint32_t>(1u << d, n) : n;
+            gb_flag_kernel<<<(bound + 255) / 256, 256, 0, ctx->stream>>>(P, lvl, d, bound, n_max, flag);
+            IGS_LAUNCHED(ctx);
+            if ((e = igs_scan_excl_u32(ctx, flag, scan_o, bound))) return e;
+            gb_split_kernel<<<(bound + 127) / 128, 128, 0, ctx->stream>>>(ctx->scan, ord[axis], P, lvl, d, bound,
+                                                                         n_max, flag, scan_o);
+            IGS_LAUNCHED(ctx);
+            gb_side_kernel<<<tb_n, 256, 0, ctx->stream>>>(ord[axis], n, P, node_of, side);
+            IGS_LAUNCHED(ctx);
+            uint32_t* ob = ord[axis ^ 1];
+            gb_lowflag_kernel<<<tb_n, 256, 0, ctx->stream>>>(ob, n, P, node_of, side, flag);
+            IGS_LAUNCHED(ctx);
+            if ((e = igs_scan_excl_u32(ctx, flag, scan_o, n))) return e;
+            gb_scatter_kernel<<<tb_n, 256, 0, ctx->stream>>>(ob, n, P, node_of, side, scan_o, lvl, d, spare,
+                                                             p->d_leaf_of);
+            IGS_LAUNCHED(ctx);
+            ord[axis ^ 1] = spare;
+            spare = ob;
         }
-        uint32_t *d_start = small, *d_size = small + na, *d_pos = small + 2 * (size_t)na,
-                 *d_child = small + 3 * (size_t)na;  // 2 na entries
-        IGS_CUDA(ctx, cudaMemcpyAsync(d_start, hs.data(), 2 * (size_t)na * 4, cudaMemcpyHostToDevice, ctx->stream));
-        const int axis = d % 2;
-        const uint32_t* ord = axis == 0 ? ordX : ordY;
-        // node key per point in the global order; inactive points sort last
-        gb_gather_kernel<<<(unsigned)tb_n, 256, 0, ctx->stream>>>(ord, node_of, n, key);
-        IGS_LAUNCHED(ctx);
-        int bits = 1;
-        while (bits < 32 && (1u << bits) <= na) ++bits;
-        tb = tcap;
-        IGS_CUDA(ctx, cub::DeviceRadixSort::SortPairs(temp, tb, key, key_sorted, ord, seg, (int)n, 0, bits,
-                                                      ctx->stream));
-        ctx->launches += 2 * ((bits + 7) / 8) + 1;
-        gb_split_kernel<<<(na + 127) / 128, 128, 0, ctx->stream>>>(ctx->scan, seg, d_start, d_size, na, axis, d_pos,
-                                                                  line_d);
-        IGS_LAUNCHED(ctx);
-        std::vector<double> hl(na);
-        IGS_CUDA(ctx, cudaMemcpyAsync(hs.data() + 2 * (size_t)na, d_pos, (size_t)na * 4, cudaMemcpyDeviceToHost,
-                                      ctx->stream));
-        IGS_CUDA(ctx, cudaMemcpyAsync(hl.data(), line_d, (size_t)na * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        uint32_t next = 0;
+        IGS_CUDA(ctx, cudaMemcpyAsync(&next, lvl + 2 * d + 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
         IGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-        // children (bsp.cpp:96-117): low = [0, pos), high = [pos, n)
-        levels.emplace_back();
-        std::vector<GbLevelNode>& nx = levels[d + 1];
-        std::vector<GbLevelNode>& cur = levels[d];  // (levels may have reallocated)
-        std::vector<uint32_t> child(2 * (size_t)na);
-        uint32_t next_active = 0;
-        for (uint32_t a = 0; a < na; ++a) {
-            GbLevelNode& nd = cur[act[a]];
-            nd.pos = hs[2 * (size_t)na + a];
-            nd.line = hl[a];
-            RectD lr = nd.rect, hr = nd.rect;
-            if (axis == 0) {
-                lr.x2 = nd.line;
-                hr.x1 = nd.line;
+        if (next == 0) break;
+    }
+    // levels 0 .. D-1 hold nodes (level d's count is 0 once d passed the last)
+    std::vector<uint32_t> hl(2 * (size_t)(d + 1));
+    IGS_CUDA(ctx, cudaMemcpy(hl.data(), lvl, hl.size() * 4, cudaMemcpyDeviceToHost));
+    int D = 0;
+    while (D <= d && hl[2 * D + 1] > 0) ++D;
+    const uint32_t total = hl[2 * (D - 1)] + hl[2 * (D - 1) + 1];
+    std::vector<uint32_t> hsize(total), hact(total), hpos(total);
+    std::vector<double> hline(total);
+    std::vector<RectD> hrect(total);
+    IGS_CUDA(ctx, cudaMemcpy(hsize.data(), P.size, total * 4, cudaMemcpyDeviceToHost));
+    IGS_CUDA(ctx, cudaMemcpy(hact.data(), P.act, total * 4, cudaMemcpyDeviceToHost));
+    IGS_CUDA(ctx, cudaMemcpy(hpos.data(), P.pos, total * 4, cudaMemcpyDeviceToHost));
+    IGS_CUDA(ctx, cudaMemcpy(hline.data(), P.line, total * 8, cudaMemcpyDeviceToHost));
+    IGS_CUDA(ctx, cudaMemcpy(hrect.data(), P.rect, total * sizeof(RectD), cudaMemcpyDeviceToHost));
+    // DFS numbering (bsp.cpp:32-118): preorder node ids, leaves in visit
+    // order.  Node j of level l with active index a has children 2a, 2a+1 of
+    // level l + 1.  Subtree node / leaf counts bottom-up, then ids top-down.
+    auto base = [&](int l) { return hl[2 * l]; };
+    auto count = [&](int l) { return hl[2 * l + 1]; };
+    std::vector<uint32_t> cnt(total), leaves(total);
+    for (int l = D - 1; l >= 0; --l)
+        for (uint32_t j = 0; j < count(l); ++j) {
+            const uint32_t g = base(l) + j;
+            if (hact[g] == kInact) {
+                cnt[g] = leaves[g] = 1;
             } else {
-                lr.y2 = nd.line;
-                hr.y1 = nd.line;
-            }
-            const uint32_t sz[2] = {nd.pos, nd.size - nd.pos};
-            const RectD rc[2] = {lr, hr};
-            for (int h = 0; h < 2; ++h) {
-                const bool leaf = (long long)sz[h] <= (long long)n_max;
-                (h == 0 ? nd.low : nd.high) = (uint32_t)nx.size();
-                child[2 * (size_t)a + h] = leaf ? 0xFFFFFFFFu : next_active++;
-                nx.push_back(GbLevelNode{sz[h], leaf, 0, 0.0, 0, 0, rc[h]});
+                const uint32_t c0 = base(l + 1) + 2 * hact[g];
+                cnt[g] = 1 + cnt[c0] + cnt[c0 + 1];
+                leaves[g] = leaves[c0] + leaves[c0 + 1];
             }
         }
-        IGS_CUDA(ctx, cudaMemcpyAsync(d_child, child.data(), child.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
-        gb_move_kernel<<<(total + 255) / 256, 256, 0, ctx->stream>>>(seg, key_sorted, total, d_start, d_pos, d_child,
-                                                                    node_of);
-        IGS_LAUNCHED(ctx);
-        // (the next level's host staging reuses `small`; order the copies)
-        IGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    }
-    // DFS numbering (bsp.cpp:32-118): preorder node ids, leaves in visit order
-    const int D = (int)levels.size();
-    std::vector<std::vector<uint32_t>> cnt(D), leaves(D);
-    for (int d = D - 1; d >= 0; --d) {
-        cnt[d].resize(levels[d].size());
-        leaves[d].resize(levels[d].size());
-        for (size_t k = 0; k < levels[d].size(); ++k) {
-            const GbLevelNode& nd = levels[d][k];
-            if (nd.leaf) {
-                cnt[d][k] = 1;
-                leaves[d][k] = 1;
-            } else {
-                cnt[d][k] = 1 + cnt[d + 1][nd.low] + cnt[d + 1][nd.high];
-                leaves[d][k] = leaves[d + 1][nd.low] + leaves[d + 1][nd.high];
-            }
-        }
-    }
-    p->nodes.assign(cnt[0][0], NodeD{0, 0.0, -1, -1, -1});
-    p->blocks.assign(leaves[0][0], RectD{});
-    std::vector<std::vector<int32_t>> id(D), boff(D);
-    for (int d = 0; d < D; ++d) {
-        id[d].resize(levels[d].size());
-        boff[d].resize(levels[d].size());
-    }
-    id[0][0] = 0;
-    boff[0][0] = 0;
-    for (int d = 0; d < D; ++d)
-        for (size_t k = 0; k < levels[d].size(); ++k) {
-            const GbLevelNode& nd = levels[d][k];
-            NodeD& out = p->nodes[id[d][k]];
-            if (nd.leaf) {
-                out.block = boff[d][k];
-                p->blocks[boff[d][k]] = nd.rect;
+    p->nodes.assign(cnt[0], NodeD{0, 0.0, -1, -1, -1});
+    p->blocks.assign(leaves[0], RectD{});
+    std::vector<int32_t> id(total), boff(total);
+    p->leaf_block.assign(total, -1);
+    id[0] = 0;
+    boff[0] = 0;
+    for (int l = 0; l < D; ++l)
+        for (uint32_t j = 0; j < count(l); ++j) {
+            const uint32_t g = base(l) + j;
+            NodeD& out = p->nodes[id[g]];
+            if (hact[g] == kInact) {
+                out.block = boff[g];
+                p->blocks[boff[g]] = hrect[g];
+                p->leaf_block[g] = boff[g];
                 continue;
             }
-            out.axis = d % 2;
-            out.line = nd.line;
-            id[d + 1][nd.low] = id[d][k] + 1;
-            id[d + 1][nd.high] = id[d][k] + 1 + (int32_t)cnt[d + 1][nd.low];
-            boff[d + 1][nd.low] = boff[d][k];
-            boff[d + 1][nd.high] = boff[d][k] + (int32_t)leaves[d + 1][nd.low];
-            out.low = id[d + 1][nd.low];
-            out.high = id[d + 1][nd.high];
+            const uint32_t c0 = base(l + 1) + 2 * hact[g];
+            out.axis = l % 2;
+            out.line = hline[g];
+            id[c0] = id[g] + 1;
+            id[c0 + 1] = id[g] + 1 + (int32_t)cnt[c0];
+            boff[c0] = boff[g];
+            boff[c0 + 1] = boff[g] + (int32_t)leaves[c0];
+            out.low = id[c0];
+            out.high = id[c0 + 1];
         }
     p->root = 0;
     return IGS_OK;
 }
 
-int download_centres(igs_ctx* ctx, std::vector<double>& mx, std::vector<double>& my) {
-    std::vector<double> p((size_t)ctx->n * 8);
-    if (ctx->n) {
-        IGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-        IGS_CUDA(ctx, cudaMemcpy(p.data(), ctx->params, p.size() * 8, cudaMemcpyDeviceToHost));
-    }
-    mx.resize(ctx->n);
-    my.resize(ctx->n);
-    for (uint32_t i = 0; i < ctx->n; ++i) {
-        mx[i] = p[(size_t)i * 8];
-        my[i] = p[(size_t)i * 8 + 1];
+}  // namespace
+
+// drops the resident partition; its device arrays are kept for the next one
+int igs_partition_free(igs_ctx* ctx) {
+    if (ctx->part) {
+        if (ctx->part_spare) {
+            free_dev(ctx->part_spare);
+            delete ctx->part_spare;
+        }
+        ctx->part_spare = ctx->part;
+        ctx->part = nullptr;
     }
     return IGS_OK;
 }
 
-}  // namespace
-
-int igs_partition_free(igs_ctx* ctx) {
-    if (ctx->part) {
-        free_dev(ctx->part);
-        delete ctx->part;
-        ctx->part = nullptr;
+void igs_partition_release(igs_ctx* ctx) {
+    igs_partition_free(ctx);
+    if (ctx->part_spare) {
+        free_dev(ctx->part_spare);
+        delete ctx->part_spare;
+        ctx->part_spare = nullptr;
     }
-    return IGS_OK;
 }
 
 extern "C" {
@@ -738,12 +813,13 @@ int igs_partition_build(igs_ctx* ctx, int n_max) {
     cudaSetDevice(ctx->device);
     if (ctx->n == 0) return igs_fail(ctx, IGS_E_EMPTY_SET, "build_partition requires a non-empty GaussianSet");
     if (n_max < 1) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "n_max must be >= 1");
-    auto* p = new PartitionDev();
+    auto* p = new_partition(ctx);
     p->tree = true;
     p->n_max = n_max;
     p->source_size = ctx->n;
     int e = build_tree_device(ctx, p, n_max);
     if (e) {
+        free_dev(p);
         delete p;
         return e;
     }
@@ -762,7 +838,7 @@ int igs_partition_rebuild(igs_ctx* ctx, const double* rects4, uint32_t n_blocks)
     cudaSetDevice(ctx->device);
     if (n_blocks == 0 || !rects4)
         return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "rebuild_partition requires at least one block");
-    auto* p = new PartitionDev();
+    auto* p = new_partition(ctx);
     p->tree = false;
     p->source_size = ctx->n;
     p->blocks.resize(n_blocks);
@@ -798,6 +874,122 @@ int igs_partition_get(igs_ctx* ctx, double* blocks4, double* shells4, uint32_t* 
     if (shell_members && p->shell_total)
         IGS_CUDA(ctx, cudaMemcpy(shell_members, p->d_shell_mem, p->shell_total * 4, cudaMemcpyDeviceToHost));
     return IGS_OK;
+}
+
+// ---- the whole BspPartition (bsp.hpp:44-66) for the C++ drop-in ----------------
+int igs_partition_export(igs_ctx* ctx, int* n_max, uint32_t* source_size, int32_t* root, uint32_t* n_nodes,
+                         int* grid_dim, uint32_t* grid_total) {
+    if (!ctx) return IGS_E_INVALID_PARAMETER;
+    if (!ctx->part) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "no partition");
+    const PartitionDev* p = ctx->part;
+    if (n_max) *n_max = p->n_max;
+    if (source_size) *source_size = p->source_size;
+    if (root) *root = p->tree ? p->root : -1;
+    if (n_nodes) *n_nodes = p->tree ? (uint32_t)p->nodes.size() : 0u;
+    if (grid_dim) *grid_dim = p->tree ? 0 : p->grid_dim;
+    if (grid_total) *grid_total = p->tree ? 0u : (uint32_t)p->grid_blk_h.size();
+    return IGS_OK;
+}
+
+int igs_partition_get_tree(igs_ctx* ctx, int32_t* nodes4, double* lines) {
+    if (!ctx) return IGS_E_INVALID_PARAMETER;
+    if (!ctx->part) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "no partition");
+    const PartitionDev* p = ctx->part;
+    if (!p->tree) return IGS_OK;
+    for (size_t i = 0; i < p->nodes.size(); ++i) {
+        const NodeD& nd = p->nodes[i];
+        if (nodes4) {
+            nodes4[4 * i] = nd.axis;
+            nodes4[4 * i + 1] = nd.low;
+            nodes4[4 * i + 2] = nd.high;
+            nodes4[4 * i + 3] = nd.block;
+        }
+        if (lines) lines[i] = nd.line;
+    }
+    return IGS_OK;
+}
+
+int igs_partition_get_grid(igs_ctx* ctx, uint32_t* cell_offsets, uint32_t* cell_blocks) {
+    if (!ctx) return IGS_E_INVALID_PARAMETER;
+    if (!ctx->part) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "no partition");
+    const PartitionDev* p = ctx->part;
+    if (p->tree) return IGS_OK;
+    if (cell_offsets) std::memcpy(cell_offsets, p->grid_off_h.data(), p->grid_off_h.size() * 4);
+    if (cell_blocks && !p->grid_blk_h.empty())
+        std::memcpy(cell_blocks, p->grid_blk_h.data(), p->grid_blk_h.size() * 4);
+    return IGS_OK;
+}
+
+// block_members: the split's leaf lists for a built partition (bsp.cpp:32-40),
+// locate_block of every resident centre for a rebuilt one (bsp.cpp:208-211);
+// ascending within each block
+int igs_partition_block_members(igs_ctx* ctx, uint32_t* offsets, uint32_t* members) {
+    if (!ctx) return IGS_E_INVALID_PARAMETER;
+    cudaSetDevice(ctx->device);
+    if (!ctx->part) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "no partition");
+    PartitionDev* p = ctx->part;
+    const uint32_t n = p->source_size;
+    std::vector<int32_t> blk(n);
+    if (p->tree && !p->leaf_block.empty() && p->d_leaf_of) {
+        std::vector<uint32_t> leaf(n);
+        IGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        if (n) IGS_CUDA(ctx, cudaMemcpy(leaf.data(), p->d_leaf_of, (size_t)n * 4, cudaMemcpyDeviceToHost));
+        for (uint32_t i = 0; i < n; ++i) blk[i] = p->leaf_block[leaf[i]];
+    } else {
+        if (n != ctx->n) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "stale partition: Gaussian count changed since construction");
+        std::vector<double> uv((size_t)n * 2);
+        std::vector<double> scan6((size_t)n * 6);
+        int e;
+        if ((e = igs_get_prepared(ctx, scan6.data(), n))) return e;
+        for (uint32_t i = 0; i < n; ++i) {
+            uv[2 * (size_t)i] = scan6[6 * (size_t)i];
+            uv[2 * (size_t)i + 1] = scan6[6 * (size_t)i + 1];
+        }
+        if ((e = igs_locate_blocks(ctx, uv.data(), n, blk.data()))) return e;
+    }
+    std::vector<uint32_t> off(p->nb + 1, 0);
+    for (uint32_t i = 0; i < n; ++i) ++off[blk[i] + 1];
+    for (uint32_t b = 0; b < p->nb; ++b) off[b + 1] += off[b];
+    if (offsets) std::memcpy(offsets, off.data(), off.size() * 4);
+    if (members) {
+        std::vector<uint32_t> cur(off.begin(), off.end() - 1);
+        for (uint32_t i = 0; i < n; ++i) members[cur[blk[i]]++] = i;
+    }
+    return IGS_OK;
+}
+
+// installs a caller-held partition (a BspPartition from the reference or from
+// igs_partition_export): blocks + the split tree (n_nodes > 0) or, without a
+// tree, the grid locator; shells and shell members are re-derived from the
+// resident set (the rectangle test both builders apply)
+int igs_partition_set(igs_ctx* ctx, const double* blocks4, uint32_t n_blocks, const int32_t* nodes4,
+                      const double* lines, uint32_t n_nodes, int32_t root, int n_max, uint32_t source_size) {
+    if (!ctx) return IGS_E_INVALID_PARAMETER;
+    cudaSetDevice(ctx->device);
+    if (n_blocks == 0 || !blocks4) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "partition has no blocks");
+    if (n_nodes && (!nodes4 || !lines || root < 0 || (uint32_t)root >= n_nodes))
+        return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "bad partition tree");
+    for (uint32_t i = 0; i < n_nodes; ++i) {
+        const int32_t lo = nodes4[4 * i + 1], hi = nodes4[4 * i + 2], b = nodes4[4 * i + 3];
+        const bool leaf_ok = b >= 0 && (uint32_t)b < n_blocks;
+        const bool inner_ok = b < 0 && lo >= 0 && hi >= 0 && (uint32_t)lo < n_nodes && (uint32_t)hi < n_nodes;
+        if (!leaf_ok && !inner_ok) return igs_fail(ctx, IGS_E_INVALID_PARAMETER, "bad partition tree");
+    }
+    auto* p = new_partition(ctx);
+    p->tree = n_nodes > 0;
+    p->n_max = n_max;
+    p->source_size = source_size;
+    p->blocks.resize(n_blocks);
+    std::memcpy(p->blocks.data(), blocks4, sizeof(RectD) * n_blocks);
+    p->nodes.resize(n_nodes);
+    for (uint32_t i = 0; i < n_nodes; ++i)
+        p->nodes[i] = NodeD{nodes4[4 * i], lines[i], nodes4[4 * i + 1], nodes4[4 * i + 2], nodes4[4 * i + 3]};
+    p->root = p->tree ? root : -1;
+    igs_partition_free(ctx);
+    ctx->part = p;
+    const int e = finish_partition(ctx, p);
+    if (e) igs_partition_free(ctx);
+    return e;
 }
 
 int igs_locate_blocks(igs_ctx* ctx, const double* uv, uint32_t npts, int32_t* blocks) {

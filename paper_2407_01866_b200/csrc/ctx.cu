@@ -238,7 +238,7 @@ void igs_ctx_destroy(igs_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    igs_partition_free(ctx);
+    igs_partition_release(ctx);
     igs_cull_free(ctx);
     igs_knn_free(ctx);
     igs_comm_release(ctx);

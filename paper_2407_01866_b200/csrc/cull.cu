@@ -21,14 +21,15 @@
 // whose list exceeded the buffer capacity is detected by its consumer, which
 // then scans all N candidates for that tile (exact, just slower); the host
 // grows the buffer for the next build.  See cull_math.cuh for the proof.
-#include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 #include <vector>
 
 #include "cull_math.cuh"
 #include "igs_internal.cuh"
+#include "scan.cuh"
 
 using namespace igs_dev;
 using igs_cull::G;
@@ -470,17 +471,13 @@ int build_lists(igs_ctx* ctx, int W, int H, int pts_cells, int kk) {
     IGS_CUDA(ctx, cudaMemsetAsync(bin_cnt, 0, (size_t)ntiles * 4, ctx->stream));
     bin_count_kernel<<<(n + 255) / 256, 256, 0, ctx->stream>>>(ctx->scan, n, gr, bin_cnt, (uint32_t*)b.bin_of.p);
     IGS_LAUNCHED(ctx);
-    size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, bin_cnt, bin_off, ntiles, ctx->stream);
-    if (!grow(b.cub_tmp, tb)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (scan)");
-    IGS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(b.cub_tmp.p, tb, bin_cnt, bin_off, ntiles, ctx->stream));
-    ctx->launches += 2;
+    int e;
+    if ((e = igs_scan_excl_u32(ctx, bin_cnt, bin_off, (size_t)ntiles))) return e;
     IGS_CUDA(ctx, cudaMemsetAsync(tile_cnt, 0, (size_t)ntiles * 8, ctx->stream));  // reuse as bin cursors
     bin_fill_kernel<<<(n + 255) / 256, 256, 0, ctx->stream>>>(n, (const uint32_t*)b.bin_of.p, bin_off, tile_cnt,
                                                               (uint32_t*)b.bins.p);
     IGS_LAUNCHED(ctx);
     // 2. tau per tile
-    int e;
     if (kk <= 4) e = launch_tau<4>(ctx, gr, kk, b);
     else if (kk <= 8) e = launch_tau<8>(ctx, gr, kk, b);
     else if (kk <= 16) e = launch_tau<16>(ctx, gr, kk, b);
@@ -497,8 +494,7 @@ int build_lists(igs_ctx* ctx, int W, int H, int pts_cells, int kk) {
     emit_count_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(ctx->scan, n, gr, (const unsigned long long*)b.tau.p,
                                                                 tile_cnt);
     IGS_LAUNCHED(ctx);
-    IGS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(b.cub_tmp.p, tb, tile_cnt, tile_off, ntiles, ctx->stream));
-    ctx->launches += 2;
+    if ((e = igs_scan_excl_u32(ctx, tile_cnt, tile_off, (size_t)ntiles))) return e;
     emit_fill_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(ctx->scan, n, gr, (const unsigned long long*)b.tau.p,
                                                                tile_off, tile_cur, (uint32_t*)b.list.p, b.cap);
     IGS_LAUNCHED(ctx);

@@ -310,6 +310,7 @@ struct igs_ctx {
     uint32_t samples_ns = 0, samples_steps = 0;
 
     PartitionDev* part = nullptr;
+    PartitionDev* part_spare = nullptr;  // a replaced partition's device arrays, reused by the next
     void* cull = nullptr;            // CullBufs (cull.cu)
     void* knn = nullptr;             // KnnBufs (knn.cu)
     uint64_t params_version = 0;     // bumped on every change of the set
@@ -472,6 +473,7 @@ int igs_blocked_points_dev(igs_ctx* ctx, const double* duv, uint32_t npts, int k
 extern "C" int igs_blocked_render_rows(igs_ctx* ctx, int width, int height, int k, int row0, int row1);
 
 int igs_partition_free(igs_ctx* ctx);
+void igs_partition_release(igs_ctx* ctx);
 void igs_cull_free(igs_ctx* ctx);
 void igs_knn_free(igs_ctx* ctx);
 int igs_topk_knn(igs_ctx* ctx, const double* uv, uint32_t npts, int k, uint32_t* oi, double* oq);

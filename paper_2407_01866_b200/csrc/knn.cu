@@ -31,7 +31,6 @@
 // inserted in lane order into a top-K replicated in every lane, so the kept
 // set is exactly the kk smallest (q, idx) -- the reference's selection.
 // A frontier larger than the per-warp queue restarts over all N (exact).
-#include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -41,6 +40,7 @@
 #include "igs_internal.cuh"
 #include "knn_tree.cuh"
 #include "reduce.cuh"
+#include "scan.cuh"
 
 using namespace igs_dev;
 
@@ -145,12 +145,6 @@ __global__ void __launch_bounds__(kBuildThreads) lq_build_kernel(
     uint32_t* __restrict__ cur, uint32_t* __restrict__ off, uint32_t* __restrict__ key, uint32_t* __restrict__ mem,
     ScanRec* __restrict__ mrec, uint32_t* __restrict__ minv, Acc* __restrict__ acc, uint32_t* __restrict__ lcount,
     unsigned* __restrict__ bar) {
-    using BlockScan = cub::BlockScan<uint32_t, kBuildThreads>;
-    using BlockReduce = cub::BlockReduce<uint32_t, kBuildThreads>;
-    __shared__ union {
-        typename BlockScan::TempStorage scan;
-        typename BlockReduce::TempStorage red;
-    } tmp;
     __shared__ uint32_t s_base;
     uint32_t* chunk_sum = bar + 2;
     pdl_wait();
@@ -191,14 +185,16 @@ __global__ void __launch_bounds__(kBuildThreads) lq_build_kernel(
             if (c < c1) total += __ldcg(cnt + c);
         }
     {
-        const uint32_t agg = BlockReduce(tmp.red).Sum(total);
+        uint32_t agg;
+        block_excl_sum<kBuildThreads>(total, &agg);
         if (threadIdx.x == 0) chunk_sum[blockIdx.x] = agg;
     }
     igs_grid_sync(bar, 3 * G);
     uint32_t mine = 0;
     for (uint32_t b = threadIdx.x; b < blockIdx.x; b += kBuildThreads) mine += __ldcg(chunk_sum + b);
     {
-        const uint32_t base = BlockReduce(tmp.red).Sum(mine);
+        uint32_t base;
+        block_excl_sum<kBuildThreads>(mine, &base);
         if (threadIdx.x == 0) s_base = base;
     }
     __syncthreads();
@@ -211,9 +207,8 @@ __global__ void __launch_bounds__(kBuildThreads) lq_build_kernel(
             v[j] = c < c1 ? __ldcg(cnt + c) : 0u;
             sum += v[j];
         }
-        uint32_t excl, agg;
-        BlockScan(tmp.scan).ExclusiveSum(sum, excl, agg);
-        __syncthreads();
+        uint32_t agg;
+        const uint32_t excl = block_excl_sum<kBuildThreads>(sum, &agg);
         uint32_t o = run + excl;
 #pragma unroll
         for (int j = 0; j < kBuildPer; ++j) {
@@ -1711,11 +1706,8 @@ int knn_build(igs_ctx* ctx) {
         IGS_PDL(ctx, lq_clear, 2 * ctx->sm_count, 256, 0, cells, cnt, (Acc*)b.acc.p, (uint32_t*)b.lcount.p);
         IGS_PDL(ctx, lq_count, (n + 255) / 256, 256, 0, (const ScanRec*)ctx->scan, n, L, cnt, (uint32_t*)b.key.p,
                 (uint32_t*)b.lcount.p);
-        size_t tb = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, (int)cells, ctx->stream);
-        if (!grow(b.cub_tmp, tb)) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn scan)");
-        IGS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(b.cub_tmp.p, tb, cnt, off, (int)cells, ctx->stream));
-        ctx->launches += 2;
+        const int es = igs_scan_excl_u32(ctx, cnt, off, (size_t)cells);
+        if (es) return es;
         IGS_PDL(ctx, lq_fill, (n + 255) / 256, 256, 0, (const ScanRec*)ctx->scan, n, (const uint32_t*)b.key.p,
                 (const uint32_t*)off, cur, (uint32_t*)b.mem.p, (ScanRec*)b.mrec.p, (uint32_t*)b.minv.p,
                 (Acc*)b.acc.p);

@@ -3,9 +3,8 @@
 // hard-point scan + offsets launch (knn.cu).
 #pragma once
 
-#include <cub/cub.cuh>
-
 #include "igs_internal.cuh"
+#include "scan.cuh"
 
 namespace igs_dev {
 
@@ -24,8 +23,6 @@ constexpr int kOffPer = 4;  // counts per thread and chunk pass
 // targets start at bar_base (arrivals already counted by the caller); the
 // last CTA out resets the counters for the next launch.
 __device__ __forceinline__ void offsets_scatter_body(const OffArgs& A, unsigned bar_base) {
-    using BlockScan = cub::BlockScan<uint32_t, kOffThreads>;
-    __shared__ typename BlockScan::TempStorage tmp;
     __shared__ uint32_t s_base;
     const uint32_t* __restrict__ gcnt = A.gcnt;
     const uint32_t n = A.n;
@@ -55,9 +52,8 @@ __device__ __forceinline__ void offsets_scatter_body(const OffArgs& A, unsigned 
         total += v;
     }
     {
-        using BlockReduce = cub::BlockReduce<uint32_t, kOffThreads>;
-        __shared__ typename BlockReduce::TempStorage rtmp;
-        const uint32_t agg = BlockReduce(rtmp).Sum(total);
+        uint32_t agg;
+        block_excl_sum<kOffThreads>(total, &agg);
         if (threadIdx.x == 0) chunk_sum[blockIdx.x] = agg;
     }
     igs_grid_sync(A.bar, bar_base + G);
@@ -65,9 +61,8 @@ __device__ __forceinline__ void offsets_scatter_body(const OffArgs& A, unsigned 
     uint32_t mine = 0;
     for (uint32_t b = threadIdx.x; b < blockIdx.x; b += kOffThreads) mine += *(volatile uint32_t*)(chunk_sum + b);
     {
-        using BlockReduce = cub::BlockReduce<uint32_t, kOffThreads>;
-        __shared__ typename BlockReduce::TempStorage rtmp2;
-        const uint32_t base = BlockReduce(rtmp2).Sum(mine);
+        uint32_t base;
+        block_excl_sum<kOffThreads>(mine, &base);
         if (threadIdx.x == 0) s_base = base;
     }
     __syncthreads();
@@ -81,9 +76,8 @@ __device__ __forceinline__ void offsets_scatter_body(const OffArgs& A, unsigned 
             v[j] = i < c1 ? gcnt[i] : 0u;
             sum += v[j];
         }
-        uint32_t excl, agg;
-        BlockScan(tmp).ExclusiveSum(sum, excl, agg);
-        __syncthreads();  // tmp reused next pass
+        uint32_t agg;
+        const uint32_t excl = block_excl_sum<kOffThreads>(sum, &agg);
         uint32_t o = run + excl;
 #pragma unroll
         for (int j = 0; j < kOffPer; ++j) {

@@ -20,7 +20,6 @@
 // Gaussian), long ones by long_segment_kernel (a CTA each).  Fast mode
 // accumulates with fp64 atomics instead (order-nondeterministic, ~1e-16
 // relative).
-#include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -29,6 +28,7 @@
 #include "igs_internal.cuh"
 #include "knn_tree.cuh"
 #include "reduce.cuh"
+#include "scan.cuh"
 
 using namespace igs_dev;
 
@@ -996,7 +996,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
         // the reduction's offsets + scatter too (hard_offsets_kernel)
         ctx->fuse_off.ready = false;
         ctx->fuse_off.done = false;
-        if (ctx->opt_deterministic && !exch && !getenv("IGS_CUB_SCAN")) {
+        if (ctx->opt_deterministic && !exch && !getenv("IGS_SCAN_LAUNCHES")) {
             uint32_t* ctl = off_ctl(ctx);
             if (!ctl) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (scan)");
             ctx->fuse_off.args = OffArgs{(const uint32_t*)gcnt, n, goff, ctl + 2, (const uint32_t*)keys, (uint32_t)items,
@@ -1065,7 +1065,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
         }
         if (ctx->fuse_off.done) {
             // done by the search's hard_offsets_kernel
-        } else if (!getenv("IGS_CUB_SCAN")) {
+        } else if (!getenv("IGS_SCAN_LAUNCHES")) {
             // offsets + scatter in one persistent launch (two grid barriers)
             uint32_t* ctl = off_ctl(ctx);
             if (!ctl) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (scan)");
@@ -1073,12 +1073,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
                       long_ctl, long_ctl + 1, (unsigned*)ctl};
             IGS_PDL_COOP(ctx, offsets_scatter_kernel, (unsigned)ctx->sm_count, kOffThreads, 0, A);
         } else {
-            size_t tb = 0;
-            cub::DeviceScan::ExclusiveSum(nullptr, tb, gcnt, goff, (int)n, ctx->stream);
-            void* temp = igs_scratch(ctx, 8, tb);
-            if (!temp) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (scan)");
-            IGS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(temp, tb, gcnt, goff, (int)n, ctx->stream));
-            ctx->launches += 2;
+            if ((e = igs_scan_excl_u32(ctx, gcnt, goff, (size_t)n))) return e;
             IGS_PDL(ctx, scatter_slots_kernel, (unsigned)((items + 255) / 256), 256, 0, (const uint32_t*)keys,
                     (uint32_t)items, n, (const uint32_t*)goff, (const uint32_t*)gcnt, gcnt + n, perm, long_ctl,
                     long_ctl + 1);

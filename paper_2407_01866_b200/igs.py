@@ -137,6 +137,11 @@ SIGNATURES = {
     "igs_decode": (C.c_int, [_vp, _u8p, C.c_size_t, _up, _up, C.POINTER(C.c_int), _up]),
     "igs_quantize_set": (C.c_int, [_vp]),
     "igs_locate_blocks": (C.c_int, [_vp, _dp, C.c_uint32, _i32p]),
+    "igs_partition_export": (C.c_int, [_vp, C.POINTER(C.c_int), _up, _i32p, _up, C.POINTER(C.c_int), _up]),
+    "igs_partition_get_tree": (C.c_int, [_vp, _i32p, _dp]),
+    "igs_partition_get_grid": (C.c_int, [_vp, _up, _up]),
+    "igs_partition_block_members": (C.c_int, [_vp, _up, _up]),
+    "igs_partition_set": (C.c_int, [_vp, _dp, C.c_uint32, _i32p, _dp, C.c_uint32, C.c_int32, C.c_int, C.c_uint32]),
     "igs_render_image_blocked": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _fp]),
     "igs_render_image_blocked_rows": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _fp]),
     "igs_render_points_blocked": (C.c_int, [_vp, _dp, C.c_uint32, C.c_int, _dp]),
@@ -479,6 +484,32 @@ class Context:
 
     def quantize_set(self):
         self._chk(self.lib.igs_quantize_set(self.h))
+
+    def partition_block_members(self):
+        nb, _ = self.partition_info()
+        off = np.zeros(nb + 1, np.uint32)
+        self._chk(self.lib.igs_partition_block_members(self.h, _p(off, _up), None))
+        mem = np.zeros(max(int(off[-1]), 1), np.uint32)
+        self._chk(self.lib.igs_partition_block_members(self.h, _p(off, _up), _p(mem, _up)))
+        return off, mem[:int(off[-1])]
+
+    def partition_tree(self):
+        """(root, nodes [n x 4: axis, low, high, block], lines) of a built partition."""
+        n_max = C.c_int(0); src = C.c_uint32(0); root = C.c_int32(0); nn = C.c_uint32(0)
+        gd = C.c_int(0); gt = C.c_uint32(0)
+        self._chk(self.lib.igs_partition_export(self.h, C.byref(n_max), C.byref(src), C.byref(root), C.byref(nn),
+                                                C.byref(gd), C.byref(gt)))
+        nodes = np.zeros((max(nn.value, 1), 4), np.int32); lines = np.zeros(max(nn.value, 1))
+        self._chk(self.lib.igs_partition_get_tree(self.h, _p(nodes, _i32p), _p(lines, _dp)))
+        return root.value, nodes[:nn.value], lines[:nn.value]
+
+    def partition_set(self, blocks, nodes=None, lines=None, root=-1, n_max=0, source_size=None):
+        b = _f64(blocks, 4)
+        nn = 0 if nodes is None else len(nodes)
+        nd = None if nodes is None else np.ascontiguousarray(nodes, np.int32)
+        ln = None if lines is None else np.ascontiguousarray(lines, np.float64)
+        self._chk(self.lib.igs_partition_set(self.h, _p(b, _dp), b.shape[0], _p(nd, _i32p), _p(ln, _dp), nn, root,
+                                             n_max, self.n if source_size is None else source_size))
 
     def locate_blocks(self, uv):
         uv = _f64(uv, 2)
