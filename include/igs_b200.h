@@ -166,6 +166,15 @@ int igs_image_gradient_magnitude(igs_ctx* ctx, const float* img, int width, int 
  * is zero.  img nullable = the target; p = H*W doubles. */
 int igs_gradient_mixture(igs_ctx* ctx, const float* img, int width, int height, double lambda, double* p);
 
+/* initialize_set(img, count, lambda, rng) (sampling.cpp:154-174): count
+ * Gaussians at init_distribution draws (pixel centres, the pixel's colour,
+ * s = 2/max(W,H), theta = 0).  raw2: the 2*count raw mt19937_64 outputs the
+ * reference's draws consume (next_index, then next_double, per Gaussian),
+ * taken from the caller's Rng (Rng::next_u64) -- so the caller's engine
+ * advances exactly as the reference's would.  out8: count records. */
+int igs_initialize_set(igs_ctx* ctx, const float* img, int width, int height, int count, double lambda,
+                       const uint64_t* raw2, double* out8);
+
 /* ssim(rendered, target) (metrics.cpp:33-112); rendered nullable = last image. */
 int igs_ssim(igs_ctx* ctx, const float* rendered, int width, int height, double* out);
 

@@ -213,6 +213,31 @@ struct Fail {
 
 extern "C" {
 
+// sampling.cpp:154-174 initialize_set(img, count, lambda, rng): the init
+// distribution (device Sobel, the Kahan total and mixture here), the Vose
+// table, and `count` draws that consume raw2[2j] (next_index) and
+// raw2[2j + 1] (next_double) -- the caller's engine outputs, in order.
+int igs_initialize_set(igs_ctx* ctx, const float* img, int W, int H, int count, double lambda,
+                       const uint64_t* raw2, double* out8) {
+    if (!ctx || !img || (count > 0 && (!raw2 || !out8))) return IGS_E_INVALID_PARAMETER;
+    if (count < 1) return igs_internal_fail(ctx, IGS_E_INVALID_PARAMETER, "initialization count must be >= 1");
+    std::vector<double> p((size_t)W * H);
+    int e;
+    if ((e = igs_gradient_mixture(ctx, img, W, H, lambda, p.data()))) return e;
+    const Alias table(p);
+    if (!table.ok) return igs_internal_fail(ctx, IGS_E_INVALID_PARAMETER, "alias table weights must have positive sum");
+    std::vector<double> set;
+    set.reserve((size_t)count * 8);
+    const double s0 = 2.0 / std::max(W, H);
+    for (int j = 0; j < count; ++j) {
+        const size_t i = (size_t)(raw2[2 * (size_t)j] % table.prob.size());
+        const double coin = (double)(raw2[2 * (size_t)j + 1] >> 11) * 0x1.0p-53;
+        add_gaussian(set, img, W, H, coin < table.prob[i] ? (uint32_t)i : table.alias[i], s0);
+    }
+    std::memcpy(out8, set.data(), set.size() * sizeof(double));
+    return IGS_OK;
+}
+
 void igs_fit_config_default(igs_fit_config* c) {
     c->budget = 0;
     c->k = 10;

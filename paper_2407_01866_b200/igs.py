@@ -165,6 +165,7 @@ SIGNATURES = {
     "igs_ssim": (C.c_int, [_vp, _fp, C.c_int, C.c_int, _dp]),
     "igs_image_gradient_magnitude": (C.c_int, [_vp, _fp, C.c_int, C.c_int, _dp]),
     "igs_gradient_mixture": (C.c_int, [_vp, _fp, C.c_int, C.c_int, C.c_double, _dp]),
+    "igs_initialize_set": (C.c_int, [_vp, _fp, C.c_int, C.c_int, C.c_int, C.c_double, _u64p, _dp]),
     "igs_fit_config_default": (None, [C.POINTER(FitConfig)]),
     "igs_fit": (C.c_int, [_vp, _fp, C.c_int, C.c_int, C.POINTER(FitConfig), CHECKPOINT_FN, C.c_void_p,
                           C.POINTER(EvalRecord), C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
@@ -396,6 +397,15 @@ class Context:
         H, W = img.shape[:2]
         out = np.zeros((H, W))
         self._chk(self.lib.igs_gradient_mixture(self.h, _p(img, _fp), W, H, lam, _p(out, _dp)))
+        return out
+
+    def initialize_set(self, img, count: int, lam: float, raw2):
+        """initialize_set (sampling.cpp:154-174) drawing from 2*count raw engine outputs."""
+        img = np.ascontiguousarray(img, np.float32)
+        H, W = img.shape[:2]
+        raw2 = np.ascontiguousarray(raw2, np.uint64)
+        out = np.zeros((count, 8))
+        self._chk(self.lib.igs_initialize_set(self.h, _p(img, _fp), W, H, count, lam, _p(raw2, _u64p), _p(out, _dp)))
         return out
 
     def train_iteration_async(self, sample_idx, k: int = DEFAULT_K, lr=DEFAULT_LR, t: int = 1):
