@@ -17,21 +17,6 @@ constexpr int kSortRounds = 4;                          // 1024 items per tile
 constexpr uint32_t kSortTile = kSortThreads * kSortRounds;
 constexpr int kRadix = 256;
 
-// tile status word: epoch (30 bits) | flag (2 bits: 1 aggregate, 2 prefix) | value (32 bits)
-__device__ __forceinline__ unsigned long long pack_status(uint32_t epoch, uint32_t flag, uint32_t v) {
-    return ((unsigned long long)epoch << 34) | ((unsigned long long)flag << 32) | v;
-}
-
-__device__ __forceinline__ void store_release(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-__device__ __forceinline__ unsigned long long load_acquire(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
 // One pass; tiles claimed in order from ctl[0]; ctl[1] counts finished
 // tiles (the last one re-arms both for the next call on the stream).
 __global__ void __launch_bounds__(kScanThreads) scan_lookback_kernel(const uint32_t* in, uint32_t* out, size_t n,
@@ -51,24 +36,9 @@ __global__ void __launch_bounds__(kScanThreads) scan_lookback_kernel(const uint3
     }
     uint32_t agg;
     const uint32_t excl = block_excl_sum<kScanThreads>(local, &agg);
-    if (threadIdx.x == 0) {
-        uint32_t prefix = 0;
-        if (tile == 0) {
-            store_release(status, pack_status(epoch, 2, agg));
-        } else {
-            store_release(status + tile, pack_status(epoch, 1, agg));
-            for (int p = (int)tile - 1; p >= 0;) {
-                const unsigned long long s = load_acquire(status + p);
-                if ((uint32_t)(s >> 34) != epoch) continue;  // not yet published this call
-                const uint32_t flag = (uint32_t)(s >> 32) & 3u;
-                if (flag == 0) continue;
-                prefix += (uint32_t)s;
-                if (flag == 2) break;
-                --p;
-            }
-            store_release(status + tile, pack_status(epoch, 2, prefix + agg));
-        }
-        s_prefix = prefix;
+    if (threadIdx.x < 32) {
+        const uint32_t pre = tile_lookback(status, tile, agg, epoch);
+        if (threadIdx.x == 0) s_prefix = pre;
     }
     __syncthreads();
     uint32_t run = s_prefix + excl;

@@ -49,6 +49,52 @@ __device__ __forceinline__ uint32_t block_excl_sum(uint32_t v, uint32_t* total) 
     return base + x - v;
 }
 
+// Decoupled look-back for tile `tile` of a single-pass scan, run by one
+// whole warp (all 32 lanes call it; all get the result): publishes the
+// tile's aggregate, then reads 32 predecessors at once -- lane j the tile
+// j + 1 back -- waits until each is published, adds them up to the nearest
+// one that carries an inclusive prefix (or all 32 and moves on), publishes
+// the tile's inclusive prefix and returns the exclusive one.  Status words
+// carry an epoch (one per launch) so they never need clearing.  Tiles must
+// be claimed in order (a ticket) so a tile only waits on running tiles.
+__device__ __forceinline__ uint32_t tile_lookback(unsigned long long* status, uint32_t tile, uint32_t agg,
+                                                  uint32_t epoch) {
+    const int lane = threadIdx.x & 31;
+    auto pack = [&](uint32_t flag, uint32_t v) {
+        return ((unsigned long long)epoch << 34) | ((unsigned long long)flag << 32) | v;
+    };
+    auto st = [](unsigned long long* p, unsigned long long v) {
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    };
+    if (tile == 0) {
+        if (lane == 0) st(status, pack(2, agg));
+        return 0;
+    }
+    if (lane == 0) st(status + tile, pack(1, agg));
+    uint32_t prefix = 0;
+    for (int p = (int)tile - 1;; p -= 32) {
+        const int idx = p - lane;
+        uint32_t flag = 2, val = 0;  // before tile 0: nothing (tile 0 is always inclusive anyway)
+        if (idx >= 0) {
+            unsigned long long v;
+            do {
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(status + idx) : "memory");
+                flag = (uint32_t)(v >> 32) & 3u;
+            } while ((uint32_t)(v >> 34) != epoch || flag == 0);
+            val = (uint32_t)v;
+        }
+        const unsigned incl = __ballot_sync(0xffffffffu, flag == 2);
+        const int first = incl ? __ffs(incl) - 1 : 31;
+        uint32_t x = lane <= first ? val : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        prefix += x;
+        if (incl) break;
+    }
+    if (lane == 0) st(status + tile, pack(2, prefix + agg));
+    return prefix;
+}
+
 }  // namespace igs_dev
 
 // Device-wide exclusive sum of n u32 (in and out may alias).  Enqueued on
