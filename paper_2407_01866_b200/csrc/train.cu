@@ -620,24 +620,46 @@ __global__ void __launch_bounds__(128, 7) segment_adam_kernel(
             const double2 a = src[0], b = src[1];
             G[0] = a.x; G[1] = a.y; G[2] = b.x; G[3] = b.y;
         } else if (cntg > 0) {
-            uint32_t sl[kShortSeg];
-            uint32_t mseg = cntg;
-            for (uint32_t e = 0; e < mseg; ++e) {
-                const uint32_t val = perm[og + e];
-                uint32_t pos = e;
-                while (pos > 0 && sl[pos - 1] > val) {
-                    sl[pos] = sl[pos - 1];
-                    --pos;
-                }
-                sl[pos] = val;
-            }
-            for (uint32_t e = 0; e < mseg; ++e) {
-                const double2* c = reinterpret_cast<const double2*>(contrib + (size_t)sl[e] * 8 + 4 * h);
+            auto add_row = [&](uint32_t slot) {
+                const double2* c = reinterpret_cast<const double2*>(contrib + (size_t)slot * 8 + 4 * h);
                 const double2 a = c[0], b = c[1];
                 G[0] = __dadd_rn(G[0], a.x);
                 G[1] = __dadd_rn(G[1], a.y);
                 G[2] = __dadd_rn(G[2], b.x);
                 G[3] = __dadd_rn(G[3], b.y);
+            };
+            if (cntg <= 4) {
+                // nearly every segment: its slot ids sorted in registers
+                // (a 5-exchange network), no local-memory array
+                uint32_t s0 = perm[og], s1 = cntg > 1 ? perm[og + 1] : 0xFFFFFFFFu,
+                         s2 = cntg > 2 ? perm[og + 2] : 0xFFFFFFFFu, s3 = cntg > 3 ? perm[og + 3] : 0xFFFFFFFFu;
+                auto cx = [](uint32_t& a, uint32_t& b) {
+                    const uint32_t lo = min(a, b), hi = max(a, b);
+                    a = lo;
+                    b = hi;
+                };
+                cx(s0, s1);
+                cx(s2, s3);
+                cx(s0, s2);
+                cx(s1, s3);
+                cx(s1, s2);
+                add_row(s0);
+                if (cntg > 1) add_row(s1);
+                if (cntg > 2) add_row(s2);
+                if (cntg > 3) add_row(s3);
+            } else {
+                uint32_t sl[kShortSeg];
+                const uint32_t mseg = cntg;
+                for (uint32_t e = 0; e < mseg; ++e) {
+                    const uint32_t val = perm[og + e];
+                    uint32_t pos = e;
+                    while (pos > 0 && sl[pos - 1] > val) {
+                        sl[pos] = sl[pos - 1];
+                        --pos;
+                    }
+                    sl[pos] = val;
+                }
+                for (uint32_t e = 0; e < mseg; ++e) add_row(sl[e]);
             }
             if (live) {
                 double2* o2 = reinterpret_cast<double2*>(grads + (size_t)g * 8 + 4 * h);
