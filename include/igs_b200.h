@@ -122,8 +122,10 @@ int igs_train_step(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, int k,
  * scale, theta; t = 1-based step (bias correction 1 - beta^t uses the
  * host's libm pow exactly like the reference). */
 int igs_adam_step(igs_ctx* ctx, const double* lr4, long long t);
-/* Fused iteration: train_step + adam_step (+ NCCL gradient all-reduce
- * between them when a communicator is attached). */
+/* Fused iteration: train_step + adam_step.  With a communicator attached
+ * the contributions of every rank's sample block are all-gathered between
+ * them (and, with IGS_OPT_SHARD_ADAM, each rank updates its slice of the set
+ * and the parameters are all-gathered); bit-identical to one GPU. */
 int igs_train_iteration(igs_ctx* ctx, const uint32_t* sample_idx, uint32_t ns, int k, const double* lr4,
                         long long t, double* loss);
 /* Asynchronous form for pipelined drivers: enqueues the iteration (the

@@ -3,17 +3,22 @@
 * Training: one iteration's samples are split across ranks in contiguous
   equal blocks (rank r: samples [r ns, (r+1) ns)); every rank runs the exact
   global top-K + contribution epilogue on its block with the upstream scaled
-  by 1 / (total samples), one in-place NCCL all-gather over NVLink (inside
-  the C-ABI, igs_comm_init) completes the contribution and loss arrays in
-  global sample order, and every rank runs the single-GPU sample-ordered
-  reduction and Adam on all of them -- the result is bit-identical to one
-  GPU's, and the replicated sets stay identical across ranks.
+  by 1 / (total samples), in-place all-gathers (NCCL over NVLink, or the
+  in-process loopback group for tests; inside the C-ABI) complete the
+  contribution, key and loss arrays in global sample order, every rank runs
+  the sample-ordered reduction, and -- with IGS_OPT_SHARD_ADAM -- rank r
+  updates its ceil(n/R) slice of the set before an all-gather of the
+  parameters.  Bit-identical to one GPU.
+* Eval / densify (igs_fit on every rank): each rank renders a band of the
+  evaluation image, an all-gather assembles it, and metrics, alias tables
+  and appends are replicated -- every rank writes the single-GPU log.
 * Rendering: pixels are independent; rank r renders the band of tile rows
   [row0, row1) (igs_render_image_rows) with no communication.
 
 The helpers here are the host-side logic; tests/test_dist.py checks the
-decomposition on CPU with gloo (world size 2) against the single-process
-oracle.
+decomposition on CPU with gloo (world size 2 and 3) against the
+single-process oracle, tests/test_gpu_multirank.py the device path through
+the loopback transport.
 """
 from __future__ import annotations
 

@@ -281,7 +281,7 @@ def test_alternate_kernels_bit_identical(gctx, port, monkeypatch, k):
     """The K <= 16 search runs two points per warp (knn_points16_kernel) and
     the reduction's offsets + scatter run as one persistent launch; the
     one-point-per-warp search (IGS_KNN_FULLWARP), the CUB scan + scatter
-    (IGS_CUB_SCAN) and the five-launch tree build (IGS_KNN_BUILD_LAUNCHES)
+    (IGS_SCAN_LAUNCHES) and the five-launch tree build (IGS_KNN_BUILD_LAUNCHES)
     select and sum identically, so 8 iterations give the same
     losses and parameters bit for bit (K = 24 takes the full-warp search
     either way)."""
@@ -297,7 +297,7 @@ def test_alternate_kernels_bit_identical(gctx, port, monkeypatch, k):
 
     l0, p0 = run()
     monkeypatch.setenv("IGS_KNN_FULLWARP", "1")
-    monkeypatch.setenv("IGS_CUB_SCAN", "1")
+    monkeypatch.setenv("IGS_SCAN_LAUNCHES", "1")
     monkeypatch.setenv("IGS_KNN_BUILD_LAUNCHES", "1")
     l1, p1 = run()
     assert l0 == l1
