@@ -365,6 +365,16 @@ def run_ours(args, rank, world, local_rank, dist):
     if world == 1 and not args.no_secondary:
         secondary = {"c1": secondary_c1(ctx), "c3": secondary_c3(ctx), "c4": secondary_c4(ctx),
                      "c5": secondary_c5(ctx), "fit_c2": secondary_fit(ctx)}
+    elif world > 1 and not args.no_secondary:
+        # configs[4] across the ranks: 64 textures, 64 / N per GPU, no communication;
+        # the sweep time is the max over ranks
+        barrier()
+        c5 = secondary_c5(ctx, range(rank, 64, world))
+        c5_ms = max_over_ranks(c5["sweep_ms"])
+        secondary = {"c5_all_ranks": {"config": f"C5: 64 x 1024x1024 textures over {world} GPUs ({64 // world} each), "
+                                                "50k G, 5 LoD prefixes each, blocked (n_max 64)",
+                                      "sweep_ms_max_over_ranks": c5_ms, "renders": 320,
+                                      "mpix_s_incl_partition": 320 * 1024 * 1024 / c5_ms / 1e3}}
 
     out = {
         "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
@@ -489,14 +499,15 @@ def secondary_c4(ctx):
             "global_render_ms": glob_ms, "global_render_mpix_s": W * H / glob_ms / 1e3}
 
 
-def secondary_c5(ctx):
-    """configs[4] (C5), one GPU's share: 8 texture-like 1024x1024 sets of 50k
-    random-local Gaussians; for each, the LoD prefixes {25k, 31.25k, 37.5k,
-    43.75k, 50k} (fit.cpp:182-201's stage counts) are partitioned (n_max 64)
-    and rendered blocked."""
+def secondary_c5(ctx, textures=range(8)):
+    """configs[4] (C5): texture-like 1024x1024 sets of 50k random-local
+    Gaussians; for each, the LoD prefixes {25k, 31.25k, 37.5k, 43.75k, 50k}
+    (fit.cpp:182-201's stage counts) are partitioned (n_max 64) and rendered
+    blocked.  One GPU's share of the 64 textures is 8 of them; with N ranks
+    rank r takes textures r, r + N, ... (64 / N each)."""
     from paper_2407_01866_b200 import synth
     W = H = 1024
-    sets = [synth.random_local_set(50_000, W, H, seed=100 + t) for t in range(8)]
+    sets = [synth.random_local_set(50_000, W, H, seed=100 + t) for t in textures]
     prefixes = [25_000, 31_250, 37_500, 43_750, 50_000]
 
     def sweep():
@@ -507,8 +518,9 @@ def secondary_c5(ctx):
                 ctx.render_image_blocked(W, H, K, host=False)
     sweep()
     ms = _best_ms(ctx, sweep, reps=2)
-    return {"config": "C5 (1 GPU share): 8 x 1024x1024 textures, 50k G, 5 LoD prefixes each, blocked (n_max 64)",
-            "sweep_ms": ms, "renders": 40, "mpix_s_incl_partition": 40 * W * H / ms / 1e3}
+    n = 5 * len(sets)
+    return {"config": f"C5: {len(sets)} x 1024x1024 textures on this GPU, 50k G, 5 LoD prefixes each, blocked "
+                      "(n_max 64)", "sweep_ms": ms, "renders": n, "mpix_s_incl_partition": n * W * H / ms / 1e3}
 
 
 def secondary_fit(ctx):
