@@ -301,7 +301,7 @@ __device__ __forceinline__ Sum own_from(uint32_t m, const Acc& a) {
 __global__ void __launch_bounds__(256) lq_tree_kernel(Acc* __restrict__ acc, Lq L,
                                                       const uint32_t* __restrict__ cnt, Sum* __restrict__ own,
                                                       Sum* __restrict__ sub, unsigned int* __restrict__ ticket,
-                                                      L2Prefetch pf, StageJob job) {
+                                                      L2Prefetch pf, StageJob job, int full) {
     __shared__ Sum sm[2][kBlk * kBlk];
     __shared__ Sum up[kUpCells];
     __shared__ int s_loff[kMaxLv];
@@ -342,15 +342,18 @@ __global__ void __launch_bounds__(256) lq_tree_kernel(Acc* __restrict__ acc, Lq 
     for (int l = 0; l < kInLv; ++l) {
         const int side = kBlk >> l;
         if (t < side * side) {
+            // a cell with no members, or a subtree with none, stays empty
+            // between builds (membership only changes at a build): after the
+            // build's full pass a refit writes only the others
             const Sum o = own_from(m[l], a[l]);
-            own[cell[l]] = o;
+            if (full || m[l]) own[cell[l]] = o;
             Sum s = o;
             if (l > 0) {
                 const int cs = side * 2;
                 for (int dy = 0; dy < 2; ++dy)
                     for (int dx = 0; dx < 2; ++dx) merge(s, sm[cur][(2 * (t / side) + dy) * cs + 2 * (t % side) + dx]);
             }
-            sub[cell[l]] = s;
+            if (full || s.count) sub[cell[l]] = s;
             sm[cur ^ 1][t] = s;
         }
         __syncthreads();
@@ -1654,7 +1657,7 @@ int knn_build(igs_ctx* ctx) {
         const int nb = (b.lq.G0 + kBlk - 1) / kBlk;
         igs_prof_begin(ctx, IGS_PROF_CULL);
         IGS_PDL(ctx, lq_tree_kernel, nb * nb, 256, 0, (Acc*)b.acc.p, b.lq, (const uint32_t*)b.cnt.p, (Sum*)b.own.p,
-                (Sum*)b.sub.p, (unsigned int*)b.ticket.p, search_inputs(ctx, b), job);
+                (Sum*)b.sub.p, (unsigned int*)b.ticket.p, search_inputs(ctx, b), job, 0);
         igs_prof_end(ctx, IGS_PROF_CULL, 0.0);
         b.since_build++;
         b.version = b.chain = ctx->params_version;
@@ -1714,7 +1717,7 @@ int knn_build(igs_ctx* ctx) {
     }
     const int nb = (G0 + kBlk - 1) / kBlk;
     IGS_PDL(ctx, lq_tree_kernel, nb * nb, 256, 0, (Acc*)b.acc.p, L, (const uint32_t*)cnt, (Sum*)b.own.p,
-            (Sum*)b.sub.p, (unsigned int*)b.ticket.p, search_inputs(ctx, b), job);
+            (Sum*)b.sub.p, (unsigned int*)b.ticket.p, search_inputs(ctx, b), job, 1);
     igs_prof_end(ctx, IGS_PROF_CULL, 0.0);
     b.lq = L;
     b.builds++;
