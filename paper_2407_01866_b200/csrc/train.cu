@@ -586,7 +586,10 @@ __device__ __forceinline__ double shx(double v) { return __shfl_xor_sync(0xfffff
 // Two lanes per Gaussian: lane h = 0 owns parameters 0-3 (mu, theta, s1),
 // h = 1 owns 4-7 (s2, colour); the Adam chains split in half, lane 1 forms
 // sin/cos while lane 0 forms both reciprocals.
-__global__ void __launch_bounds__(128, 7) segment_adam_kernel(
+#ifndef IGS_ADAM_MINB
+#define IGS_ADAM_MINB 7
+#endif
+__global__ void __launch_bounds__(128, IGS_ADAM_MINB) segment_adam_kernel(
     uint32_t* __restrict__ gcnt, const uint32_t* __restrict__ goff, const uint32_t* __restrict__ perm,
     const double* __restrict__ contrib, uint32_t n, double* __restrict__ grads, double* __restrict__ params,
     double* __restrict__ m, double* __restrict__ v, ScanRec* __restrict__ scan, ShadeRec* __restrict__ shade,
