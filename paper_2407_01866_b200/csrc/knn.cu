@@ -117,7 +117,8 @@ __global__ void lq_clear(uint32_t cells, uint32_t* __restrict__ cnt2, Acc* __res
 
 __global__ void lq_fill(const ScanRec* __restrict__ scan, uint32_t n, const uint32_t* __restrict__ key,
                         const uint32_t* __restrict__ off, uint32_t* __restrict__ cur, uint32_t* __restrict__ mem,
-                        ScanRec* __restrict__ mrec, uint32_t* __restrict__ minv, Acc* __restrict__ acc) {
+                        ScanRec* __restrict__ mrec, uint32_t* __restrict__ minv, uint32_t* __restrict__ mcell,
+                        Acc* __restrict__ acc) {
     pdl_wait();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -127,6 +128,7 @@ __global__ void lq_fill(const ScanRec* __restrict__ scan, uint32_t n, const uint
     mem[pos] = i;
     mrec[pos] = r;  // the records in member order (the searches' evaluation stream)
     minv[i] = pos;
+    mcell[pos] = k;
     acc_add(acc + k, r);
 }
 
@@ -143,8 +145,8 @@ constexpr int kBuildPer = 4;  // cell counts per thread and scan pass
 __global__ void __launch_bounds__(kBuildThreads) lq_build_kernel(
     const ScanRec* __restrict__ scan, uint32_t n, Lq L, uint32_t cells, uint32_t* __restrict__ cnt,
     uint32_t* __restrict__ cur, uint32_t* __restrict__ off, uint32_t* __restrict__ key, uint32_t* __restrict__ mem,
-    ScanRec* __restrict__ mrec, uint32_t* __restrict__ minv, Acc* __restrict__ acc, uint32_t* __restrict__ lcount,
-    unsigned* __restrict__ bar) {
+    ScanRec* __restrict__ mrec, uint32_t* __restrict__ minv, uint32_t* __restrict__ mcell, Acc* __restrict__ acc,
+    uint32_t* __restrict__ lcount, unsigned* __restrict__ bar) {
     __shared__ uint32_t s_base;
     uint32_t* chunk_sum = bar + 2;
     pdl_wait();
@@ -227,12 +229,64 @@ __global__ void __launch_bounds__(kBuildThreads) lq_build_kernel(
         mem[pos] = i;
         mrec[pos] = r;
         minv[i] = pos;
+        mcell[pos] = k;
         acc_add(acc + k, r);
     }
     __syncthreads();
     if (threadIdx.x == 0 && atomicAdd(bar + 1, 1u) == G - 1) {
         bar[0] = 0;
         bar[1] = 0;
+    }
+}
+
+// Refit, step 1: every cell's accumulator from the member-ordered records
+// (kept current by the Adam launches, tree_acc_add), one thread per member
+// position.  Members of a cell are contiguous, so a warp min/max-reduces its
+// runs of equal cells with shuffles (min/max are idempotent, so overlapping
+// windows are harmless) and the first lane of each run writes it: a plain
+// store when the whole cell lies inside this warp's 32 positions, the
+// order-preserving atomics otherwise (a cell spanning warps; lq_tree_kernel
+// resets those accumulators after reading them, as after a build).
+__global__ void __launch_bounds__(256) lq_own_kernel(const ScanRec* __restrict__ mrec,
+                                                     const uint32_t* __restrict__ mcell,
+                                                     const uint32_t* __restrict__ off,
+                                                     const uint32_t* __restrict__ cnt, uint32_t n,
+                                                     Acc* __restrict__ acc) {
+    pdl_wait();
+    const uint32_t p = blockIdx.x * 256 + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const uint32_t c = p < n ? mcell[p] : ~0u;
+    Acc a = acc_empty();
+    if (p < n) acc_add_local(a, mrec[p]);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t yc = __shfl_down_sync(0xffffffffu, c, o);
+        const unsigned x0 = __shfl_down_sync(0xffffffffu, a.x0, o), y0 = __shfl_down_sync(0xffffffffu, a.y0, o);
+        const unsigned x1 = __shfl_down_sync(0xffffffffu, a.x1, o), y1 = __shfl_down_sync(0xffffffffu, a.y1, o);
+        const unsigned lm = __shfl_down_sync(0xffffffffu, a.lmin, o);
+        const unsigned an = __shfl_down_sync(0xffffffffu, a.aniso, o);
+        if (lane + o < 32 && yc == c) {
+            a.x0 = min(a.x0, x0);
+            a.y0 = min(a.y0, y0);
+            a.x1 = max(a.x1, x1);
+            a.y1 = max(a.y1, y1);
+            a.lmin = min(a.lmin, lm);
+            a.aniso = max(a.aniso, an);
+        }
+    }
+    const uint32_t pc = __shfl_up_sync(0xffffffffu, c, 1);
+    if (c == ~0u || (lane > 0 && pc == c)) return;  // not the first lane of a run
+    const uint32_t base = p - (uint32_t)lane, o0 = off[c];
+    if (o0 >= base && o0 + cnt[c] <= base + 32) {
+        acc[c] = a;
+    } else {
+        Acc* d = acc + c;
+        atomicMin(&d->x0, a.x0);
+        atomicMin(&d->y0, a.y0);
+        atomicMax(&d->x1, a.x1);
+        atomicMax(&d->y1, a.y1);
+        atomicMin(&d->lmin, a.lmin);
+        atomicMax(&d->aniso, a.aniso);
     }
 }
 
@@ -1601,7 +1655,7 @@ __global__ void __launch_bounds__(kOffThreads) hard_offsets_kernel(const ScanRec
 
 
 struct KnnBufs {
-    DevBuf cnt, off, key, mem, own, sub, cub_tmp, hard, ticket, part, lcount, acc;
+    DevBuf cnt, off, key, mem, own, sub, cub_tmp, hard, ticket, part, lcount, acc, mcell;
     DevBuf mrec, minv;  // records in member order, and each Gaussian's position there
     DevBuf bctl;        // lq_build_kernel: barrier counters + chunk totals
     int hard_phase = 0;  // which (hard count, cursor) pair the next search uses
@@ -1656,6 +1710,9 @@ int knn_build(igs_ctx* ctx) {
         // launches since the last build: re-derive the summaries only
         const int nb = (b.lq.G0 + kBlk - 1) / kBlk;
         igs_prof_begin(ctx, IGS_PROF_CULL);
+        IGS_PDL(ctx, lq_own_kernel, (ctx->n + 255) / 256, 256, 0, (const ScanRec*)b.mrec.p,
+                (const uint32_t*)b.mcell.p, (const uint32_t*)b.off.p, (const uint32_t*)b.cnt.p, ctx->n,
+                (Acc*)b.acc.p);
         IGS_PDL(ctx, lq_tree_kernel, nb * nb, 256, 0, (Acc*)b.acc.p, b.lq, (const uint32_t*)b.cnt.p, (Sum*)b.own.p,
                 (Sum*)b.sub.p, (unsigned int*)b.ticket.p, search_inputs(ctx, b), job, 0);
         igs_prof_end(ctx, IGS_PROF_CULL, 0.0);
@@ -1681,7 +1738,7 @@ int knn_build(igs_ctx* ctx) {
     const uint32_t cells = (uint32_t)o;
     if (!grow(b.cnt, (size_t)cells * 8) || !grow(b.off, (size_t)cells * 4) || !grow(b.key, (size_t)n * 4) ||
         !grow(b.mem, (size_t)n * 4) || !grow(b.mrec, (size_t)n * sizeof(ScanRec)) || !grow(b.minv, (size_t)n * 4) ||
-        !grow(b.own, (size_t)cells * sizeof(Sum)) ||
+        !grow(b.mcell, (size_t)n * 4) || !grow(b.own, (size_t)cells * sizeof(Sum)) ||
         !grow(b.sub, (size_t)cells * sizeof(Sum)))
         return igs_fail(ctx, IGS_E_CUDA, "out of device memory (knn)");
     if (!b.ticket.p) {
@@ -1704,7 +1761,7 @@ int knn_build(igs_ctx* ctx) {
         }
         IGS_PDL_COOP(ctx, lq_build_kernel, ctx->sm_count, kBuildThreads, 0, (const ScanRec*)ctx->scan, n, L, cells, cnt,
                 cur, off, (uint32_t*)b.key.p, (uint32_t*)b.mem.p, (ScanRec*)b.mrec.p, (uint32_t*)b.minv.p,
-                (Acc*)b.acc.p, (uint32_t*)b.lcount.p, (unsigned*)b.bctl.p);
+                (uint32_t*)b.mcell.p, (Acc*)b.acc.p, (uint32_t*)b.lcount.p, (unsigned*)b.bctl.p);
     } else {
         IGS_PDL(ctx, lq_clear, 2 * ctx->sm_count, 256, 0, cells, cnt, (Acc*)b.acc.p, (uint32_t*)b.lcount.p);
         IGS_PDL(ctx, lq_count, (n + 255) / 256, 256, 0, (const ScanRec*)ctx->scan, n, L, cnt, (uint32_t*)b.key.p,
@@ -1713,7 +1770,7 @@ int knn_build(igs_ctx* ctx) {
         if (es) return es;
         IGS_PDL(ctx, lq_fill, (n + 255) / 256, 256, 0, (const ScanRec*)ctx->scan, n, (const uint32_t*)b.key.p,
                 (const uint32_t*)off, cur, (uint32_t*)b.mem.p, (ScanRec*)b.mrec.p, (uint32_t*)b.minv.p,
-                (Acc*)b.acc.p);
+                (uint32_t*)b.mcell.p, (Acc*)b.acc.p);
     }
     const int nb = (G0 + kBlk - 1) / kBlk;
     IGS_PDL(ctx, lq_tree_kernel, nb * nb, 256, 0, (Acc*)b.acc.p, L, (const uint32_t*)cnt, (Sum*)b.own.p,
@@ -2143,7 +2200,7 @@ void igs_knn_free(igs_ctx* ctx) {
                 (unsigned long long)b->refits);
     for (DevBuf* d : {&b->bctl, &b->mrec, &b->minv, &b->cnt, &b->off, &b->key, &b->mem, &b->own, &b->sub, &b->cub_tmp,
                       &b->hard, &b->ticket,
-                      &b->part, &b->lcount, &b->acc})
+                      &b->part, &b->lcount, &b->acc, &b->mcell})
         cudaFree(d->p);
     delete b;
     ctx->knn = nullptr;

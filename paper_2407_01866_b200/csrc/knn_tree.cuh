@@ -41,8 +41,9 @@ __device__ __forceinline__ uint32_t key_of(const Lq& L, const ScanRec& r) {
     return (uint32_t)(L.loff[l] + cell_of(r.mu_y, G) * G + cell_of(r.mu_x, G));
 }
 
-// Own-cell summaries are accumulated with order-preserving 32-bit atomics
-// while the members are scattered (no per-cell member loop): a float's bit
+// Own-cell summaries are accumulated with order-preserving 32-bit min/max
+// (atomics while a build scatters the members, warp shuffles over the
+// member-ordered records in a refit -- no per-cell member loop): a float's bit
 // pattern, sign-flipped, orders like the float itself.  Values are rounded
 // in the direction that keeps the summary conservative (bbox outward,
 // lambda_min down, anisotropy up), as the 32-byte Sum stores them.
@@ -55,6 +56,23 @@ __device__ __forceinline__ unsigned okey(float f) {
     return (b >> 31) ? ~b : (b | 0x80000000u);
 }
 __device__ __forceinline__ float odec(unsigned k) { return __uint_as_float((k >> 31) ? (k & 0x7fffffffu) : ~k); }
+
+// Adds Gaussian r to a cell accumulator held by one thread (no atomics):
+// the refit (lq_own_kernel) forms each cell's accumulator from the
+// member-ordered records with the same keys and the same outward rounding
+// as acc_add (min/max are order-free).
+__device__ __forceinline__ void acc_add_local(Acc& a, const ScanRec& r) {
+    const double lo = fmin(r.inv_a, r.inv_b), hi = fmax(r.inv_a, r.inv_b);
+    double aniso = hi / lo;
+    if (!(lo > 0.0) || !isfinite(hi) || !isfinite(r.mu_x) || !isfinite(r.mu_y))
+        aniso = __longlong_as_double(0x7ff0000000000000LL);
+    a.x0 = min(a.x0, okey(__double2float_rd(r.mu_x)));
+    a.y0 = min(a.y0, okey(__double2float_rd(r.mu_y)));
+    a.x1 = max(a.x1, okey(__double2float_ru(r.mu_x)));
+    a.y1 = max(a.y1, okey(__double2float_ru(r.mu_y)));
+    a.lmin = min(a.lmin, okey(__double2float_rd(lo)));
+    a.aniso = max(a.aniso, okey(__double2float_ru(aniso)));
+}
 
 // Adds Gaussian r to a cell accumulator.  A non-finite or degenerate record
 // gets aniso = inf, whose slack 0 makes the cell never prunable.
@@ -87,16 +105,17 @@ struct TreeAcc {
     const uint32_t* minv;           // position of every Gaussian there
 };
 
-// Accumulates Gaussian i (record r) into its stored cell and counts it in
-// *grown when its scale now calls for a coarser level than the one it is
+// Stores Gaussian i's new record r at its member position (the refit reads
+// it there) and counts it in *grown when its scale now calls for a coarser level than the one it is
 // stored at: such a Gaussian weakens the bounds of its cell and every
 // ancestor, so the host re-buckets before the next search (knn_build).  The
 // level here is a float estimate of level_of: it only steers that decision.
 __device__ __forceinline__ void tree_acc_add(const TreeAcc& ta, uint32_t i, const ScanRec& r) {
     if (!ta.acc) return;
     const uint32_t k = ta.key[i];
+    // the member-ordered copy the searches read; the next refit re-derives
+    // every cell accumulator from it (lq_own_kernel), so no atomics here
     ta.mrec[ta.minv[i]] = r;
-    acc_add(ta.acc + (k & kKeyCellMask), r);
     // level_of: smallest l with cell 2^l / G0 >= 2 sigma_max = 2 / sqrt(lmin)
     const float lmin = (float)fmin(r.inv_a, r.inv_b);
     const float l = fminf(ceilf(log2f(2.0f * (float)ta.L.G0 * rsqrtf(lmin))), (float)(ta.L.levels - 1));

@@ -558,7 +558,7 @@ __global__ void adam_kernel(double* __restrict__ params, const double* __restric
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     if (status[0] != LLONG_MAX || status[2] != LLONG_MAX) {
-        tree_acc_add(ta, i, scan[i]);  // every Gaussian is accumulated, updated or not
+        tree_acc_add(ta, i, scan[i]);  // (unchanged)
         return;
     }
     double gg[8], gp[8], mm[8], vv[8];
