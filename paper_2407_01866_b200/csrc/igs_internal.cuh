@@ -187,6 +187,8 @@ struct OffArgs {
     uint32_t* long_count;
     uint32_t* long_list;
     unsigned* bar;         // [0] arrivals, [1] exits
+    const uint32_t* ovf;   // this iteration's bucket-overflow flag: 0 = every segment is in
+                           // its bucket, nothing to scatter (null: always scatter)
 };
 
 }  // namespace igs_dev
@@ -296,7 +298,12 @@ struct igs_ctx {
     struct {
         igs_dev::OffArgs args;   // reduce.cuh: offsets + scatter the kNN launch may take over
         bool ready = false, done = false;
+        uint32_t* bucket = nullptr;    // [n][kBucket] slot ids per Gaussian (search epilogue)
+        uint32_t* ovf = nullptr;       // this iteration's overflow flag (args.ovf)
+        uint32_t* ovf_zero = nullptr;  // the next iteration's, zeroed by the search
     } fuse_off;
+    bool ovf_ready = false;  // the overflow flag pair (scratch 47) zeroed
+    int ovf_phase = 0;
     bool off_ctl_ready = false;  // its barrier counters zeroed (scratch 34)
     bool loss_ticket_ready = false;  // long_segment_kernel's loss ticket zeroed (scratch 35)
     int async_head = 0, async_count = 0;

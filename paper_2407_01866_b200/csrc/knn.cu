@@ -670,6 +670,9 @@ struct Epi {
     double* contrib;             // modes 0/1: [pt][kk][8] (deterministic reduction) or null
     uint32_t* keys;              // modes 0/1: [pt][kk] Gaussian index, n for empty slots
     uint32_t* gcnt;              // modes 0/1 (deterministic): contributions per Gaussian
+    uint32_t* bucket;            // with gcnt: [n][kBucket] slot ids by arrival (reduce.cuh), or null
+    uint32_t* ovf;               // with bucket: raised when a Gaussian gets more than kBucket
+    uint32_t* ovf_zero;          // the next iteration's flag, zeroed at the start of the search
     double* grads_atomic;        // modes 0/1: fast mode (fp64 atomics) or null
     long long* status;           // status[2]: first non-finite loss
     double* oq;                  // mode 2
@@ -804,7 +807,15 @@ __device__ __forceinline__ void warp_epilogue(const Epi& E, const ScanRec* __res
         o[2] = make_double2(d[4], d[5]);
         o[3] = make_double2(d[6], d[7]);
         E.keys[slot] = myi;
-        if (E.gcnt) atomicAdd(E.gcnt + myi, 1u);
+        if (E.gcnt) {
+            const uint32_t pos = atomicAdd(E.gcnt + myi, 1u);
+            if (E.bucket) {
+                if (pos < kBucket)
+                    E.bucket[(size_t)myi * kBucket + pos] = (uint32_t)slot;
+                else
+                    *E.ovf = 1u;
+            }
+        }
     }
 }
 
@@ -835,6 +846,7 @@ __global__ void __launch_bounds__(128, 9) knn_points_kernel(const ScanRec* __res
     // word are zeroed for the next search: nothing reads them before it
     if (blockIdx.x == 0 && threadIdx.x < 2) zero_next[threadIdx.x] = 0;
     if (blockIdx.x == 0 && threadIdx.x == 2 && E.zero_word) *E.zero_word = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 3 && E.ovf_zero) *E.ovf_zero = 0;
     prefetch_l2(E.pf, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -1235,6 +1247,7 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
     pdl_wait();
     if (blockIdx.x == 0 && threadIdx.x < 2) zero_next[threadIdx.x] = 0;
     if (blockIdx.x == 0 && threadIdx.x == 2 && E.zero_word) *E.zero_word = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 3 && E.ovf_zero) *E.ovf_zero = 0;
     prefetch_l2(E.pf, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -2244,6 +2257,11 @@ int igs_knn_forward_backward(igs_ctx* ctx, int mode, const uint32_t* sidx, const
     E.zero_word = zero_word;
     if (pf) E.pf = *pf;
     E.gcnt = gcnt;
+    if (gcnt && ctx->fuse_off.ready && ctx->fuse_off.bucket) {
+        E.bucket = ctx->fuse_off.bucket;
+        E.ovf = ctx->fuse_off.ovf;
+        E.ovf_zero = ctx->fuse_off.ovf_zero;
+    }
     E.mode = mode;
     E.sidx = sidx;
     E.target = (const float*)ctx->target.p;

@@ -9,6 +9,12 @@
 namespace igs_dev {
 
 constexpr uint32_t kShortSeg = 32;  // longer segments go to long_segment_kernel
+// Segment buckets: the search epilogue also files each slot id at
+// bucket[g][arrival rank] while the rank is below kBucket, and raises the
+// iteration's overflow flag otherwise.  With the flag down every segment
+// is short and complete in its bucket, so the offsets + scatter are skipped
+// and Adam reads the buckets (the slot ids are sorted there all the same).
+constexpr uint32_t kBucket = kShortSeg;
 constexpr int kOffThreads = 256;
 constexpr int kOffPer = 4;  // counts per thread and chunk pass
 
@@ -36,6 +42,16 @@ __device__ __forceinline__ void offsets_scatter_body(const OffArgs& A, unsigned 
     uint32_t* __restrict__ long_list = A.long_list;
     unsigned* __restrict__ bar = A.bar;
     const uint32_t G = gridDim.x;
+    if (A.ovf && *(volatile const uint32_t*)A.ovf == 0) {
+        // every segment is in its bucket (uniform: all CTAs read the same
+        // flag); only the exit count, which resets the counters
+        __syncthreads();
+        if (threadIdx.x == 0 && atomicAdd(bar + 1, 1u) == G - 1) {
+            bar[0] = 0;
+            bar[1] = 0;
+        }
+        return;
+    }
     // chunk of CTA b: [b * per_cta, (b + 1) * per_cta), per_cta a multiple of kOffThreads * kOffPer
     const uint32_t tile = kOffThreads * kOffPer;
     const uint32_t per_cta = ((n + G - 1) / G + tile - 1) / tile * tile;

@@ -594,7 +594,8 @@ __global__ void __launch_bounds__(128, IGS_ADAM_MINB) segment_adam_kernel(
     const double* __restrict__ contrib, uint32_t n, double* __restrict__ grads, double* __restrict__ params,
     double* __restrict__ m, double* __restrict__ v, ScanRec* __restrict__ scan, ShadeRec* __restrict__ shade,
     double lr_mu, double lr_color, double lr_scale, double lr_theta, double bc1, double bc2, double ibc1, double ibc2,
-    long long* __restrict__ status, TreeAcc ta, uint32_t g_begin, uint32_t g_end) {
+    long long* __restrict__ status, TreeAcc ta, uint32_t g_begin, uint32_t g_end, const uint32_t* __restrict__ bucket,
+    const uint32_t* __restrict__ ovf) {
     pdl_wait();
     // Gaussians [g_begin, g_end): the whole set, or this rank's slice when
     // the multi-rank update is sharded (n stays the set size: gcnt is [2n])
@@ -602,10 +603,15 @@ __global__ void __launch_bounds__(128, IGS_ADAM_MINB) segment_adam_kernel(
     const int h = threadIdx.x & 1;
     const bool live = g0 < g_end;
     const uint32_t g = live ? g0 : g_end - 1;  // dead pairs shadow a live one (no writes) to keep shuffles full
-    uint32_t cntg = 0, og = 0;
+    // the segment's slot ids: its bucket when no Gaussian overflowed one
+    // (reduce.cuh; uniform), else perm[goff[g] ...]
+    const bool from_bucket = bucket && *ovf == 0u;
+    const uint32_t* __restrict__ seg = from_bucket ? bucket : perm;
+    uint32_t cntg = 0;
+    size_t og = 0;
     if (h == 0) {
         cntg = gcnt[g];
-        og = goff[g];
+        og = from_bucket ? (size_t)g * kBucket : goff[g];
     }
     cntg = __shfl_sync(0xffffffffu, cntg, threadIdx.x & ~1);
     og = __shfl_sync(0xffffffffu, og, threadIdx.x & ~1);
@@ -634,8 +640,8 @@ __global__ void __launch_bounds__(128, IGS_ADAM_MINB) segment_adam_kernel(
             if (cntg <= 4) {
                 // nearly every segment: its slot ids sorted in registers
                 // (a 5-exchange network), no local-memory array
-                uint32_t s0 = perm[og], s1 = cntg > 1 ? perm[og + 1] : 0xFFFFFFFFu,
-                         s2 = cntg > 2 ? perm[og + 2] : 0xFFFFFFFFu, s3 = cntg > 3 ? perm[og + 3] : 0xFFFFFFFFu;
+                uint32_t s0 = seg[og], s1 = cntg > 1 ? seg[og + 1] : 0xFFFFFFFFu,
+                         s2 = cntg > 2 ? seg[og + 2] : 0xFFFFFFFFu, s3 = cntg > 3 ? seg[og + 3] : 0xFFFFFFFFu;
                 auto cx = [](uint32_t& a, uint32_t& b) {
                     const uint32_t lo = min(a, b), hi = max(a, b);
                     a = lo;
@@ -654,7 +660,7 @@ __global__ void __launch_bounds__(128, IGS_ADAM_MINB) segment_adam_kernel(
                 uint32_t sl[kShortSeg];
                 const uint32_t mseg = cntg;
                 for (uint32_t e = 0; e < mseg; ++e) {
-                    const uint32_t val = perm[og + e];
+                    const uint32_t val = seg[og + e];
                     uint32_t pos = e;
                     while (pos > 0 && sl[pos - 1] > val) {
                         sl[pos] = sl[pos - 1];
@@ -985,6 +991,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
     double* losses = (double*)igs_scratch(ctx, 9, (size_t)std::max<uint32_t>(ns_all, 1) * sizeof(double));
     double* contrib = nullptr;
     uint32_t *keys = nullptr, *gcnt = nullptr, *goff = nullptr, *perm = nullptr, *long_ctl = nullptr;
+    uint32_t *bucket = nullptr, *ovf = nullptr;  // segment buckets, when the search files them
     bool gcnt_filled = false;
     if (ctx->opt_deterministic) {
         contrib = (double*)igs_scratch(ctx, 3, items * 8 * sizeof(double));
@@ -1025,8 +1032,25 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
             uint32_t* ctl = off_ctl(ctx);
             if (!ctl) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (scan)");
             ctx->fuse_off.args = OffArgs{(const uint32_t*)gcnt, n, goff, ctl + 2, (const uint32_t*)keys, (uint32_t)items,
-                                         gcnt + n, perm, long_ctl, long_ctl + 1, (unsigned*)ctl};
+                                         gcnt + n, perm, long_ctl, long_ctl + 1, (unsigned*)ctl, nullptr};
             ctx->fuse_off.ready = true;
+            if (fuse_lr4 && !igs_has_comm(ctx) && !getenv("IGS_NO_BUCKET")) {
+                // segment buckets (reduce.cuh): read by the fused Adam, so only
+                // when it follows; two overflow flags used alternately
+                bucket = (uint32_t*)igs_scratch(ctx, 46, (size_t)n * kBucket * sizeof(uint32_t));
+                uint32_t* flags = (uint32_t*)igs_scratch(ctx, 47, 2 * sizeof(uint32_t));
+                if (!bucket || !flags) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (buckets)");
+                if (!ctx->ovf_ready) {
+                    IGS_CUDA(ctx, cudaMemsetAsync(flags, 0, 2 * sizeof(uint32_t), ctx->stream));
+                    ctx->ovf_ready = true;
+                }
+                ctx->ovf_phase ^= 1;
+                ovf = flags + ctx->ovf_phase;
+                ctx->fuse_off.bucket = bucket;
+                ctx->fuse_off.ovf = ovf;
+                ctx->fuse_off.ovf_zero = flags + (ctx->ovf_phase ^ 1);
+                ctx->fuse_off.args.ovf = ovf;
+            }
         }
         e = igs_knn_forward_backward(ctx, mode, dev_sidx, dev_samples5, ns, kk, inv_n, losses + (size_t)rk * ns,
                                      contrib ? contrib + rk * items_local * 8 : nullptr,
@@ -1034,6 +1058,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
                                      ctx->opt_deterministic ? nullptr : ctx->grads, long_ctl, &pf, exch ? 1 : 0);
         ctx->stage_job = StageJob{};
         ctx->fuse_off.ready = false;
+        ctx->fuse_off.bucket = nullptr;
         if (e) return e;
         gcnt_filled = !exch;
     } else {
@@ -1095,7 +1120,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
             uint32_t* ctl = off_ctl(ctx);
             if (!ctl) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (scan)");
             OffArgs A{(const uint32_t*)gcnt, n, goff, ctl + 2, (const uint32_t*)keys, (uint32_t)items, gcnt + n, perm,
-                      long_ctl, long_ctl + 1, (unsigned*)ctl};
+                      long_ctl, long_ctl + 1, (unsigned*)ctl, ovf};
             IGS_PDL_COOP(ctx, offsets_scatter_kernel, (unsigned)ctx->sm_count, kOffThreads, 0, A);
         } else {
             if ((e = igs_scan_excl_u32(ctx, gcnt, goff, (size_t)n))) return e;
@@ -1132,7 +1157,8 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
                 IGS_PDL(ctx, segment_adam_kernel, (hi - lo + 63) / 64, 128, 0, gcnt, (const uint32_t*)goff,
                         (const uint32_t*)perm, (const double*)contrib, n, ctx->grads, ctx->params, ctx->adam_m,
                         ctx->adam_v, ctx->scan, ctx->shade, fuse_lr4[0], fuse_lr4[1], fuse_lr4[2], fuse_lr4[3], bc1,
-                        bc2, 1.0 / bc1, 1.0 / bc2, ctx->status, ta, lo, hi);
+                        bc2, 1.0 / bc1, 1.0 / bc2, ctx->status, ta, lo, hi, (const uint32_t*)bucket,
+                        (const uint32_t*)ovf);
             if (shard) {
                 // flags of every slice, then every slice's parameters, then
                 // the records + tree accumulation of the other slices here
