@@ -187,8 +187,11 @@ struct OffArgs {
     uint32_t* long_count;
     uint32_t* long_list;
     unsigned* bar;         // [0] arrivals, [1] exits
-    const uint32_t* ovf;   // this iteration's bucket-overflow flag: 0 = every segment is in
-                           // its bucket, nothing to scatter (null: always scatter)
+    // bucket mode (reduce.cuh; null: CSR of every segment): this
+    // iteration's [0] overflow entries, [1] allocation cursor, and the
+    // (slot, rank) pairs of the overflow entries
+    uint32_t* ovf;
+    const uint32_t* ovf_list;
 };
 
 }  // namespace igs_dev
@@ -299,10 +302,12 @@ struct igs_ctx {
         igs_dev::OffArgs args;   // reduce.cuh: offsets + scatter the kNN launch may take over
         bool ready = false, done = false;
         uint32_t* bucket = nullptr;    // [n][kBucket] slot ids per Gaussian (search epilogue)
-        uint32_t* ovf = nullptr;       // this iteration's overflow flag (args.ovf)
-        uint32_t* ovf_zero = nullptr;  // the next iteration's, zeroed by the search
+        uint32_t* ovf = nullptr;       // this iteration's counters: overflow entries, allocation, long segments
+        uint32_t* ovf_list = nullptr;  // (slot, rank) of every overflow entry
+        uint32_t* long_list = nullptr; // Gaussians with more than kBucket contributions
+        uint32_t* ovf_zero = nullptr;  // the next iteration's counters, zeroed by the search
     } fuse_off;
-    bool ovf_ready = false;  // the overflow flag pair (scratch 47) zeroed
+    bool ovf_ready = false;  // the counter pair (scratch 47) zeroed
     int ovf_phase = 0;
     bool off_ctl_ready = false;  // its barrier counters zeroed (scratch 34)
     bool loss_ticket_ready = false;  // long_segment_kernel's loss ticket zeroed (scratch 35)

@@ -671,8 +671,10 @@ struct Epi {
     uint32_t* keys;              // modes 0/1: [pt][kk] Gaussian index, n for empty slots
     uint32_t* gcnt;              // modes 0/1 (deterministic): contributions per Gaussian
     uint32_t* bucket;            // with gcnt: [n][kBucket] slot ids by arrival (reduce.cuh), or null
-    uint32_t* ovf;               // with bucket: raised when a Gaussian gets more than kBucket
-    uint32_t* ovf_zero;          // the next iteration's flag, zeroed at the start of the search
+    uint32_t* ovf;               // with bucket: [0] overflow entries, [2] long segments (reduce.cuh)
+    uint32_t* ovf_list;          // with bucket: (slot, rank) of every overflow entry
+    uint32_t* long_list;         // with bucket: the long segments' Gaussians
+    uint32_t* ovf_zero;          // the next iteration's counters (3 words), zeroed at the start of the search
     double* grads_atomic;        // modes 0/1: fast mode (fp64 atomics) or null
     long long* status;           // status[2]: first non-finite loss
     double* oq;                  // mode 2
@@ -810,10 +812,20 @@ __device__ __forceinline__ void warp_epilogue(const Epi& E, const ScanRec* __res
         if (E.gcnt) {
             const uint32_t pos = atomicAdd(E.gcnt + myi, 1u);
             if (E.bucket) {
-                if (pos < kBucket)
+                // overflow entries appended with one atomic per warp
+                const unsigned act = __activemask();
+                const unsigned over = __ballot_sync(act, pos >= kBucket);
+                if (pos < kBucket) {
                     E.bucket[(size_t)myi * kBucket + pos] = (uint32_t)slot;
-                else
-                    *E.ovf = 1u;
+                } else {
+                    const int leader = __ffs(over) - 1;
+                    uint32_t q0 = 0;
+                    if ((int)(threadIdx.x & 31) == leader) q0 = atomicAdd(E.ovf, (unsigned)__popc(over));
+                    const uint32_t q = __shfl_sync(over, q0, leader) + __popc(over & ((1u << (threadIdx.x & 31)) - 1));
+                    E.ovf_list[2 * q] = (uint32_t)slot;
+                    E.ovf_list[2 * q + 1] = pos;
+                    if (pos == kBucket) E.long_list[atomicAdd(E.ovf + 2, 1u)] = myi;
+                }
             }
         }
     }
@@ -846,7 +858,7 @@ __global__ void __launch_bounds__(128, 9) knn_points_kernel(const ScanRec* __res
     // word are zeroed for the next search: nothing reads them before it
     if (blockIdx.x == 0 && threadIdx.x < 2) zero_next[threadIdx.x] = 0;
     if (blockIdx.x == 0 && threadIdx.x == 2 && E.zero_word) *E.zero_word = 0;
-    if (blockIdx.x == 0 && threadIdx.x == 3 && E.ovf_zero) *E.ovf_zero = 0;
+    if (blockIdx.x == 0 && threadIdx.x >= 3 && threadIdx.x < 6 && E.ovf_zero) E.ovf_zero[threadIdx.x - 3] = 0;
     prefetch_l2(E.pf, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -1247,7 +1259,7 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
     pdl_wait();
     if (blockIdx.x == 0 && threadIdx.x < 2) zero_next[threadIdx.x] = 0;
     if (blockIdx.x == 0 && threadIdx.x == 2 && E.zero_word) *E.zero_word = 0;
-    if (blockIdx.x == 0 && threadIdx.x == 3 && E.ovf_zero) *E.ovf_zero = 0;
+    if (blockIdx.x == 0 && threadIdx.x >= 3 && threadIdx.x < 6 && E.ovf_zero) E.ovf_zero[threadIdx.x - 3] = 0;
     prefetch_l2(E.pf, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -2260,6 +2272,8 @@ int igs_knn_forward_backward(igs_ctx* ctx, int mode, const uint32_t* sidx, const
     if (gcnt && ctx->fuse_off.ready && ctx->fuse_off.bucket) {
         E.bucket = ctx->fuse_off.bucket;
         E.ovf = ctx->fuse_off.ovf;
+        E.ovf_list = ctx->fuse_off.ovf_list;
+        E.long_list = ctx->fuse_off.long_list;
         E.ovf_zero = ctx->fuse_off.ovf_zero;
     }
     E.mode = mode;

@@ -9,11 +9,15 @@
 namespace igs_dev {
 
 constexpr uint32_t kShortSeg = 32;  // longer segments go to long_segment_kernel
-// Segment buckets: the search epilogue also files each slot id at
-// bucket[g][arrival rank] while the rank is below kBucket, and raises the
-// iteration's overflow flag otherwise.  With the flag down every segment
-// is short and complete in its bucket, so the offsets + scatter are skipped
-// and Adam reads the buckets (the slot ids are sorted there all the same).
+// Segment buckets: the search epilogue files each slot id at
+// bucket[g][arrival rank] while the rank is below kBucket (every short
+// segment is then complete in its bucket: Adam sorts and sums it there, no
+// offsets, no scatter).  Later arrivals are overflow entries -- (slot, rank)
+// appended to a list -- and a Gaussian's first one queues it as a long
+// segment.  The offsets body then gives each long segment a region of
+// perm (bump allocation: regions in any order, ranks inside), a grid
+// barrier, and drops the overflow entries at region + rank; the long
+// kernel reads ranks < kBucket from the bucket and the rest from perm.
 constexpr uint32_t kBucket = kShortSeg;
 constexpr int kOffThreads = 256;
 constexpr int kOffPer = 4;  // counts per thread and chunk pass
@@ -42,9 +46,20 @@ __device__ __forceinline__ void offsets_scatter_body(const OffArgs& A, unsigned 
     uint32_t* __restrict__ long_list = A.long_list;
     unsigned* __restrict__ bar = A.bar;
     const uint32_t G = gridDim.x;
-    if (A.ovf && *(volatile const uint32_t*)A.ovf == 0) {
-        // every segment is in its bucket (uniform: all CTAs read the same
-        // flag); only the exit count, which resets the counters
+    if (A.ovf) {
+        const uint32_t no = *(volatile const uint32_t*)A.ovf;  // (uniform)
+        if (no) {
+            const uint32_t nl = *(volatile const uint32_t*)long_count;
+            for (uint32_t i = blockIdx.x * kOffThreads + threadIdx.x; i < nl; i += G * kOffThreads) {
+                const uint32_t g = long_list[i];
+                goff[g] = atomicAdd(A.ovf + 1, gcnt[g]);  // (ranks < kBucket of the region stay unused)
+            }
+            igs_grid_sync(A.bar, bar_base + G);
+            for (uint32_t i = blockIdx.x * kOffThreads + threadIdx.x; i < no; i += G * kOffThreads) {
+                const uint32_t slot = A.ovf_list[2 * i], pos = A.ovf_list[2 * i + 1];
+                perm[__ldcg(goff + keys[slot]) + pos] = slot;
+            }
+        }
         __syncthreads();
         if (threadIdx.x == 0 && atomicAdd(bar + 1, 1u) == G - 1) {
             bar[0] = 0;

@@ -275,7 +275,8 @@ __global__ void __launch_bounds__(kLongThreads) long_segment_kernel(const uint32
                                                                     uint32_t ns, double inv_n,
                                                                     double* __restrict__ dloss,
                                                                     double* __restrict__ loss_part,
-                                                                    unsigned* __restrict__ loss_ticket) {
+                                                                    unsigned* __restrict__ loss_ticket,
+                                                                    const uint32_t* __restrict__ bucket) {
     pdl_wait();
     __shared__ uint32_t keys[kLongCap];
     __shared__ uint32_t sorted[kLongCap];
@@ -313,10 +314,14 @@ __global__ void __launch_bounds__(kLongThreads) long_segment_kernel(const uint32
     for (uint32_t it = blockIdx.x; it < total; it += gridDim.x) {
         const uint32_t g = long_list[it];
         const uint32_t m = gcnt[g], o = goff[g];
+        // slot id of rank e: bucket mode keeps ranks < kBucket in the bucket
+        auto slot_at = [&](uint32_t e) {
+            return bucket && e < kBucket ? bucket[(size_t)g * kBucket + e] : perm[o + e];
+        };
         const uint32_t* out = sorted;
         __syncthreads();
         if (m <= kLongRank) {
-            for (uint32_t e = t; e < m; e += kLongThreads) keys[e] = perm[o + e];
+            for (uint32_t e = t; e < m; e += kLongThreads) keys[e] = slot_at(e);
             __syncthreads();
             for (uint32_t e = t; e < m; e += kLongThreads) {
                 const uint32_t v = keys[e];
@@ -328,7 +333,7 @@ __global__ void __launch_bounds__(kLongThreads) long_segment_kernel(const uint32
             // bitonic sort in shared memory, padded to a power of two
             uint32_t pow2 = 1;
             while (pow2 < m) pow2 <<= 1;
-            for (uint32_t e = t; e < pow2; e += kLongThreads) keys[e] = e < m ? perm[o + e] : 0xFFFFFFFFu;
+            for (uint32_t e = t; e < pow2; e += kLongThreads) keys[e] = e < m ? slot_at(e) : 0xFFFFFFFFu;
             __syncthreads();
             for (uint32_t size = 2; size <= pow2; size <<= 1)
                 for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
@@ -350,9 +355,9 @@ __global__ void __launch_bounds__(kLongThreads) long_segment_kernel(const uint32
             // beyond shared memory (degenerate sets): rank from global
             // memory into the same range of a second slot array
             for (uint32_t e = t; e < m; e += kLongThreads) {
-                const uint32_t v = perm[o + e];
+                const uint32_t v = slot_at(e);
                 uint32_t r = 0;
-                for (uint32_t j = 0; j < m; ++j) r += perm[o + j] < v;
+                for (uint32_t j = 0; j < m; ++j) r += slot_at(j) < v;
                 big[o + r] = v;
             }
             out = big + o;
@@ -594,8 +599,7 @@ __global__ void __launch_bounds__(128, IGS_ADAM_MINB) segment_adam_kernel(
     const double* __restrict__ contrib, uint32_t n, double* __restrict__ grads, double* __restrict__ params,
     double* __restrict__ m, double* __restrict__ v, ScanRec* __restrict__ scan, ShadeRec* __restrict__ shade,
     double lr_mu, double lr_color, double lr_scale, double lr_theta, double bc1, double bc2, double ibc1, double ibc2,
-    long long* __restrict__ status, TreeAcc ta, uint32_t g_begin, uint32_t g_end, const uint32_t* __restrict__ bucket,
-    const uint32_t* __restrict__ ovf) {
+    long long* __restrict__ status, TreeAcc ta, uint32_t g_begin, uint32_t g_end, const uint32_t* __restrict__ bucket) {
     pdl_wait();
     // Gaussians [g_begin, g_end): the whole set, or this rank's slice when
     // the multi-rank update is sharded (n stays the set size: gcnt is [2n])
@@ -603,9 +607,8 @@ __global__ void __launch_bounds__(128, IGS_ADAM_MINB) segment_adam_kernel(
     const int h = threadIdx.x & 1;
     const bool live = g0 < g_end;
     const uint32_t g = live ? g0 : g_end - 1;  // dead pairs shadow a live one (no writes) to keep shuffles full
-    // the segment's slot ids: its bucket when no Gaussian overflowed one
-    // (reduce.cuh; uniform), else perm[goff[g] ...]
-    const bool from_bucket = bucket && *ovf == 0u;
+    // a short segment's slot ids: its bucket (reduce.cuh), else perm[goff[g] ...]
+    const bool from_bucket = bucket != nullptr;
     const uint32_t* __restrict__ seg = from_bucket ? bucket : perm;
     uint32_t cntg = 0;
     size_t og = 0;
@@ -621,6 +624,28 @@ __global__ void __launch_bounds__(128, IGS_ADAM_MINB) segment_adam_kernel(
         gcnt[n + g] = 0;
     }
     const bool skip_all = status[2] != LLONG_MAX;
+    // segments of 5..kShortSeg slot ids: put in slot order by the whole warp,
+    // one segment at a time (lane e loads id e -- one row of the bucket --
+    // and takes its rank among the others by shuffles; distinct ids), into
+    // this pair's row of s_sorted.  Dead pairs shadow a live Gaussian, so
+    // they sort (and later read) a valid segment too.
+    __shared__ uint32_t s_sorted[4][16][kShortSeg];
+    uint32_t* my_sorted = s_sorted[(threadIdx.x >> 5) & 3][(threadIdx.x & 31) >> 1];
+    {
+        const int lane = threadIdx.x & 31;
+        unsigned med = __ballot_sync(0xffffffffu, !skip_all && h == 0 && cntg > 4 && cntg <= kShortSeg);
+        while (med) {
+            const int src = __ffs(med) - 1;
+            med &= med - 1;
+            const uint32_t mm = __shfl_sync(0xffffffffu, cntg, src);
+            const size_t oo = __shfl_sync(0xffffffffu, og, src);
+            const uint32_t v = (uint32_t)lane < mm ? seg[oo + lane] : 0xFFFFFFFFu;
+            uint32_t r = 0;
+            for (uint32_t j = 0; j < mm; ++j) r += __shfl_sync(0xffffffffu, v, j) < v;
+            if ((uint32_t)lane < mm) s_sorted[(threadIdx.x >> 5) & 3][src >> 1][r] = v;
+        }
+        __syncwarp();
+    }
     // gradient components 4h .. 4h+3
     double G[4] = {0, 0, 0, 0};
     if (!skip_all) {
@@ -657,18 +682,7 @@ __global__ void __launch_bounds__(128, IGS_ADAM_MINB) segment_adam_kernel(
                 if (cntg > 2) add_row(s2);
                 if (cntg > 3) add_row(s3);
             } else {
-                uint32_t sl[kShortSeg];
-                const uint32_t mseg = cntg;
-                for (uint32_t e = 0; e < mseg; ++e) {
-                    const uint32_t val = seg[og + e];
-                    uint32_t pos = e;
-                    while (pos > 0 && sl[pos - 1] > val) {
-                        sl[pos] = sl[pos - 1];
-                        --pos;
-                    }
-                    sl[pos] = val;
-                }
-                for (uint32_t e = 0; e < mseg; ++e) add_row(sl[e]);
+                for (uint32_t e = 0; e < cntg; ++e) add_row(my_sorted[e]);  // (sorted above)
             }
             if (live) {
                 double2* o2 = reinterpret_cast<double2*>(grads + (size_t)g * 8 + 4 * h);
@@ -991,7 +1005,8 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
     double* losses = (double*)igs_scratch(ctx, 9, (size_t)std::max<uint32_t>(ns_all, 1) * sizeof(double));
     double* contrib = nullptr;
     uint32_t *keys = nullptr, *gcnt = nullptr, *goff = nullptr, *perm = nullptr, *long_ctl = nullptr;
-    uint32_t *bucket = nullptr, *ovf = nullptr;  // segment buckets, when the search files them
+    // segment buckets, when the search files them (reduce.cuh)
+    uint32_t *bucket = nullptr, *ovf = nullptr, *ovf_list = nullptr;
     bool gcnt_filled = false;
     if (ctx->opt_deterministic) {
         contrib = (double*)igs_scratch(ctx, 3, items * 8 * sizeof(double));
@@ -1032,24 +1047,30 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
             uint32_t* ctl = off_ctl(ctx);
             if (!ctl) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (scan)");
             ctx->fuse_off.args = OffArgs{(const uint32_t*)gcnt, n, goff, ctl + 2, (const uint32_t*)keys, (uint32_t)items,
-                                         gcnt + n, perm, long_ctl, long_ctl + 1, (unsigned*)ctl, nullptr};
+                                         gcnt + n, perm, long_ctl, long_ctl + 1, (unsigned*)ctl, nullptr, nullptr};
             ctx->fuse_off.ready = true;
             if (fuse_lr4 && !igs_has_comm(ctx) && !getenv("IGS_NO_BUCKET")) {
                 // segment buckets (reduce.cuh): read by the fused Adam, so only
-                // when it follows; two overflow flags used alternately
-                bucket = (uint32_t*)igs_scratch(ctx, 46, (size_t)n * kBucket * sizeof(uint32_t));
-                uint32_t* flags = (uint32_t*)igs_scratch(ctx, 47, 2 * sizeof(uint32_t));
-                if (!bucket || !flags) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (buckets)");
+                // when it follows; two sets of counters used alternately (the
+                // search zeroes the other set)
+                bucket = (uint32_t*)igs_scratch(ctx, 46, ((size_t)n * kBucket + 2 * items) * sizeof(uint32_t));
+                uint32_t* ctr = (uint32_t*)igs_scratch(ctx, 47, 8 * sizeof(uint32_t));
+                if (!bucket || !ctr) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (buckets)");
                 if (!ctx->ovf_ready) {
-                    IGS_CUDA(ctx, cudaMemsetAsync(flags, 0, 2 * sizeof(uint32_t), ctx->stream));
+                    IGS_CUDA(ctx, cudaMemsetAsync(ctr, 0, 8 * sizeof(uint32_t), ctx->stream));
                     ctx->ovf_ready = true;
                 }
                 ctx->ovf_phase ^= 1;
-                ovf = flags + ctx->ovf_phase;
+                ovf = ctr + 4 * ctx->ovf_phase;
+                ovf_list = bucket + (size_t)n * kBucket;
                 ctx->fuse_off.bucket = bucket;
                 ctx->fuse_off.ovf = ovf;
-                ctx->fuse_off.ovf_zero = flags + (ctx->ovf_phase ^ 1);
+                ctx->fuse_off.ovf_list = ovf_list;
+                ctx->fuse_off.long_list = long_ctl + 1;
+                ctx->fuse_off.ovf_zero = ctr + 4 * (ctx->ovf_phase ^ 1);
                 ctx->fuse_off.args.ovf = ovf;
+                ctx->fuse_off.args.ovf_list = ovf_list;
+                ctx->fuse_off.args.long_count = ovf + 2;
             }
         }
         e = igs_knn_forward_backward(ctx, mode, dev_sidx, dev_samples5, ns, kk, inv_n, losses + (size_t)rk * ns,
@@ -1120,7 +1141,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
             uint32_t* ctl = off_ctl(ctx);
             if (!ctl) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (scan)");
             OffArgs A{(const uint32_t*)gcnt, n, goff, ctl + 2, (const uint32_t*)keys, (uint32_t)items, gcnt + n, perm,
-                      long_ctl, long_ctl + 1, (unsigned*)ctl, ovf};
+                      bucket ? ovf + 2 : long_ctl, long_ctl + 1, (unsigned*)ctl, ovf, ovf_list};
             IGS_PDL_COOP(ctx, offsets_scatter_kernel, (unsigned)ctx->sm_count, kOffThreads, 0, A);
         } else {
             if ((e = igs_scan_excl_u32(ctx, gcnt, goff, (size_t)n))) return e;
@@ -1138,9 +1159,10 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
             ctx->loss_ticket_ready = true;
         }
         IGS_PDL(ctx, long_segment_kernel, 8 * ctx->sm_count, kLongThreads, 0, (const uint32_t*)gcnt,
-                (const uint32_t*)goff, perm, (const double*)contrib, ctx->grads, (const uint32_t*)long_ctl,
+                (const uint32_t*)goff, perm, (const double*)contrib, ctx->grads,
+                (const uint32_t*)(bucket ? ovf + 2 : long_ctl),
                 (const uint32_t*)(long_ctl + 1), ctx->status, big, (const double*)losses, ns_all, inv_n,
-                mode == 0 ? dev_loss : nullptr, loss_part, (unsigned*)(loss_part + kLossCtas));
+                mode == 0 ? dev_loss : nullptr, loss_part, (unsigned*)(loss_part + kLossCtas), (const uint32_t*)bucket);
         if (fuse_lr4 && (exch || !igs_has_comm(ctx))) {
             // short segments summed inside the Adam kernel (one pass over the set)
             const double bc1 = 1.0 - std::pow(0.9, (double)t);  // adam.cpp:16-17, host libm
@@ -1157,8 +1179,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
                 IGS_PDL(ctx, segment_adam_kernel, (hi - lo + 63) / 64, 128, 0, gcnt, (const uint32_t*)goff,
                         (const uint32_t*)perm, (const double*)contrib, n, ctx->grads, ctx->params, ctx->adam_m,
                         ctx->adam_v, ctx->scan, ctx->shade, fuse_lr4[0], fuse_lr4[1], fuse_lr4[2], fuse_lr4[3], bc1,
-                        bc2, 1.0 / bc1, 1.0 / bc2, ctx->status, ta, lo, hi, (const uint32_t*)bucket,
-                        (const uint32_t*)ovf);
+                        bc2, 1.0 / bc1, 1.0 / bc2, ctx->status, ta, lo, hi, (const uint32_t*)bucket);
             if (shard) {
                 // flags of every slice, then every slice's parameters, then
                 // the records + tree accumulation of the other slices here
