@@ -194,6 +194,27 @@ struct OffArgs {
     const uint32_t* ovf_list;
 };
 
+// Long segments (more than kShortSeg contributions) and the loss (reduce.cuh:
+// long_segments, loss_chunk).
+struct LongArgs {
+    const uint32_t* gcnt;
+    const uint32_t* goff;
+    const uint32_t* perm;
+    const double* contrib;
+    double* grads;
+    const uint32_t* long_count;
+    const uint32_t* long_list;
+    long long* status;
+    uint32_t* big;            // scratch beyond shared memory (items entries)
+    const double* losses;
+    uint32_t ns;
+    double inv_n;
+    double* dloss;            // null: no loss
+    double* loss_part;        // kLossCtas partials, then the combining ticket
+    unsigned* loss_ticket;
+    const uint32_t* bucket;   // bucket mode: ranks < kBucket live there
+};
+
 }  // namespace igs_dev
 
 // ---------------------------------------------------------------------------
@@ -306,6 +327,8 @@ struct igs_ctx {
         uint32_t* ovf_list = nullptr;  // (slot, rank) of every overflow entry
         uint32_t* long_list = nullptr; // Gaussians with more than kBucket contributions
         uint32_t* ovf_zero = nullptr;  // the next iteration's counters, zeroed by the search
+        igs_dev::LongArgs long_args;   // bucket mode: the long segments + loss ride in the same launch
+        bool fuse_long = false;
     } fuse_off;
     bool ovf_ready = false;  // the counter pair (scratch 47) zeroed
     int ovf_phase = 0;

@@ -1657,6 +1657,9 @@ __global__ void __launch_bounds__(kHardThreads) hard_scan_kernel(const ScanRec* 
 // launch (one CTA per SM): the hard points' contributions (when there are
 // any) land before a grid barrier, then offsets_scatter_body.  Saves the
 // hard-point scan's own launch, which the chain pays even when it is empty.
+// With fuse_long (bucket mode) the loss (CTAs 0..kLossCtas-1, first) and the
+// long segments (after one more barrier, only when there are any) ride here
+// too, and the separate long-segment launch is skipped.
 template <int KCAP>
 __global__ void __launch_bounds__(kOffThreads) hard_offsets_kernel(const ScanRec* __restrict__ scan, uint32_t n,
                                                                    const double* __restrict__ uv, int W, int H, int kk,
@@ -1666,8 +1669,9 @@ __global__ void __launch_bounds__(kOffThreads) hard_offsets_kernel(const ScanRec
                                                                    uint32_t* __restrict__ part_i,
                                                                    unsigned int* __restrict__ point_done,
                                                                    unsigned long long* __restrict__ pairs,
-                                                                   OffArgs A) {
+                                                                   OffArgs A, LongArgs LA, int fuse_long) {
     pdl_wait();
+    if (fuse_long && LA.dloss && blockIdx.x < kLossCtas) loss_chunk(LA, blockIdx.x);
     const uint32_t cnt = min(*hard_count, kHardCap);
     unsigned base = 0;
     if (cnt) {  // (uniform: every CTA read the same count)
@@ -1675,7 +1679,14 @@ __global__ void __launch_bounds__(kOffThreads) hard_offsets_kernel(const ScanRec
         igs_grid_sync(A.bar, gridDim.x);
         base = gridDim.x;
     }
-    offsets_scatter_body(A, base);
+    base = offsets_scatter_body(A, base);
+    // bucket mode: the long-segment queue was complete before the launch
+    // (search epilogue) or the barrier above (hard points) -- uniform
+    if (fuse_long && *(volatile const uint32_t*)LA.long_count) {
+        igs_grid_sync(A.bar, base + gridDim.x);  // the overflow entries scattered
+        long_segments(LA, blockIdx.x, gridDim.x);
+    }
+    grid_exit(A.bar);
 }
 
 
@@ -1871,10 +1882,18 @@ int launch_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int 
             // (profiled with the reduction: mostly its offsets + scatter)
             igs_prof_end(ctx, IGS_PROF_SCAN, 0.0);
             igs_prof_begin(ctx, IGS_PROF_REDUCE);
-            IGS_PDL_COOP(ctx, hard_offsets_kernel<KCAP>, ctx->sm_count, kOffThreads, 0, (const ScanRec*)ctx->scan, ctx->n,
+            // up to kOffCtasPerSm co-resident CTAs per SM (the long segments
+            // take one CTA each)
+            static int per_sm = 0;
+            if (!per_sm) {
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hard_offsets_kernel<KCAP>, kOffThreads, 0);
+                per_sm = std::max(1, std::min(per_sm, kOffCtasPerSm));
+            }
+            IGS_PDL_COOP(ctx, hard_offsets_kernel<KCAP>, per_sm * ctx->sm_count, kOffThreads, 0,
+                    (const ScanRec*)ctx->scan, ctx->n,
                     uv, W, H, kk, (const uint32_t*)hard_count, (const uint32_t*)hard_list, E, part_q, part_i,
                     (unsigned int*)((uint32_t*)b.hard.p + 4 + kHardCap), igs_prof_counter(ctx, IGS_PROF_SCAN),
-                    ctx->fuse_off.args);
+                    ctx->fuse_off.args, ctx->fuse_off.long_args, (int)ctx->fuse_off.fuse_long);
             igs_prof_end(ctx, IGS_PROF_REDUCE, 0.0);
             return IGS_OK;
         }

@@ -21,6 +21,7 @@ constexpr uint32_t kShortSeg = 32;  // longer segments go to long_segment_kernel
 constexpr uint32_t kBucket = kShortSeg;
 constexpr int kOffThreads = 256;
 constexpr int kOffPer = 4;  // counts per thread and chunk pass
+constexpr int kOffCtasPerSm = 2;  // persistent offsets launches: at most this many CTAs per SM (chunk_sum sizing)
 
 // (OffArgs: igs_internal.cuh)
 
@@ -29,10 +30,11 @@ constexpr int kOffPer = 4;  // counts per thread and chunk pass
 // every CTA scans its chunk of the counts, a grid barrier publishes the
 // chunk totals, each CTA adds its base and writes the offsets, a second
 // barrier, then the scatter (slot ids at offset + arrival rank; every
-// Gaussian with more than kShortSeg contributions queued once).  Barrier
-// targets start at bar_base (arrivals already counted by the caller); the
-// last CTA out resets the counters for the next launch.
-__device__ __forceinline__ void offsets_scatter_body(const OffArgs& A, unsigned bar_base) {
+// Gaussian with more than kShortSeg contributions queued once); in bucket
+// mode only the overflow entries (see kBucket).  Barrier targets start at
+// bar_base (arrivals already counted by the caller); returns the target
+// reached.  The launch ends with grid_exit, which resets the counters.
+__device__ __forceinline__ unsigned offsets_scatter_body(const OffArgs& A, unsigned bar_base) {
     __shared__ uint32_t s_base;
     const uint32_t* __restrict__ gcnt = A.gcnt;
     const uint32_t n = A.n;
@@ -60,12 +62,7 @@ __device__ __forceinline__ void offsets_scatter_body(const OffArgs& A, unsigned 
                 perm[__ldcg(goff + keys[slot]) + pos] = slot;
             }
         }
-        __syncthreads();
-        if (threadIdx.x == 0 && atomicAdd(bar + 1, 1u) == G - 1) {
-            bar[0] = 0;
-            bar[1] = 0;
-        }
-        return;
+        return no ? bar_base + G : bar_base;
     }
     // chunk of CTA b: [b * per_cta, (b + 1) * per_cta), per_cta a multiple of kOffThreads * kOffPer
     const uint32_t tile = kOffThreads * kOffPer;
@@ -127,10 +124,139 @@ __device__ __forceinline__ void offsets_scatter_body(const OffArgs& A, unsigned 
         perm[__ldcg(goff + g) + pos] = slot;  // (written by other CTAs: read through L2)
         if (pos == 0 && gcnt[g] > kShortSeg) long_list[atomicAdd(long_count, 1u)] = g;
     }
+    return bar_base + 2 * G;
+}
+
+// The end of a persistent launch that used grid barriers on bar: the last
+// CTA out resets the counters for the next launch.
+__device__ __forceinline__ void grid_exit(unsigned* bar) {
     __syncthreads();
-    if (threadIdx.x == 0 && atomicAdd(bar + 1, 1u) == G - 1) {
+    if (threadIdx.x == 0 && atomicAdd(bar + 1, 1u) == gridDim.x - 1) {
         bar[0] = 0;
         bar[1] = 0;
+    }
+}
+
+// Long segments: one CTA (kLongThreads threads) per queued Gaussian,
+// CTAs first, first + stride, ...  The slot ids are put in slot (= sample)
+// order in shared memory: up to kLongRank by counting ranks (rank = number
+// of smaller ids; ids are distinct), up to kLongCap by a bitonic sort, and
+// beyond shared memory by ranks straight from global memory into `big`;
+// then 8 threads, one per parameter, accumulate the contribution rows in
+// that order, kLongRows rows gathered ahead of the dependent adds.
+constexpr uint32_t kLongCap = 2048;
+constexpr uint32_t kLongRank = 256;  // up to here: rank by counting; above: bitonic sort
+constexpr int kLongThreads = 256;
+constexpr int kLongRows = 128;
+constexpr uint32_t kLossCtas = 8;    // CTAs that form the loss
+
+__device__ __forceinline__ void long_segments(const LongArgs& A, uint32_t first, uint32_t stride) {
+    __shared__ uint32_t keys[kLongCap];
+    __shared__ uint32_t sorted[kLongRank];
+    __shared__ double rows[kLongRows][8];
+    const uint32_t total = *(volatile const uint32_t*)A.long_count;
+    const int t = threadIdx.x;
+    for (uint32_t it = first; it < total; it += stride) {
+        const uint32_t g = A.long_list[it];
+        const uint32_t m = A.gcnt[g], o = A.goff[g];
+        // slot id of rank e: bucket mode keeps ranks < kBucket in the bucket
+        auto slot_at = [&](uint32_t e) {
+            return A.bucket && e < kBucket ? A.bucket[(size_t)g * kBucket + e] : A.perm[o + e];
+        };
+        const uint32_t* out = sorted;
+        __syncthreads();
+        if (m <= kLongRank) {
+            for (uint32_t e = t; e < m; e += kLongThreads) keys[e] = slot_at(e);
+            __syncthreads();
+            for (uint32_t e = t; e < m; e += kLongThreads) {
+                const uint32_t v = keys[e];
+                uint32_t r = 0;
+                for (uint32_t j = 0; j < m; ++j) r += keys[j] < v;
+                sorted[r] = v;
+            }
+        } else if (m <= kLongCap) {
+            // bitonic sort in shared memory, padded to a power of two
+            uint32_t pow2 = 1;
+            while (pow2 < m) pow2 <<= 1;
+            for (uint32_t e = t; e < pow2; e += kLongThreads) keys[e] = e < m ? slot_at(e) : 0xFFFFFFFFu;
+            __syncthreads();
+            for (uint32_t size = 2; size <= pow2; size <<= 1)
+                for (uint32_t stride2 = size >> 1; stride2 > 0; stride2 >>= 1) {
+                    for (uint32_t e = t; e < pow2; e += kLongThreads) {
+                        const uint32_t partner = e ^ stride2;
+                        if (partner > e) {
+                            const bool up = (e & size) == 0;
+                            const uint32_t a = keys[e], b = keys[partner];
+                            if ((a > b) == up) {
+                                keys[e] = b;
+                                keys[partner] = a;
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            out = keys;
+        } else {
+            // beyond shared memory (degenerate sets): rank from global
+            // memory into the same range of a second slot array
+            for (uint32_t e = t; e < m; e += kLongThreads) {
+                const uint32_t v = slot_at(e);
+                uint32_t r = 0;
+                for (uint32_t j = 0; j < m; ++j) r += slot_at(j) < v;
+                A.big[o + r] = v;
+            }
+            out = A.big + o;
+        }
+        __syncthreads();
+        double acc = 0.0;
+        for (uint32_t base = 0; base < m; base += kLongRows) {
+            const uint32_t cnt = min((uint32_t)kLongRows, m - base);
+            if ((uint32_t)t < cnt) {
+                const double2* c = reinterpret_cast<const double2*>(A.contrib + (size_t)out[base + t] * 8);
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const double2 v = c[h];
+                    rows[t][2 * h] = v.x;
+                    rows[t][2 * h + 1] = v.y;
+                }
+            }
+            __syncthreads();
+            if (t < 8)
+                for (uint32_t r = 0; r < cnt; ++r) acc = __dadd_rn(acc, rows[r][t]);
+            __syncthreads();
+        }
+        if (t < 8) {
+            A.grads[(size_t)g * 8 + t] = acc;
+            if (!isfinite(acc)) atomicMin(A.status, (long long)g * 8 + t);  // adam.cpp:29-31 (first (i, p))
+        }
+    }
+}
+
+// The loss (fit.cpp:87-89: mean of the per-sample L1 losses): chunk c of
+// kLossCtas summed by one CTA (kLongThreads threads, a fixed tree), the
+// chunks combined in order by whichever CTA finishes last.
+__device__ __forceinline__ void loss_chunk(const LongArgs& A, uint32_t c) {
+    __shared__ double red[kLongThreads];
+    const int t = threadIdx.x;
+    const uint32_t per = (A.ns + kLossCtas - 1) / kLossCtas, l0 = c * per, l1 = min(A.ns, l0 + per);
+    double acc = 0.0;
+    for (uint32_t i = l0 + t; i < l1; i += kLongThreads) acc = __dadd_rn(acc, A.losses[i]);
+    red[t] = acc;
+    __syncthreads();
+    for (int s = kLongThreads / 2; s > 0; s >>= 1) {
+        if (t < s) red[t] = __dadd_rn(red[t], red[t + s]);
+        __syncthreads();
+    }
+    if (t == 0) {
+        A.loss_part[c] = red[0];
+        __threadfence();
+        if (atomicAdd(A.loss_ticket, 1u) == kLossCtas - 1) {
+            __threadfence();
+            double l = 0.0;
+            for (uint32_t k = 0; k < kLossCtas; ++k) l = __dadd_rn(l, __ldcg(A.loss_part + k));
+            *A.dloss = __dmul_rn(l, A.inv_n);
+            *A.loss_ticket = 0;
+        }
     }
 }
 

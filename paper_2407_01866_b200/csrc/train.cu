@@ -170,6 +170,7 @@ __global__ void scatter_slots_kernel(const uint32_t* __restrict__ keys, uint32_t
 __global__ void __launch_bounds__(kOffThreads) offsets_scatter_kernel(OffArgs A) {
     pdl_wait();
     offsets_scatter_body(A, 0);
+    grid_exit(A.bar);
 }
 
 __device__ __forceinline__ void sum_row(const double* __restrict__ contrib, uint32_t slot, double* acc) {
@@ -250,143 +251,18 @@ __global__ void segment_sum_kernel(const uint32_t* __restrict__ gcnt, const uint
     store_grad(grads, g, acc, status);
 }
 
-// One CTA per long segment (persistent over the queue).  The slot ids are
-// put in slot (= sample) order in shared memory: up to 256 by counting ranks
-// (rank = number of smaller ids; ids are distinct -- two barriers), larger
-// by a bitonic sort; then 8 threads, one per parameter, accumulate the
-// contribution rows in that order with the row loads issued ahead of the
-// dependent adds.  Segments beyond the shared capacity rank straight from
-// global memory.
-constexpr uint32_t kLongCap = 2048;
-constexpr uint32_t kLongRank = 256;  // up to here: rank by counting; above: bitonic sort
-constexpr int kLongThreads = 256;
-constexpr uint32_t kLossCtas = 8;  // long_segment_kernel CTAs that form the loss
-
-__global__ void __launch_bounds__(kLongThreads) long_segment_kernel(const uint32_t* __restrict__ gcnt,
-                                                                    const uint32_t* __restrict__ goff,
-                                                                    uint32_t* __restrict__ perm,
-                                                                    const double* __restrict__ contrib,
-                                                                    double* __restrict__ grads,
-                                                                    const uint32_t* __restrict__ long_count,
-                                                                    const uint32_t* __restrict__ long_list,
-                                                                    long long* __restrict__ status,
-                                                                    uint32_t* __restrict__ big,
-                                                                    const double* __restrict__ losses,
-                                                                    uint32_t ns, double inv_n,
-                                                                    double* __restrict__ dloss,
-                                                                    double* __restrict__ loss_part,
-                                                                    unsigned* __restrict__ loss_ticket,
-                                                                    const uint32_t* __restrict__ bucket) {
+// One CTA per long segment, and the loss: reduce.cuh (long_segments,
+// loss_chunk); this launch is the path where the search's hard-point launch
+// does not take them over.
+__global__ void __launch_bounds__(kLongThreads) long_segment_kernel(LongArgs A) {
     pdl_wait();
-    __shared__ uint32_t keys[kLongCap];
-    __shared__ uint32_t sorted[kLongCap];
-    __shared__ double rows[kLongThreads][8];
-    const uint32_t total = *long_count;
-    const int t = threadIdx.x;
-    if (dloss && blockIdx.x >= gridDim.x - kLossCtas) {
-        // the loss (fit.cpp:87-89: mean of the per-sample L1 losses) by the
-        // last kLossCtas CTAs while the others take the long segments: chunk
-        // c summed by CTA c (a fixed tree), the chunks combined in order by
-        // whichever finishes last
-        const uint32_t c = blockIdx.x - (gridDim.x - kLossCtas);
-        const uint32_t per = (ns + kLossCtas - 1) / kLossCtas, l0 = c * per, l1 = min(ns, l0 + per);
-        double acc = 0.0;
-        for (uint32_t i = l0 + t; i < l1; i += kLongThreads) acc = __dadd_rn(acc, losses[i]);
-        double* sm = &rows[0][0];
-        sm[t] = acc;
-        __syncthreads();
-        for (int s = kLongThreads / 2; s > 0; s >>= 1) {
-            if (t < s) sm[t] = __dadd_rn(sm[t], sm[t + s]);
-            __syncthreads();
-        }
-        if (t == 0) {
-            loss_part[c] = sm[0];
-            __threadfence();
-            if (atomicAdd(loss_ticket, 1u) == kLossCtas - 1) {
-                __threadfence();
-                double l = 0.0;
-                for (uint32_t k = 0; k < kLossCtas; ++k) l = __dadd_rn(l, __ldcg(loss_part + k));
-                *dloss = __dmul_rn(l, inv_n);
-                *loss_ticket = 0;
-            }
-        }
+    if (A.dloss && blockIdx.x >= gridDim.x - kLossCtas) {
+        // the last kLossCtas CTAs form the loss while the others take the
+        // long segments
+        loss_chunk(A, blockIdx.x - (gridDim.x - kLossCtas));
+        return;
     }
-    for (uint32_t it = blockIdx.x; it < total; it += gridDim.x) {
-        const uint32_t g = long_list[it];
-        const uint32_t m = gcnt[g], o = goff[g];
-        // slot id of rank e: bucket mode keeps ranks < kBucket in the bucket
-        auto slot_at = [&](uint32_t e) {
-            return bucket && e < kBucket ? bucket[(size_t)g * kBucket + e] : perm[o + e];
-        };
-        const uint32_t* out = sorted;
-        __syncthreads();
-        if (m <= kLongRank) {
-            for (uint32_t e = t; e < m; e += kLongThreads) keys[e] = slot_at(e);
-            __syncthreads();
-            for (uint32_t e = t; e < m; e += kLongThreads) {
-                const uint32_t v = keys[e];
-                uint32_t r = 0;
-                for (uint32_t j = 0; j < m; ++j) r += keys[j] < v;
-                sorted[r] = v;
-            }
-        } else if (m <= kLongCap) {
-            // bitonic sort in shared memory, padded to a power of two
-            uint32_t pow2 = 1;
-            while (pow2 < m) pow2 <<= 1;
-            for (uint32_t e = t; e < pow2; e += kLongThreads) keys[e] = e < m ? slot_at(e) : 0xFFFFFFFFu;
-            __syncthreads();
-            for (uint32_t size = 2; size <= pow2; size <<= 1)
-                for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-                    for (uint32_t e = t; e < pow2; e += kLongThreads) {
-                        const uint32_t partner = e ^ stride;
-                        if (partner > e) {
-                            const bool up = (e & size) == 0;
-                            const uint32_t a = keys[e], b = keys[partner];
-                            if ((a > b) == up) {
-                                keys[e] = b;
-                                keys[partner] = a;
-                            }
-                        }
-                    }
-                    __syncthreads();
-                }
-            out = keys;
-        } else {
-            // beyond shared memory (degenerate sets): rank from global
-            // memory into the same range of a second slot array
-            for (uint32_t e = t; e < m; e += kLongThreads) {
-                const uint32_t v = slot_at(e);
-                uint32_t r = 0;
-                for (uint32_t j = 0; j < m; ++j) r += slot_at(j) < v;
-                big[o + r] = v;
-            }
-            out = big + o;
-        }
-        __syncthreads();
-        // chunks of rows gathered by all threads (loads in flight together),
-        // then summed in order by thread p < 8 (parameter p)
-        double acc = 0.0;
-        for (uint32_t base = 0; base < m; base += kLongThreads) {
-            const uint32_t cnt = min((uint32_t)kLongThreads, m - base);
-            if ((uint32_t)t < cnt) {
-                const double2* c = reinterpret_cast<const double2*>(contrib + (size_t)out[base + t] * 8);
-#pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                    const double2 v = c[h];
-                    rows[t][2 * h] = v.x;
-                    rows[t][2 * h + 1] = v.y;
-                }
-            }
-            __syncthreads();
-            if (t < 8)
-                for (uint32_t r = 0; r < cnt; ++r) acc = __dadd_rn(acc, rows[r][t]);
-            __syncthreads();
-        }
-        if (t < 8) {
-            grads[(size_t)g * 8 + t] = acc;
-            if (!isfinite(acc)) atomicMin(status, (long long)g * 8 + t);  // adam.cpp:29-31 (first (i, p))
-        }
-    }
+    long_segments(A, blockIdx.x, A.dloss ? gridDim.x - kLossCtas : gridDim.x);
 }
 
 // Multi-rank exchange: per-Gaussian counts over every rank's contributions,
@@ -974,7 +850,7 @@ int igs_status_reset(igs_ctx* ctx) {
 // barrier counters [0, 2) + chunk totals of the persistent offsets launch
 // (one CTA per SM), zeroed once
 static uint32_t* off_ctl(igs_ctx* ctx) {
-    uint32_t* ctl = (uint32_t*)igs_scratch(ctx, 34, ((size_t)ctx->sm_count + 2) * sizeof(uint32_t));
+    uint32_t* ctl = (uint32_t*)igs_scratch(ctx, 34, ((size_t)kOffCtasPerSm * ctx->sm_count + 2) * sizeof(uint32_t));
     if (ctl && !ctx->off_ctl_ready) {
         if (cudaMemsetAsync(ctl, 0, 2 * sizeof(uint32_t), ctx->stream) != cudaSuccess) return nullptr;
         ctx->off_ctl_ready = true;
@@ -988,6 +864,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
     if (fused) *fused = false;
     ctx->fuse_off.ready = false;
     ctx->fuse_off.done = false;
+    ctx->fuse_off.fuse_long = false;
     const uint32_t n = ctx->n;
     const int kk = (int)std::min<uint32_t>((uint32_t)k, n);
     const bool knn_path = ctx->opt_cull && kk <= 32;
@@ -1006,7 +883,15 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
     double* contrib = nullptr;
     uint32_t *keys = nullptr, *gcnt = nullptr, *goff = nullptr, *perm = nullptr, *long_ctl = nullptr;
     // segment buckets, when the search files them (reduce.cuh)
-    uint32_t *bucket = nullptr, *ovf = nullptr, *ovf_list = nullptr;
+    uint32_t *bucket = nullptr, *ovf = nullptr, *ovf_list = nullptr, *big = nullptr;
+    double* loss_part = nullptr;
+    bool long_fused = false;  // the long segments + loss ran in the search's hard-point launch
+    auto long_args = [&]() {
+        return LongArgs{(const uint32_t*)gcnt, (const uint32_t*)goff, (const uint32_t*)perm, (const double*)contrib,
+                        ctx->grads, (const uint32_t*)(bucket ? ovf + 2 : long_ctl), (const uint32_t*)(long_ctl + 1),
+                        ctx->status, big, (const double*)losses, ns_all, inv_n, mode == 0 ? dev_loss : nullptr,
+                        loss_part, (unsigned*)(loss_part + kLossCtas), (const uint32_t*)bucket};
+    };
     bool gcnt_filled = false;
     if (ctx->opt_deterministic) {
         contrib = (double*)igs_scratch(ctx, 3, items * 8 * sizeof(double));
@@ -1015,8 +900,15 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
         goff = (uint32_t*)igs_scratch(ctx, 6, (size_t)n * sizeof(uint32_t));
         perm = (uint32_t*)igs_scratch(ctx, 7, items * sizeof(uint32_t));
         long_ctl = (uint32_t*)igs_scratch(ctx, 24, ((size_t)n + 1) * sizeof(uint32_t));
-        if (!contrib || !keys || !gcnt || !goff || !perm || !long_ctl)
+        big = (uint32_t*)igs_scratch(ctx, 32, items * sizeof(uint32_t));
+        // loss partials + the combining ticket (zeroed once; the last CTA re-zeroes it)
+        loss_part = (double*)igs_scratch(ctx, 35, kLossCtas * sizeof(double) + 16);
+        if (!contrib || !keys || !gcnt || !goff || !perm || !long_ctl || !big || !loss_part)
             return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
+        if (!ctx->loss_ticket_ready) {
+            IGS_CUDA(ctx, cudaMemsetAsync(loss_part + kLossCtas, 0, 16, ctx->stream));
+            ctx->loss_ticket_ready = true;
+        }
         // counters | cursors: the fused Adam leaves them zeroed for the next step
         if (ctx->gcnt_clean != gcnt || ctx->gcnt_clean_n != n)
             IGS_CUDA(ctx, cudaMemsetAsync(gcnt, 0, (size_t)n * 2 * sizeof(uint32_t), ctx->stream));
@@ -1071,6 +963,8 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
                 ctx->fuse_off.args.ovf = ovf;
                 ctx->fuse_off.args.ovf_list = ovf_list;
                 ctx->fuse_off.args.long_count = ovf + 2;
+                ctx->fuse_off.long_args = long_args();
+                ctx->fuse_off.fuse_long = getenv("IGS_LONG_LAUNCH") == nullptr;  // (A/B: the separate launch)
             }
         }
         e = igs_knn_forward_backward(ctx, mode, dev_sidx, dev_samples5, ns, kk, inv_n, losses + (size_t)rk * ns,
@@ -1080,6 +974,8 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
         ctx->stage_job = StageJob{};
         ctx->fuse_off.ready = false;
         ctx->fuse_off.bucket = nullptr;
+        long_fused = ctx->fuse_off.done && ctx->fuse_off.fuse_long;
+        ctx->fuse_off.fuse_long = false;
         if (e) return e;
         gcnt_filled = !exch;
     } else {
@@ -1149,20 +1045,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
                     (uint32_t)items, n, (const uint32_t*)goff, (const uint32_t*)gcnt, gcnt + n, perm, long_ctl,
                     long_ctl + 1);
         }
-        uint32_t* big = (uint32_t*)igs_scratch(ctx, 32, items * sizeof(uint32_t));
-        if (!big) return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
-        // loss partials + the combining ticket (zeroed once; the last CTA re-zeroes it)
-        double* loss_part = (double*)igs_scratch(ctx, 35, kLossCtas * sizeof(double) + 16);
-        if (!loss_part) return igs_fail(ctx, IGS_E_CUDA, "out of device memory");
-        if (!ctx->loss_ticket_ready) {
-            IGS_CUDA(ctx, cudaMemsetAsync(loss_part + kLossCtas, 0, 16, ctx->stream));
-            ctx->loss_ticket_ready = true;
-        }
-        IGS_PDL(ctx, long_segment_kernel, 8 * ctx->sm_count, kLongThreads, 0, (const uint32_t*)gcnt,
-                (const uint32_t*)goff, perm, (const double*)contrib, ctx->grads,
-                (const uint32_t*)(bucket ? ovf + 2 : long_ctl),
-                (const uint32_t*)(long_ctl + 1), ctx->status, big, (const double*)losses, ns_all, inv_n,
-                mode == 0 ? dev_loss : nullptr, loss_part, (unsigned*)(loss_part + kLossCtas), (const uint32_t*)bucket);
+        if (!long_fused) IGS_PDL(ctx, long_segment_kernel, 8 * ctx->sm_count, kLongThreads, 0, long_args());
         if (fuse_lr4 && (exch || !igs_has_comm(ctx))) {
             // short segments summed inside the Adam kernel (one pass over the set)
             const double bc1 = 1.0 - std::pow(0.9, (double)t);  // adam.cpp:16-17, host libm

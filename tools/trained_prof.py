@@ -30,4 +30,5 @@ for s in range(20):
 c.sync()
 prof = {PROF_NAMES[f]: c.profile_read(f) for f in range(len(PROF_NAMES))}
 print(json.dumps({"bucket": os.environ.get("IGS_NO_BUCKET") is None, "ms_per_step": sum(ms) / len(ms), "counts": hist,
-                  "per_family_us": {k: round(v[0] / 20 * 1e3, 1) for k, v in prof.items() if v[1]}}))
+                  "per_family_us": {k: round(v[0] / 20 * 1e3, 1) for k, v in prof.items() if v[1]},
+                  "raw": {k: v for k, v in prof.items()}}))
