@@ -129,7 +129,6 @@ __global__ void lq_fill(const ScanRec* __restrict__ scan, uint32_t n, const uint
     mrec[pos] = r;  // the records in member order (the searches' evaluation stream)
     minv[i] = pos;
     mcell[pos] = k;
-    acc_add(acc + k, r);
 }
 
 // A full re-bucketing in one persistent launch (one CTA per SM, all
@@ -230,63 +229,11 @@ __global__ void __launch_bounds__(kBuildThreads) lq_build_kernel(
         mrec[pos] = r;
         minv[i] = pos;
         mcell[pos] = k;
-        acc_add(acc + k, r);
     }
     __syncthreads();
     if (threadIdx.x == 0 && atomicAdd(bar + 1, 1u) == G - 1) {
         bar[0] = 0;
         bar[1] = 0;
-    }
-}
-
-// Refit, step 1: every cell's accumulator from the member-ordered records
-// (kept current by the Adam launches, tree_acc_add), one thread per member
-// position.  Members of a cell are contiguous, so a warp min/max-reduces its
-// runs of equal cells with shuffles (min/max are idempotent, so overlapping
-// windows are harmless) and the first lane of each run writes it: a plain
-// store when the whole cell lies inside this warp's 32 positions, the
-// order-preserving atomics otherwise (a cell spanning warps; lq_tree_kernel
-// resets those accumulators after reading them, as after a build).
-__global__ void __launch_bounds__(256) lq_own_kernel(const ScanRec* __restrict__ mrec,
-                                                     const uint32_t* __restrict__ mcell,
-                                                     const uint32_t* __restrict__ off,
-                                                     const uint32_t* __restrict__ cnt, uint32_t n,
-                                                     Acc* __restrict__ acc) {
-    pdl_wait();
-    const uint32_t p = blockIdx.x * 256 + threadIdx.x;
-    const int lane = threadIdx.x & 31;
-    const uint32_t c = p < n ? mcell[p] : ~0u;
-    Acc a = acc_empty();
-    if (p < n) acc_add_local(a, mrec[p]);
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t yc = __shfl_down_sync(0xffffffffu, c, o);
-        const unsigned x0 = __shfl_down_sync(0xffffffffu, a.x0, o), y0 = __shfl_down_sync(0xffffffffu, a.y0, o);
-        const unsigned x1 = __shfl_down_sync(0xffffffffu, a.x1, o), y1 = __shfl_down_sync(0xffffffffu, a.y1, o);
-        const unsigned lm = __shfl_down_sync(0xffffffffu, a.lmin, o);
-        const unsigned an = __shfl_down_sync(0xffffffffu, a.aniso, o);
-        if (lane + o < 32 && yc == c) {
-            a.x0 = min(a.x0, x0);
-            a.y0 = min(a.y0, y0);
-            a.x1 = max(a.x1, x1);
-            a.y1 = max(a.y1, y1);
-            a.lmin = min(a.lmin, lm);
-            a.aniso = max(a.aniso, an);
-        }
-    }
-    const uint32_t pc = __shfl_up_sync(0xffffffffu, c, 1);
-    if (c == ~0u || (lane > 0 && pc == c)) return;  // not the first lane of a run
-    const uint32_t base = p - (uint32_t)lane, o0 = off[c];
-    if (o0 >= base && o0 + cnt[c] <= base + 32) {
-        acc[c] = a;
-    } else {
-        Acc* d = acc + c;
-        atomicMin(&d->x0, a.x0);
-        atomicMin(&d->y0, a.y0);
-        atomicMax(&d->x1, a.x1);
-        atomicMax(&d->y1, a.y1);
-        atomicMin(&d->lmin, a.lmin);
-        atomicMax(&d->aniso, a.aniso);
     }
 }
 
@@ -310,14 +257,13 @@ __device__ __forceinline__ void merge(Sum& a, const Sum& b) {
     a.count += b.count;
 }
 
-// Own summary of cell c from its accumulator, which is reset for the next
-// round of accumulation (lq_fill or the Adam kernels).
+// Own summary of cell c from its accumulator (written by another CTA of
+// lq_tree_kernel).
 __device__ __forceinline__ Sum own_of(Acc* __restrict__ acc, const uint32_t* __restrict__ cnt, uint32_t c) {
     Sum s = empty_sum();
     const uint32_t m = cnt[c];
     if (m == 0) return s;
-    const Acc a = acc[c];
-    acc[c] = acc_empty();
+    const Acc a = acc_ldcg(acc + c);  // (written by another CTA)
     s.x0 = odec(a.x0);
     s.y0 = odec(a.y0);
     s.x1 = odec(a.x1);
@@ -328,17 +274,35 @@ __device__ __forceinline__ Sum own_of(Acc* __restrict__ acc, const uint32_t* __r
     return s;
 }
 
-// All own + subtree summaries in one launch.  CTA (bx, by) owns a 16 x 16
-// block of level-0 cells and builds levels 0..4 of that block in shared
-// memory (subtree = own + the four children); the last CTA to finish (atomic
-// ticket after a fence) builds the levels above.  Every own summary a
-// thread needs is fetched up front (all levels at once), so a CTA waits on
-// memory twice rather than twice per level.
+// All own + subtree summaries in one launch, from the member-ordered
+// records (mrec, kept current by the Adam launches) -- no per-Gaussian
+// atomics anywhere.  CTA (bx, by) owns a 16 x 16 block of level-0 cells and
+// levels 0..4 above it (341 cells, 31 rows of cells).  A row's members are
+// one contiguous range of mrec (members are ordered by cell), so the CTA
+// walks the concatenation of its 31 ranges, one member per thread: each
+// warp min/max-reduces its runs of equal cells with shuffles (min/max are
+// idempotent, so overlapping windows are harmless) and the first lane of a
+// run folds it into the cell's shared-memory accumulator (shared atomics:
+// runs can span warps).  Then the summaries level by level (subtree = own +
+// the four children).  The members of the levels above 4 (large Gaussians)
+// are split evenly over all CTAs and folded into global accumulators the
+// same way; the last CTA to finish (atomic ticket after a fence) reads them
+// (resetting them for the next launch) and builds the levels above.
 constexpr int kBlk = 16;
-constexpr int kInLv = 5;     // levels 0..4 live inside a block
+constexpr int kInLv = 5;       // levels 0..4 live inside a block
+constexpr int kTileRows = 31;  // 16 + 8 + 4 + 2 + 1
+constexpr int kTileCells = 341;
 constexpr int kUpCells = 341;  // 16^2 + 8^2 + 4^2 + 2^2 + 1: upper levels kept in shared memory
+#ifndef IGS_KWALK
+#define IGS_KWALK 1
+#endif
+constexpr int kWalk = IGS_KWALK;  // member-walk loads in flight per thread
+#ifndef IGS_TREE_THREADS
+#define IGS_TREE_THREADS 256
+#endif
+constexpr int kTreeThreads = IGS_TREE_THREADS;  // >= 256 (the level-0 block)
 
-// own summary from prefetched (count, accumulator); resets the accumulator
+// own summary from (count, accumulator)
 __device__ __forceinline__ Sum own_from(uint32_t m, const Acc& a) {
     Sum s = empty_sum();
     if (m == 0) return s;
@@ -352,26 +316,69 @@ __device__ __forceinline__ Sum own_from(uint32_t m, const Acc& a) {
     return s;
 }
 
-__global__ void __launch_bounds__(256) lq_tree_kernel(Acc* __restrict__ acc, Lq L,
+// Warp step of the member walk: lane holds (key, a) -- key ~0u for no
+// member; runs of equal keys are contiguous.  Returns true in the first
+// lane of each run, whose a then covers the whole run within the warp.
+__device__ __forceinline__ bool warp_runs(uint32_t key, Acc& a) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t yk = __shfl_down_sync(0xffffffffu, key, o);
+        const unsigned x0 = __shfl_down_sync(0xffffffffu, a.x0, o), y0 = __shfl_down_sync(0xffffffffu, a.y0, o);
+        const unsigned x1 = __shfl_down_sync(0xffffffffu, a.x1, o), y1 = __shfl_down_sync(0xffffffffu, a.y1, o);
+        const unsigned lm = __shfl_down_sync(0xffffffffu, a.lmin, o);
+        const unsigned an = __shfl_down_sync(0xffffffffu, a.aniso, o);
+        if (lane + o < 32 && yk == key) {
+            a.x0 = min(a.x0, x0);
+            a.y0 = min(a.y0, y0);
+            a.x1 = max(a.x1, x1);
+            a.y1 = max(a.y1, y1);
+            a.lmin = min(a.lmin, lm);
+            a.aniso = max(a.aniso, an);
+        }
+    }
+    const uint32_t pk = __shfl_up_sync(0xffffffffu, key, 1);
+    return key != ~0u && (lane == 0 || pk != key);
+}
+
+__device__ __forceinline__ void acc_fold(Acc* d, const Acc& a) {
+    atomicMin(&d->x0, a.x0);
+    atomicMin(&d->y0, a.y0);
+    atomicMax(&d->x1, a.x1);
+    atomicMax(&d->y1, a.y1);
+    atomicMin(&d->lmin, a.lmin);
+    atomicMax(&d->aniso, a.aniso);
+}
+
+__global__ void __launch_bounds__(kTreeThreads) lq_tree_kernel(const ScanRec* __restrict__ mrec,
+                                                      const uint32_t* __restrict__ mcell,
+                                                      const uint32_t* __restrict__ off, uint32_t n,
+                                                      Acc* __restrict__ acc, Lq L,
                                                       const uint32_t* __restrict__ cnt, Sum* __restrict__ own,
                                                       Sum* __restrict__ sub, unsigned int* __restrict__ ticket,
                                                       L2Prefetch pf, StageJob job, int full) {
     __shared__ Sum sm[2][kBlk * kBlk];
     __shared__ Sum up[kUpCells];
+    __shared__ Acc s_acc[kTileCells];
     __shared__ int s_loff[kMaxLv];
+    // per tile row: first cell, first member, local index of the first cell,
+    // and the row's start in the concatenated walk (s_v0[kTileRows] = total)
+    __shared__ uint32_t s_c0[kTileRows], s_p0[kTileRows], s_l0[kTileRows], s_v0[kTileRows + 1];
     const int t = threadIdx.x;
     if (t == 0) {
 #pragma unroll
         for (int l = 0; l < kMaxLv; ++l) s_loff[l] = L.loff[l];
     }
+    for (int i = t; i < kTileCells; i += kTreeThreads) s_acc[i] = acc_empty();
+    __syncthreads();
     const int nb = L.G0 / kBlk;  // G0 is a power of two >= 16
     const int bx = blockIdx.x % nb, by = blockIdx.x / nb;
     pdl_wait();
-    stage_job_run(job, blockIdx.x * 256 + t, gridDim.x * 256);  // the iteration's start (StageJob)
-    prefetch_l2(pf, blockIdx.x * 256 + t, gridDim.x * 256);  // the search's inputs
-    // prefetch: the cell this thread owns at each in-block level
+    stage_job_run(job, blockIdx.x * kTreeThreads + t, gridDim.x * kTreeThreads);  // the iteration's start (StageJob)
+    prefetch_l2(pf, blockIdx.x * kTreeThreads + t, gridDim.x * kTreeThreads);  // the search's inputs
+    // the counts of the cells this thread owns at each in-block level, and
+    // (threads < 31) one row's member range -- one round trip
     uint32_t cell[kInLv], m[kInLv];
-    Acc a[kInLv];
 #pragma unroll
     for (int l = 0; l < kInLv; ++l) {
         const int side = kBlk >> l, G = L.G0 >> l;
@@ -383,15 +390,59 @@ __global__ void __launch_bounds__(256) lq_tree_kernel(Acc* __restrict__ acc, Lq 
             m[l] = cnt[cell[l]];
         }
     }
-    // (an empty cell's accumulator holds acc_empty(): loaded unconditionally,
-    // the counts and accumulators arrive in one round trip)
+    uint32_t rlen = 0;
+    if (t < kTileRows) {
+        int l = 0, r = t, lbase = 0;
+        while (r >= (kBlk >> l)) {
+            r -= kBlk >> l;
+            lbase += (kBlk >> l) * (kBlk >> l);
+            ++l;
+        }
+        const int side = kBlk >> l, G = L.G0 >> l;
+        const uint32_t c0 = (uint32_t)(s_loff[l] + (by * side + r) * G + bx * side), c1 = c0 + side - 1;
+        const uint32_t p0 = off[c0];
+        rlen = off[c1] + cnt[c1] - p0;
+        s_c0[t] = c0;
+        s_p0[t] = p0;
+        s_l0[t] = (uint32_t)(lbase + r * side);
+    }
+    if (t < 32) {  // exclusive scan of the row lengths (warp 0)
+        uint32_t x = rlen;
 #pragma unroll
-    for (int l = 0; l < kInLv; ++l)
-        if (cell[l] != ~0u) a[l] = acc[cell[l]];
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (t >= o) x += y;
+        }
+        if (t <= kTileRows) s_v0[t] = x - rlen;  // (t == kTileRows: rlen 0, the total)
+    }
+    __syncthreads();
+    // the members, one per thread, kWalk batches of loads in flight (whole
+    // warps iterate alike)
+    const uint32_t total = s_v0[kTileRows];
+    for (uint32_t vb = 0; vb < total; vb += kTreeThreads * kWalk) {
+        uint32_t key[kWalk];
+        Acc a[kWalk];
 #pragma unroll
-    for (int l = 0; l < kInLv; ++l)
-        if (m[l]) acc[cell[l]] = acc_empty();  // ready for the next accumulation
-    int cur = 0;
+        for (int u = 0; u < kWalk; ++u) {
+            const uint32_t v = vb + kTreeThreads * u + t;
+            key[u] = ~0u;
+            a[u] = acc_empty();
+            if (v < total) {
+                int r = 0;  // the row holding walk position v (last start <= v)
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1)
+                    if (r + step < kTileRows && s_v0[r + step] <= v) r += step;
+                const uint32_t p = s_p0[r] + (v - s_v0[r]);
+                key[u] = s_l0[r] + (mcell[p] - s_c0[r]);
+                acc_add_local(a[u], mrec[p]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kWalk; ++u)
+            if (vb + kTreeThreads * u < total && warp_runs(key[u], a[u])) acc_fold(&s_acc[key[u]], a[u]);
+    }
+    __syncthreads();
+    int cur = 0, lbase = 0;
 #pragma unroll
     for (int l = 0; l < kInLv; ++l) {
         const int side = kBlk >> l;
@@ -399,7 +450,7 @@ __global__ void __launch_bounds__(256) lq_tree_kernel(Acc* __restrict__ acc, Lq 
             // a cell with no members, or a subtree with none, stays empty
             // between builds (membership only changes at a build): after the
             // build's full pass a refit writes only the others
-            const Sum o = own_from(m[l], a[l]);
+            const Sum o = own_from(m[l], s_acc[lbase + t]);
             if (full || m[l]) own[cell[l]] = o;
             Sum s = o;
             if (l > 0) {
@@ -412,29 +463,64 @@ __global__ void __launch_bounds__(256) lq_tree_kernel(Acc* __restrict__ acc, Lq 
         }
         __syncthreads();
         cur ^= 1;
+        lbase += side * side;
     }
     if (L.levels <= kInLv) return;
+    // the cells of the levels above (large Gaussians; few cells, possibly
+    // many members each): cell by cell over the CTAs, each cell's members
+    // reduced by the whole CTA into its global accumulator (plain store)
+    {
+        __shared__ Acc s_wacc[kTreeThreads / 32];
+        const uint32_t cu0 = (uint32_t)s_loff[kInLv], cu1 = (uint32_t)s_loff[L.levels - 1] + 1;
+        for (uint32_t c = cu0 + blockIdx.x; c < cu1; c += gridDim.x) {
+            const uint32_t mc = cnt[c];
+            if (mc == 0) continue;  // (uniform)
+            const uint32_t p0 = off[c];
+            Acc a = acc_empty();
+            for (uint32_t e = t; e < mc; e += kTreeThreads) acc_add_local(a, mrec[p0 + e]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                a.x0 = min(a.x0, __shfl_xor_sync(0xffffffffu, a.x0, o));
+                a.y0 = min(a.y0, __shfl_xor_sync(0xffffffffu, a.y0, o));
+                a.x1 = max(a.x1, __shfl_xor_sync(0xffffffffu, a.x1, o));
+                a.y1 = max(a.y1, __shfl_xor_sync(0xffffffffu, a.y1, o));
+                a.lmin = min(a.lmin, __shfl_xor_sync(0xffffffffu, a.lmin, o));
+                a.aniso = max(a.aniso, __shfl_xor_sync(0xffffffffu, a.aniso, o));
+            }
+            if ((t & 31) == 0) s_wacc[t >> 5] = a;
+            __syncthreads();
+            if (t == 0) {
+                for (int w = 1; w < kTreeThreads / 32; ++w) {
+                    const Acc& b = s_wacc[w];
+                    a.x0 = min(a.x0, b.x0);
+                    a.y0 = min(a.y0, b.y0);
+                    a.x1 = max(a.x1, b.x1);
+                    a.y1 = max(a.y1, b.y1);
+                    a.lmin = min(a.lmin, b.lmin);
+                    a.aniso = max(a.aniso, b.aniso);
+                }
+                acc[c] = a;
+            }
+            __syncthreads();
+        }
+    }
     // upper levels: the first level from which every level fits in shared
     // memory (<= 16 x 16 cells), and the cells from there to the root
     int l0 = kInLv;
     while (l0 < L.levels && (L.G0 >> l0) > kBlk) ++l0;
     int ncell = 0;
     for (int j = l0; j < L.levels; ++j) ncell += (L.G0 >> j) * (L.G0 >> j);
-    // speculative prefetch (every CTA; L2 hits after the first): the own
-    // data of the shared-memory levels, so the last CTA does not wait for it
+    // speculative prefetch (every CTA; L2 hits after the first): the counts
+    // of the shared-memory levels, so the last CTA does not wait for them
     uint32_t um[2] = {0, 0}, uc[2] = {0, 0};
-    Acc ua[2];
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
-        const int i = t + 256 * r;
+        const int i = t + kTreeThreads * r;
         if (i < ncell) {
             uc[r] = (uint32_t)(s_loff[l0] + i);  // levels are contiguous in the cell numbering
             um[r] = cnt[uc[r]];
         }
     }
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-        if (t + 256 * r < ncell) ua[r] = acc[uc[r]];
     __shared__ bool last;
     // the block's stores are ordered before thread 0's fence by the barrier
     // (the cooperative-groups grid-barrier pattern): one fence per block
@@ -450,7 +536,7 @@ __global__ void __launch_bounds__(256) lq_tree_kernel(Acc* __restrict__ acc, Lq 
     // through global memory
     for (int l = kInLv; l < l0; ++l) {
         const int G = L.G0 >> l, cw = G * 2;
-        for (int i = t; i < G * G; i += 256) {
+        for (int i = t; i < G * G; i += kTreeThreads) {
             const int x = i % G, y = i / G;
             const uint32_t c = (uint32_t)(s_loff[l] + i);
             Sum s = own_of(acc, cnt, c);
@@ -462,16 +548,17 @@ __global__ void __launch_bounds__(256) lq_tree_kernel(Acc* __restrict__ acc, Lq 
         __threadfence();
         __syncthreads();
     }
-    // the shared-memory levels: own summaries from the prefetch, children of
-    // level l0 from global memory, the rest merged in shared memory
+    // the shared-memory levels: own summaries from the accumulators,
+    // children of level l0 from global memory, the rest merged in shared
+    // memory
     {
         const int G = L.G0 >> l0, cw = G * 2;
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
-            const int i = t + 256 * r;
+            const int i = t + kTreeThreads * r;
             if (i >= ncell) continue;
-            if (um[r]) acc[uc[r]] = acc_empty();
-            const Sum o = own_from(um[r], ua[r]);
+            const Acc ua = um[r] ? acc_ldcg(acc + uc[r]) : acc_empty();
+            const Sum o = own_from(um[r], ua);
             own[uc[r]] = o;
             Sum s = o;
             if (i < G * G) {
@@ -486,7 +573,7 @@ __global__ void __launch_bounds__(256) lq_tree_kernel(Acc* __restrict__ acc, Lq 
     __syncthreads();
     for (int j = l0 + 1, b0 = 0; j < L.levels; ++j) {
         const int G = L.G0 >> j, cw = G * 2, b1 = b0 + cw * cw;  // b0: first cell of level j-1 in up[]
-        for (int i = t; i < G * G; i += 256) {
+        for (int i = t; i < G * G; i += kTreeThreads) {
             const int x = i % G, y = i / G;
             Sum s = up[b1 + i];
             for (int dy = 0; dy < 2; ++dy)
@@ -1746,10 +1833,8 @@ int knn_build(igs_ctx* ctx) {
         // launches since the last build: re-derive the summaries only
         const int nb = (b.lq.G0 + kBlk - 1) / kBlk;
         igs_prof_begin(ctx, IGS_PROF_CULL);
-        IGS_PDL(ctx, lq_own_kernel, (ctx->n + 255) / 256, 256, 0, (const ScanRec*)b.mrec.p,
-                (const uint32_t*)b.mcell.p, (const uint32_t*)b.off.p, (const uint32_t*)b.cnt.p, ctx->n,
-                (Acc*)b.acc.p);
-        IGS_PDL(ctx, lq_tree_kernel, nb * nb, 256, 0, (Acc*)b.acc.p, b.lq, (const uint32_t*)b.cnt.p, (Sum*)b.own.p,
+        IGS_PDL(ctx, lq_tree_kernel, nb * nb, kTreeThreads, 0, (const ScanRec*)b.mrec.p, (const uint32_t*)b.mcell.p,
+                (const uint32_t*)b.off.p, ctx->n, (Acc*)b.acc.p, b.lq, (const uint32_t*)b.cnt.p, (Sum*)b.own.p,
                 (Sum*)b.sub.p, (unsigned int*)b.ticket.p, search_inputs(ctx, b), job, 0);
         igs_prof_end(ctx, IGS_PROF_CULL, 0.0);
         b.since_build++;
@@ -1809,7 +1894,8 @@ int knn_build(igs_ctx* ctx) {
                 (uint32_t*)b.mcell.p, (Acc*)b.acc.p);
     }
     const int nb = (G0 + kBlk - 1) / kBlk;
-    IGS_PDL(ctx, lq_tree_kernel, nb * nb, 256, 0, (Acc*)b.acc.p, L, (const uint32_t*)cnt, (Sum*)b.own.p,
+    IGS_PDL(ctx, lq_tree_kernel, nb * nb, kTreeThreads, 0, (const ScanRec*)b.mrec.p, (const uint32_t*)b.mcell.p,
+            (const uint32_t*)off, n, (Acc*)b.acc.p, L, (const uint32_t*)cnt, (Sum*)b.own.p,
             (Sum*)b.sub.p, (unsigned int*)b.ticket.p, search_inputs(ctx, b), job, 1);
     igs_prof_end(ctx, IGS_PROF_CULL, 0.0);
     b.lq = L;
@@ -2203,7 +2289,7 @@ int launch_knn_raster(igs_ctx* ctx, int W, int H, int row0, int row1, int kk, fl
 
 }  // namespace
 
-// The refit's inputs (cell accumulators and counts), for the step's first
+// The refit's inputs (member records, cells, offsets and counts), for the step's first
 // kernel to prefetch; empty unless the next search can refit.
 L2Prefetch igs_knn_tree_inputs(igs_ctx* ctx) {
     L2Prefetch pf{};
@@ -2211,7 +2297,9 @@ L2Prefetch igs_knn_tree_inputs(igs_ctx* ctx) {
     KnnBufs& b = *static_cast<KnnBufs*>(ctx->knn);
     if (!b.acc_ok || b.version == ctx->params_version) return pf;
     const size_t cells = (size_t)b.lq.loff[b.lq.levels - 1] + 1;
-    l2pf_add(pf, b.acc.p, cells * sizeof(Acc));
+    l2pf_add(pf, b.mrec.p, (size_t)b.built_n * sizeof(ScanRec));
+    l2pf_add(pf, b.mcell.p, (size_t)b.built_n * 4);
+    l2pf_add(pf, b.off.p, cells * 4);
     l2pf_add(pf, b.cnt.p, cells * 4);
     return pf;
 }

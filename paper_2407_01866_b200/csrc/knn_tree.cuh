@@ -42,9 +42,9 @@ __device__ __forceinline__ uint32_t key_of(const Lq& L, const ScanRec& r) {
 }
 
 // Own-cell summaries are accumulated with order-preserving 32-bit min/max
-// (atomics while a build scatters the members, warp shuffles over the
-// member-ordered records in a refit -- no per-cell member loop): a float's bit
-// pattern, sign-flipped, orders like the float itself.  Values are rounded
+// over the member-ordered records (lq_tree_kernel: warp shuffles, then
+// shared or global atomics per run of equal cells): a float's bit pattern,
+// sign-flipped, orders like the float itself.  Values are rounded
 // in the direction that keeps the summary conservative (bbox outward,
 // lambda_min down, anisotropy up), as the 32-byte Sum stores them.
 struct Acc {
@@ -57,10 +57,9 @@ __device__ __forceinline__ unsigned okey(float f) {
 }
 __device__ __forceinline__ float odec(unsigned k) { return __uint_as_float((k >> 31) ? (k & 0x7fffffffu) : ~k); }
 
-// Adds Gaussian r to a cell accumulator held by one thread (no atomics):
-// the refit (lq_own_kernel) forms each cell's accumulator from the
-// member-ordered records with the same keys and the same outward rounding
-// as acc_add (min/max are order-free).
+// Adds Gaussian r to a cell accumulator held by one thread.  A non-finite
+// or degenerate record gets aniso = inf, whose slack 0 makes the cell never
+// prunable.
 __device__ __forceinline__ void acc_add_local(Acc& a, const ScanRec& r) {
     const double lo = fmin(r.inv_a, r.inv_b), hi = fmax(r.inv_a, r.inv_b);
     double aniso = hi / lo;
@@ -74,19 +73,10 @@ __device__ __forceinline__ void acc_add_local(Acc& a, const ScanRec& r) {
     a.aniso = max(a.aniso, okey(__double2float_ru(aniso)));
 }
 
-// Adds Gaussian r to a cell accumulator.  A non-finite or degenerate record
-// gets aniso = inf, whose slack 0 makes the cell never prunable.
-__device__ __forceinline__ void acc_add(Acc* a, const ScanRec& r) {
-    const double lo = fmin(r.inv_a, r.inv_b), hi = fmax(r.inv_a, r.inv_b);
-    double aniso = hi / lo;
-    if (!(lo > 0.0) || !isfinite(hi) || !isfinite(r.mu_x) || !isfinite(r.mu_y))
-        aniso = __longlong_as_double(0x7ff0000000000000LL);
-    atomicMin(&a->x0, okey(__double2float_rd(r.mu_x)));
-    atomicMin(&a->y0, okey(__double2float_rd(r.mu_y)));
-    atomicMax(&a->x1, okey(__double2float_ru(r.mu_x)));
-    atomicMax(&a->y1, okey(__double2float_ru(r.mu_y)));
-    atomicMin(&a->lmin, okey(__double2float_rd(lo)));
-    atomicMax(&a->aniso, okey(__double2float_ru(aniso)));
+// An accumulator other CTAs folded into with atomics: read through L2.
+__device__ __forceinline__ Acc acc_ldcg(const Acc* a) {
+    const unsigned* u = reinterpret_cast<const unsigned*>(a);
+    return Acc{__ldcg(u), __ldcg(u + 1), __ldcg(u + 2), __ldcg(u + 3), __ldcg(u + 4), __ldcg(u + 5)};
 }
 
 __device__ __forceinline__ Acc acc_empty() {
@@ -114,7 +104,7 @@ __device__ __forceinline__ void tree_acc_add(const TreeAcc& ta, uint32_t i, cons
     if (!ta.acc) return;
     const uint32_t k = ta.key[i];
     // the member-ordered copy the searches read; the next refit re-derives
-    // every cell accumulator from it (lq_own_kernel), so no atomics here
+    // every cell summary from it (lq_tree_kernel), so no atomics here
     ta.mrec[ta.minv[i]] = r;
     // level_of: smallest l with cell 2^l / G0 >= 2 sigma_max = 2 / sqrt(lmin)
     const float lmin = (float)fmin(r.inv_a, r.inv_b);

@@ -46,7 +46,6 @@ __device__ __forceinline__ unsigned offsets_scatter_body(const OffArgs& A, unsig
     uint32_t* __restrict__ perm = A.perm;
     uint32_t* __restrict__ long_count = A.long_count;
     uint32_t* __restrict__ long_list = A.long_list;
-    unsigned* __restrict__ bar = A.bar;
     const uint32_t G = gridDim.x;
     if (A.ovf) {
         const uint32_t no = *(volatile const uint32_t*)A.ovf;  // (uniform)
