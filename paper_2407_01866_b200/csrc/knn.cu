@@ -587,12 +587,28 @@ __global__ void __launch_bounds__(kTreeThreads) lq_tree_kernel(const ScanRec* __
     if (t == 0) *ticket = 0;  // ready for the next build
 }
 
-__device__ __forceinline__ double sum_lb(const Sum& s, double px, double py) {
-    if (s.count == 0) return __longlong_as_double(0x7ff0000000000000LL);
-    const double dx = fmax(fmax((double)s.x0 - px, px - (double)s.x1), 0.0);
-    const double dy = fmax(fmax((double)s.y0 - py, py - (double)s.y1), 0.0);
-    return (double)s.lmin * (dx * dx + dy * dy) * (double)s.slack;
+// The query point as a float box [xl, xh] x [yl, yh] around (px, py), so
+// the pruning bound below runs in fp32.
+struct PtBox {
+    float xl, xh, yl, yh;
+};
+__device__ __forceinline__ PtBox pt_box(double px, double py) {
+    return PtBox{__double2float_rd(px), __double2float_ru(px), __double2float_rd(py), __double2float_ru(py)};
 }
+
+// Lower bound of q over a cell's members: lmin * dist(point, bbox)^2 * slack,
+// in fp32 with every step rounded down and the point widened to its float
+// box (so never above the exact bound) -- compared against the threshold
+// rounded up (tqf).  slack 0
+// (a degenerate member) never prunes; an empty cell always does.
+__device__ __forceinline__ float sum_lb_f(const Sum& s, const PtBox& b) {
+    if (s.count == 0) return __int_as_float(0x7f800000);
+    if (!(s.slack > 0.0f)) return 0.0f;
+    const float dx = fmaxf(fmaxf(__fsub_rd(s.x0, b.xh), __fsub_rd(b.xl, s.x1)), 0.0f);
+    const float dy = fmaxf(fmaxf(__fsub_rd(s.y0, b.yh), __fsub_rd(b.yl, s.y1)), 0.0f);
+    return __fmul_rd(__fmul_rd(s.lmin, __fadd_rd(__fmul_rd(dx, dx), __fmul_rd(dy, dy))), s.slack);
+}
+
 
 // Warp-distributed top-K: lane j holds the j-th best (q, idx) for j < kk,
 // ascending in the strict (q, idx) order of select_top_k_entries
@@ -604,6 +620,7 @@ struct WarpTopK {
     double q;
     uint32_t i;
     double tq_;
+    float tqf_;
     uint32_t ti;
     int kk, lane;
 
@@ -613,9 +630,11 @@ struct WarpTopK {
         q = __longlong_as_double(0x7ff0000000000000LL);
         i = kNoIdx;
         tq_ = q;
+        tqf_ = __int_as_float(0x7f800000);
         ti = kNoIdx;
     }
     __device__ __forceinline__ double tq() const { return tq_; }
+    __device__ __forceinline__ float tqf() const { return tqf_; }  // tq rounded up (fp32 pruning)
     __device__ __forceinline__ bool beats(double cq, uint32_t ci) const {
         return cq < tq_ || (cq == tq_ && ci < ti);
     }
@@ -645,6 +664,7 @@ struct WarpTopK {
     }
     __device__ __forceinline__ void refresh() {
         tq_ = __shfl_sync(0xffffffffu, q, kk - 1);
+        tqf_ = __double2float_ru(tq_);
         ti = __shfl_sync(0xffffffffu, i, kk - 1);
     }
     static __device__ __forceinline__ bool lt(double aq, uint32_t ai, double bq, uint32_t bi) {
@@ -969,6 +989,7 @@ __global__ void __launch_bounds__(128, 9) knn_points_kernel(const ScanRec* __res
     if (lane == 0) claim = nwarps + atomicAdd(next_point, 1u);
     double px, py;
     point_of(uv, E, W, H, pt, px, py);
+    const PtBox pb = pt_box(px, py);
     WarpTopK t;
     t.init(kk, lane);
     unsigned long long evaluated = 0;
@@ -1007,7 +1028,7 @@ __global__ void __launch_bounds__(128, 9) knn_points_kernel(const ScanRec* __res
                         m = own[c].count;
                     } else {
                         const Sum so = own[c];
-                        if (so.count && sum_lb(so, px, py) <= t.tq()) {
+                        if (so.count && sum_lb_f(so, pb) <= t.tqf()) {
                             o = off[c];
                             m = so.count;
                         }
@@ -1066,7 +1087,7 @@ __global__ void __launch_bounds__(128, 9) knn_points_kernel(const ScanRec* __res
                 const int Rl = l == lfine ? R : 1;  // the seed window at this level
                 if (abs(x - (cx0 >> l)) > Rl || abs(y - (cy0 >> l)) > Rl) {
                     const Sum so = own[c];
-                    if (so.count && sum_lb(so, px, py) <= t.tq()) {
+                    if (so.count && sum_lb_f(so, pb) <= t.tqf()) {
                         o = off[c];
                         m = so.count;
                     }
@@ -1090,11 +1111,11 @@ __global__ void __launch_bounds__(128, 9) knn_points_kernel(const ScanRec* __res
             bool keep = false;
             uint32_t o = 0, m = 0;
             if (node < nls) {
-                keep = sum_lb(sub[lo + node], px, py) <= t.tq();
+                keep = sum_lb_f(sub[lo + node], pb) <= t.tqf();
                 const int x = node & ((1 << lg) - 1), y = node >> lg;
                 if (keep && (abs(x - sx) > Rl || abs(y - sy) > Rl)) {
                     const Sum so = own[lo + node];
-                    if (so.count && sum_lb(so, px, py) <= t.tq()) {
+                    if (so.count && sum_lb_f(so, pb) <= t.tqf()) {
                         o = off[lo + node];
                         m = so.count;
                     }
@@ -1125,10 +1146,10 @@ __global__ void __launch_bounds__(128, 9) knn_points_kernel(const ScanRec* __res
                 const uint32_t x = node & (uint32_t)wmask, y = node >> lg;
                 const uint32_t cx = 2 * x + (item & 1), cy = 2 * y + ((item >> 1) & 1);
                 child = (cy << clg) + cx;
-                keep = sum_lb(sub[clo + child], px, py) <= t.tq();
+                keep = sum_lb_f(sub[clo + child], pb) <= t.tqf();
                 if (keep && (abs((int)cx - csx) > cR || abs((int)cy - csy) > cR)) {
                     const Sum so = own[clo + child];
-                    if (so.count && sum_lb(so, px, py) <= t.tq()) {
+                    if (so.count && sum_lb_f(so, pb) <= t.tqf()) {
                         o = off[clo + child];
                         m = so.count;
                     }
@@ -1205,6 +1226,7 @@ struct HalfTopK {
     double q;
     uint32_t i;
     double tq_;
+    float tqf_;
     uint32_t ti;
     int kk, hl;
 
@@ -1214,9 +1236,11 @@ struct HalfTopK {
         q = __longlong_as_double(0x7ff0000000000000LL);
         i = kNoIdx;
         tq_ = q;
+        tqf_ = __int_as_float(0x7f800000);
         ti = kNoIdx;
     }
     __device__ __forceinline__ double tq() const { return tq_; }
+    __device__ __forceinline__ float tqf() const { return tqf_; }  // tq rounded up (fp32 pruning)
     __device__ __forceinline__ bool beats(double cq, uint32_t ci) const {
         return cq < tq_ || (cq == tq_ && ci < ti);
     }
@@ -1238,6 +1262,7 @@ struct HalfTopK {
     }
     __device__ __forceinline__ void refresh() {
         tq_ = __shfl_sync(0xffffffffu, q, kk - 1, 16);
+        tqf_ = __double2float_ru(tq_);
         ti = __shfl_sync(0xffffffffu, i, kk - 1, 16);
     }
     // a half-batch (one candidate per lane, (inf, kNoIdx) for none): bitonic
@@ -1370,6 +1395,7 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
     const bool active = pt < npts;  // the second half of an odd tail searches a dummy point
     double px = 0.5, py = 0.5;
     if (active) point_of(uv, E, W, H, pt, px, py);
+    const PtBox pb = pt_box(px, py);
     if (active && E.mode == 0) {  // the target pixel the epilogue reads
         const float* tp = E.target + (size_t)E.sidx[pt] * 3;
         asm volatile("prefetch.global.L1 [%0];" ::"l"(tp));
@@ -1405,7 +1431,7 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
                         m = own[c].count;
                     } else {
                         const Sum so = own[c];
-                        if (so.count && sum_lb(so, px, py) <= t.tq()) {
+                        if (so.count && sum_lb_f(so, pb) <= t.tqf()) {
                             o = off[c];
                             m = so.count;
                         }
@@ -1460,7 +1486,7 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
                 const int Rl = l == lfine ? R : 1;
                 if (abs(x - (cx0 >> l)) > Rl || abs(y - (cy0 >> l)) > Rl) {
                     const Sum so = own[c];
-                    if (so.count && sum_lb(so, px, py) <= t.tq()) {
+                    if (so.count && sum_lb_f(so, pb) <= t.tqf()) {
                         o = off[c];
                         m = so.count;
                     }
@@ -1479,11 +1505,11 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
             bool keep = false;
             uint32_t o = 0, m = 0;
             if (node < nls) {
-                keep = sum_lb(sub[lo + node], px, py) <= t.tq();
+                keep = sum_lb_f(sub[lo + node], pb) <= t.tqf();
                 const int x = node & ((1 << lg) - 1), y = node >> lg;
                 if (keep && (abs(x - sx) > Rl || abs(y - sy) > Rl)) {
                     const Sum so = own[lo + node];
-                    if (so.count && sum_lb(so, px, py) <= t.tq()) {
+                    if (so.count && sum_lb_f(so, pb) <= t.tqf()) {
                         o = off[lo + node];
                         m = so.count;
                     }
@@ -1516,10 +1542,10 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
                 const uint32_t x = node & (uint32_t)wmask, y = node >> lg;
                 const uint32_t cx = 2 * x + (item & 1), cy = 2 * y + ((item >> 1) & 1);
                 child = (cy << clg) + cx;
-                keep = sum_lb(sub[clo + child], px, py) <= t.tq();
+                keep = sum_lb_f(sub[clo + child], pb) <= t.tqf();
                 if (keep && (abs((int)cx - csx) > cR || abs((int)cy - csy) > cR)) {
                     const Sum so = own[clo + child];
-                    if (so.count && sum_lb(so, px, py) <= t.tq()) {
+                    if (so.count && sum_lb_f(so, pb) <= t.tqf()) {
                         o = off[clo + child];
                         m = so.count;
                     }
@@ -1616,6 +1642,7 @@ __device__ __forceinline__ void hard_merge_point(const ScanRec* __restrict__ sca
     const uint32_t pt = hard_list[slot];
     double px, py;
     point_of(uv, E, W, H, pt, px, py);
+    const PtBox pb = pt_box(px, py);
     WarpTopK t;
     t.init(kk, lane);
     for (int sp = 0; sp < kHardSplit; ++sp) {
@@ -1650,6 +1677,7 @@ __device__ __forceinline__ void hard_scan_items(const ScanRec* __restrict__ scan
         const uint32_t pt = hard_list[slot];
         double px, py;
         point_of(uv, E, W, H, pt, px, py);
+    const PtBox pb = pt_box(px, py);
         const uint32_t g0 = split * per, g1 = min(n, g0 + per);
         TopK<KCAP> t;
         t.init(kk);
