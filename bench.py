@@ -559,9 +559,9 @@ def secondary_fit(ctx):
 
 def ncu_traffic(kernel: str):
     """DRAM bytes (read + write) per launch of `kernel` from the committed
-    `ncu --set full` capture summary (profiles/r1_traffic.json), or None."""
+    `ncu --set full` capture summary (profiles/r2_traffic.json), or None."""
     try:
-        d = json.loads((ROOT / "profiles" / "r1_traffic.json").read_text())
+        d = json.loads((ROOT / "profiles" / "r2_traffic.json").read_text())
         return d[kernel]["dram_bytes_per_launch"]
     except Exception:
         return None
