@@ -1523,6 +1523,10 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
         }
         __syncwarp();
     }
+    // one level per pass (two per pass -- a kept node's 16 grandchildren on
+    // the 16 lanes -- halves the dependent rounds but measured 20 % slower:
+    // the search is issue-bound, and it tests more nodes).  Own lists of
+    // levels with no members (lvmask) are not read.
     for (int l = ls; l > 0; --l) {
         if (__ballot_sync(0xffffffffu, ncur > 0) == 0) break;
         const int lg = s_lg[l];
@@ -1531,6 +1535,7 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
         const int clg = lg + 1;
         const int csx = cx0 >> (l - 1), csy = cy0 >> (l - 1);
         const int cR = l - 1 == lfine ? R : 1;
+        const bool cpop = (lvmask >> (l - 1)) & 1u;
         int nnext = 0;
         const int items = ncur * 4, imax = max(items, other_half(items));
         for (int base = 0; base < imax; base += 16) {
@@ -1543,7 +1548,7 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
                 const uint32_t cx = 2 * x + (item & 1), cy = 2 * y + ((item >> 1) & 1);
                 child = (cy << clg) + cx;
                 keep = sum_lb_f(sub[clo + child], pb) <= t.tqf();
-                if (keep && (abs((int)cx - csx) > cR || abs((int)cy - csy) > cR)) {
+                if (keep && cpop && (abs((int)cx - csx) > cR || abs((int)cy - csy) > cR)) {
                     const Sum so = own[clo + child];
                     if (so.count && sum_lb_f(so, pb) <= t.tqf()) {
                         o = off[clo + child];
