@@ -449,6 +449,19 @@ __device__ __forceinline__ void prefetch_l2(const L2Prefetch& pf, uint32_t tid, 
 // must execute pdl_wait() before it reads or writes any memory a
 // predecessor touches.  Without the launch attribute pdl_wait is a no-op.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Lets the stream successor (launched with IGS_PDL) be scheduled before this
+// grid completes: once every CTA has executed it (or exited), the
+// successor's CTAs may become resident and run up to their pdl_wait, which
+// still waits for this grid's completion and memory.  A CTA calls it when
+// its remaining work is short.  Used by lq_tree_kernel only: the same
+// trigger in the search (+0.0 %) and in the hard-point/offsets launch
+// (-6 %: Adam's CTAs then crowd the SMs while it runs) measured no gain.
+// (IGS_NO_PDL_TRIGGER: compiled out, A/B.)
+__device__ __forceinline__ void pdl_trigger() {
+#ifndef IGS_NO_PDL_TRIGGER
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t igs_launch_pdl(cudaStream_t st, bool coop, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,

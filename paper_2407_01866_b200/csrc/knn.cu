@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(kTreeThreads) lq_tree_kernel(const ScanRec* __
         cur ^= 1;
         lbase += side * side;
     }
-    if (L.levels <= kInLv) return;
+    if (L.levels <= kInLv) return;  // (exit: counts as the launch trigger)
     // the cells of the levels above (large Gaussians; few cells, possibly
     // many members each): cell by cell over the CTAs, each cell's members
     // reduced by the whole CTA into its global accumulator (plain store)
@@ -526,6 +526,7 @@ __global__ void __launch_bounds__(kTreeThreads) lq_tree_kernel(const ScanRec* __
     // (the cooperative-groups grid-barrier pattern): one fence per block
     __syncthreads();
     if (t == 0) {
+        pdl_trigger();  // only the last CTA's upper levels remain
         __threadfence();
         last = atomicAdd(ticket, 1u) == (unsigned)(nb * nb - 1);
     }
