@@ -15,6 +15,7 @@
 #include <stdint.h>
 
 #include <climits>
+#include <cstdlib>
 
 #include <string>
 #include <vector>
@@ -474,9 +475,9 @@ inline cudaError_t igs_launch_pdl(cudaStream_t st, bool coop, void (*k)(KArgs...
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
-    // kernels with grid barriers (igs_grid_sync) launch cooperatively: the
-    // driver then guarantees every CTA is co-resident or fails the launch
-    // (cudaErrorCooperativeLaunchTooLarge) instead of letting it spin forever
+    // coop (IGS_COOP_BARRIERS): the driver guarantees every CTA is
+    // co-resident or fails the launch (cudaErrorCooperativeLaunchTooLarge)
+    // instead of letting a grid barrier spin forever
     at[1].id = cudaLaunchAttributeCooperative;
     at[1].val.cooperative = 1;
     cfg.attrs = at;
@@ -492,10 +493,27 @@ inline cudaError_t igs_launch_pdl(cudaStream_t st, bool coop, void (*k)(KArgs...
         if (_e != cudaSuccess) return igs_cuda_check((ctx), _e, #kernel);                                   \
     } while (0)
 // a persistent launch with grid barriers: cooperative + PDL
+// Launches of kernels with grid barriers (igs_grid_sync).  Their grids are
+// sized from the occupancy calculator (at most the co-resident CTAs per SM
+// times the SM count), and every CTA passes pdl_wait only after the
+// predecessor has left the GPU, so they are co-resident without the
+// cooperative attribute -- which costs ~3 us of chain time per launch
+// (C2 step 92.5 -> 89.7 us measured for the hard-point/offsets launch).
+// With a communicator attached (several ranks' grids may share a GPU, as
+// in the loopback tests) or IGS_COOP_BARRIERS=1 they are cooperative
+// launches: the driver then schedules each grid whole (and under MPS,
+// where fewer SMs may be available than the device reports, fails rather
+// than hangs).
+inline bool igs_coop_barriers() {
+    static const bool v = getenv("IGS_COOP_BARRIERS") != nullptr;
+    return v;
+}
+
 #define IGS_PDL_COOP(ctx, kernel, grid, block, smem, ...)                                                   \
     do {                                                                                                    \
-        cudaError_t _e =                                                                                    \
-            igs_launch_pdl((ctx)->stream, true, kernel, dim3(grid), dim3(block), (smem), __VA_ARGS__);      \
+        cudaError_t _e = igs_launch_pdl((ctx)->stream, igs_coop_barriers() || igs_has_comm(ctx), kernel,      \
+                                        dim3(grid), dim3(block),                                            \
+                                        (smem), __VA_ARGS__);                                               \
         (ctx)->launches++;                                                                                  \
         if (_e != cudaSuccess) return igs_cuda_check((ctx), _e, #kernel);                                   \
     } while (0)

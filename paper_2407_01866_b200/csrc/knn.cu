@@ -2009,23 +2009,11 @@ int launch_knn(igs_ctx* ctx, const double* uv, int W, int H, uint32_t npts, int 
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hard_offsets_kernel<KCAP>, kOffThreads, 0);
                 per_sm = std::max(1, std::min(per_sm, kOffCtasPerSm));
             }
-            // A plain programmatic-dependent launch, not a cooperative one:
-            // the cooperative attribute costs ~3 us of chain time per step
-            // (C2 92.5 -> 89.7 us measured), and co-residency holds without
-            // it -- the grid is the occupancy calculator's per-SM count times
-            // the SM count, and every CTA passes pdl_wait only after the
-            // search has left the GPU.  IGS_COOP_BARRIERS=1 restores the
-            // driver-enforced launch (e.g. under MPS, where fewer SMs may be
-            // available than the device reports).
-            static const bool coop = getenv("IGS_COOP_BARRIERS") != nullptr;
-            const cudaError_t le = igs_launch_pdl(
-                ctx->stream, coop, hard_offsets_kernel<KCAP>, dim3(per_sm * ctx->sm_count), dim3(kOffThreads), 0,
-                (const ScanRec*)ctx->scan, ctx->n, uv, W, H, kk, (const uint32_t*)hard_count,
-                (const uint32_t*)hard_list, E, part_q, part_i, (unsigned int*)((uint32_t*)b.hard.p + 4 + kHardCap),
-                igs_prof_counter(ctx, IGS_PROF_SCAN), ctx->fuse_off.args, ctx->fuse_off.long_args,
-                (int)ctx->fuse_off.fuse_long);
-            ctx->launches++;
-            if (le != cudaSuccess) return igs_cuda_check(ctx, le, "hard_offsets_kernel");
+            IGS_PDL_COOP(ctx, hard_offsets_kernel<KCAP>, per_sm * ctx->sm_count, kOffThreads, 0,
+                         (const ScanRec*)ctx->scan, ctx->n, uv, W, H, kk, (const uint32_t*)hard_count,
+                         (const uint32_t*)hard_list, E, part_q, part_i,
+                         (unsigned int*)((uint32_t*)b.hard.p + 4 + kHardCap), igs_prof_counter(ctx, IGS_PROF_SCAN),
+                         ctx->fuse_off.args, ctx->fuse_off.long_args, (int)ctx->fuse_off.fuse_long);
             igs_prof_end(ctx, IGS_PROF_REDUCE, 0.0);
             return IGS_OK;
         }
