@@ -29,6 +29,7 @@
 #include "knn_tree.cuh"
 #include "reduce.cuh"
 #include "scan.cuh"
+#include "adam.cuh"
 
 using namespace igs_dev;
 
@@ -316,28 +317,6 @@ __global__ void grad_check_kernel(const double* __restrict__ grads, uint32_t n, 
         }
 }
 
-// a / b correctly rounded; a zero dividend (every parameter of a Gaussian no
-// sample selected) skips __ddiv_rn's slow path: 0 / b == 0 * b for finite
-// nonzero b, sign included.
-__device__ __forceinline__ double div_rn(double a, double b) {
-    return (a == 0.0 && b != 0.0 && fabs(b) < __longlong_as_double(0x7ff0000000000000LL)) ? __dmul_rn(a, b)
-                                                                                         : __ddiv_rn(a, b);
-}
-
-// a / b for the per-step constants b = bc1, bc2 with y = RN(1/b) from the
-// host: two Markstein corrections (igs_math::div_by_recip), exact IEEE
-// division outside its operand range (zero, tiny, huge, non-finite).
-__device__ __forceinline__ double div_const(double a, double b, double y) {
-    const double aa = fabs(a);
-    if (aa >= 0x1p-960 && aa <= 0x1p1000) return igs_math::div_by_recip(a, b, y);
-    return div_rn(a, b);
-}
-
-__device__ __forceinline__ double clamp01d(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
-__device__ __forceinline__ double clamp_scale(double v) {
-    return v < kScaleMin ? kScaleMin : (v > kScaleMax ? kScaleMax : v);
-}
-
 // Kernel 5: Adam (adam.cpp:21-51) + constrain (gaussian.cpp:74-90) +
 // PreparedSet refresh for the next step, for one Gaussian.  HBM: 256 B read
 // + 192 B written for params/grads/m/v, plus 96 B of refreshed scan/shade.
@@ -454,230 +433,6 @@ __global__ void adam_kernel(double* __restrict__ params, const double* __restric
     adam_one(i, gg, gp, mm, vv, params, m, v, scan, shade, lr_mu, lr_color, lr_scale, lr_theta, bc1, bc2, ibc1, ibc2,
              status, ta);
 }
-
-__device__ __forceinline__ double shx(double v) { return __shfl_xor_sync(0xffffffffu, v, 1); }
-
-// Fused short-segment reduction + Adam: a lane pair per Gaussian sums its
-// short segment in sample order (or reads the long-segment result), stores
-// the gradient, and updates Gaussian g unless that gradient is non-finite
-// (then it flags status[0] = first (i, p) and leaves g untouched -- every
-// finite Gaussian is still updated, deterministically; the reference has
-// updated Gaussians 0..i-1 when it throws, adam.cpp:29-31).  A non-finite
-// loss (flagged by the search epilogue) skips the whole step, as fit.cpp:155.
-// Two lanes per Gaussian: lane h = 0 owns parameters 0-3 (mu, theta, s1),
-// h = 1 owns 4-7 (s2, colour); the Adam chains split in half, lane 1 forms
-// sin/cos while lane 0 forms both reciprocals.
-#ifndef IGS_ADAM_MINB
-#define IGS_ADAM_MINB 7
-#endif
-__global__ void __launch_bounds__(128, IGS_ADAM_MINB) segment_adam_kernel(
-    uint32_t* __restrict__ gcnt, const uint32_t* __restrict__ goff, const uint32_t* __restrict__ perm,
-    const double* __restrict__ contrib, uint32_t n, double* __restrict__ grads, double* __restrict__ params,
-    double* __restrict__ m, double* __restrict__ v, ScanRec* __restrict__ scan, ShadeRec* __restrict__ shade,
-    double lr_mu, double lr_color, double lr_scale, double lr_theta, double bc1, double bc2, double ibc1, double ibc2,
-    long long* __restrict__ status, TreeAcc ta, uint32_t g_begin, uint32_t g_end, const uint32_t* __restrict__ bucket) {
-    pdl_wait();
-    // Gaussians [g_begin, g_end): the whole set, or this rank's slice when
-    // the multi-rank update is sharded (n stays the set size: gcnt is [2n])
-    const uint32_t g0 = g_begin + blockIdx.x * (blockDim.x / 2) + (threadIdx.x >> 1);
-    const int h = threadIdx.x & 1;
-    const bool live = g0 < g_end;
-    const uint32_t g = live ? g0 : g_end - 1;  // dead pairs shadow a live one (no writes) to keep shuffles full
-    // a short segment's slot ids: its bucket (reduce.cuh), else perm[goff[g] ...]
-    const bool from_bucket = bucket != nullptr;
-    const uint32_t* __restrict__ seg = from_bucket ? bucket : perm;
-    uint32_t cntg = 0;
-    size_t og = 0;
-    if (h == 0) {
-        cntg = gcnt[g];
-        og = from_bucket ? (size_t)g * kBucket : goff[g];
-    }
-    cntg = __shfl_sync(0xffffffffu, cntg, threadIdx.x & ~1);
-    og = __shfl_sync(0xffffffffu, og, threadIdx.x & ~1);
-    __syncwarp();
-    if (live && h == 0) {
-        gcnt[g] = 0;
-        gcnt[n + g] = 0;
-    }
-    const bool skip_all = status[2] != LLONG_MAX;
-    // segments of 5..kShortSeg slot ids: put in slot order by the whole warp,
-    // one segment at a time (lane e loads id e -- one row of the bucket --
-    // and takes its rank among the others by shuffles; distinct ids), into
-    // this pair's row of s_sorted.  Dead pairs shadow a live Gaussian, so
-    // they sort (and later read) a valid segment too.
-    __shared__ uint32_t s_sorted[4][16][kShortSeg];
-    uint32_t* my_sorted = s_sorted[(threadIdx.x >> 5) & 3][(threadIdx.x & 31) >> 1];
-    {
-        const int lane = threadIdx.x & 31;
-        unsigned med = __ballot_sync(0xffffffffu, !skip_all && h == 0 && cntg > 4 && cntg <= kShortSeg);
-        while (med) {
-            const int src = __ffs(med) - 1;
-            med &= med - 1;
-            const uint32_t mm = __shfl_sync(0xffffffffu, cntg, src);
-            const size_t oo = __shfl_sync(0xffffffffu, og, src);
-            const uint32_t v = (uint32_t)lane < mm ? seg[oo + lane] : 0xFFFFFFFFu;
-            uint32_t r = 0;
-            for (uint32_t j = 0; j < mm; ++j) r += __shfl_sync(0xffffffffu, v, j) < v;
-            if ((uint32_t)lane < mm) s_sorted[(threadIdx.x >> 5) & 3][src >> 1][r] = v;
-        }
-        __syncwarp();
-    }
-    // gradient components 4h .. 4h+3
-    double G[4] = {0, 0, 0, 0};
-    if (!skip_all) {
-        if (cntg > kShortSeg) {
-            const double2* src = reinterpret_cast<const double2*>(grads + (size_t)g * 8 + 4 * h);
-            const double2 a = src[0], b = src[1];
-            G[0] = a.x; G[1] = a.y; G[2] = b.x; G[3] = b.y;
-        } else if (cntg > 0) {
-            auto add_row = [&](uint32_t slot) {
-                const double2* c = reinterpret_cast<const double2*>(contrib + (size_t)slot * 8 + 4 * h);
-                const double2 a = c[0], b = c[1];
-                G[0] = __dadd_rn(G[0], a.x);
-                G[1] = __dadd_rn(G[1], a.y);
-                G[2] = __dadd_rn(G[2], b.x);
-                G[3] = __dadd_rn(G[3], b.y);
-            };
-            if (cntg <= 4) {
-                // nearly every segment: its slot ids sorted in registers
-                // (a 5-exchange network), no local-memory array
-                uint32_t s0 = seg[og], s1 = cntg > 1 ? seg[og + 1] : 0xFFFFFFFFu,
-                         s2 = cntg > 2 ? seg[og + 2] : 0xFFFFFFFFu, s3 = cntg > 3 ? seg[og + 3] : 0xFFFFFFFFu;
-                auto cx = [](uint32_t& a, uint32_t& b) {
-                    const uint32_t lo = min(a, b), hi = max(a, b);
-                    a = lo;
-                    b = hi;
-                };
-                cx(s0, s1);
-                cx(s2, s3);
-                cx(s0, s2);
-                cx(s1, s3);
-                cx(s1, s2);
-                add_row(s0);
-                if (cntg > 1) add_row(s1);
-                if (cntg > 2) add_row(s2);
-                if (cntg > 3) add_row(s3);
-            } else {
-                for (uint32_t e = 0; e < cntg; ++e) add_row(my_sorted[e]);  // (sorted above)
-            }
-            if (live) {
-                double2* o2 = reinterpret_cast<double2*>(grads + (size_t)g * 8 + 4 * h);
-                o2[0] = make_double2(G[0], G[1]);
-                o2[1] = make_double2(G[2], G[3]);
-            }
-        } else if (live) {
-            double2* o2 = reinterpret_cast<double2*>(grads + (size_t)g * 8 + 4 * h);
-            o2[0] = make_double2(0.0, 0.0);
-            o2[1] = make_double2(0.0, 0.0);
-        }
-    }
-    // first non-finite gradient component of the pair (h = 0's first)
-    int badp = 8;
-    for (int j = 3; j >= 0; --j)
-        if (!isfinite(G[j])) badp = 4 * h + j;
-    const int other = __shfl_xor_sync(0xffffffffu, badp, 1);
-    const int firstbad = min(badp, other);
-    if (skip_all || firstbad < 8) {
-        if (live && h == 0) {
-            if (!skip_all) atomicMin(status, (long long)g * 8 + firstbad);
-            tree_acc_add(ta, g, scan[g]);
-        }
-        return;  // pair-uniform
-    }
-    const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
-    const double omb1 = 1.0 - b1, omb2 = 1.0 - b2;
-    const double2* P2 = reinterpret_cast<const double2*>(params + (size_t)g * 8 + 4 * h);
-    const double2* M2 = reinterpret_cast<const double2*>(m + (size_t)g * 8 + 4 * h);
-    const double2* V2 = reinterpret_cast<const double2*>(v + (size_t)g * 8 + 4 * h);
-    double gp[4], mm[4], vv[4];
-    {
-        const double2 p0 = P2[0], p1 = P2[1], m0 = M2[0], m1 = M2[1], v0 = V2[0], v1 = V2[1];
-        gp[0] = p0.x; gp[1] = p0.y; gp[2] = p1.x; gp[3] = p1.y;
-        mm[0] = m0.x; mm[1] = m0.y; mm[2] = m1.x; mm[3] = m1.y;
-        vv[0] = v0.x; vv[1] = v0.y; vv[2] = v1.x; vv[3] = v1.y;
-    }
-    const double lrh[4] = {h ? lr_scale : lr_mu, h ? lr_color : lr_mu, h ? lr_color : lr_theta,
-                           h ? lr_color : lr_scale};
-    bool fin = true;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        mm[j] = __dadd_rn(__dmul_rn(b1, mm[j]), __dmul_rn(omb1, G[j]));
-        vv[j] = __dadd_rn(__dmul_rn(b2, vv[j]), __dmul_rn(__dmul_rn(omb2, G[j]), G[j]));
-        const double m_hat = div_const(mm[j], bc1, ibc1);
-        const double v_hat = div_const(vv[j], bc2, ibc2);
-        const double upd = div_rn(__dmul_rn(lrh[j], m_hat), __dadd_rn(__dsqrt_rn(v_hat), eps));
-        gp[j] = __dsub_rn(gp[j], upd);
-        fin = fin && isfinite(gp[j]);
-    }
-    const bool fin_pair = __shfl_xor_sync(0xffffffffu, fin ? 1 : 0, 1) && fin;
-    if (!fin_pair) {
-        if (live && h == 0) {
-            atomicMin(status + 1, (long long)g);
-            tree_acc_add(ta, g, scan[g]);
-        }
-        return;
-    }
-    // constrain (gaussian.cpp:74-90)
-    if (h == 0) {
-        gp[0] = clamp01d(gp[0]);
-        gp[1] = clamp01d(gp[1]);
-        double th = fmod(gp[2], kPi);
-        if (th < 0.0) th = __dadd_rn(th, kPi);
-        if (th >= kPi) th = 0.0;
-        gp[2] = th;
-        gp[3] = clamp_scale(gp[3]);
-    } else {
-        gp[0] = clamp_scale(gp[0]);
-        gp[1] = clamp01d(gp[1]);
-        gp[2] = clamp01d(gp[2]);
-        gp[3] = clamp01d(gp[3]);
-    }
-    if (live) {
-        double2* Pw = reinterpret_cast<double2*>(params + (size_t)g * 8 + 4 * h);
-        double2* Mw = reinterpret_cast<double2*>(m + (size_t)g * 8 + 4 * h);
-        double2* Vw = reinterpret_cast<double2*>(v + (size_t)g * 8 + 4 * h);
-        Pw[0] = make_double2(gp[0], gp[1]);
-        Pw[1] = make_double2(gp[2], gp[3]);
-        Mw[0] = make_double2(mm[0], mm[1]);
-        Mw[1] = make_double2(mm[2], mm[3]);
-        Vw[0] = make_double2(vv[0], vv[1]);
-        Vw[1] = make_double2(vv[2], vv[3]);
-    }
-    // prepared records: h = 1 gets theta and forms sin/cos; h = 0 gets s2
-    // and forms both reciprocals
-    const double theta = shx(gp[2]);  // on h = 1: lane 0's theta
-    const double s2 = shx(gp[0]);     // on h = 0: lane 1's s2
-    double a = 0.0, b = 0.0;          // h = 0: inv_s1, inv_s2; h = 1: sin, cos
-    if (h == 0) {
-        a = __ddiv_rn(1.0, gp[3]);
-        b = __ddiv_rn(1.0, s2);
-    } else {
-        glibc_math::sincos(theta, &a, &b);
-    }
-    const double oa = shx(a), ob = shx(b);
-    if (!live) return;
-    if (h == 0) {
-        ScanRec r;
-        r.mu_x = gp[0];
-        r.mu_y = gp[1];
-        r.cos_t = ob;
-        r.sin_t = oa;
-        r.inv_a = __dmul_rn(a, a);
-        r.inv_b = __dmul_rn(b, b);
-        scan[g] = r;
-        tree_acc_add(ta, g, r);
-    } else {
-        ShadeRec hh;
-        hh.r = gp[1];
-        hh.g = gp[2];
-        hh.b = gp[3];
-        hh.inv_s1 = oa;
-        hh.inv_s2 = ob;
-        hh.pad = 0.0;
-        shade[g] = hh;
-    }
-}
-
 
 // Sharded multi-rank update, after the parameter all-gather: the Gaussians
 // outside this rank's slice get their prepared records (kernel 1), their
@@ -1059,10 +814,12 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
             const bool shard = exch && R > 1 && ctx->opt_shard_adam && (size_t)B * R <= ctx->cap;
             const uint32_t lo = shard ? std::min(n, rk * B) : 0u, hi = shard ? std::min(n, lo + B) : n;
             if (hi > lo)
-                IGS_PDL(ctx, segment_adam_kernel, (hi - lo + 63) / 64, 128, 0, gcnt, (const uint32_t*)goff,
-                        (const uint32_t*)perm, (const double*)contrib, n, ctx->grads, ctx->params, ctx->adam_m,
-                        ctx->adam_v, ctx->scan, ctx->shade, fuse_lr4[0], fuse_lr4[1], fuse_lr4[2], fuse_lr4[3], bc1,
-                        bc2, 1.0 / bc1, 1.0 / bc2, ctx->status, ta, lo, hi, (const uint32_t*)bucket);
+                IGS_PDL(ctx, segment_adam_kernel<NoTail>, (hi - lo + 63) / 64, kAdamThreads, 0,
+                        AdamArgs{gcnt, (const uint32_t*)goff, (const uint32_t*)perm, (const uint32_t*)bucket,
+                                 (const double*)contrib, n, ctx->grads, ctx->params, ctx->adam_m, ctx->adam_v,
+                                 ctx->scan, ctx->shade, fuse_lr4[0], fuse_lr4[1], fuse_lr4[2], fuse_lr4[3], bc1, bc2,
+                                 1.0 / bc1, 1.0 / bc2, ctx->status, ta, lo, hi},
+                        NoTail{});
             if (shard) {
                 // flags of every slice, then every slice's parameters, then
                 // the records + tree accumulation of the other slices here
