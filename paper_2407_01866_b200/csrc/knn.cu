@@ -1667,18 +1667,19 @@ __device__ __forceinline__ void hard_merge_point(const ScanRec* __restrict__ sca
 }
 
 // The (point, split) items of the hard points (cnt of them) for a CTA of
-// at least kHardThreads threads, item = blockIdx.x, += gridDim.x.
+// at least kHardThreads threads: items first, first + stride, ...; sq / si:
+// kHardThreads * KCAP entries of the caller's shared memory.
 template <int KCAP>
 __device__ __forceinline__ void hard_scan_items(const ScanRec* __restrict__ scan, uint32_t n,
                                                 const double* __restrict__ uv, int W, int H, int kk, uint32_t cnt,
                                                 const uint32_t* __restrict__ hard_list, const Epi& E,
                                                 double* __restrict__ part_q, uint32_t* __restrict__ part_i,
                                                 unsigned int* __restrict__ point_done,
-                                                unsigned long long* __restrict__ pairs) {
-    __shared__ double sq[kHardThreads * KCAP];
-    __shared__ uint32_t si[kHardThreads * KCAP];
+                                                unsigned long long* __restrict__ pairs, uint32_t first,
+                                                uint32_t stride, double* sq /* kHardThreads * KCAP */,
+                                                uint32_t* si /* kHardThreads * KCAP */) {
     const uint32_t per = (n + kHardSplit - 1) / kHardSplit;
-    for (uint32_t item = blockIdx.x; item < cnt * kHardSplit; item += gridDim.x) {
+    for (uint32_t item = first; item < cnt * kHardSplit; item += stride) {
         const uint32_t slot = item / kHardSplit, split = item % kHardSplit;
         const uint32_t pt = hard_list[slot];
         double px, py;
@@ -1769,9 +1770,11 @@ __global__ void __launch_bounds__(kHardThreads) hard_scan_kernel(const ScanRec* 
                                                                  uint32_t* __restrict__ part_i,
                                                                  unsigned int* __restrict__ point_done,
                                                                  unsigned long long* __restrict__ pairs) {
+    __shared__ double sq[kHardThreads * KCAP];
+    __shared__ uint32_t si[kHardThreads * KCAP];
     pdl_wait();
     hard_scan_items<KCAP>(scan, n, uv, W, H, kk, min(*hard_count, kHardCap), hard_list, E, part_q, part_i, point_done,
-                          pairs);
+                          pairs, blockIdx.x, gridDim.x, sq, si);
 }
 
 // The hard-point scan and the reduction's offsets + scatter in one persistent
@@ -1791,12 +1794,17 @@ __global__ void __launch_bounds__(kOffThreads) hard_offsets_kernel(const ScanRec
                                                                    unsigned int* __restrict__ point_done,
                                                                    unsigned long long* __restrict__ pairs,
                                                                    OffArgs A, LongArgs LA, int fuse_long) {
+    __shared__ __align__(16) unsigned char s_raw[kLongSmemBytes > kHardThreads * KCAP * 12 ? kLongSmemBytes
+                                                                                         : kHardThreads * KCAP * 12];
     pdl_wait();
-    if (fuse_long && LA.dloss && blockIdx.x < kLossCtas) loss_chunk(LA, blockIdx.x);
+    if (fuse_long && LA.dloss && blockIdx.x < kLossCtas)
+        loss_chunk<kOffThreads>(LA, blockIdx.x, reinterpret_cast<double*>(s_raw));
     const uint32_t cnt = min(*hard_count, kHardCap);
     unsigned base = 0;
     if (cnt) {  // (uniform: every CTA read the same count)
-        hard_scan_items<KCAP>(scan, n, uv, W, H, kk, cnt, hard_list, E, part_q, part_i, point_done, pairs);
+        hard_scan_items<KCAP>(scan, n, uv, W, H, kk, cnt, hard_list, E, part_q, part_i, point_done, pairs, blockIdx.x,
+                              gridDim.x, reinterpret_cast<double*>(s_raw),
+                              reinterpret_cast<uint32_t*>(s_raw + kHardThreads * KCAP * 8));
         igs_grid_sync(A.bar, gridDim.x);
         base = gridDim.x;
     }
@@ -1805,7 +1813,9 @@ __global__ void __launch_bounds__(kOffThreads) hard_offsets_kernel(const ScanRec
     // (search epilogue) or the barrier above (hard points) -- uniform
     if (fuse_long && *(volatile const uint32_t*)LA.long_count) {
         igs_grid_sync(A.bar, base + gridDim.x);  // the overflow entries scattered
-        long_segments(LA, blockIdx.x, gridDim.x);
+        long_segments<kOffThreads>(LA, blockIdx.x, gridDim.x, reinterpret_cast<uint32_t*>(s_raw),
+                                   reinterpret_cast<uint32_t*>(s_raw) + kLongCap,
+                                   reinterpret_cast<double(*)[8]>(s_raw + (kLongCap + kLongRank) * 4));
     }
     grid_exit(A.bar);
 }

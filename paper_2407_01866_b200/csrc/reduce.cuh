@@ -136,23 +136,29 @@ __device__ __forceinline__ void grid_exit(unsigned* bar) {
     }
 }
 
-// Long segments: one CTA (kLongThreads threads) per queued Gaussian,
-// CTAs first, first + stride, ...  The slot ids are put in slot (= sample)
-// order in shared memory: up to kLongRank by counting ranks (rank = number
-// of smaller ids; ids are distinct), up to kLongCap by a bitonic sort, and
+// Long segments: one CTA (NT threads) per queued Gaussian, CTAs first,
+// first + stride, ...  The slot ids are put in slot (= sample) order in
+// shared memory: up to kLongRank by counting ranks (rank = number of
+// smaller ids; ids are distinct), up to kLongCap by a bitonic sort, and
 // beyond shared memory by ranks straight from global memory into `big`;
 // then 8 threads, one per parameter, accumulate the contribution rows in
-// that order, kLongRows rows gathered ahead of the dependent adds.
+// that order, kLongRows rows gathered ahead of the dependent adds.  After a
+// Gaussian's gradient is stored the whole CTA calls fin(g).  Shared memory
+// (the caller's): keys[kLongCap], sorted[kLongRank], rows[kLongRows][8].
 constexpr uint32_t kLongCap = 2048;
 constexpr uint32_t kLongRank = 256;  // up to here: rank by counting; above: bitonic sort
 constexpr int kLongThreads = 256;
 constexpr int kLongRows = 128;
 constexpr uint32_t kLossCtas = 8;    // CTAs that form the loss
+constexpr size_t kLongSmemBytes = kLongCap * 4 + kLongRank * 4 + kLongRows * 8 * sizeof(double);
 
-__device__ __forceinline__ void long_segments(const LongArgs& A, uint32_t first, uint32_t stride) {
-    __shared__ uint32_t keys[kLongCap];
-    __shared__ uint32_t sorted[kLongRank];
-    __shared__ double rows[kLongRows][8];
+struct NoFin {
+    __device__ void operator()(uint32_t) const {}
+};
+
+template <int NT, class Fin = NoFin>
+__device__ __forceinline__ void long_segments(const LongArgs& A, uint32_t first, uint32_t stride, uint32_t* keys,
+                                              uint32_t* sorted, double (*rows)[8], Fin fin = Fin{}) {
     const uint32_t total = *(volatile const uint32_t*)A.long_count;
     const int t = threadIdx.x;
     for (uint32_t it = first; it < total; it += stride) {
@@ -165,9 +171,9 @@ __device__ __forceinline__ void long_segments(const LongArgs& A, uint32_t first,
         const uint32_t* out = sorted;
         __syncthreads();
         if (m <= kLongRank) {
-            for (uint32_t e = t; e < m; e += kLongThreads) keys[e] = slot_at(e);
+            for (uint32_t e = t; e < m; e += NT) keys[e] = slot_at(e);
             __syncthreads();
-            for (uint32_t e = t; e < m; e += kLongThreads) {
+            for (uint32_t e = t; e < m; e += NT) {
                 const uint32_t v = keys[e];
                 uint32_t r = 0;
                 for (uint32_t j = 0; j < m; ++j) r += keys[j] < v;
@@ -177,11 +183,11 @@ __device__ __forceinline__ void long_segments(const LongArgs& A, uint32_t first,
             // bitonic sort in shared memory, padded to a power of two
             uint32_t pow2 = 1;
             while (pow2 < m) pow2 <<= 1;
-            for (uint32_t e = t; e < pow2; e += kLongThreads) keys[e] = e < m ? slot_at(e) : 0xFFFFFFFFu;
+            for (uint32_t e = t; e < pow2; e += NT) keys[e] = e < m ? slot_at(e) : 0xFFFFFFFFu;
             __syncthreads();
             for (uint32_t size = 2; size <= pow2; size <<= 1)
                 for (uint32_t stride2 = size >> 1; stride2 > 0; stride2 >>= 1) {
-                    for (uint32_t e = t; e < pow2; e += kLongThreads) {
+                    for (uint32_t e = t; e < pow2; e += NT) {
                         const uint32_t partner = e ^ stride2;
                         if (partner > e) {
                             const bool up = (e & size) == 0;
@@ -198,7 +204,7 @@ __device__ __forceinline__ void long_segments(const LongArgs& A, uint32_t first,
         } else {
             // beyond shared memory (degenerate sets): rank from global
             // memory into the same range of a second slot array
-            for (uint32_t e = t; e < m; e += kLongThreads) {
+            for (uint32_t e = t; e < m; e += NT) {
                 const uint32_t v = slot_at(e);
                 uint32_t r = 0;
                 for (uint32_t j = 0; j < m; ++j) r += slot_at(j) < v;
@@ -210,13 +216,13 @@ __device__ __forceinline__ void long_segments(const LongArgs& A, uint32_t first,
         double acc = 0.0;
         for (uint32_t base = 0; base < m; base += kLongRows) {
             const uint32_t cnt = min((uint32_t)kLongRows, m - base);
-            if ((uint32_t)t < cnt) {
-                const double2* c = reinterpret_cast<const double2*>(A.contrib + (size_t)out[base + t] * 8);
+            for (uint32_t r = t; r < cnt; r += NT) {
+                const double2* c = reinterpret_cast<const double2*>(A.contrib + (size_t)out[base + r] * 8);
 #pragma unroll
                 for (int h = 0; h < 4; ++h) {
                     const double2 v = c[h];
-                    rows[t][2 * h] = v.x;
-                    rows[t][2 * h + 1] = v.y;
+                    rows[r][2 * h] = v.x;
+                    rows[r][2 * h + 1] = v.y;
                 }
             }
             __syncthreads();
@@ -228,21 +234,23 @@ __device__ __forceinline__ void long_segments(const LongArgs& A, uint32_t first,
             A.grads[(size_t)g * 8 + t] = acc;
             if (!isfinite(acc)) atomicMin(A.status, (long long)g * 8 + t);  // adam.cpp:29-31 (first (i, p))
         }
+        __syncthreads();
+        fin(g);
     }
 }
 
 // The loss (fit.cpp:87-89: mean of the per-sample L1 losses): chunk c of
-// kLossCtas summed by one CTA (kLongThreads threads, a fixed tree), the
+// kLossCtas summed by one CTA (NT threads, a fixed tree), the
 // chunks combined in order by whichever CTA finishes last.
-__device__ __forceinline__ void loss_chunk(const LongArgs& A, uint32_t c) {
-    __shared__ double red[kLongThreads];
+template <int NT>
+__device__ __forceinline__ void loss_chunk(const LongArgs& A, uint32_t c, double* red /* NT */) {
     const int t = threadIdx.x;
     const uint32_t per = (A.ns + kLossCtas - 1) / kLossCtas, l0 = c * per, l1 = min(A.ns, l0 + per);
     double acc = 0.0;
-    for (uint32_t i = l0 + t; i < l1; i += kLongThreads) acc = __dadd_rn(acc, A.losses[i]);
+    for (uint32_t i = l0 + t; i < l1; i += NT) acc = __dadd_rn(acc, A.losses[i]);
     red[t] = acc;
     __syncthreads();
-    for (int s = kLongThreads / 2; s > 0; s >>= 1) {
+    for (int s = NT / 2; s > 0; s >>= 1) {
         if (t < s) red[t] = __dadd_rn(red[t], red[t + s]);
         __syncthreads();
     }

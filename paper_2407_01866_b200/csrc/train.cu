@@ -256,14 +256,17 @@ __global__ void segment_sum_kernel(const uint32_t* __restrict__ gcnt, const uint
 // loss_chunk); this launch is the path where the search's hard-point launch
 // does not take them over.
 __global__ void __launch_bounds__(kLongThreads) long_segment_kernel(LongArgs A) {
+    __shared__ __align__(16) unsigned char s_raw[kLongSmemBytes];
     pdl_wait();
     if (A.dloss && blockIdx.x >= gridDim.x - kLossCtas) {
         // the last kLossCtas CTAs form the loss while the others take the
         // long segments
-        loss_chunk(A, blockIdx.x - (gridDim.x - kLossCtas));
+        loss_chunk<kLongThreads>(A, blockIdx.x - (gridDim.x - kLossCtas), reinterpret_cast<double*>(s_raw));
         return;
     }
-    long_segments(A, blockIdx.x, A.dloss ? gridDim.x - kLossCtas : gridDim.x);
+    long_segments<kLongThreads>(A, blockIdx.x, A.dloss ? gridDim.x - kLossCtas : gridDim.x,
+                                reinterpret_cast<uint32_t*>(s_raw), reinterpret_cast<uint32_t*>(s_raw) + kLongCap,
+                                reinterpret_cast<double(*)[8]>(s_raw + (kLongCap + kLongRank) * 4));
 }
 
 // Multi-rank exchange: per-Gaussian counts over every rank's contributions,
