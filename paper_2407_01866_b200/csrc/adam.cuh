@@ -184,12 +184,26 @@ __device__ __forceinline__ void adam_pair_update(const AdamArgs& A, uint32_t g, 
 struct NoTail {
     static constexpr bool kWorkers = false;
     static constexpr size_t kSmemBytes = 0;
+    __device__ void pre(unsigned char*) const {}
     __device__ void run(uint32_t, uint32_t, const AdamArgs&, unsigned char*) const {}
     __device__ bool hold() const { return false; }
     __device__ void wait() const {}
 };
 
 constexpr int kAdamThreads = 128;  // 64 Gaussians per CTA
+
+// The loss chunks (reduce.cuh loss_chunk) by the first kLossCtas CTAs before
+// their Gaussians: the launch before the update then has nothing to do in
+// the common case (no hard points, no long segments).
+struct LossTail : NoTail {
+    LongArgs L;
+    __device__ void pre(unsigned char* smem) const {
+        if (L.dloss && blockIdx.x < kLossCtas) {
+            loss_chunk<kAdamThreads>(L, blockIdx.x, reinterpret_cast<double*>(smem));
+            __syncthreads();  // (the shared memory is the sort's next)
+        }
+    }
+};
 
 }  // namespace igs_dev
 
@@ -209,6 +223,7 @@ __global__ void __launch_bounds__(kAdamThreads, IGS_ADAM_MINB) segment_adam_kern
     constexpr size_t kSorted = 4 * 16 * kShortSeg * sizeof(uint32_t);
     __shared__ __align__(16) unsigned char s_raw[Tail::kSmemBytes > kSorted ? Tail::kSmemBytes : kSorted];
     pdl_wait();
+    T.pre(s_raw);
     uint32_t blk = blockIdx.x;
     if constexpr (Tail::kWorkers) {
         __shared__ uint32_t s_role;

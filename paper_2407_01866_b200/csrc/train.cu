@@ -644,6 +644,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
     uint32_t *bucket = nullptr, *ovf = nullptr, *ovf_list = nullptr, *big = nullptr;
     double* loss_part = nullptr;
     bool long_fused = false;  // the long segments + loss ran in the search's hard-point launch
+    bool loss_in_adam = false;  // the loss runs in the update's first CTAs instead
     auto long_args = [&]() {
         return LongArgs{(const uint32_t*)gcnt, (const uint32_t*)goff, (const uint32_t*)perm, (const double*)contrib,
                         ctx->grads, (const uint32_t*)(bucket ? ovf + 2 : long_ctl), (const uint32_t*)(long_ctl + 1),
@@ -723,6 +724,11 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
                 ctx->fuse_off.args.long_count = ovf + 2;
                 ctx->fuse_off.long_args = long_args();
                 ctx->fuse_off.fuse_long = getenv("IGS_LONG_LAUNCH") == nullptr;  // (A/B: the separate launch)
+                if (ctx->fuse_off.fuse_long && getenv("IGS_LOSS_OFF") == nullptr) {
+                    // the loss moves on into the update's first CTAs (LossTail)
+                    ctx->fuse_off.long_args.dloss = nullptr;
+                    loss_in_adam = mode == 0 && dev_loss;
+                }
             }
         }
         e = igs_knn_forward_backward(ctx, mode, dev_sidx, dev_samples5, ns, kk, inv_n, losses + (size_t)rk * ns,
@@ -817,12 +823,12 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
             const bool shard = exch && R > 1 && ctx->opt_shard_adam && (size_t)B * R <= ctx->cap;
             const uint32_t lo = shard ? std::min(n, rk * B) : 0u, hi = shard ? std::min(n, lo + B) : n;
             if (hi > lo)
-                IGS_PDL(ctx, segment_adam_kernel<NoTail>, (hi - lo + 63) / 64, kAdamThreads, 0,
+                IGS_PDL(ctx, segment_adam_kernel<LossTail>, (hi - lo + 63) / 64, kAdamThreads, 0,
                         AdamArgs{gcnt, (const uint32_t*)goff, (const uint32_t*)perm, (const uint32_t*)bucket,
                                  (const double*)contrib, n, ctx->grads, ctx->params, ctx->adam_m, ctx->adam_v,
                                  ctx->scan, ctx->shade, fuse_lr4[0], fuse_lr4[1], fuse_lr4[2], fuse_lr4[3], bc1, bc2,
                                  1.0 / bc1, 1.0 / bc2, ctx->status, ta, lo, hi},
-                        NoTail{});
+                        LossTail{{}, loss_in_adam ? long_args() : LongArgs{}});
             if (shard) {
                 // flags of every slice, then every slice's parameters, then
                 // the records + tree accumulation of the other slices here
