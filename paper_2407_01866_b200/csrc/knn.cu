@@ -1812,12 +1812,13 @@ __global__ void __launch_bounds__(kOffThreads) hard_offsets_kernel(const ScanRec
     // bucket mode: the long-segment queue was complete before the launch
     // (search epilogue) or the barrier above (hard points) -- uniform
     if (fuse_long && *(volatile const uint32_t*)LA.long_count) {
-        igs_grid_sync(A.bar, base + gridDim.x);  // the overflow entries scattered
+        base += gridDim.x;
+        igs_grid_sync(A.bar, base);  // the overflow entries scattered
         long_segments<kOffThreads>(LA, blockIdx.x, gridDim.x, reinterpret_cast<uint32_t*>(s_raw),
                                    reinterpret_cast<uint32_t*>(s_raw) + kLongCap,
                                    reinterpret_cast<double(*)[8]>(s_raw + (kLongCap + kLongRank) * 4));
     }
-    grid_exit(A.bar);
+    if (base) grid_exit(A.bar);  // (no barrier used -- the common case -- nothing to reset; uniform)
 }
 
 

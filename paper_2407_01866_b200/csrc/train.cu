@@ -170,8 +170,7 @@ __global__ void scatter_slots_kernel(const uint32_t* __restrict__ keys, uint32_t
 
 __global__ void __launch_bounds__(kOffThreads) offsets_scatter_kernel(OffArgs A) {
     pdl_wait();
-    offsets_scatter_body(A, 0);
-    grid_exit(A.bar);
+    if (offsets_scatter_body(A, 0)) grid_exit(A.bar);  // (a barrier was used: reset the counters)
 }
 
 __device__ __forceinline__ void sum_row(const double* __restrict__ contrib, uint32_t slot, double* acc) {
