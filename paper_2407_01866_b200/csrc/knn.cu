@@ -1217,7 +1217,10 @@ __global__ void __launch_bounds__(128, 9) knn_points_kernel(const ScanRec* __res
 // shuffles, the epilogue's blend chain), and a batch merge sorts 16
 // candidates instead of 32.  The selection is the same exact (q, idx) top-K.
 constexpr int kQueue16 = 256;   // per-half frontier capacity
-constexpr int kMergeMin16 = 5;  // candidates per half-batch from which merge() is used
+#ifndef IGS_MERGE_MIN16
+#define IGS_MERGE_MIN16 4
+#endif
+constexpr int kMergeMin16 = IGS_MERGE_MIN16;  // candidates per half-batch from which merge() is used
 
 __device__ __forceinline__ unsigned half_bits(unsigned ballot) { return (ballot >> (threadIdx.x & 16)) & 0xffffu; }
 __device__ __forceinline__ int other_half(int v) { return __shfl_xor_sync(0xffffffffu, v, 16); }

@@ -44,5 +44,5 @@ for r in data:
         pass
 ti, ts = sum(agg_i.values()), sum(agg_s.values())
 print(f"total instructions {ti}, stall samples {ts}")
-for k, v in agg_i.most_common(40):
+for k, v in agg_i.most_common(int(os.environ.get("LP_TOP", "40"))):
     print(f"{k:32s} instr {v:9d} ({100*v/ti:5.1f}%)  stalls {agg_s[k]:6d} ({100*agg_s[k]/max(ts,1):5.1f}%)")
