@@ -1221,6 +1221,10 @@ constexpr int kQueue16 = 256;   // per-half frontier capacity
 #define IGS_MERGE_MIN16 4
 #endif
 constexpr int kMergeMin16 = IGS_MERGE_MIN16;  // candidates per half-batch from which merge() is used
+#ifndef IGS_FLAT_START16
+#define IGS_FLAT_START16 2
+#endif
+constexpr int kFlatStart16 = IGS_FLAT_START16;  // the descent starts flat at level lg0 - this (a 4^this-cell grid)
 
 __device__ __forceinline__ unsigned half_bits(unsigned ballot) { return (ballot >> (threadIdx.x & 16)) & 0xffffu; }
 __device__ __forceinline__ int other_half(int v) { return __shfl_xor_sync(0xffffffffu, v, 16); }
@@ -1474,7 +1478,7 @@ __global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __r
     bool overflow = false;
     uint32_t* cur = queue[warp][hh][0];
     uint32_t* nxt = queue[warp][hh][1];
-    const int ls = min(L.levels - 1, max(lg0 - 2, 0));
+    const int ls = min(L.levels - 1, max(lg0 - kFlatStart16, 0));
     {
         const uint32_t c0 = ls + 1 < L.levels ? (uint32_t)s_loff[ls + 1] : 0u;
         const uint32_t nup = ls + 1 < L.levels ? (uint32_t)(s_loff[L.levels - 1] + 1) - c0 : 0u;
