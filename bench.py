@@ -319,6 +319,27 @@ def run_ours(args, rank, world, local_rank, dist):
                 "reference_equivalent_pairs_per_launch": float(NS) * N / world,
                 "reference_equivalent_gop_s": float(NS) * N / world * OPS_PER_PAIR / (
                     scan_ms * 1e-3 / max(scan_launches, 1)) / 1e9}
+    # the search is issue-bound (ncu: ~54 % of issue slots busy), so its
+    # other roofline is instruction issue: the committed capture's warp
+    # instructions per launch over this run's launch time, against 4 warp
+    # instructions per cycle per SM at the SM clock
+    issue_roof = None
+    ninstr = ncu_field("knn_points16_kernel", "warp_instructions_per_launch")
+    if scan_ms > 0 and ninstr:
+        try:
+            import torch
+            sms = torch.cuda.get_device_properties(local_rank).multi_processor_count
+        except Exception:
+            sms = 148
+        mhz = float(clk.get("sm_max_mhz") or 1965.0)
+        peak_wi = sms * 4 * mhz * 1e6
+        wi_s = ninstr / (scan_ms * 1e-3 / max(scan_launches, 1))
+        issue_roof = {"kernel": "top-K candidate scan (knn_points16_kernel)", "bound": "issue",
+                      "achieved": wi_s / 1e9, "peak": peak_wi / 1e9, "unit": "G warp-instructions/s",
+                      "frac": wi_s / peak_wi,
+                      "work_per_launch": f"{ninstr:.4g} warp instructions (profiles/r2_traffic.json, ncu at "
+                                        "--steps 20 --warmup 5)",
+                      "peak_source": f"{sms} SMs x 4 schedulers x {mhz:.0f} MHz"}
     adam_ms, adam_launches, adam_bytes = prof["adam"]
     hbm = None
     try:
@@ -395,7 +416,7 @@ def run_ours(args, rank, world, local_rank, dist):
                 "wall_clock_note": "host perf_counter over the whole loop, including the 512 MiB L2 flush "
                                    "memsets between steps; _excl_flush subtracts those memsets' device time "
                                    "(timed alone)"},
-        "roofline": roof, "roofline_adam": adam_roof,
+        "roofline": roof, "roofline_issue": issue_roof, "roofline_adam": adam_roof,
         "profile_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
         "knn_hard_points_per_step": prof["knn_hard"][2] / args.steps,
         "pairs_per_sample": prof["scan"][2] / args.steps / max(NS // world, 1),
@@ -555,6 +576,13 @@ def secondary_fit(ctx):
             "trained_state_step": {"t": "5006-5025", "iters_per_s": 1e3 * len(ms) / sum(ms),
                                    "ms_per_step": sum(ms) / len(ms),
                                    "note": "the fitted 100k set (t = 5000), uniform samples, L2 flushed per step"}}
+
+
+def ncu_field(kernel: str, field: str):
+    try:
+        return json.loads((ROOT / "profiles" / "r2_traffic.json").read_text())[kernel][field]
+    except Exception:
+        return None
 
 
 def ncu_traffic(kernel: str):
