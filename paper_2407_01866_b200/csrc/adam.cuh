@@ -45,8 +45,8 @@ __device__ __forceinline__ double shx(double v) { return __shfl_xor_sync(0xfffff
 struct AdamArgs {
     uint32_t* gcnt;          // per-Gaussian contribution counts | [n, 2n) cursors; left zeroed
     const uint32_t* goff;    // CSR mode: segment offsets
-    const uint32_t* perm;    // CSR mode: slot ids by segment
-    const uint32_t* bucket;  // bucket mode (reduce.cuh): slot ids by Gaussian, or null
+    uint32_t* perm;          // CSR mode: slot ids by segment (short ones put in order in place)
+    uint32_t* bucket;        // bucket mode (reduce.cuh): slot ids by Gaussian, or null (ditto)
     const double* contrib;
     uint32_t n;
     double* grads;
@@ -196,6 +196,7 @@ constexpr int kAdamThreads = 128;  // 64 Gaussians per CTA
 // their Gaussians: the launch before the update then has nothing to do in
 // the common case (no hard points, no long segments).
 struct LossTail : NoTail {
+    static constexpr size_t kSmemBytes = kAdamThreads * sizeof(double);
     LongArgs L;
     __device__ void pre(unsigned char* smem) const {
         if (L.dloss && blockIdx.x < kLossCtas) {
@@ -220,8 +221,7 @@ using namespace igs_dev;
 #endif
 template <class Tail>
 __global__ void __launch_bounds__(kAdamThreads, IGS_ADAM_MINB) segment_adam_kernel(AdamArgs A, Tail T) {
-    constexpr size_t kSorted = 4 * 16 * kShortSeg * sizeof(uint32_t);
-    __shared__ __align__(16) unsigned char s_raw[Tail::kSmemBytes > kSorted ? Tail::kSmemBytes : kSorted];
+    __shared__ __align__(16) unsigned char s_raw[Tail::kSmemBytes > 16 ? Tail::kSmemBytes : 16];
     pdl_wait();
     T.pre(s_raw);
     uint32_t blk = blockIdx.x;
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kAdamThreads, IGS_ADAM_MINB) segment_adam_kern
     const uint32_t g = g0 < A.g_end ? g0 : A.g_end - 1;  // dead pairs shadow a live one (no writes): full shuffles
     // a short segment's slot ids: its bucket (reduce.cuh), else perm[goff[g] ...]
     const bool from_bucket = A.bucket != nullptr;
-    const uint32_t* __restrict__ seg = from_bucket ? A.bucket : A.perm;
+    uint32_t* __restrict__ seg = from_bucket ? A.bucket : A.perm;
     uint32_t cntg = 0;
     size_t og = 0;
     if (h == 0) {
@@ -261,25 +261,44 @@ __global__ void __launch_bounds__(kAdamThreads, IGS_ADAM_MINB) segment_adam_kern
         A.gcnt[A.n + g] = 0;
     }
     const bool skip_all = A.status[2] != LLONG_MAX;
-    // segments of 5..kShortSeg slot ids: put in slot order by the whole warp,
-    // one segment at a time (lane e loads id e -- one row of the bucket --
-    // and takes its rank among the others by shuffles; distinct ids), into
-    // this pair's row of s_sorted.  Dead pairs shadow a live Gaussian, so
-    // they sort (and later read) a valid segment too.
-    auto s_sorted = reinterpret_cast<uint32_t(*)[16][kShortSeg]>(s_raw);
-    uint32_t* my_sorted = s_sorted[(threadIdx.x >> 5) & 3][(threadIdx.x & 31) >> 1];
+    // segments of 5..kShortSeg slot ids: put in slot order in place by the
+    // whole warp, one segment at a time -- lane e loads ids e, e + 32, ...
+    // (one row of the bucket), takes each one's rank among the others by
+    // shuffles (ids are distinct) and writes it back at its rank; the pair
+    // then reads its segment in order.  Only live pairs sort (a dead pair
+    // shadowing a Gaussian of another warp would sort the same ids
+    // concurrently); a dead pair's sum reads whatever is there and is
+    // never written.
     {
+        constexpr int kPer = (kShortSeg + 31) / 32;
         const int lane = threadIdx.x & 31;
-        unsigned med = __ballot_sync(0xffffffffu, !skip_all && h == 0 && cntg > 4 && cntg <= kShortSeg);
+        unsigned med = __ballot_sync(0xffffffffu, live && !skip_all && h == 0 && cntg > 4 && cntg <= kShortSeg);
         while (med) {
             const int src = __ffs(med) - 1;
             med &= med - 1;
             const uint32_t mm = __shfl_sync(0xffffffffu, cntg, src);
             const size_t oo = __shfl_sync(0xffffffffu, og, src);
-            const uint32_t v = (uint32_t)lane < mm ? seg[oo + lane] : 0xFFFFFFFFu;
-            uint32_t r = 0;
-            for (uint32_t j = 0; j < mm; ++j) r += __shfl_sync(0xffffffffu, v, j) < v;
-            if ((uint32_t)lane < mm) s_sorted[(threadIdx.x >> 5) & 3][src >> 1][r] = v;
+            uint32_t v[kPer], r[kPer];
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) {
+                const uint32_t e = (uint32_t)(lane + 32 * j);
+                v[j] = e < mm ? seg[oo + e] : 0xFFFFFFFFu;
+                r[j] = 0;
+            }
+#pragma unroll
+            for (int jj = 0; jj < kPer; ++jj) {
+                if (32u * jj >= mm) break;  // (uniform)
+                const uint32_t lim = min(32u, mm - 32u * jj);
+                for (uint32_t sl = 0; sl < lim; ++sl) {
+                    const uint32_t u = __shfl_sync(0xffffffffu, v[jj], sl);
+#pragma unroll
+                    for (int j = 0; j < kPer; ++j) r[j] += u < v[j];
+                }
+            }
+            __syncwarp();  // every id read before any is overwritten
+#pragma unroll
+            for (int j = 0; j < kPer; ++j)
+                if ((uint32_t)(lane + 32 * j) < mm) seg[oo + r[j]] = v[j];
         }
         __syncwarp();
     }
@@ -321,7 +340,7 @@ __global__ void __launch_bounds__(kAdamThreads, IGS_ADAM_MINB) segment_adam_kern
                 if (cntg > 2) add_row(s2);
                 if (cntg > 3) add_row(s3);
             } else {
-                for (uint32_t e = 0; e < cntg; ++e) add_row(my_sorted[e]);  // (sorted above)
+                for (uint32_t e = 0; e < cntg; ++e) add_row(seg[og + e]);  // (sorted in place above)
             }
             if (live) {
                 double2* o2 = reinterpret_cast<double2*>(A.grads + (size_t)g * 8 + 4 * h);

@@ -8,9 +8,9 @@
 
 namespace igs_dev {
 
-constexpr uint32_t kShortSeg = 32;  // longer segments go to long_segment_kernel
+constexpr uint32_t kShortSeg = 128;  // longer segments go to long_segment_kernel
 // Segment buckets: the search epilogue files each slot id at
-// bucket[g][arrival rank] while the rank is below kBucket (every short
+// bucket[g][arrival rank] while the rank is below kBucket = 128 (every short
 // segment is then complete in its bucket: Adam sorts and sums it there, no
 // offsets, no scatter).  Later arrivals are overflow entries -- (slot, rank)
 // appended to a list -- and a Gaussian's first one queues it as a long

@@ -823,7 +823,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
             const uint32_t lo = shard ? std::min(n, rk * B) : 0u, hi = shard ? std::min(n, lo + B) : n;
             if (hi > lo)
                 IGS_PDL(ctx, segment_adam_kernel<LossTail>, (hi - lo + 63) / 64, kAdamThreads, 0,
-                        AdamArgs{gcnt, (const uint32_t*)goff, (const uint32_t*)perm, (const uint32_t*)bucket,
+                        AdamArgs{gcnt, (const uint32_t*)goff, perm, bucket,
                                  (const double*)contrib, n, ctx->grads, ctx->params, ctx->adam_m, ctx->adam_v,
                                  ctx->scan, ctx->shade, fuse_lr4[0], fuse_lr4[1], fuse_lr4[2], fuse_lr4[3], bc1, bc2,
                                  1.0 / bc1, 1.0 / bc2, ctx->status, ta, lo, hi},
