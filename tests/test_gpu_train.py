@@ -304,13 +304,16 @@ def test_alternate_kernels_bit_identical(gctx, port, monkeypatch, k):
     assert np.array_equal(p0, p1)
 
 
-@pytest.mark.parametrize("n,ns,k", [(5, 9000, 10), (40, 9000, 10), (300, 9000, 10), (3000, 4000, 10)])
+@pytest.mark.parametrize("n,ns,k", [(5, 9000, 10), (40, 9000, 10), (300, 9000, 10), (3000, 4000, 10),
+                                    (1057, 6000, 10)])
 def test_fused_iterations_long_segments_vs_reference(gctx, ref, monkeypatch, n, ns, k):
     """Fused iterations (search -> segment buckets -> long segments -> Adam)
     where Gaussians take from a few to thousands of contributions each: the
     bucket path (ranks < 32 in the bucket, later ranks as overflow entries
     in a bump-allocated region) and the plain CSR path (IGS_NO_BUCKET) both
-    reproduce the reference's losses, parameters and moments bit for bit."""
+    reproduce the reference's losses, parameters and moments bit for bit.
+    (1057: a partial last CTA whose dead pairs shadow a Gaussian with a
+    5..128-slot segment, which only its live pair may sort in place.)"""
     target = synth.photo_like_image(64, 48, 31013)
     params = np.ascontiguousarray(ref.initialize_set(target, n, 0.3, 41))
     if n <= 300:
