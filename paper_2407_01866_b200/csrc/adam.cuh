@@ -190,7 +190,10 @@ struct NoTail {
     __device__ void wait() const {}
 };
 
-constexpr int kAdamThreads = 128;  // 64 Gaussians per CTA
+#ifndef IGS_ADAM_THREADS
+#define IGS_ADAM_THREADS 128
+#endif
+constexpr int kAdamThreads = IGS_ADAM_THREADS;  // kAdamThreads / 2 Gaussians per CTA
 
 // The loss chunks (reduce.cuh loss_chunk) by the first kLossCtas CTAs before
 // their Gaussians: the launch before the update then has nothing to do in

@@ -822,7 +822,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
             const bool shard = exch && R > 1 && ctx->opt_shard_adam && (size_t)B * R <= ctx->cap;
             const uint32_t lo = shard ? std::min(n, rk * B) : 0u, hi = shard ? std::min(n, lo + B) : n;
             if (hi > lo)
-                IGS_PDL(ctx, segment_adam_kernel<LossTail>, (hi - lo + 63) / 64, kAdamThreads, 0,
+                IGS_PDL(ctx, segment_adam_kernel<LossTail>, (hi - lo + kAdamThreads / 2 - 1) / (kAdamThreads / 2), kAdamThreads, 0,
                         AdamArgs{gcnt, (const uint32_t*)goff, perm, bucket,
                                  (const double*)contrib, n, ctx->grads, ctx->params, ctx->adam_m, ctx->adam_v,
                                  ctx->scan, ctx->shade, fuse_lr4[0], fuse_lr4[1], fuse_lr4[2], fuse_lr4[3], bc1, bc2,
