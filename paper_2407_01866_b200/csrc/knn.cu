@@ -1352,7 +1352,10 @@ __device__ __forceinline__ void eval_members16(HalfTopK& t, uint32_t o_mine, uin
     }
 }
 
-__global__ void __launch_bounds__(128, 9) knn_points16_kernel(const ScanRec* __restrict__ scan, uint32_t n, Lq L,
+#ifndef IGS_KNN16_MINB
+#define IGS_KNN16_MINB 9
+#endif
+__global__ void __launch_bounds__(128, IGS_KNN16_MINB) knn_points16_kernel(const ScanRec* __restrict__ scan, uint32_t n, Lq L,
                                                               const Sum* __restrict__ own,
                                                               const Sum* __restrict__ sub,
                                                               const uint32_t* __restrict__ off,
