@@ -575,6 +575,8 @@ def secondary_fit(ctx):
             "psnr_per_eval": [round(e["psnr"], 4) for e in rep["evals"]],
             "trained_state_step": {"t": "5006-5025", "iters_per_s": 1e3 * len(ms) / sum(ms),
                                    "ms_per_step": sum(ms) / len(ms),
+                                   "ms_per_step_median": statistics.median(ms),
+                                   "ms_per_step_min_max": [min(ms), max(ms)],
                                    "note": "the fitted 100k set (t = 5000), uniform samples, L2 flushed per step"}}
 
 
