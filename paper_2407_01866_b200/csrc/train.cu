@@ -683,7 +683,12 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
         // fused: exact top-K search + blend / loss / gradient epilogue per warp
         // the fused Adam's parameter rows and moments, prefetched during the search
         L2Prefetch pf{};
-        if (fuse_lr4) {
+        // only while the rows fit comfortably in L2 (126 MB): at C4 (192 MB of
+        // rows) the prefetch only slowed the search, 107.6 -> 80.5 us without
+        // it, Adam unchanged (IGS_ADAM_PF_LIMIT_MB overrides the 48 MB limit)
+        static const size_t pf_limit =
+            (size_t)(getenv("IGS_ADAM_PF_LIMIT_MB") ? atol(getenv("IGS_ADAM_PF_LIMIT_MB")) : 48) << 20;
+        if (fuse_lr4 && (size_t)n * 192 <= pf_limit) {
             l2pf_add(pf, ctx->params, (size_t)n * 64);
             l2pf_add(pf, ctx->adam_m, (size_t)n * 64);
             l2pf_add(pf, ctx->adam_v, (size_t)n * 64);
