@@ -281,8 +281,9 @@ def test_alternate_kernels_bit_identical(gctx, port, monkeypatch, k):
     """The K <= 16 search runs two points per warp (knn_points16_kernel) and
     the reduction's offsets + scatter run as one persistent launch; the
     one-point-per-warp search (IGS_KNN_FULLWARP), the CUB scan + scatter
-    (IGS_SCAN_LAUNCHES) and the five-launch tree build (IGS_KNN_BUILD_LAUNCHES)
-    select and sum identically, so 8 iterations give the same
+    (IGS_SCAN_LAUNCHES), the five-launch tree build (IGS_KNN_BUILD_LAUNCHES)
+    and the long-segment / loss placement switches (IGS_LONG_LAUNCH,
+    IGS_LOSS_OFF) select and sum identically, so 8 iterations give the same
     losses and parameters bit for bit (K = 24 takes the full-warp search
     either way)."""
     target = synth.photo_like_image(160, 120, 31013)
@@ -299,6 +300,8 @@ def test_alternate_kernels_bit_identical(gctx, port, monkeypatch, k):
     monkeypatch.setenv("IGS_KNN_FULLWARP", "1")
     monkeypatch.setenv("IGS_SCAN_LAUNCHES", "1")
     monkeypatch.setenv("IGS_KNN_BUILD_LAUNCHES", "1")
+    monkeypatch.setenv("IGS_LONG_LAUNCH", "1")
+    monkeypatch.setenv("IGS_LOSS_OFF", "1")
     l1, p1 = run()
     assert l0 == l1
     assert np.array_equal(p0, p1)
