@@ -300,9 +300,14 @@ def test_alternate_kernels_bit_identical(gctx, port, monkeypatch, k):
     monkeypatch.setenv("IGS_KNN_FULLWARP", "1")
     monkeypatch.setenv("IGS_SCAN_LAUNCHES", "1")
     monkeypatch.setenv("IGS_KNN_BUILD_LAUNCHES", "1")
-    monkeypatch.setenv("IGS_LONG_LAUNCH", "1")
-    monkeypatch.setenv("IGS_LOSS_OFF", "1")
     l1, p1 = run()
+    for v in ("IGS_KNN_FULLWARP", "IGS_SCAN_LAUNCHES", "IGS_KNN_BUILD_LAUNCHES"):
+        monkeypatch.delenv(v)
+    monkeypatch.setenv("IGS_LONG_LAUNCH", "1")  # (bucket mode: the default reduction)
+    monkeypatch.setenv("IGS_LOSS_OFF", "1")
+    l2, p2 = run()
+    assert l0 == l2
+    assert np.array_equal(p0, p2)
     assert l0 == l1
     assert np.array_equal(p0, p1)
 
