@@ -48,7 +48,8 @@ struct Rng {
 };
 
 // sampling.cpp:14-23
-double kahan_sum(const std::vector<double>& v) {
+template <class V>
+double kahan_sum(const V& v) {
     double sum = 0.0, comp = 0.0;
     for (double x : v) {
         const double y = x - comp;
@@ -61,19 +62,53 @@ double kahan_sum(const std::vector<double>& v) {
 
 // Runs f(begin, end) over [0, n) on the host's cores (per-element work with
 // no cross-element arithmetic, so the split does not change any result).
-template <class F>
-void parallel_for(size_t n, F f) {
+// A vector whose resize leaves new elements uninitialised (they are
+// written by the caller, in parallel -- which also spreads the first-touch
+// page faults of a fresh 32 MB table over the host's cores).
+template <class T>
+struct NoInit : std::allocator<T> {
+    template <class U>
+    struct rebind {
+        using other = NoInit<U>;
+    };
+    NoInit() = default;
+    template <class U>
+    NoInit(const NoInit<U>&) {}
+    template <class U>
+    void construct(U* p) noexcept {
+        ::new (static_cast<void*>(p)) U;
+    }
+    template <class U, class... A>
+    void construct(U* p, A&&... a) {
+        ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+    }
+};
+template <class T>
+using fast_vector = std::vector<T, NoInit<T>>;
+
+size_t parallel_parts(size_t n) {
     const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-    const size_t parts = std::min<size_t>(hw, std::max<size_t>(1, n / 65536));
+    return std::min<size_t>(hw, std::max<size_t>(1, n / 65536));
+}
+
+// f(part, begin, end) over parallel_parts(n) contiguous parts of [0, n)
+template <class F>
+void parallel_parts_for(size_t n, F f) {
+    const size_t parts = parallel_parts(n);
+    const size_t step = (n + parts - 1) / parts;
     if (parts <= 1) {
-        f((size_t)0, n);
+        f((size_t)0, (size_t)0, n);
         return;
     }
     std::vector<std::thread> th;
-    const size_t step = (n + parts - 1) / parts;
-    for (size_t p = 1; p < parts; ++p) th.emplace_back(f, p * step, std::min(n, (p + 1) * step));
-    f((size_t)0, std::min(n, step));
+    for (size_t p = 1; p < parts; ++p) th.emplace_back(f, p, std::min(n, p * step), std::min(n, (p + 1) * step));
+    f((size_t)0, (size_t)0, std::min(n, step));
     for (auto& t : th) t.join();
+}
+
+template <class F>
+void parallel_for(size_t n, F f) {
+    parallel_parts_for(n, [&](size_t, size_t b, size_t e) { f(b, e); });
 }
 
 }  // namespace
@@ -100,15 +135,15 @@ extern "C" void igs_internal_kahan_normalize(double* p, size_t n) {
 }
 
 namespace {
-double kahan_sum(const std::vector<double>& v);
-std::vector<double> gradient_mixture(const std::vector<double>& mag, double total, double lambda);
+template <class V>
+fast_vector<double> gradient_mixture(const V& mag, double total, double lambda);
 }  // namespace
 
 // sampling.cpp:25-40 gradient_mixture from a magnitude table (in place
 // allowed): Kahan total in index order, then the elementwise mixture.
 extern "C" void igs_internal_gradient_mixture(const double* mag, size_t n, double lambda, double* p) {
     std::vector<double> m(mag, mag + n);
-    const std::vector<double> q = gradient_mixture(m, kahan_sum(m), lambda);
+    const fast_vector<double> q = gradient_mixture(m, kahan_sum(m), lambda);
     std::memcpy(p, q.data(), n * sizeof(double));
 }
 
@@ -118,51 +153,99 @@ namespace {
 // from a precomputed gradient magnitude and its Kahan total: the init and
 // optimisation distributions share both (only lambda differs), so the
 // Sobel pass and the sum run once.
-std::vector<double> gradient_mixture(const std::vector<double>& mag, double total, double lambda) {
-    std::vector<double> p(mag.size());
-    const double uniform = 1.0 / (double)p.size();
-    if (total > 0.0) {
-        const double scale = (1.0 - lambda) / total;
-        for (size_t i = 0; i < p.size(); ++i) p[i] = mag[i] * scale + lambda * uniform;
-    } else {
-        std::fill(p.begin(), p.end(), uniform);
-    }
-    return p;
+template <class V>
+fast_vector<double> gradient_mixture(const V& mag, double total, double lambda) {
+    fast_vector<double> q(mag.size());
+    const double uniform = 1.0 / (double)q.size();
+    const double scale = total > 0.0 ? (1.0 - lambda) / total : 0.0;
+    parallel_for(q.size(), [&](size_t b, size_t e) {  // (elementwise: any split)
+        for (size_t i = b; i < e; ++i) q[i] = total > 0.0 ? mag[i] * scale + lambda * uniform : uniform;
+    });
+    return q;
 }
 
-// sampling.cpp:96-133 Walker/Vose table; draw = index, then coin
+// sampling.cpp:96-133 Walker/Vose table; draw = index, then coin.  The
+// scratch (scaled weights, the two stacks) and the table's own vectors are
+// reused from build to build: at 4M entries a fresh ~110 MB costs more in
+// first-touch page faults than the table itself.
+struct AliasScratch {
+    fast_vector<double> scaled;
+    fast_vector<uint32_t> small, large;
+    std::vector<size_t> part_small;  // per part: small entries (then their offsets)
+};
+
 struct Alias {
-    std::vector<double> prob;
-    std::vector<uint32_t> alias;
+    fast_vector<double> prob;
+    fast_vector<uint32_t> alias;
     bool ok = false;
 
-    explicit Alias(const std::vector<double>& w) {
-        const size_t n = w.size();
+    Alias() = default;
+    template <class V>
+    explicit Alias(const V& w) {
+        AliasScratch S;
+        build(w.data(), w.size(), S);
+    }
+    template <class V>
+    void build(const V& w, AliasScratch& S) {
+        build(w.data(), w.size(), S);
+    }
+    void build(const double* w, size_t n, AliasScratch& S) {
+        ok = false;
         if (n == 0) return;
-        const double total = kahan_sum(w);
-        if (!(total > 0.0)) return;
-        for (size_t i = 0; i < n; ++i)
-            if (w[i] < 0.0) return;
-        prob.assign(n, 0.0);
-        alias.assign(n, 0);
-        std::vector<double> scaled(n);
-        parallel_for(n, [&](size_t b, size_t e) {
-            for (size_t i = b; i < e; ++i) scaled[i] = w[i] * n / total;
-        });
-        // small / large stacks in index order (branch-free partition)
-        std::vector<uint32_t> small(n), large(n);
-        size_t ns = 0, nl = 0;
+        // the Kahan total in index order (and, in the same pass, the
+        // reference's check for negative weights -- which fails either way)
+        double total = 0.0, comp = 0.0;
+        bool neg = false;
         for (size_t i = 0; i < n; ++i) {
-            const bool sm = scaled[i] < 1.0;
-            small[ns] = (uint32_t)i;
-            large[nl] = (uint32_t)i;
-            ns += sm;
-            nl += !sm;
+            const double x = w[i];
+            neg |= x < 0.0;
+            const double y = x - comp;
+            const double t = total + y;
+            comp = (t - total) - y;
+            total = t;
         }
+        if (!(total > 0.0) || neg) return;
+        // (every prob entry is written below; alias stays 0 where prob = 1)
+        prob.resize(n);
+        alias.resize(n);
+        S.scaled.resize(n);
+        S.small.resize(n);
+        S.large.resize(n);
+        parallel_for(n, [&](size_t b, size_t e) {
+            std::memset(alias.data() + b, 0, (e - b) * sizeof(uint32_t));
+            std::memset(prob.data() + b, 0, (e - b) * sizeof(double));
+        });
+        // scaled weights and the small / large stacks in index order: a
+        // stable partition (per-part counts, offsets, then each part writes
+        // its own range -- the order of a sequential pass)
+        const size_t parts = parallel_parts(n);
+        S.part_small.assign(parts + 1, 0);
+        parallel_parts_for(n, [&](size_t p, size_t b, size_t e) {
+            size_t k = 0;
+            for (size_t i = b; i < e; ++i) {
+                S.scaled[i] = w[i] * n / total;
+                k += S.scaled[i] < 1.0;
+            }
+            S.part_small[p + 1] = k;
+        });
+        for (size_t p = 0; p < parts; ++p) S.part_small[p + 1] += S.part_small[p];
+        parallel_parts_for(n, [&](size_t p, size_t b, size_t e) {
+            size_t ks = S.part_small[p], kl = b - S.part_small[p];
+            for (size_t i = b; i < e; ++i) {
+                if (S.scaled[i] < 1.0)
+                    S.small[ks++] = (uint32_t)i;
+                else
+                    S.large[kl++] = (uint32_t)i;
+            }
+        });
+        size_t ns = S.part_small[parts], nl = n - ns;
         // Vose's loop, the reference's stack order: pop s and l; l takes
         // s's deficit and goes back on top of the small or large stack.
         // The large item stays in a register while it remains large (it
         // would be popped again at once).
+        double* scaled = S.scaled.data();
+        uint32_t* small = S.small.data();
+        uint32_t* large = S.large.data();
         while (ns > 0 && nl > 0) {
             uint32_t l = large[--nl];
             double sl = scaled[l];
@@ -308,23 +391,40 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
     std::vector<double> set;
     // image_gradient_magnitude on the device (sobel_kernel, bit-identical),
     // its Kahan total and the mixtures here
+    auto mark = [&](const char* what, clk::time_point& t) {
+        if (trace) std::fprintf(stderr, "igs_fit:   %s %.2f ms\n", what, since(t));
+        t = clk::now();
+    };
+    AliasScratch alias_ws;  // shared by every table of the fit (see Alias)
+    Alias add;              // the densification tables, one at a time
+    auto tm = clk::now();
     if ((e = igs_set_target(ctx, target, W, H))) return e;
-    std::vector<double> mag((size_t)W * H);
+    fast_vector<double> mag((size_t)W * H);  // (written by igs_image_gradient_magnitude)
     if ((e = igs_image_gradient_magnitude(ctx, nullptr, W, H, mag.data()))) return e;
+    mark("target + gradient magnitude", tm);
     const double mag_total = kahan_sum(mag);
+    mark("kahan total", tm);
     {
-        const Alias init(gradient_mixture(mag, mag_total, c.lambda_init));
+        const fast_vector<double> mix = gradient_mixture(mag, mag_total, c.lambda_init);
+        mark("init mixture", tm);
+        Alias init;
+        init.build(mix, alias_ws);
+        mark("init alias table", tm);
         if (!init.ok) return bad("alias table weights must have positive sum");
         const double s0 = 2.0 / std::max(W, H);
         set.reserve((size_t)init_count * 8);
         for (int i = 0; i < init_count; ++i) add_gaussian(set, target, W, H, init.sample(rng), s0);
+        mark("init draws", tm);
     }
-    const Alias opt(gradient_mixture(mag, mag_total, c.lambda_opt));
+    Alias opt;
+    opt.build(gradient_mixture(mag, mag_total, c.lambda_opt), alias_ws);
+    mark("opt mixture + alias table", tm);
     if (!opt.ok) return bad("alias table weights must have positive sum");
     if ((e = igs_set_params(ctx, set.data(), (uint32_t)init_count))) return e;
     // the per-iteration draws from `opt` happen on the device (the host only
     // advances the engine): the table goes up once
     if ((e = igs_internal_set_sampler(ctx, opt.prob.data(), opt.alias.data(), opt.prob.size()))) return e;
+    mark("set_params + sampler upload", tm);
     t_init = since(t_start);
 
     double lr[4] = {c.lr[0], c.lr[1], c.lr[2], c.lr[3]};
@@ -337,8 +437,7 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
     int stage = 0;
     std::vector<igs_eval_record> recs;
     std::vector<std::string> checkpoints;
-    std::vector<float> rendered((size_t)W * H * 3);
-    std::vector<double> dist((size_t)W * H);
+    fast_vector<double> dist((size_t)W * H);  // (written by igs_add_distribution)
     // one sample = opt.sample(rng) = next_index (one engine output) then
     // next_double (one more): the raw outputs, in that order
     std::vector<unsigned long long> cur(2 * (size_t)c.samples_per_iter), next(2 * (size_t)c.samples_per_iter);
@@ -397,6 +496,7 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
             if ((e = render_current())) return e;
             igs_sync(ctx);
             t_render += since(t_r);
+            if (trace) std::fprintf(stderr, "igs_fit: eval render at %d: %.2f ms\n", iter, since(t_r));
             const auto t_m = clk::now();
             have_render = true;
             double p = 0.0, s = 0.0;
@@ -420,16 +520,21 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
         t_eval += since(t_post);
         const auto t_dens = clk::now();
         if (do_densify) {
+            auto td = clk::now();
             if ((e = emit_checkpoint(iter))) return e;
             if (!have_render && (e = render_current())) return e;
+            mark("densify: checkpoint + render", td);
             // add_distribution(rendered, target) on the device, Vose + draws here
             if ((e = igs_add_distribution(ctx, nullptr, W, H, dist.data()))) return e;
-            const Alias add(dist);
+            mark("densify: add_distribution", td);
+            add.build(dist, alias_ws);
+            mark("densify: alias table", td);
             if (!add.ok) return bad("alias table weights must have positive sum");
             std::vector<double> fresh;
             fresh.reserve((size_t)add_count * 8);
             for (int a = 0; a < add_count; ++a) add_gaussian(fresh, target, W, H, add.sample(rng), default_scale);
             if (add_count > 0 && (e = igs_append_params(ctx, fresh.data(), (uint32_t)add_count))) return e;
+            mark("densify: draws + append", td);
             ++stage;
         }
         t_densify += since(t_dens);
