@@ -61,8 +61,14 @@ __device__ __forceinline__ int ring_dy(int it, int R) {
 // Builds between full re-bucketings (in between, the summaries are refit
 // from the Adam kernels' accumulation; exact either way, only the tightness
 // of the bounds drifts as Gaussians move and change scale).
-constexpr int kRefitPeriod = 16;
-constexpr int kGrowShift = 3;  // re-bucket when more than n >> kGrowShift Gaussians grew
+#ifndef IGS_REFIT_PERIOD
+#define IGS_REFIT_PERIOD 16
+#endif
+#ifndef IGS_GROW_SHIFT
+#define IGS_GROW_SHIFT 3
+#endif
+constexpr int kRefitPeriod = IGS_REFIT_PERIOD;
+constexpr int kGrowShift = IGS_GROW_SHIFT;  // re-bucket when more than n >> kGrowShift Gaussians grew
 
 // 32 bytes (one sector).  The bbox is rounded outward and lambda_min down
 // to float: a box that contains the true one and a smaller eigenvalue only
