@@ -564,11 +564,14 @@ def secondary_fit(ctx):
     ctx.upload_samples(synth.sample_indices(NS, C2["W"], C2["H"], seed=98, steps=25))
     ctx.train_iterations(5, K, LR, 5001, want_losses=False)
     ms = []
+    clocks = Clocks(physical_gpu(int(os.environ.get("LOCAL_RANK", "0"))))
+    clocks.start()
     for s in range(20):
         ctx.flush_l2(FLUSH_BYTES)
         ctx.timer_begin()
         ctx.train_iterations(1, K, LR, 5006 + s, want_losses=False)
         ms.append(ctx.timer_end())
+    clk = clocks.stop()
     return {"config": "C2 fit (SURVEY.md 8d schedule): 2048x2048, budget 100k (50k init + 4 x 12.5k), 5000 "
                       "iterations, warmup 1000, densify every 1000, eval every 500",
             "wall_s": wall, "iters_per_s_incl_everything": 5000 / wall, "final_count": rep["final_count"],
@@ -576,7 +579,7 @@ def secondary_fit(ctx):
             "trained_state_step": {"t": "5006-5025", "iters_per_s": 1e3 * len(ms) / sum(ms),
                                    "ms_per_step": sum(ms) / len(ms),
                                    "ms_per_step_median": statistics.median(ms),
-                                   "ms_per_step_min_max": [min(ms), max(ms)],
+                                   "ms_per_step_min_max": [min(ms), max(ms)], "clocks": clk,
                                    "note": "the fitted 100k set (t = 5000), uniform samples, L2 flushed per step"}}
 
 
