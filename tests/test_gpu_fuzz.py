@@ -127,3 +127,28 @@ def test_frontier_overflow_in_training_step(gctx, port, seed):
     assert abs(loss - wl) <= 1e-12 * abs(wl)
     scale = np.maximum(np.abs(wg), np.max(np.abs(wg), axis=0) * 1e-3)
     assert np.max(np.abs(grads - wg) / np.maximum(scale, 1e-300)) <= 1e-12
+
+
+@pytest.mark.parametrize("seed", [9, 26])
+def test_frontier_overflow_in_fused_iterations(gctx, ref, seed):
+    """Fused iterations (search -> segment buckets -> hard-point / overflow /
+    long-segment launch -> update with the loss) on sets whose searches
+    overflow the frontier: the hard points' contributions land in the
+    buckets before the update, and losses, parameters and moments match the
+    reference's train_iteration bit for bit."""
+    params = np.ascontiguousarray(random_case(np.random.default_rng(1000 + seed)))
+    W, H = 96, 80
+    target = synth.photo_like_image(W, H, 31200 + seed)
+    steps = synth.sample_indices(3000, W, H, seed=seed, steps=3)
+    gctx.set_params(params)
+    gctx.set_target(target)
+    gctx.profile_enable(True)
+    got = [gctx.train_iteration(steps[t], 10, LR, t + 1) for t in range(3)]
+    hard = gctx.profile_read(PROF_KNN_HARD)[2]
+    gctx.profile_enable(False)
+    assert hard > 0  # the iterations do overflow
+    p = params.copy(); m = np.zeros_like(p); v = np.zeros_like(p)
+    want = [ref.train_iteration(p, m, v, target, steps[t], 10, LR, t + 1) for t in range(3)]
+    gm, gv = gctx.get_adam_state()
+    assert got == want
+    assert np.array_equal(gctx.get_params(), p) and np.array_equal(gm, m) and np.array_equal(gv, v)
