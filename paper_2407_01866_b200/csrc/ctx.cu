@@ -13,6 +13,11 @@
 
 #include "igs_internal.cuh"
 
+#include <atomic>
+
+// contexts alive in the process (igs_coop_barriers)
+static std::atomic<int> g_live_contexts{0};
+
 using namespace igs_dev;
 
 // train.cu
@@ -231,11 +236,15 @@ int igs_ctx_create(int device, igs_ctx** out) {
         return IGS_E_CUDA;
     }
     *out = ctx;
+    g_live_contexts.fetch_add(1);
     return IGS_OK;
 }
 
+int igs_live_contexts() { return g_live_contexts.load(std::memory_order_relaxed); }
+
 void igs_ctx_destroy(igs_ctx* ctx) {
     if (!ctx) return;
+    g_live_contexts.fetch_sub(1);
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     igs_partition_release(ctx);

@@ -504,9 +504,12 @@ inline cudaError_t igs_launch_pdl(cudaStream_t st, bool coop, void (*k)(KArgs...
 // launches: the driver then schedules each grid whole (and under MPS,
 // where fewer SMs may be available than the device reports, fails rather
 // than hangs).
+// Likewise when several contexts are alive in the process (their streams
+// could run two barrier grids side by side).
+extern "C" int igs_live_contexts();  // ctx.cu
 inline bool igs_coop_barriers() {
     static const bool v = getenv("IGS_COOP_BARRIERS") != nullptr;
-    return v;
+    return v || igs_live_contexts() > 1;
 }
 
 #define IGS_PDL_COOP(ctx, kernel, grid, block, smem, ...)                                                   \
