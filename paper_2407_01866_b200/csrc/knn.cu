@@ -59,7 +59,7 @@ __device__ __forceinline__ int ring_dy(int it, int R) {
     return side == 0 ? -R : (side == 1 ? -R + t : (side == 2 ? R : R - t));
 }
 // Builds between full re-bucketings (in between, the summaries are refit
-// from the Adam kernels' accumulation; exact either way, only the tightness
+// from the member-ordered records the Adam kernels keep current; exact either way, only the tightness
 // of the bounds drifts as Gaussians move and change scale).
 #ifndef IGS_REFIT_PERIOD
 #define IGS_REFIT_PERIOD 16

@@ -438,7 +438,7 @@ __global__ void adam_kernel(double* __restrict__ params, const double* __restric
 
 // Sharded multi-rank update, after the parameter all-gather: the Gaussians
 // outside this rank's slice get their prepared records (kernel 1), their
-// tree accumulation (as the Adam kernel does for its own) and their
+// member-ordered records for the tree refit (as the Adam kernel does for its own) and their
 // contribution counters cleared for the next step.
 __global__ void complement_prepare_kernel(const double* __restrict__ params, uint32_t n, uint32_t lo, uint32_t hi,
                                           ScanRec* __restrict__ scan, ShadeRec* __restrict__ shade,
@@ -835,7 +835,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
                         LossTail{{}, loss_in_adam ? long_args() : LongArgs{}});
             if (shard) {
                 // flags of every slice, then every slice's parameters, then
-                // the records + tree accumulation of the other slices here
+                // the records (and member-ordered copies) of the other slices here
                 long long* st = (long long*)igs_scratch(ctx, 40, (size_t)R * 4 * sizeof(long long));
                 if (!st) return igs_fail(ctx, IGS_E_CUDA, "out of device memory (shard)");
                 IGS_CUDA(ctx, cudaMemcpyAsync(st + 4 * rk, ctx->status, 4 * sizeof(long long),
