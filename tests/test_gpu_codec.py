@@ -79,3 +79,33 @@ def test_codec_errors_match_reference(gctx, ref):
     with pytest.raises(IgsError) as e:
         gctx.encode(32, 32, 10)
     assert e.value.kind == "empty_set"
+
+
+def test_failed_decode_and_quantize_leave_the_set(gctx, ref):
+    """The reference's decode() and quantize_set() are pure functions: a file
+    with a NaN half, or a parameter beyond binary16, raises and the caller's
+    set is untouched -- so the resident set must be too."""
+    params = _set(60, 5)
+    data = bytearray(ref.encode(params, 32, 32, 10))
+    data[20:22] = (0x7e00).to_bytes(2, "little")  # the first Gaussian's mu_u: a NaN half
+    other = _set(40, 6)
+    gctx.set_params(other)
+    with pytest.raises(IgsError):
+        gctx.decode(bytes(data))
+    with pytest.raises(Exception):
+        ref.decode(bytes(data))
+    assert np.array_equal(gctx.get_params(), other)
+    # the search over the untouched set still answers exactly
+    uv = np.random.default_rng(3).random((50, 2))
+    idx, _, cnt = gctx.select_top_k(uv, 10)
+    gctx.set_params(other)
+    idx2, _, _ = gctx.select_top_k(uv, 10)
+    assert np.array_equal(idx, idx2)
+    p = other.copy()
+    p[3, 3] = 7e4  # beyond binary16
+    gctx.set_params(p)
+    with pytest.raises(IgsError):
+        gctx.quantize_set()
+    with pytest.raises(Exception):
+        ref.quantize_set(p)
+    assert np.array_equal(gctx.get_params(), p)
