@@ -404,6 +404,17 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
     mark("target + gradient magnitude", tm);
     const double mag_total = kahan_sum(mag);
     mark("kahan total", tm);
+    // the optimisation table needs no engine output, so it is built on a
+    // second host thread while the init table is built and drawn from
+    Alias opt;
+    AliasScratch opt_ws;
+    std::thread opt_builder([&] { opt.build(gradient_mixture(mag, mag_total, c.lambda_opt), opt_ws); });
+    struct Joiner {
+        std::thread& t;
+        ~Joiner() {
+            if (t.joinable()) t.join();
+        }
+    } join_opt{opt_builder};
     {
         const fast_vector<double> mix = gradient_mixture(mag, mag_total, c.lambda_init);
         mark("init mixture", tm);
@@ -416,9 +427,8 @@ int igs_fit(igs_ctx* ctx, const float* target, int W, int H, const igs_fit_confi
         for (int i = 0; i < init_count; ++i) add_gaussian(set, target, W, H, init.sample(rng), s0);
         mark("init draws", tm);
     }
-    Alias opt;
-    opt.build(gradient_mixture(mag, mag_total, c.lambda_opt), alias_ws);
-    mark("opt mixture + alias table", tm);
+    opt_builder.join();
+    mark("opt mixture + alias table (join)", tm);
     if (!opt.ok) return bad("alias table weights must have positive sum");
     if ((e = igs_set_params(ctx, set.data(), (uint32_t)init_count))) return e;
     // the per-iteration draws from `opt` happen on the device (the host only
