@@ -2,7 +2,7 @@
  * igs_b200.h -- C-ABI of the B200-native Image-GS hot path.
  *
  * The reference (/root/reference/proj) exposes its hot path as a C++ header
- * API in namespace igs (proj/include/igs/(proj/include/igs/*.hpp)lt;name(proj/include/igs/*.hpp)gt;.hpp); it has no FFI of its own.
+ * API in namespace igs (the headers proj/include/igs/NAME.hpp); it has no FFI of its own.
  * This header is the thin C boundary a maintainer binds to replace that
  * path: plain pointers and sizes, no C++ or torch types.
  * shows the C++ shim (same igs:: signatures) and the Python ctypes binding.
