@@ -307,6 +307,11 @@ constexpr int kWalk = IGS_KWALK;  // member-walk loads in flight per thread
 #define IGS_TREE_THREADS 256
 #endif
 constexpr int kTreeThreads = IGS_TREE_THREADS;  // >= 256 (the level-0 block)
+// Sets up to this size refit with 512-thread CTAs: twice the threads on a
+// tile's member walk, which evens out tiles of very different populations
+// (trained sets: refit 24.2 -> 22.6 us at C2 t = 5,000, fit start equal);
+// larger sets keep 256 (C4: 100 -> 147 us at 512, fewer CTAs per SM).
+constexpr uint32_t kTreeWideMaxN = 400000;
 
 // own summary from (count, accumulator)
 __device__ __forceinline__ Sum own_from(uint32_t m, const Acc& a) {
@@ -356,7 +361,8 @@ __device__ __forceinline__ void acc_fold(Acc* d, const Acc& a) {
     atomicMax(&d->aniso, a.aniso);
 }
 
-__global__ void __launch_bounds__(kTreeThreads) lq_tree_kernel(const ScanRec* __restrict__ mrec,
+template <int NT>
+__global__ void __launch_bounds__(NT) lq_tree_kernel(const ScanRec* __restrict__ mrec,
                                                       const uint32_t* __restrict__ mcell,
                                                       const uint32_t* __restrict__ off, uint32_t n,
                                                       Acc* __restrict__ acc, Lq L,
@@ -375,13 +381,13 @@ __global__ void __launch_bounds__(kTreeThreads) lq_tree_kernel(const ScanRec* __
 #pragma unroll
         for (int l = 0; l < kMaxLv; ++l) s_loff[l] = L.loff[l];
     }
-    for (int i = t; i < kTileCells; i += kTreeThreads) s_acc[i] = acc_empty();
+    for (int i = t; i < kTileCells; i += NT) s_acc[i] = acc_empty();
     __syncthreads();
     const int nb = L.G0 / kBlk;  // G0 is a power of two >= 16
     const int bx = blockIdx.x % nb, by = blockIdx.x / nb;
     pdl_wait();
-    stage_job_run(job, blockIdx.x * kTreeThreads + t, gridDim.x * kTreeThreads);  // the iteration's start (StageJob)
-    prefetch_l2(pf, blockIdx.x * kTreeThreads + t, gridDim.x * kTreeThreads);  // the search's inputs
+    stage_job_run(job, blockIdx.x * NT + t, gridDim.x * NT);  // the iteration's start (StageJob)
+    prefetch_l2(pf, blockIdx.x * NT + t, gridDim.x * NT);  // the search's inputs
     // the counts of the cells this thread owns at each in-block level, and
     // (threads < 31) one row's member range -- one round trip
     uint32_t cell[kInLv], m[kInLv];
@@ -425,12 +431,12 @@ __global__ void __launch_bounds__(kTreeThreads) lq_tree_kernel(const ScanRec* __
     // the members, one per thread, kWalk batches of loads in flight (whole
     // warps iterate alike)
     const uint32_t total = s_v0[kTileRows];
-    for (uint32_t vb = 0; vb < total; vb += kTreeThreads * kWalk) {
+    for (uint32_t vb = 0; vb < total; vb += NT * kWalk) {
         uint32_t key[kWalk];
         Acc a[kWalk];
 #pragma unroll
         for (int u = 0; u < kWalk; ++u) {
-            const uint32_t v = vb + kTreeThreads * u + t;
+            const uint32_t v = vb + NT * u + t;
             key[u] = ~0u;
             a[u] = acc_empty();
             if (v < total) {
@@ -445,7 +451,7 @@ __global__ void __launch_bounds__(kTreeThreads) lq_tree_kernel(const ScanRec* __
         }
 #pragma unroll
         for (int u = 0; u < kWalk; ++u)
-            if (vb + kTreeThreads * u < total && warp_runs(key[u], a[u])) acc_fold(&s_acc[key[u]], a[u]);
+            if (vb + NT * u < total && warp_runs(key[u], a[u])) acc_fold(&s_acc[key[u]], a[u]);
     }
     __syncthreads();
     int cur = 0, lbase = 0;
@@ -476,14 +482,14 @@ __global__ void __launch_bounds__(kTreeThreads) lq_tree_kernel(const ScanRec* __
     // many members each): cell by cell over the CTAs, each cell's members
     // reduced by the whole CTA into its global accumulator (plain store)
     {
-        __shared__ Acc s_wacc[kTreeThreads / 32];
+        __shared__ Acc s_wacc[NT / 32];
         const uint32_t cu0 = (uint32_t)s_loff[kInLv], cu1 = (uint32_t)s_loff[L.levels - 1] + 1;
         for (uint32_t c = cu0 + blockIdx.x; c < cu1; c += gridDim.x) {
             const uint32_t mc = cnt[c];
             if (mc == 0) continue;  // (uniform)
             const uint32_t p0 = off[c];
             Acc a = acc_empty();
-            for (uint32_t e = t; e < mc; e += kTreeThreads) acc_add_local(a, mrec[p0 + e]);
+            for (uint32_t e = t; e < mc; e += NT) acc_add_local(a, mrec[p0 + e]);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 a.x0 = min(a.x0, __shfl_xor_sync(0xffffffffu, a.x0, o));
@@ -496,7 +502,7 @@ __global__ void __launch_bounds__(kTreeThreads) lq_tree_kernel(const ScanRec* __
             if ((t & 31) == 0) s_wacc[t >> 5] = a;
             __syncthreads();
             if (t == 0) {
-                for (int w = 1; w < kTreeThreads / 32; ++w) {
+                for (int w = 1; w < NT / 32; ++w) {
                     const Acc& b = s_wacc[w];
                     a.x0 = min(a.x0, b.x0);
                     a.y0 = min(a.y0, b.y0);
@@ -521,7 +527,7 @@ __global__ void __launch_bounds__(kTreeThreads) lq_tree_kernel(const ScanRec* __
     uint32_t um[2] = {0, 0}, uc[2] = {0, 0};
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
-        const int i = t + kTreeThreads * r;
+        const int i = t + NT * r;
         if (i < ncell) {
             uc[r] = (uint32_t)(s_loff[l0] + i);  // levels are contiguous in the cell numbering
             um[r] = cnt[uc[r]];
@@ -543,7 +549,7 @@ __global__ void __launch_bounds__(kTreeThreads) lq_tree_kernel(const ScanRec* __
     // through global memory
     for (int l = kInLv; l < l0; ++l) {
         const int G = L.G0 >> l, cw = G * 2;
-        for (int i = t; i < G * G; i += kTreeThreads) {
+        for (int i = t; i < G * G; i += NT) {
             const int x = i % G, y = i / G;
             const uint32_t c = (uint32_t)(s_loff[l] + i);
             Sum s = own_of(acc, cnt, c);
@@ -562,7 +568,7 @@ __global__ void __launch_bounds__(kTreeThreads) lq_tree_kernel(const ScanRec* __
         const int G = L.G0 >> l0, cw = G * 2;
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
-            const int i = t + kTreeThreads * r;
+            const int i = t + NT * r;
             if (i >= ncell) continue;
             const Acc ua = um[r] ? acc_ldcg(acc + uc[r]) : acc_empty();
             const Sum o = own_from(um[r], ua);
@@ -580,7 +586,7 @@ __global__ void __launch_bounds__(kTreeThreads) lq_tree_kernel(const ScanRec* __
     __syncthreads();
     for (int j = l0 + 1, b0 = 0; j < L.levels; ++j) {
         const int G = L.G0 >> j, cw = G * 2, b1 = b0 + cw * cw;  // b0: first cell of level j-1 in up[]
-        for (int i = t; i < G * G; i += kTreeThreads) {
+        for (int i = t; i < G * G; i += NT) {
             const int x = i % G, y = i / G;
             Sum s = up[b1 + i];
             for (int dy = 0; dy < 2; ++dy)
@@ -1894,9 +1900,16 @@ int knn_build(igs_ctx* ctx) {
         // launches since the last build: re-derive the summaries only
         const int nb = (b.lq.G0 + kBlk - 1) / kBlk;
         igs_prof_begin(ctx, IGS_PROF_CULL);
-        IGS_PDL(ctx, lq_tree_kernel, nb * nb, kTreeThreads, 0, (const ScanRec*)b.mrec.p, (const uint32_t*)b.mcell.p,
-                (const uint32_t*)b.off.p, ctx->n, (Acc*)b.acc.p, b.lq, (const uint32_t*)b.cnt.p, (Sum*)b.own.p,
-                (Sum*)b.sub.p, (unsigned int*)b.ticket.p, search_inputs(ctx, b), job, 0);
+        if (ctx->n <= kTreeWideMaxN)
+            IGS_PDL(ctx, lq_tree_kernel<2 * kTreeThreads>, nb * nb, 2 * kTreeThreads, 0, (const ScanRec*)b.mrec.p,
+                    (const uint32_t*)b.mcell.p, (const uint32_t*)b.off.p, ctx->n, (Acc*)b.acc.p, b.lq,
+                    (const uint32_t*)b.cnt.p, (Sum*)b.own.p, (Sum*)b.sub.p, (unsigned int*)b.ticket.p,
+                    search_inputs(ctx, b), job, 0);
+        else
+            IGS_PDL(ctx, lq_tree_kernel<kTreeThreads>, nb * nb, kTreeThreads, 0, (const ScanRec*)b.mrec.p,
+                    (const uint32_t*)b.mcell.p, (const uint32_t*)b.off.p, ctx->n, (Acc*)b.acc.p, b.lq,
+                    (const uint32_t*)b.cnt.p, (Sum*)b.own.p, (Sum*)b.sub.p, (unsigned int*)b.ticket.p,
+                    search_inputs(ctx, b), job, 0);
         igs_prof_end(ctx, IGS_PROF_CULL, 0.0);
         b.since_build++;
         b.version = b.chain = ctx->params_version;
@@ -1955,9 +1968,14 @@ int knn_build(igs_ctx* ctx) {
                 (uint32_t*)b.mcell.p, (Acc*)b.acc.p);
     }
     const int nb = (G0 + kBlk - 1) / kBlk;
-    IGS_PDL(ctx, lq_tree_kernel, nb * nb, kTreeThreads, 0, (const ScanRec*)b.mrec.p, (const uint32_t*)b.mcell.p,
-            (const uint32_t*)off, n, (Acc*)b.acc.p, L, (const uint32_t*)cnt, (Sum*)b.own.p,
-            (Sum*)b.sub.p, (unsigned int*)b.ticket.p, search_inputs(ctx, b), job, 1);
+    if (n <= kTreeWideMaxN)
+        IGS_PDL(ctx, lq_tree_kernel<2 * kTreeThreads>, nb * nb, 2 * kTreeThreads, 0, (const ScanRec*)b.mrec.p,
+                (const uint32_t*)b.mcell.p, (const uint32_t*)off, n, (Acc*)b.acc.p, L, (const uint32_t*)cnt,
+                (Sum*)b.own.p, (Sum*)b.sub.p, (unsigned int*)b.ticket.p, search_inputs(ctx, b), job, 1);
+    else
+        IGS_PDL(ctx, lq_tree_kernel<kTreeThreads>, nb * nb, kTreeThreads, 0, (const ScanRec*)b.mrec.p,
+                (const uint32_t*)b.mcell.p, (const uint32_t*)off, n, (Acc*)b.acc.p, L, (const uint32_t*)cnt,
+                (Sum*)b.own.p, (Sum*)b.sub.p, (unsigned int*)b.ticket.p, search_inputs(ctx, b), job, 1);
     igs_prof_end(ctx, IGS_PROF_CULL, 0.0);
     b.lq = L;
     b.builds++;
