@@ -59,6 +59,8 @@ struct AdamArgs {
     long long* status;
     TreeAcc ta;
     uint32_t g_begin, g_end;  // the Gaussians of this launch (a rank's slice when sharded)
+    uint32_t nblk;            // blocks of kAdamThreads / 2 Gaussians in [g_begin, g_end)
+    uint32_t loop_stride;     // 0: one block per CTA; else the grid, walking the blocks
 };
 
 // The update of Gaussian g from its gradient, by lane h of its pair (h = 0:
@@ -219,27 +221,10 @@ using namespace igs_dev;
 // update CTA can wait on them) run T.run; the update CTAs take the
 // Gaussians by ticket order, leave long segments (> kShortSeg) to the
 // workers and, when T.hold(), wait for the workers' hard points first.
-#ifndef IGS_ADAM_MINB
-#define IGS_ADAM_MINB 7
-#endif
+// One block of kAdamThreads / 2 Gaussians: the short-segment sums and the
+// update (the kernel body below, once or per pass of its loop).
 template <class Tail>
-__global__ void __launch_bounds__(kAdamThreads, IGS_ADAM_MINB) segment_adam_kernel(AdamArgs A, Tail T) {
-    __shared__ __align__(16) unsigned char s_raw[Tail::kSmemBytes > 16 ? Tail::kSmemBytes : 16];
-    pdl_wait();
-    T.pre(s_raw);
-    uint32_t blk = blockIdx.x;
-    if constexpr (Tail::kWorkers) {
-        __shared__ uint32_t s_role;
-        if (threadIdx.x == 0) s_role = atomicAdd(T.ticket, 1u) - T.tick_base;
-        __syncthreads();
-        const uint32_t role = s_role;
-        if (role < T.nworkers) {
-            T.run(role, T.nworkers, A, s_raw);
-            return;
-        }
-        blk = role - T.nworkers;
-        if (T.hold()) T.wait();
-    }
+__device__ __forceinline__ void adam_block(const AdamArgs& A, uint32_t blk) {
     // Gaussians [g_begin, g_end): the whole set, or this rank's slice when
     // the multi-rank update is sharded (n stays the set size: gcnt is [2n])
     const uint32_t g0 = A.g_begin + blk * (kAdamThreads / 2) + (threadIdx.x >> 1);
@@ -357,6 +342,47 @@ __global__ void __launch_bounds__(kAdamThreads, IGS_ADAM_MINB) segment_adam_kern
         }
     }
     adam_pair_update(A, g, h, live, skip_all, G);
+}
+
+#ifndef IGS_ADAM_MINB
+#define IGS_ADAM_MINB 7
+#endif
+template <class Tail>
+__global__ void __launch_bounds__(kAdamThreads, IGS_ADAM_MINB) segment_adam_kernel(AdamArgs A, Tail T) {
+    __shared__ __align__(16) unsigned char s_raw[Tail::kSmemBytes > 16 ? Tail::kSmemBytes : 16];
+    pdl_wait();
+    T.pre(s_raw);
+    uint32_t blk = blockIdx.x;
+    if constexpr (Tail::kWorkers) {
+        __shared__ uint32_t s_role;
+        if (threadIdx.x == 0) s_role = atomicAdd(T.ticket, 1u) - T.tick_base;
+        __syncthreads();
+        const uint32_t role = s_role;
+        if (role < T.nworkers) {
+            T.run(role, T.nworkers, A, s_raw);
+            return;
+        }
+        blk = role - T.nworkers;
+        if (T.hold()) T.wait();
+    }
+    // large sets (loop_stride = the grid): a resident wave walks the
+    // blocks; each pass first prefetches its next block's parameter and
+    // moment rows into L2, so their DRAM latency hides behind this block's
+    // chain and fp64 work (C4: 178 -> 164 us).  Otherwise one pass.
+    const uint32_t stride = A.loop_stride ? A.loop_stride : A.nblk;
+    for (; blk < A.nblk; blk += stride) {
+        const uint32_t nb = blk + stride;
+        if (nb < A.nblk) {
+            const uint32_t gn = A.g_begin + nb * (kAdamThreads / 2) + (threadIdx.x >> 1);
+            if (gn < A.g_end) {
+                const size_t o = (size_t)gn * 8 + 4 * (threadIdx.x & 1);
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(A.params + o));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(A.m + o));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(A.v + o));
+            }
+        }
+        adam_block<Tail>(A, blk);
+    }
 }
 
 }  // namespace

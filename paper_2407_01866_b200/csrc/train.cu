@@ -625,6 +625,7 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
     const uint32_t n = ctx->n;
     const int kk = (int)std::min<uint32_t>((uint32_t)k, n);
     const bool knn_path = ctx->opt_cull && kk <= 32;
+    bool adam_pf = false;  // the search prefetches the update's rows into L2
     // the iteration's staging: absorbed by the kNN tree launch, else its own
     if (job && job->kind && !knn_path) {
         const int es = igs_stage_launch(ctx, *job);
@@ -688,7 +689,8 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
         // it, Adam unchanged (IGS_ADAM_PF_LIMIT_MB overrides the 48 MB limit)
         static const size_t pf_limit =
             (size_t)(getenv("IGS_ADAM_PF_LIMIT_MB") ? atol(getenv("IGS_ADAM_PF_LIMIT_MB")) : 48) << 20;
-        if (fuse_lr4 && (size_t)n * 192 <= pf_limit) {
+        adam_pf = fuse_lr4 && (size_t)n * 192 <= pf_limit;
+        if (adam_pf) {
             l2pf_add(pf, ctx->params, (size_t)n * 64);
             l2pf_add(pf, ctx->adam_m, (size_t)n * 64);
             l2pf_add(pf, ctx->adam_v, (size_t)n * 64);
@@ -826,13 +828,26 @@ int igs_forward_backward(igs_ctx* ctx, uint32_t ns, int k, int mode, const uint3
             const uint32_t B = (n + R - 1) / R;
             const bool shard = exch && R > 1 && ctx->opt_shard_adam && (size_t)B * R <= ctx->cap;
             const uint32_t lo = shard ? std::min(n, rk * B) : 0u, hi = shard ? std::min(n, lo + B) : n;
-            if (hi > lo)
-                IGS_PDL(ctx, segment_adam_kernel<LossTail>, (hi - lo + kAdamThreads / 2 - 1) / (kAdamThreads / 2), kAdamThreads, 0,
-                        AdamArgs{gcnt, (const uint32_t*)goff, perm, bucket,
-                                 (const double*)contrib, n, ctx->grads, ctx->params, ctx->adam_m, ctx->adam_v,
-                                 ctx->scan, ctx->shade, fuse_lr4[0], fuse_lr4[1], fuse_lr4[2], fuse_lr4[3], bc1, bc2,
-                                 1.0 / bc1, 1.0 / bc2, ctx->status, ta, lo, hi},
-                        LossTail{{}, loss_in_adam ? long_args() : LongArgs{}});
+            // rows the search did not prefetch (above its L2 limit): one
+            // resident wave walks the blocks, prefetching each next block's
+            // rows (IGS_ADAM_LOOP_GRID: 0 never, g > 0 that grid always)
+            const uint32_t nblk = (hi - lo + kAdamThreads / 2 - 1) / (kAdamThreads / 2);
+            static int loop_per_sm = 0;
+            if (!loop_per_sm && cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                                    &loop_per_sm, segment_adam_kernel<LossTail>, kAdamThreads, 0) != cudaSuccess)
+                loop_per_sm = 1;
+            const char* lg = getenv("IGS_ADAM_LOOP_GRID");
+            uint32_t stride = lg ? (uint32_t)atol(lg)
+                                 : adam_pf ? 0u : (uint32_t)std::max(loop_per_sm, 1) * (uint32_t)ctx->sm_count;
+            AdamArgs aa{gcnt, (const uint32_t*)goff, perm, bucket,
+                        (const double*)contrib, n, ctx->grads, ctx->params, ctx->adam_m, ctx->adam_v,
+                        ctx->scan, ctx->shade, fuse_lr4[0], fuse_lr4[1], fuse_lr4[2], fuse_lr4[3], bc1, bc2,
+                        1.0 / bc1, 1.0 / bc2, ctx->status, ta, lo, hi, nblk, 0};
+            const LossTail tail{{}, loss_in_adam ? long_args() : LongArgs{}};
+            if (stride) stride = std::max<uint32_t>(stride, kLossCtas);  // LossTail: CTAs 0..kLossCtas-1
+            if (stride >= nblk) stride = 0;
+            aa.loop_stride = stride;
+            if (hi > lo) IGS_PDL(ctx, segment_adam_kernel<LossTail>, stride ? stride : nblk, kAdamThreads, 0, aa, tail);
             if (shard) {
                 // flags of every slice, then every slice's parameters, then
                 // the records (and member-ordered copies) of the other slices here

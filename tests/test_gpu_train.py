@@ -282,8 +282,9 @@ def test_alternate_kernels_bit_identical(gctx, port, monkeypatch, k):
     the reduction's offsets + scatter run as one persistent launch; the
     one-point-per-warp search (IGS_KNN_FULLWARP), the CUB scan + scatter
     (IGS_SCAN_LAUNCHES), the five-launch tree build (IGS_KNN_BUILD_LAUNCHES)
-    and the long-segment / loss placement switches (IGS_LONG_LAUNCH,
-    IGS_LOSS_OFF) select and sum identically, so 8 iterations give the same
+    the long-segment / loss placement switches (IGS_LONG_LAUNCH,
+    IGS_LOSS_OFF) and the looping large-set update (IGS_ADAM_LOOP_GRID)
+    select and sum identically, so 8 iterations give the same
     losses and parameters bit for bit (K = 24 takes the full-warp search
     either way)."""
     target = synth.photo_like_image(160, 120, 31013)
@@ -306,6 +307,12 @@ def test_alternate_kernels_bit_identical(gctx, port, monkeypatch, k):
     monkeypatch.setenv("IGS_LONG_LAUNCH", "1")  # (bucket mode: the default reduction)
     monkeypatch.setenv("IGS_LOSS_OFF", "1")
     l2, p2 = run()
+    for v in ("IGS_LONG_LAUNCH", "IGS_LOSS_OFF"):
+        monkeypatch.delenv(v)
+    monkeypatch.setenv("IGS_ADAM_LOOP_GRID", "9")  # the large-set update: 9 CTAs walk the 47 blocks
+    l3, p3 = run()
+    assert l0 == l3
+    assert np.array_equal(p0, p3)
     assert l0 == l2
     assert np.array_equal(p0, p2)
     assert l0 == l1
